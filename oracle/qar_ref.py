@@ -1,0 +1,77 @@
+"""Quantised all-reduce oracle (TEST INFRASTRUCTURE ONLY).
+
+PAPER.md:352-359 (§4.4) quantises the communicated tensor "to a lower-precision
+representation ... for transfer and reduction, and then dequantizing them
+back".  The build's reading (north_star; SURVEY.md §8(c) qar_ref, Q6-Q9):
+
+  per rank r, per block b of `block` consecutive elements of a row:
+      amax = max |o|                       (exact in fp32)
+      s    = fl32(amax / 127)              (IEEE fp32 division, round-nearest-even)
+      q    = clamp(rint_even(fl32(o / s)), -127, 127)   (int8, never -128)
+      amax == 0  ->  s = 0, q = 0
+  result = sum_{r=0..k-1} s_r * q_r        (fixed rank order)
+  bound  |result - sum_r o_r| <= sum_r s_r / 2 <= k * max_r amax_r / 254
+
+Codes and scales are integer/byte results decided in fp32 on both sides, so the
+GPU must reproduce them bit-for-bit.  The dequantised sum is formed here in
+float64 (each s*q is exact in float64).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def quantize_blocks(o, block):
+    """o: float32 array [..., n] with n % block == 0.
+    Returns (q int8 [..., n], s float32 [..., n // block])."""
+    o = np.asarray(o, dtype=np.float32)
+    n = o.shape[-1]
+    assert n % block == 0, "block must divide the row length (Q7)"
+    ob = o.reshape(o.shape[:-1] + (n // block, block))
+    amax = np.max(np.abs(ob), axis=-1)                                   # fp32, exact
+    s = (amax / np.float32(127.0)).astype(np.float32)                    # fp32 IEEE division
+    safe = np.where(s == 0, np.float32(1.0), s).astype(np.float32)
+    ratio = (ob / safe[..., None]).astype(np.float32)                    # fp32 IEEE division
+    q = np.clip(np.rint(ratio), -127, 127)                               # rint = half-to-even
+    q = np.where(s[..., None] == 0, 0, q).astype(np.int8)
+    return q.reshape(o.shape), s
+
+
+def dequantize_blocks(q, s, block):
+    """s * q in float64 (exact)."""
+    q = np.asarray(q, dtype=np.float64)
+    n = q.shape[-1]
+    qb = q.reshape(q.shape[:-1] + (n // block, block))
+    return (qb * np.asarray(s, dtype=np.float64)[..., None]).reshape(q.shape)
+
+
+def qallreduce(partials, block):
+    """partials: sequence of k float32 arrays (one per rank, same shape).
+    Returns (result float64, codes list, scales list)."""
+    codes, scales = [], []
+    acc = None
+    for o in partials:                      # fixed rank order 0..k-1 (Q12)
+        q, s = quantize_blocks(o, block)
+        codes.append(q)
+        scales.append(s)
+        d = dequantize_blocks(q, s, block)
+        acc = d if acc is None else acc + d
+    return acc, codes, scales
+
+
+def error_bound(scales, block):
+    """Per-element bound sum_r s_r / 2 (exact rounding bound of the scheme)."""
+    tot = np.sum([np.asarray(s, dtype=np.float64) for s in scales], axis=0) / 2.0
+    return np.repeat(tot, block, axis=-1)
+
+
+def northstar_bound(partials, block):
+    """k * max_r amax_{r,b} / 254 per element (north_star closed-form bound)."""
+    k = len(partials)
+    amaxes = []
+    for o in partials:
+        o = np.asarray(o, dtype=np.float64)
+        n = o.shape[-1]
+        amaxes.append(np.max(np.abs(o.reshape(o.shape[:-1] + (n // block, block))), axis=-1))
+    m = np.max(np.stack(amaxes), axis=0)
+    return np.repeat(k * m / 254.0, block, axis=-1)

@@ -1,0 +1,161 @@
+"""Tensor-parallel mixer, ranks simulated in-process (TEST INFRASTRUCTURE ONLY).
+
+Channel splitter (§4.2) and packed-parameter placement
+(§4.3) with exactly two all-reduces per block
+(PAPER.md:306-311): AR#1 on the SSM-parameter projection, AR#2 at the
+residual boundary.  Reduction order is fixed 0..k-1 (Q12).
+Readings: A/D row-sharded (C4), B/C taken from AR#1's full vector (C5),
+AR#1 unquantised (Q3), AR#2 exact or int8 (qar_ref, Q6-Q9).
+Zamba heads (Q17): channel d belongs to head d // (E/H); AR#1 sums only over
+the ranks that own channels of a head.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import mixer_ref as M
+from . import qar_ref
+
+
+class ShardError(ValueError):
+    pass
+
+
+class RankError(ValueError):
+    pass
+
+
+def channel_range(d_inner, k, r):
+    """[lo, hi) owned by rank r."""
+    if k < 1 or d_inner % k != 0:
+        raise ShardError(f"d_inner={d_inner} not divisible by tp={k}")
+    if not 0 <= r < k:
+        raise RankError(f"rank {r} not in [0,{k})")
+    Ek = d_inner // k
+    return r * Ek, (r + 1) * Ek
+
+
+def in_proj_rows(d_inner, k, r):
+    """Global rows of the packed W_in owned by rank r: its x block and its z block
+    (SPEC.md:359 example d_inner=4,k=2,r=1 -> {2,3,6,7})."""
+    lo, hi = channel_range(d_inner, k, r)
+    return list(range(lo, hi)) + list(range(d_inner + lo, d_inner + hi))
+
+
+def local_heads(dims, k, r):
+    """[(head, local channel slice, head-relative column slice)] for rank r."""
+    lo, hi = channel_range(dims.d_inner, k, r)
+    Eh = dims.d_inner // dims.n_heads
+    out = []
+    for hd in range(dims.n_heads):
+        a, b = max(lo, hd * Eh), min(hi, (hd + 1) * Eh)
+        if a < b:
+            out.append((hd, slice(a - lo, b - lo), slice(a - hd * Eh, b - hd * Eh)))
+    return out
+
+
+def shard_weights(dims, w, k, r):
+    """Rank-local weights (pure slicing, no arithmetic)."""
+    lo, hi = channel_range(dims.d_inner, k, r)
+    rows = in_proj_rows(dims.d_inner, k, r)
+    s = {
+        "w_in": np.asarray(w["w_in"])[rows],
+        "conv_w": np.asarray(w["conv_w"])[lo:hi],
+        "conv_b": np.asarray(w["conv_b"])[lo:hi],
+        "w_dt": np.asarray(w["w_dt"])[lo:hi],
+        "b_dt": np.asarray(w["b_dt"])[lo:hi],
+        "a_log": np.asarray(w["a_log"])[lo:hi],
+        "d_skip": np.asarray(w["d_skip"])[lo:hi],
+        "w_out": np.asarray(w["w_out"])[:, lo:hi],
+        "heads": [],
+    }
+    for hd, loc, col in local_heads(dims, k, r):
+        s["heads"].append((hd, loc, np.asarray(w["w_x"])[hd][:, col]))
+    return s
+
+
+def shard_state(state, d_inner, k, r):
+    lo, hi = channel_range(d_inner, k, r)
+    conv, h = state
+    return conv[:, lo:hi].copy(), h[:, lo:hi].copy()
+
+
+def gather_state(states):
+    return (np.concatenate([s[0] for s in states], axis=1),
+            np.concatenate([s[1] for s in states], axis=1))
+
+
+def tp_mixer_forward(dims, w, x_in, residual, k, states=None, ar2="exact", block=128, stats=None):
+    """All k ranks of one TP mixer block, lock-step.
+
+    Returns (outs: list of k [B,L,D] arrays (replicas), states', stats) where
+    stats counts collectives with more than one participant.
+    """
+    x_in, residual = np.asarray(x_in, np.float64), np.asarray(residual, np.float64)
+    Bsz, L, _ = x_in.shape
+    E, N, K, R = dims.d_inner, dims.d_state, dims.d_conv, dims.dt_rank
+    Ek = E // k
+    if stats is None:
+        stats = {"allreduce": 0, "allgather": 0}
+    shards = [shard_weights(dims, w, k, r) for r in range(k)]
+    if states is None:
+        states = [M.zero_state(Bsz, Ek, N, K) for _ in range(k)]
+
+    # (1)-(3) rank-local in_proj, conv+SiLU, partial x_proj per head
+    loc = []
+    for r in range(k):
+        s = shards[r]
+        x, z = M.in_proj(x_in, s["w_in"])
+        xc, conv_new = M.causal_conv1d(x, s["conv_w"], s["conv_b"], states[r][0])
+        u = M.silu(xc)
+        parts = {hd: u[:, :, lc] @ wx.T for hd, lc, wx in s["heads"]}
+        loc.append(dict(z=z, u=u, conv=conv_new, parts=parts))
+
+    # AR#1: per head, fixed rank order over the ranks owning that head
+    full = {}
+    ar1_multi = False
+    for hd in range(dims.n_heads):
+        owners = [r for r in range(k) if hd in loc[r]["parts"]]
+        ar1_multi |= len(owners) > 1
+        acc = None
+        for r in owners:
+            acc = loc[r]["parts"][hd] if acc is None else acc + loc[r]["parts"][hd]
+        full[hd] = acc
+    if ar1_multi:
+        stats["allreduce"] += 1
+
+    # (4)-(7) local unpack, dt_proj, scan, gate, partial out_proj
+    partial_out, new_states = [], []
+    for r in range(k):
+        s, lr = shards[r], loc[r]
+        A = -np.exp(s["a_log"])
+        y = np.zeros((Bsz, L, Ek))
+        h_new = np.zeros((Bsz, Ek, N))
+        for hd, lc, _ in s["heads"]:
+            dt_low, Bm, Cm = M.split_ssm_params(full[hd], R, N)
+            if dims.bcdt_rmsnorm:
+                dt_low = M.rmsnorm(dt_low, eps=dims.rms_eps)
+                Bm = M.rmsnorm(Bm, eps=dims.rms_eps)
+                Cm = M.rmsnorm(Cm, eps=dims.rms_eps)
+            delta = M.softplus(dt_low @ s["w_dt"][lc].T + s["b_dt"][lc])
+            y[:, :, lc], h_new[:, lc, :] = M.scan_full(lr["u"][:, :, lc], delta, A[lc], Bm, Cm,
+                                                       s["d_skip"][lc], states[r][1][:, lc, :])
+        g = y * M.silu(lr["z"])
+        partial_out.append(g @ s["w_out"].T)
+        new_states.append((lr["conv"], h_new))
+
+    # AR#2 at the residual boundary
+    if k == 1:
+        total = partial_out[0]                     # TP=1: no AR, no quantisation (Q13)
+    elif ar2 == "exact":
+        total = partial_out[0].copy()
+        for r in range(1, k):
+            total = total + partial_out[r]
+    elif ar2 == "int8":
+        total, _, _ = qar_ref.qallreduce([p.astype(np.float32) for p in partial_out], block)
+    else:
+        raise ValueError(ar2)
+    if k > 1:
+        stats["allreduce"] += 1
+    out = residual + total
+    return [out.copy() for _ in range(k)], new_states, stats
