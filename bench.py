@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark of the tensor-parallel selective-SSM mixer path (arXiv 2602.21144) on B200.
+
+One STEP = the whole hot path over one batch: chunked prefill of the prompt through
+all layers (SSM cache populated), then token-by-token decode from the cache
+(SURVEY.md §8(a) rows a1-a11), for BASELINE.json configs[1] by default:
+Mamba-2.8B (64 layers, d_model 2560), batch 16, prompt 2048 + 256 decode.
+Metric: batch tokens/s = B * (L_in + L_out) / (TTFT + sum of decode steps)
+(SPEC.md:420-423).  TP degree = number of ranks (torchrun), so the
+total work is fixed as N grows ("scaling": "strong").
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config mamba2.8b]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="mamba2.8b", choices=["mamba2.8b", "falcon7b", "zamba7b", "mamba2.8b-long"])
+    p.add_argument("--ar2", default="int8", choices=["int8", "fp32"])
+    p.add_argument("--prompt", type=int, default=0, help="override prompt length (smoke runs only)")
+    p.add_argument("--decode", type=int, default=-1, help="override decode length (smoke runs only)")
+    p.add_argument("--layers", type=int, default=0, help="override layer count (smoke runs only)")
+    p.add_argument("--chunk", type=int, default=0, help="prefill chunk length (default: whole prompt if it fits)")
+    p.add_argument("--probe", default="in_proj", help="kernel timed for the roofline line")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.gpu_id, self.proc, self.lines = gpu_id, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu_id), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def gpu_smi_id(dev):
+    import torch
+    try:
+        u = str(torch.cuda.get_device_properties(dev).uuid)
+        return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        return dev
+
+
+# ---------------------------------------------------------------------------- oracle timing
+def oracle_sample(dims, prompt, decode, batch=1):
+    """Time the CPU oracle (as it stands) on a bounded sample: one layer, `batch` rows,
+    `prompt` + `decode` tokens.  Returns (seconds, tokens)."""
+    import numpy as np
+    import synth
+    from oracle import mixer_ref as M
+    w = {k: v.numpy() for k, v in synth.layer_weights(dims, 0).items()}
+    x, res = synth.activations(batch, prompt + decode, dims.d_model)
+    x, res = x.numpy(), res.numpy()
+    t0 = time.perf_counter()
+    _, st = M.mixer_prefill(dims, w, x[:, :prompt], res[:, :prompt])
+    for t in range(prompt, prompt + decode):
+        _, st = M.mixer_decode(dims, w, x[:, t:t + 1], res[:, t:t + 1], st)
+    dt = time.perf_counter() - t0
+    return dt, batch * (prompt + decode)
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"), default=1)
+    except Exception:
+        return None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(dims, n_layers, prompt=512, decode=8):
+    dt, toks = oracle_sample(dims, prompt, decode)
+    per_layer = toks / dt
+    return {"value": per_layer / n_layers, "unit": "tokens/s", "cores": blas_threads() or len(os.sched_getaffinity(0)),
+            "affinity_cores": len(os.sched_getaffinity(0)), "cpu": cpu_model(), "kind": "oracle",
+            "sample": f"numpy fp64 oracle, 1 layer of {n_layers}, batch 1, prompt {prompt} + {decode} decode "
+                      f"({dt:.1f} s); tokens/s extrapolated linearly to full depth (cost is linear in layers); "
+                      f"GEMMs on multithreaded BLAS, per-token scan loop single-threaded"}
+
+
+def run_reference(args, dims, wl, n_layers):
+    """--impl reference: the oracle timed as it stands on host cores, same metric/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    prompt, decode = 128, 4
+    for _ in range(args.warmup):
+        oracle_sample(dims, 32, 1)
+    secs = []
+    for _ in range(args.steps):
+        dt, toks = oracle_sample(dims, prompt, decode)
+        secs.append(dt)
+    per_layer = 1 * (prompt + decode) / statistics.mean(secs)
+    value = per_layer / n_layers
+    line = {"impl": "reference", "metric": "batch tokens/sec", "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * statistics.mean(secs), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {n_layers} layers, d_model {dims.d_model}, batch {wl['batch']}, "
+                                   f"prompt {wl['prompt']} + {wl['decode']} decode",
+                       "sample": f"per step: 1 layer, batch 1, prompt {prompt} + {decode} decode"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "kind": "oracle",
+                             "cores": blas_threads() or len(os.sched_getaffinity(0)),
+                             "sample": f"1 layer, batch 1, prompt {prompt} + {decode} decode per step, "
+                                       f"extrapolated to {n_layers} layers"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- main
+def main():
+    args = parse()
+    import synth
+    dims = synth.CONFIGS["mamba2.8b" if args.config == "mamba2.8b-long" else args.config]
+    wl = dict(synth.WORKLOADS[args.config])
+    n_layers = args.layers or dims.n_layers
+    if args.prompt:
+        wl["prompt"] = args.prompt
+    if args.decode >= 0:
+        wl["decode"] = args.decode
+    if args.impl == "reference":
+        run_reference(args, dims, wl, n_layers)
+        return
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    k = world
+
+    from paper_2602_21144_b200 import _lib as L
+    from paper_2602_21144_b200.mixer import LayerWeights, TPMixer
+    from paper_2602_21144_b200.stack import MixerStack, synthetic_layer
+
+    B, Lp, Ld = wl["batch"], wl["prompt"], wl["decode"]
+    chunk = args.chunk or Lp
+    while B * chunk > 65536 and chunk % 2 == 0:
+        chunk //= 2
+    n_chunks = math.ceil(Lp / chunk)
+    flags = {"int8": L.SSM_AR2_INT8, "fp32": L.SSM_AR2_FP32}[args.ar2]
+
+    peer_bufs, nbytes, symm = None, 0, None
+    if k > 1:
+        import torch.distributed._symmetric_memory as symm_mem
+        cfg = L.make_config(dims, "bf16")
+        nbytes = L.comm_bytes(cfg, k, B * chunk)
+        buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=dev)
+        buf.zero_()
+        hdl = symm_mem.rendezvous(buf, dist.group.WORLD.group_name)
+        peer_bufs = [int(p) for p in hdl.buffer_ptrs]
+        symm = (buf, hdl)
+        dist.barrier()
+    mx = TPMixer(dims, "bf16", rank=rank, tp_size=k, peer_bufs=peer_bufs, buf_bytes=nbytes, device=dev)
+    layers = []
+    for l in range(n_layers):
+        full = synthetic_layer(dims, l, device=dev)
+        layers.append(LayerWeights(dims, full, k, rank, "bf16", dev))
+        del full
+    torch.cuda.empty_cache()
+    stack = MixerStack(mx, layers, B, chunk, flags)
+
+    # inputs: replicated on all ranks (same seed); larger than L2 (126 MB) -> no flush needed
+    g = torch.Generator(device=dev).manual_seed(42)
+    prompt_in = [torch.randn((B * min(chunk, Lp - c * chunk), dims.d_model), generator=g, device=dev)
+                 for c in range(n_chunks)]
+    dec_in = torch.randn((max(Ld, 1), B, dims.d_model), generator=g, device=dev)
+    work = [p.clone() for p in prompt_in]
+    res_t = torch.empty((B, dims.d_model), device=dev)
+    dec_out = torch.empty((max(Ld, 1), B, dims.d_model), device=dev)
+    stream = torch.cuda.current_stream()
+
+    graph = None
+    if Ld > 0:
+        res_t.copy_(dec_in[0])
+        graph = stack.capture_decode(res_t)
+
+    def step(timers=None):
+        stack.reset()
+        for c in range(n_chunks):
+            work[c].copy_(prompt_in[c])
+        if timers is not None:
+            timers[0].record()
+        for c in range(n_chunks):
+            stack.prefill_chunk(work[c])
+        if timers is not None:
+            timers[1].record()
+        for j in range(Ld):
+            res_t.copy_(dec_in[j])
+            graph.replay()
+            dec_out[j].copy_(res_t)
+        if timers is not None:
+            timers[2].record()
+
+    def barrier():
+        if k > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    mx.probe(args.probe, 4 * n_layers * n_chunks * args.steps + 16)
+    launches0 = mx.launches()
+    timers = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(gpu_smi_id(local)) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        t_start.record()
+        for i in range(args.steps):
+            step(timers[i])
+        t_end.record()
+        torch.cuda.synchronize()
+        barrier()
+    probe_ms = mx.probe_read()
+    mx.probe(args.probe, 0)
+    prefill_launches = mx.launches() - launches0
+    total_ms = t_start.elapsed_time(t_end)
+    ttft = [t[0].elapsed_time(t[1]) for t in timers]
+    dec_ms = [t[1].elapsed_time(t[2]) for t in timers]
+    if k > 1:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / args.steps
+    tokens = B * (Lp + Ld)
+    value = tokens * args.steps / (total_ms / 1000.0)
+
+    # e2e: same metric through the public API with host buffers (pinned H2D in, D2H out)
+    e2e = None
+    if not args.no_e2e:
+        h_prompt = [p.cpu().pin_memory() for p in prompt_in]
+        h_dec = dec_in.cpu().pin_memory()
+        h_out = torch.empty_like(dec_out, device="cpu").pin_memory()
+        h2d = sum(p.numel() * 4 for p in h_prompt) + h_dec.numel() * 4
+        d2h = h_out.numel() * 4
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            for c in range(n_chunks):
+                prompt_in[c].copy_(h_prompt[c], non_blocking=True)
+            dec_in.copy_(h_dec, non_blocking=True)
+            step()
+            h_out.copy_(dec_out, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        e_ms = e0.elapsed_time(e1)
+        if k > 1:
+            tt = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_ms = float(tt.item())
+        e2e = {"value": tokens * args.steps / (e_ms / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    # roofline of the probed (dominant) kernel
+    import json as _j
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = _j.load(f)
+    except Exception:
+        pass
+    Ek, D, R, P = dims.d_inner // k, dims.d_model, dims.dt_rank, dims.dt_rank + 2 * dims.d_state
+    Mc = B * chunk
+    roof = None
+    if probe_ms:
+        avg = statistics.mean(probe_ms)
+        if args.probe in ("in_proj", "out_proj", "x_proj", "dt_proj"):
+            flops = {"in_proj": 2 * Mc * D * 2 * Ek, "out_proj": 2 * Mc * Ek * D, "x_proj": 2 * Mc * Ek * P,
+                     "dt_proj": 2 * Mc * R * Ek}[args.probe]
+            peak = peaks.get("bf16_tflops_sustained", 1394.1)
+            ach = flops / (avg / 1000) / 1e12
+            roof = {"kernel": args.probe, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                    "frac": ach / peak, "traffic": None, "launch_ms": avg, "launches": len(probe_ms),
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
+        else:
+            es = 2
+            byts = {"scan": Mc * Ek * (4 * es) + Mc * 2 * dims.d_state * 4,
+                    "conv": Mc * Ek * 2 * es}.get(args.probe, 0)
+            peak = peaks.get("hbm_gbs", 6535.1)
+            ach = byts / (avg / 1000) / 1e9
+            roof = {"kernel": args.probe, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "traffic": None, "launch_ms": avg, "launches": len(probe_ms),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+
+    cpu = None
+    if rank == 0 and k == 1 and not args.no_cpu:
+        cpu = cpu_baseline(dims, n_layers)
+
+    gpu_launches = prefill_launches + args.steps * Ld * stack.graph_launches
+    if rank == 0:
+        line = {"metric": "batch tokens/sec", "value": value, "unit": "tokens/s", "n_gpus": k, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": f"{args.config}: {n_layers} layers, d_model {dims.d_model}, batch {B}, "
+                                       f"prompt {Lp} + {Ld} decode", "model": args.config, "global_batch": B,
+                           "seq_len": Lp + Ld, "parallelism": f"tp{k}", "ar2": args.ar2 if k > 1 else "none",
+                           "prefill_chunk": chunk, "l2": "inputs larger than L2 (prompt residual "
+                                                         f"{B * Lp * D * 4 / 1e6:.0f} MB > 126 MB)"},
+                "ttft_ms": statistics.mean(ttft), "tpot_ms": statistics.mean(dec_ms) / max(Ld, 1),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if k > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,220 @@
+/*
+ * ssm_tp.h — C ABI of libssmtp.so: the tensor-parallel selective-SSM (Mamba)
+ * mixer forward of arXiv 2602.21144 on B200 (sm_100a).
+ *
+ * The operation (§2.2 fig:mamba_mixer_block; §4.1-4.4):
+ *   xz = x_in W_in,r^T               column-parallel in_proj, packed [x_r || z_r]
+ *   u  = SiLU(causal_conv1d(x_r))    channel-separable, no communication
+ *   dbc = AR#1( u W_x,r^T )          partial SSM-parameter projection + all-reduce
+ *   dt_low, B, C = split(dbc)        column ranges [0,R) [R,R+N) [R+N,R+2N)
+ *   delta = softplus(dt_low W_dt,r^T + b_dt,r)   "shard delta with channels"
+ *   h_t = exp(delta A) h_{t-1} + delta B_t u_t ;  y_t = <C_t, h_t> + D u_t
+ *   g  = y * SiLU(z)                 gate
+ *   residual += AR#2( g W_out,r^T )  row-parallel out_proj, int8 quantised AR
+ * with the SSM cache (conv window + h) carried from chunked prefill into decode
+ * (§4.1).  Readings of points the paper leaves open are listed
+ * in DESIGN.md §Readings.
+ *
+ * Conventions
+ *  - Status: every function returns ssm_status_t (0 = OK).  The message of the
+ *    last error on the calling thread is returned by ssm_last_error().
+ *  - Ownership: the caller (PyTorch) allocates ALL device memory — weights,
+ *    activations, state, workspace, symmetric communication buffers — and keeps
+ *    it alive while handles that reference it exist.  The library never calls
+ *    cudaMalloc; it owns only its host-side handles.
+ *  - Streams: compute calls enqueue on the given stream and return.  Argument
+ *    and shape errors are returned synchronously and nothing is enqueued.
+ *    Device-side protocol failures (peer flag timeout) set an error word that
+ *    ssm_tp_check() reports as SSM_ERR_PROTOCOL.
+ *  - Collectives: with tp_size > 1, ssm_mixer_prefill/decode and
+ *    ssm_qallreduce are collective: every rank calls them in the same order with
+ *    the same (batch, seqlen, n, flags).  TP=1 performs no all-reduce and no
+ *    quantisation (reading Q13).
+ *  - Layouts: activations are token-major row-major [M x C], M = batch*seqlen,
+ *    row m = b*seqlen + t, channels contiguous.  Weight matrices are nn.Linear
+ *    [out, in] of the RANK-LOCAL shard (slicing the packed tensors per logical
+ *    field is the caller's job — PAPER.md:336-345).  All pointers 16-B aligned.
+ *  - dtype: SSM_BF16 = bf16 activations and weight matrices, fp32 accumulation,
+ *    fp32 state, fp32 residual; SSM_FP32 = fp32 everywhere (true fp32 GEMMs,
+ *    no TF32).  Per-channel vectors (conv_w, conv_b, b_dt, a_log, d_skip) are
+ *    always fp32.
+ *  - Threading: one ssm_tp_t per process/GPU; a handle is not thread-safe.
+ *  - No fallback: there is no CPU path and no alternative backend.
+ */
+#ifndef SSM_TP_H
+#define SSM_TP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SSM_OK = 0,
+  SSM_ERR_ARG = 1,         /* null/misaligned pointer, bad flag, buffer too small              */
+  SSM_ERR_DIM = 2,         /* shape mismatch                       */
+  SSM_ERR_SHARD = 3,       /* d_inner % tp_size != 0, or heads not shardable */
+  SSM_ERR_RANK = 4,        /* rank not in [0, tp_size)                            */
+  SSM_ERR_CACHE = 5,       /* state does not belong to this handle / batch mismatch */
+  SSM_ERR_PROTOCOL = 6,    /* collective timeout or order violation          */
+  SSM_ERR_CUDA = 7,        /* CUDA runtime error                                               */
+  SSM_ERR_UNSUPPORTED = 8  /* tp_size > 8, d_state > 16, qar_block does not divide d_model ... */
+} ssm_status_t;
+
+enum { SSM_BF16 = 0, SSM_FP32 = 1 };
+
+/* flags for ssm_mixer_prefill / ssm_mixer_decode / ssm_qallreduce */
+enum {
+  SSM_AR2_INT8 = 0x1,      /* AR#2 = int8 per-block quantised all-reduce (default when tp>1)   */
+  SSM_AR2_FP32 = 0x2,      /* AR#2 = exact fp32 one-shot all-reduce (unquantised arm)           */
+  SSM_AR2_EXTERNAL = 0x4,  /* no AR#2: `residual` receives this rank's fp32 partial out_proj
+                              (overwritten, not added) so the caller can all-reduce it itself
+                              (the NCCL baseline arm)                                            */
+  SSM_QAR_ACCUMULATE = 0x10 /* ssm_qallreduce: out += result instead of out = result            */
+};
+
+enum { SSM_COMM_VIRTUAL = 0x1 }; /* ssm_comm_t.flags: all peer buffers live on THIS device
+                                    (single-GPU virtual ranks, each driven on its own stream) */
+
+typedef struct {
+  int32_t d_model;       /* D                                                        */
+  int32_t d_inner;       /* E = expand * D (global, unsharded)                        */
+  int32_t d_state;       /* N <= 16                                                   */
+  int32_t d_conv;        /* K, 2 <= K <= 8                                            */
+  int32_t dt_rank;       /* R                                                        */
+  int32_t n_heads;       /* x_proj groups H: 1 (Mamba, Falcon-Mamba) or 2 (Zamba);
+                            channel d belongs to head d / (E/H) (reading Q17)           */
+  int32_t dtype;         /* SSM_BF16 | SSM_FP32                                       */
+  int32_t bcdt_rmsnorm;  /* 1: weightless RMSNorm on dt_low, B, C after AR#1 (Falcon-Mamba, Q18) */
+  float rms_eps;         /* eps of that norm (1e-6)                                   */
+  int32_t qar_block;     /* int8 block length along d_model (128; must divide D)      */
+} ssm_config_t;
+
+typedef struct {
+  int32_t rank;          /* r in [0, tp_size)                                         */
+  int32_t tp_size;       /* k in {1..8}                                               */
+  void* const* peer_bufs;/* tp_size device pointers: the symmetric buffer of each rank,
+                            mapped into this process (torch symmetric-memory rendezvous,
+                            or same-device buffers with SSM_COMM_VIRTUAL).  peer_bufs[rank]
+                            is this rank's own buffer.  May be NULL when tp_size == 1.  */
+  size_t buf_bytes;      /* bytes of each symmetric buffer (>= ssm_comm_bytes())       */
+  int32_t flags;         /* SSM_COMM_VIRTUAL or 0                                      */
+} ssm_comm_t;
+
+/* Rank-local weight shard of one mixer layer (E_k = d_inner / tp_size, P = R + 2N,
+ * h_loc = max(1, n_heads / tp_size)).  Matrices in cfg.dtype, vectors fp32.       */
+typedef struct {
+  const void* w_in;      /* [2*E_k, D]  rows [0,E_k) = x of the owned channels,
+                                        rows [E_k,2E_k) = z of the owned channels       */
+  const float* conv_w;   /* [E_k, K]    tap K-1 multiplies the current token            */
+  const float* conv_b;   /* [E_k]                                                       */
+  const void* w_x;       /* [h_loc*P, E_k] block-diagonal over local heads              */
+  const void* w_dt;      /* [E_k, R]                                                    */
+  const float* b_dt;     /* [E_k]                                                       */
+  const float* a_log;    /* [E_k, N]    A = -exp(a_log)                                 */
+  const float* d_skip;   /* [E_k]                                                       */
+  const void* w_out;     /* [D, E_k]                                                    */
+} ssm_layer_weights_t;
+
+typedef struct ssm_tp_s* ssm_tp_t;
+typedef struct ssm_state_s* ssm_state_t;
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* ssm_last_error(void);
+
+/* Library version string. */
+const char* ssm_version(void);
+
+/* Validate cfg/comm and create a handle.  Errors: SSM_ERR_SHARD (d_inner % tp,
+ * head split), SSM_ERR_RANK, SSM_ERR_UNSUPPORTED, SSM_ERR_ARG (buffer too small for
+ * a zero-token call).  Allocates no device memory. */
+ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp_t* out);
+ssm_status_t ssm_tp_destroy(ssm_tp_t tp);
+
+/* Bytes of one rank's symmetric communication buffer for calls of up to
+ * max_tokens (= batch*seqlen) tokens. */
+ssm_status_t ssm_comm_bytes(const ssm_config_t* cfg, int32_t tp_size, int64_t max_tokens, size_t* bytes);
+
+/* Bytes of the per-call workspace for (batch, seqlen). */
+ssm_status_t ssm_workspace_bytes(ssm_tp_t tp, int32_t batch, int32_t seqlen, size_t* bytes);
+
+/* SSM cache of one layer on this rank:
+ *   conv window [batch][K-1][E_k] in cfg.dtype (raw x values, oldest first),
+ *   h           [batch][E_k][N]   fp32.
+ * ssm_state_bytes reports the two sizes; ssm_state_alloc binds caller buffers of
+ * at least those sizes and zero-fills them on `stream` (the prefill start state). */
+ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, size_t* h_bytes);
+ssm_status_t ssm_state_alloc(ssm_tp_t tp, int32_t batch, void* conv_buf, size_t conv_bytes,
+                             void* h_buf, size_t h_bytes, void* stream, ssm_state_t* out);
+ssm_status_t ssm_state_reset(ssm_state_t st, void* stream);
+ssm_status_t ssm_state_free(ssm_state_t st);
+
+/* One mixer layer over a chunk of `seqlen` tokens for `batch` sequences, continuing
+ * from the state (chunked prefill: call again with the next chunk).
+ *   x_in     [batch*seqlen, D] cfg.dtype, replicated on all ranks (block input after the pre-norm)
+ *   residual [batch*seqlen, D] fp32, replicated; residual += mixer(x_in)
+ *            (with SSM_AR2_EXTERNAL: residual := this rank's partial out_proj)
+ *   flags    SSM_AR2_INT8 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL (ignored when tp_size == 1)
+ *   workspace >= ssm_workspace_bytes(batch, seqlen) bytes of device memory, 256-B aligned.
+ * Errors: SSM_ERR_CACHE if st was allocated for another handle or batch;
+ *         SSM_ERR_ARG if the symmetric buffer is too small for batch*seqlen tokens. */
+ssm_status_t ssm_mixer_prefill(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st,
+                               const void* x_in, float* residual, int32_t batch, int32_t seqlen,
+                               uint32_t flags, void* workspace, size_t ws_bytes, void* stream);
+
+/* One decode step (seqlen = 1) reading and updating the state in place.
+ * Same arguments as prefill with seqlen = 1.  Graph-capturable. */
+ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st,
+                              const void* x_in, float* residual, int32_t batch,
+                              uint32_t flags, void* workspace, size_t ws_bytes, void* stream);
+
+/* Quantised all-reduce of n fp32 values (n % qar_block == 0), rows of D = d_model:
+ * every rank quantises its partial per block (s = amax/127, q = rint(o/s) clamped to
+ * +-127), exchanges int8 codes + fp32 scales peer-to-peer, and forms
+ * out = sum_{r=0..k-1} s_r q_r in fixed rank order in fp32 (bitwise identical on all
+ * ranks).  out may alias partial.  tp_size == 1: out = partial (no quantisation).
+ * flags: SSM_QAR_ACCUMULATE.  Error bound per element: sum_r s_r / 2. */
+ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n,
+                            uint32_t flags, void* stream);
+
+/* Pre-norm glue (reading Q16): x[m,:] = residual[m,:] / sqrt(mean(residual[m,:]^2) + eps) * weight,
+ * residual fp32 [M, D] -> x cfg.dtype [M, D]; weight fp32 [D] (may be NULL = ones). */
+ssm_status_t ssm_rmsnorm(ssm_tp_t tp, const float* residual, const float* weight, float eps,
+                         void* x_out, int64_t M, void* stream);
+
+/* Synchronise the stream and report device-side protocol errors (SSM_ERR_PROTOCOL). */
+ssm_status_t ssm_tp_check(ssm_tp_t tp, void* stream);
+
+/* Collective counters: all-reduces issued by this handle, and the
+ * bytes this rank wrote into its symmetric buffer for them. */
+ssm_status_t ssm_tp_stats(ssm_tp_t tp, int64_t* allreduce_count, int64_t* bytes_sent);
+
+/* Kernel launches enqueued by this handle since creation (for bench.py gpu_launches). */
+ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches);
+
+/* Per-kernel timing probe (bench.py roofline): while enabled, the library records a CUDA
+ * event pair on the launching stream around every launch of `kernel` (outside graph
+ * capture), up to `capacity` launches.  capacity 0 disables and releases the events. */
+enum { SSM_PROBE_IN_PROJ = 1, SSM_PROBE_CONV = 2, SSM_PROBE_X_PROJ = 3, SSM_PROBE_DT_PROJ = 4, SSM_PROBE_SCAN = 5,
+       SSM_PROBE_OUT_PROJ = 6, SSM_PROBE_AR2 = 7, SSM_PROBE_DECODE_STEP = 8 };
+ssm_status_t ssm_tp_probe(ssm_tp_t tp, int32_t kernel, int32_t capacity);
+/* Synchronises the recorded events and writes up to `capacity` per-launch durations (ms). */
+ssm_status_t ssm_tp_probe_read(ssm_tp_t tp, float* ms, int32_t capacity, int32_t* n);
+
+/* ------------------------------------------------------------------ test-only */
+/* C = A B^T with A [M,K], B [N,K] (cfg.dtype), C fp32 [M,N]; exercises the GEMM used
+ * by the projections (tcgen05 for bf16 when K*2 % 16 == 0, SIMT otherwise). */
+ssm_status_t ssm_dbg_gemm(ssm_tp_t tp, const void* A, const void* B, float* C,
+                          int32_t M, int32_t N, int32_t K, int32_t swap_ab, int32_t ksplit, void* stream);
+/* Selective scan + D skip + gate on prepared inputs (u, delta, z bf16/fp32 [batch*L, E_k],
+ * z row stride ldz; BC fp32 [batch*L, 2N]); h [batch][E_k][N] fp32 in/out; g out. */
+ssm_status_t ssm_dbg_scan(ssm_tp_t tp, const void* u, const void* delta, const void* z, int32_t ldz,
+                          const float* BC, const float* a_log, const float* d_skip, float* h,
+                          void* g, int32_t batch, int32_t seqlen, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSM_TP_H */

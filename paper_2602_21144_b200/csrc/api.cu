@@ -1,0 +1,632 @@
+// api.cu — C ABI of libssmtp (include/ssm_tp.h): validation, handles, workspace and
+// symmetric-buffer layout, and the per-layer orchestration of the TP mixer
+// (SURVEY.md §3 call stack (2)/(3); §4.1-4.4).
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/ssm_tp.h"
+#include "internal.h"
+
+using namespace ssm;
+
+namespace {
+
+thread_local std::string g_err;
+
+ssm_status_t fail(ssm_status_t code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(expr)                                                                                   \
+  do {                                                                                             \
+    cudaError_t _e = (expr);                                                                       \
+    if (_e != cudaSuccess) return fail(SSM_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+constexpr size_t kSigBytes = 256;  // signal slots [0,32) B, error word at +64 B, epoch counter at +128 B
+
+}  // namespace
+
+struct ssm_tp_s {
+  ssm_config_t cfg;
+  int rank, k, flags;
+  Peers peers;
+  size_t buf_bytes;
+  int Ek, P, hloc, cph;   // local channels, packed width, local heads, channels per local head
+  int ar1_group;          // ranks summed by AR#1 (1 = no AR#1)
+  int bf16, es;           // activation dtype flag and element size
+  uint32_t epoch;
+  int64_t ar_count, bytes_sent, launches;
+  int num_sms;
+  // timing probe
+  int probe_kind = 0, probe_cap = 0, probe_n = 0;
+  cudaEvent_t* probe_ev = nullptr;  // 2 * probe_cap events
+};
+
+struct ssm_state_s {
+  ssm_tp_s* owner;
+  int batch;
+  void* conv;
+  float* h;
+};
+
+namespace {
+
+struct WsLayout {
+  size_t xz, u, dbc, dlow, bc, delta, g, part, total;
+};
+
+WsLayout ws_layout(const ssm_tp_s* t, int64_t M) {
+  WsLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += al256(bytes); return o; };
+  const size_t es = t->es;
+  L.xz = take(M * 2 * t->Ek * es);
+  L.u = take(M * t->Ek * es);
+  L.dbc = take(M * t->hloc * t->P * 4);
+  L.dlow = take((size_t)t->hloc * M * t->cfg.dt_rank * es);
+  L.bc = take((size_t)t->hloc * M * 2 * t->cfg.d_state * 4);
+  L.delta = take(M * t->Ek * es);
+  L.g = take(M * t->Ek * es);
+  L.part = take(t->k > 1 ? M * t->cfg.d_model * 4 : 0);
+  L.total = off;
+  return L;
+}
+
+size_t payload_bytes(const ssm_config_t* c, int k, int64_t M) {
+  const int H = c->n_heads < 1 ? 1 : c->n_heads;
+  const int hloc = H > k ? H / k : 1;
+  const int P = c->dt_rank + 2 * c->d_state;
+  size_t ar1 = (size_t)M * hloc * P * 4;
+  size_t ar2q = al256((size_t)M * c->d_model) + (size_t)M * (c->d_model / (c->qar_block > 0 ? c->qar_block : 128)) * 4;
+  size_t ar2f = (size_t)M * c->d_model * 4;
+  size_t m = ar1 > ar2q ? ar1 : ar2q;
+  return al256(m > ar2f ? m : ar2f);
+}
+
+size_t half_bytes(const ssm_tp_s* t) {
+  if (t->buf_bytes <= kSigBytes) return 0;
+  return ((t->buf_bytes - kSigBytes) / 2) & ~size_t(255);
+}
+
+ssm_status_t validate_cfg(const ssm_config_t* c, int k) {
+  if (!c) return fail(SSM_ERR_ARG, "cfg is NULL");
+  if (c->d_model <= 0 || c->d_inner <= 0 || c->d_state <= 0 || c->d_conv <= 0 || c->dt_rank <= 0)
+    return fail(SSM_ERR_DIM, "non-positive dimension (d_model=%d d_inner=%d d_state=%d d_conv=%d dt_rank=%d)",
+                c->d_model, c->d_inner, c->d_state, c->d_conv, c->dt_rank);
+  if (c->dtype != SSM_BF16 && c->dtype != SSM_FP32) return fail(SSM_ERR_UNSUPPORTED, "dtype %d", c->dtype);
+  if (c->d_state != 16 && c->d_state != 8) return fail(SSM_ERR_UNSUPPORTED, "d_state=%d (supported: 8, 16)", c->d_state);
+  if (c->d_conv < 2 || c->d_conv > 4) return fail(SSM_ERR_UNSUPPORTED, "d_conv=%d (supported: 2..4)", c->d_conv);
+  if (c->dt_rank + 2 * c->d_state > 320) return fail(SSM_ERR_UNSUPPORTED, "dt_rank + 2*d_state > 320");
+  const int H = c->n_heads;
+  if (H < 1 || c->d_inner % H) return fail(SSM_ERR_SHARD, "n_heads=%d does not divide d_inner=%d", H, c->d_inner);
+  if (k < 1 || k > kMaxTP) return fail(SSM_ERR_UNSUPPORTED, "tp_size=%d (supported: 1..8)", k);
+  if (c->d_inner % k) return fail(SSM_ERR_SHARD, "d_inner=%d not divisible by tp_size=%d", c->d_inner, k);
+  if (H % k && k % H) return fail(SSM_ERR_SHARD, "n_heads=%d and tp_size=%d: heads cannot be split evenly", H, k);
+  const int Ek = c->d_inner / k;
+  if (Ek % 8) return fail(SSM_ERR_UNSUPPORTED, "d_inner/tp=%d must be a multiple of 8", Ek);
+  const int cph = H > k ? Ek / (H / k) : Ek;
+  if (cph % 32) return fail(SSM_ERR_UNSUPPORTED, "channels per local head (%d) must be a multiple of 32", cph);
+  if (c->d_model % 16) return fail(SSM_ERR_UNSUPPORTED, "d_model=%d must be a multiple of 16", c->d_model);
+  if (k > 1) {
+    const int blk = c->qar_block;
+    if (!(blk == 32 || blk == 64 || blk == 128 || blk == 256) || c->d_model % blk)
+      return fail(SSM_ERR_UNSUPPORTED, "qar_block=%d must be 32/64/128/256 and divide d_model=%d", blk, c->d_model);
+  }
+  return SSM_OK;
+}
+
+cudaError_t gemm(ssm_tp_s* t, const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
+                 int ksplit, const Epilogue& e, cudaStream_t s) {
+  t->launches++;
+  if (t->bf16 && gemm_tc_supported(A, lda, B, ldb))
+    return gemm_tc_bf16(reinterpret_cast<const __nv_bfloat16*>(A), lda, reinterpret_cast<const __nv_bfloat16*>(B),
+                        ldb, M, N, K, ksplit, e, t->num_sms, s);
+  return gemm_simt(A, lda, B, ldb, t->bf16, M, N, K, ksplit, e, s);
+}
+
+int pick_ksplit(const ssm_tp_s* t, int M, int N, int K) {
+  const int tiles = ((M + 127) / 128) * ((N + 255) / 256);
+  const int kb = (K + 63) / 64;
+  int ks = t->num_sms / (tiles > 0 ? tiles : 1);
+  if (ks > kb) ks = kb;
+  if (ks > 32) ks = 32;
+  return ks < 1 ? 1 : ks;
+}
+
+// RAII probe: records an event pair around the launches in its scope when `kind` is probed.
+struct Probe {
+  ssm_tp_s* t;
+  cudaStream_t s;
+  int idx = -1;
+  Probe(ssm_tp_s* t_, int kind, cudaStream_t s_) : t(t_), s(s_) {
+    if (t->probe_kind != kind || t->probe_n >= t->probe_cap) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    idx = t->probe_n++;
+    cudaEventRecord(t->probe_ev[2 * idx], s);
+  }
+  ~Probe() {
+    if (idx >= 0) cudaEventRecord(t->probe_ev[2 * idx + 1], s);
+  }
+};
+
+Epilogue epi(int kind, int trans, void* C, int64_t ldc, const float* bias = nullptr) {
+  Epilogue e;
+  e.kind = kind;
+  e.trans = trans;
+  e.C = C;
+  e.ldc = ldc;
+  e.bias = bias;
+  return e;
+}
+
+Peers group_peers(const ssm_tp_s* t, int gsize) {
+  Peers p{};
+  const int g0 = (t->rank / gsize) * gsize;
+  for (int i = 0; i < gsize; ++i) p.p[i] = t->peers.p[g0 + i];
+  return p;
+}
+
+// One mixer layer. decode: seqlen == 1 path with in-place state update.
+ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* st, const void* x_in, float* residual,
+                       int batch, int seqlen, uint32_t flags, void* ws, bool decode, cudaStream_t s) {
+  const ssm_config_t& c = t->cfg;
+  const int64_t M = (int64_t)batch * seqlen;
+  const int D = c.d_model, Ek = t->Ek, R = c.dt_rank, N = c.d_state, K = c.d_conv, P = t->P, hl = t->hloc;
+  const int bf = t->bf16;
+  const WsLayout L = ws_layout(t, M);
+  char* W = reinterpret_cast<char*>(ws);
+  void* xz = W + L.xz;
+  void* u = W + L.u;
+  float* dbc = reinterpret_cast<float*>(W + L.dbc);
+  void* dlow = W + L.dlow;
+  float* BC = reinterpret_cast<float*>(W + L.bc);
+  void* delta = W + L.delta;
+  void* g = W + L.g;
+  float* part = reinterpret_cast<float*>(W + L.part);
+  const int kst = bf ? EPI_STORE_BF16 : EPI_STORE_F32;
+  const int ksp = bf ? EPI_SOFTPLUS_BF16 : EPI_SOFTPLUS_F32;
+  const bool swap = decode && bf;  // swap-AB: weights fill the 128-row MMA tile, batch is N
+  const size_t es = t->es;
+  const size_t half = half_bytes(t);
+  auto own_half = [&](uint32_t ep) -> char* {
+    return reinterpret_cast<char*>(t->peers.p[t->rank]) + kSigBytes + (ep & 1) * half;
+  };
+  auto half_off = [&](uint32_t ep) -> int64_t { return (int64_t)(kSigBytes + (ep & 1) * half); };
+
+  // (a1) in_proj, column-parallel: xz = x_in W_in,r^T   [M, 2E_k]
+  {
+  Probe pr(t, SSM_PROBE_IN_PROJ, s);
+  if (swap)
+    CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s));
+  else
+    CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, epi(kst, 0, xz, 2 * Ek), s));
+  }
+
+  // (a2) conv1d + SiLU, rank-local; conv window of the cache updated
+  if (decode) {
+    t->launches++;
+    CU(launch_conv_decode(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, Ek, K, s));
+  } else {
+    Probe pr(t, SSM_PROBE_CONV, s);
+    t->launches += 2;
+    CU(launch_conv1d_silu(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, seqlen, Ek, K, s));
+    CU(launch_conv_state_update(bf, xz, 2 * Ek, st->conv, batch, seqlen, Ek, K, s));
+  }
+
+  // (a3) x_proj partial [M, hloc*P] fp32, straight into the symmetric buffer when AR#1 follows
+  const bool ar1 = t->ar1_group > 1;
+  uint32_t ep1 = 0;
+  float* xdst = dbc;
+  if (ar1) {
+    ep1 = ++t->epoch;
+    xdst = reinterpret_cast<float*>(own_half(ep1));
+    t->ar_count++;
+    t->bytes_sent += M * hl * P * 4;
+  }
+  {
+  Probe pr(t, SSM_PROBE_X_PROJ, s);
+  if (swap) {
+    const int ks = pick_ksplit(t, hl * P, (int)M, Ek);
+    if (ks > 1) CU(cudaMemsetAsync(xdst, 0, (size_t)M * hl * P * 4, s));
+    CU(gemm(t, w->w_x, Ek, u, Ek, hl * P, (int)M, Ek, ks, epi(ks > 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s));
+  } else {
+    CU(gemm(t, u, Ek, w->w_x, Ek, (int)M, hl * P, Ek, 1, epi(EPI_STORE_F32, 0, xdst, hl * P), s));
+  }
+  }
+
+  // (a4) AR#1 (fixed rank order within the head group) + unpack dt_low / B / C
+  if (ar1) {
+    t->launches += 2;
+    CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
+    CU(launch_unpack(bf, group_peers(t, t->ar1_group), t->ar1_group, half_off(ep1), (int)M, hl, R, N,
+                     c.bcdt_rmsnorm, c.rms_eps, dlow, BC, s));
+  } else {
+    Peers one{};
+    one.p[0] = dbc;
+    t->launches++;
+    CU(launch_unpack(bf, one, 1, 0, (int)M, hl, R, N, c.bcdt_rmsnorm, c.rms_eps, dlow, BC, s));
+  }
+
+  // (a5)+(a6)+(a7) dt_proj + softplus, selective scan, D skip, gate
+  if (decode) {
+    Probe pr(t, SSM_PROBE_DECODE_STEP, s);
+    t->launches++;
+    CU(launch_decode_step(bf, u, reinterpret_cast<char*>(xz) + Ek * es, 2 * Ek, dlow, BC, w->w_dt, w->b_dt,
+                          w->a_log, w->d_skip, st->h, g, batch, Ek, R, N, t->cph, hl, s));
+  } else {
+    {
+    Probe pr(t, SSM_PROBE_DT_PROJ, s);
+    for (int j = 0; j < hl; ++j) {
+      const int c0 = j * t->cph;
+      const char* dl_j = reinterpret_cast<const char*>(dlow) + (size_t)j * M * R * es;
+      CU(gemm(t, dl_j, R, reinterpret_cast<const char*>(w->w_dt) + (size_t)c0 * R * es, R, (int)M, t->cph, R, 1,
+              epi(ksp, 0, reinterpret_cast<char*>(delta) + c0 * es, Ek, w->b_dt + c0), s));
+    }
+    }
+    Probe pr(t, SSM_PROBE_SCAN, s);
+    for (int j = 0; j < hl; ++j) {
+      const int c0 = j * t->cph;
+      t->launches++;
+      CU(launch_scan(bf, bf, reinterpret_cast<char*>(u) + c0 * es, Ek, reinterpret_cast<char*>(delta) + c0 * es, Ek,
+                     reinterpret_cast<char*>(xz) + (Ek + c0) * es, 2 * Ek, BC + (size_t)j * M * 2 * N, 2 * N,
+                     w->a_log + (size_t)c0 * N, w->d_skip + c0, st->h + (size_t)c0 * N, (int64_t)Ek * N,
+                     reinterpret_cast<char*>(g) + c0 * es, Ek, batch, seqlen, t->cph, N, s));
+    }
+  }
+
+  // (a8)+(a9) out_proj, row-parallel partial, finished by AR#2 at the residual boundary
+  const int64_t nD = M * D;
+  auto out_gemm = [&](float* dst, bool accumulate_into) -> cudaError_t {
+    // dst += partial (accumulate_into) or dst = partial
+    if (swap) {
+      const int ks = pick_ksplit(t, D, (int)M, Ek);
+      if (ks > 1 || accumulate_into) {
+        if (!accumulate_into) {
+          cudaError_t e = cudaMemsetAsync(dst, 0, nD * 4, s);
+          if (e != cudaSuccess) return e;
+        }
+        return gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks, epi(EPI_ATOMIC_F32, 1, dst, D), s);
+      }
+      return gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, 1, epi(EPI_STORE_F32, 1, dst, D), s);
+    }
+    return gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(accumulate_into ? EPI_ADD_F32 : EPI_STORE_F32, 0, dst, D), s);
+  };
+  Probe pr(t, SSM_PROBE_OUT_PROJ, s);
+  if (t->k == 1) {
+    CU(out_gemm(residual, true));
+  } else if (flags & SSM_AR2_EXTERNAL) {
+    CU(out_gemm(residual, false));
+  } else if (flags & SSM_AR2_FP32) {
+    const uint32_t ep = ++t->epoch;
+    CU(out_gemm(reinterpret_cast<float*>(own_half(ep)), false));
+    t->ar_count++;
+    t->bytes_sent += nD * 4;
+    t->launches += 2;
+    CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
+    CU(launch_f32_reduce(t->peers, t->k, half_off(ep), nD, residual, 1, s));
+  } else {  // SSM_AR2_INT8 (default)
+    const uint32_t ep = ++t->epoch;
+    CU(out_gemm(part, false));
+    int8_t* q = reinterpret_cast<int8_t*>(own_half(ep));
+    float* sc = reinterpret_cast<float*>(own_half(ep) + al256(nD));
+    t->launches += 3;
+    CU(launch_quantize(part, nD, c.qar_block, q, sc, s));
+    t->ar_count++;
+    t->bytes_sent += nD + nD / c.qar_block * 4;
+    CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
+    CU(launch_qar_reduce(t->peers, t->k, half_off(ep), half_off(ep) + (int64_t)al256(nD), nD, c.qar_block, residual,
+                         1, s));
+  }
+  return SSM_OK;
+}
+
+ssm_status_t check_call(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* st, const void* x_in,
+                        const float* residual, int batch, int seqlen, uint32_t flags, void* ws, size_t ws_bytes) {
+  if (!t) return fail(SSM_ERR_ARG, "tp handle is NULL");
+  if (!w || !w->w_in || !w->conv_w || !w->conv_b || !w->w_x || !w->w_dt || !w->b_dt || !w->a_log || !w->d_skip ||
+      !w->w_out)
+    return fail(SSM_ERR_ARG, "weights struct or one of its pointers is NULL");
+  if (!st) return fail(SSM_ERR_ARG, "state is NULL");
+  if (st->owner != t) return fail(SSM_ERR_CACHE, "state belongs to another handle");
+  if (st->batch != batch) return fail(SSM_ERR_CACHE, "state batch %d != call batch %d", st->batch, batch);
+  if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
+  if (!x_in || !residual) return fail(SSM_ERR_ARG, "x_in/residual is NULL");
+  if ((reinterpret_cast<uintptr_t>(x_in) | reinterpret_cast<uintptr_t>(residual)) & 15)
+    return fail(SSM_ERR_ARG, "x_in/residual must be 16-B aligned");
+  if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL))
+    return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  const int nmode = !!(flags & SSM_AR2_INT8) + !!(flags & SSM_AR2_FP32) + !!(flags & SSM_AR2_EXTERNAL);
+  if (nmode > 1) return fail(SSM_ERR_ARG, "at most one AR#2 mode flag");
+  const int64_t M = (int64_t)batch * seqlen;
+  const WsLayout L = ws_layout(t, M);
+  if (M > 0 && (!ws || ws_bytes < L.total))
+    return fail(SSM_ERR_ARG, "workspace %zu B < required %zu B", ws_bytes, L.total);
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(SSM_ERR_ARG, "workspace must be 256-B aligned");
+  if (t->k > 1 && !(flags & SSM_AR2_EXTERNAL) && payload_bytes(&t->cfg, t->k, M) > half_bytes(t))
+    return fail(SSM_ERR_ARG, "symmetric buffer (%zu B) too small for %lld tokens (need %zu B)", t->buf_bytes,
+                (long long)M, kSigBytes + 2 * payload_bytes(&t->cfg, t->k, M));
+  return SSM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ssm_last_error(void) { return g_err.c_str(); }
+const char* ssm_version(void) { return "libssmtp 0.1 (sm_100a)"; }
+
+ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp_t* out) {
+  if (!out) return fail(SSM_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (!comm) return fail(SSM_ERR_ARG, "comm is NULL");
+  const int k = comm->tp_size;
+  if (k < 1 || k > kMaxTP) return fail(SSM_ERR_UNSUPPORTED, "tp_size=%d (supported: 1..8)", k);
+  if (comm->rank < 0 || comm->rank >= k) return fail(SSM_ERR_RANK, "rank %d not in [0,%d)", comm->rank, k);
+  ssm_status_t st = validate_cfg(cfg, k);
+  if (st != SSM_OK) return st;
+  if (k > 1) {
+    if (!comm->peer_bufs) return fail(SSM_ERR_ARG, "peer_bufs is NULL with tp_size=%d", k);
+    for (int i = 0; i < k; ++i)
+      if (!comm->peer_bufs[i] || (reinterpret_cast<uintptr_t>(comm->peer_bufs[i]) & 255))
+        return fail(SSM_ERR_ARG, "peer_bufs[%d] is NULL or not 256-B aligned", i);
+    if (comm->buf_bytes < kSigBytes + 2 * payload_bytes(cfg, k, 1))
+      return fail(SSM_ERR_ARG, "buf_bytes=%zu too small", comm->buf_bytes);
+  }
+  ssm_tp_s* t = new (std::nothrow) ssm_tp_s();
+  if (!t) return fail(SSM_ERR_ARG, "out of host memory");
+  t->cfg = *cfg;
+  if (t->cfg.qar_block <= 0) t->cfg.qar_block = 128;
+  t->rank = comm->rank;
+  t->k = k;
+  t->flags = comm->flags;
+  for (int i = 0; i < k && comm->peer_bufs; ++i) t->peers.p[i] = comm->peer_bufs[i];
+  t->buf_bytes = comm->buf_bytes;
+  const int H = cfg->n_heads;
+  t->Ek = cfg->d_inner / k;
+  t->P = cfg->dt_rank + 2 * cfg->d_state;
+  t->hloc = H > k ? H / k : 1;
+  t->cph = t->Ek / t->hloc;
+  t->ar1_group = k > H ? k / H : 1;
+  t->bf16 = cfg->dtype == SSM_BF16;
+  t->es = t->bf16 ? 2 : 4;
+  t->epoch = 0;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+    t->num_sms = sms;
+  else {
+    cudaGetLastError();
+    t->num_sms = 148;
+  }
+  *out = t;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_destroy(ssm_tp_t tp) {
+  if (tp) ssm_tp_probe(tp, 0, 0);
+  delete tp;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_probe(ssm_tp_t tp, int32_t kernel, int32_t capacity) {
+  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
+  if (capacity < 0) return fail(SSM_ERR_ARG, "capacity < 0");
+  if (tp->probe_ev) {
+    for (int i = 0; i < 2 * tp->probe_cap; ++i) cudaEventDestroy(tp->probe_ev[i]);
+    delete[] tp->probe_ev;
+    tp->probe_ev = nullptr;
+  }
+  tp->probe_kind = 0;
+  tp->probe_cap = 0;
+  tp->probe_n = 0;
+  if (capacity == 0) return SSM_OK;
+  tp->probe_ev = new (std::nothrow) cudaEvent_t[2 * capacity];
+  if (!tp->probe_ev) return fail(SSM_ERR_ARG, "out of host memory");
+  for (int i = 0; i < 2 * capacity; ++i) CU(cudaEventCreate(&tp->probe_ev[i]));
+  tp->probe_kind = kernel;
+  tp->probe_cap = capacity;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_probe_read(ssm_tp_t tp, float* ms, int32_t capacity, int32_t* n) {
+  if (!tp || !n) return fail(SSM_ERR_ARG, "NULL argument");
+  const int cnt = tp->probe_n < capacity ? tp->probe_n : capacity;
+  for (int i = 0; i < cnt; ++i) {
+    CU(cudaEventSynchronize(tp->probe_ev[2 * i + 1]));
+    CU(cudaEventElapsedTime(&ms[i], tp->probe_ev[2 * i], tp->probe_ev[2 * i + 1]));
+  }
+  *n = cnt;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_comm_bytes(const ssm_config_t* cfg, int32_t tp_size, int64_t max_tokens, size_t* bytes) {
+  if (!bytes) return fail(SSM_ERR_ARG, "bytes is NULL");
+  ssm_status_t st = validate_cfg(cfg, tp_size);
+  if (st != SSM_OK) return st;
+  if (max_tokens < 1) max_tokens = 1;
+  *bytes = kSigBytes + 2 * payload_bytes(cfg, tp_size, max_tokens);
+  return SSM_OK;
+}
+
+ssm_status_t ssm_workspace_bytes(ssm_tp_t tp, int32_t batch, int32_t seqlen, size_t* bytes) {
+  if (!tp || !bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
+  *bytes = ws_layout(tp, (int64_t)batch * seqlen).total;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, size_t* h_bytes) {
+  if (!tp || !conv_bytes || !h_bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
+  *conv_bytes = (size_t)batch * (tp->cfg.d_conv - 1) * tp->Ek * tp->es;
+  *h_bytes = (size_t)batch * tp->Ek * tp->cfg.d_state * 4;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_state_alloc(ssm_tp_t tp, int32_t batch, void* conv_buf, size_t conv_bytes, void* h_buf,
+                             size_t h_bytes, void* stream, ssm_state_t* out) {
+  if (!out) return fail(SSM_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  size_t cb = 0, hb = 0;
+  ssm_status_t s = ssm_state_bytes(tp, batch, &cb, &hb);
+  if (s != SSM_OK) return s;
+  if (!conv_buf || !h_buf) return fail(SSM_ERR_ARG, "state buffers are NULL");
+  if (conv_bytes < cb || h_bytes < hb)
+    return fail(SSM_ERR_ARG, "state buffers too small (%zu/%zu B, need %zu/%zu B)", conv_bytes, h_bytes, cb, hb);
+  if ((reinterpret_cast<uintptr_t>(conv_buf) | reinterpret_cast<uintptr_t>(h_buf)) & 15)
+    return fail(SSM_ERR_ARG, "state buffers must be 16-B aligned");
+  ssm_state_s* st = new (std::nothrow) ssm_state_s();
+  if (!st) return fail(SSM_ERR_ARG, "out of host memory");
+  st->owner = tp;
+  st->batch = batch;
+  st->conv = conv_buf;
+  st->h = reinterpret_cast<float*>(h_buf);
+  cudaStream_t s_ = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(conv_buf, 0, cb, s_) != cudaSuccess || cudaMemsetAsync(h_buf, 0, hb, s_) != cudaSuccess) {
+    delete st;
+    return fail(SSM_ERR_CUDA, "zero-fill of the state failed: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  *out = st;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_state_reset(ssm_state_t st, void* stream) {
+  if (!st) return fail(SSM_ERR_ARG, "state is NULL");
+  size_t cb = 0, hb = 0;
+  ssm_state_bytes(st->owner, st->batch, &cb, &hb);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CU(cudaMemsetAsync(st->conv, 0, cb, s));
+  CU(cudaMemsetAsync(st->h, 0, hb, s));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_state_free(ssm_state_t st) {
+  delete st;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_mixer_prefill(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, const void* x_in,
+                               float* residual, int32_t batch, int32_t seqlen, uint32_t flags, void* workspace,
+                               size_t ws_bytes, void* stream) {
+  ssm_status_t s = check_call(tp, w, st, x_in, residual, batch, seqlen, flags, workspace, ws_bytes);
+  if (s != SSM_OK) return s;
+  if ((int64_t)batch * seqlen == 0) return SSM_OK;
+  return run_layer(tp, w, st, x_in, residual, batch, seqlen, flags, workspace, false,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, const void* x_in,
+                              float* residual, int32_t batch, uint32_t flags, void* workspace, size_t ws_bytes,
+                              void* stream) {
+  ssm_status_t s = check_call(tp, w, st, x_in, residual, batch, 1, flags, workspace, ws_bytes);
+  if (s != SSM_OK) return s;
+  if (batch == 0) return SSM_OK;
+  return run_layer(tp, w, st, x_in, residual, batch, 1, flags, workspace, true,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
+  if (!tp || !partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
+  if (flags & ~(uint32_t)SSM_QAR_ACCUMULATE) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  const int blk = tp->cfg.qar_block;
+  if (n % blk) return fail(SSM_ERR_DIM, "n=%zu not a multiple of qar_block=%d", n, blk);
+  if ((reinterpret_cast<uintptr_t>(partial) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool acc = flags & SSM_QAR_ACCUMULATE;
+  if (n == 0) return SSM_OK;
+  if (tp->k == 1) {  // reading Q13: no quantisation at TP=1
+    Peers one{};
+    one.p[0] = const_cast<float*>(partial);
+    tp->launches++;
+    CU(launch_f32_reduce(one, 1, 0, (int64_t)n, out, acc, s));
+    return SSM_OK;
+  }
+  const size_t need = al256(n) + n / blk * 4;
+  if (need > half_bytes(tp)) return fail(SSM_ERR_ARG, "symmetric buffer too small for n=%zu", n);
+  const uint32_t ep = ++tp->epoch;
+  const size_t half = half_bytes(tp);
+  char* own = reinterpret_cast<char*>(tp->peers.p[tp->rank]) + kSigBytes + (ep & 1) * half;
+  const int64_t off = (int64_t)(kSigBytes + (ep & 1) * half);
+  tp->launches += 3;
+  CU(launch_quantize(partial, (int64_t)n, blk, reinterpret_cast<int8_t*>(own), reinterpret_cast<float*>(own + al256(n)), s));
+  tp->ar_count++;
+  tp->bytes_sent += n + n / blk * 4;
+  CU(launch_peer_barrier(tp->peers, tp->rank, tp->k, s));
+  CU(launch_qar_reduce(tp->peers, tp->k, off, off + (int64_t)al256(n), (int64_t)n, blk, out, acc, s));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_rmsnorm(ssm_tp_t tp, const float* residual, const float* weight, float eps, void* x_out, int64_t M,
+                         void* stream) {
+  if (!tp || !residual || !x_out) return fail(SSM_ERR_ARG, "NULL argument");
+  if ((reinterpret_cast<uintptr_t>(residual) | reinterpret_cast<uintptr_t>(weight) | reinterpret_cast<uintptr_t>(x_out)) & 15)
+    return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
+  tp->launches++;
+  CU(launch_rmsnorm(tp->bf16, residual, weight, eps, x_out, M, tp->cfg.d_model, reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_check(ssm_tp_t tp, void* stream) {
+  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
+  CU(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+  if (tp->k > 1) {
+    uint32_t errw = 0;
+    CU(cudaMemcpy(&errw, reinterpret_cast<char*>(tp->peers.p[tp->rank]) + 64, 4, cudaMemcpyDeviceToHost));
+    if (errw) return fail(SSM_ERR_PROTOCOL, "peer flag wait timed out on rank %d (epoch %u)", tp->rank, tp->epoch);
+  }
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_stats(ssm_tp_t tp, int64_t* allreduce_count, int64_t* bytes_sent) {
+  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
+  if (allreduce_count) *allreduce_count = tp->ar_count;
+  if (bytes_sent) *bytes_sent = tp->bytes_sent;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches) {
+  if (!tp || !launches) return fail(SSM_ERR_ARG, "NULL argument");
+  *launches = tp->launches;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_dbg_gemm(ssm_tp_t tp, const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
+                          int32_t swap_ab, int32_t ksplit, void* stream) {
+  if (!tp || !A || !B || !C) return fail(SSM_ERR_ARG, "NULL argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (ksplit > 1) CU(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
+  const int kind = ksplit > 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32;
+  if (swap_ab)
+    CU(gemm(tp, B, K, A, K, N, M, K, ksplit, epi(kind, 1, C, N), s));
+  else
+    CU(gemm(tp, A, K, B, K, M, N, K, ksplit, epi(kind, 0, C, N), s));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_dbg_scan(ssm_tp_t tp, const void* u, const void* delta, const void* z, int32_t ldz, const float* BC,
+                          const float* a_log, const float* d_skip, float* h, void* g, int32_t batch, int32_t seqlen,
+                          void* stream) {
+  if (!tp || !u || !delta || !z || !BC || !a_log || !d_skip || !h || !g) return fail(SSM_ERR_ARG, "NULL argument");
+  const int Ek = tp->Ek, N = tp->cfg.d_state;
+  tp->launches++;
+  CU(launch_scan(tp->bf16, tp->bf16, u, Ek, delta, Ek, z, ldz, BC, 2 * N, a_log, d_skip, h, (int64_t)Ek * N, g, Ek,
+                 batch, seqlen, Ek, N, reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+}  // extern "C"

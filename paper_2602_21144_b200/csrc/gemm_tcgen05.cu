@@ -1,0 +1,330 @@
+// gemm_tcgen05.cu — persistent warp-specialised bf16 GEMM for sm_100a.
+//
+// C = A B^T, A [M,K] and B [N,K] K-major bf16 (activations x nn.Linear weights),
+// fp32 accumulation in TMEM.  Used for the token-wise projections of the mixer
+// ("token-wise matrix multiplications"): in_proj, x_proj, dt_proj,
+// out_proj.
+//
+// Structure (one CTA per SM, persistent over output tiles):
+//   warp 0  : TMA producer — cp.async.bulk.tensor 2D loads of A (128 x 64) and
+//             B (BN x 64) tiles, SWIZZLE_128B, into a 4-stage smem ring (mbarrier full/empty)
+//   warp 1  : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per
+//             instruction), commits to the smem-empty barriers and the TMEM-full barrier
+//   warps 2-5: epilogue — tcgen05.ld 32x32b.x32 TMEM -> registers, fused epilogue op
+//             (bf16 store / fp32 store / softplus(+bias) / fp32 add / fp32 atomic add),
+//             optionally transposed for swap-AB decode GEMMs.
+// TMEM holds two 256-column accumulators so the epilogue of tile i overlaps the MMAs
+// of tile i+1.  Split-K (ksplit > 1) requires the atomic epilogue.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace ssm {
+
+namespace {
+constexpr int BM = 128, BK = 64, STAGES = 4, BN_MAX = 256;
+constexpr int A_STAGE = BM * BK * 2;      // 16 KB
+constexpr int B_STAGE = BN_MAX * BK * 2;  // 32 KB
+constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + 256;
+constexpr int kThreads = 192;
+
+struct TileSched {
+  int m_tiles, n_tiles, kb_total, kbs, ksplit, units;
+  __device__ void decode(int u, int& mt, int& nt, int& kb0, int& kb1) const {
+    nt = u % n_tiles;
+    int rest = u / n_tiles;
+    mt = rest % m_tiles;
+    int ks = rest / m_tiles;
+    kb0 = ks * kbs;
+    kb1 = min(kb_total, kb0 + kbs);
+  }
+};
+
+__device__ __forceinline__ void epi_store32(const Epilogue& e, int m, int n0, int M, int N, const uint32_t (&r)[32]) {
+  if (m >= M) return;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  const int kind = e.kind;
+  if (kind == EPI_SOFTPLUS_BF16 || kind == EPI_SOFTPLUS_F32) {
+    const float* b = e.bias + (e.trans ? 0 : n0);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float bb = e.trans ? e.bias[m] : ((n0 + j < N) ? b[j] : 0.f);
+      v[j] = softplus(v[j] + bb);
+    }
+  }
+  const bool full = (n0 + 32 <= N);
+  if (!e.trans) {
+    const int64_t base = (int64_t)m * e.ldc + n0;
+    if (kind == EPI_STORE_BF16 || kind == EPI_SOFTPLUS_BF16) {
+      __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(e.C) + base;
+      if (full && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 pk;
+          uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]);
+            pw[j] = *reinterpret_cast<uint32_t*>(&t2);
+          }
+          reinterpret_cast<uint4*>(C)[q] = pk;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < N) C[j] = __float2bfloat16_rn(v[j]);
+      }
+    } else {
+      float* C = reinterpret_cast<float*>(e.C) + base;
+      if (kind == EPI_STORE_F32 || kind == EPI_SOFTPLUS_F32) {
+        if (full && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            reinterpret_cast<float4*>(C)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (n0 + j < N) C[j] = v[j];
+        }
+      } else if (kind == EPI_ADD_F32) {
+        if (full && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 o = reinterpret_cast<float4*>(C)[q];
+            o.x += v[4 * q]; o.y += v[4 * q + 1]; o.z += v[4 * q + 2]; o.w += v[4 * q + 3];
+            reinterpret_cast<float4*>(C)[q] = o;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (n0 + j < N) C[j] += v[j];
+        }
+      } else {  // EPI_ATOMIC_F32
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < N) atomicAdd(C + j, v[j]);
+      }
+    }
+  } else {
+    // transposed: element (m, n) -> C[n * ldc + m]; lanes hold consecutive m -> coalesced per n
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = n0 + j;
+      if (n >= N) break;
+      const int64_t idx = (int64_t)n * e.ldc + m;
+      switch (kind) {
+        case EPI_STORE_BF16:
+        case EPI_SOFTPLUS_BF16:
+          reinterpret_cast<__nv_bfloat16*>(e.C)[idx] = __float2bfloat16_rn(v[j]);
+          break;
+        case EPI_STORE_F32:
+        case EPI_SOFTPLUS_F32:
+          reinterpret_cast<float*>(e.C)[idx] = v[j];
+          break;
+        case EPI_ADD_F32:
+          reinterpret_cast<float*>(e.C)[idx] += v[j];
+          break;
+        default:
+          atomicAdd(reinterpret_cast<float*>(e.C) + idx, v[j]);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int BN, TileSched ts, Epilogue epi) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t ph = 0;
+      const uint32_t tx = (uint32_t)(BM + BN) * BK * 2;
+      for (int u = blockIdx.x; u < ts.units; u += gridDim.x) {
+        int mt, nt, kb0, kb1;
+        ts.decode(u, mt, nt, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], ph ^ 1);
+          mbar_arrive_expect_tx(&full[stage], tx);
+          tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, mt * BM);
+          tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, nt * BN);
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread)
+      const uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      for (int u = blockIdx.x; u < ts.units; u += gridDim.x) {
+        int mt, nt, kb0, kb1;
+        ts.decode(u, mt, nt, kb0, kb1);
+        if (kb0 >= kb1) continue;
+        mbar_wait(&tempty[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * BN_MAX);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * A_STAGE);
+          const uint32_t b0 = smem_u32(sB + stage * B_STAGE);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            umma_bf16(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                      (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5; TMEM lane group = warp % 4
+    const int eg = warp & 3;
+    const int row = eg * 32 + lane;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int u = blockIdx.x; u < ts.units; u += gridDim.x) {
+      int mt, nt, kb0, kb1;
+      ts.decode(u, mt, nt, kb0, kb1);
+      if (kb0 >= kb1) continue;
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      const int m = mt * BM + row;
+      const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * BN_MAX);
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tbase + c * 32, r);
+        tmem_ld_wait();
+        epi_store32(epi, m, nt * BN + c * 32, M, N, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+}  // namespace
+
+bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb) {
+  return ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) &&
+         ((lda * 2) % 16 == 0) && ((ldb * 2) % 16 == 0) && get_encode() != nullptr;
+}
+
+cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
+                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  // BN: multiple of 32 in [32, 256] (UMMA needs N % 16 == 0; the epilogue drains TMEM in
+  // 32-column chunks) covering N in as few tiles as possible
+  int n_tiles = (N + BN_MAX - 1) / BN_MAX;
+  int BN = (N + n_tiles - 1) / n_tiles;
+  BN = (BN + 31) / 32 * 32;
+  n_tiles = (N + BN - 1) / BN;
+  TileSched ts;
+  ts.m_tiles = (M + BM - 1) / BM;
+  ts.n_tiles = n_tiles;
+  ts.kb_total = (K + BK - 1) / BK;
+  if (ksplit < 1) ksplit = 1;
+  if (ksplit > ts.kb_total) ksplit = ts.kb_total;
+  ts.kbs = (ts.kb_total + ksplit - 1) / ksplit;
+  ts.ksplit = (ts.kb_total + ts.kbs - 1) / ts.kbs;
+  ts.units = ts.m_tiles * ts.n_tiles * ts.ksplit;
+  if (ts.ksplit > 1 && epi.kind != EPI_ATOMIC_F32) return cudaErrorInvalidValue;
+
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, lda, BM)) return cudaErrorInvalidValue;
+  if (!make_map(&mb, B, N, K, ldb, BN)) return cudaErrorInvalidValue;
+
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int grid = ts.units < num_sms ? ts.units : num_sms;
+  gemm_tc_kernel<<<grid, kThreads, SMEM_BYTES, s>>>(ma, mb, M, N, BN, ts, epi);
+  return cudaGetLastError();
+}
+
+}  // namespace ssm

@@ -1,0 +1,78 @@
+// internal.h — launchers shared between the kernels and the C-ABI layer (api.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace ssm {
+
+constexpr int kMaxTP = 8;
+constexpr int kMaxState = 16;
+
+// GEMM epilogue: C = A B^T (+ op).  Logical output element (m, n), m < M rows of A,
+// n < N rows of B.  trans = 1 stores C[n * ldc + m] (swap-AB decode: A = weights).
+enum EpiKind : int {
+  EPI_STORE_BF16 = 0,     // C bf16 = acc
+  EPI_STORE_F32 = 1,      // C f32 = acc
+  EPI_SOFTPLUS_BF16 = 2,  // C bf16 = softplus(acc + bias[feature])
+  EPI_SOFTPLUS_F32 = 3,   // C f32  = softplus(acc + bias[feature])
+  EPI_ADD_F32 = 4,        // C f32 += acc            (read-modify-write; ksplit must be 1)
+  EPI_ATOMIC_F32 = 5,     // C f32 += acc atomically (split-K; C pre-initialised)
+};
+
+struct Epilogue {
+  int kind;
+  int trans;
+  void* C;
+  int64_t ldc;
+  const float* bias;  // indexed by the output feature: n (trans=0) or m (trans=1)
+};
+
+struct Peers {
+  void* p[kMaxTP];
+};
+
+// ---- GEMM launchers (return cudaSuccess or the launch error) ----
+// tcgen05/TMEM/TMA bf16 GEMM: A [M,K] row stride lda, B [N,K] row stride ldb (elements).
+// Requires lda*2 % 16 == 0, ldb*2 % 16 == 0, 16-B aligned bases.
+cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
+                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s);
+bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb);
+// SIMT GEMM, fp32 accumulation, T = float or bf16 inputs.
+cudaError_t gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, int dtype_bf16, int M, int N, int K,
+                      int ksplit, const Epilogue& epi, cudaStream_t s);
+
+// ---- mixer kernels (T = bf16 if bf16 != 0 else float) ----
+cudaError_t launch_conv1d_silu(int bf16, const void* xz, int64_t ldxz, const void* conv_state, const float* conv_w,
+                               const float* conv_b, void* u, int64_t ldu, int batch, int L, int Ek, int K,
+                               cudaStream_t s);
+cudaError_t launch_conv_state_update(int bf16, const void* xz, int64_t ldxz, void* conv_state, int batch, int L,
+                                     int Ek, int K, cudaStream_t s);
+cudaError_t launch_conv_decode(int bf16, const void* xz, int64_t ldxz, void* conv_state, const float* conv_w,
+                               const float* conv_b, void* u, int64_t ldu, int batch, int Ek, int K, cudaStream_t s);
+// Sum k_src fp32 partials [M, ldp] (fixed order), optional per-field RMSNorm, split into
+// dt_low (T, [hloc][M][R]) and BC (f32, [hloc][M][2N]).
+cudaError_t launch_unpack(int bf16, Peers src, int nsrc, int64_t src_off_bytes, int M, int hloc, int R, int N,
+                          int rmsnorm, float eps, void* dlow, float* BC, cudaStream_t s);
+cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const void* delta, int64_t ldd,
+                        const void* z, int64_t ldz, const float* BC, int64_t ldbc, const float* a_log,
+                        const float* d_skip, float* h, int64_t h_bstride, void* g, int64_t ldg, int batch, int L,
+                        int nch, int N, cudaStream_t s);
+cudaError_t launch_decode_step(int bf16, const void* u, const void* z, int64_t ldz, const void* dlow,
+                               const float* BC, const void* w_dt, const float* b_dt, const float* a_log,
+                               const float* d_skip, float* h, void* g, int batch, int Ek, int R, int N,
+                               int ch_per_head, int hloc, cudaStream_t s);
+cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
+                           cudaStream_t s);
+// int8 quantisation of n fp32 values in blocks of blk: q [n] int8, scale [n/blk] f32.
+cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float* scale, cudaStream_t s);
+// out (+)= sum_r s_r q_r over k sources (fixed order 0..k-1).
+cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, int64_t n, int blk, float* out,
+                              int accumulate, cudaStream_t s);
+cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s);
+// Cross-rank barrier: advance this rank's device-side epoch counter, write it into slot[rank]
+// of every peer's signal area, wait for all peers' slots in our own area to reach it
+// (bounded; sets the error word on timeout).
+cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s);
+
+}  // namespace ssm

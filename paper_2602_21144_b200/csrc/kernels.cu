@@ -1,0 +1,671 @@
+// kernels.cu — the rank-local mixer kernels of libssmtp (sm_100a) and the
+// peer-to-peer all-reduce kernels.  All HBM-bound work: 16-byte vector / cp.async
+// loads, token-major activations with channels contiguous.
+//
+//  conv1d_silu      SURVEY §8(a) a2  causal depthwise conv + SiLU
+//  conv_state_upd   a11              conv window of the SSM cache
+//  conv_decode      a10              conv update for one token, in place
+//  unpack           a4               AR#1 fixed-order sum + dt/B/C split (+Falcon RMSNorm)
+//  scan_chunked     a6/a7            selective scan, D skip, SiLU(z) gate, h carried
+//  decode_step      a10              dt_proj + softplus + one scan step + gate, h in place
+//  quantize/qar     a8/a9            int8 per-block codes, fixed-order dequant-accumulate
+//  peer_barrier     a4/a9            epoch flags over NVLink (st.release.sys / ld.acquire.sys)
+//  rmsnorm                           pre-norm glue (reading Q16)
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace ssm {
+namespace {
+
+// ---------------------------------------------------------------- vector IO
+template <typename T, int V>
+struct Vec;
+template <>
+struct Vec<__nv_bfloat16, 8> {
+  __device__ static void load(const __nv_bfloat16* p, float (&v)[8]) {
+    uint4 r = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x;
+      v[2 * i + 1] = f.y;
+    }
+  }
+  __device__ static void store(__nv_bfloat16* p, const float (&v)[8]) {
+    uint4 r;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = r;
+  }
+};
+template <>
+struct Vec<float, 4> {
+  __device__ static void load(const float* p, float (&v)[4]) {
+    float4 r = *reinterpret_cast<const float4*>(p);
+    v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w;
+  }
+  __device__ static void store(float* p, const float (&v)[4]) { *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]); }
+};
+
+template <typename T>
+constexpr int vec_of() { return 16 / sizeof(T); }
+
+// ---------------------------------------------------------------- conv1d + SiLU (prefill)
+// u[b,t,d] = SiLU(conv_b[d] + sum_j conv_w[d,j] * xt[b, t-K+1+j, d]), xt = conv_state || x
+template <typename T, int K, bool FAST>
+__global__ void __launch_bounds__(64) conv1d_silu_kernel(const T* __restrict__ xz, int64_t ldxz,
+                                                         const T* __restrict__ cst, const float* __restrict__ cw,
+                                                         const float* __restrict__ cb, T* __restrict__ u,
+                                                         int64_t ldu, int L, int Ek, int TCH) {
+  constexpr int V = vec_of<T>();
+  const int cg = blockIdx.x * blockDim.x + threadIdx.x;
+  const int d0 = cg * V;
+  if (d0 >= Ek) return;
+  const int b = blockIdx.z;
+  const int t0 = blockIdx.y * TCH;
+  const int t1 = min(L, t0 + TCH);
+  float w[K][V], bias[V], win[K][V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    bias[v] = cb[d0 + v];
+#pragma unroll
+    for (int j = 0; j < K; ++j) w[j][v] = cw[(d0 + v) * K + j];
+  }
+#pragma unroll
+  for (int j = 0; j < K - 1; ++j) {
+    const int t = t0 - (K - 1) + j;
+    if (t >= 0)
+      Vec<T, V>::load(xz + ((int64_t)b * L + t) * ldxz + d0, win[j + 1]);
+    else
+      Vec<T, V>::load(cst + ((int64_t)b * (K - 1) + (K - 1) + t) * Ek + d0, win[j + 1]);
+  }
+  for (int t = t0; t < t1; ++t) {
+#pragma unroll
+    for (int j = 0; j < K - 1; ++j)
+#pragma unroll
+      for (int v = 0; v < V; ++v) win[j][v] = win[j + 1][v];
+    Vec<T, V>::load(xz + ((int64_t)b * L + t) * ldxz + d0, win[K - 1]);
+    float o[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float acc = bias[v];
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc = fmaf(w[j][v], win[j][v], acc);
+      o[v] = silu<FAST>(acc);
+    }
+    Vec<T, V>::store(u + ((int64_t)b * L + t) * ldu + d0, o);
+  }
+}
+
+// conv window after the chunk: last K-1 entries of xt = conv_state || x
+template <typename T>
+__global__ void conv_state_update_kernel(const T* __restrict__ xz, int64_t ldxz, T* __restrict__ cst, int batch,
+                                         int L, int Ek, int K) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= batch * Ek) return;
+  const int b = idx / Ek, d = idx % Ek;
+  float vals[8];
+  for (int j = 0; j < K - 1; ++j) {
+    const int p = L + j;  // position in xt
+    vals[j] = (p < K - 1) ? io<T>::ld(cst + ((int64_t)b * (K - 1) + p) * Ek + d)
+                          : io<T>::ld(xz + ((int64_t)b * L + (p - (K - 1))) * ldxz + d);
+  }
+  for (int j = 0; j < K - 1; ++j) io<T>::st(cst + ((int64_t)b * (K - 1) + j) * Ek + d, vals[j]);
+}
+
+// decode: one token, conv window shifted in place
+template <typename T, bool FAST>
+__global__ void conv_decode_kernel(const T* __restrict__ xz, int64_t ldxz, T* __restrict__ cst,
+                                   const float* __restrict__ cw, const float* __restrict__ cb, T* __restrict__ u,
+                                   int64_t ldu, int batch, int Ek, int K) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= batch * Ek) return;
+  const int b = idx / Ek, d = idx % Ek;
+  float win[8];
+  for (int j = 0; j < K - 1; ++j) win[j] = io<T>::ld(cst + ((int64_t)b * (K - 1) + j) * Ek + d);
+  win[K - 1] = io<T>::ld(xz + (int64_t)b * ldxz + d);
+  float acc = cb[d];
+  for (int j = 0; j < K; ++j) acc = fmaf(cw[d * K + j], win[j], acc);
+  io<T>::st(u + (int64_t)b * ldu + d, silu<FAST>(acc));
+  for (int j = 0; j < K - 1; ++j) io<T>::st(cst + ((int64_t)b * (K - 1) + j) * Ek + d, win[j + 1]);
+}
+
+// ---------------------------------------------------------------- unpack (AR#1 consumer)
+constexpr int kMaxP = 320;  // R + 2N <= 320
+template <typename T>
+__global__ void __launch_bounds__(256) unpack_kernel(Peers src, int nsrc, int64_t off, int M, int hloc, int R, int N,
+                                                     int rmsnorm, float eps, T* __restrict__ dlow,
+                                                     float* __restrict__ BC) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= M * hloc) return;
+  const int m = warp / hloc, hd = warp % hloc;
+  const int P = R + 2 * N;
+  const int64_t base = (int64_t)m * hloc * P + (int64_t)hd * P;
+  constexpr int CPL = kMaxP / 32;
+  float v[CPL];
+  float ss[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int c = lane + 32 * i;
+    float acc = 0.f;
+    if (c < P) {
+      for (int s = 0; s < nsrc; ++s)  // fixed rank order 0..nsrc-1 (reading Q12)
+        acc = (s == 0) ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[s]) + off)[base + c]
+                       : acc + reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[s]) + off)[base + c];
+      const int f = c < R ? 0 : (c < R + N ? 1 : 2);
+      ss[f] = fmaf(acc, acc, ss[f]);
+    }
+    v[i] = acc;
+  }
+  float scale[3] = {1.f, 1.f, 1.f};
+  if (rmsnorm) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      float x = ss[f];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      const int cnt = f == 0 ? R : N;
+      scale[f] = 1.0f / sqrtf(x / (float)cnt + eps);
+    }
+  }
+  T* dl = dlow + ((int64_t)hd * M + m) * R;
+  float* bc = BC + ((int64_t)hd * M + m) * 2 * N;
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < R)
+      io<T>::st(dl + c, v[i] * scale[0]);
+    else if (c < R + N)
+      bc[c - R] = v[i] * scale[1];
+    else if (c < P)
+      bc[c - R] = v[i] * scale[2];
+  }
+}
+
+// ---------------------------------------------------------------- selective scan (prefill)
+SSM_DEV void cp_async16(void* sdst, const void* gsrc, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(pred ? 16 : 0)
+               : "memory");
+}
+SSM_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+SSM_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int SC_THREADS = 128;  // channels per block
+
+// One thread per (batch row, channel); N states in registers; tiles of u, delta, z
+// (bf16 or fp32) and B||C (fp32) staged through shared memory with cp.async double
+// buffering.  h_t = exp(delta A) h_{t-1} + delta B_t u_t;  y = <C_t, h_t> + D u;  g = y SiLU(z).
+template <typename T, int N, bool FAST>
+__global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ u, int64_t ldu,
+                                                          const T* __restrict__ dl, int64_t ldd,
+                                                          const T* __restrict__ z, int64_t ldz,
+                                                          const float* __restrict__ BC, int64_t ldbc,
+                                                          const float* __restrict__ a_log,
+                                                          const float* __restrict__ d_skip, float* __restrict__ h,
+                                                          int64_t h_bstride, T* __restrict__ g, int64_t ldg, int L,
+                                                          int nch) {
+  constexpr int V = vec_of<T>();
+  constexpr int SC_TT = sizeof(T) == 2 ? 16 : 8;  // tokens per staged tile (static smem < 48 KB)
+  constexpr int CH_CHUNKS = SC_THREADS / V;  // 16-B chunks per channel row
+  constexpr int BC_CHUNKS = 2 * N * 4 / 16;
+  __shared__ __align__(16) T su[2][SC_TT][SC_THREADS];
+  __shared__ __align__(16) T sd[2][SC_TT][SC_THREADS];
+  __shared__ __align__(16) T sz[2][SC_TT][SC_THREADS];
+  __shared__ __align__(16) float sbc[2][SC_TT][2 * N];
+
+  const int tid = threadIdx.x;
+  const int b = blockIdx.y;
+  const int cbase = blockIdx.x * SC_THREADS;
+  const int d = cbase + tid;
+  const bool valid = d < nch;
+  const int64_t row0 = (int64_t)b * L;
+
+  auto load_tile = [&](int buf, int tile) {
+    const int tb = tile * SC_TT;
+    for (int i = tid; i < SC_TT * CH_CHUNKS; i += SC_THREADS) {
+      const int r = i / CH_CHUNKS, c = i % CH_CHUNKS;
+      const int t = tb + r;
+      const int ch = cbase + c * V;
+      const bool ok = (t < L) && (ch < nch);
+      const int64_t row = row0 + (ok ? t : 0);
+      const int chs = ok ? ch : 0;
+      cp_async16(&su[buf][r][c * V], u + row * ldu + chs, ok);
+      cp_async16(&sd[buf][r][c * V], dl + row * ldd + chs, ok);
+      cp_async16(&sz[buf][r][c * V], z + row * ldz + chs, ok);
+    }
+    for (int i = tid; i < SC_TT * BC_CHUNKS; i += SC_THREADS) {
+      const int r = i / BC_CHUNKS, c = i % BC_CHUNKS;
+      const int t = tb + r;
+      const bool ok = t < L;
+      cp_async16(&sbc[buf][r][c * 4], BC + (row0 + (ok ? t : 0)) * ldbc + c * 4, ok);
+    }
+  };
+
+  float A[N], hs[N];
+  float Dd = 0.f;
+  float* hp = h + (int64_t)b * h_bstride + (int64_t)(valid ? d : 0) * N;
+  if (valid) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const float a = -expf(a_log[(int64_t)d * N + n]);
+      A[n] = FAST ? a * 1.4426950408889634f : a;
+      hs[n] = hp[n];
+    }
+    Dd = d_skip[d];
+  }
+
+  const int ntiles = (L + SC_TT - 1) / SC_TT;
+  load_tile(0, 0);
+  cp_async_commit();
+  for (int it = 0; it < ntiles; ++it) {
+    const int buf = it & 1;
+    if (it + 1 < ntiles) {
+      load_tile(buf ^ 1, it + 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (valid) {
+      const int tb = it * SC_TT;
+      const int tn = min(SC_TT, L - tb);
+      for (int r = 0; r < tn; ++r) {
+        const float uu = io<T>::ld(&su[buf][r][tid]);
+        const float de = io<T>::ld(&sd[buf][r][tid]);
+        const float zz = io<T>::ld(&sz[buf][r][tid]);
+        const float du = de * uu;
+        const float* Bt = sbc[buf][r];
+        const float* Ct = Bt + N;
+        float y = 0.f;
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+          const float a = FAST ? ex2_approx(de * A[n]) : expf(de * A[n]);
+          hs[n] = fmaf(a, hs[n], du * Bt[n]);
+          y = fmaf(Ct[n], hs[n], y);
+        }
+        y = fmaf(Dd, uu, y);
+        io<T>::st(g + (row0 + tb + r) * ldg + d, y * silu<FAST>(zz));
+      }
+    }
+    __syncthreads();
+  }
+  if (valid) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) hp[n] = hs[n];
+  }
+}
+
+// ---------------------------------------------------------------- decode step
+// dt_proj + softplus + one scan step + gate for 32 channels x all batch rows per block.
+template <typename T, int N, bool FAST>
+__global__ void __launch_bounds__(256) decode_step_kernel(const T* __restrict__ u, const T* __restrict__ z,
+                                                          int64_t ldz, const T* __restrict__ dlow,
+                                                          const float* __restrict__ BC, const T* __restrict__ w_dt,
+                                                          const float* __restrict__ b_dt,
+                                                          const float* __restrict__ a_log,
+                                                          const float* __restrict__ d_skip, float* __restrict__ h,
+                                                          T* __restrict__ g, int batch, int Ek, int R,
+                                                          int ch_per_head) {
+  extern __shared__ float dsm[];
+  const int Rp = R + 1;
+  float* sW = dsm;                 // [32][Rp]
+  float* sdl = dsm + 32 * Rp;      // [batch][R]
+  const int c0 = blockIdx.x * 32;
+  const int hd = c0 / ch_per_head;  // local head of this block (ch_per_head % 32 == 0)
+  for (int i = threadIdx.x; i < 32 * R; i += blockDim.x) {
+    const int c = i / R, r = i % R;
+    sW[c * Rp + r] = (c0 + c < Ek) ? io<T>::ld(w_dt + (int64_t)(c0 + c) * R + r) : 0.f;
+  }
+  for (int i = threadIdx.x; i < batch * R; i += blockDim.x) {
+    const int bb = i / R, r = i % R;
+    sdl[bb * R + r] = io<T>::ld(dlow + ((int64_t)hd * batch + bb) * R + r);
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < batch * 32; it += blockDim.x) {
+    const int bb = it / 32, c = it % 32;
+    const int d = c0 + c;
+    if (d >= Ek) continue;
+    float dt = b_dt[d];
+    const float* wr = sW + c * Rp;
+    const float* xr = sdl + bb * R;
+    for (int r = 0; r < R; ++r) dt = fmaf(xr[r], wr[r], dt);
+    const float de = softplus(dt);
+    const float uu = io<T>::ld(u + (int64_t)bb * Ek + d);
+    const float zz = io<T>::ld(z + (int64_t)bb * ldz + d);
+    const float* Bt = BC + ((int64_t)hd * batch + bb) * 2 * N;
+    const float* Ct = Bt + N;
+    float* hp = h + ((int64_t)bb * Ek + d) * N;
+    const float du = de * uu;
+    float y = 0.f;
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const float a = -expf(a_log[(int64_t)d * N + n]);
+      const float ab = FAST ? ex2_approx(de * a * 1.4426950408889634f) : expf(de * a);
+      const float hn = fmaf(ab, hp[n], du * Bt[n]);
+      hp[n] = hn;
+      y = fmaf(Ct[n], hn, y);
+    }
+    y = fmaf(d_skip[d], uu, y);
+    io<T>::st(g + (int64_t)bb * Ek + d, y * silu<FAST>(zz));
+  }
+}
+
+// ---------------------------------------------------------------- RMSNorm (glue)
+template <typename T>
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, float eps, T* __restrict__ y,
+                               int64_t M, int D) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* xr = x + row * D;
+  float ss = 0.f;
+  for (int i = lane * 4; i < D; i += 128) {
+    float4 v = *reinterpret_cast<const float4*>(xr + i);
+    ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float rs = 1.0f / sqrtf(ss / (float)D + eps);
+  T* yr = y + row * D;
+  for (int i = lane * 4; i < D; i += 128) {
+    float4 v = *reinterpret_cast<const float4*>(xr + i);
+    float ww[4] = {1.f, 1.f, 1.f, 1.f};
+    if (w) { float4 t = *reinterpret_cast<const float4*>(w + i); ww[0] = t.x; ww[1] = t.y; ww[2] = t.z; ww[3] = t.w; }
+    io<T>::st(yr + i, v.x * rs * ww[0]);
+    io<T>::st(yr + i + 1, v.y * rs * ww[1]);
+    io<T>::st(yr + i + 2, v.z * rs * ww[2]);
+    io<T>::st(yr + i + 3, v.w * rs * ww[3]);
+  }
+}
+
+// ---------------------------------------------------------------- int8 quantise / reduce
+// One warp per block of blk = 32*VPL values: amax, s = amax/127 (IEEE), q = rint(o/s) in [-127,127].
+template <int VPL>
+__global__ void quantize_kernel(const float* __restrict__ x, int64_t nblocks, int8_t* __restrict__ q,
+                                float* __restrict__ scale) {
+  const int64_t blk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (blk >= nblocks) return;
+  const float* xb = x + blk * 32 * VPL + lane * VPL;
+  float v[VPL];
+  float am = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    v[i] = xb[i];
+    am = fmaxf(am, fabsf(v[i]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  const float s = __fdiv_rn(am, 127.0f);
+  int8_t* qb = q + blk * 32 * VPL + lane * VPL;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    int c = 0;
+    if (s != 0.f) {
+      c = __float2int_rn(__fdiv_rn(v[i], s));
+      c = max(-127, min(127, c));
+    }
+    qb[i] = (int8_t)c;
+  }
+  if (lane == 0) scale[blk] = s;
+}
+
+__global__ void qar_reduce_kernel(Peers src, int k, int64_t q_off, int64_t s_off, int64_t n16, int blk,
+                                  float* __restrict__ out, int accumulate) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n16) return;
+  float acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+  const int64_t sidx = (i * 16) / blk;
+  for (int r = 0; r < k; ++r) {  // fixed rank order 0..k-1: bitwise-identical on every rank
+    const char* base = reinterpret_cast<const char*>(src.p[r]);
+    const int4 qv = *reinterpret_cast<const int4*>(base + q_off + i * 16);
+    const float s = reinterpret_cast<const float*>(base + s_off)[sidx];
+    const int8_t* qq = reinterpret_cast<const int8_t*>(&qv);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = fmaf(s, (float)qq[j], acc[j]);
+  }
+  float4* o = reinterpret_cast<float4*>(out + i * 16);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float4 v = accumulate ? o[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    v.x += acc[4 * q]; v.y += acc[4 * q + 1]; v.z += acc[4 * q + 2]; v.w += acc[4 * q + 3];
+    o[q] = v;
+  }
+}
+
+__global__ void f32_reduce_kernel(Peers src, int k, int64_t off, int64_t n4, float* __restrict__ out, int accumulate) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  float4 acc = reinterpret_cast<const float4*>(reinterpret_cast<const char*>(src.p[0]) + off)[i];
+  for (int r = 1; r < k; ++r) {
+    const float4 v = reinterpret_cast<const float4*>(reinterpret_cast<const char*>(src.p[r]) + off)[i];
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  float4* o = reinterpret_cast<float4*>(out) + i;
+  if (accumulate) {
+    float4 v = *o;
+    acc.x = v.x + acc.x; acc.y = v.y + acc.y; acc.z = v.z + acc.z; acc.w = v.w + acc.w;
+  }
+  *o = acc;
+}
+
+// ---------------------------------------------------------------- cross-rank barrier
+// Signal area at the head of every symmetric buffer: uint32 slot[8] (slot[p] = last epoch
+// rank p announced to us), uint32 error word at +64 B, uint32 epoch counter at +128 B.
+// The epoch lives in device memory so a captured CUDA graph advances it on every replay
+// (every rank executes the same barrier sequence, so the counters agree).
+__global__ void peer_barrier_kernel(Peers bufs, int rank, int k) {
+  __shared__ uint32_t s_epoch;
+  const int t = threadIdx.x;
+  uint32_t* own = reinterpret_cast<uint32_t*>(bufs.p[rank]);
+  if (t == 0) s_epoch = atomicAdd(own + 32, 1u) + 1u;
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  if (t < k) {
+    fence_sys();
+    st_release_sys(reinterpret_cast<uint32_t*>(bufs.p[t]) + rank, epoch);
+  }
+  __syncwarp();
+  if (t < k) {
+    const uint32_t* slot = own + t;
+    const uint64_t t0 = globaltimer();
+    while ((int32_t)(ld_acquire_sys(slot) - epoch) < 0) {
+      if (globaltimer() - t0 > 20ull * 1000000000ull) {
+        atomicExch(own + 16, 1u);
+        break;
+      }
+    }
+  }
+  __syncwarp();
+  fence_sys();
+}
+
+template <typename T, bool F>
+cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const float* cw, const float* cb, void* u,
+                          int64_t ldu, int batch, int L, int Ek, int K, cudaStream_t s) {
+  constexpr int V = vec_of<T>();
+  const int TCH = 32;
+  dim3 grid((Ek / V + 63) / 64, (L + TCH - 1) / TCH, batch);
+  const T* x = reinterpret_cast<const T*>(xz);
+  const T* c = reinterpret_cast<const T*>(cs);
+  T* uu = reinterpret_cast<T*>(u);
+  switch (K) {
+    case 2: conv1d_silu_kernel<T, 2, F><<<grid, 64, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek, TCH); break;
+    case 3: conv1d_silu_kernel<T, 3, F><<<grid, 64, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek, TCH); break;
+    case 4: conv1d_silu_kernel<T, 4, F><<<grid, 64, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek, TCH); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// ==================================================================== launchers
+cudaError_t launch_conv1d_silu(int bf16, const void* xz, int64_t ldxz, const void* cs, const float* cw,
+                               const float* cb, void* u, int64_t ldu, int batch, int L, int Ek, int K,
+                               cudaStream_t s) {
+  if (batch <= 0 || L <= 0) return cudaSuccess;
+  if (bf16) return conv_dispatch<__nv_bfloat16, true>(xz, ldxz, cs, cw, cb, u, ldu, batch, L, Ek, K, s);
+  return conv_dispatch<float, false>(xz, ldxz, cs, cw, cb, u, ldu, batch, L, Ek, K, s);
+}
+
+cudaError_t launch_conv_state_update(int bf16, const void* xz, int64_t ldxz, void* cs, int batch, int L, int Ek,
+                                     int K, cudaStream_t s) {
+  const int n = batch * Ek;
+  if (n <= 0 || L <= 0) return cudaSuccess;
+  if (bf16)
+    conv_state_update_kernel<__nv_bfloat16><<<(n + 255) / 256, 256, 0, s>>>(
+        reinterpret_cast<const __nv_bfloat16*>(xz), ldxz, reinterpret_cast<__nv_bfloat16*>(cs), batch, L, Ek, K);
+  else
+    conv_state_update_kernel<float><<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const float*>(xz), ldxz,
+                                                                     reinterpret_cast<float*>(cs), batch, L, Ek, K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_decode(int bf16, const void* xz, int64_t ldxz, void* cs, const float* cw, const float* cb,
+                               void* u, int64_t ldu, int batch, int Ek, int K, cudaStream_t s) {
+  const int n = batch * Ek;
+  if (n <= 0) return cudaSuccess;
+  if (bf16)
+    conv_decode_kernel<__nv_bfloat16, true><<<(n + 255) / 256, 256, 0, s>>>(
+        reinterpret_cast<const __nv_bfloat16*>(xz), ldxz, reinterpret_cast<__nv_bfloat16*>(cs), cw, cb,
+        reinterpret_cast<__nv_bfloat16*>(u), ldu, batch, Ek, K);
+  else
+    conv_decode_kernel<float, false><<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const float*>(xz), ldxz,
+                                                                     reinterpret_cast<float*>(cs), cw, cb,
+                                                                     reinterpret_cast<float*>(u), ldu, batch, Ek, K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(int bf16, Peers src, int nsrc, int64_t off, int M, int hloc, int R, int N, int rmsnorm,
+                          float eps, void* dlow, float* BC, cudaStream_t s) {
+  const int64_t warps = (int64_t)M * hloc;
+  if (warps <= 0) return cudaSuccess;
+  if (R + 2 * N > kMaxP) return cudaErrorInvalidValue;
+  const int blocks = (int)((warps * 32 + 255) / 256);
+  if (bf16)
+    unpack_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(src, nsrc, off, M, hloc, R, N, rmsnorm, eps,
+                                                        reinterpret_cast<__nv_bfloat16*>(dlow), BC);
+  else
+    unpack_kernel<float><<<blocks, 256, 0, s>>>(src, nsrc, off, M, hloc, R, N, rmsnorm, eps,
+                                                reinterpret_cast<float*>(dlow), BC);
+  return cudaGetLastError();
+}
+
+template <typename T, int N, bool F>
+static cudaError_t scan_t(const void* u, int64_t ldu, const void* dl, int64_t ldd, const void* z, int64_t ldz,
+                          const float* BC, int64_t ldbc, const float* a_log, const float* d_skip, float* h,
+                          int64_t hbs, void* g, int64_t ldg, int batch, int L, int nch, cudaStream_t s) {
+  dim3 grid((nch + SC_THREADS - 1) / SC_THREADS, batch);
+  scan_kernel<T, N, F><<<grid, SC_THREADS, 0, s>>>(
+      reinterpret_cast<const T*>(u), ldu, reinterpret_cast<const T*>(dl), ldd, reinterpret_cast<const T*>(z), ldz, BC,
+      ldbc, a_log, d_skip, h, hbs, reinterpret_cast<T*>(g), ldg, L, nch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const void* dl, int64_t ldd, const void* z,
+                        int64_t ldz, const float* BC, int64_t ldbc, const float* a_log, const float* d_skip, float* h,
+                        int64_t hbs, void* g, int64_t ldg, int batch, int L, int nch, int N, cudaStream_t s) {
+  if (batch <= 0 || L <= 0 || nch <= 0) return cudaSuccess;
+  if (N != 16 && N != 8) return cudaErrorInvalidValue;
+  if (bf16) {
+    if (N == 16) return fast ? scan_t<__nv_bfloat16, 16, true>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s)
+                             : scan_t<__nv_bfloat16, 16, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
+    return fast ? scan_t<__nv_bfloat16, 8, true>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s)
+                : scan_t<__nv_bfloat16, 8, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
+  }
+  if (N == 16) return scan_t<float, 16, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
+  return scan_t<float, 8, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
+}
+
+template <typename T, int N, bool F>
+static cudaError_t dstep_t(const void* u, const void* z, int64_t ldz, const void* dlow, const float* BC,
+                           const void* w_dt, const float* b_dt, const float* a_log, const float* d_skip, float* h,
+                           void* g, int batch, int Ek, int R, int cph, cudaStream_t s) {
+  const size_t smem = (size_t)(32 * (R + 1) + batch * R) * sizeof(float);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(decode_step_kernel<T, N, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  decode_step_kernel<T, N, F><<<(Ek + 31) / 32, 256, smem, s>>>(
+      reinterpret_cast<const T*>(u), reinterpret_cast<const T*>(z), ldz, reinterpret_cast<const T*>(dlow), BC,
+      reinterpret_cast<const T*>(w_dt), b_dt, a_log, d_skip, h, reinterpret_cast<T*>(g), batch, Ek, R, cph);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_step(int bf16, const void* u, const void* z, int64_t ldz, const void* dlow,
+                               const float* BC, const void* w_dt, const float* b_dt, const float* a_log,
+                               const float* d_skip, float* h, void* g, int batch, int Ek, int R, int N,
+                               int ch_per_head, int hloc, cudaStream_t s) {
+  (void)hloc;
+  if (batch <= 0) return cudaSuccess;
+  if (ch_per_head % 32 != 0) return cudaErrorInvalidValue;
+  if ((size_t)(32 * (R + 1) + batch * R) * sizeof(float) > 200 * 1024) return cudaErrorInvalidValue;
+  if (N != 16 && N != 8) return cudaErrorInvalidValue;
+  if (bf16) {
+    return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(u, z, ldz, dlow, BC, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s)
+                   : dstep_t<__nv_bfloat16, 8, true>(u, z, ldz, dlow, BC, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s);
+  }
+  return N == 16 ? dstep_t<float, 16, false>(u, z, ldz, dlow, BC, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s)
+                 : dstep_t<float, 8, false>(u, z, ldz, dlow, BC, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s);
+}
+
+cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
+                           cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if (D % 4) return cudaErrorInvalidValue;
+  const int blocks = (int)((M + 7) / 8);
+  if (bf16)
+    rmsnorm_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(x, w, eps, reinterpret_cast<__nv_bfloat16*>(y), M, D);
+  else
+    rmsnorm_kernel<float><<<blocks, 256, 0, s>>>(x, w, eps, reinterpret_cast<float*>(y), M, D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float* scale, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t nb = n / blk;
+  const int blocks = (int)((nb * 32 + 255) / 256);
+  switch (blk) {
+    case 32: quantize_kernel<1><<<blocks, 256, 0, s>>>(x, nb, q, scale); break;
+    case 64: quantize_kernel<2><<<blocks, 256, 0, s>>>(x, nb, q, scale); break;
+    case 128: quantize_kernel<4><<<blocks, 256, 0, s>>>(x, nb, q, scale); break;
+    case 256: quantize_kernel<8><<<blocks, 256, 0, s>>>(x, nb, q, scale); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, int64_t n, int blk, float* out,
+                              int accumulate, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t n16 = n / 16;
+  qar_reduce_kernel<<<(int)((n16 + 255) / 256), 256, 0, s>>>(src, k, q_off, s_off, n16, blk, out, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t n4 = n / 4;
+  f32_reduce_kernel<<<(int)((n4 + 255) / 256), 256, 0, s>>>(src, k, off, n4, out, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s) {
+  peer_barrier_kernel<<<1, 32, 0, s>>>(bufs, rank, k);
+  return cudaGetLastError();
+}
+
+}  // namespace ssm

@@ -1,0 +1,93 @@
+"""Layer stack of one TP rank: n_layers x [pre-norm RMSNorm -> TP mixer -> residual add],
+chunk-major prefill carrying the per-layer SSM cache into CUDA-graph decode
+(§4.1; SURVEY.md §3 call stacks (2)-(3)).  Every kernel is
+launched through libssmtp's C ABI; PyTorch provides memory, streams and the graph.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+from .mixer import LayerWeights, State, TPMixer
+
+
+def synthetic_layer(dims, layer, seed=1000, device="cuda"):
+    """Full (unsharded) weights of one layer generated ON the device with a seeded
+    generator (same recipe as synth.layer_weights: Mamba init ranges, jittered A).
+    Used for the full-depth bench where host generation of billions of parameters
+    would dominate; parity tests use synth.layer_weights on the host."""
+    import math
+    g = torch.Generator(device=device).manual_seed(seed + layer)
+    D, E, N, K, R, H = dims.d_model, dims.d_inner, dims.d_state, dims.d_conv, dims.dt_rank, dims.n_heads
+    Eh = E // H
+    f = dict(device=device, dtype=torch.float32)
+
+    def u(shape, bound):
+        return (torch.rand(shape, generator=g, **f) * 2 - 1) * bound
+
+    w = {"w_in": u((2 * E, D), 1 / math.sqrt(D)), "conv_w": u((E, K), 1 / math.sqrt(K)),
+         "conv_b": u((E,), 1 / math.sqrt(K)), "w_x": u((H, R + 2 * N, Eh), 1 / math.sqrt(Eh)),
+         "w_dt": u((E, R), 1 / math.sqrt(R))}
+    lo, hi = math.log(1e-3), math.log(1e-1)
+    dt0 = torch.exp(torch.rand((E,), generator=g, **f) * (hi - lo) + lo)
+    w["b_dt"] = dt0 + torch.log(-torch.expm1(-dt0))
+    n = torch.arange(1, N + 1, **f)
+    w["a_log"] = torch.log(n)[None, :].expand(E, N) + 0.05 * torch.randn((E, N), generator=g, **f)
+    w["d_skip"] = torch.ones((E,), **f)
+    w["w_out"] = u((D, E), 1 / math.sqrt(E)) / math.sqrt(2.0 * max(dims.n_layers, 1))
+    return w
+
+
+class MixerStack:
+    def __init__(self, mixer: TPMixer, layers: list, batch: int, max_chunk: int, flags=L.SSM_AR2_INT8,
+                 norm_eps=1e-5):
+        self.mx, self.layers, self.batch, self.flags, self.eps = mixer, layers, batch, flags, norm_eps
+        d = mixer.dims
+        dt = torch.bfloat16 if mixer.dtype == "bf16" else torch.float32
+        self.ws = mixer.workspace(batch, max_chunk)
+        self.ws_dec = mixer.workspace(batch, 1)
+        self.xbuf = torch.empty((batch * max_chunk, d.d_model), dtype=dt, device=mixer.device)
+        self.xbuf_dec = torch.empty((batch, d.d_model), dtype=dt, device=mixer.device)
+        self.states = [State(mixer, batch) for _ in layers]
+        self.graph = None
+        self.graph_launches = 0
+
+    def reset(self, stream=None):
+        for s in self.states:
+            s.reset(stream)
+
+    def prefill_chunk(self, res, stream=None):
+        """res: [batch * Lc, D] fp32, this chunk's residual rows (row = b*Lc + t), updated in place."""
+        n = res.shape[0]
+        x = self.xbuf[:n]
+        for lw, st in zip(self.layers, self.states):
+            self.mx.rmsnorm(res, x, None, self.eps, stream)
+            self.mx.prefill(lw, st, x, res, self.flags, self.ws, stream)
+
+    def decode_step(self, res_t, stream=None):
+        """res_t: [batch, D] fp32, updated in place through all layers."""
+        for lw, st in zip(self.layers, self.states):
+            self.mx.rmsnorm(res_t, self.xbuf_dec, None, self.eps, stream)
+            self.mx.decode(lw, st, self.xbuf_dec, res_t, self.flags, self.ws_dec, stream)
+
+    def capture_decode(self, res_t):
+        """Capture one decode step over all layers into a CUDA graph reading/writing res_t.
+        The decode path is graph-safe: no host sync, fixed pointers; the all-reduce epoch
+        counters live in device memory and advance on every replay, and each step issues an
+        even number of collectives so the double-buffer halves alternate across replays."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.decode_step(res_t, s)   # warm-up (attribute setup outside capture)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        before = self.mx.launches()
+        ar_before = self.mx.stats()["allreduce"]
+        with torch.cuda.graph(g):
+            self.decode_step(res_t)
+        self.graph_launches = self.mx.launches() - before
+        if (self.mx.stats()["allreduce"] - ar_before) % 2:
+            raise RuntimeError("odd number of collectives per decode step: double-buffer halves would not alternate")
+        self.graph = g
+        return g

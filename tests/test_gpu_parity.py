@@ -1,0 +1,254 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle on the same seeded
+inputs (north_star tolerances: 1e-5 fp32 mode, 2e-2 bf16 I/O, normwise)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import mixer_ref as M
+from oracle import qar_ref as Q
+from oracle import tp_sim as T
+from paper_2602_21144_b200 import LayerWeights, State, TPMixer, _lib as L
+from gpu_helpers import (TOL, VirtualGroup, np64, oracle_state_from_gpu_layout, prep_acts, prep_weights, rel,
+                               to_dev)
+
+pytestmark = pytest.mark.gpu
+
+MED = synth.MixerDims(d_model=256, d_inner=512, d_state=16, d_conv=4, dt_rank=16, n_layers=2)
+
+
+# ------------------------------------------------------------------ GEMM
+@pytest.mark.parametrize("M,N,K,swap,ks", [(300, 200, 320, 0, 1), (384, 512, 2560, 0, 1), (1000, 192, 640, 0, 1),
+                                           (16, 10240 // 8, 2560, 1, 1), (16, 192, 5120, 1, 8), (32, 2560, 640, 1, 4),
+                                           (5, 48, 64, 0, 1)])
+def test_gemm_tcgen05_bf16(M, N, K, swap, ks):
+    dims = synth.MixerDims(d_model=64, d_inner=128, dt_rank=4)
+    mx = TPMixer(dims, "bf16")
+    g = torch.Generator().manual_seed(M * 7 + N)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, generator=g).to(torch.bfloat16)
+    C = torch.empty(M, N, device="cuda")
+    mx.dbg_gemm(A.cuda(), B.cuda(), C, swap_ab=bool(swap), ksplit=ks)
+    torch.cuda.synchronize()
+    ref = A.double() @ B.double().T            # library matmul in fp64 on the same bf16 values
+    assert rel(C.cpu(), ref) < 1e-5
+
+
+def test_gemm_simt_fp32():
+    dims = synth.MixerDims(d_model=64, d_inner=128, dt_rank=4)
+    mx = TPMixer(dims, "fp32")
+    g = torch.Generator().manual_seed(3)
+    A = torch.randn(77, 130, generator=g)
+    B = torch.randn(45, 130, generator=g)
+    C = torch.empty(77, 45, device="cuda")
+    mx.dbg_gemm(A.cuda(), B.cuda(), C)
+    torch.cuda.synchronize()
+    assert rel(C.cpu(), A.double() @ B.double().T) < 1e-6
+
+
+# ------------------------------------------------------------------ scan
+@pytest.mark.parametrize("dtype,L_", [("fp32", 37), ("bf16", 37), ("bf16", 130)])
+def test_scan_kernel_vs_oracle(dtype, L_):
+    dims = synth.MixerDims(d_model=128, d_inner=384, d_state=16, dt_rank=8)
+    mx = TPMixer(dims, dtype)
+    B, E, N = 2, 384, 16
+    g = torch.Generator().manual_seed(5)
+    rnd = lambda *s: torch.randn(*s, generator=g, dtype=torch.float64)
+    u = rnd(B, L_, E)
+    delta = torch.exp(torch.rand(B, L_, E, generator=g, dtype=torch.float64) * 4.6 - 6.9)   # 1e-3 .. 1e-1
+    z = rnd(B, L_, E)
+    BC = rnd(B, L_, 2 * N)
+    w = prep_weights(dims, 0, dtype)
+    a_log, d_skip = w["a_log"], w["d_skip"]
+    h0 = rnd(B, E, N) * 0.5
+    if dtype == "bf16":
+        u, delta, z = synth.bf16_round(u), synth.bf16_round(delta), synth.bf16_round(z)
+    BC = BC.to(torch.float32).double()
+    h0 = h0.to(torch.float32).double()
+    h = h0.to(torch.float32).cuda()
+    gout = torch.empty(B * L_, E, dtype=torch.bfloat16 if dtype == "bf16" else torch.float32, device="cuda")
+    mx.dbg_scan(to_dev(u, dtype), to_dev(delta, dtype), to_dev(z, dtype), E, BC.float().cuda(),
+                a_log.float().cuda(), d_skip.float().cuda(), h, gout, B, L_)
+    torch.cuda.synchronize()
+    A = -np.exp(a_log.numpy())
+    y, hL = M.scan_full(u.numpy(), delta.numpy(), A, BC[..., :N].numpy(), BC[..., N:].numpy(), d_skip.numpy(),
+                        h0.numpy())
+    gref = y * M.silu(z.numpy())
+    assert rel(gout.float().cpu().view(B, L_, E), gref) < TOL[dtype]
+    assert rel(h.cpu(), hL) < TOL[dtype]
+
+
+# ------------------------------------------------------------------ full mixer, TP=1
+def _run_tp1(dims, dtype, B, L_in, L_out, chunks=None, layer=0):
+    w = prep_weights(dims, layer, dtype)
+    x, res = prep_acts(B, L_in + L_out, dims, dtype, seed=11 + layer)
+    mx = TPMixer(dims, dtype)
+    lw = LayerWeights(dims, w, dtype=dtype)
+    st = State(mx, B)
+    outs = []
+    chunks = chunks or [L_in]
+    t0 = 0
+    for c in chunks:
+        xi = to_dev(x[:, t0:t0 + c], dtype).view(B * c, -1)
+        r = res[:, t0:t0 + c].float().cuda().contiguous().view(B * c, -1)
+        mx.prefill(lw, st, xi, r)
+        outs.append(r.view(B, c, -1))
+        t0 += c
+    for t in range(L_in, L_in + L_out):
+        xi = to_dev(x[:, t:t + 1], dtype).view(B, -1)
+        r = res[:, t:t + 1].float().cuda().contiguous().view(B, -1)
+        mx.decode(lw, st, xi, r)
+        outs.append(r.view(B, 1, -1))
+    torch.cuda.synchronize()
+    gpu = torch.cat([o.cpu() for o in outs], 1).double().numpy()
+    ref, st_ref = M.mixer_forward(dims, np64(w), x.numpy(), res.numpy())
+    conv, h = oracle_state_from_gpu_layout(st.conv, st.h)
+    return gpu, ref, res.numpy(), (conv, h), st_ref, mx
+
+
+def test_mixer_tp1_fp32_tiny_prefill_decode():
+    dims = synth.CONFIGS["tiny"]
+    wl = synth.WORKLOADS["tiny"]
+    gpu, ref, res, st, st_ref, _ = _run_tp1(dims, "fp32", wl["batch"], wl["prompt"], wl["decode"])
+    assert rel(gpu - res, ref - res) < TOL["fp32"]
+    assert rel(st[1], st_ref[1]) < TOL["fp32"]
+    assert rel(st[0], st_ref[0]) < TOL["fp32"]
+
+
+@pytest.mark.parametrize("dims_name", ["med", "med_falcon", "med_zamba"])
+def test_mixer_tp1_bf16_prefill_decode(dims_name):
+    dims = {"med": MED,
+            "med_falcon": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, bcdt_rmsnorm=True),
+            "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2)}[dims_name]
+    gpu, ref, res, st, st_ref, mx = _run_tp1(dims, "bf16", 3, 150, 6)
+    assert rel(gpu - res, ref - res) < TOL["bf16"]
+    assert rel(st[1], st_ref[1]) < TOL["bf16"]
+    assert rel(st[0], st_ref[0]) < TOL["bf16"]
+    assert mx.stats()["allreduce"] == 0         # TP=1: no all-reduce (reading Q13)
+
+
+def test_mixer_chunked_prefill_matches_oracle_and_is_chunk_invariant():
+    dims = MED
+    g1, ref, res, st1, _, _ = _run_tp1(dims, "bf16", 2, 100, 0)
+    g2, _, _, st2, _, _ = _run_tp1(dims, "bf16", 2, 100, 0, chunks=[1, 30, 3, 66])
+    assert rel(g2 - res, ref - res) < TOL["bf16"]
+    assert rel(g2 - res, g1 - res) < TOL["bf16"]
+    assert rel(st2[1], st1[1]) < TOL["bf16"]
+    np.testing.assert_array_equal(st2[0], st1[0])     # conv window holds raw x values
+
+
+def test_mixer_fp32_edge_cases():
+    dims = synth.CONFIGS["tiny"]
+    # L=1 prefill, L < K-1 chunks mixing old state and new input, batch 1
+    g, ref, res, st, st_ref, _ = _run_tp1(dims, "fp32", 1, 5, 3, chunks=[1, 2, 2])
+    assert rel(g - res, ref - res) < TOL["fp32"]
+    assert rel(st[1], st_ref[1]) < TOL["fp32"]
+
+
+def test_api_errors_on_gpu():
+    dims = MED
+    mx = TPMixer(dims, "bf16")
+    other = TPMixer(dims, "bf16")
+    st = State(other, 2)
+    w = LayerWeights(dims, prep_weights(dims, 0, "bf16"))
+    x = torch.zeros(2 * 4, dims.d_model, dtype=torch.bfloat16, device="cuda")
+    r = torch.zeros(2 * 4, dims.d_model, device="cuda")
+    with pytest.raises(L.SSMError) as e:
+        mx.prefill(w, st, x, r)
+    assert e.value.name == "SSM_ERR_CACHE"
+    st2 = State(mx, 2)
+    with pytest.raises(L.SSMError) as e:
+        mx.prefill(w, st2, x, r, workspace=torch.empty(256, dtype=torch.uint8, device="cuda"))
+    assert e.value.name == "SSM_ERR_ARG"
+
+
+# ------------------------------------------------------------------ virtual TP (single GPU, k streams)
+def _tp_virtual(dims, dtype, k, B, L_in, L_out, flags, qar_block=128):
+    """All device inputs and workspaces are created BEFORE the ranks' work is enqueued:
+    a pageable H2D copy or a cudaMalloc inside the enqueue loop can serialise against a
+    spinning peer barrier of another virtual rank on the same device."""
+    w = prep_weights(dims, 0, dtype)
+    x, res = prep_acts(B, L_in + L_out, dims, dtype, seed=17)
+    grp = VirtualGroup(dims, k, dtype, B * max(L_in, 1), qar_block)
+    lws = [LayerWeights(dims, w, k, r, dtype) for r in range(k)]
+    sts = [State(grp.mixers[r], B) for r in range(k)]
+    ws_p = [grp.mixers[r].workspace(B, L_in) for r in range(k)]
+    ws_d = [grp.mixers[r].workspace(B, 1) for r in range(k)]
+    xp = [to_dev(x[:, :L_in], dtype).view(B * L_in, -1) for _ in range(k)]
+    rp = [res[:, :L_in].float().cuda().contiguous().view(B * L_in, -1) for _ in range(k)]
+    xd = [[to_dev(x[:, t:t + 1], dtype).view(B, -1) for t in range(L_in, L_in + L_out)] for _ in range(k)]
+    rd = [[res[:, t:t + 1].float().cuda().contiguous().view(B, -1) for t in range(L_in, L_in + L_out)]
+          for _ in range(k)]
+    torch.cuda.synchronize()
+    grp.run(lambda r, mx, s: mx.prefill(lws[r], sts[r], xp[r], rp[r], flags=flags, workspace=ws_p[r], stream=s))
+    for j in range(L_out):
+        grp.run(lambda r, mx, s, j=j: mx.decode(lws[r], sts[r], xd[r][j], rd[r][j], flags=flags, workspace=ws_d[r],
+                                                stream=s))
+    outs = [torch.cat([rp[r].view(B, L_in, -1)] + [o.view(B, 1, -1) for o in rd[r]], 1).cpu() for r in range(k)]
+    return outs, w, x, res, grp, sts
+
+
+@pytest.mark.parametrize("k,mode", [(2, "int8"), (4, "int8"), (2, "fp32"), (4, "fp32")])
+def test_virtual_tp_mixer_vs_oracle(k, mode):
+    dims = MED
+    flags = L.SSM_AR2_INT8 if mode == "int8" else L.SSM_AR2_FP32
+    outs, w, x, res, grp, sts = _tp_virtual(dims, "bf16", k, 2, 40, 4, flags)
+    # replicas bitwise identical on every rank (fixed-order reductions, reading Q12 / H7)
+    for r in range(1, k):
+        assert torch.equal(outs[r], outs[0])
+    ref, st_ref = M.mixer_forward(dims, np64(w), x.numpy(), res.numpy())
+    resn = res.numpy()
+    assert rel(outs[0].double().numpy() - resn, ref - resn) < TOL["bf16"]
+    # per-rank cache shard == oracle channel slice
+    h = np.concatenate([sts[r].h.cpu().double().numpy() for r in range(k)], 1)
+    assert rel(h, st_ref[1]) < TOL["bf16"]
+    # exactly two all-reduces per layer call
+    assert grp.mixers[0].stats()["allreduce"] == 2 * (1 + 4)
+
+
+def test_virtual_tp_zamba_heads_k2_one_allreduce():
+    dims = synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2)
+    outs, w, x, res, grp, _ = _tp_virtual(dims, "bf16", 2, 2, 24, 2, L.SSM_AR2_FP32)
+    ref, _ = M.mixer_forward(dims, np64(w), x.numpy(), res.numpy())
+    resn = res.numpy()
+    assert rel(outs[0].double().numpy() - resn, ref - resn) < TOL["bf16"]
+    assert grp.mixers[0].stats()["allreduce"] == 1 * 3       # head-aligned shards: no AR#1 (Q17)
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_virtual_qallreduce_codes_bitexact_and_bound(k):
+    dims = MED
+    n = 6 * dims.d_model
+    parts = synth.partials(k, n, seed=100 + k)
+    grp = VirtualGroup(dims, k, "bf16", 64)
+    outs = [torch.empty(n, device="cuda") for _ in range(k)]
+    dev_parts = [parts[r].cuda() for r in range(k)]
+    grp.run(lambda r, mx, s: mx.qallreduce(dev_parts[r], outs[r], stream=s))
+    res_ref, codes, scales = Q.qallreduce(list(parts.numpy()), 128)
+    # epoch 1 -> half 1 of each rank's symmetric buffer: codes at 0, scales at align256(n)
+    half = ((grp.bufs[0].numel() - 256) // 2) & ~255
+    for r in range(k):
+        base = 256 + half
+        q = grp.bufs[r][base:base + n].cpu().view(torch.int8).numpy()
+        soff = base + ((n + 255) // 256) * 256
+        s = grp.bufs[r][soff:soff + 4 * (n // 128)].cpu().view(torch.float32).numpy()
+        np.testing.assert_array_equal(q, codes[r])
+        np.testing.assert_array_equal(s, scales[r])
+    for r in range(1, k):
+        assert torch.equal(outs[r], outs[0])
+    got = outs[0].cpu().double().numpy()
+    assert np.abs(got - res_ref).max() <= 1e-6 * np.abs(res_ref).max()
+    exact = parts.double().sum(0).numpy()
+    assert np.all(np.abs(got - exact) <= Q.northstar_bound(list(parts.numpy()), 128) * (1 + 1e-5) + 1e-7)
+
+
+def test_rmsnorm_kernel():
+    dims = MED
+    mx = TPMixer(dims, "fp32")
+    g = torch.Generator().manual_seed(9)
+    x = torch.randn(37, dims.d_model, generator=g, dtype=torch.float64)
+    w = torch.rand(dims.d_model, generator=g, dtype=torch.float64)
+    y = torch.empty(37, dims.d_model, device="cuda")
+    mx.rmsnorm(x.float().cuda(), y, w.float().cuda(), eps=1e-5)
+    torch.cuda.synchronize()
+    assert rel(y.cpu(), M.rmsnorm(x.numpy(), w.numpy(), 1e-5)) < 1e-6
