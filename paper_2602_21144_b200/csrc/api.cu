@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -208,19 +209,60 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   };
   auto half_off = [&](uint32_t ep) -> int64_t { return (int64_t)(kSigBytes + (ep & 1) * half); };
 
+  const int64_t nD = M * D;
+  // Collective epochs and destinations, fixed up front in execution order (AR#1 then AR#2).
+  const bool ar1 = t->ar1_group > 1;
+  uint32_t ep1 = 0, ep2 = 0;
+  float* xdst = dbc;
+  if (ar1) {
+    ep1 = ++t->epoch;
+    xdst = reinterpret_cast<float*>(own_half(ep1));
+    t->ar_count++;
+    t->bytes_sent += M * hl * P * 4;
+  }
+  enum { OUT_RESID, OUT_EXTERNAL, OUT_FP32, OUT_INT8 } omode;
+  float* odst;
+  if (t->k == 1) {
+    omode = OUT_RESID;
+    odst = residual;
+  } else if (flags & SSM_AR2_EXTERNAL) {
+    omode = OUT_EXTERNAL;
+    odst = residual;
+  } else if (flags & SSM_AR2_FP32) {
+    omode = OUT_FP32;
+    ep2 = ++t->epoch;
+    odst = reinterpret_cast<float*>(own_half(ep2));
+  } else {
+    omode = OUT_INT8;
+    ep2 = ++t->epoch;
+    odst = part;
+  }
+  const bool oacc = omode == OUT_RESID;  // out_proj accumulates into its destination
+  const int ks_x = swap ? pick_ksplit(t, hl * P, (int)M, Ek) : 1;
+  const int ks_o = swap ? pick_ksplit(t, D, (int)M, Ek) : 1;
+
   // (a1) in_proj, column-parallel: xz = x_in W_in,r^T   [M, 2E_k]
   {
-  Probe pr(t, SSM_PROBE_IN_PROJ, s);
-  if (swap)
-    CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s));
-  else
-    CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, epi(kst, 0, xz, 2 * Ek), s));
+    Probe pr(t, SSM_PROBE_IN_PROJ, s);
+    if (swap)
+      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s));
+    else
+      CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, epi(kst, 0, xz, 2 * Ek), s));
   }
 
   // (a2) conv1d + SiLU, rank-local; conv window of the cache updated
   if (decode) {
+    // split-K targets of x_proj / out_proj are zeroed by the conv kernel (one launch fewer)
+    float* z0 = nullptr;
+    int64_t n0 = 0;
+    float* z1 = nullptr;
+    int64_t n1 = 0;
+    if (ks_x > 1) { z0 = xdst; n0 = M * hl * P; }
+    if (swap && !oacc) { z1 = odst; n1 = nD; }
+    if ((n0 & 3) && n0) { CU(cudaMemsetAsync(z0, 0, n0 * 4, s)); n0 = 0; }
+    if ((n1 & 3) && n1) { CU(cudaMemsetAsync(z1, 0, n1 * 4, s)); n1 = 0; }
     t->launches++;
-    CU(launch_conv_decode(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, Ek, K, s));
+    CU(launch_conv_decode(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, Ek, K, z0, n0, z1, n1, s));
   } else {
     Probe pr(t, SSM_PROBE_CONV, s);
     t->launches += 2;
@@ -229,54 +271,48 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   }
 
   // (a3) x_proj partial [M, hloc*P] fp32, straight into the symmetric buffer when AR#1 follows
-  const bool ar1 = t->ar1_group > 1;
-  uint32_t ep1 = 0;
-  float* xdst = dbc;
-  if (ar1) {
-    ep1 = ++t->epoch;
-    xdst = reinterpret_cast<float*>(own_half(ep1));
-    t->ar_count++;
-    t->bytes_sent += M * hl * P * 4;
-  }
   {
-  Probe pr(t, SSM_PROBE_X_PROJ, s);
-  if (swap) {
-    const int ks = pick_ksplit(t, hl * P, (int)M, Ek);
-    if (ks > 1) CU(cudaMemsetAsync(xdst, 0, (size_t)M * hl * P * 4, s));
-    CU(gemm(t, w->w_x, Ek, u, Ek, hl * P, (int)M, Ek, ks, epi(ks > 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s));
-  } else {
-    CU(gemm(t, u, Ek, w->w_x, Ek, (int)M, hl * P, Ek, 1, epi(EPI_STORE_F32, 0, xdst, hl * P), s));
-  }
+    Probe pr(t, SSM_PROBE_X_PROJ, s);
+    if (swap)
+      CU(gemm(t, w->w_x, Ek, u, Ek, hl * P, (int)M, Ek, ks_x,
+              epi(ks_x > 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s));
+    else
+      CU(gemm(t, u, Ek, w->w_x, Ek, (int)M, hl * P, Ek, 1, epi(EPI_STORE_F32, 0, xdst, hl * P), s));
   }
 
-  // (a4) AR#1 (fixed rank order within the head group) + unpack dt_low / B / C
+  // (a4) AR#1: barrier, then the fixed-order sum is done by its consumer
+  Peers dsrc{};
+  int nsrc = 1;
+  int64_t doff = 0;
   if (ar1) {
-    t->launches += 2;
-    CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
-    CU(launch_unpack(bf, group_peers(t, t->ar1_group), t->ar1_group, half_off(ep1), (int)M, hl, R, N,
-                     c.bcdt_rmsnorm, c.rms_eps, dlow, BC, s));
-  } else {
-    Peers one{};
-    one.p[0] = dbc;
     t->launches++;
-    CU(launch_unpack(bf, one, 1, 0, (int)M, hl, R, N, c.bcdt_rmsnorm, c.rms_eps, dlow, BC, s));
+    CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
+    dsrc = group_peers(t, t->ar1_group);
+    nsrc = t->ar1_group;
+    doff = half_off(ep1);
+  } else {
+    dsrc.p[0] = dbc;
   }
 
-  // (a5)+(a6)+(a7) dt_proj + softplus, selective scan, D skip, gate
   if (decode) {
+    // (a4)-(a7) decode: AR#1 sum + unpack + dt_proj + softplus + scan step + gate, one kernel
     Probe pr(t, SSM_PROBE_DECODE_STEP, s);
     t->launches++;
-    CU(launch_decode_step(bf, u, reinterpret_cast<char*>(xz) + Ek * es, 2 * Ek, dlow, BC, w->w_dt, w->b_dt,
-                          w->a_log, w->d_skip, st->h, g, batch, Ek, R, N, t->cph, hl, s));
+    CU(launch_decode_step(bf, dsrc, nsrc, doff, hl * P, c.bcdt_rmsnorm, c.rms_eps, u,
+                          reinterpret_cast<char*>(xz) + Ek * es, 2 * Ek, w->w_dt, w->b_dt, w->a_log, w->d_skip, st->h,
+                          g, batch, Ek, R, N, t->cph, s));
   } else {
+    // (a4) unpack dt_low / B / C; (a5) dt_proj + softplus; (a6)+(a7) scan, D skip, gate
+    t->launches++;
+    CU(launch_unpack(bf, dsrc, nsrc, doff, (int)M, hl, R, N, c.bcdt_rmsnorm, c.rms_eps, dlow, BC, s));
     {
-    Probe pr(t, SSM_PROBE_DT_PROJ, s);
-    for (int j = 0; j < hl; ++j) {
-      const int c0 = j * t->cph;
-      const char* dl_j = reinterpret_cast<const char*>(dlow) + (size_t)j * M * R * es;
-      CU(gemm(t, dl_j, R, reinterpret_cast<const char*>(w->w_dt) + (size_t)c0 * R * es, R, (int)M, t->cph, R, 1,
-              epi(ksp, 0, reinterpret_cast<char*>(delta) + c0 * es, Ek, w->b_dt + c0), s));
-    }
+      Probe pr(t, SSM_PROBE_DT_PROJ, s);
+      for (int j = 0; j < hl; ++j) {
+        const int c0 = j * t->cph;
+        const char* dl_j = reinterpret_cast<const char*>(dlow) + (size_t)j * M * R * es;
+        CU(gemm(t, dl_j, R, reinterpret_cast<const char*>(w->w_dt) + (size_t)c0 * R * es, R, (int)M, t->cph, R, 1,
+                epi(ksp, 0, reinterpret_cast<char*>(delta) + c0 * es, Ek, w->b_dt + c0), s));
+      }
     }
     Probe pr(t, SSM_PROBE_SCAN, s);
     for (int j = 0; j < hl; ++j) {
@@ -289,47 +325,32 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     }
   }
 
-  // (a8)+(a9) out_proj, row-parallel partial, finished by AR#2 at the residual boundary
-  const int64_t nD = M * D;
-  auto out_gemm = [&](float* dst, bool accumulate_into) -> cudaError_t {
-    // dst += partial (accumulate_into) or dst = partial
-    if (swap) {
-      const int ks = pick_ksplit(t, D, (int)M, Ek);
-      if (ks > 1 || accumulate_into) {
-        if (!accumulate_into) {
-          cudaError_t e = cudaMemsetAsync(dst, 0, nD * 4, s);
-          if (e != cudaSuccess) return e;
-        }
-        return gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks, epi(EPI_ATOMIC_F32, 1, dst, D), s);
-      }
-      return gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, 1, epi(EPI_STORE_F32, 1, dst, D), s);
-    }
-    return gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(accumulate_into ? EPI_ADD_F32 : EPI_STORE_F32, 0, dst, D), s);
-  };
-  Probe pr(t, SSM_PROBE_OUT_PROJ, s);
-  if (t->k == 1) {
-    CU(out_gemm(residual, true));
-  } else if (flags & SSM_AR2_EXTERNAL) {
-    CU(out_gemm(residual, false));
-  } else if (flags & SSM_AR2_FP32) {
-    const uint32_t ep = ++t->epoch;
-    CU(out_gemm(reinterpret_cast<float*>(own_half(ep)), false));
+  // (a8) out_proj, row-parallel partial (TP=1: added straight into the fp32 residual)
+  {
+    Probe pr(t, SSM_PROBE_OUT_PROJ, s);
+    if (swap)
+      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, epi(EPI_ATOMIC_F32, 1, odst, D), s));
+    else
+      CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D), s));
+  }
+  // (a9) AR#2 at the residual boundary
+  if (omode == OUT_FP32) {
+    Probe pr(t, SSM_PROBE_AR2, s);
     t->ar_count++;
     t->bytes_sent += nD * 4;
     t->launches += 2;
     CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
-    CU(launch_f32_reduce(t->peers, t->k, half_off(ep), nD, residual, 1, s));
-  } else {  // SSM_AR2_INT8 (default)
-    const uint32_t ep = ++t->epoch;
-    CU(out_gemm(part, false));
-    int8_t* q = reinterpret_cast<int8_t*>(own_half(ep));
-    float* sc = reinterpret_cast<float*>(own_half(ep) + al256(nD));
+    CU(launch_f32_reduce(t->peers, t->k, half_off(ep2), nD, residual, 1, s));
+  } else if (omode == OUT_INT8) {
+    Probe pr(t, SSM_PROBE_AR2, s);
+    int8_t* q = reinterpret_cast<int8_t*>(own_half(ep2));
+    float* sc = reinterpret_cast<float*>(own_half(ep2) + al256(nD));
     t->launches += 3;
     CU(launch_quantize(part, nD, c.qar_block, q, sc, s));
     t->ar_count++;
     t->bytes_sent += nD + nD / c.qar_block * 4;
     CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
-    CU(launch_qar_reduce(t->peers, t->k, half_off(ep), half_off(ep) + (int64_t)al256(nD), nD, c.qar_block, residual,
+    CU(launch_qar_reduce(t->peers, t->k, half_off(ep2), half_off(ep2) + (int64_t)al256(nD), nD, c.qar_block, residual,
                          1, s));
   }
   return SSM_OK;
@@ -406,9 +427,20 @@ ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp
   t->es = t->bf16 ? 2 : 4;
   t->epoch = 0;
   int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) {
     t->num_sms = sms;
-  else {
+    static std::once_flag once;
+    static cudaError_t pre = cudaSuccess;
+    std::call_once(once, [] {
+      pre = preload_kernels();
+      if (pre == cudaSuccess) pre = preload_gemm_simt();
+      if (pre == cudaSuccess) pre = preload_gemm_tc();
+    });
+    if (pre != cudaSuccess) {
+      delete t;
+      return fail(SSM_ERR_CUDA, "kernel preload failed: %s", cudaGetErrorString(pre));
+    }
+  } else {
     cudaGetLastError();
     t->num_sms = 148;
   }

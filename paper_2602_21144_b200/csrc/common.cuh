@@ -24,6 +24,33 @@ SSM_DEV float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+SSM_DEV float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// Packed fp32x2 FMA-pipe ops (sm_100: FFMA2 / FMUL2 — one issue slot for two lanes of work).
+SSM_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+SSM_DEV float2 fmul2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
+// SiLU with a single MUFU op: v * sigmoid(v) = 0.5 v (1 + tanh(v/2))  (bf16 mode; the tanh.approx
+// error ~2^-11 is below bf16 output rounding)
+SSM_DEV float silu_tanh(float v) {
+  const float hv = 0.5f * v;
+  return fmaf(hv, tanh_approx(hv), hv);
+}
 // SiLU(v) = v * sigmoid(v).  Fast form for bf16 mode (MUFU ex2 + rcp); accurate form
 // (expf, IEEE division) for the fp32 mode's 1e-5 tolerance.
 template <bool kFast>

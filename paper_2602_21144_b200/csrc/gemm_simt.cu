@@ -75,6 +75,13 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ A,
 }
 }  // namespace
 
+cudaError_t preload_gemm_simt() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, (const void*)gemm_simt_kernel<float>);
+  if (e != cudaSuccess) return e;
+  return cudaFuncGetAttributes(&a, (const void*)gemm_simt_kernel<__nv_bfloat16>);
+}
+
 cudaError_t gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, int dtype_bf16, int M, int N, int K,
                       int ksplit, const Epilogue& epi, cudaStream_t s) {
   if (M <= 0 || N <= 0) return cudaSuccess;

@@ -26,10 +26,17 @@
 namespace ssm {
 
 namespace {
-constexpr int BM = 128, BK = 64, STAGES = 4, BN_MAX = 256;
+constexpr int BM = 128, BK = 64, BN_MAX = 256, MAX_STAGES = 16;
 constexpr int A_STAGE = BM * BK * 2;      // 16 KB
-constexpr int B_STAGE = BN_MAX * BK * 2;  // 32 KB
-constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + 256;
+constexpr int SMEM_BYTES = 227 * 1024;              // ring stages are sized to fill what is left
+constexpr int RING_BYTES = SMEM_BYTES - 1024 - 512;
+// stage = A tile (128 x 64 bf16) + B tile (BN x 64 bf16); as many stages as fit (small-N decode
+// GEMMs are latency-bound weight streams and need many bytes in flight)
+__host__ __device__ inline int stage_bytes(int BN) { return A_STAGE + BN * BK * 2; }
+__host__ __device__ inline int num_stages(int BN) {
+  const int s = RING_BYTES / stage_bytes(BN);
+  return s > MAX_STAGES ? MAX_STAGES : s;
+}
 constexpr int kThreads = 192;
 
 struct TileSched {
@@ -44,95 +51,104 @@ struct TileSched {
   }
 };
 
-__device__ __forceinline__ void epi_store32(const Epilogue& e, int m, int n0, int M, int N, const uint32_t (&r)[32]) {
+// Epilogue for one warp's 32 x 32 chunk: lane = row m0 + lane, columns n0..n0+31, stored
+// straight from registers (staging through shared memory would compete with the UMMA operand
+// reads for smem bandwidth in the MMA-bound projections).
+__device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int M, int N, uint32_t (&r)[32]) {
+  const int kind = e.kind;
+  const int m = m0 + threadIdx.x % 32;
   if (m >= M) return;
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-  const int kind = e.kind;
-  if (kind == EPI_SOFTPLUS_BF16 || kind == EPI_SOFTPLUS_F32) {
-    const float* b = e.bias + (e.trans ? 0 : n0);
+  if (kind == EPI_SOFTPLUS_BF16) {  // bf16 output: 2-MUFU softplus (error far below bf16 rounding)
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      float bb = e.trans ? e.bias[m] : ((n0 + j < N) ? b[j] : 0.f);
-      v[j] = softplus(v[j] + bb);
+      const float x = v[j] + (e.trans ? e.bias[m] : ((n0 + j < N) ? e.bias[n0 + j] : 0.f));
+      v[j] = x > 20.f ? x : 0.6931471805599453f * __log2f(1.f + ex2_approx(x * 1.4426950408889634f));
     }
+  } else if (kind == EPI_SOFTPLUS_F32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      v[j] = softplus(v[j] + (e.trans ? e.bias[m] : ((n0 + j < N) ? e.bias[n0 + j] : 0.f)));
   }
-  const bool full = (n0 + 32 <= N);
-  if (!e.trans) {
-    const int64_t base = (int64_t)m * e.ldc + n0;
-    if (kind == EPI_STORE_BF16 || kind == EPI_SOFTPLUS_BF16) {
-      __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(e.C) + base;
-      if (full && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 pk;
-          uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            __nv_bfloat162 t2 = __floats2bfloat162_rn(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]);
-            pw[j] = *reinterpret_cast<uint32_t*>(&t2);
-          }
-          reinterpret_cast<uint4*>(C)[q] = pk;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (n0 + j < N) C[j] = __float2bfloat16_rn(v[j]);
-      }
-    } else {
-      float* C = reinterpret_cast<float*>(e.C) + base;
-      if (kind == EPI_STORE_F32 || kind == EPI_SOFTPLUS_F32) {
-        if (full && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            reinterpret_cast<float4*>(C)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (n0 + j < N) C[j] = v[j];
-        }
-      } else if (kind == EPI_ADD_F32) {
-        if (full && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float4 o = reinterpret_cast<float4*>(C)[q];
-            o.x += v[4 * q]; o.y += v[4 * q + 1]; o.z += v[4 * q + 2]; o.w += v[4 * q + 3];
-            reinterpret_cast<float4*>(C)[q] = o;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (n0 + j < N) C[j] += v[j];
-        }
-      } else {  // EPI_ATOMIC_F32
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (n0 + j < N) atomicAdd(C + j, v[j]);
-      }
-    }
-  } else {
-    // transposed: element (m, n) -> C[n * ldc + m]; lanes hold consecutive m -> coalesced per n
+  if (e.trans) {
+    // element (m, n) -> C[n * ldc + m]; lanes hold consecutive m -> coalesced per n
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int n = n0 + j;
-      if (n >= N) break;
+      if (n >= N) continue;
       const int64_t idx = (int64_t)n * e.ldc + m;
       switch (kind) {
         case EPI_STORE_BF16:
-        case EPI_SOFTPLUS_BF16:
-          reinterpret_cast<__nv_bfloat16*>(e.C)[idx] = __float2bfloat16_rn(v[j]);
-          break;
+        case EPI_SOFTPLUS_BF16: reinterpret_cast<__nv_bfloat16*>(e.C)[idx] = __float2bfloat16_rn(v[j]); break;
         case EPI_STORE_F32:
-        case EPI_SOFTPLUS_F32:
-          reinterpret_cast<float*>(e.C)[idx] = v[j];
-          break;
-        case EPI_ADD_F32:
-          reinterpret_cast<float*>(e.C)[idx] += v[j];
-          break;
-        default:
-          atomicAdd(reinterpret_cast<float*>(e.C) + idx, v[j]);
+        case EPI_SOFTPLUS_F32: reinterpret_cast<float*>(e.C)[idx] = v[j]; break;
+        case EPI_ADD_F32: reinterpret_cast<float*>(e.C)[idx] += v[j]; break;
+        default: atomicAdd(reinterpret_cast<float*>(e.C) + idx, v[j]);
       }
+    }
+    return;
+  }
+  const bool full = (n0 + 32 <= N);
+  const int64_t base = (int64_t)m * e.ldc + n0;
+  if (kind == EPI_STORE_BF16 || kind == EPI_SOFTPLUS_BF16) {
+    __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(e.C) + base;
+    if (full && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 pk;
+        uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          __nv_bfloat162 t2 = __floats2bfloat162_rn(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]);
+          pw[j] = *reinterpret_cast<uint32_t*>(&t2);
+        }
+        reinterpret_cast<uint4*>(C)[q] = pk;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) C[j] = __float2bfloat16_rn(v[j]);
+    }
+    return;
+  }
+  float* C = reinterpret_cast<float*>(e.C) + base;
+  const bool vec = full && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+  if (kind == EPI_STORE_F32 || kind == EPI_SOFTPLUS_F32) {
+    if (vec) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(C)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) C[j] = v[j];
+    }
+  } else if (kind == EPI_ADD_F32) {
+    if (vec) {
+      float4 o[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] = reinterpret_cast<const float4*>(C)[q];   // all loads first
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        o[q].x += v[4 * q]; o[q].y += v[4 * q + 1]; o[q].z += v[4 * q + 2]; o[q].w += v[4 * q + 3];
+        reinterpret_cast<float4*>(C)[q] = o[q];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) C[j] += v[j];
+    }
+  } else {  // EPI_ATOMIC_F32
+    if (vec) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        atomicAdd(reinterpret_cast<float4*>(C) + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) atomicAdd(C + j, v[j]);
     }
   }
 }
@@ -142,11 +158,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                    int BN, TileSched ts, Epilogue epi) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  const int STAGES = num_stages(BN);
+  const int SB = stage_bytes(BN);
+  uint8_t* ring = smem;  // stage i: A at ring + i*SB, B at ring + i*SB + A_STAGE (1024-B aligned)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
+  uint64_t* empty = full + MAX_STAGES;
+  uint64_t* tfull = empty + MAX_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -184,8 +201,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], ph ^ 1);
           mbar_arrive_expect_tx(&full[stage], tx);
-          tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, mt * BM);
-          tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, nt * BN);
+          tma_load_2d(ring + stage * SB, &tmA, &full[stage], kb * BK, mt * BM);
+          tma_load_2d(ring + stage * SB + A_STAGE, &tmB, &full[stage], kb * BK, nt * BN);
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
       }
@@ -208,8 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], ph);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * A_STAGE);
-          const uint32_t b0 = smem_u32(sB + stage * B_STAGE);
+          const uint32_t a0 = smem_u32(ring + stage * SB);
+          const uint32_t b0 = a0 + A_STAGE;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             umma_bf16(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
@@ -225,7 +242,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ---------------- epilogue warps 2..5; TMEM lane group = warp % 4
     const int eg = warp & 3;
-    const int row = eg * 32 + lane;
     int acc = 0;
     uint32_t acc_ph = 0;
     for (int u = blockIdx.x; u < ts.units; u += gridDim.x) {
@@ -234,13 +250,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (kb0 >= kb1) continue;
       mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
-      const int m = mt * BM + row;
+      const int m0 = mt * BM + eg * 32;
       const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * BN_MAX);
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tbase + c * 32, r);
         tmem_ld_wait();
-        epi_store32(epi, m, nt * BN + c * 32, M, N, r);
+        epi_chunk(epi, m0, nt * BN + c * 32, M, N, r);
       }
       tc_fence_before();
       __syncwarp();
@@ -286,6 +302,13 @@ bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int
   return r == CUDA_SUCCESS;
 }
 }  // namespace
+
+cudaError_t preload_gemm_tc() {
+  cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, (const void*)gemm_tc_kernel);
+}
 
 bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb) {
   return ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) &&

@@ -48,8 +48,11 @@ cudaError_t launch_conv1d_silu(int bf16, const void* xz, int64_t ldxz, const voi
                                cudaStream_t s);
 cudaError_t launch_conv_state_update(int bf16, const void* xz, int64_t ldxz, void* conv_state, int batch, int L,
                                      int Ek, int K, cudaStream_t s);
+// Decode conv update; also zero-fills [zero0, zero0+nzero0) and [zero1, zero1+nzero1) floats
+// (split-K accumulation targets of the next GEMMs; counts multiple of 4, 16-B aligned).
 cudaError_t launch_conv_decode(int bf16, const void* xz, int64_t ldxz, void* conv_state, const float* conv_w,
-                               const float* conv_b, void* u, int64_t ldu, int batch, int Ek, int K, cudaStream_t s);
+                               const float* conv_b, void* u, int64_t ldu, int batch, int Ek, int K, float* zero0,
+                               int64_t nzero0, float* zero1, int64_t nzero1, cudaStream_t s);
 // Sum k_src fp32 partials [M, ldp] (fixed order), optional per-field RMSNorm, split into
 // dt_low (T, [hloc][M][R]) and BC (f32, [hloc][M][2N]).
 cudaError_t launch_unpack(int bf16, Peers src, int nsrc, int64_t src_off_bytes, int M, int hloc, int R, int N,
@@ -58,10 +61,12 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
                         const void* z, int64_t ldz, const float* BC, int64_t ldbc, const float* a_log,
                         const float* d_skip, float* h, int64_t h_bstride, void* g, int64_t ldg, int batch, int L,
                         int nch, int N, cudaStream_t s);
-cudaError_t launch_decode_step(int bf16, const void* u, const void* z, int64_t ldz, const void* dlow,
-                               const float* BC, const void* w_dt, const float* b_dt, const float* a_log,
-                               const float* d_skip, float* h, void* g, int batch, int Ek, int R, int N,
-                               int ch_per_head, int hloc, cudaStream_t s);
+// Decode step: sum of nsrc dbc partials [batch][ldp] at src_off (fixed order) (+RMSNorm),
+// dt_proj + softplus, scan step, gate; h [batch][Ek][N] in place.
+cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
+                               const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
+                               const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
+                               int N, int ch_per_head, cudaStream_t s);
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
                            cudaStream_t s);
 // int8 quantisation of n fp32 values in blocks of blk: q [n] int8, scale [n/blk] f32.
@@ -74,5 +79,10 @@ cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* o
 // of every peer's signal area, wait for all peers' slots in our own area to reach it
 // (bounded; sets the error word on timeout).
 cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s);
+
+// Load every kernel eagerly (called once per process from ssm_tp_init when a device exists).
+cudaError_t preload_kernels();
+cudaError_t preload_gemm_simt();
+cudaError_t preload_gemm_tc();
 
 }  // namespace ssm

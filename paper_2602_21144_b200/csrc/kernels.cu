@@ -83,21 +83,32 @@ __global__ void __launch_bounds__(64) conv1d_silu_kernel(const T* __restrict__ x
     else
       Vec<T, V>::load(cst + ((int64_t)b * (K - 1) + (K - 1) + t) * Ek + d0, win[j + 1]);
   }
-  for (int t = t0; t < t1; ++t) {
+  // 4 tokens per step: the 4 row loads are issued before any is consumed (latency hiding)
+  constexpr int TB = 4;
+  for (int tb = t0; tb < t1; tb += TB) {
+    float xin[TB][V];
 #pragma unroll
-    for (int j = 0; j < K - 1; ++j)
+    for (int i = 0; i < TB; ++i)
+      if (tb + i < t1) Vec<T, V>::load(xz + ((int64_t)b * L + tb + i) * ldxz + d0, xin[i]);
 #pragma unroll
-      for (int v = 0; v < V; ++v) win[j][v] = win[j + 1][v];
-    Vec<T, V>::load(xz + ((int64_t)b * L + t) * ldxz + d0, win[K - 1]);
-    float o[V];
+    for (int i = 0; i < TB; ++i) {
+      if (tb + i >= t1) break;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      float acc = bias[v];
+      for (int j = 0; j < K - 1; ++j)
 #pragma unroll
-      for (int j = 0; j < K; ++j) acc = fmaf(w[j][v], win[j][v], acc);
-      o[v] = silu<FAST>(acc);
+        for (int v = 0; v < V; ++v) win[j][v] = win[j + 1][v];
+#pragma unroll
+      for (int v = 0; v < V; ++v) win[K - 1][v] = xin[i][v];
+      float o[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        float acc = bias[v];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = fmaf(w[j][v], win[j][v], acc);
+        o[v] = FAST ? silu_tanh(acc) : silu<false>(acc);
+      }
+      Vec<T, V>::store(u + ((int64_t)b * L + tb + i) * ldu + d0, o);
     }
-    Vec<T, V>::store(u + ((int64_t)b * L + t) * ldu + d0, o);
   }
 }
 
@@ -121,8 +132,12 @@ __global__ void conv_state_update_kernel(const T* __restrict__ xz, int64_t ldxz,
 template <typename T, bool FAST>
 __global__ void conv_decode_kernel(const T* __restrict__ xz, int64_t ldxz, T* __restrict__ cst,
                                    const float* __restrict__ cw, const float* __restrict__ cb, T* __restrict__ u,
-                                   int64_t ldu, int batch, int Ek, int K) {
+                                   int64_t ldu, int batch, int Ek, int K, float4* __restrict__ z0, int64_t n0,
+                                   float4* __restrict__ z1, int64_t n1) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  // zero the split-K accumulation targets of the following GEMMs (x_proj, out_proj partial)
+  for (int64_t i = idx; i < n0; i += (int64_t)gridDim.x * blockDim.x) z0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t i = idx; i < n1; i += (int64_t)gridDim.x * blockDim.x) z1[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (idx >= batch * Ek) return;
   const int b = idx / Ek, d = idx % Ek;
   float win[8];
@@ -250,6 +265,7 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
   };
 
   float A[N], hs[N];
+  float2 A2[N / 2], h2[N / 2];
   float Dd = 0.f;
   float* hp = h + (int64_t)b * h_bstride + (int64_t)(valid ? d : 0) * N;
   if (valid) {
@@ -258,6 +274,11 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
       const float a = -expf(a_log[(int64_t)d * N + n]);
       A[n] = FAST ? a * 1.4426950408889634f : a;
       hs[n] = hp[n];
+    }
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      A2[i] = make_float2(A[2 * i], A[2 * i + 1]);
+      h2[i] = make_float2(hs[2 * i], hs[2 * i + 1]);
     }
     Dd = d_skip[d];
   }
@@ -278,112 +299,246 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
     if (valid) {
       const int tb = it * SC_TT;
       const int tn = min(SC_TT, L - tb);
-      for (int r = 0; r < tn; ++r) {
-        const float uu = io<T>::ld(&su[buf][r][tid]);
-        const float de = io<T>::ld(&sd[buf][r][tid]);
-        const float zz = io<T>::ld(&sz[buf][r][tid]);
-        const float du = de * uu;
-        const float* Bt = sbc[buf][r];
-        const float* Ct = Bt + N;
-        float y = 0.f;
+      if constexpr (FAST) {
+        // packed fp32x2 state math: 16 ex2 on the MUFU pipe, 32 FFMA2/FMUL2 on the FMA pipe per token
+        for (int r = 0; r < tn; ++r) {
+          const float uu = io<T>::ld(&su[buf][r][tid]);
+          const float de = io<T>::ld(&sd[buf][r][tid]);
+          const float zz = io<T>::ld(&sz[buf][r][tid]);
+          const float2 de2 = make_float2(de, de);
+          const float du = de * uu;
+          const float2 du2 = make_float2(du, du);
+          const float4* B4 = reinterpret_cast<const float4*>(sbc[buf][r]);
+          const float4* C4 = reinterpret_cast<const float4*>(sbc[buf][r] + N);
+          float2 ya = make_float2(0.f, 0.f), yb = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int n = 0; n < N; ++n) {
-          const float a = FAST ? ex2_approx(de * A[n]) : expf(de * A[n]);
-          hs[n] = fmaf(a, hs[n], du * Bt[n]);
-          y = fmaf(Ct[n], hs[n], y);
+          for (int q = 0; q < N / 4; ++q) {
+            const float4 b4 = B4[q], c4 = C4[q];
+            const float2 dA0 = fmul2(de2, A2[2 * q]);
+            const float2 dA1 = fmul2(de2, A2[2 * q + 1]);
+            const float2 a0 = make_float2(ex2_approx(dA0.x), ex2_approx(dA0.y));
+            const float2 a1 = make_float2(ex2_approx(dA1.x), ex2_approx(dA1.y));
+            h2[2 * q] = ffma2(a0, h2[2 * q], fmul2(du2, make_float2(b4.x, b4.y)));
+            h2[2 * q + 1] = ffma2(a1, h2[2 * q + 1], fmul2(du2, make_float2(b4.z, b4.w)));
+            ya = ffma2(make_float2(c4.x, c4.y), h2[2 * q], ya);
+            yb = ffma2(make_float2(c4.z, c4.w), h2[2 * q + 1], yb);
+          }
+          float y = (ya.x + ya.y) + (yb.x + yb.y);
+          y = fmaf(Dd, uu, y);
+          io<T>::st(g + (row0 + tb + r) * ldg + d, y * silu_tanh(zz));
         }
-        y = fmaf(Dd, uu, y);
-        io<T>::st(g + (row0 + tb + r) * ldg + d, y * silu<FAST>(zz));
+      } else {
+        for (int r = 0; r < tn; ++r) {
+          const float uu = io<T>::ld(&su[buf][r][tid]);
+          const float de = io<T>::ld(&sd[buf][r][tid]);
+          const float zz = io<T>::ld(&sz[buf][r][tid]);
+          const float du = de * uu;
+          const float* Bt = sbc[buf][r];
+          const float* Ct = Bt + N;
+          float y = 0.f;
+#pragma unroll
+          for (int n = 0; n < N; ++n) {
+            const float a = expf(de * A[n]);
+            hs[n] = fmaf(a, hs[n], du * Bt[n]);
+            y = fmaf(Ct[n], hs[n], y);
+          }
+          y = fmaf(Dd, uu, y);
+          io<T>::st(g + (row0 + tb + r) * ldg + d, y * silu<false>(zz));
+        }
       }
     }
     __syncthreads();
   }
   if (valid) {
+    if constexpr (FAST) {
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) { hs[2 * i] = h2[i].x; hs[2 * i + 1] = h2[i].y; }
+    }
 #pragma unroll
     for (int n = 0; n < N; ++n) hp[n] = hs[n];
   }
 }
 
 // ---------------------------------------------------------------- decode step
-// dt_proj + softplus + one scan step + gate for 32 channels x all batch rows per block.
+// One token per sequence: AR#1 fixed-order sum of the dbc partials (+ Falcon dt/B/C RMSNorm),
+// dt_proj + softplus, one scan step and the gate, for 32 channels x all batch rows per block;
+// h updated in place.  All global loads of a phase are issued before they are consumed
+// (decode is latency-bound: one HBM round trip per phase).
+constexpr int DS_CH = 32;
 template <typename T, int N, bool FAST>
-__global__ void __launch_bounds__(256) decode_step_kernel(const T* __restrict__ u, const T* __restrict__ z,
-                                                          int64_t ldz, const T* __restrict__ dlow,
-                                                          const float* __restrict__ BC, const T* __restrict__ w_dt,
+__global__ void __launch_bounds__(256) decode_step_kernel(Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm,
+                                                          float eps, const T* __restrict__ u, const T* __restrict__ z,
+                                                          int64_t ldz, const T* __restrict__ w_dt,
                                                           const float* __restrict__ b_dt,
                                                           const float* __restrict__ a_log,
                                                           const float* __restrict__ d_skip, float* __restrict__ h,
                                                           T* __restrict__ g, int batch, int Ek, int R,
                                                           int ch_per_head) {
-  extern __shared__ float dsm[];
-  const int Rp = R + 1;
-  float* sW = dsm;                 // [32][Rp]
-  float* sdl = dsm + 32 * Rp;      // [batch][R]
-  const int c0 = blockIdx.x * 32;
-  const int hd = c0 / ch_per_head;  // local head of this block (ch_per_head % 32 == 0)
-  for (int i = threadIdx.x; i < 32 * R; i += blockDim.x) {
-    const int c = i / R, r = i % R;
-    sW[c * Rp + r] = (c0 + c < Ek) ? io<T>::ld(w_dt + (int64_t)(c0 + c) * R + r) : 0.f;
+  extern __shared__ __align__(16) float dsm[];
+  const int P = R + 2 * N;
+  const int R4 = ((R + 3) & ~3) + 4;      // padded fp32 row of W_dt (16-B aligned, bank-spread)
+  const int P4 = (P + 3) & ~3;
+  float* sW = dsm;                        // [DS_CH][R4]
+  float* sD = sW + DS_CH * R4;            // [batch][P4]  summed dbc rows of this block's head
+  float* sA = sD + batch * P4;            // [DS_CH][N]   A (log2e-scaled in FAST mode)
+  float* sS = sA + DS_CH * N;             // [batch][3]   RMSNorm scales
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * DS_CH;
+  const int hd = c0 / ch_per_head;
+
+  // phase 1: W_dt rows, dbc rows (sum over sources), A
+  constexpr int V = 16 / sizeof(T);
+  if ((R % V) == 0) {
+    const int cpr = R / V;
+    for (int i = tid; i < DS_CH * cpr; i += blockDim.x) {
+      const int c = i / cpr, q = i % cpr;
+      float v[V];
+      if (c0 + c < Ek) {
+        if constexpr (sizeof(T) == 2) {
+          uint4 raw = *reinterpret_cast<const uint4*>(w_dt + (int64_t)(c0 + c) * R + q * V);
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+          for (int k = 0; k < V / 2; ++k) { float2 f = __bfloat1622float2(b2[k]); v[2 * k] = f.x; v[2 * k + 1] = f.y; }
+        } else {
+          float4 f = *reinterpret_cast<const float4*>(w_dt + (int64_t)(c0 + c) * R + q * V);
+          v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) sW[c * R4 + q * V + k] = v[k];
+    }
+  } else {
+    for (int i = tid; i < DS_CH * R; i += blockDim.x) {
+      const int c = i / R, r = i % R;
+      sW[c * R4 + r] = (c0 + c < Ek) ? io<T>::ld(w_dt + (int64_t)(c0 + c) * R + r) : 0.f;
+    }
   }
-  for (int i = threadIdx.x; i < batch * R; i += blockDim.x) {
-    const int bb = i / R, r = i % R;
-    sdl[bb * R + r] = io<T>::ld(dlow + ((int64_t)hd * batch + bb) * R + r);
+  for (int i = tid; i < batch * P; i += blockDim.x) {
+    const int b = i / P, c = i % P;
+    const int64_t idx = (int64_t)b * ldp + (int64_t)hd * P + c;
+    float acc = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[0]) + src_off)[idx];
+    for (int r = 1; r < nsrc; ++r)  // fixed rank order (reading Q12)
+      acc += reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[r]) + src_off)[idx];
+    sD[b * P4 + c] = acc;
+  }
+  for (int i = tid; i < DS_CH * N; i += blockDim.x) {
+    const int c = i / N, n = i % N;
+    const float a = (c0 + c < Ek) ? -expf(a_log[(int64_t)(c0 + c) * N + n]) : 0.f;
+    sA[i] = FAST ? a * 1.4426950408889634f : a;
   }
   __syncthreads();
-  for (int it = threadIdx.x; it < batch * 32; it += blockDim.x) {
-    const int bb = it / 32, c = it % 32;
+  if (rmsnorm) {  // weightless RMSNorm of dt_low, B, C per batch row (Falcon-Mamba, reading Q18)
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int b = warp; b < batch; b += blockDim.x >> 5) {
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+      for (int c = lane; c < P; c += 32) {
+        const float v = sD[b * P4 + c];
+        if (c < R) s0 = fmaf(v, v, s0);
+        else if (c < R + N) s1 = fmaf(v, v, s1);
+        else s2 = fmaf(v, v, s2);
+      }
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        float x = f == 0 ? s0 : (f == 1 ? s1 : s2);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) sS[b * 3 + f] = 1.0f / sqrtf(x / (float)(f == 0 ? R : N) + eps);
+      }
+    }
+  }
+  __syncthreads();
+
+  // phase 2: items (b, c), warp = fixed b, lane = channel
+  for (int it = tid; it < batch * DS_CH; it += blockDim.x) {
+    const int b = it / DS_CH, c = it % DS_CH;
     const int d = c0 + c;
     if (d >= Ek) continue;
-    float dt = b_dt[d];
-    const float* wr = sW + c * Rp;
-    const float* xr = sdl + bb * R;
-    for (int r = 0; r < R; ++r) dt = fmaf(xr[r], wr[r], dt);
-    const float de = softplus(dt);
-    const float uu = io<T>::ld(u + (int64_t)bb * Ek + d);
-    const float zz = io<T>::ld(z + (int64_t)bb * ldz + d);
-    const float* Bt = BC + ((int64_t)hd * batch + bb) * 2 * N;
-    const float* Ct = Bt + N;
-    float* hp = h + ((int64_t)bb * Ek + d) * N;
+    float* hp = h + ((int64_t)b * Ek + d) * N;
+    float hs[N];
+#pragma unroll
+    for (int n = 0; n < N; n += 4) {
+      const float4 t4 = *reinterpret_cast<const float4*>(hp + n);
+      hs[n] = t4.x; hs[n + 1] = t4.y; hs[n + 2] = t4.z; hs[n + 3] = t4.w;
+    }
+    const float uu = io<T>::ld(u + (int64_t)b * Ek + d);
+    const float zz = io<T>::ld(z + (int64_t)b * ldz + d);
+    const float bias = b_dt[d], Dd = d_skip[d];
+    const float* wr = sW + c * R4;
+    const float* xr = sD + b * P4;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    const int R4e = R & ~3;
+    for (int r = 0; r < R4e; r += 4) {
+      const float4 wv = *reinterpret_cast<const float4*>(wr + r);
+      const float4 xv = *reinterpret_cast<const float4*>(xr + r);
+      s0 = fmaf(xv.x, wv.x, s0); s1 = fmaf(xv.y, wv.y, s1); s2 = fmaf(xv.z, wv.z, s2); s3 = fmaf(xv.w, wv.w, s3);
+    }
+    for (int r = R4e; r < R; ++r) s0 = fmaf(xr[r], wr[r], s0);
+    float dt = (s0 + s1) + (s2 + s3);
+    if (rmsnorm) dt *= sS[b * 3 + 0];
+    const float de = softplus(dt + bias);
     const float du = de * uu;
+    const float sB = rmsnorm ? sS[b * 3 + 1] : 1.f;
+    const float sC = rmsnorm ? sS[b * 3 + 2] : 1.f;
+    const float* Bt = xr + R;
+    const float* Ct = xr + R + N;
+    const float* Ac = sA + c * N;
     float y = 0.f;
 #pragma unroll
     for (int n = 0; n < N; ++n) {
-      const float a = -expf(a_log[(int64_t)d * N + n]);
-      const float ab = FAST ? ex2_approx(de * a * 1.4426950408889634f) : expf(de * a);
-      const float hn = fmaf(ab, hp[n], du * Bt[n]);
-      hp[n] = hn;
-      y = fmaf(Ct[n], hn, y);
+      const float ab = FAST ? ex2_approx(de * Ac[n]) : expf(de * Ac[n]);
+      hs[n] = fmaf(ab, hs[n], du * (Bt[n] * sB));
+      y = fmaf(Ct[n] * sC, hs[n], y);
     }
-    y = fmaf(d_skip[d], uu, y);
-    io<T>::st(g + (int64_t)bb * Ek + d, y * silu<FAST>(zz));
+#pragma unroll
+    for (int n = 0; n < N; n += 4) *reinterpret_cast<float4*>(hp + n) = make_float4(hs[n], hs[n + 1], hs[n + 2], hs[n + 3]);
+    y = fmaf(Dd, uu, y);
+    io<T>::st(g + (int64_t)b * Ek + d, y * silu<FAST>(zz));
   }
 }
 
 // ---------------------------------------------------------------- RMSNorm (glue)
+// One 128-thread block per row, the row cached in registers (<= 16 float4 per thread).
 template <typename T>
-__global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, float eps, T* __restrict__ y,
-                               int64_t M, int D) {
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= M) return;
-  const float* xr = x + row * D;
+__global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                                                      float eps, T* __restrict__ y, int64_t M, int D) {
+  constexpr int MAXV = 16;
+  __shared__ float red[4];
+  const int64_t row = blockIdx.x;
+  const int tid = threadIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * D);
+  const int nv = D / 4;
+  float4 v[MAXV];
   float ss = 0.f;
-  for (int i = lane * 4; i < D; i += 128) {
-    float4 v = *reinterpret_cast<const float4*>(xr + i);
-    ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int k = tid + i * 128;
+    if (k < nv) {
+      v[i] = xr[k];
+      ss = fmaf(v[i].x, v[i].x, ss); ss = fmaf(v[i].y, v[i].y, ss);
+      ss = fmaf(v[i].z, v[i].z, ss); ss = fmaf(v[i].w, v[i].w, ss);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const float rs = 1.0f / sqrtf(ss / (float)D + eps);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  __syncthreads();
+  const float tot = (red[0] + red[1]) + (red[2] + red[3]);
+  const float rs = 1.0f / sqrtf(tot / (float)D + eps);
   T* yr = y + row * D;
-  for (int i = lane * 4; i < D; i += 128) {
-    float4 v = *reinterpret_cast<const float4*>(xr + i);
-    float ww[4] = {1.f, 1.f, 1.f, 1.f};
-    if (w) { float4 t = *reinterpret_cast<const float4*>(w + i); ww[0] = t.x; ww[1] = t.y; ww[2] = t.z; ww[3] = t.w; }
-    io<T>::st(yr + i, v.x * rs * ww[0]);
-    io<T>::st(yr + i + 1, v.y * rs * ww[1]);
-    io<T>::st(yr + i + 2, v.z * rs * ww[2]);
-    io<T>::st(yr + i + 3, v.w * rs * ww[3]);
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int k = tid + i * 128;
+    if (k < nv) {
+      float4 ww = make_float4(1.f, 1.f, 1.f, 1.f);
+      if (w) ww = reinterpret_cast<const float4*>(w)[k];
+      io<T>::st(yr + 4 * k, v[i].x * rs * ww.x);
+      io<T>::st(yr + 4 * k + 1, v[i].y * rs * ww.y);
+      io<T>::st(yr + 4 * k + 2, v[i].z * rs * ww.z);
+      io<T>::st(yr + 4 * k + 3, v[i].w * rs * ww.w);
+    }
   }
 }
 
@@ -495,7 +650,7 @@ template <typename T, bool F>
 cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const float* cw, const float* cb, void* u,
                           int64_t ldu, int batch, int L, int Ek, int K, cudaStream_t s) {
   constexpr int V = vec_of<T>();
-  const int TCH = 32;
+  const int TCH = 16;
   dim3 grid((Ek / V + 63) / 64, (L + TCH - 1) / TCH, batch);
   const T* x = reinterpret_cast<const T*>(xz);
   const T* c = reinterpret_cast<const T*>(cs);
@@ -534,17 +689,21 @@ cudaError_t launch_conv_state_update(int bf16, const void* xz, int64_t ldxz, voi
 }
 
 cudaError_t launch_conv_decode(int bf16, const void* xz, int64_t ldxz, void* cs, const float* cw, const float* cb,
-                               void* u, int64_t ldu, int batch, int Ek, int K, cudaStream_t s) {
+                               void* u, int64_t ldu, int batch, int Ek, int K, float* zero0, int64_t nzero0,
+                               float* zero1, int64_t nzero1, cudaStream_t s) {
   const int n = batch * Ek;
   if (n <= 0) return cudaSuccess;
+  if ((nzero0 | nzero1) & 3) return cudaErrorInvalidValue;
+  float4* z0 = reinterpret_cast<float4*>(zero0);
+  float4* z1 = reinterpret_cast<float4*>(zero1);
   if (bf16)
     conv_decode_kernel<__nv_bfloat16, true><<<(n + 255) / 256, 256, 0, s>>>(
         reinterpret_cast<const __nv_bfloat16*>(xz), ldxz, reinterpret_cast<__nv_bfloat16*>(cs), cw, cb,
-        reinterpret_cast<__nv_bfloat16*>(u), ldu, batch, Ek, K);
+        reinterpret_cast<__nv_bfloat16*>(u), ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4);
   else
-    conv_decode_kernel<float, false><<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const float*>(xz), ldxz,
-                                                                     reinterpret_cast<float*>(cs), cw, cb,
-                                                                     reinterpret_cast<float*>(u), ldu, batch, Ek, K);
+    conv_decode_kernel<float, false><<<(n + 255) / 256, 256, 0, s>>>(
+        reinterpret_cast<const float*>(xz), ldxz, reinterpret_cast<float*>(cs), cw, cb, reinterpret_cast<float*>(u),
+        ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4);
   return cudaGetLastError();
 }
 
@@ -589,48 +748,52 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
   return scan_t<float, 8, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
 }
 
+static size_t dstep_smem(int batch, int R, int N) {
+  const int P = R + 2 * N;
+  const int R4 = ((R + 3) & ~3) + 4, P4 = (P + 3) & ~3;
+  return (size_t)(DS_CH * R4 + batch * P4 + DS_CH * N + batch * 3) * sizeof(float);
+}
+
 template <typename T, int N, bool F>
-static cudaError_t dstep_t(const void* u, const void* z, int64_t ldz, const void* dlow, const float* BC,
-                           const void* w_dt, const float* b_dt, const float* a_log, const float* d_skip, float* h,
-                           void* g, int batch, int Ek, int R, int cph, cudaStream_t s) {
-  const size_t smem = (size_t)(32 * (R + 1) + batch * R) * sizeof(float);
-  if (smem > 48 * 1024) {
+static cudaError_t dstep_t(Peers src, int nsrc, int64_t off, int ldp, int rms, float eps, const void* u, const void* z,
+                           int64_t ldz, const void* w_dt, const float* b_dt, const float* a_log, const float* d_skip,
+                           float* h, void* g, int batch, int Ek, int R, int cph, cudaStream_t s) {
+  const size_t smem = dstep_smem(batch, R, N);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(decode_step_kernel<T, N, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
+    attr = smem;
   }
-  decode_step_kernel<T, N, F><<<(Ek + 31) / 32, 256, smem, s>>>(
-      reinterpret_cast<const T*>(u), reinterpret_cast<const T*>(z), ldz, reinterpret_cast<const T*>(dlow), BC,
+  decode_step_kernel<T, N, F><<<(Ek + DS_CH - 1) / DS_CH, 256, smem, s>>>(
+      src, nsrc, off, ldp, rms, eps, reinterpret_cast<const T*>(u), reinterpret_cast<const T*>(z), ldz,
       reinterpret_cast<const T*>(w_dt), b_dt, a_log, d_skip, h, reinterpret_cast<T*>(g), batch, Ek, R, cph);
   return cudaGetLastError();
 }
 
-cudaError_t launch_decode_step(int bf16, const void* u, const void* z, int64_t ldz, const void* dlow,
-                               const float* BC, const void* w_dt, const float* b_dt, const float* a_log,
-                               const float* d_skip, float* h, void* g, int batch, int Ek, int R, int N,
-                               int ch_per_head, int hloc, cudaStream_t s) {
-  (void)hloc;
+cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
+                               const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
+                               const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
+                               int N, int ch_per_head, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
-  if (ch_per_head % 32 != 0) return cudaErrorInvalidValue;
-  if ((size_t)(32 * (R + 1) + batch * R) * sizeof(float) > 200 * 1024) return cudaErrorInvalidValue;
+  if (ch_per_head % DS_CH != 0) return cudaErrorInvalidValue;
+  if (dstep_smem(batch, R, N) > 200 * 1024) return cudaErrorInvalidValue;
   if (N != 16 && N != 8) return cudaErrorInvalidValue;
-  if (bf16) {
-    return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(u, z, ldz, dlow, BC, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s)
-                   : dstep_t<__nv_bfloat16, 8, true>(u, z, ldz, dlow, BC, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s);
-  }
-  return N == 16 ? dstep_t<float, 16, false>(u, z, ldz, dlow, BC, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s)
-                 : dstep_t<float, 8, false>(u, z, ldz, dlow, BC, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s);
+#define DS_ARGS src, nsrc, src_off, ldp, rmsnorm, eps, u, z, ldz, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s
+  if (bf16) return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(DS_ARGS) : dstep_t<__nv_bfloat16, 8, true>(DS_ARGS);
+  return N == 16 ? dstep_t<float, 16, false>(DS_ARGS) : dstep_t<float, 8, false>(DS_ARGS);
+#undef DS_ARGS
 }
 
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
                            cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
-  if (D % 4) return cudaErrorInvalidValue;
-  const int blocks = (int)((M + 7) / 8);
+  if (D % 4 || D > 16 * 128 * 4) return cudaErrorInvalidValue;
   if (bf16)
-    rmsnorm_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(x, w, eps, reinterpret_cast<__nv_bfloat16*>(y), M, D);
+    rmsnorm_kernel<__nv_bfloat16><<<(unsigned)M, 128, 0, s>>>(x, w, eps, reinterpret_cast<__nv_bfloat16*>(y), M, D);
   else
-    rmsnorm_kernel<float><<<blocks, 256, 0, s>>>(x, w, eps, reinterpret_cast<float*>(y), M, D);
+    rmsnorm_kernel<float><<<(unsigned)M, 128, 0, s>>>(x, w, eps, reinterpret_cast<float*>(y), M, D);
   return cudaGetLastError();
 }
 
@@ -661,6 +824,34 @@ cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* o
   const int64_t n4 = n / 4;
   f32_reduce_kernel<<<(int)((n4 + 255) / 256), 256, 0, s>>>(src, k, off, n4, out, accumulate);
   return cudaGetLastError();
+}
+
+// Force-load every kernel of this translation unit (CUDA lazy loading would otherwise load
+// a kernel at its first launch, which can wait on a spinning peer barrier of another
+// virtual rank on the same device).
+cudaError_t preload_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      (const void*)conv1d_silu_kernel<__nv_bfloat16, 2, true>, (const void*)conv1d_silu_kernel<__nv_bfloat16, 3, true>,
+      (const void*)conv1d_silu_kernel<__nv_bfloat16, 4, true>, (const void*)conv1d_silu_kernel<float, 2, false>,
+      (const void*)conv1d_silu_kernel<float, 3, false>, (const void*)conv1d_silu_kernel<float, 4, false>,
+      (const void*)conv_state_update_kernel<__nv_bfloat16>, (const void*)conv_state_update_kernel<float>,
+      (const void*)conv_decode_kernel<__nv_bfloat16, true>, (const void*)conv_decode_kernel<float, false>,
+      (const void*)unpack_kernel<__nv_bfloat16>, (const void*)unpack_kernel<float>,
+      (const void*)scan_kernel<__nv_bfloat16, 16, true>, (const void*)scan_kernel<__nv_bfloat16, 16, false>,
+      (const void*)scan_kernel<__nv_bfloat16, 8, true>, (const void*)scan_kernel<__nv_bfloat16, 8, false>,
+      (const void*)scan_kernel<float, 16, false>, (const void*)scan_kernel<float, 8, false>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 16, true>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true>,
+      (const void*)decode_step_kernel<float, 16, false>, (const void*)decode_step_kernel<float, 8, false>,
+      (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>,
+      (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,
+      (const void*)quantize_kernel<8>, (const void*)qar_reduce_kernel, (const void*)f32_reduce_kernel,
+      (const void*)peer_barrier_kernel};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s) {
