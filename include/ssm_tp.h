@@ -142,8 +142,10 @@ ssm_status_t ssm_workspace_bytes(ssm_tp_t tp, int32_t batch, int32_t seqlen, siz
 
 /* SSM cache of one layer on this rank:
  *   conv window [batch][K-1][E_k] in cfg.dtype (raw x values, oldest first),
- *   h           [batch][E_k][N]   fp32.
- * ssm_state_bytes reports the two sizes; ssm_state_alloc binds caller buffers of
+ *   h           [batch][E_k][N]   fp32, at the start of the h buffer, followed by a
+ *               [batch][2 E_k] fp32 decode accumulator owned by the library (kept zero
+ *               between calls; do not write it).
+ * ssm_state_bytes reports the two buffer sizes; ssm_state_alloc binds caller buffers of
  * at least those sizes and zero-fills them on `stream` (the prefill start state). */
 ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, size_t* h_bytes);
 ssm_status_t ssm_state_alloc(ssm_tp_t tp, int32_t batch, void* conv_buf, size_t conv_bytes,

@@ -62,6 +62,7 @@ struct ssm_state_s {
   int batch;
   void* conv;
   float* h;
+  float* xzacc;  // decode in_proj fp32 accumulator [batch][2 E_k], follows h in the h buffer
 };
 
 namespace {
@@ -139,14 +140,6 @@ cudaError_t gemm(ssm_tp_s* t, const void* A, int64_t lda, const void* B, int64_t
   return gemm_simt(A, lda, B, ldb, t->bf16, M, N, K, ksplit, e, s);
 }
 
-int pick_ksplit(const ssm_tp_s* t, int M, int N, int K) {
-  const int tiles = ((M + 127) / 128) * ((N + 255) / 256);
-  const int kb = (K + 63) / 64;
-  int ks = t->num_sms / (tiles > 0 ? tiles : 1);
-  if (ks > kb) ks = kb;
-  if (ks > 32) ks = 32;
-  return ks < 1 ? 1 : ks;
-}
 
 // RAII probe: records an event pair around the launches in its scope when `kind` is probed.
 struct Probe {
@@ -238,14 +231,14 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     odst = part;
   }
   const bool oacc = omode == OUT_RESID;  // out_proj accumulates into its destination
-  const int ks_x = swap ? pick_ksplit(t, hl * P, (int)M, Ek) : 1;
-  const int ks_o = swap ? pick_ksplit(t, D, (int)M, Ek) : 1;
+  const int ks_x = swap ? -1 : 1;  // decode GEMMs: stream-K over all SMs, fp32 atomic epilogue
+  const int ks_o = swap ? -1 : 1;
 
   // (a1) in_proj, column-parallel: xz = x_in W_in,r^T   [M, 2E_k]
   {
     Probe pr(t, SSM_PROBE_IN_PROJ, s);
-    if (swap)
-      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s));
+    if (swap)  // decode: accumulate into the state's zeroed fp32 buffer (stream-K, atomics)
+      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, -1, epi(EPI_ATOMIC_F32, 1, st->xzacc, 2 * Ek), s));
     else
       CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, epi(kst, 0, xz, 2 * Ek), s));
   }
@@ -257,12 +250,13 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     int64_t n0 = 0;
     float* z1 = nullptr;
     int64_t n1 = 0;
-    if (ks_x > 1) { z0 = xdst; n0 = M * hl * P; }
+    if (ks_x != 1) { z0 = xdst; n0 = M * hl * P; }
     if (swap && !oacc) { z1 = odst; n1 = nD; }
     if ((n0 & 3) && n0) { CU(cudaMemsetAsync(z0, 0, n0 * 4, s)); n0 = 0; }
     if ((n1 & 3) && n1) { CU(cudaMemsetAsync(z1, 0, n1 * 4, s)); n1 = 0; }
     t->launches++;
-    CU(launch_conv_decode(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, Ek, K, z0, n0, z1, n1, s));
+    CU(launch_conv_decode(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, Ek, K, z0, n0, z1, n1,
+                          swap ? st->xzacc : nullptr, s));
   } else {
     Probe pr(t, SSM_PROBE_CONV, s);
     t->launches += 2;
@@ -275,7 +269,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     Probe pr(t, SSM_PROBE_X_PROJ, s);
     if (swap)
       CU(gemm(t, w->w_x, Ek, u, Ek, hl * P, (int)M, Ek, ks_x,
-              epi(ks_x > 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s));
+              epi(ks_x != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s));
     else
       CU(gemm(t, u, Ek, w->w_x, Ek, (int)M, hl * P, Ek, 1, epi(EPI_STORE_F32, 0, xdst, hl * P), s));
   }
@@ -300,7 +294,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->launches++;
     CU(launch_decode_step(bf, dsrc, nsrc, doff, hl * P, c.bcdt_rmsnorm, c.rms_eps, u,
                           reinterpret_cast<char*>(xz) + Ek * es, 2 * Ek, w->w_dt, w->b_dt, w->a_log, w->d_skip, st->h,
-                          g, batch, Ek, R, N, t->cph, s));
+                          g, batch, Ek, R, N, t->cph, swap ? st->xzacc + Ek : nullptr, s));
   } else {
     // (a4) unpack dt_low / B / C; (a5) dt_proj + softplus; (a6)+(a7) scan, D skip, gate
     t->launches++;
@@ -505,7 +499,9 @@ ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, siz
   if (!tp || !conv_bytes || !h_bytes) return fail(SSM_ERR_ARG, "NULL argument");
   if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
   *conv_bytes = (size_t)batch * (tp->cfg.d_conv - 1) * tp->Ek * tp->es;
-  *h_bytes = (size_t)batch * tp->Ek * tp->cfg.d_state * 4;
+  // h [batch][E_k][N] fp32, then the decode in_proj accumulator [batch][2 E_k] fp32 (kept zero
+  // between calls: its single readers re-zero each element after use)
+  *h_bytes = (size_t)batch * tp->Ek * tp->cfg.d_state * 4 + (size_t)batch * 2 * tp->Ek * 4;
   return SSM_OK;
 }
 
@@ -527,6 +523,7 @@ ssm_status_t ssm_state_alloc(ssm_tp_t tp, int32_t batch, void* conv_buf, size_t 
   st->batch = batch;
   st->conv = conv_buf;
   st->h = reinterpret_cast<float*>(h_buf);
+  st->xzacc = st->h + (size_t)batch * tp->Ek * tp->cfg.d_state;
   cudaStream_t s_ = reinterpret_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(conv_buf, 0, cb, s_) != cudaSuccess || cudaMemsetAsync(h_buf, 0, hb, s_) != cudaSuccess) {
     delete st;
@@ -641,8 +638,8 @@ ssm_status_t ssm_dbg_gemm(ssm_tp_t tp, const void* A, const void* B, float* C, i
                           int32_t swap_ab, int32_t ksplit, void* stream) {
   if (!tp || !A || !B || !C) return fail(SSM_ERR_ARG, "NULL argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (ksplit > 1) CU(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
-  const int kind = ksplit > 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32;
+  if (ksplit != 1) CU(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
+  const int kind = ksplit != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32;
   if (swap_ab)
     CU(gemm(tp, B, K, A, K, N, M, K, ksplit, epi(kind, 1, C, N), s));
   else

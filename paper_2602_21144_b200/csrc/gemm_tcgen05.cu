@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -32,23 +33,47 @@ constexpr int SMEM_BYTES = 227 * 1024;              // ring stages are sized to 
 constexpr int RING_BYTES = SMEM_BYTES - 1024 - 512;
 // stage = A tile (128 x 64 bf16) + B tile (BN x 64 bf16); as many stages as fit (small-N decode
 // GEMMs are latency-bound weight streams and need many bytes in flight)
-__host__ __device__ inline int stage_bytes(int BN) { return A_STAGE + BN * BK * 2; }
-__host__ __device__ inline int num_stages(int BN) {
-  const int s = RING_BYTES / stage_bytes(BN);
+// A stage holds KBS consecutive 64-wide k-blocks of A and B: [KBS x A tile][KBS x B tile].
+__host__ __device__ inline int stage_bytes(int BN, int KBS) { return KBS * (A_STAGE + BN * BK * 2); }
+__host__ __device__ inline int num_stages(int BN, int KBS) {
+  const int s = RING_BYTES / stage_bytes(BN, KBS);
   return s > MAX_STAGES ? MAX_STAGES : s;
 }
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane group)
 
+// Work decomposition.  Data-parallel mode: unit u = (k-split, m-tile, n-tile), CTAs stride
+// over units.  Stream-K mode (streamk != 0): the linearised (tile, k-block) space is cut into
+// gridDim.x equal contiguous ranges, one per CTA; a range may cover the tail of one tile and
+// the head of the next, so partial tiles are combined by the atomic epilogue.
 struct TileSched {
-  int m_tiles, n_tiles, kb_total, kbs, ksplit, units;
-  __device__ void decode(int u, int& mt, int& nt, int& kb0, int& kb1) const {
-    nt = u % n_tiles;
-    int rest = u / n_tiles;
-    mt = rest % m_tiles;
-    int ks = rest / m_tiles;
-    kb0 = ks * kbs;
-    kb1 = min(kb_total, kb0 + kbs);
+  int m_tiles, n_tiles, kb_total, kbs, ksplit, units, streamk;
+  // iterate segments (mt, nt, kb0, kb1) of this CTA; returns false when done
+  __device__ bool next(int& cursor, int& mt, int& nt, int& kb0, int& kb1) const {
+    if (!streamk) {
+      const int u = cursor;
+      if (u >= units) return false;
+      cursor += gridDim.x;
+      nt = u % n_tiles;
+      const int rest = u / n_tiles;
+      mt = rest % m_tiles;
+      const int ks = rest / m_tiles;
+      kb0 = ks * kbs;
+      kb1 = min(kb_total, kb0 + kbs);
+      return true;
+    }
+    const long long W = (long long)m_tiles * n_tiles * kb_total;
+    const long long end = W * (blockIdx.x + 1) / gridDim.x;
+    long long pos = cursor < 0 ? W * blockIdx.x / gridDim.x : (long long)cursor;
+    if (pos >= end) return false;
+    const int tile = (int)(pos / kb_total);
+    kb0 = (int)(pos % kb_total);
+    kb1 = (int)min((long long)kb_total, kb0 + (end - pos));
+    nt = tile % n_tiles;
+    mt = tile / n_tiles;
+    cursor = (int)(pos + (kb1 - kb0));
+    return true;
   }
+  __device__ int first() const { return streamk ? -1 : (int)blockIdx.x; }
 };
 
 // Epilogue for one warp's 32 x 32 chunk: lane = row m0 + lane, columns n0..n0+31, stored
@@ -61,16 +86,33 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-  if (kind == EPI_SOFTPLUS_BF16) {  // bf16 output: 2-MUFU softplus (error far below bf16 rounding)
+  if (kind == EPI_SOFTPLUS_BF16 || kind == EPI_SOFTPLUS_F32) {
+    float bb[32];
+    if (e.trans) {
+      const float b0 = e.bias[m];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float x = v[j] + (e.trans ? e.bias[m] : ((n0 + j < N) ? e.bias[n0 + j] : 0.f));
-      v[j] = x > 20.f ? x : 0.6931471805599453f * __log2f(1.f + ex2_approx(x * 1.4426950408889634f));
+      for (int j = 0; j < 32; ++j) bb[j] = b0;
+    } else if (n0 + 32 <= N && ((reinterpret_cast<uintptr_t>(e.bias + n0) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // 8 broadcast 16-B loads, all issued before use
+        const float4 t4 = reinterpret_cast<const float4*>(e.bias + n0)[q];
+        bb[4 * q] = t4.x; bb[4 * q + 1] = t4.y; bb[4 * q + 2] = t4.z; bb[4 * q + 3] = t4.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bb[j] = (n0 + j < N) ? e.bias[n0 + j] : 0.f;
     }
-  } else if (kind == EPI_SOFTPLUS_F32) {
+    if (kind == EPI_SOFTPLUS_BF16) {  // bf16 output: 2-MUFU softplus (error far below bf16 rounding)
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      v[j] = softplus(v[j] + (e.trans ? e.bias[m] : ((n0 + j < N) ? e.bias[n0 + j] : 0.f)));
+      for (int j = 0; j < 32; ++j) {
+        const float x = v[j] + bb[j];
+        const float sp = 0.6931471805599453f * __log2f(1.f + ex2_approx(x * 1.4426950408889634f));
+        v[j] = x > 20.f ? x : sp;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = softplus(v[j] + bb[j]);
+    }
   }
   if (e.trans) {
     // element (m, n) -> C[n * ldc + m]; lanes hold consecutive m -> coalesced per n
@@ -155,12 +197,14 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
 
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int BN, TileSched ts, Epilogue epi) {
+                   int BN, int KBS, TileSched ts, Epilogue epi) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int STAGES = num_stages(BN);
-  const int SB = stage_bytes(BN);
-  uint8_t* ring = smem;  // stage i: A at ring + i*SB, B at ring + i*SB + A_STAGE (1024-B aligned)
+  const int STAGES = num_stages(BN, KBS);
+  const int SB = stage_bytes(BN, KBS);
+  const int BOFF = KBS * A_STAGE;  // B tiles follow the KBS A tiles (1024-B aligned)
+  const int BSUB = BN * BK * 2;
+  uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
   uint64_t* empty = full + MAX_STAGES;
   uint64_t* tfull = empty + MAX_STAGES;
@@ -179,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 8);
     }
     fence_barrier_init();
   }
@@ -194,15 +238,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer
       int stage = 0;
       uint32_t ph = 0;
-      const uint32_t tx = (uint32_t)(BM + BN) * BK * 2;
-      for (int u = blockIdx.x; u < ts.units; u += gridDim.x) {
-        int mt, nt, kb0, kb1;
-        ts.decode(u, mt, nt, kb0, kb1);
-        for (int kb = kb0; kb < kb1; ++kb) {
+      int cur = ts.first(), mt, nt, kb0, kb1;
+      while (ts.next(cur, mt, nt, kb0, kb1)) {
+        for (int kb = kb0; kb < kb1; kb += KBS) {
+          const int nk = min(KBS, kb1 - kb);
           mbar_wait(&empty[stage], ph ^ 1);
-          mbar_arrive_expect_tx(&full[stage], tx);
-          tma_load_2d(ring + stage * SB, &tmA, &full[stage], kb * BK, mt * BM);
-          tma_load_2d(ring + stage * SB + A_STAGE, &tmB, &full[stage], kb * BK, nt * BN);
+          mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * (BM + BN) * BK * 2);
+          uint8_t* st = ring + stage * SB;
+          for (int j = 0; j < nk; ++j) tma_load_2d(st + j * A_STAGE, &tmA, &full[stage], (kb + j) * BK, mt * BM);
+          for (int j = 0; j < nk; ++j) tma_load_2d(st + BOFF + j * BSUB, &tmB, &full[stage], (kb + j) * BK, nt * BN);
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
       }
@@ -215,22 +259,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t acc_ph = 0;
-      for (int u = blockIdx.x; u < ts.units; u += gridDim.x) {
-        int mt, nt, kb0, kb1;
-        ts.decode(u, mt, nt, kb0, kb1);
+      int cur = ts.first(), mt, nt, kb0, kb1;
+      while (ts.next(cur, mt, nt, kb0, kb1)) {
         if (kb0 >= kb1) continue;
         mbar_wait(&tempty[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * BN_MAX);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += KBS) {
+          const int nk = min(KBS, kb1 - kb);
           mbar_wait(&full[stage], ph);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(ring + stage * SB);
-          const uint32_t b0 = a0 + A_STAGE;
+          const uint32_t s0 = smem_u32(ring + stage * SB);
+          for (int j = 0; j < nk; ++j) {
+            const uint32_t a0 = s0 + j * A_STAGE;
+            const uint32_t b0 = s0 + BOFF + j * BSUB;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            umma_bf16(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                      (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              umma_bf16(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                        (kb > kb0 || j > 0 || k > 0) ? 1u : 0u);
+            }
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
@@ -240,19 +287,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue warps 2..5; TMEM lane group = warp % 4
+    // ---------------- epilogue warps 2..9; TMEM lane group = warp % 4, column half = (warp-2)/4
     const int eg = warp & 3;
+    const int half = (warp - 2) >> 2;
     int acc = 0;
     uint32_t acc_ph = 0;
-    for (int u = blockIdx.x; u < ts.units; u += gridDim.x) {
-      int mt, nt, kb0, kb1;
-      ts.decode(u, mt, nt, kb0, kb1);
+    int cur = ts.first(), mt, nt, kb0, kb1;
+    while (ts.next(cur, mt, nt, kb0, kb1)) {
       if (kb0 >= kb1) continue;
       mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       const int m0 = mt * BM + eg * 32;
       const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * BN_MAX);
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tbase + c * 32, r);
         tmem_ld_wait();
@@ -318,6 +365,7 @@ bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb) {
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
                          int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  const int ksplit_in = ksplit;
   // BN: multiple of 32 in [32, 256] (UMMA needs N % 16 == 0; the epilogue drains TMEM in
   // 32-column chunks) covering N in as few tiles as possible
   int n_tiles = (N + BN_MAX - 1) / BN_MAX;
@@ -333,7 +381,14 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   ts.kbs = (ts.kb_total + ksplit - 1) / ksplit;
   ts.ksplit = (ts.kb_total + ts.kbs - 1) / ts.kbs;
   ts.units = ts.m_tiles * ts.n_tiles * ts.ksplit;
-  if (ts.ksplit > 1 && epi.kind != EPI_ATOMIC_F32) return cudaErrorInvalidValue;
+  ts.streamk = 0;
+  if (ksplit_in < 0) {  // stream-K over all SMs (atomic epilogue)
+    ts.streamk = 1;
+    ts.ksplit = 1;
+    ts.kbs = ts.kb_total;
+    ts.units = ts.m_tiles * ts.n_tiles;
+  }
+  if ((ts.ksplit > 1 || ts.streamk) && epi.kind != EPI_ATOMIC_F32) return cudaErrorInvalidValue;
 
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, M, K, lda, BM)) return cudaErrorInvalidValue;
@@ -345,8 +400,17 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  // k-blocks per stage: skinny-N (weight-streaming) GEMMs fetch longer contiguous row segments
+  int kbs = BN <= 64 ? 2 : 1;
+  if (const char* env = getenv("SSM_GEMM_KBS")) kbs = atoi(env);
+  if (kbs < 1) kbs = 1;
+  while (kbs > 1 && num_stages(BN, kbs) < 2) --kbs;
   int grid = ts.units < num_sms ? ts.units : num_sms;
-  gemm_tc_kernel<<<grid, kThreads, SMEM_BYTES, s>>>(ma, mb, M, N, BN, ts, epi);
+  if (ts.streamk) {
+    const long long W = (long long)ts.units * ts.kb_total;
+    grid = (int)(W < num_sms ? W : num_sms);
+  }
+  gemm_tc_kernel<<<grid, kThreads, SMEM_BYTES, s>>>(ma, mb, M, N, BN, kbs, ts, epi);
   return cudaGetLastError();
 }
 

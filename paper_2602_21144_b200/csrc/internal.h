@@ -34,6 +34,7 @@ struct Peers {
 
 // ---- GEMM launchers (return cudaSuccess or the launch error) ----
 // tcgen05/TMEM/TMA bf16 GEMM: A [M,K] row stride lda, B [N,K] row stride ldb (elements).
+// ksplit > 1: data-parallel split-K; ksplit < 0: stream-K over all SMs (both need EPI_ATOMIC_F32).
 // Requires lda*2 % 16 == 0, ldb*2 % 16 == 0, 16-B aligned bases.
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
                          int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s);
@@ -52,7 +53,7 @@ cudaError_t launch_conv_state_update(int bf16, const void* xz, int64_t ldxz, voi
 // (split-K accumulation targets of the next GEMMs; counts multiple of 4, 16-B aligned).
 cudaError_t launch_conv_decode(int bf16, const void* xz, int64_t ldxz, void* conv_state, const float* conv_w,
                                const float* conv_b, void* u, int64_t ldu, int batch, int Ek, int K, float* zero0,
-                               int64_t nzero0, float* zero1, int64_t nzero1, cudaStream_t s);
+                               int64_t nzero0, float* zero1, int64_t nzero1, float* xacc, cudaStream_t s);
 // Sum k_src fp32 partials [M, ldp] (fixed order), optional per-field RMSNorm, split into
 // dt_low (T, [hloc][M][R]) and BC (f32, [hloc][M][2N]).
 cudaError_t launch_unpack(int bf16, Peers src, int nsrc, int64_t src_off_bytes, int M, int hloc, int R, int N,
@@ -66,7 +67,7 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
 cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
                                const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
-                               int N, int ch_per_head, cudaStream_t s);
+                               int N, int ch_per_head, float* zacc, cudaStream_t s);
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
                            cudaStream_t s);
 // int8 quantisation of n fp32 values in blocks of blk: q [n] int8, scale [n/blk] f32.

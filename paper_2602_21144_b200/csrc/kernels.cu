@@ -13,6 +13,8 @@
 //  rmsnorm                           pre-norm glue (reading Q16)
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -55,20 +57,33 @@ template <typename T>
 constexpr int vec_of() { return 16 / sizeof(T); }
 
 // ---------------------------------------------------------------- conv1d + SiLU (prefill)
-// u[b,t,d] = SiLU(conv_b[d] + sum_j conv_w[d,j] * xt[b, t-K+1+j, d]), xt = conv_state || x
+// u[b,t,d] = SiLU(conv_b[d] + sum_j conv_w[d,j] * xt[b, t-K+1+j, d]), xt = conv_state || x.
+// One thread per (b, 16-B channel group, CONV_TT consecutive tokens): conv weights held in
+// registers, all CONV_TT + K - 1 input rows loaded up front (16-B vectors, independent, in
+// flight together), then the window slides in registers.  Lanes span channels -> every warp
+// access is a contiguous 512-B row segment.
+constexpr int CONV_CG = 64, CONV_TT = 8;
 template <typename T, int K, bool FAST>
-__global__ void __launch_bounds__(64) conv1d_silu_kernel(const T* __restrict__ xz, int64_t ldxz,
-                                                         const T* __restrict__ cst, const float* __restrict__ cw,
-                                                         const float* __restrict__ cb, T* __restrict__ u,
-                                                         int64_t ldu, int L, int Ek, int TCH) {
+__global__ void __launch_bounds__(CONV_CG) conv1d_silu_kernel(const T* __restrict__ xz, int64_t ldxz,
+                                                              const T* __restrict__ cst, const float* __restrict__ cw,
+                                                              const float* __restrict__ cb, T* __restrict__ u,
+                                                              int64_t ldu, int L, int Ek) {
   constexpr int V = vec_of<T>();
-  const int cg = blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int NR = CONV_TT + K - 1;
+  const int cg = blockIdx.x * CONV_CG + threadIdx.x;
   const int d0 = cg * V;
   if (d0 >= Ek) return;
+  const int t0 = blockIdx.y * CONV_TT;
   const int b = blockIdx.z;
-  const int t0 = blockIdx.y * TCH;
-  const int t1 = min(L, t0 + TCH);
-  float w[K][V], bias[V], win[K][V];
+  uint4 raw[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const int tt = t0 - (K - 1) + i;
+    const T* src = tt < 0 ? cst + ((int64_t)b * (K - 1) + (K - 1) + tt) * Ek + d0
+                          : xz + ((int64_t)b * L + (tt < L ? tt : L - 1)) * ldxz + d0;
+    raw[i] = *reinterpret_cast<const uint4*>(src);
+  }
+  float w[K][V], bias[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     bias[v] = cb[d0 + v];
@@ -76,39 +91,30 @@ __global__ void __launch_bounds__(64) conv1d_silu_kernel(const T* __restrict__ x
     for (int j = 0; j < K; ++j) w[j][v] = cw[(d0 + v) * K + j];
   }
 #pragma unroll
-  for (int j = 0; j < K - 1; ++j) {
-    const int t = t0 - (K - 1) + j;
-    if (t >= 0)
-      Vec<T, V>::load(xz + ((int64_t)b * L + t) * ldxz + d0, win[j + 1]);
-    else
-      Vec<T, V>::load(cst + ((int64_t)b * (K - 1) + (K - 1) + t) * Ek + d0, win[j + 1]);
-  }
-  // 4 tokens per step: the 4 row loads are issued before any is consumed (latency hiding)
-  constexpr int TB = 4;
-  for (int tb = t0; tb < t1; tb += TB) {
-    float xin[TB][V];
+  for (int i = 0; i < CONV_TT; ++i) {
+    const int t = t0 + i;
+    if (t >= L) break;
+    float o[V];
 #pragma unroll
-    for (int i = 0; i < TB; ++i)
-      if (tb + i < t1) Vec<T, V>::load(xz + ((int64_t)b * L + tb + i) * ldxz + d0, xin[i]);
+    for (int v = 0; v < V; ++v) o[v] = bias[v];
 #pragma unroll
-    for (int i = 0; i < TB; ++i) {
-      if (tb + i >= t1) break;
+    for (int j = 0; j < K; ++j) {
+      float xv[V];
+      if constexpr (sizeof(T) == 2) {
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[i + j]);
 #pragma unroll
-      for (int j = 0; j < K - 1; ++j)
+        for (int q = 0; q < V / 2; ++q) { const float2 f = __bfloat1622float2(h2[q]); xv[2 * q] = f.x; xv[2 * q + 1] = f.y; }
+      } else {
+        const float* f = reinterpret_cast<const float*>(&raw[i + j]);
 #pragma unroll
-        for (int v = 0; v < V; ++v) win[j][v] = win[j + 1][v];
-#pragma unroll
-      for (int v = 0; v < V; ++v) win[K - 1][v] = xin[i][v];
-      float o[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        float acc = bias[v];
-#pragma unroll
-        for (int j = 0; j < K; ++j) acc = fmaf(w[j][v], win[j][v], acc);
-        o[v] = FAST ? silu_tanh(acc) : silu<false>(acc);
+        for (int q = 0; q < V; ++q) xv[q] = f[q];
       }
-      Vec<T, V>::store(u + ((int64_t)b * L + tb + i) * ldu + d0, o);
+#pragma unroll
+      for (int v = 0; v < V; ++v) o[v] = fmaf(w[j][v], xv[v], o[v]);
     }
+#pragma unroll
+    for (int v = 0; v < V; ++v) o[v] = FAST ? silu_tanh(o[v]) : silu<false>(o[v]);
+    Vec<T, V>::store(u + ((int64_t)b * L + t) * ldu + d0, o);
   }
 }
 
@@ -133,7 +139,7 @@ template <typename T, bool FAST>
 __global__ void conv_decode_kernel(const T* __restrict__ xz, int64_t ldxz, T* __restrict__ cst,
                                    const float* __restrict__ cw, const float* __restrict__ cb, T* __restrict__ u,
                                    int64_t ldu, int batch, int Ek, int K, float4* __restrict__ z0, int64_t n0,
-                                   float4* __restrict__ z1, int64_t n1) {
+                                   float4* __restrict__ z1, int64_t n1, float* __restrict__ xacc) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   // zero the split-K accumulation targets of the following GEMMs (x_proj, out_proj partial)
   for (int64_t i = idx; i < n0; i += (int64_t)gridDim.x * blockDim.x) z0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -142,7 +148,13 @@ __global__ void conv_decode_kernel(const T* __restrict__ xz, int64_t ldxz, T* __
   const int b = idx / Ek, d = idx % Ek;
   float win[8];
   for (int j = 0; j < K - 1; ++j) win[j] = io<T>::ld(cst + ((int64_t)b * (K - 1) + j) * Ek + d);
-  win[K - 1] = io<T>::ld(xz + (int64_t)b * ldxz + d);
+  if (xacc) {  // x from the decode in_proj fp32 accumulator; this thread is its only reader -> re-zero
+    float* p = xacc + (int64_t)b * ldxz + d;
+    win[K - 1] = *p;
+    *p = 0.f;
+  } else {
+    win[K - 1] = io<T>::ld(xz + (int64_t)b * ldxz + d);
+  }
   float acc = cb[d];
   for (int j = 0; j < K; ++j) acc = fmaf(cw[d * K + j], win[j], acc);
   io<T>::st(u + (int64_t)b * ldu + d, silu<FAST>(acc));
@@ -359,21 +371,147 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------- selective scan v3 (bf16 fast path)
+// Two channels per thread (B/C smem broadcasts and u/delta/z loads shared, bf16x2 IO) and
+// NPOLY of the N states' exponentials evaluated on the FMA pipe (exp2_poly2) so the MUFU
+// pipe (the binding unit) carries fewer ops per channel-token.
+constexpr int S3_THREADS = 128, S3_CH = 2 * S3_THREADS, S3_TT = 8;
+template <int N, int NPOLY>
+__global__ void __launch_bounds__(S3_THREADS) scan2_kernel(
+    const __nv_bfloat16* __restrict__ u, int64_t ldu, const __nv_bfloat16* __restrict__ dl, int64_t ldd,
+    const __nv_bfloat16* __restrict__ z, int64_t ldz, const float* __restrict__ BC, int64_t ldbc,
+    const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ h, int64_t h_bstride,
+    __nv_bfloat16* __restrict__ g, int64_t ldg, int L, int nch) {
+  static_assert(N % 4 == 0 && NPOLY % 2 == 0 && NPOLY <= N, "bad N/NPOLY");
+  constexpr int CH_CHUNKS = S3_CH * 2 / 16;  // 16-B chunks per staged row
+  constexpr int BC_CHUNKS = 2 * N * 4 / 16;
+  __shared__ __align__(16) __nv_bfloat16 su[2][S3_TT][S3_CH];
+  __shared__ __align__(16) __nv_bfloat16 sd[2][S3_TT][S3_CH];
+  __shared__ __align__(16) __nv_bfloat16 sz[2][S3_TT][S3_CH];
+  __shared__ __align__(16) float sbc[2][S3_TT][2 * N];
+  const int tid = threadIdx.x;
+  const int b = blockIdx.y;
+  const int cbase = blockIdx.x * S3_CH;
+  const int d = cbase + 2 * tid;  // this thread: channels d, d+1
+  const bool valid = d < nch;     // nch % 2 == 0
+  const int64_t row0 = (int64_t)b * L;
+
+  auto load_tile = [&](int buf, int tile) {
+    const int tb = tile * S3_TT;
+    for (int i = tid; i < S3_TT * CH_CHUNKS; i += S3_THREADS) {
+      const int r = i / CH_CHUNKS, c = i % CH_CHUNKS;
+      const int t = tb + r, ch = cbase + c * 8;
+      const bool ok = (t < L) && (ch < nch);
+      const int64_t row = row0 + (ok ? t : 0);
+      const int chs = ok ? ch : 0;
+      cp_async16(&su[buf][r][c * 8], u + row * ldu + chs, ok);
+      cp_async16(&sd[buf][r][c * 8], dl + row * ldd + chs, ok);
+      cp_async16(&sz[buf][r][c * 8], z + row * ldz + chs, ok);
+    }
+    for (int i = tid; i < S3_TT * BC_CHUNKS; i += S3_THREADS) {
+      const int r = i / BC_CHUNKS, c = i % BC_CHUNKS;
+      const int t = tb + r;
+      const bool ok = t < L;
+      cp_async16(&sbc[buf][r][c * 4], BC + (row0 + (ok ? t : 0)) * ldbc + c * 4, ok);
+    }
+  };
+
+  float2 A2[2][N / 2], h2[2][N / 2];
+  float Dd[2] = {0.f, 0.f};
+  float* hp = h + (int64_t)b * h_bstride + (int64_t)(valid ? d : 0) * N;
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) {
+        A2[c][i] = make_float2(-expf(a_log[(int64_t)(d + c) * N + 2 * i]) * 1.4426950408889634f,
+                               -expf(a_log[(int64_t)(d + c) * N + 2 * i + 1]) * 1.4426950408889634f);
+        h2[c][i] = make_float2(hp[c * N + 2 * i], hp[c * N + 2 * i + 1]);
+      }
+      Dd[c] = d_skip[d + c];
+    }
+  }
+
+  const int ntiles = (L + S3_TT - 1) / S3_TT;
+  load_tile(0, 0);
+  cp_async_commit();
+  for (int it = 0; it < ntiles; ++it) {
+    const int buf = it & 1;
+    if (it + 1 < ntiles) {
+      load_tile(buf ^ 1, it + 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (valid) {
+      const int tb = it * S3_TT;
+      const int tn = min(S3_TT, L - tb);
+      for (int r = 0; r < tn; ++r) {
+        const float2 uu = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&su[buf][r][2 * tid]));
+        const float2 de = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sd[buf][r][2 * tid]));
+        const float2 zz = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sz[buf][r][2 * tid]));
+        float4 Bq[N / 4], Cq[N / 4];
+#pragma unroll
+        for (int q = 0; q < N / 4; ++q) {
+          Bq[q] = reinterpret_cast<const float4*>(sbc[buf][r])[q];
+          Cq[q] = reinterpret_cast<const float4*>(sbc[buf][r] + N)[q];
+        }
+        float y[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float dec = c ? de.y : de.x;
+          const float uc = c ? uu.y : uu.x;
+          const float2 de2 = make_float2(dec, dec);
+          const float2 du2 = make_float2(dec * uc, dec * uc);
+          float2 ya = make_float2(0.f, 0.f), yb = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < N / 4; ++q) {
+            const float2 dA0 = fmul2(de2, A2[c][2 * q]);
+            const float2 dA1 = fmul2(de2, A2[c][2 * q + 1]);
+            float2 a0, a1;
+            if (4 * q + 2 <= N - NPOLY) a0 = make_float2(ex2_approx(dA0.x), ex2_approx(dA0.y));
+            else a0 = exp2_poly2(dA0);
+            if (4 * q + 4 <= N - NPOLY) a1 = make_float2(ex2_approx(dA1.x), ex2_approx(dA1.y));
+            else a1 = exp2_poly2(dA1);
+            h2[c][2 * q] = ffma2(a0, h2[c][2 * q], fmul2(du2, make_float2(Bq[q].x, Bq[q].y)));
+            h2[c][2 * q + 1] = ffma2(a1, h2[c][2 * q + 1], fmul2(du2, make_float2(Bq[q].z, Bq[q].w)));
+            ya = ffma2(make_float2(Cq[q].x, Cq[q].y), h2[c][2 * q], ya);
+            yb = ffma2(make_float2(Cq[q].z, Cq[q].w), h2[c][2 * q + 1], yb);
+          }
+          y[c] = fmaf(Dd[c], uc, (ya.x + ya.y) + (yb.x + yb.y));
+        }
+        const float g0 = y[0] * silu_tanh(zz.x), g1 = y[1] * silu_tanh(zz.y);
+        *reinterpret_cast<__nv_bfloat162*>(g + (row0 + tb + r) * ldg + d) = __floats2bfloat162_rn(g0, g1);
+      }
+    }
+    __syncthreads();
+  }
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) {
+        hp[c * N + 2 * i] = h2[c][i].x;
+        hp[c * N + 2 * i + 1] = h2[c][i].y;
+      }
+  }
+}
+
 // ---------------------------------------------------------------- decode step
 // One token per sequence: AR#1 fixed-order sum of the dbc partials (+ Falcon dt/B/C RMSNorm),
 // dt_proj + softplus, one scan step and the gate, for 32 channels x all batch rows per block;
-// h updated in place.  All global loads of a phase are issued before they are consumed
-// (decode is latency-bound: one HBM round trip per phase).
+// h updated in place.  Decode is latency-bound, so every phase issues all of its global loads
+// (16-B vectors, unrolled into registers) before consuming any of them.
 constexpr int DS_CH = 32;
-template <typename T, int N, bool FAST>
-__global__ void __launch_bounds__(256) decode_step_kernel(Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm,
-                                                          float eps, const T* __restrict__ u, const T* __restrict__ z,
-                                                          int64_t ldz, const T* __restrict__ w_dt,
-                                                          const float* __restrict__ b_dt,
-                                                          const float* __restrict__ a_log,
-                                                          const float* __restrict__ d_skip, float* __restrict__ h,
-                                                          T* __restrict__ g, int batch, int Ek, int R,
-                                                          int ch_per_head) {
+constexpr int DS_THREADS = 256;
+template <typename T, int N, bool FAST, int IPT>
+__global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
+    Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps, const T* __restrict__ u,
+    const T* __restrict__ z, int64_t ldz, const T* __restrict__ w_dt, const float* __restrict__ b_dt,
+    const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ h, T* __restrict__ g,
+    int batch, int Ek, int R, int ch_per_head, float* __restrict__ zacc) {
   extern __shared__ __align__(16) float dsm[];
   const int P = R + 2 * N;
   const int R4 = ((R + 3) & ~3) + 4;      // padded fp32 row of W_dt (16-B aligned, bank-spread)
@@ -386,53 +524,101 @@ __global__ void __launch_bounds__(256) decode_step_kernel(Peers src, int nsrc, i
   const int c0 = blockIdx.x * DS_CH;
   const int hd = c0 / ch_per_head;
 
-  // phase 1: W_dt rows, dbc rows (sum over sources), A
-  constexpr int V = 16 / sizeof(T);
-  if ((R % V) == 0) {
+  // ---- phase 1: W_dt rows (16-B vectors), dbc rows (float4, summed over sources), A
+  {
+    constexpr int V = 16 / sizeof(T);
+    constexpr int WMAX = 4;  // vectors per thread per pass
     const int cpr = R / V;
-    for (int i = tid; i < DS_CH * cpr; i += blockDim.x) {
-      const int c = i / cpr, q = i % cpr;
-      float v[V];
-      if (c0 + c < Ek) {
-        if constexpr (sizeof(T) == 2) {
-          uint4 raw = *reinterpret_cast<const uint4*>(w_dt + (int64_t)(c0 + c) * R + q * V);
-          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+    const int nw = DS_CH * cpr;
+    for (int base = 0; base < nw; base += WMAX * DS_THREADS) {
+      uint4 raw[WMAX];
 #pragma unroll
-          for (int k = 0; k < V / 2; ++k) { float2 f = __bfloat1622float2(b2[k]); v[2 * k] = f.x; v[2 * k + 1] = f.y; }
-        } else {
-          float4 f = *reinterpret_cast<const float4*>(w_dt + (int64_t)(c0 + c) * R + q * V);
-          v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < V; ++k) v[k] = 0.f;
+      for (int k = 0; k < WMAX; ++k) {
+        const int i = base + tid + k * DS_THREADS;
+        const int c = i / cpr, q = i % cpr;
+        raw[k] = (i < nw && c0 + c < Ek) ? *reinterpret_cast<const uint4*>(w_dt + (int64_t)(c0 + c) * R + q * V)
+                                         : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int k = 0; k < V; ++k) sW[c * R4 + q * V + k] = v[k];
+      for (int k = 0; k < WMAX; ++k) {
+        const int i = base + tid + k * DS_THREADS;
+        if (i >= nw) break;
+        const int c = i / cpr, q = i % cpr;
+        float* dst = sW + c * R4 + q * V;
+        if constexpr (sizeof(T) == 2) {
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) { const float2 f = __bfloat1622float2(b2[j]); dst[2 * j] = f.x; dst[2 * j + 1] = f.y; }
+        } else {
+          const float* f = reinterpret_cast<const float*>(&raw[k]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dst[j] = f[j];
+        }
+      }
     }
-  } else {
-    for (int i = tid; i < DS_CH * R; i += blockDim.x) {
-      const int c = i / R, r = i % R;
-      sW[c * R4 + r] = (c0 + c < Ek) ? io<T>::ld(w_dt + (int64_t)(c0 + c) * R + r) : 0.f;
+    // dbc: batch rows of P floats at column hd*P of a [batch][ldp] fp32 buffer (P % 4 == 0)
+    const int p4 = P / 4;
+    const int nd = batch * p4;
+    constexpr int DMAX = 4;
+    for (int base = 0; base < nd; base += DMAX * DS_THREADS) {
+      float4 acc[DMAX];
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r = 0; r < nsrc; ++r) {  // fixed rank order (reading Q12)
+        const float* sp = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[r]) + src_off);
+        float4 ld[DMAX];
+#pragma unroll
+        for (int k = 0; k < DMAX; ++k) {
+          const int i = base + tid + k * DS_THREADS;
+          const int b = i / p4, q = i % p4;
+          ld[k] = i < nd ? *reinterpret_cast<const float4*>(sp + (int64_t)b * ldp + (int64_t)hd * P + 4 * q)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < DMAX; ++k) {
+          acc[k].x += ld[k].x; acc[k].y += ld[k].y; acc[k].z += ld[k].z; acc[k].w += ld[k].w;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) {
+        const int i = base + tid + k * DS_THREADS;
+        if (i < nd) *reinterpret_cast<float4*>(sD + (i / p4) * P4 + 4 * (i % p4)) = acc[k];
+      }
+    }
+    for (int i = tid; i < DS_CH * N; i += DS_THREADS) {
+      const int c = i / N, n = i % N;
+      const float a = (c0 + c < Ek) ? -expf(a_log[(int64_t)(c0 + c) * N + n]) : 0.f;
+      sA[i] = FAST ? a * 1.4426950408889634f : a;
     }
   }
-  for (int i = tid; i < batch * P; i += blockDim.x) {
-    const int b = i / P, c = i % P;
-    const int64_t idx = (int64_t)b * ldp + (int64_t)hd * P + c;
-    float acc = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[0]) + src_off)[idx];
-    for (int r = 1; r < nsrc; ++r)  // fixed rank order (reading Q12)
-      acc += reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[r]) + src_off)[idx];
-    sD[b * P4 + c] = acc;
-  }
-  for (int i = tid; i < DS_CH * N; i += blockDim.x) {
-    const int c = i / N, n = i % N;
-    const float a = (c0 + c < Ek) ? -expf(a_log[(int64_t)(c0 + c) * N + n]) : 0.f;
-    sA[i] = FAST ? a * 1.4426950408889634f : a;
+  // ---- phase 2 loads (independent of phase 1): h rows, u, z, biases for this thread's items
+  float hs[IPT][N];
+  float uu[IPT], zz[IPT], bias[IPT], Dd[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int it = tid + k * DS_THREADS;
+    const int b = it / DS_CH, d = c0 + it % DS_CH;
+    const bool ok = b < batch && d < Ek;
+    const float* hp = h + ((int64_t)(ok ? b : 0) * Ek + (ok ? d : 0)) * N;
+#pragma unroll
+    for (int n = 0; n < N; n += 4) {
+      const float4 t4 = ok ? *reinterpret_cast<const float4*>(hp + n) : make_float4(0.f, 0.f, 0.f, 0.f);
+      hs[k][n] = t4.x; hs[k][n + 1] = t4.y; hs[k][n + 2] = t4.z; hs[k][n + 3] = t4.w;
+    }
+    uu[k] = ok ? io<T>::ld(u + (int64_t)b * Ek + d) : 0.f;
+    if (zacc) {  // z from the decode in_proj fp32 accumulator; only reader -> re-zero after use
+      zz[k] = ok ? zacc[(int64_t)b * ldz + d] : 0.f;
+      if (ok) zacc[(int64_t)b * ldz + d] = 0.f;
+    } else {
+      zz[k] = ok ? io<T>::ld(z + (int64_t)b * ldz + d) : 0.f;
+    }
+    bias[k] = ok ? b_dt[d] : 0.f;
+    Dd[k] = ok ? d_skip[d] : 0.f;
   }
   __syncthreads();
   if (rmsnorm) {  // weightless RMSNorm of dt_low, B, C per batch row (Falcon-Mamba, reading Q18)
     const int warp = tid >> 5, lane = tid & 31;
-    for (int b = warp; b < batch; b += blockDim.x >> 5) {
+    for (int b = warp; b < batch; b += DS_THREADS / 32) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f;
       for (int c = lane; c < P; c += 32) {
         const float v = sD[b * P4 + c];
@@ -441,31 +627,27 @@ __global__ void __launch_bounds__(256) decode_step_kernel(Peers src, int nsrc, i
         else s2 = fmaf(v, v, s2);
       }
 #pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        float x = f == 0 ? s0 : (f == 1 ? s1 : s2);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (lane == 0) sS[b * 3 + f] = 1.0f / sqrtf(x / (float)(f == 0 ? R : N) + eps);
+      for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (lane == 0) {
+        sS[b * 3 + 0] = 1.0f / sqrtf(s0 / (float)R + eps);
+        sS[b * 3 + 1] = 1.0f / sqrtf(s1 / (float)N + eps);
+        sS[b * 3 + 2] = 1.0f / sqrtf(s2 / (float)N + eps);
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
 
-  // phase 2: items (b, c), warp = fixed b, lane = channel
-  for (int it = tid; it < batch * DS_CH; it += blockDim.x) {
+  // ---- phase 2 compute: items (b, c), warp = fixed b, lane = channel
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int it = tid + k * DS_THREADS;
     const int b = it / DS_CH, c = it % DS_CH;
     const int d = c0 + c;
-    if (d >= Ek) continue;
-    float* hp = h + ((int64_t)b * Ek + d) * N;
-    float hs[N];
-#pragma unroll
-    for (int n = 0; n < N; n += 4) {
-      const float4 t4 = *reinterpret_cast<const float4*>(hp + n);
-      hs[n] = t4.x; hs[n + 1] = t4.y; hs[n + 2] = t4.z; hs[n + 3] = t4.w;
-    }
-    const float uu = io<T>::ld(u + (int64_t)b * Ek + d);
-    const float zz = io<T>::ld(z + (int64_t)b * ldz + d);
-    const float bias = b_dt[d], Dd = d_skip[d];
+    if (b >= batch || d >= Ek) continue;
     const float* wr = sW + c * R4;
     const float* xr = sD + b * P4;
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
@@ -478,8 +660,8 @@ __global__ void __launch_bounds__(256) decode_step_kernel(Peers src, int nsrc, i
     for (int r = R4e; r < R; ++r) s0 = fmaf(xr[r], wr[r], s0);
     float dt = (s0 + s1) + (s2 + s3);
     if (rmsnorm) dt *= sS[b * 3 + 0];
-    const float de = softplus(dt + bias);
-    const float du = de * uu;
+    const float de = softplus(dt + bias[k]);
+    const float du = de * uu[k];
     const float sB = rmsnorm ? sS[b * 3 + 1] : 1.f;
     const float sC = rmsnorm ? sS[b * 3 + 2] : 1.f;
     const float* Bt = xr + R;
@@ -489,13 +671,15 @@ __global__ void __launch_bounds__(256) decode_step_kernel(Peers src, int nsrc, i
 #pragma unroll
     for (int n = 0; n < N; ++n) {
       const float ab = FAST ? ex2_approx(de * Ac[n]) : expf(de * Ac[n]);
-      hs[n] = fmaf(ab, hs[n], du * (Bt[n] * sB));
-      y = fmaf(Ct[n] * sC, hs[n], y);
+      hs[k][n] = fmaf(ab, hs[k][n], du * (Bt[n] * sB));
+      y = fmaf(Ct[n] * sC, hs[k][n], y);
     }
+    float* hp = h + ((int64_t)b * Ek + d) * N;
 #pragma unroll
-    for (int n = 0; n < N; n += 4) *reinterpret_cast<float4*>(hp + n) = make_float4(hs[n], hs[n + 1], hs[n + 2], hs[n + 3]);
-    y = fmaf(Dd, uu, y);
-    io<T>::st(g + (int64_t)b * Ek + d, y * silu<FAST>(zz));
+    for (int n = 0; n < N; n += 4)
+      *reinterpret_cast<float4*>(hp + n) = make_float4(hs[k][n], hs[k][n + 1], hs[k][n + 2], hs[k][n + 3]);
+    y = fmaf(Dd[k], uu[k], y);
+    io<T>::st(g + (int64_t)b * Ek + d, y * silu<FAST>(zz[k]));
   }
 }
 
@@ -650,21 +834,26 @@ template <typename T, bool F>
 cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const float* cw, const float* cb, void* u,
                           int64_t ldu, int batch, int L, int Ek, int K, cudaStream_t s) {
   constexpr int V = vec_of<T>();
-  const int TCH = 16;
-  dim3 grid((Ek / V + 63) / 64, (L + TCH - 1) / TCH, batch);
+  dim3 grid((Ek / V + CONV_CG - 1) / CONV_CG, (L + CONV_TT - 1) / CONV_TT, batch);
   const T* x = reinterpret_cast<const T*>(xz);
   const T* c = reinterpret_cast<const T*>(cs);
   T* uu = reinterpret_cast<T*>(u);
+  constexpr int NT = CONV_CG;
   switch (K) {
-    case 2: conv1d_silu_kernel<T, 2, F><<<grid, 64, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek, TCH); break;
-    case 3: conv1d_silu_kernel<T, 3, F><<<grid, 64, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek, TCH); break;
-    case 4: conv1d_silu_kernel<T, 4, F><<<grid, 64, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek, TCH); break;
+    case 2: conv1d_silu_kernel<T, 2, F><<<grid, NT, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek); break;
+    case 3: conv1d_silu_kernel<T, 3, F><<<grid, NT, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek); break;
+    case 4: conv1d_silu_kernel<T, 4, F><<<grid, NT, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
 
 }  // namespace
+
+// scan variant knobs (SSM_SCAN_VERSION=1 selects the 1-channel kernel; SSM_SCAN_NPOLY = states per
+// channel on the FMA-pipe exp2), read once per process
+static int g_scan_version = [] { const char* e = getenv("SSM_SCAN_VERSION"); return e ? atoi(e) : 2; }();
+static int g_scan_npoly = [] { const char* e = getenv("SSM_SCAN_NPOLY"); return e ? atoi(e) : 4; }();
 
 // ==================================================================== launchers
 cudaError_t launch_conv1d_silu(int bf16, const void* xz, int64_t ldxz, const void* cs, const float* cw,
@@ -690,7 +879,7 @@ cudaError_t launch_conv_state_update(int bf16, const void* xz, int64_t ldxz, voi
 
 cudaError_t launch_conv_decode(int bf16, const void* xz, int64_t ldxz, void* cs, const float* cw, const float* cb,
                                void* u, int64_t ldu, int batch, int Ek, int K, float* zero0, int64_t nzero0,
-                               float* zero1, int64_t nzero1, cudaStream_t s) {
+                               float* zero1, int64_t nzero1, float* xacc, cudaStream_t s) {
   const int n = batch * Ek;
   if (n <= 0) return cudaSuccess;
   if ((nzero0 | nzero1) & 3) return cudaErrorInvalidValue;
@@ -699,11 +888,11 @@ cudaError_t launch_conv_decode(int bf16, const void* xz, int64_t ldxz, void* cs,
   if (bf16)
     conv_decode_kernel<__nv_bfloat16, true><<<(n + 255) / 256, 256, 0, s>>>(
         reinterpret_cast<const __nv_bfloat16*>(xz), ldxz, reinterpret_cast<__nv_bfloat16*>(cs), cw, cb,
-        reinterpret_cast<__nv_bfloat16*>(u), ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4);
+        reinterpret_cast<__nv_bfloat16*>(u), ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4, xacc);
   else
     conv_decode_kernel<float, false><<<(n + 255) / 256, 256, 0, s>>>(
         reinterpret_cast<const float*>(xz), ldxz, reinterpret_cast<float*>(cs), cw, cb, reinterpret_cast<float*>(u),
-        ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4);
+        ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4, xacc);
   return cudaGetLastError();
 }
 
@@ -738,6 +927,18 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
                         int64_t hbs, void* g, int64_t ldg, int batch, int L, int nch, int N, cudaStream_t s) {
   if (batch <= 0 || L <= 0 || nch <= 0) return cudaSuccess;
   if (N != 16 && N != 8) return cudaErrorInvalidValue;
+  if (bf16 && fast && N == 16 && nch % 2 == 0 && ldg % 2 == 0 && g_scan_version >= 2) {
+    dim3 grid((nch + S3_CH - 1) / S3_CH, batch);
+    const int npoly = g_scan_npoly;
+#define S2A reinterpret_cast<const __nv_bfloat16*>(u), ldu, reinterpret_cast<const __nv_bfloat16*>(dl), ldd, \
+      reinterpret_cast<const __nv_bfloat16*>(z), ldz, BC, ldbc, a_log, d_skip, h, hbs, reinterpret_cast<__nv_bfloat16*>(g), ldg, L, nch
+    if (npoly == 0) scan2_kernel<16, 0><<<grid, S3_THREADS, 0, s>>>(S2A);
+    else if (npoly == 2) scan2_kernel<16, 2><<<grid, S3_THREADS, 0, s>>>(S2A);
+    else if (npoly == 4) scan2_kernel<16, 4><<<grid, S3_THREADS, 0, s>>>(S2A);
+    else scan2_kernel<16, 6><<<grid, S3_THREADS, 0, s>>>(S2A);
+#undef S2A
+    return cudaGetLastError();
+  }
   if (bf16) {
     if (N == 16) return fast ? scan_t<__nv_bfloat16, 16, true>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s)
                              : scan_t<__nv_bfloat16, 16, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
@@ -754,35 +955,52 @@ static size_t dstep_smem(int batch, int R, int N) {
   return (size_t)(DS_CH * R4 + batch * P4 + DS_CH * N + batch * 3) * sizeof(float);
 }
 
-template <typename T, int N, bool F>
+template <typename T, int N, bool F, int IPT>
 static cudaError_t dstep_t(Peers src, int nsrc, int64_t off, int ldp, int rms, float eps, const void* u, const void* z,
                            int64_t ldz, const void* w_dt, const float* b_dt, const float* a_log, const float* d_skip,
-                           float* h, void* g, int batch, int Ek, int R, int cph, cudaStream_t s) {
+                           float* h, void* g, int batch, int Ek, int R, int cph, float* zacc, cudaStream_t s) {
   const size_t smem = dstep_smem(batch, R, N);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_step_kernel<T, N, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_step_kernel<T, N, F, IPT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  decode_step_kernel<T, N, F><<<(Ek + DS_CH - 1) / DS_CH, 256, smem, s>>>(
+  decode_step_kernel<T, N, F, IPT><<<(Ek + DS_CH - 1) / DS_CH, DS_THREADS, smem, s>>>(
       src, nsrc, off, ldp, rms, eps, reinterpret_cast<const T*>(u), reinterpret_cast<const T*>(z), ldz,
-      reinterpret_cast<const T*>(w_dt), b_dt, a_log, d_skip, h, reinterpret_cast<T*>(g), batch, Ek, R, cph);
+      reinterpret_cast<const T*>(w_dt), b_dt, a_log, d_skip, h, reinterpret_cast<T*>(g), batch, Ek, R, cph, zacc);
   return cudaGetLastError();
+}
+
+template <typename T, int N, bool F>
+static cudaError_t dstep_ipt(int batch, Peers src, int nsrc, int64_t off, int ldp, int rms, float eps, const void* u,
+                             const void* z, int64_t ldz, const void* w_dt, const float* b_dt, const float* a_log,
+                             const float* d_skip, float* h, void* g, int Ek, int R, int cph, float* zacc,
+                             cudaStream_t s) {
+  const int ipt = (batch * DS_CH + DS_THREADS - 1) / DS_THREADS;
+#define DSA src, nsrc, off, ldp, rms, eps, u, z, ldz, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, cph, zacc, s
+  if (ipt <= 1) return dstep_t<T, N, F, 1>(DSA);
+  if (ipt <= 2) return dstep_t<T, N, F, 2>(DSA);
+  if (ipt <= 4) return dstep_t<T, N, F, 4>(DSA);
+  if (ipt <= 8) return dstep_t<T, N, F, 8>(DSA);
+#undef DSA
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
                                const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
-                               int N, int ch_per_head, cudaStream_t s) {
+                               int N, int ch_per_head, float* zacc, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   if (ch_per_head % DS_CH != 0) return cudaErrorInvalidValue;
-  if (dstep_smem(batch, R, N) > 200 * 1024) return cudaErrorInvalidValue;
+  if (dstep_smem(batch, R, N) > 200 * 1024 || batch > 64) return cudaErrorInvalidValue;
   if (N != 16 && N != 8) return cudaErrorInvalidValue;
-#define DS_ARGS src, nsrc, src_off, ldp, rmsnorm, eps, u, z, ldz, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, s
-  if (bf16) return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(DS_ARGS) : dstep_t<__nv_bfloat16, 8, true>(DS_ARGS);
-  return N == 16 ? dstep_t<float, 16, false>(DS_ARGS) : dstep_t<float, 8, false>(DS_ARGS);
+  const int es = bf16 ? 2 : 4;
+  if ((R * es) % 16 || (R + 2 * N) % 4 || ldp % 4) return cudaErrorInvalidValue;
+#define DS_ARGS batch, src, nsrc, src_off, ldp, rmsnorm, eps, u, z, ldz, w_dt, b_dt, a_log, d_skip, h, g, Ek, R, ch_per_head, zacc, s
+  if (bf16) return N == 16 ? dstep_ipt<__nv_bfloat16, 16, true>(DS_ARGS) : dstep_ipt<__nv_bfloat16, 8, true>(DS_ARGS);
+  return N == 16 ? dstep_ipt<float, 16, false>(DS_ARGS) : dstep_ipt<float, 8, false>(DS_ARGS);
 #undef DS_ARGS
 }
 
@@ -841,8 +1059,16 @@ cudaError_t preload_kernels() {
       (const void*)scan_kernel<__nv_bfloat16, 16, true>, (const void*)scan_kernel<__nv_bfloat16, 16, false>,
       (const void*)scan_kernel<__nv_bfloat16, 8, true>, (const void*)scan_kernel<__nv_bfloat16, 8, false>,
       (const void*)scan_kernel<float, 16, false>, (const void*)scan_kernel<float, 8, false>,
-      (const void*)decode_step_kernel<__nv_bfloat16, 16, true>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true>,
-      (const void*)decode_step_kernel<float, 16, false>, (const void*)decode_step_kernel<float, 8, false>,
+      (const void*)scan2_kernel<16, 0>, (const void*)scan2_kernel<16, 2>, (const void*)scan2_kernel<16, 4>,
+      (const void*)scan2_kernel<16, 6>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 1>, (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 2>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 4>, (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 8>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 1>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 2>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 4>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 8>,
+      (const void*)decode_step_kernel<float, 16, false, 1>, (const void*)decode_step_kernel<float, 16, false, 2>,
+      (const void*)decode_step_kernel<float, 16, false, 4>, (const void*)decode_step_kernel<float, 16, false, 8>,
+      (const void*)decode_step_kernel<float, 8, false, 1>, (const void*)decode_step_kernel<float, 8, false, 2>,
+      (const void*)decode_step_kernel<float, 8, false, 4>, (const void*)decode_step_kernel<float, 8, false, 8>,
       (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>,
       (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,
       (const void*)quantize_kernel<8>, (const void*)qar_reduce_kernel, (const void*)f32_reduce_kernel,

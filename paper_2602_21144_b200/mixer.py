@@ -84,9 +84,11 @@ class State:
         dt = torch.bfloat16 if mixer.dtype == "bf16" else torch.float32
         ek, K, N = mixer.ek, mixer.dims.d_conv, mixer.dims.d_state
         self.conv = torch.empty((batch, K - 1, ek), dtype=dt, device=mixer.device)
-        self.h = torch.empty((batch, ek, N), dtype=torch.float32, device=mixer.device)
+        # h [batch][E_k][N] fp32 followed by the library's decode accumulator (same buffer)
+        self._hbuf = torch.empty(hb.value // 4, dtype=torch.float32, device=mixer.device)
+        self.h = self._hbuf[:batch * ek * N].view(batch, ek, N)
         self.handle = C.c_void_p()
-        L.call("ssm_state_alloc", mixer.handle, batch, _ptr(self.conv), cb.value, _ptr(self.h), hb.value,
+        L.call("ssm_state_alloc", mixer.handle, batch, _ptr(self.conv), cb.value, _ptr(self._hbuf), hb.value,
                _stream(stream), C.byref(self.handle))
         self.batch = batch
 

@@ -39,9 +39,14 @@ def synthetic_layer(dims, layer, seed=1000, device="cuda"):
 
 
 class MixerStack:
+    """flags: SSM_AR2_INT8 / SSM_AR2_FP32 (the library's peer-to-peer AR#2), or SSM_AR2_EXTERNAL
+    with nccl_group set: the NCCL bf16 all-reduce BASELINE arm (library writes the rank's fp32
+    partial, torch.distributed all-reduces it in bf16, torch adds it to the residual)."""
+
     def __init__(self, mixer: TPMixer, layers: list, batch: int, max_chunk: int, flags=L.SSM_AR2_INT8,
-                 norm_eps=1e-5):
+                 norm_eps=1e-5, nccl_group=None):
         self.mx, self.layers, self.batch, self.flags, self.eps = mixer, layers, batch, flags, norm_eps
+        self.nccl = nccl_group if flags == L.SSM_AR2_EXTERNAL else None
         d = mixer.dims
         dt = torch.bfloat16 if mixer.dtype == "bf16" else torch.float32
         self.ws = mixer.workspace(batch, max_chunk)
@@ -49,6 +54,8 @@ class MixerStack:
         self.xbuf = torch.empty((batch * max_chunk, d.d_model), dtype=dt, device=mixer.device)
         self.xbuf_dec = torch.empty((batch, d.d_model), dtype=dt, device=mixer.device)
         self.states = [State(mixer, batch) for _ in layers]
+        if self.nccl is not None:
+            self.part = torch.empty((batch * max_chunk, d.d_model), dtype=torch.float32, device=mixer.device)
         self.graph = None
         self.graph_launches = 0
 
@@ -62,13 +69,28 @@ class MixerStack:
         x = self.xbuf[:n]
         for lw, st in zip(self.layers, self.states):
             self.mx.rmsnorm(res, x, None, self.eps, stream)
-            self.mx.prefill(lw, st, x, res, self.flags, self.ws, stream)
+            if self.nccl is None:
+                self.mx.prefill(lw, st, x, res, self.flags, self.ws, stream)
+            else:
+                self._nccl_layer(lambda p: self.mx.prefill(lw, st, x, p, self.flags, self.ws, stream), res)
 
     def decode_step(self, res_t, stream=None):
         """res_t: [batch, D] fp32, updated in place through all layers."""
         for lw, st in zip(self.layers, self.states):
             self.mx.rmsnorm(res_t, self.xbuf_dec, None, self.eps, stream)
-            self.mx.decode(lw, st, self.xbuf_dec, res_t, self.flags, self.ws_dec, stream)
+            if self.nccl is None:
+                self.mx.decode(lw, st, self.xbuf_dec, res_t, self.flags, self.ws_dec, stream)
+            else:
+                self._nccl_layer(lambda p: self.mx.decode(lw, st, self.xbuf_dec, p, self.flags, self.ws_dec, stream),
+                                 res_t)
+
+    def _nccl_layer(self, run, res):
+        import torch.distributed as dist
+        p = self.part[:res.shape[0]]
+        run(p)                                   # p := this rank's fp32 partial out_proj
+        pb = p.to(torch.bfloat16)
+        dist.all_reduce(pb, group=self.nccl)     # NCCL bf16 all-reduce (baseline arm)
+        res.add_(pb.float())
 
     def capture_decode(self, res_t):
         """Capture one decode step over all layers into a CUDA graph reading/writing res_t.

@@ -10,7 +10,9 @@ full) ARGS="--layers 2 --prompt 2048 --decode 8 --steps 1 --warmup 1 --no-e2e --
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv1d_silu -s 0 -c 1 -o gpurun_out/conv_$TAG python bench.py $ARGS > /dev/null 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_step -s 2 -c 1 -o gpurun_out/dstep_$TAG python bench.py $ARGS > /dev/null 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 8 -c 1 -o gpurun_out/dtproj_$TAG python bench.py $ARGS > /dev/null 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 0 -c 1 -o gpurun_out/scan_$TAG python bench.py $ARGS > /dev/null 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 0 -c 1 -o gpurun_out/decinproj_$TAG python bench.py $ARGS > /dev/null 2>&1
   ls gpurun_out/*$TAG* ;;
+micro) timeout 600 python scripts/gemm_micro.py > gpurun_out/micro_$TAG.txt 2>&1; cat gpurun_out/micro_$TAG.txt ;;
+scanmicro) for v in "1 4" "2 0" "2 2" "2 4" "2 6"; do set -- $v; SSM_SCAN_VERSION=$1 SSM_SCAN_NPOLY=$2 timeout 120 python scripts/scan_micro.py; done > gpurun_out/scanmicro_$TAG.txt 2>&1; cat gpurun_out/scanmicro_$TAG.txt ;;
 esac
 done

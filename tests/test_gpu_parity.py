@@ -20,7 +20,8 @@ MED = synth.MixerDims(d_model=256, d_inner=512, d_state=16, d_conv=4, dt_rank=16
 # ------------------------------------------------------------------ GEMM
 @pytest.mark.parametrize("M,N,K,swap,ks", [(300, 200, 320, 0, 1), (384, 512, 2560, 0, 1), (1000, 192, 640, 0, 1),
                                            (16, 10240 // 8, 2560, 1, 1), (16, 192, 5120, 1, 8), (32, 2560, 640, 1, 4),
-                                           (5, 48, 64, 0, 1)])
+                                           (5, 48, 64, 0, 1), (16, 10240, 2560, 1, -1), (16, 192, 5120, 1, -1),
+                                           (32, 2560, 5120, 1, -1), (300, 200, 640, 0, -1)])
 def test_gemm_tcgen05_bf16(M, N, K, swap, ks):
     dims = synth.MixerDims(d_model=64, d_inner=128, dt_rank=4)
     mx = TPMixer(dims, "bf16")
@@ -76,6 +77,9 @@ def test_scan_kernel_vs_oracle(dtype, L_):
     gref = y * M.silu(z.numpy())
     assert rel(gout.float().cpu().view(B, L_, E), gref) < TOL[dtype]
     assert rel(h.cpu(), hL) < TOL[dtype]
+    # the state is fp32 and the inputs are exactly the oracle's, so only the exp2 (MUFU ex2 or the
+    # FMA-pipe polynomial, both ~2.4e-7 relative) and fp32 rounding separate h from the oracle
+    assert rel(h.cpu(), hL) < 1e-4
 
 
 # ------------------------------------------------------------------ full mixer, TP=1
