@@ -142,9 +142,7 @@ ssm_status_t ssm_workspace_bytes(ssm_tp_t tp, int32_t batch, int32_t seqlen, siz
 
 /* SSM cache of one layer on this rank:
  *   conv window [batch][K-1][E_k] in cfg.dtype (raw x values, oldest first),
- *   h           [batch][E_k][N]   fp32, at the start of the h buffer, followed by a
- *               [batch][2 E_k] fp32 decode accumulator owned by the library (kept zero
- *               between calls; do not write it).
+ *   h           [batch][E_k][N]   fp32.
  * ssm_state_bytes reports the two buffer sizes; ssm_state_alloc binds caller buffers of
  * at least those sizes and zero-fills them on `stream` (the prefill start state). */
 ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, size_t* h_bytes);
@@ -210,6 +208,9 @@ ssm_status_t ssm_tp_probe_read(ssm_tp_t tp, float* ms, int32_t capacity, int32_t
  * by the projections (tcgen05 for bf16 when K*2 % 16 == 0, SIMT otherwise). */
 ssm_status_t ssm_dbg_gemm(ssm_tp_t tp, const void* A, const void* B, float* C,
                           int32_t M, int32_t N, int32_t K, int32_t swap_ab, int32_t ksplit, void* stream);
+/* Same with explicit row strides (elements) of A and B. */
+ssm_status_t ssm_dbg_gemm_ld(ssm_tp_t tp, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int32_t M,
+                             int32_t N, int32_t K, int32_t swap_ab, int32_t ksplit, void* stream);
 /* Selective scan + D skip + gate on prepared inputs (u, delta, z bf16/fp32 [batch*L, E_k],
  * z row stride ldz; BC fp32 [batch*L, 2N]); h [batch][E_k][N] fp32 in/out; g out. */
 ssm_status_t ssm_dbg_scan(ssm_tp_t tp, const void* u, const void* delta, const void* z, int32_t ldz,

@@ -5,6 +5,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -14,6 +15,10 @@
 #include "internal.h"
 
 using namespace ssm;
+
+namespace ssm {
+thread_local bool t_launch_pdl = false;
+}
 
 namespace {
 
@@ -36,6 +41,19 @@ ssm_status_t fail(ssm_status_t code, const char* fmt, ...) {
   } while (0)
 
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Programmatic dependent launch for the decode path (SSM_PDL=0 disables).
+// Debug-only ablation knob (timing experiments): SSM_DEBUG_SKIP bitmask of decode kernels to
+// skip (1 in_proj, 2 conv, 4 x_proj, 8 decode_step, 16 out_proj).  Results are wrong when set.
+const int g_dbg_skip = [] { const char* e = getenv("SSM_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
+
+// Off by default: measured slightly slower on the Mamba-2.8B decode step (SSM_PDL=1 enables).
+const bool g_pdl_enabled = [] { const char* e = getenv("SSM_PDL"); return e && atoi(e) != 0; }();
+struct PdlScope {
+  bool prev;
+  explicit PdlScope(bool on) : prev(ssm::t_launch_pdl) { ssm::t_launch_pdl = on; }
+  ~PdlScope() { ssm::t_launch_pdl = prev; }
+};
 
 constexpr size_t kSigBytes = 256;  // signal slots [0,32) B, error word at +64 B, epoch counter at +128 B
 
@@ -62,7 +80,6 @@ struct ssm_state_s {
   int batch;
   void* conv;
   float* h;
-  float* xzacc;  // decode in_proj fp32 accumulator [batch][2 E_k], follows h in the h buffer
 };
 
 namespace {
@@ -132,11 +149,11 @@ ssm_status_t validate_cfg(const ssm_config_t* c, int k) {
 }
 
 cudaError_t gemm(ssm_tp_s* t, const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
-                 int ksplit, const Epilogue& e, cudaStream_t s) {
+                 int ksplit, const Epilogue& e, cudaStream_t s, bool a_is_weight = false) {
   t->launches++;
   if (t->bf16 && gemm_tc_supported(A, lda, B, ldb))
     return gemm_tc_bf16(reinterpret_cast<const __nv_bfloat16*>(A), lda, reinterpret_cast<const __nv_bfloat16*>(B),
-                        ldb, M, N, K, ksplit, e, t->num_sms, s);
+                        ldb, M, N, K, ksplit, e, t->num_sms, s, a_is_weight && t_launch_pdl);
   return gemm_simt(A, lda, B, ldb, t->bf16, M, N, K, ksplit, e, s);
 }
 
@@ -157,6 +174,17 @@ struct Probe {
     if (idx >= 0) cudaEventRecord(t->probe_ev[2 * idx + 1], s);
   }
 };
+
+// split-K factor for a swap-AB decode GEMM with `rows` weight rows and reduction length K:
+// enough units to cover ~half the SMs, at least 4 k-blocks per unit
+int split_for(const ssm_tp_s* t, int rows, int K) {
+  const int tiles = (rows + 127) / 128;
+  const int kb = (K + 63) / 64;
+  int ks = t->num_sms / tiles;
+  if (ks > kb) ks = kb;
+  if (ks > 32) ks = 32;
+  return ks < 1 ? 1 : ks;
+}
 
 Epilogue epi(int kind, int trans, void* C, int64_t ldc, const float* bias = nullptr) {
   Epilogue e;
@@ -231,20 +259,23 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     odst = part;
   }
   const bool oacc = omode == OUT_RESID;  // out_proj accumulates into its destination
-  const int ks_x = swap ? -1 : 1;  // decode GEMMs: stream-K over all SMs, fp32 atomic epilogue
-  const int ks_o = swap ? -1 : 1;
+  // decode GEMMs (swap-AB): split-K with the fp32 atomic epilogue so the few weight-row tiles
+  // spread over the SMs (measured best: ~1 unit per SM, <= 32 splits)
+  const int ks_x = swap ? split_for(t, hl * P, Ek) : 1;
+  const int ks_o = swap ? split_for(t, D, Ek) : 1;
 
   // (a1) in_proj, column-parallel: xz = x_in W_in,r^T   [M, 2E_k]
-  {
+  const int skip = decode ? g_dbg_skip : 0;
+  if (!(skip & 1)) {
     Probe pr(t, SSM_PROBE_IN_PROJ, s);
-    if (swap)  // decode: accumulate into the state's zeroed fp32 buffer (stream-K, atomics)
-      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, -1, epi(EPI_ATOMIC_F32, 1, st->xzacc, 2 * Ek), s));
+    if (swap)
+      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s, true));
     else
       CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, epi(kst, 0, xz, 2 * Ek), s));
   }
 
   // (a2) conv1d + SiLU, rank-local; conv window of the cache updated
-  if (decode) {
+  if (decode && !(skip & 2)) {
     // split-K targets of x_proj / out_proj are zeroed by the conv kernel (one launch fewer)
     float* z0 = nullptr;
     int64_t n0 = 0;
@@ -254,10 +285,11 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     if (swap && !oacc) { z1 = odst; n1 = nD; }
     if ((n0 & 3) && n0) { CU(cudaMemsetAsync(z0, 0, n0 * 4, s)); n0 = 0; }
     if ((n1 & 3) && n1) { CU(cudaMemsetAsync(z1, 0, n1 * 4, s)); n1 = 0; }
+    Probe pr(t, SSM_PROBE_CONV, s);
     t->launches++;
     CU(launch_conv_decode(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, Ek, K, z0, n0, z1, n1,
-                          swap ? st->xzacc : nullptr, s));
-  } else {
+                          nullptr, s));
+  } else if (!decode) {
     Probe pr(t, SSM_PROBE_CONV, s);
     t->launches += 2;
     CU(launch_conv1d_silu(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, seqlen, Ek, K, s));
@@ -265,11 +297,11 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   }
 
   // (a3) x_proj partial [M, hloc*P] fp32, straight into the symmetric buffer when AR#1 follows
-  {
+  if (!(skip & 4)) {
     Probe pr(t, SSM_PROBE_X_PROJ, s);
     if (swap)
       CU(gemm(t, w->w_x, Ek, u, Ek, hl * P, (int)M, Ek, ks_x,
-              epi(ks_x != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s));
+              epi(ks_x != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s, true));
     else
       CU(gemm(t, u, Ek, w->w_x, Ek, (int)M, hl * P, Ek, 1, epi(EPI_STORE_F32, 0, xdst, hl * P), s));
   }
@@ -289,12 +321,14 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   }
 
   if (decode) {
+    if (!(skip & 8)) {
     // (a4)-(a7) decode: AR#1 sum + unpack + dt_proj + softplus + scan step + gate, one kernel
     Probe pr(t, SSM_PROBE_DECODE_STEP, s);
     t->launches++;
     CU(launch_decode_step(bf, dsrc, nsrc, doff, hl * P, c.bcdt_rmsnorm, c.rms_eps, u,
                           reinterpret_cast<char*>(xz) + Ek * es, 2 * Ek, w->w_dt, w->b_dt, w->a_log, w->d_skip, st->h,
-                          g, batch, Ek, R, N, t->cph, swap ? st->xzacc + Ek : nullptr, s));
+                          g, batch, Ek, R, N, t->cph, nullptr, s));
+    }
   } else {
     // (a4) unpack dt_low / B / C; (a5) dt_proj + softplus; (a6)+(a7) scan, D skip, gate
     t->launches++;
@@ -320,10 +354,10 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   }
 
   // (a8) out_proj, row-parallel partial (TP=1: added straight into the fp32 residual)
-  {
+  if (!(skip & 16)) {
     Probe pr(t, SSM_PROBE_OUT_PROJ, s);
     if (swap)
-      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, epi(EPI_ATOMIC_F32, 1, odst, D), s));
+      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, epi(EPI_ATOMIC_F32, 1, odst, D), s, true));
     else
       CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D), s));
   }
@@ -499,9 +533,7 @@ ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, siz
   if (!tp || !conv_bytes || !h_bytes) return fail(SSM_ERR_ARG, "NULL argument");
   if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
   *conv_bytes = (size_t)batch * (tp->cfg.d_conv - 1) * tp->Ek * tp->es;
-  // h [batch][E_k][N] fp32, then the decode in_proj accumulator [batch][2 E_k] fp32 (kept zero
-  // between calls: its single readers re-zero each element after use)
-  *h_bytes = (size_t)batch * tp->Ek * tp->cfg.d_state * 4 + (size_t)batch * 2 * tp->Ek * 4;
+  *h_bytes = (size_t)batch * tp->Ek * tp->cfg.d_state * 4;
   return SSM_OK;
 }
 
@@ -523,7 +555,6 @@ ssm_status_t ssm_state_alloc(ssm_tp_t tp, int32_t batch, void* conv_buf, size_t 
   st->batch = batch;
   st->conv = conv_buf;
   st->h = reinterpret_cast<float*>(h_buf);
-  st->xzacc = st->h + (size_t)batch * tp->Ek * tp->cfg.d_state;
   cudaStream_t s_ = reinterpret_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(conv_buf, 0, cb, s_) != cudaSuccess || cudaMemsetAsync(h_buf, 0, hb, s_) != cudaSuccess) {
     delete st;
@@ -564,6 +595,7 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
   ssm_status_t s = check_call(tp, w, st, x_in, residual, batch, 1, flags, workspace, ws_bytes);
   if (s != SSM_OK) return s;
   if (batch == 0) return SSM_OK;
+  PdlScope pdl(g_pdl_enabled);
   return run_layer(tp, w, st, x_in, residual, batch, 1, flags, workspace, true,
                    reinterpret_cast<cudaStream_t>(stream));
 }
@@ -602,6 +634,7 @@ ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_
 
 ssm_status_t ssm_rmsnorm(ssm_tp_t tp, const float* residual, const float* weight, float eps, void* x_out, int64_t M,
                          void* stream) {
+  PdlScope pdl(g_pdl_enabled && M <= 256);  // decode-sized rows: overlap with the neighbours
   if (!tp || !residual || !x_out) return fail(SSM_ERR_ARG, "NULL argument");
   if ((reinterpret_cast<uintptr_t>(residual) | reinterpret_cast<uintptr_t>(weight) | reinterpret_cast<uintptr_t>(x_out)) & 15)
     return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
@@ -636,14 +669,19 @@ ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches) {
 
 ssm_status_t ssm_dbg_gemm(ssm_tp_t tp, const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
                           int32_t swap_ab, int32_t ksplit, void* stream) {
+  return ssm_dbg_gemm_ld(tp, A, K, B, K, C, M, N, K, swap_ab, ksplit, stream);
+}
+
+ssm_status_t ssm_dbg_gemm_ld(ssm_tp_t tp, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int32_t M,
+                             int32_t N, int32_t K, int32_t swap_ab, int32_t ksplit, void* stream) {
   if (!tp || !A || !B || !C) return fail(SSM_ERR_ARG, "NULL argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (ksplit != 1) CU(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
   const int kind = ksplit != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32;
   if (swap_ab)
-    CU(gemm(tp, B, K, A, K, N, M, K, ksplit, epi(kind, 1, C, N), s));
+    CU(gemm(tp, B, ldb, A, lda, N, M, K, ksplit, epi(kind, 1, C, N), s, true));
   else
-    CU(gemm(tp, A, K, B, K, M, N, K, ksplit, epi(kind, 0, C, N), s));
+    CU(gemm(tp, A, lda, B, ldb, M, N, K, ksplit, epi(kind, 0, C, N), s));
   return SSM_OK;
 }
 

@@ -200,6 +200,17 @@ __host__ __device__ inline uint32_t umma_idesc_bf16(int M, int N) {
          | ((uint32_t)(M >> 4) << 24);   // M >> 4
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// griddepcontrol.wait: block until the predecessor grid completed (no-op when the kernel was not
+// launched with programmatic stream serialization).  launch_dependents: let the successor grid
+// start its independent prologue now.
+SSM_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SSM_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Bulk L2 prefetch of a contiguous global range (16-B aligned, size multiple of 16).
+SSM_DEV void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // ------------------------------------------------------------------ system-scope flags (P2P AR)
 SSM_DEV void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -214,6 +225,26 @@ SSM_DEV uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// ------------------------------------------------------------------ launch helper
+// Launches with the programmatic-stream-serialization attribute when launch_pdl() is set (the
+// decode path: successive small kernels overlap their prologues with the predecessor's tail).
+extern thread_local bool t_launch_pdl;
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = t_launch_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 }  // namespace ssm

@@ -34,6 +34,8 @@ __device__ __forceinline__ void epi_one(const Epilogue& e, int m, int n, float v
 template <typename T>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ A, int64_t lda, const T* __restrict__ B,
                                                         int64_t ldb, int M, int N, int K, int kper, Epilogue epi) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sA[TK][TM + 4];
   __shared__ float sB[TK][TN + 4];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -94,12 +96,12 @@ cudaError_t gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, in
   if (nz > 1 && epi.kind != EPI_ATOMIC_F32) return cudaErrorInvalidValue;
   dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM, nz);
   if (dtype_bf16)
-    gemm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(A), lda,
+    { cudaError_t e_ = launch(gemm_simt_kernel<__nv_bfloat16>, grid, 256, 0, s, reinterpret_cast<const __nv_bfloat16*>(A), lda,
                                                          reinterpret_cast<const __nv_bfloat16*>(B), ldb, M, N, K,
-                                                         kper, epi);
+                                                         kper, epi); if (e_ != cudaSuccess) return e_; }
   else
-    gemm_simt_kernel<float><<<grid, 256, 0, s>>>(reinterpret_cast<const float*>(A), lda,
-                                                 reinterpret_cast<const float*>(B), ldb, M, N, K, kper, epi);
+    { cudaError_t e_ = launch(gemm_simt_kernel<float>, grid, 256, 0, s, reinterpret_cast<const float*>(A), lda,
+                                                 reinterpret_cast<const float*>(B), ldb, M, N, K, kper, epi); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 

@@ -35,10 +35,18 @@ constexpr int RING_BYTES = SMEM_BYTES - 1024 - 512;
 // GEMMs are latency-bound weight streams and need many bytes in flight)
 // A stage holds KBS consecutive 64-wide k-blocks of A and B: [KBS x A tile][KBS x B tile].
 __host__ __device__ inline int stage_bytes(int BN, int KBS) { return KBS * (A_STAGE + BN * BK * 2); }
-__host__ __device__ inline int num_stages(int BN, int KBS) {
-  const int s = RING_BYTES / stage_bytes(BN, KBS);
+__host__ __device__ inline int num_stages(int BN, int KBS, int ring = RING_BYTES) {
+  const int s = ring / stage_bytes(BN, KBS);
   return s > MAX_STAGES ? MAX_STAGES : s;
 }
+// Per-launch shape of the CTA's resources: smem ring size and TMEM accumulator columns (two
+// accumulators of acc_stride columns).  Smaller values let two CTAs share an SM.
+struct CtaRes {
+  int ring;          // bytes of the stage ring
+  int tmem_cols;     // power of two >= 32
+  int acc_stride;    // columns per accumulator
+  int nomma;         // experiment knob: skip the MMAs (TMA pipeline only)
+};
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane group)
 
 // Work decomposition.  Data-parallel mode: unit u = (k-split, m-tile, n-tile), CTAs stride
@@ -197,15 +205,16 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
 
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int BN, int KBS, TileSched ts, Epilogue epi) {
+                   int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_pf, int64_t lda, int K,
+                   CtaRes cr) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int STAGES = num_stages(BN, KBS);
+  const int STAGES = num_stages(BN, KBS, cr.ring);
   const int SB = stage_bytes(BN, KBS);
   const int BOFF = KBS * A_STAGE;  // B tiles follow the KBS A tiles (1024-B aligned)
   const int BSUB = BN * BK * 2;
   uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + cr.ring);
   uint64_t* empty = full + MAX_STAGES;
   uint64_t* tfull = empty + MAX_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -213,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -227,13 +237,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, cr.tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
+    // A is the weight operand (swap-AB decode): stream this CTA's whole A range into L2 as long
+    // contiguous row segments (DRAM-friendly) while the predecessor kernel finishes
+    if (a_pf) {
+      int cur = ts.first(), mt, nt, kb0, kb1;
+      while (ts.next(cur, mt, nt, kb0, kb1)) {
+        const int c0 = kb0 * BK;
+        const int c1 = min(K, kb1 * BK);
+        if (c1 <= c0) continue;
+        for (int r = mt * BM + lane; r < min(M, mt * BM + BM); r += 32)
+          prefetch_l2(a_pf + (int64_t)r * lda + c0, (uint32_t)(c1 - c0) * 2);
+      }
+    }
+    pdl_wait();
     if (lane == 0) {
       // ---------------- TMA producer
       int stage = 0;
@@ -252,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
+    pdl_wait();
     if (lane == 0) {
       // ---------------- MMA issuer (single thread)
       const uint32_t idesc = umma_idesc_bf16(BM, BN);
@@ -264,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (kb0 >= kb1) continue;
         mbar_wait(&tempty[acc], acc_ph ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + (uint32_t)(acc * BN_MAX);
+        const uint32_t d = tmem_base + (uint32_t)(acc * cr.acc_stride);
         for (int kb = kb0; kb < kb1; kb += KBS) {
           const int nk = min(KBS, kb1 - kb);
           mbar_wait(&full[stage], ph);
@@ -273,10 +297,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < nk; ++j) {
             const uint32_t a0 = s0 + j * A_STAGE;
             const uint32_t b0 = s0 + BOFF + j * BSUB;
+            if (!cr.nomma) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              umma_bf16(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                        (kb > kb0 || j > 0 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < BK / 16; ++k) {
+                umma_bf16(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                          (kb > kb0 || j > 0 || k > 0) ? 1u : 0u);
+              }
             }
           }
           umma_commit(&empty[stage]);
@@ -288,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- epilogue warps 2..9; TMEM lane group = warp % 4, column half = (warp-2)/4
+    pdl_wait();
     const int eg = warp & 3;
     const int half = (warp - 2) >> 2;
     int acc = 0;
@@ -298,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       const int m0 = mt * BM + eg * 32;
-      const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * BN_MAX);
+      const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * cr.acc_stride);
       for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tbase + c * 32, r);
@@ -315,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    tmem_dealloc(tmem_base, cr.tmem_cols);
   }
 }
 
@@ -363,7 +390,7 @@ bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb) {
 }
 
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
-                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s) {
+                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool prefetch_a) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   const int ksplit_in = ksplit;
   // BN: multiple of 32 in [32, 256] (UMMA needs N % 16 == 0; the epilogue drains TMEM in
@@ -404,13 +431,30 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   int kbs = BN <= 64 ? 2 : 1;
   if (const char* env = getenv("SSM_GEMM_KBS")) kbs = atoi(env);
   if (kbs < 1) kbs = 1;
-  while (kbs > 1 && num_stages(BN, kbs) < 2) --kbs;
+  CtaRes cr;
+  cr.ring = RING_BYTES;
+  cr.acc_stride = BN_MAX;
+  cr.tmem_cols = 512;
+  cr.nomma = 0;
+  if (const char* env = getenv("SSM_GEMM_NOMMA")) cr.nomma = atoi(env);
+  if (const char* env = getenv("SSM_GEMM_RING_KB")) {  // experiment: smaller CTA footprint
+    cr.ring = atoi(env) * 1024;
+    int cols = 32;
+    while (cols < 2 * BN) cols *= 2;
+    cr.tmem_cols = cols;
+    cr.acc_stride = cols / 2;
+  }
+  while (kbs > 1 && num_stages(BN, kbs, cr.ring) < 2) --kbs;
+  const int smem_bytes = 1024 + cr.ring + 512;
   int grid = ts.units < num_sms ? ts.units : num_sms;
   if (ts.streamk) {
+    long long cap = num_sms;
+    if (const char* env = getenv("SSM_GEMM_SK_CTAS")) cap = atoi(env);
     const long long W = (long long)ts.units * ts.kb_total;
-    grid = (int)(W < num_sms ? W : num_sms);
+    grid = (int)(W < cap ? W : cap);
   }
-  gemm_tc_kernel<<<grid, kThreads, SMEM_BYTES, s>>>(ma, mb, M, N, BN, kbs, ts, epi);
+  { cudaError_t e_ = launch(gemm_tc_kernel, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi,
+                                      prefetch_a && ((lda * 2) % 16 == 0) && (K % 8 == 0) ? A : nullptr, lda, K, cr); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 

@@ -36,8 +36,10 @@ struct Peers {
 // tcgen05/TMEM/TMA bf16 GEMM: A [M,K] row stride lda, B [N,K] row stride ldb (elements).
 // ksplit > 1: data-parallel split-K; ksplit < 0: stream-K over all SMs (both need EPI_ATOMIC_F32).
 // Requires lda*2 % 16 == 0, ldb*2 % 16 == 0, 16-B aligned bases.
+// prefetch_a: A is a weight (independent of the predecessor kernel): bulk-prefetch each CTA's A
+// rows into L2 before griddepcontrol.wait.
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
-                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s);
+                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool prefetch_a = false);
 bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb);
 // SIMT GEMM, fp32 accumulation, T = float or bf16 inputs.
 cudaError_t gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, int dtype_bf16, int M, int N, int K,

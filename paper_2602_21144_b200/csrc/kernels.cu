@@ -58,63 +58,68 @@ constexpr int vec_of() { return 16 / sizeof(T); }
 
 // ---------------------------------------------------------------- conv1d + SiLU (prefill)
 // u[b,t,d] = SiLU(conv_b[d] + sum_j conv_w[d,j] * xt[b, t-K+1+j, d]), xt = conv_state || x.
-// One thread per (b, 16-B channel group, CONV_TT consecutive tokens): conv weights held in
-// registers, all CONV_TT + K - 1 input rows loaded up front (16-B vectors, independent, in
-// flight together), then the window slides in registers.  Lanes span channels -> every warp
-// access is a contiguous 512-B row segment.
-constexpr int CONV_CG = 64, CONV_TT = 8;
+// One thread per (b, 16-B channel group, CONV_TCH consecutive tokens): conv weights and the
+// K-1 window in registers, rows prefetched CONV_PF tokens ahead (software pipelining).  A
+// block spans CONV_CG channel groups = a 4-KB contiguous segment of each row (bf16).
+constexpr int CONV_CG = 256, CONV_TCH = 16, CONV_PF = 2;
 template <typename T, int K, bool FAST>
 __global__ void __launch_bounds__(CONV_CG) conv1d_silu_kernel(const T* __restrict__ xz, int64_t ldxz,
                                                               const T* __restrict__ cst, const float* __restrict__ cw,
                                                               const float* __restrict__ cb, T* __restrict__ u,
                                                               int64_t ldu, int L, int Ek) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int V = vec_of<T>();
-  constexpr int NR = CONV_TT + K - 1;
   const int cg = blockIdx.x * CONV_CG + threadIdx.x;
   const int d0 = cg * V;
   if (d0 >= Ek) return;
-  const int t0 = blockIdx.y * CONV_TT;
+  const int t0 = blockIdx.y * CONV_TCH;
+  const int t1 = min(L, t0 + CONV_TCH);
   const int b = blockIdx.z;
-  uint4 raw[NR];
+  auto row = [&](int t) -> const T* {
+    return t < 0 ? cst + ((int64_t)b * (K - 1) + (K - 1) + t) * Ek + d0 : xz + ((int64_t)b * L + t) * ldxz + d0;
+  };
+  uint4 pf[CONV_PF];
 #pragma unroll
-  for (int i = 0; i < NR; ++i) {
-    const int tt = t0 - (K - 1) + i;
-    const T* src = tt < 0 ? cst + ((int64_t)b * (K - 1) + (K - 1) + tt) * Ek + d0
-                          : xz + ((int64_t)b * L + (tt < L ? tt : L - 1)) * ldxz + d0;
-    raw[i] = *reinterpret_cast<const uint4*>(src);
-  }
-  float w[K][V], bias[V];
+  for (int i = 0; i < CONV_PF; ++i) pf[i] = (t0 + i < t1) ? *reinterpret_cast<const uint4*>(row(t0 + i)) : make_uint4(0, 0, 0, 0);
+  float w[K][V], bias[V], win[K][V];
+#pragma unroll
+  for (int j = 0; j < K - 1; ++j) Vec<T, V>::load(row(t0 - (K - 1) + j), win[j + 1]);
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     bias[v] = cb[d0 + v];
 #pragma unroll
     for (int j = 0; j < K; ++j) w[j][v] = cw[(d0 + v) * K + j];
   }
+  for (int t = t0; t < t1; t += CONV_PF) {
 #pragma unroll
-  for (int i = 0; i < CONV_TT; ++i) {
-    const int t = t0 + i;
-    if (t >= L) break;
-    float o[V];
+    for (int i = 0; i < CONV_PF; ++i) {
+      if (t + i >= t1) break;
+      const uint4 cur = pf[i];
+      if (t + i + CONV_PF < t1) pf[i] = *reinterpret_cast<const uint4*>(row(t + i + CONV_PF));  // prefetch
 #pragma unroll
-    for (int v = 0; v < V; ++v) o[v] = bias[v];
+      for (int j = 0; j < K - 1; ++j)
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      float xv[V];
+        for (int v = 0; v < V; ++v) win[j][v] = win[j + 1][v];
       if constexpr (sizeof(T) == 2) {
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[i + j]);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&cur);
 #pragma unroll
-        for (int q = 0; q < V / 2; ++q) { const float2 f = __bfloat1622float2(h2[q]); xv[2 * q] = f.x; xv[2 * q + 1] = f.y; }
+        for (int q = 0; q < V / 2; ++q) { const float2 f = __bfloat1622float2(h2[q]); win[K - 1][2 * q] = f.x; win[K - 1][2 * q + 1] = f.y; }
       } else {
-        const float* f = reinterpret_cast<const float*>(&raw[i + j]);
+        const float* f = reinterpret_cast<const float*>(&cur);
 #pragma unroll
-        for (int q = 0; q < V; ++q) xv[q] = f[q];
+        for (int q = 0; q < V; ++q) win[K - 1][q] = f[q];
       }
+      float o[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) o[v] = fmaf(w[j][v], xv[v], o[v]);
+      for (int v = 0; v < V; ++v) {
+        float acc = bias[v];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = fmaf(w[j][v], win[j][v], acc);
+        o[v] = FAST ? silu_tanh(acc) : silu<false>(acc);
+      }
+      Vec<T, V>::store(u + ((int64_t)b * L + t + i) * ldu + d0, o);
     }
-#pragma unroll
-    for (int v = 0; v < V; ++v) o[v] = FAST ? silu_tanh(o[v]) : silu<false>(o[v]);
-    Vec<T, V>::store(u + ((int64_t)b * L + t) * ldu + d0, o);
   }
 }
 
@@ -122,6 +127,8 @@ __global__ void __launch_bounds__(CONV_CG) conv1d_silu_kernel(const T* __restric
 template <typename T>
 __global__ void conv_state_update_kernel(const T* __restrict__ xz, int64_t ldxz, T* __restrict__ cst, int batch,
                                          int L, int Ek, int K) {
+  pdl_trigger();
+  pdl_wait();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= batch * Ek) return;
   const int b = idx / Ek, d = idx % Ek;
@@ -140,6 +147,8 @@ __global__ void conv_decode_kernel(const T* __restrict__ xz, int64_t ldxz, T* __
                                    const float* __restrict__ cw, const float* __restrict__ cb, T* __restrict__ u,
                                    int64_t ldu, int batch, int Ek, int K, float4* __restrict__ z0, int64_t n0,
                                    float4* __restrict__ z1, int64_t n1, float* __restrict__ xacc) {
+  pdl_trigger();
+  pdl_wait();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   // zero the split-K accumulation targets of the following GEMMs (x_proj, out_proj partial)
   for (int64_t i = idx; i < n0; i += (int64_t)gridDim.x * blockDim.x) z0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -167,6 +176,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) unpack_kernel(Peers src, int nsrc, int64_t off, int M, int hloc, int R, int N,
                                                      int rmsnorm, float eps, T* __restrict__ dlow,
                                                      float* __restrict__ BC) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= M * hloc) return;
@@ -239,6 +250,8 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
                                                           const float* __restrict__ d_skip, float* __restrict__ h,
                                                           int64_t h_bstride, T* __restrict__ g, int64_t ldg, int L,
                                                           int nch) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int V = vec_of<T>();
   constexpr int SC_TT = sizeof(T) == 2 ? 16 : 8;  // tokens per staged tile (static smem < 48 KB)
   constexpr int CH_CHUNKS = SC_THREADS / V;  // 16-B chunks per channel row
@@ -382,6 +395,8 @@ __global__ void __launch_bounds__(S3_THREADS) scan2_kernel(
     const __nv_bfloat16* __restrict__ z, int64_t ldz, const float* __restrict__ BC, int64_t ldbc,
     const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ h, int64_t h_bstride,
     __nv_bfloat16* __restrict__ g, int64_t ldg, int L, int nch) {
+  pdl_trigger();
+  pdl_wait();
   static_assert(N % 4 == 0 && NPOLY % 2 == 0 && NPOLY <= N, "bad N/NPOLY");
   constexpr int CH_CHUNKS = S3_CH * 2 / 16;  // 16-B chunks per staged row
   constexpr int BC_CHUNKS = 2 * N * 4 / 16;
@@ -501,12 +516,14 @@ __global__ void __launch_bounds__(S3_THREADS) scan2_kernel(
 
 // ---------------------------------------------------------------- decode step
 // One token per sequence: AR#1 fixed-order sum of the dbc partials (+ Falcon dt/B/C RMSNorm),
-// dt_proj + softplus, one scan step and the gate, for 32 channels x all batch rows per block;
-// h updated in place.  Decode is latency-bound, so every phase issues all of its global loads
-// (16-B vectors, unrolled into registers) before consuming any of them.
+// dt_proj + softplus, one scan step and the gate; h updated in place.  A block owns DS_CH
+// channels x DS_BB batch rows (one item per thread), so the grid has many small blocks that all
+// co-reside (no wave tail).  Decode is latency-bound: every global load of the kernel is issued
+// before any is consumed.
 constexpr int DS_CH = 32;
-constexpr int DS_THREADS = 256;
-template <typename T, int N, bool FAST, int IPT>
+constexpr int DS_BB = 4;
+constexpr int DS_THREADS = DS_CH * DS_BB;
+template <typename T, int N, bool FAST>
 __global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
     Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps, const T* __restrict__ u,
     const T* __restrict__ z, int64_t ldz, const T* __restrict__ w_dt, const float* __restrict__ b_dt,
@@ -517,111 +534,130 @@ __global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
   const int R4 = ((R + 3) & ~3) + 4;      // padded fp32 row of W_dt (16-B aligned, bank-spread)
   const int P4 = (P + 3) & ~3;
   float* sW = dsm;                        // [DS_CH][R4]
-  float* sD = sW + DS_CH * R4;            // [batch][P4]  summed dbc rows of this block's head
-  float* sA = sD + batch * P4;            // [DS_CH][N]   A (log2e-scaled in FAST mode)
-  float* sS = sA + DS_CH * N;             // [batch][3]   RMSNorm scales
+  float* sD = sW + DS_CH * R4;            // [DS_BB][P4]  summed dbc rows of this block's head
+  float* sA = sD + DS_BB * P4;            // [DS_CH][N]   A (log2e-scaled in FAST mode)
+  float* sS = sA + DS_CH * N;             // [DS_BB][3]   RMSNorm scales
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * DS_CH;
+  const int b0 = blockIdx.y * DS_BB;
   const int hd = c0 / ch_per_head;
+  const int nb = min(DS_BB, batch - b0);
+  pdl_trigger();
 
-  // ---- phase 1: W_dt rows (16-B vectors), dbc rows (float4, summed over sources), A
-  {
-    constexpr int V = 16 / sizeof(T);
-    constexpr int WMAX = 4;  // vectors per thread per pass
-    const int cpr = R / V;
-    const int nw = DS_CH * cpr;
-    for (int base = 0; base < nw; base += WMAX * DS_THREADS) {
-      uint4 raw[WMAX];
+  // ---- weights first (independent of the predecessor kernels): W_dt rows, a_log
+  constexpr int V = 16 / sizeof(T);
+  constexpr int WMAX = 8;  // W_dt 16-B vectors per thread (32 rows x R <= 256 bf16)
+  constexpr int AMAX = (DS_CH * N + DS_THREADS - 1) / DS_THREADS;
+  const int cpr = R / V;
+  const int nw = DS_CH * cpr;
+  uint4 wraw[WMAX];
 #pragma unroll
-      for (int k = 0; k < WMAX; ++k) {
-        const int i = base + tid + k * DS_THREADS;
-        const int c = i / cpr, q = i % cpr;
-        raw[k] = (i < nw && c0 + c < Ek) ? *reinterpret_cast<const uint4*>(w_dt + (int64_t)(c0 + c) * R + q * V)
-                                         : make_uint4(0, 0, 0, 0);
-      }
+  for (int k = 0; k < WMAX; ++k) {
+    const int i = tid + k * DS_THREADS;
+    const int c = i / cpr, q = i % cpr;
+    wraw[k] = (i < nw && c0 + c < Ek) ? *reinterpret_cast<const uint4*>(w_dt + (int64_t)(c0 + c) * R + q * V)
+                                      : make_uint4(0, 0, 0, 0);
+  }
+  float al[AMAX];
 #pragma unroll
-      for (int k = 0; k < WMAX; ++k) {
-        const int i = base + tid + k * DS_THREADS;
-        if (i >= nw) break;
-        const int c = i / cpr, q = i % cpr;
-        float* dst = sW + c * R4 + q * V;
-        if constexpr (sizeof(T) == 2) {
-          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
+  for (int k = 0; k < AMAX; ++k) {
+    const int i = tid + k * DS_THREADS;
+    const int c = i / N, n = i % N;
+    al[k] = (i < DS_CH * N && c0 + c < Ek) ? a_log[(int64_t)(c0 + c) * N + n] : 0.f;
+  }
+  const int cc = tid % DS_CH, bl = tid / DS_CH;
+  const int d = c0 + cc, b = b0 + bl;
+  const bool ok = bl < nb && d < Ek;
+  const float bias = ok ? b_dt[d] : 0.f;
+  const float Dd = ok ? d_skip[d] : 0.f;
+  pdl_wait();  // everything below reads what the predecessor kernels produced
+  // ---- activations: dbc rows (first source), this thread's h row, u, z
+  const int p4 = P / 4;
+  const int nd = nb * p4;
+  constexpr int DMAX = 4;
+  float4 acc[DMAX];
+  const float* sp0 = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[0]) + src_off);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) { const float2 f = __bfloat1622float2(b2[j]); dst[2 * j] = f.x; dst[2 * j + 1] = f.y; }
-        } else {
-          const float* f = reinterpret_cast<const float*>(&raw[k]);
+  for (int k = 0; k < DMAX; ++k) {
+    const int i = tid + k * DS_THREADS;
+    acc[k] = i < nd ? *reinterpret_cast<const float4*>(sp0 + (int64_t)(b0 + i / p4) * ldp + (int64_t)hd * P + 4 * (i % p4))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float hs[N];
+  float* hp = h + ((int64_t)(ok ? b : 0) * Ek + (ok ? d : 0)) * N;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dst[j] = f[j];
-        }
-      }
+  for (int n = 0; n < N; n += 4) {
+    const float4 t4 = ok ? *reinterpret_cast<const float4*>(hp + n) : make_float4(0.f, 0.f, 0.f, 0.f);
+    hs[n] = t4.x; hs[n + 1] = t4.y; hs[n + 2] = t4.z; hs[n + 3] = t4.w;
+  }
+  const float uu = ok ? io<T>::ld(u + (int64_t)b * Ek + d) : 0.f;
+  float zz = 0.f;
+  if (zacc) {
+    if (ok) { zz = zacc[(int64_t)b * ldz + d]; zacc[(int64_t)b * ldz + d] = 0.f; }
+  } else if (ok) {
+    zz = io<T>::ld(z + (int64_t)b * ldz + d);
+  }
+  // ---- consume into shared memory
+#pragma unroll
+  for (int k = 0; k < WMAX; ++k) {
+    const int i = tid + k * DS_THREADS;
+    if (i >= nw) break;
+    const int c = i / cpr, q = i % cpr;
+    float* dst = sW + c * R4 + q * V;
+    if constexpr (sizeof(T) == 2) {
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&wraw[k]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { const float2 f = __bfloat1622float2(b2[j]); dst[2 * j] = f.x; dst[2 * j + 1] = f.y; }
+    } else {
+      const float* f = reinterpret_cast<const float*>(&wraw[k]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[j] = f[j];
     }
-    // dbc: batch rows of P floats at column hd*P of a [batch][ldp] fp32 buffer (P % 4 == 0)
-    const int p4 = P / 4;
-    const int nd = batch * p4;
-    constexpr int DMAX = 4;
-    for (int base = 0; base < nd; base += DMAX * DS_THREADS) {
-      float4 acc[DMAX];
-#pragma unroll
-      for (int k = 0; k < DMAX; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int r = 0; r < nsrc; ++r) {  // fixed rank order (reading Q12)
-        const float* sp = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[r]) + src_off);
-        float4 ld[DMAX];
-#pragma unroll
-        for (int k = 0; k < DMAX; ++k) {
-          const int i = base + tid + k * DS_THREADS;
-          const int b = i / p4, q = i % p4;
-          ld[k] = i < nd ? *reinterpret_cast<const float4*>(sp + (int64_t)b * ldp + (int64_t)hd * P + 4 * q)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int k = 0; k < DMAX; ++k) {
-          acc[k].x += ld[k].x; acc[k].y += ld[k].y; acc[k].z += ld[k].z; acc[k].w += ld[k].w;
-        }
-      }
+  }
+  for (int base = 0; base < nd; base += DMAX * DS_THREADS) {
+    if (base > 0) {
 #pragma unroll
       for (int k = 0; k < DMAX; ++k) {
         const int i = base + tid + k * DS_THREADS;
-        if (i < nd) *reinterpret_cast<float4*>(sD + (i / p4) * P4 + 4 * (i % p4)) = acc[k];
+        acc[k] = i < nd ? *reinterpret_cast<const float4*>(sp0 + (int64_t)(b0 + i / p4) * ldp + (int64_t)hd * P + 4 * (i % p4))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
-    for (int i = tid; i < DS_CH * N; i += DS_THREADS) {
-      const int c = i / N, n = i % N;
-      const float a = (c0 + c < Ek) ? -expf(a_log[(int64_t)(c0 + c) * N + n]) : 0.f;
-      sA[i] = FAST ? a * 1.4426950408889634f : a;
+    for (int r = 1; r < nsrc; ++r) {  // fixed rank order (reading Q12)
+      const float* sp = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[r]) + src_off);
+      float4 ld[DMAX];
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) {
+        const int i = base + tid + k * DS_THREADS;
+        ld[k] = i < nd ? *reinterpret_cast<const float4*>(sp + (int64_t)(b0 + i / p4) * ldp + (int64_t)hd * P + 4 * (i % p4))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) {
+        acc[k].x += ld[k].x; acc[k].y += ld[k].y; acc[k].z += ld[k].z; acc[k].w += ld[k].w;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < DMAX; ++k) {
+      const int i = base + tid + k * DS_THREADS;
+      if (i < nd) *reinterpret_cast<float4*>(sD + (i / p4) * P4 + 4 * (i % p4)) = acc[k];
     }
   }
-  // ---- phase 2 loads (independent of phase 1): h rows, u, z, biases for this thread's items
-  float hs[IPT][N];
-  float uu[IPT], zz[IPT], bias[IPT], Dd[IPT];
 #pragma unroll
-  for (int k = 0; k < IPT; ++k) {
-    const int it = tid + k * DS_THREADS;
-    const int b = it / DS_CH, d = c0 + it % DS_CH;
-    const bool ok = b < batch && d < Ek;
-    const float* hp = h + ((int64_t)(ok ? b : 0) * Ek + (ok ? d : 0)) * N;
-#pragma unroll
-    for (int n = 0; n < N; n += 4) {
-      const float4 t4 = ok ? *reinterpret_cast<const float4*>(hp + n) : make_float4(0.f, 0.f, 0.f, 0.f);
-      hs[k][n] = t4.x; hs[k][n + 1] = t4.y; hs[k][n + 2] = t4.z; hs[k][n + 3] = t4.w;
+  for (int k = 0; k < AMAX; ++k) {
+    const int i = tid + k * DS_THREADS;
+    if (i < DS_CH * N) {
+      const float a = -expf(al[k]);
+      sA[i] = FAST ? a * 1.4426950408889634f : a;
     }
-    uu[k] = ok ? io<T>::ld(u + (int64_t)b * Ek + d) : 0.f;
-    if (zacc) {  // z from the decode in_proj fp32 accumulator; only reader -> re-zero after use
-      zz[k] = ok ? zacc[(int64_t)b * ldz + d] : 0.f;
-      if (ok) zacc[(int64_t)b * ldz + d] = 0.f;
-    } else {
-      zz[k] = ok ? io<T>::ld(z + (int64_t)b * ldz + d) : 0.f;
-    }
-    bias[k] = ok ? b_dt[d] : 0.f;
-    Dd[k] = ok ? d_skip[d] : 0.f;
   }
   __syncthreads();
   if (rmsnorm) {  // weightless RMSNorm of dt_low, B, C per batch row (Falcon-Mamba, reading Q18)
     const int warp = tid >> 5, lane = tid & 31;
-    for (int b = warp; b < batch; b += DS_THREADS / 32) {
+    for (int r = warp; r < nb; r += DS_THREADS / 32) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f;
       for (int c = lane; c < P; c += 32) {
-        const float v = sD[b * P4 + c];
+        const float v = sD[r * P4 + c];
         if (c < R) s0 = fmaf(v, v, s0);
         else if (c < R + N) s1 = fmaf(v, v, s1);
         else s2 = fmaf(v, v, s2);
@@ -633,54 +669,45 @@ __global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       }
       if (lane == 0) {
-        sS[b * 3 + 0] = 1.0f / sqrtf(s0 / (float)R + eps);
-        sS[b * 3 + 1] = 1.0f / sqrtf(s1 / (float)N + eps);
-        sS[b * 3 + 2] = 1.0f / sqrtf(s2 / (float)N + eps);
+        sS[r * 3 + 0] = 1.0f / sqrtf(s0 / (float)R + eps);
+        sS[r * 3 + 1] = 1.0f / sqrtf(s1 / (float)N + eps);
+        sS[r * 3 + 2] = 1.0f / sqrtf(s2 / (float)N + eps);
       }
     }
     __syncthreads();
   }
-
-  // ---- phase 2 compute: items (b, c), warp = fixed b, lane = channel
-#pragma unroll
-  for (int k = 0; k < IPT; ++k) {
-    const int it = tid + k * DS_THREADS;
-    const int b = it / DS_CH, c = it % DS_CH;
-    const int d = c0 + c;
-    if (b >= batch || d >= Ek) continue;
-    const float* wr = sW + c * R4;
-    const float* xr = sD + b * P4;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    const int R4e = R & ~3;
-    for (int r = 0; r < R4e; r += 4) {
-      const float4 wv = *reinterpret_cast<const float4*>(wr + r);
-      const float4 xv = *reinterpret_cast<const float4*>(xr + r);
-      s0 = fmaf(xv.x, wv.x, s0); s1 = fmaf(xv.y, wv.y, s1); s2 = fmaf(xv.z, wv.z, s2); s3 = fmaf(xv.w, wv.w, s3);
-    }
-    for (int r = R4e; r < R; ++r) s0 = fmaf(xr[r], wr[r], s0);
-    float dt = (s0 + s1) + (s2 + s3);
-    if (rmsnorm) dt *= sS[b * 3 + 0];
-    const float de = softplus(dt + bias[k]);
-    const float du = de * uu[k];
-    const float sB = rmsnorm ? sS[b * 3 + 1] : 1.f;
-    const float sC = rmsnorm ? sS[b * 3 + 2] : 1.f;
-    const float* Bt = xr + R;
-    const float* Ct = xr + R + N;
-    const float* Ac = sA + c * N;
-    float y = 0.f;
-#pragma unroll
-    for (int n = 0; n < N; ++n) {
-      const float ab = FAST ? ex2_approx(de * Ac[n]) : expf(de * Ac[n]);
-      hs[k][n] = fmaf(ab, hs[k][n], du * (Bt[n] * sB));
-      y = fmaf(Ct[n] * sC, hs[k][n], y);
-    }
-    float* hp = h + ((int64_t)b * Ek + d) * N;
-#pragma unroll
-    for (int n = 0; n < N; n += 4)
-      *reinterpret_cast<float4*>(hp + n) = make_float4(hs[k][n], hs[k][n + 1], hs[k][n + 2], hs[k][n + 3]);
-    y = fmaf(Dd[k], uu[k], y);
-    io<T>::st(g + (int64_t)b * Ek + d, y * silu<FAST>(zz[k]));
+  if (!ok) return;
+  // ---- compute: warp = one batch row, lane = channel
+  const float* wr = sW + cc * R4;
+  const float* xr = sD + bl * P4;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  const int R4e = R & ~3;
+  for (int r = 0; r < R4e; r += 4) {
+    const float4 wv = *reinterpret_cast<const float4*>(wr + r);
+    const float4 xv = *reinterpret_cast<const float4*>(xr + r);
+    s0 = fmaf(xv.x, wv.x, s0); s1 = fmaf(xv.y, wv.y, s1); s2 = fmaf(xv.z, wv.z, s2); s3 = fmaf(xv.w, wv.w, s3);
   }
+  for (int r = R4e; r < R; ++r) s0 = fmaf(xr[r], wr[r], s0);
+  float dt = (s0 + s1) + (s2 + s3);
+  if (rmsnorm) dt *= sS[bl * 3 + 0];
+  const float de = softplus(dt + bias);
+  const float du = de * uu;
+  const float sBs = rmsnorm ? sS[bl * 3 + 1] : 1.f;
+  const float sCs = rmsnorm ? sS[bl * 3 + 2] : 1.f;
+  const float* Bt = xr + R;
+  const float* Ct = xr + R + N;
+  const float* Ac = sA + cc * N;
+  float y = 0.f;
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    const float ab = FAST ? ex2_approx(de * Ac[n]) : expf(de * Ac[n]);
+    hs[n] = fmaf(ab, hs[n], du * (Bt[n] * sBs));
+    y = fmaf(Ct[n] * sCs, hs[n], y);
+  }
+#pragma unroll
+  for (int n = 0; n < N; n += 4) *reinterpret_cast<float4*>(hp + n) = make_float4(hs[n], hs[n + 1], hs[n + 2], hs[n + 3]);
+  y = fmaf(Dd, uu, y);
+  io<T>::st(g + (int64_t)b * Ek + d, y * silu<FAST>(zz));
 }
 
 // ---------------------------------------------------------------- RMSNorm (glue)
@@ -688,6 +715,8 @@ __global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
 template <typename T>
 __global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w,
                                                       float eps, T* __restrict__ y, int64_t M, int D) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int MAXV = 16;
   __shared__ float red[4];
   const int64_t row = blockIdx.x;
@@ -731,6 +760,8 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ 
 template <int VPL>
 __global__ void quantize_kernel(const float* __restrict__ x, int64_t nblocks, int8_t* __restrict__ q,
                                 float* __restrict__ scale) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t blk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (blk >= nblocks) return;
@@ -760,6 +791,8 @@ __global__ void quantize_kernel(const float* __restrict__ x, int64_t nblocks, in
 
 __global__ void qar_reduce_kernel(Peers src, int k, int64_t q_off, int64_t s_off, int64_t n16, int blk,
                                   float* __restrict__ out, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n16) return;
   float acc[16];
@@ -784,6 +817,8 @@ __global__ void qar_reduce_kernel(Peers src, int k, int64_t q_off, int64_t s_off
 }
 
 __global__ void f32_reduce_kernel(Peers src, int k, int64_t off, int64_t n4, float* __restrict__ out, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n4) return;
   float4 acc = reinterpret_cast<const float4*>(reinterpret_cast<const char*>(src.p[0]) + off)[i];
@@ -805,6 +840,8 @@ __global__ void f32_reduce_kernel(Peers src, int k, int64_t off, int64_t n4, flo
 // The epoch lives in device memory so a captured CUDA graph advances it on every replay
 // (every rank executes the same barrier sequence, so the counters agree).
 __global__ void peer_barrier_kernel(Peers bufs, int rank, int k) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ uint32_t s_epoch;
   const int t = threadIdx.x;
   uint32_t* own = reinterpret_cast<uint32_t*>(bufs.p[rank]);
@@ -834,15 +871,15 @@ template <typename T, bool F>
 cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const float* cw, const float* cb, void* u,
                           int64_t ldu, int batch, int L, int Ek, int K, cudaStream_t s) {
   constexpr int V = vec_of<T>();
-  dim3 grid((Ek / V + CONV_CG - 1) / CONV_CG, (L + CONV_TT - 1) / CONV_TT, batch);
+  dim3 grid((Ek / V + CONV_CG - 1) / CONV_CG, (L + CONV_TCH - 1) / CONV_TCH, batch);
   const T* x = reinterpret_cast<const T*>(xz);
   const T* c = reinterpret_cast<const T*>(cs);
   T* uu = reinterpret_cast<T*>(u);
   constexpr int NT = CONV_CG;
   switch (K) {
-    case 2: conv1d_silu_kernel<T, 2, F><<<grid, NT, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek); break;
-    case 3: conv1d_silu_kernel<T, 3, F><<<grid, NT, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek); break;
-    case 4: conv1d_silu_kernel<T, 4, F><<<grid, NT, 0, s>>>(x, ldxz, c, cw, cb, uu, ldu, L, Ek); break;
+    case 2: { cudaError_t e_ = launch(conv1d_silu_kernel<T, 2, F>, grid, NT, 0, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek); if (e_ != cudaSuccess) return e_; } break;
+    case 3: { cudaError_t e_ = launch(conv1d_silu_kernel<T, 3, F>, grid, NT, 0, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek); if (e_ != cudaSuccess) return e_; } break;
+    case 4: { cudaError_t e_ = launch(conv1d_silu_kernel<T, 4, F>, grid, NT, 0, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek); if (e_ != cudaSuccess) return e_; } break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -852,7 +889,7 @@ cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const fl
 
 // scan variant knobs (SSM_SCAN_VERSION=1 selects the 1-channel kernel; SSM_SCAN_NPOLY = states per
 // channel on the FMA-pipe exp2), read once per process
-static int g_scan_version = [] { const char* e = getenv("SSM_SCAN_VERSION"); return e ? atoi(e) : 2; }();
+static int g_scan_version = [] { const char* e = getenv("SSM_SCAN_VERSION"); return e ? atoi(e) : 1; }();
 static int g_scan_npoly = [] { const char* e = getenv("SSM_SCAN_NPOLY"); return e ? atoi(e) : 4; }();
 
 // ==================================================================== launchers
@@ -869,11 +906,11 @@ cudaError_t launch_conv_state_update(int bf16, const void* xz, int64_t ldxz, voi
   const int n = batch * Ek;
   if (n <= 0 || L <= 0) return cudaSuccess;
   if (bf16)
-    conv_state_update_kernel<__nv_bfloat16><<<(n + 255) / 256, 256, 0, s>>>(
-        reinterpret_cast<const __nv_bfloat16*>(xz), ldxz, reinterpret_cast<__nv_bfloat16*>(cs), batch, L, Ek, K);
+    { cudaError_t e_ = launch(conv_state_update_kernel<__nv_bfloat16>, (n + 255) / 256, 256, 0, s, 
+        reinterpret_cast<const __nv_bfloat16*>(xz), ldxz, reinterpret_cast<__nv_bfloat16*>(cs), batch, L, Ek, K); if (e_ != cudaSuccess) return e_; }
   else
-    conv_state_update_kernel<float><<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const float*>(xz), ldxz,
-                                                                     reinterpret_cast<float*>(cs), batch, L, Ek, K);
+    { cudaError_t e_ = launch(conv_state_update_kernel<float>, (n + 255) / 256, 256, 0, s, reinterpret_cast<const float*>(xz), ldxz,
+                                                                     reinterpret_cast<float*>(cs), batch, L, Ek, K); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 
@@ -886,13 +923,13 @@ cudaError_t launch_conv_decode(int bf16, const void* xz, int64_t ldxz, void* cs,
   float4* z0 = reinterpret_cast<float4*>(zero0);
   float4* z1 = reinterpret_cast<float4*>(zero1);
   if (bf16)
-    conv_decode_kernel<__nv_bfloat16, true><<<(n + 255) / 256, 256, 0, s>>>(
+    { cudaError_t e_ = launch(conv_decode_kernel<__nv_bfloat16, true>, (n + 255) / 256, 256, 0, s, 
         reinterpret_cast<const __nv_bfloat16*>(xz), ldxz, reinterpret_cast<__nv_bfloat16*>(cs), cw, cb,
-        reinterpret_cast<__nv_bfloat16*>(u), ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4, xacc);
+        reinterpret_cast<__nv_bfloat16*>(u), ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4, xacc); if (e_ != cudaSuccess) return e_; }
   else
-    conv_decode_kernel<float, false><<<(n + 255) / 256, 256, 0, s>>>(
+    { cudaError_t e_ = launch(conv_decode_kernel<float, false>, (n + 255) / 256, 256, 0, s, 
         reinterpret_cast<const float*>(xz), ldxz, reinterpret_cast<float*>(cs), cw, cb, reinterpret_cast<float*>(u),
-        ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4, xacc);
+        ldu, batch, Ek, K, z0, nzero0 / 4, z1, nzero1 / 4, xacc); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 
@@ -903,11 +940,11 @@ cudaError_t launch_unpack(int bf16, Peers src, int nsrc, int64_t off, int M, int
   if (R + 2 * N > kMaxP) return cudaErrorInvalidValue;
   const int blocks = (int)((warps * 32 + 255) / 256);
   if (bf16)
-    unpack_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(src, nsrc, off, M, hloc, R, N, rmsnorm, eps,
-                                                        reinterpret_cast<__nv_bfloat16*>(dlow), BC);
+    { cudaError_t e_ = launch(unpack_kernel<__nv_bfloat16>, blocks, 256, 0, s, src, nsrc, off, M, hloc, R, N, rmsnorm, eps,
+                                                        reinterpret_cast<__nv_bfloat16*>(dlow), BC); if (e_ != cudaSuccess) return e_; }
   else
-    unpack_kernel<float><<<blocks, 256, 0, s>>>(src, nsrc, off, M, hloc, R, N, rmsnorm, eps,
-                                                reinterpret_cast<float*>(dlow), BC);
+    { cudaError_t e_ = launch(unpack_kernel<float>, blocks, 256, 0, s, src, nsrc, off, M, hloc, R, N, rmsnorm, eps,
+                                                reinterpret_cast<float*>(dlow), BC); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 
@@ -916,9 +953,9 @@ static cudaError_t scan_t(const void* u, int64_t ldu, const void* dl, int64_t ld
                           const float* BC, int64_t ldbc, const float* a_log, const float* d_skip, float* h,
                           int64_t hbs, void* g, int64_t ldg, int batch, int L, int nch, cudaStream_t s) {
   dim3 grid((nch + SC_THREADS - 1) / SC_THREADS, batch);
-  scan_kernel<T, N, F><<<grid, SC_THREADS, 0, s>>>(
+  { cudaError_t e_ = launch(scan_kernel<T, N, F>, grid, SC_THREADS, 0, s, 
       reinterpret_cast<const T*>(u), ldu, reinterpret_cast<const T*>(dl), ldd, reinterpret_cast<const T*>(z), ldz, BC,
-      ldbc, a_log, d_skip, h, hbs, reinterpret_cast<T*>(g), ldg, L, nch);
+      ldbc, a_log, d_skip, h, hbs, reinterpret_cast<T*>(g), ldg, L, nch); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 
@@ -932,10 +969,10 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
     const int npoly = g_scan_npoly;
 #define S2A reinterpret_cast<const __nv_bfloat16*>(u), ldu, reinterpret_cast<const __nv_bfloat16*>(dl), ldd, \
       reinterpret_cast<const __nv_bfloat16*>(z), ldz, BC, ldbc, a_log, d_skip, h, hbs, reinterpret_cast<__nv_bfloat16*>(g), ldg, L, nch
-    if (npoly == 0) scan2_kernel<16, 0><<<grid, S3_THREADS, 0, s>>>(S2A);
-    else if (npoly == 2) scan2_kernel<16, 2><<<grid, S3_THREADS, 0, s>>>(S2A);
-    else if (npoly == 4) scan2_kernel<16, 4><<<grid, S3_THREADS, 0, s>>>(S2A);
-    else scan2_kernel<16, 6><<<grid, S3_THREADS, 0, s>>>(S2A);
+    if (npoly == 0) { cudaError_t e_ = launch(scan2_kernel<16, 0>, grid, S3_THREADS, 0, s, S2A); if (e_ != cudaSuccess) return e_; }
+    else if (npoly == 2) { cudaError_t e_ = launch(scan2_kernel<16, 2>, grid, S3_THREADS, 0, s, S2A); if (e_ != cudaSuccess) return e_; }
+    else if (npoly == 4) { cudaError_t e_ = launch(scan2_kernel<16, 4>, grid, S3_THREADS, 0, s, S2A); if (e_ != cudaSuccess) return e_; }
+    else { cudaError_t e_ = launch(scan2_kernel<16, 6>, grid, S3_THREADS, 0, s, S2A); if (e_ != cudaSuccess) return e_; }
 #undef S2A
     return cudaGetLastError();
   }
@@ -949,43 +986,24 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
   return scan_t<float, 8, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
 }
 
-static size_t dstep_smem(int batch, int R, int N) {
+static size_t dstep_smem(int R, int N) {
   const int P = R + 2 * N;
   const int R4 = ((R + 3) & ~3) + 4, P4 = (P + 3) & ~3;
-  return (size_t)(DS_CH * R4 + batch * P4 + DS_CH * N + batch * 3) * sizeof(float);
-}
-
-template <typename T, int N, bool F, int IPT>
-static cudaError_t dstep_t(Peers src, int nsrc, int64_t off, int ldp, int rms, float eps, const void* u, const void* z,
-                           int64_t ldz, const void* w_dt, const float* b_dt, const float* a_log, const float* d_skip,
-                           float* h, void* g, int batch, int Ek, int R, int cph, float* zacc, cudaStream_t s) {
-  const size_t smem = dstep_smem(batch, R, N);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_step_kernel<T, N, F, IPT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  decode_step_kernel<T, N, F, IPT><<<(Ek + DS_CH - 1) / DS_CH, DS_THREADS, smem, s>>>(
-      src, nsrc, off, ldp, rms, eps, reinterpret_cast<const T*>(u), reinterpret_cast<const T*>(z), ldz,
-      reinterpret_cast<const T*>(w_dt), b_dt, a_log, d_skip, h, reinterpret_cast<T*>(g), batch, Ek, R, cph, zacc);
-  return cudaGetLastError();
+  return (size_t)(DS_CH * R4 + DS_BB * P4 + DS_CH * N + DS_BB * 3) * sizeof(float);
 }
 
 template <typename T, int N, bool F>
-static cudaError_t dstep_ipt(int batch, Peers src, int nsrc, int64_t off, int ldp, int rms, float eps, const void* u,
-                             const void* z, int64_t ldz, const void* w_dt, const float* b_dt, const float* a_log,
-                             const float* d_skip, float* h, void* g, int Ek, int R, int cph, float* zacc,
-                             cudaStream_t s) {
-  const int ipt = (batch * DS_CH + DS_THREADS - 1) / DS_THREADS;
-#define DSA src, nsrc, off, ldp, rms, eps, u, z, ldz, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, cph, zacc, s
-  if (ipt <= 1) return dstep_t<T, N, F, 1>(DSA);
-  if (ipt <= 2) return dstep_t<T, N, F, 2>(DSA);
-  if (ipt <= 4) return dstep_t<T, N, F, 4>(DSA);
-  if (ipt <= 8) return dstep_t<T, N, F, 8>(DSA);
-#undef DSA
-  return cudaErrorInvalidValue;
+static cudaError_t dstep_t(Peers src, int nsrc, int64_t off, int ldp, int rms, float eps, const void* u, const void* z,
+                           int64_t ldz, const void* w_dt, const float* b_dt, const float* a_log, const float* d_skip,
+                           float* h, void* g, int batch, int Ek, int R, int cph, float* zacc, cudaStream_t s) {
+  const size_t smem = dstep_smem(R, N);
+  dim3 grid((Ek + DS_CH - 1) / DS_CH, (batch + DS_BB - 1) / DS_BB);
+  { cudaError_t e_ = launch(decode_step_kernel<T, N, F>, grid, DS_THREADS, smem, s, src, nsrc, off, ldp, rms, eps,
+                            reinterpret_cast<const T*>(u), reinterpret_cast<const T*>(z), ldz,
+                            reinterpret_cast<const T*>(w_dt), b_dt, a_log, d_skip, h, reinterpret_cast<T*>(g), batch,
+                            Ek, R, cph, zacc);
+    if (e_ != cudaSuccess) return e_; }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
@@ -994,13 +1012,13 @@ cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, i
                                int N, int ch_per_head, float* zacc, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   if (ch_per_head % DS_CH != 0) return cudaErrorInvalidValue;
-  if (dstep_smem(batch, R, N) > 200 * 1024 || batch > 64) return cudaErrorInvalidValue;
+  if (dstep_smem(R, N) > 48 * 1024) return cudaErrorInvalidValue;
   if (N != 16 && N != 8) return cudaErrorInvalidValue;
   const int es = bf16 ? 2 : 4;
-  if ((R * es) % 16 || (R + 2 * N) % 4 || ldp % 4) return cudaErrorInvalidValue;
-#define DS_ARGS batch, src, nsrc, src_off, ldp, rmsnorm, eps, u, z, ldz, w_dt, b_dt, a_log, d_skip, h, g, Ek, R, ch_per_head, zacc, s
-  if (bf16) return N == 16 ? dstep_ipt<__nv_bfloat16, 16, true>(DS_ARGS) : dstep_ipt<__nv_bfloat16, 8, true>(DS_ARGS);
-  return N == 16 ? dstep_ipt<float, 16, false>(DS_ARGS) : dstep_ipt<float, 8, false>(DS_ARGS);
+  if ((R * es) % 16 || (R + 2 * N) % 4 || ldp % 4 || R / (16 / es) * DS_CH > 8 * DS_THREADS) return cudaErrorInvalidValue;
+#define DS_ARGS src, nsrc, src_off, ldp, rmsnorm, eps, u, z, ldz, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, zacc, s
+  if (bf16) return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(DS_ARGS) : dstep_t<__nv_bfloat16, 8, true>(DS_ARGS);
+  return N == 16 ? dstep_t<float, 16, false>(DS_ARGS) : dstep_t<float, 8, false>(DS_ARGS);
 #undef DS_ARGS
 }
 
@@ -1009,9 +1027,9 @@ cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, 
   if (M <= 0) return cudaSuccess;
   if (D % 4 || D > 16 * 128 * 4) return cudaErrorInvalidValue;
   if (bf16)
-    rmsnorm_kernel<__nv_bfloat16><<<(unsigned)M, 128, 0, s>>>(x, w, eps, reinterpret_cast<__nv_bfloat16*>(y), M, D);
+    { cudaError_t e_ = launch(rmsnorm_kernel<__nv_bfloat16>, (unsigned)M, 128, 0, s, x, w, eps, reinterpret_cast<__nv_bfloat16*>(y), M, D); if (e_ != cudaSuccess) return e_; }
   else
-    rmsnorm_kernel<float><<<(unsigned)M, 128, 0, s>>>(x, w, eps, reinterpret_cast<float*>(y), M, D);
+    { cudaError_t e_ = launch(rmsnorm_kernel<float>, (unsigned)M, 128, 0, s, x, w, eps, reinterpret_cast<float*>(y), M, D); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 
@@ -1020,10 +1038,10 @@ cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float
   const int64_t nb = n / blk;
   const int blocks = (int)((nb * 32 + 255) / 256);
   switch (blk) {
-    case 32: quantize_kernel<1><<<blocks, 256, 0, s>>>(x, nb, q, scale); break;
-    case 64: quantize_kernel<2><<<blocks, 256, 0, s>>>(x, nb, q, scale); break;
-    case 128: quantize_kernel<4><<<blocks, 256, 0, s>>>(x, nb, q, scale); break;
-    case 256: quantize_kernel<8><<<blocks, 256, 0, s>>>(x, nb, q, scale); break;
+    case 32: { cudaError_t e_ = launch(quantize_kernel<1>, blocks, 256, 0, s, x, nb, q, scale); if (e_ != cudaSuccess) return e_; } break;
+    case 64: { cudaError_t e_ = launch(quantize_kernel<2>, blocks, 256, 0, s, x, nb, q, scale); if (e_ != cudaSuccess) return e_; } break;
+    case 128: { cudaError_t e_ = launch(quantize_kernel<4>, blocks, 256, 0, s, x, nb, q, scale); if (e_ != cudaSuccess) return e_; } break;
+    case 256: { cudaError_t e_ = launch(quantize_kernel<8>, blocks, 256, 0, s, x, nb, q, scale); if (e_ != cudaSuccess) return e_; } break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -1033,14 +1051,14 @@ cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, in
                               int accumulate, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const int64_t n16 = n / 16;
-  qar_reduce_kernel<<<(int)((n16 + 255) / 256), 256, 0, s>>>(src, k, q_off, s_off, n16, blk, out, accumulate);
+  { cudaError_t e_ = launch(qar_reduce_kernel, (int)((n16 + 255) / 256), 256, 0, s, src, k, q_off, s_off, n16, blk, out, accumulate); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 
 cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const int64_t n4 = n / 4;
-  f32_reduce_kernel<<<(int)((n4 + 255) / 256), 256, 0, s>>>(src, k, off, n4, out, accumulate);
+  { cudaError_t e_ = launch(f32_reduce_kernel, (int)((n4 + 255) / 256), 256, 0, s, src, k, off, n4, out, accumulate); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 
@@ -1061,14 +1079,8 @@ cudaError_t preload_kernels() {
       (const void*)scan_kernel<float, 16, false>, (const void*)scan_kernel<float, 8, false>,
       (const void*)scan2_kernel<16, 0>, (const void*)scan2_kernel<16, 2>, (const void*)scan2_kernel<16, 4>,
       (const void*)scan2_kernel<16, 6>,
-      (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 1>, (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 2>,
-      (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 4>, (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 8>,
-      (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 1>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 2>,
-      (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 4>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 8>,
-      (const void*)decode_step_kernel<float, 16, false, 1>, (const void*)decode_step_kernel<float, 16, false, 2>,
-      (const void*)decode_step_kernel<float, 16, false, 4>, (const void*)decode_step_kernel<float, 16, false, 8>,
-      (const void*)decode_step_kernel<float, 8, false, 1>, (const void*)decode_step_kernel<float, 8, false, 2>,
-      (const void*)decode_step_kernel<float, 8, false, 4>, (const void*)decode_step_kernel<float, 8, false, 8>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 16, true>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true>,
+      (const void*)decode_step_kernel<float, 16, false>, (const void*)decode_step_kernel<float, 8, false>,
       (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>,
       (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,
       (const void*)quantize_kernel<8>, (const void*)qar_reduce_kernel, (const void*)f32_reduce_kernel,
@@ -1081,7 +1093,7 @@ cudaError_t preload_kernels() {
 }
 
 cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s) {
-  peer_barrier_kernel<<<1, 32, 0, s>>>(bufs, rank, k);
+  { cudaError_t e_ = launch(peer_barrier_kernel, 1, 32, 0, s, bufs, rank, k); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 

@@ -192,6 +192,11 @@ class TPMixer:
         L.call("ssm_dbg_gemm", self.handle, _ptr(A), _ptr(B), _ptr(C_out), M, N, K, int(swap_ab), ksplit,
                _stream(stream))
 
+    def dbg_gemm_ld(self, A, B, C_out, M, N, K, swap_ab=False, ksplit=1, stream=None):
+        """A [M, K] with row stride A.stride(0), B [N, K] with row stride B.stride(0)."""
+        L.call("ssm_dbg_gemm_ld", self.handle, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(C_out), M, N, K,
+               int(swap_ab), ksplit, _stream(stream))
+
     def dbg_scan(self, u, delta, z, ldz, BC, a_log, d_skip, h, g, batch, seqlen, stream=None):
         L.call("ssm_dbg_scan", self.handle, _ptr(u), _ptr(delta), _ptr(z), ldz, _ptr(BC), _ptr(a_log), _ptr(d_skip),
                _ptr(h), _ptr(g), batch, seqlen, _stream(stream))

@@ -5,9 +5,13 @@ launched through libssmtp's C ABI; PyTorch provides memory, streams and the grap
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib as L
+
+_DEBUG_SKIP_NORM = os.environ.get("SSM_DEBUG_SKIP_NORM") == "1"  # timing ablations only
 from .mixer import LayerWeights, State, TPMixer
 
 
@@ -76,8 +80,10 @@ class MixerStack:
 
     def decode_step(self, res_t, stream=None):
         """res_t: [batch, D] fp32, updated in place through all layers."""
+        skip_norm = _DEBUG_SKIP_NORM
         for lw, st in zip(self.layers, self.states):
-            self.mx.rmsnorm(res_t, self.xbuf_dec, None, self.eps, stream)
+            if not skip_norm:
+                self.mx.rmsnorm(res_t, self.xbuf_dec, None, self.eps, stream)
             if self.nccl is None:
                 self.mx.decode(lw, st, self.xbuf_dec, res_t, self.flags, self.ws_dec, stream)
             else:

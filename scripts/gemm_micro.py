@@ -1,9 +1,12 @@
 #!/usr/bin/env python
 """Microbenchmark of the tcgen05 GEMM on the mixer's projection shapes (GPU only).
 
-Weights rotate over enough copies to exceed L2 (126 MB), so weight-streaming decode
-GEMMs read HBM as they do in a real decode step.  Prints achieved TFLOP/s and GB/s.
-    python scripts/gemm_micro.py [--kbs 1,2,4]
+Calls are captured into a CUDA graph (decode-sized GEMMs are otherwise host-launch bound),
+and weights rotate over enough copies to exceed L2 (126 MB) so weight-streaming decode GEMMs
+read HBM as in a real decode step.  Prints device time per call, TFLOP/s and GB/s.
+    python scripts/gemm_micro.py [--only dec] [--kbs 1,2]
+"contig" rows reproduce the decode in_proj byte count with K=64, so every 128-row TMA box is
+one contiguous 16 KB block (a DRAM-locality experiment, not a mixer shape).
 """
 import argparse
 import os
@@ -19,10 +22,12 @@ SHAPES = {
     # name: (tokens M, out features N, K, swap_ab, ksplit)
     "dec_in_proj": (16, 10240, 2560, 1, 1),
     "dec_in_proj_sk": (16, 10240, 2560, 1, -1),
+    "dec_in_proj_contig": (16, 10240 * 40, 64, 1, 1),
     "dec_x_proj": (16, 192, 5120, 1, 32),
     "dec_x_proj_sk": (16, 192, 5120, 1, -1),
     "dec_out_proj": (16, 2560, 5120, 1, 7),
     "dec_out_proj_sk": (16, 2560, 5120, 1, -1),
+    "dec_out_proj_contig": (16, 2560 * 80, 64, 1, 1),
     "pre_in_proj": (32768, 10240, 2560, 0, 1),
     "pre_x_proj": (32768, 192, 5120, 0, 1),
     "pre_dt_proj": (32768, 5120, 160, 0, 1),
@@ -46,21 +51,32 @@ def main():
         C = torch.empty(M, N, device="cuda")
         for kbs in a.kbs.split(","):
             os.environ["SSM_GEMM_KBS"] = kbs
-            for i in range(3):
-                mx.dbg_gemm(X, W[i % copies], C, swap_ab=bool(swap), ksplit=ks)
+            reps = 24 if swap else 4
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                for i in range(2):
+                    mx.dbg_gemm(X, W[i % copies], C, swap_ab=bool(swap), ksplit=ks, stream=s)
+            torch.cuda.current_stream().wait_stream(s)
             torch.cuda.synchronize()
-            reps = 20 if swap else 5
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for i in range(reps):
+                    mx.dbg_gemm(X, W[i % copies], C, swap_ab=bool(swap), ksplit=ks)
+            g.replay()
+            torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for i in range(reps):
-                mx.dbg_gemm(X, W[i % copies], C, swap_ab=bool(swap), ksplit=ks)
+            g.replay()
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) * 1000 / reps
             tf = 2 * M * N * K / (us * 1e-6) / 1e12
             gbs = (wbytes + M * K * 2 + M * N * 4) / (us * 1e-6) / 1e9
-            print(f"{name:14s} M={M:6d} N={N:6d} K={K:5d} swap={swap} ks={ks:2d} kbs={kbs}: "
-                  f"{us:9.2f} us  {tf:8.1f} TFLOP/s  {gbs:8.1f} GB/s", flush=True)
+            extra = " (incl. memset)" if ks != 1 else ""
+            print(f"{name:20s} M={M:6d} N={N:7d} K={K:5d} swap={swap} ks={ks:2d} kbs={kbs}: "
+                  f"{us:9.2f} us  {tf:8.1f} TFLOP/s  {gbs:8.1f} GB/s{extra}", flush=True)
+            del g
 
 
 if __name__ == "__main__":
