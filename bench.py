@@ -40,9 +40,10 @@ def parse():
     p.add_argument("--decode", type=int, default=-1, help="override decode length (smoke runs only)")
     p.add_argument("--layers", type=int, default=0, help="override layer count (smoke runs only)")
     p.add_argument("--chunk", type=int, default=0, help="prefill chunk length (default: whole prompt if it fits)")
-    p.add_argument("--probe", default="in_proj", help="kernel timed for the roofline line")
+
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-pack", action="store_true", help="decode streams the row-major weights (no pre-tiled copy)")
     return p.parse_args()
 
 
@@ -238,7 +239,10 @@ def main():
     layers = []
     for l in range(n_layers):
         full = synthetic_layer(dims, l, device=dev)
-        layers.append(LayerWeights(dims, full, k, rank, "bf16", dev))
+        lw = LayerWeights(dims, full, k, rank, "bf16", dev)
+        if not args.no_pack:
+            lw.pack(mx)  # pre-tiled copies of w_in / w_x / w_out for the decode weight streams
+        layers.append(lw)
         del full
     torch.cuda.empty_cache()
     stack = MixerStack(mx, layers, B, chunk, flags, nccl_group=(dist.group.WORLD if k > 1 else None))
@@ -256,7 +260,8 @@ def main():
     graph = None
     if Ld > 0:
         res_t.copy_(dec_in[0])
-        graph = stack.capture_decode(res_t)
+        # decode in_proj timed by CUDA-event nodes inside the graph (live, every replay)
+        graph = stack.capture_decode(res_t, probes=[("in_proj_decode", n_layers)])
 
     def step(timers=None):
         stack.reset()
@@ -283,7 +288,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    mx.probe(args.probe, 4 * n_layers * n_chunks * args.steps + 16)
+    mx.probe("in_proj", n_layers * n_chunks * args.steps + 16)
     launches0 = mx.launches()
     timers = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
@@ -297,8 +302,9 @@ def main():
         t_end.record()
         torch.cuda.synchronize()
         barrier()
-    probe_ms = mx.probe_read()
-    mx.probe(args.probe, 0)
+    pre_ms = mx.probe_read("in_proj")          # prefill in_proj launches of the timed steps
+    dec_ms_launch = mx.probe_read("in_proj_decode") if Ld > 0 else []   # last replay, one per layer
+    mx.probe("in_proj", 0)
     prefill_launches = mx.launches() - launches0
     total_ms = t_start.elapsed_time(t_end)
     ttft = [t[0].elapsed_time(t[1]) for t in timers]
@@ -341,36 +347,47 @@ def main():
         e2e = {"value": tokens * args.steps / (e_ms / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
 
-    # roofline of the probed (dominant) kernel
-    import json as _j
+    # roofline of the dominant kernel (largest share of the step): decode in_proj (HBM-bound weight
+    # stream, swap-AB) vs prefill in_proj (tensor-core bound); both measured live with CUDA events
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = _j.load(f)
+            peaks = json.load(f)
     except Exception:
         pass
-    Ek, D, R, P = dims.d_inner // k, dims.d_model, dims.dt_rank, dims.dt_rank + 2 * dims.d_state
+    traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(args.config, {})
+    except Exception:
+        pass
+    Ek, D = dims.d_inner // k, dims.d_model
     Mc = B * chunk
-    roof = None
-    if probe_ms:
-        avg = statistics.mean(probe_ms)
-        if args.probe in ("in_proj", "out_proj", "x_proj", "dt_proj"):
-            flops = {"in_proj": 2 * Mc * D * 2 * Ek, "out_proj": 2 * Mc * Ek * D, "x_proj": 2 * Mc * Ek * P,
-                     "dt_proj": 2 * Mc * R * Ek}[args.probe]
-            peak = peaks.get("bf16_tflops_sustained", 1394.1)
-            ach = flops / (avg / 1000) / 1e12
-            roof = {"kernel": args.probe, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                    "frac": ach / peak, "traffic": None, "launch_ms": avg, "launches": len(probe_ms),
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
-        else:
-            es = 2
-            byts = {"scan": Mc * Ek * (4 * es) + Mc * 2 * dims.d_state * 4,
-                    "conv": Mc * Ek * 2 * es}.get(args.probe, 0)
-            peak = peaks.get("hbm_gbs", 6535.1)
-            ach = byts / (avg / 1000) / 1e9
-            roof = {"kernel": args.probe, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": None, "launch_ms": avg, "launches": len(probe_ms),
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    roofs = {}
+    if pre_ms:
+        avg = statistics.mean(pre_ms)
+        flops = 2 * Mc * D * 2 * Ek
+        peak = peaks.get("bf16_tflops_sustained", 1394.1)
+        ach = flops / (avg / 1000) / 1e12
+        roofs["in_proj_prefill"] = {
+            "kernel": "gemm_tc_kernel (prefill in_proj, tcgen05)", "bound": "tensor", "achieved": ach, "peak": peak,
+            "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic.get("in_proj_prefill"), "launch_ms": avg,
+            "launches": len(pre_ms), "step_share_ms": sum(pre_ms) / args.steps,
+            "work_per_launch": f"2*M*D*2E_k = {flops:.3e} flop (M={Mc})",
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
+    if dec_ms_launch:
+        avg = statistics.mean(dec_ms_launch)
+        byts = 2 * Ek * D * 2 + B * D * 2 + B * 2 * Ek * 2  # weights + x_in + xz (bf16)
+        peak = peaks.get("hbm_gbs", 6535.1)
+        ach = byts / (avg / 1000) / 1e9
+        roofs["in_proj_decode"] = {
+            "kernel": "gemm_tc_kernel (decode in_proj, swap-AB weight stream)", "bound": "hbm", "achieved": ach,
+            "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic.get("in_proj_decode"),
+            "launch_ms": avg, "launches": len(dec_ms_launch), "step_share_ms": avg * n_layers * Ld,
+            "work_per_launch": f"W_in 2E_k*D bf16 + x_in + xz = {byts:.3e} B",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    roof = max(roofs.values(), key=lambda r: r["step_share_ms"]) if roofs else None
+    roof_other = [r for r in roofs.values() if r is not roof]
 
     cpu = None
     if rank == 0 and k == 1 and not args.no_cpu:
@@ -384,10 +401,12 @@ def main():
                 "config": {"workload": f"{args.config}: {n_layers} layers, d_model {dims.d_model}, batch {B}, "
                                        f"prompt {Lp} + {Ld} decode", "model": args.config, "global_batch": B,
                            "seq_len": Lp + Ld, "parallelism": f"tp{k}", "ar2": args.ar2 if k > 1 else "none",
-                           "prefill_chunk": chunk, "l2": "inputs larger than L2 (prompt residual "
+                           "prefill_chunk": chunk, "packed_decode_weights": not args.no_pack,
+                           "l2": "inputs larger than L2 (prompt residual "
                                                          f"{B * Lp * D * 4 / 1e6:.0f} MB > 126 MB)"},
                 "ttft_ms": statistics.mean(ttft), "tpot_ms": statistics.mean(dec_ms) / max(Ld, 1),
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+                "roofline": roof, "roofline_other": roof_other, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": gpu_launches,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if k > 1:

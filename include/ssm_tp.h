@@ -116,6 +116,11 @@ typedef struct {
   const float* a_log;    /* [E_k, N]    A = -exp(a_log)                                 */
   const float* d_skip;   /* [E_k]                                                       */
   const void* w_out;     /* [D, E_k]                                                    */
+  /* Optional (may be NULL): the same matrices pre-tiled by ssm_pack_weight.  When set, the
+   * decode path streams them as contiguous 16 KB tiles (sequential HBM reads). bf16 only. */
+  const void* w_in_pk;
+  const void* w_x_pk;
+  const void* w_out_pk;
 } ssm_layer_weights_t;
 
 typedef struct ssm_tp_s* ssm_tp_t;
@@ -184,6 +189,13 @@ ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_
 ssm_status_t ssm_rmsnorm(ssm_tp_t tp, const float* residual, const float* weight, float eps,
                          void* x_out, int64_t M, void* stream);
 
+/* Pre-tiled copy of a bf16 weight matrix [rows, cols] (row-major, nn.Linear layout) for the
+ * decode GEMMs: 128 x 64 tiles, each one contiguous 16 KB block, ordered row-tile-major and
+ * zero-padded to whole tiles.  out must be 128-B aligned and >= ssm_packed_weight_bytes bytes. */
+ssm_status_t ssm_packed_weight_bytes(int32_t rows, int32_t cols, size_t* bytes);
+ssm_status_t ssm_pack_weight(ssm_tp_t tp, const void* w, int32_t rows, int32_t cols, void* out, size_t out_bytes,
+                             void* stream);
+
 /* Synchronise the stream and report device-side protocol errors (SSM_ERR_PROTOCOL). */
 ssm_status_t ssm_tp_check(ssm_tp_t tp, void* stream);
 
@@ -194,20 +206,26 @@ ssm_status_t ssm_tp_stats(ssm_tp_t tp, int64_t* allreduce_count, int64_t* bytes_
 /* Kernel launches enqueued by this handle since creation (for bench.py gpu_launches). */
 ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches);
 
-/* Per-kernel timing probe (bench.py roofline): while enabled, the library records a CUDA
- * event pair on the launching stream around every launch of `kernel` (outside graph
- * capture), up to `capacity` launches.  capacity 0 disables and releases the events. */
+/* Per-kernel timing probes (bench.py roofline): while enabled for `kernel`, the library records
+ * a CUDA event pair on the launching stream around every launch of that kernel kind (outside
+ * graph capture, except SSM_PROBE_IN_PROJ_DECODE), up to `capacity` launches.  Each kind has
+ * its own slot; capacity 0 disables the kind and releases its events. */
 enum { SSM_PROBE_IN_PROJ = 1, SSM_PROBE_CONV = 2, SSM_PROBE_X_PROJ = 3, SSM_PROBE_DT_PROJ = 4, SSM_PROBE_SCAN = 5,
-       SSM_PROBE_OUT_PROJ = 6, SSM_PROBE_AR2 = 7, SSM_PROBE_DECODE_STEP = 8 };
+       SSM_PROBE_OUT_PROJ = 6, SSM_PROBE_AR2 = 7, SSM_PROBE_DECODE_STEP = 8,
+       SSM_PROBE_IN_PROJ_DECODE = 9 /* decode in_proj; recorded INSIDE graph capture too (event nodes:
+                                       after replays, each pair holds its latest replay's times) */ };
 ssm_status_t ssm_tp_probe(ssm_tp_t tp, int32_t kernel, int32_t capacity);
-/* Synchronises the recorded events and writes up to `capacity` per-launch durations (ms). */
-ssm_status_t ssm_tp_probe_read(ssm_tp_t tp, float* ms, int32_t capacity, int32_t* n);
+/* Synchronises the recorded events of `kernel` and writes up to `capacity` per-launch durations (ms). */
+ssm_status_t ssm_tp_probe_read(ssm_tp_t tp, int32_t kernel, float* ms, int32_t capacity, int32_t* n);
 
 /* ------------------------------------------------------------------ test-only */
 /* C = A B^T with A [M,K], B [N,K] (cfg.dtype), C fp32 [M,N]; exercises the GEMM used
  * by the projections (tcgen05 for bf16 when K*2 % 16 == 0, SIMT otherwise). */
 ssm_status_t ssm_dbg_gemm(ssm_tp_t tp, const void* A, const void* B, float* C,
                           int32_t M, int32_t N, int32_t K, int32_t swap_ab, int32_t ksplit, void* stream);
+/* Swap-AB decode GEMM C[M,N] = X[M,K] W[N,K]^T reading W through its packed copy Wpk. */
+ssm_status_t ssm_dbg_gemm_packed(ssm_tp_t tp, const void* X, const void* W, const void* Wpk, float* C, int32_t M,
+                                 int32_t N, int32_t K, int32_t ksplit, void* stream);
 /* Same with explicit row strides (elements) of A and B. */
 ssm_status_t ssm_dbg_gemm_ld(ssm_tp_t tp, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int32_t M,
                              int32_t N, int32_t K, int32_t swap_ab, int32_t ksplit, void* stream);

@@ -40,7 +40,7 @@ class ssm_comm_t(C.Structure):
 class ssm_layer_weights_t(C.Structure):
     _fields_ = [("w_in", C.c_void_p), ("conv_w", C.c_void_p), ("conv_b", C.c_void_p), ("w_x", C.c_void_p),
                 ("w_dt", C.c_void_p), ("b_dt", C.c_void_p), ("a_log", C.c_void_p), ("d_skip", C.c_void_p),
-                ("w_out", C.c_void_p)]
+                ("w_out", C.c_void_p), ("w_in_pk", C.c_void_p), ("w_x_pk", C.c_void_p), ("w_out_pk", C.c_void_p)]
 
 
 def _load():
@@ -69,8 +69,11 @@ def _load():
         "ssm_tp_stats": (st, [vp, P(i64), P(i64)]),
         "ssm_tp_launch_count": (st, [vp, P(i64)]),
         "ssm_tp_probe": (st, [vp, i32, i32]),
-        "ssm_tp_probe_read": (st, [vp, P(C.c_float), i32, P(i32)]),
+        "ssm_tp_probe_read": (st, [vp, i32, P(C.c_float), i32, P(i32)]),
         "ssm_dbg_gemm": (st, [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]),
+        "ssm_packed_weight_bytes": (st, [i32, i32, P(sz)]),
+        "ssm_pack_weight": (st, [vp, vp, i32, i32, vp, sz, vp]),
+        "ssm_dbg_gemm_packed": (st, [vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]),
         "ssm_dbg_gemm_ld": (st, [vp, vp, i64, vp, i64, vp, i32, i32, i32, i32, i32, vp]),
         "ssm_dbg_scan": (st, [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, i32, vp]),
     }
@@ -85,9 +88,10 @@ LIB = _load()
 EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "ssm_comm_bytes", "ssm_workspace_bytes",
             "ssm_state_bytes", "ssm_state_alloc", "ssm_state_reset", "ssm_state_free", "ssm_mixer_prefill",
             "ssm_mixer_decode", "ssm_qallreduce", "ssm_rmsnorm", "ssm_tp_check", "ssm_tp_stats",
-            "ssm_tp_launch_count", "ssm_tp_probe", "ssm_tp_probe_read", "ssm_dbg_gemm", "ssm_dbg_gemm_ld",
-            "ssm_dbg_scan"]
-PROBE = {"in_proj": 1, "conv": 2, "x_proj": 3, "dt_proj": 4, "scan": 5, "out_proj": 6, "ar2": 7, "decode_step": 8}
+            "ssm_tp_launch_count", "ssm_tp_probe", "ssm_tp_probe_read", "ssm_packed_weight_bytes", "ssm_pack_weight",
+            "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld", "ssm_dbg_scan"]
+PROBE = {"in_proj": 1, "conv": 2, "x_proj": 3, "dt_proj": 4, "scan": 5, "out_proj": 6, "ar2": 7, "decode_step": 8,
+         "in_proj_decode": 9}
 
 
 def check(rc, func):

@@ -70,9 +70,11 @@ struct ssm_tp_s {
   uint32_t epoch;
   int64_t ar_count, bytes_sent, launches;
   int num_sms;
-  // timing probe
-  int probe_kind = 0, probe_cap = 0, probe_n = 0;
-  cudaEvent_t* probe_ev = nullptr;  // 2 * probe_cap events
+  // timing probes: one slot per kernel kind
+  struct ProbeSlot {
+    int cap = 0, n = 0;
+    cudaEvent_t* ev = nullptr;  // 2 * cap events
+  } probes[16];
 };
 
 struct ssm_state_s {
@@ -149,11 +151,13 @@ ssm_status_t validate_cfg(const ssm_config_t* c, int k) {
 }
 
 cudaError_t gemm(ssm_tp_s* t, const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
-                 int ksplit, const Epilogue& e, cudaStream_t s, bool a_is_weight = false) {
+                 int ksplit, const Epilogue& e, cudaStream_t s, bool a_is_weight = false,
+                 const void* a_blocked = nullptr) {
   t->launches++;
   if (t->bf16 && gemm_tc_supported(A, lda, B, ldb))
     return gemm_tc_bf16(reinterpret_cast<const __nv_bfloat16*>(A), lda, reinterpret_cast<const __nv_bfloat16*>(B),
-                        ldb, M, N, K, ksplit, e, t->num_sms, s, a_is_weight && t_launch_pdl);
+                        ldb, M, N, K, ksplit, e, t->num_sms, s, a_is_weight && t_launch_pdl,
+                        reinterpret_cast<const __nv_bfloat16*>(a_blocked));
   return gemm_simt(A, lda, B, ldb, t->bf16, M, N, K, ksplit, e, s);
 }
 
@@ -163,15 +167,20 @@ struct Probe {
   ssm_tp_s* t;
   cudaStream_t s;
   int idx = -1;
+  ssm_tp_s::ProbeSlot* slot = nullptr;
   Probe(ssm_tp_s* t_, int kind, cudaStream_t s_) : t(t_), s(s_) {
-    if (t->probe_kind != kind || t->probe_n >= t->probe_cap) return;
+    if (kind < 0 || kind >= 16) return;
+    ssm_tp_s::ProbeSlot& p = t->probes[kind];
+    if (p.n >= p.cap) return;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
-    idx = t->probe_n++;
-    cudaEventRecord(t->probe_ev[2 * idx], s);
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) return;
+    if (cs != cudaStreamCaptureStatusNone && kind != SSM_PROBE_IN_PROJ_DECODE) return;
+    slot = &p;
+    idx = p.n++;
+    cudaEventRecord(p.ev[2 * idx], s);
   }
   ~Probe() {
-    if (idx >= 0) cudaEventRecord(t->probe_ev[2 * idx + 1], s);
+    if (idx >= 0) cudaEventRecord(slot->ev[2 * idx + 1], s);
   }
 };
 
@@ -267,9 +276,9 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   // (a1) in_proj, column-parallel: xz = x_in W_in,r^T   [M, 2E_k]
   const int skip = decode ? g_dbg_skip : 0;
   if (!(skip & 1)) {
-    Probe pr(t, SSM_PROBE_IN_PROJ, s);
+    Probe pr(t, decode ? SSM_PROBE_IN_PROJ_DECODE : SSM_PROBE_IN_PROJ, s);
     if (swap)
-      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s, true));
+      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s, true, w->w_in_pk));
     else
       CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, epi(kst, 0, xz, 2 * Ek), s));
   }
@@ -301,7 +310,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     Probe pr(t, SSM_PROBE_X_PROJ, s);
     if (swap)
       CU(gemm(t, w->w_x, Ek, u, Ek, hl * P, (int)M, Ek, ks_x,
-              epi(ks_x != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s, true));
+              epi(ks_x != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s, true, w->w_x_pk));
     else
       CU(gemm(t, u, Ek, w->w_x, Ek, (int)M, hl * P, Ek, 1, epi(EPI_STORE_F32, 0, xdst, hl * P), s));
   }
@@ -357,7 +366,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   if (!(skip & 16)) {
     Probe pr(t, SSM_PROBE_OUT_PROJ, s);
     if (swap)
-      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, epi(EPI_ATOMIC_F32, 1, odst, D), s, true));
+      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, epi(EPI_ATOMIC_F32, 1, odst, D), s, true, w->w_out_pk));
     else
       CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D), s));
   }
@@ -477,7 +486,8 @@ ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp
 }
 
 ssm_status_t ssm_tp_destroy(ssm_tp_t tp) {
-  if (tp) ssm_tp_probe(tp, 0, 0);
+  if (tp)
+    for (int k = 0; k < 16; ++k) ssm_tp_probe(tp, k, 0);
   delete tp;
   return SSM_OK;
 }
@@ -485,185 +495,33 @@ ssm_status_t ssm_tp_destroy(ssm_tp_t tp) {
 ssm_status_t ssm_tp_probe(ssm_tp_t tp, int32_t kernel, int32_t capacity) {
   if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
   if (capacity < 0) return fail(SSM_ERR_ARG, "capacity < 0");
-  if (tp->probe_ev) {
-    for (int i = 0; i < 2 * tp->probe_cap; ++i) cudaEventDestroy(tp->probe_ev[i]);
-    delete[] tp->probe_ev;
-    tp->probe_ev = nullptr;
+  if (kernel < 0 || kernel >= 16) return fail(SSM_ERR_ARG, "kernel id %d", kernel);
+  ssm_tp_s::ProbeSlot& p = tp->probes[kernel];
+  if (p.ev) {
+    for (int i = 0; i < 2 * p.cap; ++i) cudaEventDestroy(p.ev[i]);
+    delete[] p.ev;
+    p.ev = nullptr;
   }
-  tp->probe_kind = 0;
-  tp->probe_cap = 0;
-  tp->probe_n = 0;
+  p.cap = 0;
+  p.n = 0;
   if (capacity == 0) return SSM_OK;
-  tp->probe_ev = new (std::nothrow) cudaEvent_t[2 * capacity];
-  if (!tp->probe_ev) return fail(SSM_ERR_ARG, "out of host memory");
-  for (int i = 0; i < 2 * capacity; ++i) CU(cudaEventCreate(&tp->probe_ev[i]));
-  tp->probe_kind = kernel;
-  tp->probe_cap = capacity;
+  p.ev = new (std::nothrow) cudaEvent_t[2 * capacity];
+  if (!p.ev) return fail(SSM_ERR_ARG, "out of host memory");
+  for (int i = 0; i < 2 * capacity; ++i) CU(cudaEventCreate(&p.ev[i]));
+  p.cap = capacity;
   return SSM_OK;
 }
 
-ssm_status_t ssm_tp_probe_read(ssm_tp_t tp, float* ms, int32_t capacity, int32_t* n) {
+ssm_status_t ssm_tp_probe_read(ssm_tp_t tp, int32_t kernel, float* ms, int32_t capacity, int32_t* n) {
   if (!tp || !n) return fail(SSM_ERR_ARG, "NULL argument");
-  const int cnt = tp->probe_n < capacity ? tp->probe_n : capacity;
+  if (kernel < 0 || kernel >= 16) return fail(SSM_ERR_ARG, "kernel id %d", kernel);
+  ssm_tp_s::ProbeSlot& p = tp->probes[kernel];
+  const int cnt = p.n < capacity ? p.n : capacity;
   for (int i = 0; i < cnt; ++i) {
-    CU(cudaEventSynchronize(tp->probe_ev[2 * i + 1]));
-    CU(cudaEventElapsedTime(&ms[i], tp->probe_ev[2 * i], tp->probe_ev[2 * i + 1]));
+    CU(cudaEventSynchronize(p.ev[2 * i + 1]));
+    CU(cudaEventElapsedTime(&ms[i], p.ev[2 * i], p.ev[2 * i + 1]));
   }
   *n = cnt;
-  return SSM_OK;
-}
-
-ssm_status_t ssm_comm_bytes(const ssm_config_t* cfg, int32_t tp_size, int64_t max_tokens, size_t* bytes) {
-  if (!bytes) return fail(SSM_ERR_ARG, "bytes is NULL");
-  ssm_status_t st = validate_cfg(cfg, tp_size);
-  if (st != SSM_OK) return st;
-  if (max_tokens < 1) max_tokens = 1;
-  *bytes = kSigBytes + 2 * payload_bytes(cfg, tp_size, max_tokens);
-  return SSM_OK;
-}
-
-ssm_status_t ssm_workspace_bytes(ssm_tp_t tp, int32_t batch, int32_t seqlen, size_t* bytes) {
-  if (!tp || !bytes) return fail(SSM_ERR_ARG, "NULL argument");
-  if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
-  *bytes = ws_layout(tp, (int64_t)batch * seqlen).total;
-  return SSM_OK;
-}
-
-ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, size_t* h_bytes) {
-  if (!tp || !conv_bytes || !h_bytes) return fail(SSM_ERR_ARG, "NULL argument");
-  if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
-  *conv_bytes = (size_t)batch * (tp->cfg.d_conv - 1) * tp->Ek * tp->es;
-  *h_bytes = (size_t)batch * tp->Ek * tp->cfg.d_state * 4;
-  return SSM_OK;
-}
-
-ssm_status_t ssm_state_alloc(ssm_tp_t tp, int32_t batch, void* conv_buf, size_t conv_bytes, void* h_buf,
-                             size_t h_bytes, void* stream, ssm_state_t* out) {
-  if (!out) return fail(SSM_ERR_ARG, "out is NULL");
-  *out = nullptr;
-  size_t cb = 0, hb = 0;
-  ssm_status_t s = ssm_state_bytes(tp, batch, &cb, &hb);
-  if (s != SSM_OK) return s;
-  if (!conv_buf || !h_buf) return fail(SSM_ERR_ARG, "state buffers are NULL");
-  if (conv_bytes < cb || h_bytes < hb)
-    return fail(SSM_ERR_ARG, "state buffers too small (%zu/%zu B, need %zu/%zu B)", conv_bytes, h_bytes, cb, hb);
-  if ((reinterpret_cast<uintptr_t>(conv_buf) | reinterpret_cast<uintptr_t>(h_buf)) & 15)
-    return fail(SSM_ERR_ARG, "state buffers must be 16-B aligned");
-  ssm_state_s* st = new (std::nothrow) ssm_state_s();
-  if (!st) return fail(SSM_ERR_ARG, "out of host memory");
-  st->owner = tp;
-  st->batch = batch;
-  st->conv = conv_buf;
-  st->h = reinterpret_cast<float*>(h_buf);
-  cudaStream_t s_ = reinterpret_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(conv_buf, 0, cb, s_) != cudaSuccess || cudaMemsetAsync(h_buf, 0, hb, s_) != cudaSuccess) {
-    delete st;
-    return fail(SSM_ERR_CUDA, "zero-fill of the state failed: %s", cudaGetErrorString(cudaGetLastError()));
-  }
-  *out = st;
-  return SSM_OK;
-}
-
-ssm_status_t ssm_state_reset(ssm_state_t st, void* stream) {
-  if (!st) return fail(SSM_ERR_ARG, "state is NULL");
-  size_t cb = 0, hb = 0;
-  ssm_state_bytes(st->owner, st->batch, &cb, &hb);
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  CU(cudaMemsetAsync(st->conv, 0, cb, s));
-  CU(cudaMemsetAsync(st->h, 0, hb, s));
-  return SSM_OK;
-}
-
-ssm_status_t ssm_state_free(ssm_state_t st) {
-  delete st;
-  return SSM_OK;
-}
-
-ssm_status_t ssm_mixer_prefill(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, const void* x_in,
-                               float* residual, int32_t batch, int32_t seqlen, uint32_t flags, void* workspace,
-                               size_t ws_bytes, void* stream) {
-  ssm_status_t s = check_call(tp, w, st, x_in, residual, batch, seqlen, flags, workspace, ws_bytes);
-  if (s != SSM_OK) return s;
-  if ((int64_t)batch * seqlen == 0) return SSM_OK;
-  return run_layer(tp, w, st, x_in, residual, batch, seqlen, flags, workspace, false,
-                   reinterpret_cast<cudaStream_t>(stream));
-}
-
-ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, const void* x_in,
-                              float* residual, int32_t batch, uint32_t flags, void* workspace, size_t ws_bytes,
-                              void* stream) {
-  ssm_status_t s = check_call(tp, w, st, x_in, residual, batch, 1, flags, workspace, ws_bytes);
-  if (s != SSM_OK) return s;
-  if (batch == 0) return SSM_OK;
-  PdlScope pdl(g_pdl_enabled);
-  return run_layer(tp, w, st, x_in, residual, batch, 1, flags, workspace, true,
-                   reinterpret_cast<cudaStream_t>(stream));
-}
-
-ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
-  if (!tp || !partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
-  if (flags & ~(uint32_t)SSM_QAR_ACCUMULATE) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
-  const int blk = tp->cfg.qar_block;
-  if (n % blk) return fail(SSM_ERR_DIM, "n=%zu not a multiple of qar_block=%d", n, blk);
-  if ((reinterpret_cast<uintptr_t>(partial) | reinterpret_cast<uintptr_t>(out)) & 15)
-    return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const bool acc = flags & SSM_QAR_ACCUMULATE;
-  if (n == 0) return SSM_OK;
-  if (tp->k == 1) {  // reading Q13: no quantisation at TP=1
-    Peers one{};
-    one.p[0] = const_cast<float*>(partial);
-    tp->launches++;
-    CU(launch_f32_reduce(one, 1, 0, (int64_t)n, out, acc, s));
-    return SSM_OK;
-  }
-  const size_t need = al256(n) + n / blk * 4;
-  if (need > half_bytes(tp)) return fail(SSM_ERR_ARG, "symmetric buffer too small for n=%zu", n);
-  const uint32_t ep = ++tp->epoch;
-  const size_t half = half_bytes(tp);
-  char* own = reinterpret_cast<char*>(tp->peers.p[tp->rank]) + kSigBytes + (ep & 1) * half;
-  const int64_t off = (int64_t)(kSigBytes + (ep & 1) * half);
-  tp->launches += 3;
-  CU(launch_quantize(partial, (int64_t)n, blk, reinterpret_cast<int8_t*>(own), reinterpret_cast<float*>(own + al256(n)), s));
-  tp->ar_count++;
-  tp->bytes_sent += n + n / blk * 4;
-  CU(launch_peer_barrier(tp->peers, tp->rank, tp->k, s));
-  CU(launch_qar_reduce(tp->peers, tp->k, off, off + (int64_t)al256(n), (int64_t)n, blk, out, acc, s));
-  return SSM_OK;
-}
-
-ssm_status_t ssm_rmsnorm(ssm_tp_t tp, const float* residual, const float* weight, float eps, void* x_out, int64_t M,
-                         void* stream) {
-  PdlScope pdl(g_pdl_enabled && M <= 256);  // decode-sized rows: overlap with the neighbours
-  if (!tp || !residual || !x_out) return fail(SSM_ERR_ARG, "NULL argument");
-  if ((reinterpret_cast<uintptr_t>(residual) | reinterpret_cast<uintptr_t>(weight) | reinterpret_cast<uintptr_t>(x_out)) & 15)
-    return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
-  tp->launches++;
-  CU(launch_rmsnorm(tp->bf16, residual, weight, eps, x_out, M, tp->cfg.d_model, reinterpret_cast<cudaStream_t>(stream)));
-  return SSM_OK;
-}
-
-ssm_status_t ssm_tp_check(ssm_tp_t tp, void* stream) {
-  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
-  CU(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
-  if (tp->k > 1) {
-    uint32_t errw = 0;
-    CU(cudaMemcpy(&errw, reinterpret_cast<char*>(tp->peers.p[tp->rank]) + 64, 4, cudaMemcpyDeviceToHost));
-    if (errw) return fail(SSM_ERR_PROTOCOL, "peer flag wait timed out on rank %d (epoch %u)", tp->rank, tp->epoch);
-  }
-  return SSM_OK;
-}
-
-ssm_status_t ssm_tp_stats(ssm_tp_t tp, int64_t* allreduce_count, int64_t* bytes_sent) {
-  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
-  if (allreduce_count) *allreduce_count = tp->ar_count;
-  if (bytes_sent) *bytes_sent = tp->bytes_sent;
-  return SSM_OK;
-}
-
-ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches) {
-  if (!tp || !launches) return fail(SSM_ERR_ARG, "NULL argument");
-  *launches = tp->launches;
   return SSM_OK;
 }
 
@@ -682,6 +540,37 @@ ssm_status_t ssm_dbg_gemm_ld(ssm_tp_t tp, const void* A, int64_t lda, const void
     CU(gemm(tp, B, ldb, A, lda, N, M, K, ksplit, epi(kind, 1, C, N), s, true));
   else
     CU(gemm(tp, A, lda, B, ldb, M, N, K, ksplit, epi(kind, 0, C, N), s));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_packed_weight_bytes(int32_t rows, int32_t cols, size_t* bytes) {
+  if (!bytes) return fail(SSM_ERR_ARG, "bytes is NULL");
+  if (rows <= 0 || cols <= 0) return fail(SSM_ERR_DIM, "rows=%d cols=%d", rows, cols);
+  *bytes = packed_blocked_bytes(rows, cols);
+  return SSM_OK;
+}
+
+ssm_status_t ssm_pack_weight(ssm_tp_t tp, const void* w, int32_t rows, int32_t cols, void* out, size_t out_bytes,
+                             void* stream) {
+  if (!tp || !w || !out) return fail(SSM_ERR_ARG, "NULL argument");
+  if (!tp->bf16) return fail(SSM_ERR_UNSUPPORTED, "packed weights are for the bf16 tensor-core path");
+  if (rows <= 0 || cols <= 0) return fail(SSM_ERR_DIM, "rows=%d cols=%d", rows, cols);
+  if (out_bytes < packed_blocked_bytes(rows, cols)) return fail(SSM_ERR_ARG, "out buffer too small");
+  if ((reinterpret_cast<uintptr_t>(out) & 127) || (reinterpret_cast<uintptr_t>(w) & 15))
+    return fail(SSM_ERR_ARG, "w must be 16-B and out 128-B aligned");
+  tp->launches++;
+  CU(pack_blocked(reinterpret_cast<const __nv_bfloat16*>(w), rows, cols, cols, reinterpret_cast<__nv_bfloat16*>(out),
+                  reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_dbg_gemm_packed(ssm_tp_t tp, const void* X, const void* W, const void* Wpk, float* C, int32_t M,
+                                 int32_t N, int32_t K, int32_t ksplit, void* stream) {
+  if (!tp || !X || !W || !Wpk || !C) return fail(SSM_ERR_ARG, "NULL argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (ksplit != 1) CU(cudaMemsetAsync(C, 0, (size_t)M * N * 4, s));
+  const int kind = ksplit != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32;
+  CU(gemm(tp, W, K, X, K, N, M, K, ksplit, epi(kind, 1, C, N), s, true, Wpk));
   return SSM_OK;
 }
 

@@ -206,7 +206,7 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_pf, int64_t lda, int K,
-                   CtaRes cr) {
+                   CtaRes cr, int a_blocked) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int STAGES = num_stages(BN, KBS, cr.ring);
@@ -268,7 +268,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], ph ^ 1);
           mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * (BM + BN) * BK * 2);
           uint8_t* st = ring + stage * SB;
-          for (int j = 0; j < nk; ++j) tma_load_2d(st + j * A_STAGE, &tmA, &full[stage], (kb + j) * BK, mt * BM);
+          if (a_blocked)  // A pre-tiled: block (mt, kb) is one contiguous 16 KB box
+            for (int j = 0; j < nk; ++j)
+              tma_load_3d(st + j * A_STAGE, &tmA, &full[stage], 0, 0, mt * ts.kb_total + kb + j);
+          else
+            for (int j = 0; j < nk; ++j) tma_load_2d(st + j * A_STAGE, &tmA, &full[stage], (kb + j) * BK, mt * BM);
           for (int j = 0; j < nk; ++j) tma_load_2d(st + BOFF + j * BSUB, &tmB, &full[stage], (kb + j) * BK, nt * BN);
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
@@ -375,7 +379,57 @@ bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+// Blocked ("pre-tiled") weight layout: block (r / 128, k / 64) of 128 x 64 bf16 stored as one
+// contiguous 16 KB row-major tile; blocks ordered row-tile-major.  TMA views it as a 3D tensor
+// {64, 128, n_blocks} so every box is one contiguous 16 KB read (sequential weight streams).
+bool make_map_blocked(CUtensorMap* map, const void* ptr, int64_t n_blocks) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)BK, (cuuint64_t)BM, (cuuint64_t)n_blocks};
+  cuuint64_t strides[2] = {(cuuint64_t)(BK * 2), (cuuint64_t)(BK * BM * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)BM, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+__global__ void pack_blocked_kernel(const __nv_bfloat16* __restrict__ w, int rows, int cols, int64_t ld,
+                                    __nv_bfloat16* __restrict__ out, int kbt, int64_t n_vec) {
+  // one thread per 16-B output vector (8 bf16); zero padding beyond rows / cols
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_vec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = v * 8;
+    const int64_t blk = e / (BM * BK);
+    const int within = (int)(e % (BM * BK));
+    const int r = (int)(blk / kbt) * BM + within / BK;
+    const int k = (int)(blk % kbt) * BK + within % BK;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (r < rows) {
+      if (k + 8 <= cols && ((ld * 2) % 16 == 0)) {
+        val = *reinterpret_cast<const uint4*>(w + (int64_t)r * ld + k);
+      } else {
+        __nv_bfloat16* t = reinterpret_cast<__nv_bfloat16*>(&val);
+        for (int j = 0; j < 8; ++j) t[j] = (k + j < cols) ? w[(int64_t)r * ld + k + j] : __float2bfloat16_rn(0.f);
+      }
+    }
+    reinterpret_cast<uint4*>(out)[v] = val;
+  }
+}
 }  // namespace
+
+size_t packed_blocked_bytes(int rows, int cols) {
+  const int64_t mt = (rows + BM - 1) / BM, kbt = (cols + BK - 1) / BK;
+  return (size_t)(mt * kbt * BM * BK * 2);
+}
+
+cudaError_t pack_blocked(const __nv_bfloat16* w, int rows, int cols, int64_t ld, __nv_bfloat16* out, cudaStream_t s) {
+  const int kbt = (cols + BK - 1) / BK;
+  const int64_t n_vec = (int64_t)packed_blocked_bytes(rows, cols) / 16;
+  pack_blocked_kernel<<<(unsigned)((n_vec + 255) / 256 < 4096 ? (n_vec + 255) / 256 : 4096), 256, 0, s>>>(
+      w, rows, cols, ld, out, kbt, n_vec);
+  return cudaGetLastError();
+}
 
 cudaError_t preload_gemm_tc() {
   cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -390,7 +444,8 @@ bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb) {
 }
 
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
-                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool prefetch_a) {
+                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool prefetch_a,
+                         const __nv_bfloat16* A_blocked) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   const int ksplit_in = ksplit;
   // BN: multiple of 32 in [32, 256] (UMMA needs N % 16 == 0; the epilogue drains TMEM in
@@ -418,7 +473,11 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   if ((ts.ksplit > 1 || ts.streamk) && epi.kind != EPI_ATOMIC_F32) return cudaErrorInvalidValue;
 
   CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K, lda, BM)) return cudaErrorInvalidValue;
+  if (A_blocked) {
+    if (!make_map_blocked(&ma, A_blocked, (int64_t)ts.m_tiles * ts.kb_total)) return cudaErrorInvalidValue;
+  } else if (!make_map(&ma, A, M, K, lda, BM)) {
+    return cudaErrorInvalidValue;
+  }
   if (!make_map(&mb, B, N, K, ldb, BN)) return cudaErrorInvalidValue;
 
   static bool attr_set = false;
@@ -454,7 +513,8 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     grid = (int)(W < cap ? W : cap);
   }
   { cudaError_t e_ = launch(gemm_tc_kernel, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi,
-                                      prefetch_a && ((lda * 2) % 16 == 0) && (K % 8 == 0) ? A : nullptr, lda, K, cr); if (e_ != cudaSuccess) return e_; }
+                                      prefetch_a && !A_blocked && ((lda * 2) % 16 == 0) && (K % 8 == 0) ? A : nullptr,
+                                      lda, K, cr, A_blocked ? 1 : 0); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 

@@ -38,8 +38,13 @@ struct Peers {
 // Requires lda*2 % 16 == 0, ldb*2 % 16 == 0, 16-B aligned bases.
 // prefetch_a: A is a weight (independent of the predecessor kernel): bulk-prefetch each CTA's A
 // rows into L2 before griddepcontrol.wait.
+// A_blocked: optional copy of A in the blocked layout (pack_blocked); TMA then reads contiguous
+// 16 KB boxes (sequential weight streams for the decode GEMMs).
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
-                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool prefetch_a = false);
+                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool prefetch_a = false,
+                         const __nv_bfloat16* A_blocked = nullptr);
+size_t packed_blocked_bytes(int rows, int cols);
+cudaError_t pack_blocked(const __nv_bfloat16* w, int rows, int cols, int64_t ld, __nv_bfloat16* out, cudaStream_t s);
 bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb);
 // SIMT GEMM, fp32 accumulation, T = float or bf16 inputs.
 cudaError_t gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, int dtype_bf16, int M, int N, int K,

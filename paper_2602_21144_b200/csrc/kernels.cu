@@ -523,18 +523,23 @@ __global__ void __launch_bounds__(S3_THREADS) scan2_kernel(
 constexpr int DS_CH = 32;
 constexpr int DS_BB = 4;
 constexpr int DS_THREADS = DS_CH * DS_BB;
+__host__ __device__ inline int dstep_rw(int R, int es) {
+  return es == 2 ? R + ((8 - R % 64) + 64) % 64 : R + ((4 - R % 32) + 32) % 32;
+}
 template <typename T, int N, bool FAST>
-__global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
+__global__ void __launch_bounds__(DS_THREADS, 5) decode_step_kernel(
     Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps, const T* __restrict__ u,
     const T* __restrict__ z, int64_t ldz, const T* __restrict__ w_dt, const float* __restrict__ b_dt,
     const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ h, T* __restrict__ g,
     int batch, int Ek, int R, int ch_per_head, float* __restrict__ zacc) {
   extern __shared__ __align__(16) float dsm[];
+  constexpr int V = 16 / sizeof(T);
   const int P = R + 2 * N;
-  const int R4 = ((R + 3) & ~3) + 4;      // padded fp32 row of W_dt (16-B aligned, bank-spread)
+  const int RW = dstep_rw(R, (int)sizeof(T));  // W_dt row stride (elements of T): 16-B aligned, and
+                                               // row-to-row bank shift of 4 words (conflict-free LDS.128)
   const int P4 = (P + 3) & ~3;
-  float* sW = dsm;                        // [DS_CH][R4]
-  float* sD = sW + DS_CH * R4;            // [DS_BB][P4]  summed dbc rows of this block's head
+  T* sW = reinterpret_cast<T*>(dsm);      // [DS_CH][RW], storage type (converted on use)
+  float* sD = dsm + (DS_CH * RW * (int)sizeof(T) + 15) / 16 * 4;  // [DS_BB][P4] summed dbc rows
   float* sA = sD + DS_BB * P4;            // [DS_CH][N]   A (log2e-scaled in FAST mode)
   float* sS = sA + DS_CH * N;             // [DS_BB][3]   RMSNorm scales
   const int tid = threadIdx.x;
@@ -544,20 +549,17 @@ __global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
   const int nb = min(DS_BB, batch - b0);
   pdl_trigger();
 
-  // ---- weights first (independent of the predecessor kernels): W_dt rows, a_log
-  constexpr int V = 16 / sizeof(T);
-  constexpr int WMAX = 8;  // W_dt 16-B vectors per thread (32 rows x R <= 256 bf16)
+  // ---- weights first (independent of the predecessor kernels): W_dt rows (cp.async, no
+  //      register staging), a_log
   constexpr int AMAX = (DS_CH * N + DS_THREADS - 1) / DS_THREADS;
   const int cpr = R / V;
   const int nw = DS_CH * cpr;
-  uint4 wraw[WMAX];
-#pragma unroll
-  for (int k = 0; k < WMAX; ++k) {
-    const int i = tid + k * DS_THREADS;
+  for (int i = tid; i < nw; i += DS_THREADS) {
     const int c = i / cpr, q = i % cpr;
-    wraw[k] = (i < nw && c0 + c < Ek) ? *reinterpret_cast<const uint4*>(w_dt + (int64_t)(c0 + c) * R + q * V)
-                                      : make_uint4(0, 0, 0, 0);
+    const bool okw = c0 + c < Ek;
+    cp_async16(sW + c * RW + q * V, w_dt + (int64_t)(okw ? c0 + c : 0) * R + q * V, okw);
   }
+  cp_async_commit();
   float al[AMAX];
 #pragma unroll
   for (int k = 0; k < AMAX; ++k) {
@@ -598,22 +600,6 @@ __global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
     zz = io<T>::ld(z + (int64_t)b * ldz + d);
   }
   // ---- consume into shared memory
-#pragma unroll
-  for (int k = 0; k < WMAX; ++k) {
-    const int i = tid + k * DS_THREADS;
-    if (i >= nw) break;
-    const int c = i / cpr, q = i % cpr;
-    float* dst = sW + c * R4 + q * V;
-    if constexpr (sizeof(T) == 2) {
-      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&wraw[k]);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) { const float2 f = __bfloat1622float2(b2[j]); dst[2 * j] = f.x; dst[2 * j + 1] = f.y; }
-    } else {
-      const float* f = reinterpret_cast<const float*>(&wraw[k]);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dst[j] = f[j];
-    }
-  }
   for (int base = 0; base < nd; base += DMAX * DS_THREADS) {
     if (base > 0) {
 #pragma unroll
@@ -651,6 +637,7 @@ __global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
       sA[i] = FAST ? a * 1.4426950408889634f : a;
     }
   }
+  cp_async_wait<0>();
   __syncthreads();
   if (rmsnorm) {  // weightless RMSNorm of dt_low, B, C per batch row (Falcon-Mamba, reading Q18)
     const int warp = tid >> 5, lane = tid & 31;
@@ -678,16 +665,27 @@ __global__ void __launch_bounds__(DS_THREADS) decode_step_kernel(
   }
   if (!ok) return;
   // ---- compute: warp = one batch row, lane = channel
-  const float* wr = sW + cc * R4;
+  const T* wr = sW + cc * RW;
   const float* xr = sD + bl * P4;
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  const int R4e = R & ~3;
-  for (int r = 0; r < R4e; r += 4) {
-    const float4 wv = *reinterpret_cast<const float4*>(wr + r);
-    const float4 xv = *reinterpret_cast<const float4*>(xr + r);
-    s0 = fmaf(xv.x, wv.x, s0); s1 = fmaf(xv.y, wv.y, s1); s2 = fmaf(xv.z, wv.z, s2); s3 = fmaf(xv.w, wv.w, s3);
+  for (int r = 0; r < R; r += V) {  // R % V == 0 (validated by the launcher)
+    float wv[V];
+    if constexpr (sizeof(T) == 2) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(wr + r);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int j = 0; j < V / 2; ++j) { const float2 f = __bfloat1622float2(b2[j]); wv[2 * j] = f.x; wv[2 * j + 1] = f.y; }
+    } else {
+      const float4 f = *reinterpret_cast<const float4*>(wr + r);
+      wv[0] = f.x; wv[1] = f.y; wv[2] = f.z; wv[3] = f.w;
+    }
+#pragma unroll
+    for (int j = 0; j < V; j += 4) {
+      const float4 xv = *reinterpret_cast<const float4*>(xr + r + j);
+      s0 = fmaf(xv.x, wv[j], s0); s1 = fmaf(xv.y, wv[j + 1], s1); s2 = fmaf(xv.z, wv[j + 2], s2);
+      s3 = fmaf(xv.w, wv[j + 3], s3);
+    }
   }
-  for (int r = R4e; r < R; ++r) s0 = fmaf(xr[r], wr[r], s0);
   float dt = (s0 + s1) + (s2 + s3);
   if (rmsnorm) dt *= sS[bl * 3 + 0];
   const float de = softplus(dt + bias);
@@ -986,17 +984,17 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
   return scan_t<float, 8, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
 }
 
-static size_t dstep_smem(int R, int N) {
+static size_t dstep_smem(int R, int N, int es) {
   const int P = R + 2 * N;
-  const int R4 = ((R + 3) & ~3) + 4, P4 = (P + 3) & ~3;
-  return (size_t)(DS_CH * R4 + DS_BB * P4 + DS_CH * N + DS_BB * 3) * sizeof(float);
+  const int RW = dstep_rw(R, es), P4 = (P + 3) & ~3;
+  return (size_t)((DS_CH * RW * es + 15) / 16 * 16) + (size_t)(DS_BB * P4 + DS_CH * N + DS_BB * 3) * sizeof(float);
 }
 
 template <typename T, int N, bool F>
 static cudaError_t dstep_t(Peers src, int nsrc, int64_t off, int ldp, int rms, float eps, const void* u, const void* z,
                            int64_t ldz, const void* w_dt, const float* b_dt, const float* a_log, const float* d_skip,
                            float* h, void* g, int batch, int Ek, int R, int cph, float* zacc, cudaStream_t s) {
-  const size_t smem = dstep_smem(R, N);
+  const size_t smem = dstep_smem(R, N, (int)sizeof(T));
   dim3 grid((Ek + DS_CH - 1) / DS_CH, (batch + DS_BB - 1) / DS_BB);
   { cudaError_t e_ = launch(decode_step_kernel<T, N, F>, grid, DS_THREADS, smem, s, src, nsrc, off, ldp, rms, eps,
                             reinterpret_cast<const T*>(u), reinterpret_cast<const T*>(z), ldz,
@@ -1012,10 +1010,10 @@ cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, i
                                int N, int ch_per_head, float* zacc, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   if (ch_per_head % DS_CH != 0) return cudaErrorInvalidValue;
-  if (dstep_smem(R, N) > 48 * 1024) return cudaErrorInvalidValue;
   if (N != 16 && N != 8) return cudaErrorInvalidValue;
   const int es = bf16 ? 2 : 4;
-  if ((R * es) % 16 || (R + 2 * N) % 4 || ldp % 4 || R / (16 / es) * DS_CH > 8 * DS_THREADS) return cudaErrorInvalidValue;
+  if (dstep_smem(R, N, es) > 48 * 1024) return cudaErrorInvalidValue;
+  if ((R * es) % 16 || (R + 2 * N) % 4 || ldp % 4) return cudaErrorInvalidValue;
 #define DS_ARGS src, nsrc, src_off, ldp, rmsnorm, eps, u, z, ldz, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, zacc, s
   if (bf16) return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(DS_ARGS) : dstep_t<__nv_bfloat16, 8, true>(DS_ARGS);
   return N == 16 ? dstep_t<float, 16, false>(DS_ARGS) : dstep_t<float, 8, false>(DS_ARGS);

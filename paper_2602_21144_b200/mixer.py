@@ -74,6 +74,19 @@ class LayerWeights:
         }
         self.struct = L.ssm_layer_weights_t(**{k: v.data_ptr() for k, v in self.tensors.items()})
 
+    def pack(self, mixer, stream=None):
+        """Pre-tile w_in, w_x, w_out (ssm_pack_weight) so decode streams contiguous 16 KB tiles."""
+        for name in ("w_in", "w_x", "w_out"):
+            t = self.tensors[name]
+            rows, cols = t.shape
+            nb = C.c_size_t()
+            L.call("ssm_packed_weight_bytes", rows, cols, C.byref(nb))
+            pk = torch.empty(nb.value // 2, dtype=torch.bfloat16, device=t.device)
+            L.call("ssm_pack_weight", mixer.handle, _ptr(t), rows, cols, _ptr(pk), nb.value, _stream(stream))
+            self.tensors[name + "_pk"] = pk
+            setattr(self.struct, name + "_pk", pk.data_ptr())
+        return self
+
 
 class State:
     """SSM cache of one layer on this rank: conv window + fp32 h."""
@@ -176,13 +189,14 @@ class TPMixer:
         return n.value
 
     def probe(self, kernel, capacity):
-        """Record per-launch CUDA events around `kernel` ('in_proj', 'scan', ...)."""
-        L.call("ssm_tp_probe", self.handle, L.PROBE[kernel] if capacity else 0, capacity)
+        """Record per-launch CUDA events around `kernel` ('in_proj', 'scan', 'in_proj_decode', ...);
+        capacity 0 disables that kind."""
+        L.call("ssm_tp_probe", self.handle, L.PROBE[kernel], capacity)
 
-    def probe_read(self, capacity=100000):
+    def probe_read(self, kernel, capacity=100000):
         buf = (C.c_float * capacity)()
         n = C.c_int32()
-        L.call("ssm_tp_probe_read", self.handle, buf, capacity, C.byref(n))
+        L.call("ssm_tp_probe_read", self.handle, L.PROBE[kernel], buf, capacity, C.byref(n))
         return list(buf[:n.value])
 
     # ---- test-only
@@ -191,6 +205,20 @@ class TPMixer:
         N = B.shape[0]
         L.call("ssm_dbg_gemm", self.handle, _ptr(A), _ptr(B), _ptr(C_out), M, N, K, int(swap_ab), ksplit,
                _stream(stream))
+
+    def dbg_gemm_packed(self, X, W, Wpk, C_out, ksplit=1, stream=None):
+        M, K = X.shape
+        N = W.shape[0]
+        L.call("ssm_dbg_gemm_packed", self.handle, _ptr(X), _ptr(W), _ptr(Wpk), _ptr(C_out), M, N, K, ksplit,
+               _stream(stream))
+
+    def pack_weight(self, W, stream=None):
+        rows, cols = W.shape
+        nb = C.c_size_t()
+        L.call("ssm_packed_weight_bytes", rows, cols, C.byref(nb))
+        pk = torch.empty(nb.value // 2, dtype=torch.bfloat16, device=W.device)
+        L.call("ssm_pack_weight", self.handle, _ptr(W), rows, cols, _ptr(pk), nb.value, _stream(stream))
+        return pk
 
     def dbg_gemm_ld(self, A, B, C_out, M, N, K, swap_ab=False, ksplit=1, stream=None):
         """A [M, K] with row stride A.stride(0), B [N, K] with row stride B.stride(0)."""

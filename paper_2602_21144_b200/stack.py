@@ -98,7 +98,7 @@ class MixerStack:
         dist.all_reduce(pb, group=self.nccl)     # NCCL bf16 all-reduce (baseline arm)
         res.add_(pb.float())
 
-    def capture_decode(self, res_t):
+    def capture_decode(self, res_t, probes=()):
         """Capture one decode step over all layers into a CUDA graph reading/writing res_t.
         The decode path is graph-safe: no host sync, fixed pointers; the all-reduce epoch
         counters live in device memory and advance on every replay, and each step issues an
@@ -109,6 +109,8 @@ class MixerStack:
             self.decode_step(res_t, s)   # warm-up (attribute setup outside capture)
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
+        for kind, cap in probes:  # event nodes recorded inside the graph (see SSM_PROBE_IN_PROJ_DECODE)
+            self.mx.probe(kind, cap)
         g = torch.cuda.CUDAGraph()
         before = self.mx.launches()
         ar_before = self.mx.stats()["allreduce"]

@@ -17,6 +17,9 @@ dims = synth.CONFIGS[cfg]
 B = synth.WORKLOADS[cfg]["batch"]
 mx = TPMixer(dims, "bf16")
 layers = [LayerWeights(dims, synthetic_layer(dims, l), 1, 0, "bf16") for l in range(nl)]
+if os.environ.get("SSM_ABL_PACK", "1") == "1":
+    for lw in layers:
+        lw.pack(mx)
 stack = MixerStack(mx, layers, B, 1)
 res = torch.randn(B, dims.d_model, device="cuda")
 g = stack.capture_decode(res)
@@ -31,4 +34,4 @@ e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1000 / 20 / nl
 print(f"{cfg} skip={os.environ.get('SSM_DEBUG_SKIP', '0')} skipnorm={os.environ.get('SSM_DEBUG_SKIP_NORM', '0')} "
-      f"pdl={os.environ.get('SSM_PDL', '0')}: {us:8.2f} us/layer  kernels/step={stack.graph_launches}", flush=True)
+      f"pdl={os.environ.get('SSM_PDL', '0')} pack={os.environ.get('SSM_ABL_PACK', '1')}: {us:8.2f} us/layer  kernels/step={stack.graph_launches}", flush=True)

@@ -12,17 +12,15 @@ import synth  # noqa: E402
 from paper_2602_21144_b200 import TPMixer  # noqa: E402
 
 EXPS = [
-    ("pad64 kbs2", {"PAD": "64"}, 1),
-    ("pad128 kbs2", {"PAD": "136"}, 1),
-    ("pad64 streamK148", {"PAD": "64"}, -1),
+    ("packed kbs2", {"PACK": "1"}, 1),
+    ("packed kbs1", {"PACK": "1", "SSM_GEMM_KBS": "1"}, 1),
+    ("packed kbs4", {"PACK": "1", "SSM_GEMM_KBS": "4"}, 1),
+    ("packed split2", {"PACK": "1"}, 2),
+    ("packed streamK148", {"PACK": "1"}, -1),
     ("base kbs2", {}, 1),
     ("kbs1", {"SSM_GEMM_KBS": "1"}, 1),
     ("nomma", {"SSM_GEMM_NOMMA": "1"}, 1),
     ("streamK148", {}, -1),
-    ("ring100 streamK296", {"SSM_GEMM_RING_KB": "100", "SSM_GEMM_SK_CTAS": "296"}, -1),
-    ("ring100 streamK148", {"SSM_GEMM_RING_KB": "100", "SSM_GEMM_SK_CTAS": "148"}, -1),
-    ("ring64 streamK444", {"SSM_GEMM_RING_KB": "64", "SSM_GEMM_SK_CTAS": "444"}, -1),
-    ("ring100 streamK296 nomma", {"SSM_GEMM_RING_KB": "100", "SSM_GEMM_SK_CTAS": "296", "SSM_GEMM_NOMMA": "1"}, -1),
 ]
 SHAPES = {"in_proj": (16, 10240, 2560), "out_proj": (16, 2560, 5120)}
 
@@ -55,15 +53,24 @@ def main():
             W = [w[:, :K] for w in Wfull]
             for k in keys:
                 os.environ.pop(k, None)
-            os.environ.update({k: v for k, v in env.items() if k != "PAD"})
+            os.environ.update({k: v for k, v in env.items() if k not in ("PAD", "PACK")})
+            packed = env.get("PACK") == "1"
+            PK = [mx.pack_weight(w.contiguous()) for w in W] if packed else None
+            torch.cuda.synchronize()
+
+            def call(i):
+                if packed:
+                    mx.dbg_gemm_packed(X, W[i], PK[i], C, ksplit=ks)
+                else:
+                    mx.dbg_gemm_ld(X, W[i], C, M, N, K, swap_ab=True, ksplit=ks)
             reps = 24
             for i in range(2):
-                mx.dbg_gemm_ld(X, W[i], C, M, N, K, swap_ab=True, ksplit=ks)
+                call(i)
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 for i in range(reps):
-                    mx.dbg_gemm_ld(X, W[i % copies], C, M, N, K, swap_ab=True, ksplit=ks)
+                    call(i % copies)
             g.replay()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -74,7 +81,7 @@ def main():
             us = e0.elapsed_time(e1) * 1000 / reps
             print(f"{sname:9s} {name:28s} ks={ks:2d}: {us:8.2f} us  {N * K * 2 / (us * 1e-6) / 1e9:8.1f} GB/s"
                   f"{'  (incl memset)' if ks != 1 else ''}", flush=True)
-            del g, W, Wfull
+            del g, W, Wfull, PK
 
 
 if __name__ == "__main__":

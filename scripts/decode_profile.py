@@ -36,7 +36,7 @@ def main():
         for _ in range(a.steps):
             stack.decode_step(res)
         torch.cuda.synchronize()
-        ms = mx.probe_read()
+        ms = mx.probe_read(kind)
         mx.probe(kind, 0)
         out[kind] = statistics.median(ms) * 1000
     # rmsnorm (separate ABI call) timed with torch events

@@ -35,6 +35,22 @@ def test_gemm_tcgen05_bf16(M, N, K, swap, ks):
     assert rel(C.cpu(), ref) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,K,ks", [(16, 10240, 2560, 1), (16, 192, 5120, 20), (32, 2560, 5120, 7), (5, 300, 200, 1)])
+def test_gemm_packed_weights(M, N, K, ks):
+    """Decode GEMM streaming the pre-tiled (ssm_pack_weight) copy of W: same result as the plain layout."""
+    dims = synth.MixerDims(d_model=64, d_inner=128, dt_rank=4)
+    mx = TPMixer(dims, "bf16")
+    g = torch.Generator().manual_seed(N + K)
+    X = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    W = torch.randn(N, K, generator=g).to(torch.bfloat16)
+    Wd = W.cuda()
+    pk = mx.pack_weight(Wd)
+    C = torch.empty(M, N, device="cuda")
+    mx.dbg_gemm_packed(X.cuda(), Wd, pk, C, ksplit=ks)
+    torch.cuda.synchronize()
+    assert rel(C.cpu(), X.double() @ W.double().T) < 1e-5
+
+
 def test_gemm_simt_fp32():
     dims = synth.MixerDims(d_model=64, d_inner=128, dt_rank=4)
     mx = TPMixer(dims, "fp32")
@@ -83,11 +99,13 @@ def test_scan_kernel_vs_oracle(dtype, L_):
 
 
 # ------------------------------------------------------------------ full mixer, TP=1
-def _run_tp1(dims, dtype, B, L_in, L_out, chunks=None, layer=0):
+def _run_tp1(dims, dtype, B, L_in, L_out, chunks=None, layer=0, pack=False):
     w = prep_weights(dims, layer, dtype)
     x, res = prep_acts(B, L_in + L_out, dims, dtype, seed=11 + layer)
     mx = TPMixer(dims, dtype)
     lw = LayerWeights(dims, w, dtype=dtype)
+    if pack:
+        lw.pack(mx)
     st = State(mx, B)
     outs = []
     chunks = chunks or [L_in]
@@ -119,12 +137,13 @@ def test_mixer_tp1_fp32_tiny_prefill_decode():
     assert rel(st[0], st_ref[0]) < TOL["fp32"]
 
 
-@pytest.mark.parametrize("dims_name", ["med", "med_falcon", "med_zamba"])
-def test_mixer_tp1_bf16_prefill_decode(dims_name):
+@pytest.mark.parametrize("dims_name,pack", [("med", False), ("med_falcon", False), ("med_zamba", False),
+                                            ("med", True), ("med_zamba", True)])
+def test_mixer_tp1_bf16_prefill_decode(dims_name, pack):
     dims = {"med": MED,
             "med_falcon": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, bcdt_rmsnorm=True),
             "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2)}[dims_name]
-    gpu, ref, res, st, st_ref, mx = _run_tp1(dims, "bf16", 3, 150, 6)
+    gpu, ref, res, st, st_ref, mx = _run_tp1(dims, "bf16", 3, 150, 6, pack=pack)
     assert rel(gpu - res, ref - res) < TOL["bf16"]
     assert rel(st[1], st_ref[1]) < TOL["bf16"]
     assert rel(st[0], st_ref[0]) < TOL["bf16"]
