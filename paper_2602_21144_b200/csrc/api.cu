@@ -525,6 +525,160 @@ ssm_status_t ssm_tp_probe_read(ssm_tp_t tp, int32_t kernel, float* ms, int32_t c
   return SSM_OK;
 }
 
+ssm_status_t ssm_comm_bytes(const ssm_config_t* cfg, int32_t tp_size, int64_t max_tokens, size_t* bytes) {
+  if (!bytes) return fail(SSM_ERR_ARG, "bytes is NULL");
+  ssm_status_t st = validate_cfg(cfg, tp_size);
+  if (st != SSM_OK) return st;
+  if (max_tokens < 1) max_tokens = 1;
+  *bytes = kSigBytes + 2 * payload_bytes(cfg, tp_size, max_tokens);
+  return SSM_OK;
+}
+
+ssm_status_t ssm_workspace_bytes(ssm_tp_t tp, int32_t batch, int32_t seqlen, size_t* bytes) {
+  if (!tp || !bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
+  *bytes = ws_layout(tp, (int64_t)batch * seqlen).total;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, size_t* h_bytes) {
+  if (!tp || !conv_bytes || !h_bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
+  *conv_bytes = (size_t)batch * (tp->cfg.d_conv - 1) * tp->Ek * tp->es;
+  *h_bytes = (size_t)batch * tp->Ek * tp->cfg.d_state * 4;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_state_alloc(ssm_tp_t tp, int32_t batch, void* conv_buf, size_t conv_bytes, void* h_buf,
+                             size_t h_bytes, void* stream, ssm_state_t* out) {
+  if (!out) return fail(SSM_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  size_t cb = 0, hb = 0;
+  ssm_status_t s = ssm_state_bytes(tp, batch, &cb, &hb);
+  if (s != SSM_OK) return s;
+  if (!conv_buf || !h_buf) return fail(SSM_ERR_ARG, "state buffers are NULL");
+  if (conv_bytes < cb || h_bytes < hb)
+    return fail(SSM_ERR_ARG, "state buffers too small (%zu/%zu B, need %zu/%zu B)", conv_bytes, h_bytes, cb, hb);
+  if ((reinterpret_cast<uintptr_t>(conv_buf) | reinterpret_cast<uintptr_t>(h_buf)) & 15)
+    return fail(SSM_ERR_ARG, "state buffers must be 16-B aligned");
+  ssm_state_s* st = new (std::nothrow) ssm_state_s();
+  if (!st) return fail(SSM_ERR_ARG, "out of host memory");
+  st->owner = tp;
+  st->batch = batch;
+  st->conv = conv_buf;
+  st->h = reinterpret_cast<float*>(h_buf);
+  cudaStream_t s_ = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(conv_buf, 0, cb, s_) != cudaSuccess || cudaMemsetAsync(h_buf, 0, hb, s_) != cudaSuccess) {
+    delete st;
+    return fail(SSM_ERR_CUDA, "zero-fill of the state failed: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  *out = st;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_state_reset(ssm_state_t st, void* stream) {
+  if (!st) return fail(SSM_ERR_ARG, "state is NULL");
+  size_t cb = 0, hb = 0;
+  ssm_state_bytes(st->owner, st->batch, &cb, &hb);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CU(cudaMemsetAsync(st->conv, 0, cb, s));
+  CU(cudaMemsetAsync(st->h, 0, hb, s));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_state_free(ssm_state_t st) {
+  delete st;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_mixer_prefill(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, const void* x_in,
+                               float* residual, int32_t batch, int32_t seqlen, uint32_t flags, void* workspace,
+                               size_t ws_bytes, void* stream) {
+  ssm_status_t s = check_call(tp, w, st, x_in, residual, batch, seqlen, flags, workspace, ws_bytes);
+  if (s != SSM_OK) return s;
+  if ((int64_t)batch * seqlen == 0) return SSM_OK;
+  return run_layer(tp, w, st, x_in, residual, batch, seqlen, flags, workspace, false,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, const void* x_in,
+                              float* residual, int32_t batch, uint32_t flags, void* workspace, size_t ws_bytes,
+                              void* stream) {
+  ssm_status_t s = check_call(tp, w, st, x_in, residual, batch, 1, flags, workspace, ws_bytes);
+  if (s != SSM_OK) return s;
+  if (batch == 0) return SSM_OK;
+  PdlScope pdl(g_pdl_enabled);
+  return run_layer(tp, w, st, x_in, residual, batch, 1, flags, workspace, true,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
+  if (!tp || !partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
+  if (flags & ~(uint32_t)SSM_QAR_ACCUMULATE) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  const int blk = tp->cfg.qar_block;
+  if (n % blk) return fail(SSM_ERR_DIM, "n=%zu not a multiple of qar_block=%d", n, blk);
+  if ((reinterpret_cast<uintptr_t>(partial) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool acc = flags & SSM_QAR_ACCUMULATE;
+  if (n == 0) return SSM_OK;
+  if (tp->k == 1) {  // reading Q13: no quantisation at TP=1
+    Peers one{};
+    one.p[0] = const_cast<float*>(partial);
+    tp->launches++;
+    CU(launch_f32_reduce(one, 1, 0, (int64_t)n, out, acc, s));
+    return SSM_OK;
+  }
+  const size_t need = al256(n) + n / blk * 4;
+  if (need > half_bytes(tp)) return fail(SSM_ERR_ARG, "symmetric buffer too small for n=%zu", n);
+  const uint32_t ep = ++tp->epoch;
+  const size_t half = half_bytes(tp);
+  char* own = reinterpret_cast<char*>(tp->peers.p[tp->rank]) + kSigBytes + (ep & 1) * half;
+  const int64_t off = (int64_t)(kSigBytes + (ep & 1) * half);
+  tp->launches += 3;
+  CU(launch_quantize(partial, (int64_t)n, blk, reinterpret_cast<int8_t*>(own), reinterpret_cast<float*>(own + al256(n)), s));
+  tp->ar_count++;
+  tp->bytes_sent += n + n / blk * 4;
+  CU(launch_peer_barrier(tp->peers, tp->rank, tp->k, s));
+  CU(launch_qar_reduce(tp->peers, tp->k, off, off + (int64_t)al256(n), (int64_t)n, blk, out, acc, s));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_rmsnorm(ssm_tp_t tp, const float* residual, const float* weight, float eps, void* x_out, int64_t M,
+                         void* stream) {
+  PdlScope pdl(g_pdl_enabled && M <= 256);  // decode-sized rows: overlap with the neighbours
+  if (!tp || !residual || !x_out) return fail(SSM_ERR_ARG, "NULL argument");
+  if ((reinterpret_cast<uintptr_t>(residual) | reinterpret_cast<uintptr_t>(weight) | reinterpret_cast<uintptr_t>(x_out)) & 15)
+    return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
+  tp->launches++;
+  CU(launch_rmsnorm(tp->bf16, residual, weight, eps, x_out, M, tp->cfg.d_model, reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_check(ssm_tp_t tp, void* stream) {
+  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
+  CU(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+  if (tp->k > 1) {
+    uint32_t errw = 0;
+    CU(cudaMemcpy(&errw, reinterpret_cast<char*>(tp->peers.p[tp->rank]) + 64, 4, cudaMemcpyDeviceToHost));
+    if (errw) return fail(SSM_ERR_PROTOCOL, "peer flag wait timed out on rank %d (epoch %u)", tp->rank, tp->epoch);
+  }
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_stats(ssm_tp_t tp, int64_t* allreduce_count, int64_t* bytes_sent) {
+  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
+  if (allreduce_count) *allreduce_count = tp->ar_count;
+  if (bytes_sent) *bytes_sent = tp->bytes_sent;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches) {
+  if (!tp || !launches) return fail(SSM_ERR_ARG, "NULL argument");
+  *launches = tp->launches;
+  return SSM_OK;
+}
+
 ssm_status_t ssm_dbg_gemm(ssm_tp_t tp, const void* A, const void* B, float* C, int32_t M, int32_t N, int32_t K,
                           int32_t swap_ab, int32_t ksplit, void* stream) {
   return ssm_dbg_gemm_ld(tp, A, K, B, K, C, M, N, K, swap_ab, ksplit, stream);

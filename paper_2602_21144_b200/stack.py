@@ -98,17 +98,18 @@ class MixerStack:
         dist.all_reduce(pb, group=self.nccl)     # NCCL bf16 all-reduce (baseline arm)
         res.add_(pb.float())
 
-    def capture_decode(self, res_t, probes=()):
+    def capture_decode(self, res_t, probes=(), warmup=True):
         """Capture one decode step over all layers into a CUDA graph reading/writing res_t.
         The decode path is graph-safe: no host sync, fixed pointers; the all-reduce epoch
         counters live in device memory and advance on every replay, and each step issues an
         even number of collectives so the double-buffer halves alternate across replays."""
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            self.decode_step(res_t, s)   # warm-up (attribute setup outside capture)
-        torch.cuda.current_stream().wait_stream(s)
-        torch.cuda.synchronize()
+        if warmup:  # one eager step first (attribute setup outside capture); callers driving several
+            s = torch.cuda.Stream()  # virtual ranks on one device do their warm-ups themselves
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self.decode_step(res_t, s)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
         for kind, cap in probes:  # event nodes recorded inside the graph (see SSM_PROBE_IN_PROJ_DECODE)
             self.mx.probe(kind, cap)
         g = torch.cuda.CUDAGraph()

@@ -275,3 +275,46 @@ def test_rmsnorm_kernel():
     mx.rmsnorm(x.float().cuda(), y, w.float().cuda(), eps=1e-5)
     torch.cuda.synchronize()
     assert rel(y.cpu(), M.rmsnorm(x.numpy(), w.numpy(), 1e-5)) < 1e-6
+
+
+@pytest.mark.parametrize("k,mode", [(2, "int8"), (4, "fp32")])
+def test_virtual_tp_stack_prefill_then_graph_decode(k, mode):
+    """Two-layer pre-norm stack on k virtual ranks: eager chunked prefill, then decode steps
+    replayed from per-rank CUDA graphs (device-side AR epochs, alternating buffer halves)."""
+    from paper_2602_21144_b200.stack import MixerStack
+    dims = synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_layers=2)
+    B, L_in, L_out = 2, 12, 3
+    flags = L.SSM_AR2_INT8 if mode == "int8" else L.SSM_AR2_FP32
+    ws = [prep_weights(dims, l, "bf16") for l in range(2)]
+    g = torch.Generator().manual_seed(5)
+    res0 = torch.randn(B, L_in + L_out, dims.d_model, generator=g, dtype=torch.float64).float().double()
+    grp = VirtualGroup(dims, k, "bf16", B * L_in)
+    stacks = [MixerStack(grp.mixers[r], [LayerWeights(dims, w, k, r, "bf16") for w in ws], B, L_in, flags)
+              for r in range(k)]
+    pre = [res0[:, :L_in].float().cuda().contiguous().view(B * L_in, -1) for _ in range(k)]
+    rt = [torch.empty(B, dims.d_model, device="cuda") for _ in range(k)]
+    torch.cuda.synchronize()
+    grp.run(lambda r, mx, s: stacks[r].prefill_chunk(pre[r], s))
+    # graphs: capture each rank's decode step (capture does not execute, so no cross-rank wait)
+    graphs = []
+    for r in range(k):
+        with torch.cuda.stream(grp.streams[r]):
+            graphs.append(stacks[r].capture_decode(rt[r], warmup=False))
+    outs = [[] for _ in range(k)]
+    for t in range(L_in, L_in + L_out):
+        for r in range(k):
+            rt[r].copy_(res0[:, t].float().cuda())
+        torch.cuda.synchronize()
+        grp.run(lambda r, mx, s: graphs[r].replay())
+        for r in range(k):
+            outs[r].append(rt[r].cpu().clone())
+    for r in range(1, k):
+        assert torch.equal(pre[r].cpu(), pre[0].cpu())
+        for j in range(L_out):
+            assert torch.equal(outs[r][j], outs[0][j])
+    ref, _ = M.model_forward(dims, [np64(w) for w in ws], res0.numpy())
+    got_pre = pre[0].view(B, L_in, -1).cpu().double().numpy()
+    got_dec = torch.stack(outs[0], 1).double().numpy()
+    r0 = res0.numpy()
+    assert rel(got_pre - r0[:, :L_in], ref[:, :L_in] - r0[:, :L_in]) < TOL["bf16"]
+    assert rel(got_dec - r0[:, L_in:], ref[:, L_in:] - r0[:, L_in:]) < TOL["bf16"]
