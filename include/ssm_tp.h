@@ -191,7 +191,10 @@ ssm_status_t ssm_rmsnorm(ssm_tp_t tp, const float* residual, const float* weight
 
 /* Pre-tiled copy of a bf16 weight matrix [rows, cols] (row-major, nn.Linear layout) for the
  * decode GEMMs: 128 x 64 tiles, each one contiguous 16 KB block, ordered row-tile-major and
- * zero-padded to whole tiles.  out must be 128-B aligned and >= ssm_packed_weight_bytes bytes. */
+ * zero-padded to whole tiles; inside a tile, row r's eight 16-B chunks are stored in the
+ * SWIZZLE_128B order (chunk j at slot j ^ (r % 8)) so the tile is its own shared-memory image.
+ * The layout is private to this library (consume it only through w_*_pk).  out must be 128-B
+ * aligned and >= ssm_packed_weight_bytes bytes. */
 ssm_status_t ssm_packed_weight_bytes(int32_t rows, int32_t cols, size_t* bytes);
 ssm_status_t ssm_pack_weight(ssm_tp_t tp, const void* w, int32_t rows, int32_t cols, void* out, size_t out_bytes,
                              void* stream);
@@ -202,6 +205,12 @@ ssm_status_t ssm_tp_check(ssm_tp_t tp, void* stream);
 /* Collective counters: all-reduces issued by this handle, and the
  * bytes this rank wrote into its symmetric buffer for them. */
 ssm_status_t ssm_tp_stats(ssm_tp_t tp, int64_t* allreduce_count, int64_t* bytes_sent);
+
+/* Decode calls of this handle that ran the fused in_proj kernel (conv step and x_proj in the
+ * GEMM epilogue; taken for bf16 when no AR#1 separates x_proj from the scan, batch <= 32,
+ * P <= 256 and even, 2 <= K <= 4, 128 | channels per head; SSM_FUSE_DECODE=0 in the
+ * environment at ssm_tp_init disables it).  The other decode calls run the unfused chain. */
+ssm_status_t ssm_tp_fused_calls(ssm_tp_t tp, int64_t* calls);
 
 /* Kernel launches enqueued by this handle since creation (for bench.py gpu_launches). */
 ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches);
@@ -234,6 +243,10 @@ ssm_status_t ssm_dbg_gemm_ld(ssm_tp_t tp, const void* A, int64_t lda, const void
 ssm_status_t ssm_dbg_scan(ssm_tp_t tp, const void* u, const void* delta, const void* z, int32_t ldz,
                           const float* BC, const float* a_log, const float* d_skip, float* h,
                           void* g, int32_t batch, int32_t seqlen, void* stream);
+/* Copy `capacity` u64 of the GEMM kernel's experiment timeline (16 per CTA: globaltimer at
+ * entry, clock64 at entry, then clock64 offsets of pipeline events; written only when
+ * SSM_GEMM_NOMMA has bit 8 set when the GEMM is launched).  Synchronises the device. */
+ssm_status_t ssm_dbg_gemm_trace(uint64_t* out, int32_t capacity);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,7 @@ def _load():
         "ssm_tp_check": (st, [vp, vp]),
         "ssm_tp_stats": (st, [vp, P(i64), P(i64)]),
         "ssm_tp_launch_count": (st, [vp, P(i64)]),
+        "ssm_tp_fused_calls": (st, [vp, P(i64)]),
         "ssm_tp_probe": (st, [vp, i32, i32]),
         "ssm_tp_probe_read": (st, [vp, i32, P(C.c_float), i32, P(i32)]),
         "ssm_dbg_gemm": (st, [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]),
@@ -76,6 +77,7 @@ def _load():
         "ssm_dbg_gemm_packed": (st, [vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]),
         "ssm_dbg_gemm_ld": (st, [vp, vp, i64, vp, i64, vp, i32, i32, i32, i32, i32, vp]),
         "ssm_dbg_scan": (st, [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, i32, vp]),
+        "ssm_dbg_gemm_trace": (st, [vp, i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -88,8 +90,8 @@ LIB = _load()
 EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "ssm_comm_bytes", "ssm_workspace_bytes",
             "ssm_state_bytes", "ssm_state_alloc", "ssm_state_reset", "ssm_state_free", "ssm_mixer_prefill",
             "ssm_mixer_decode", "ssm_qallreduce", "ssm_rmsnorm", "ssm_tp_check", "ssm_tp_stats",
-            "ssm_tp_launch_count", "ssm_tp_probe", "ssm_tp_probe_read", "ssm_packed_weight_bytes", "ssm_pack_weight",
-            "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld", "ssm_dbg_scan"]
+            "ssm_tp_launch_count", "ssm_tp_fused_calls", "ssm_tp_probe", "ssm_tp_probe_read", "ssm_packed_weight_bytes", "ssm_pack_weight",
+            "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld", "ssm_dbg_scan", "ssm_dbg_gemm_trace"]
 PROBE = {"in_proj": 1, "conv": 2, "x_proj": 3, "dt_proj": 4, "scan": 5, "out_proj": 6, "ar2": 7, "decode_step": 8,
          "in_proj_decode": 9}
 

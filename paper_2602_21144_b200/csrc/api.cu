@@ -47,8 +47,11 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 // skip (1 in_proj, 2 conv, 4 x_proj, 8 decode_step, 16 out_proj).  Results are wrong when set.
 const int g_dbg_skip = [] { const char* e = getenv("SSM_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
 
-// Off by default: measured slightly slower on the Mamba-2.8B decode step (SSM_PDL=1 enables).
-const bool g_pdl_enabled = [] { const char* e = getenv("SSM_PDL"); return e && atoi(e) != 0; }();
+// On by default for decode-sized launches: every kernel calls griddepcontrol.launch_dependents at
+// entry and griddepcontrol.wait before touching memory a predecessor writes, so a successor's
+// launch and prologue overlap the predecessor's tail (measured 45.3 -> 42.2 us per Mamba-2.8B
+// decode layer with the fused in_proj).  SSM_PDL=0 disables.
+const bool g_pdl_enabled = [] { const char* e = getenv("SSM_PDL"); return !e || atoi(e) != 0; }();
 struct PdlScope {
   bool prev;
   explicit PdlScope(bool on) : prev(ssm::t_launch_pdl) { ssm::t_launch_pdl = on; }
@@ -70,6 +73,8 @@ struct ssm_tp_s {
   uint32_t epoch;
   int64_t ar_count, bytes_sent, launches;
   int num_sms;
+  int fuse_decode;        // fused decode in_proj (conv + x_proj in its epilogue); SSM_FUSE_DECODE=0 disables
+  int64_t fused_calls;    // decode calls that took the fused path
   // timing probes: one slot per kernel kind
   struct ProbeSlot {
     int cap = 0, n = 0;
@@ -85,6 +90,13 @@ struct ssm_state_s {
 };
 
 namespace {
+
+// The h buffer of a state is h [batch][E_k][N] fp32 followed by the fused decode path's x_proj
+// accumulator [batch][hloc*P] fp32, which is all-zero between decode calls: the decode in_proj
+// adds into it, decode_step reads it, out_proj's CTA 0 zeroes it again.
+size_t xacc_offset(const ssm_tp_s* t, int batch) {
+  return al256((size_t)batch * t->Ek * t->cfg.d_state * 4);
+}
 
 struct WsLayout {
   size_t xz, u, dbc, dlow, bc, delta, g, part, total;
@@ -177,11 +189,14 @@ struct Probe {
     if (cs != cudaStreamCaptureStatusNone && kind != SSM_PROBE_IN_PROJ_DECODE) return;
     slot = &p;
     idx = p.n++;
-    cudaEventRecord(p.ev[2 * idx], s);
+    // inside a capture, an externally observable event-record node needs cudaEventRecordExternal
+    flags = cs != cudaStreamCaptureStatusNone ? cudaEventRecordExternal : cudaEventRecordDefault;
+    cudaEventRecordWithFlags(p.ev[2 * idx], s, flags);
   }
   ~Probe() {
-    if (idx >= 0) cudaEventRecord(slot->ev[2 * idx + 1], s);
+    if (idx >= 0) cudaEventRecordWithFlags(slot->ev[2 * idx + 1], s, flags);
   }
+  unsigned int flags = cudaEventRecordDefault;
 };
 
 // split-K factor for a swap-AB decode GEMM with `rows` weight rows and reduction length K:
@@ -196,7 +211,7 @@ int split_for(const ssm_tp_s* t, int rows, int K) {
 }
 
 Epilogue epi(int kind, int trans, void* C, int64_t ldc, const float* bias = nullptr) {
-  Epilogue e;
+  Epilogue e{};
   e.kind = kind;
   e.trans = trans;
   e.C = C;
@@ -275,16 +290,38 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
 
   // (a1) in_proj, column-parallel: xz = x_in W_in,r^T   [M, 2E_k]
   const int skip = decode ? g_dbg_skip : 0;
+  // Fused decode (no AR#1 between x_proj and the scan): the in_proj epilogue also runs the conv
+  // step (a2) and adds its x_proj partial (a3) into the state's zeroed accumulator.
+  float* xacc = reinterpret_cast<float*>(reinterpret_cast<char*>(st->h) + xacc_offset(t, batch));
+  const bool fuse = swap && !ar1 && t->fuse_decode && batch <= 32 && P <= 256 && P % 2 == 0 && K >= 2 && K <= 4 &&
+                    t->cph % 128 == 0 && !(skip & 7) &&
+                    gemm_tc_supported(w->w_in, D, x_in, D);
   if (!(skip & 1)) {
     Probe pr(t, decode ? SSM_PROBE_IN_PROJ_DECODE : SSM_PROBE_IN_PROJ, s);
-    if (swap)
+    if (fuse) {
+      t->fused_calls++;
+      Epilogue e = epi(EPI_DECODE_INPROJ, 1, xz, 2 * Ek);
+      e.cst = st->conv;
+      e.cw = w->conv_w;
+      e.cb = w->conv_b;
+      e.u = u;
+      e.wx = w->w_x;
+      e.xacc = xacc;
+      e.Ek = Ek;
+      e.K = K;
+      e.P = P;
+      e.hl = hl;
+      e.cph = t->cph;
+      if (!oacc) { e.zero = odst; e.nzero = nD; }  // out_proj partial target (AR#2 follows)
+      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, e, s, true, w->w_in_pk));
+    } else if (swap)
       CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s, true, w->w_in_pk));
     else
       CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, epi(kst, 0, xz, 2 * Ek), s));
   }
 
   // (a2) conv1d + SiLU, rank-local; conv window of the cache updated
-  if (decode && !(skip & 2)) {
+  if (decode && !(skip & 2) && !fuse) {
     // split-K targets of x_proj / out_proj are zeroed by the conv kernel (one launch fewer)
     float* z0 = nullptr;
     int64_t n0 = 0;
@@ -306,7 +343,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   }
 
   // (a3) x_proj partial [M, hloc*P] fp32, straight into the symmetric buffer when AR#1 follows
-  if (!(skip & 4)) {
+  if (!(skip & 4) && !fuse) {
     Probe pr(t, SSM_PROBE_X_PROJ, s);
     if (swap)
       CU(gemm(t, w->w_x, Ek, u, Ek, hl * P, (int)M, Ek, ks_x,
@@ -326,7 +363,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     nsrc = t->ar1_group;
     doff = half_off(ep1);
   } else {
-    dsrc.p[0] = dbc;
+    dsrc.p[0] = fuse ? xacc : dbc;
   }
 
   if (decode) {
@@ -365,8 +402,11 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   // (a8) out_proj, row-parallel partial (TP=1: added straight into the fp32 residual)
   if (!(skip & 16)) {
     Probe pr(t, SSM_PROBE_OUT_PROJ, s);
-    if (swap)
-      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, epi(EPI_ATOMIC_F32, 1, odst, D), s, true, w->w_out_pk));
+    if (swap) {
+      Epilogue e = epi(EPI_ATOMIC_F32, 1, odst, D);
+      if (fuse) { e.zero = xacc; e.nzero = (int64_t)batch * hl * P; }  // re-arm the x_proj accumulator
+      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, e, s, true, w->w_out_pk));
+    }
     else
       CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D), s));
   }
@@ -463,6 +503,10 @@ ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp
   t->bf16 = cfg->dtype == SSM_BF16;
   t->es = t->bf16 ? 2 : 4;
   t->epoch = 0;
+  {
+    const char* e = getenv("SSM_FUSE_DECODE");
+    t->fuse_decode = e ? atoi(e) != 0 : 1;
+  }
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) {
     t->num_sms = sms;
@@ -545,7 +589,7 @@ ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, siz
   if (!tp || !conv_bytes || !h_bytes) return fail(SSM_ERR_ARG, "NULL argument");
   if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
   *conv_bytes = (size_t)batch * (tp->cfg.d_conv - 1) * tp->Ek * tp->es;
-  *h_bytes = (size_t)batch * tp->Ek * tp->cfg.d_state * 4;
+  *h_bytes = xacc_offset(tp, batch) + al256((size_t)batch * tp->hloc * tp->P * 4);
   return SSM_OK;
 }
 
@@ -673,6 +717,12 @@ ssm_status_t ssm_tp_stats(ssm_tp_t tp, int64_t* allreduce_count, int64_t* bytes_
   return SSM_OK;
 }
 
+ssm_status_t ssm_tp_fused_calls(ssm_tp_t tp, int64_t* calls) {
+  if (!tp || !calls) return fail(SSM_ERR_ARG, "NULL argument");
+  *calls = tp->fused_calls;
+  return SSM_OK;
+}
+
 ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches) {
   if (!tp || !launches) return fail(SSM_ERR_ARG, "NULL argument");
   *launches = tp->launches;
@@ -736,6 +786,13 @@ ssm_status_t ssm_dbg_scan(ssm_tp_t tp, const void* u, const void* delta, const v
   tp->launches++;
   CU(launch_scan(tp->bf16, tp->bf16, u, Ek, delta, Ek, z, ldz, BC, 2 * N, a_log, d_skip, h, (int64_t)Ek * N, g, Ek,
                  batch, seqlen, Ek, N, reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_dbg_gemm_trace(uint64_t* out, int32_t capacity) {
+  if (!out || capacity < 0) return fail(SSM_ERR_ARG, "NULL argument");
+  CU(cudaDeviceSynchronize());
+  CU(gemm_trace_read(reinterpret_cast<unsigned long long*>(out), capacity));
   return SSM_OK;
 }
 

@@ -86,6 +86,7 @@ cudaError_t preload_gemm_simt() {
 
 cudaError_t gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, int dtype_bf16, int M, int N, int K,
                       int ksplit, const Epilogue& epi, cudaStream_t s) {
+  if (epi.kind == EPI_DECODE_INPROJ || epi.zero) return cudaErrorInvalidValue;  // tcgen05 path only
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (ksplit < 1) ksplit = 1;
   int kper = (K + ksplit - 1) / ksplit;

@@ -45,8 +45,13 @@ struct CtaRes {
   int ring;          // bytes of the stage ring
   int tmem_cols;     // power of two >= 32
   int acc_stride;    // columns per accumulator
-  int nomma;         // experiment knob: skip the MMAs (TMA pipeline only)
+  int nomma;         // experiment knob (bits): 1 skip the MMAs, 2 skip the B loads, 4 skip the epilogue
+  int a_indep;       // A (weights) does not depend on the predecessor grid: first ring fill before the PDL wait
+  int nacc;          // interleaved partial accumulators per tile (k-step i -> slot i % nacc), summed by the
+                     // epilogue: independent MMA chains for skinny N, where one chain is MMA-latency bound
+  int slot_cols;     // TMEM columns per partial accumulator (>= BN, multiple of 32)
 };
+const bool kMinBN16 = [] { const char* e = getenv("SSM_GEMM_BN16"); return !e || atoi(e) != 0; }();
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane group)
 
 // Work decomposition.  Data-parallel mode: unit u = (k-split, m-tile, n-tile), CTAs stride
@@ -83,6 +88,9 @@ struct TileSched {
   }
   __device__ int first() const { return streamk ? -1 : (int)blockIdx.x; }
 };
+
+// partial accumulators actually written for a tile of (kb1 - kb0) k-blocks (4 UMMA k-steps each)
+__device__ __forceinline__ int tile_nacc(const CtaRes& cr, int kb0, int kb1) { return min(cr.nacc, 4 * (kb1 - kb0)); }
 
 // Epilogue for one warp's 32 x 32 chunk: lane = row m0 + lane, columns n0..n0+31, stored
 // straight from registers (staging through shared memory would compete with the UMMA operand
@@ -123,20 +131,33 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
     }
   }
   if (e.trans) {
-    // element (m, n) -> C[n * ldc + m]; lanes hold consecutive m -> coalesced per n
+    // element (m, n) -> C[n * ldc + m]; lanes hold consecutive m -> coalesced per n.  One loop per
+    // kind (no per-element dispatch), valid columns first so all stores issue back to back.
+    const int nv = min(32, N - n0);
+    if (kind == EPI_STORE_BF16 || kind == EPI_SOFTPLUS_BF16) {
+      __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(e.C) + (int64_t)n0 * e.ldc + m;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int n = n0 + j;
-      if (n >= N) continue;
-      const int64_t idx = (int64_t)n * e.ldc + m;
-      switch (kind) {
-        case EPI_STORE_BF16:
-        case EPI_SOFTPLUS_BF16: reinterpret_cast<__nv_bfloat16*>(e.C)[idx] = __float2bfloat16_rn(v[j]); break;
-        case EPI_STORE_F32:
-        case EPI_SOFTPLUS_F32: reinterpret_cast<float*>(e.C)[idx] = v[j]; break;
-        case EPI_ADD_F32: reinterpret_cast<float*>(e.C)[idx] += v[j]; break;
-        default: atomicAdd(reinterpret_cast<float*>(e.C) + idx, v[j]);
-      }
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) C[(int64_t)j * e.ldc] = __float2bfloat16_rn(v[j]);
+    } else if (kind == EPI_STORE_F32 || kind == EPI_SOFTPLUS_F32) {
+      float* C = reinterpret_cast<float*>(e.C) + (int64_t)n0 * e.ldc + m;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) C[(int64_t)j * e.ldc] = v[j];
+    } else if (kind == EPI_ADD_F32) {
+      float* C = reinterpret_cast<float*>(e.C) + (int64_t)n0 * e.ldc + m;
+      float o[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) o[j] = C[(int64_t)j * e.ldc];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) C[(int64_t)j * e.ldc] = o[j] + v[j];
+    } else {
+      float* C = reinterpret_cast<float*>(e.C) + (int64_t)n0 * e.ldc + m;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) atomicAdd(C + (int64_t)j * e.ldc, v[j]);
     }
     return;
   }
@@ -203,9 +224,167 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
   }
 }
 
+// ---- EPI_DECODE_INPROJ: decode in_proj epilogue fused with the conv step and x_proj ----------
+// Epilogue warp w (0..7) owns TMEM lane group eg = w % 4 (feature rows f0 + 32 eg + lane) and the
+// batch columns [16 half, 16 half + 16) (half = w / 4), so a CTA covers N <= 32 decode tokens.
+constexpr int SU_LD = 136;                       // u tile row pitch (bf16): conflict-free ldmatrix
+constexpr int SU_BYTES = 32 * SU_LD * 2;         // u tile [32 tokens][128 channels] bf16
+constexpr int XP_NT = 4;                         // x_proj n-tiles (8 outputs) per warp: P <= 256
+
+__device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const TileSched& ts, int M, int N,
+                                                       uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
+                                                       const CtaRes& cr, __nv_bfloat16* su) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int eg = warp & 3, half = (warp - 2) >> 2, ew = warp - 2;
+  const int Ek = e.Ek, K = e.K, P = e.P, ldx = e.hl * e.P;
+  __nv_bfloat16* cst = reinterpret_cast<__nv_bfloat16*>(e.cst);
+  const __nv_bfloat16* wx = reinterpret_cast<const __nv_bfloat16*>(e.wx);
+  int acc = 0;
+  uint32_t acc_ph = 0;
+  int cur = ts.first(), mt, nt, kb0, kb1;
+  while (ts.next(cur, mt, nt, kb0, kb1)) {
+    if (kb0 >= kb1) continue;
+    const int f0 = mt * BM;
+    const int f = f0 + eg * 32 + lane;
+    const bool is_x = f < Ek;
+    const bool tile_x = f0 < Ek;
+    // ---- loads that do not depend on the GEMM, issued while the weight stream is in flight
+    float wv[4] = {0.f, 0.f, 0.f, 0.f}, bias = 0.f;
+    uint32_t win[3][8];  // cached window, bf16 pairs (tokens 2i, 2i+1 of this warp's 16)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) win[j][q] = 0u;
+    if (is_x) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < K) wv[j] = e.cw[(int64_t)f * K + j];
+      bias = e.cb[f];
+      const uint16_t* cs16 = reinterpret_cast<const uint16_t*>(cst);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int b = half * 16 + q;
+        if (b < N)
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (j < K - 1) win[j][q / 2] |= (uint32_t)cs16[((int64_t)b * (K - 1) + j) * Ek + f] << (16 * (q & 1));
+      }
+    }
+    uint32_t wf[XP_NT][8][2];  // W_x B-fragments: rows p = 8 nt + lane / 4, cols f0 + 16 ks + 2 (lane % 4) (+8)
+    const int hd = f0 / e.cph;
+    if (tile_x) {
+#pragma unroll
+      for (int i = 0; i < XP_NT; ++i) {
+        const int p = (ew + 8 * i) * 8 + lane / 4;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const int fc = f0 + ks * 16 + 2 * (lane & 3);
+          const __nv_bfloat16* row = wx + (int64_t)(hd * P + p) * Ek;
+          wf[i][ks][0] = (p < P && fc < Ek) ? *reinterpret_cast<const uint32_t*>(row + fc) : 0u;
+          wf[i][ks][1] = (p < P && fc + 8 < Ek) ? *reinterpret_cast<const uint32_t*>(row + fc + 8) : 0u;
+        }
+      }
+    }
+    // ---- accumulator: 16 token columns of this warp's 32 feature rows
+    mbar_wait(&tfull[acc], acc_ph);
+    tc_fence_after();
+    uint32_t r[16];
+    const uint32_t tb = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * cr.acc_stride + half * 16);
+    tmem_ld_32x32b_x16(tb, r);
+    tmem_ld_wait();
+    for (int q = 1; q < tile_nacc(cr, kb0, kb1); ++q) {  // fold the interleaved partial accumulators
+      uint32_t r2[16];
+      tmem_ld_32x32b_x16(tb + (uint32_t)(q * cr.slot_cols), r2);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM consumed: the MMA warp may reuse it
+    if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+
+    __nv_bfloat16* su_col = su + (f - f0);
+    if (is_x) {
+      // causal conv step (tap K-1 = current token) + SiLU; window shift
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int b = half * 16 + q;
+        float uq = 0.f;
+        if (b < N) {
+          const float x = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[q])));
+          float a = bias;
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (j < K - 1) a = fmaf(wv[j], __uint_as_float((win[j][q / 2] >> (16 * (q & 1))) << 16), a);
+          float wl = wv[1];
+#pragma unroll
+          for (int j = 2; j < 4; ++j)
+            if (j == K - 1) wl = wv[j];
+          a = fmaf(wl, x, a);
+          const __nv_bfloat16 ub = __float2bfloat16_rn(silu<true>(a));
+          reinterpret_cast<__nv_bfloat16*>(e.u)[(int64_t)b * Ek + f] = ub;
+          uq = __bfloat162float(ub);
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (j < K - 2)
+              reinterpret_cast<uint16_t*>(cst)[((int64_t)b * (K - 1) + j) * Ek + f] =
+                  (uint16_t)(win[j + 1][q / 2] >> (16 * (q & 1)));
+          cst[((int64_t)b * (K - 1) + (K - 2)) * Ek + f] = __float2bfloat16_rn(x);
+        }
+        su_col[b * SU_LD] = __float2bfloat16_rn(uq);
+      }
+    } else {
+      if (f < M) {
+        __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(e.C) + f;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int b = half * 16 + q;
+          if (b < N) C[(int64_t)b * e.ldc] = __float2bfloat16_rn(__uint_as_float(r[q]));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) su_col[(half * 16 + q) * SU_LD] = __float2bfloat16_rn(0.f);
+    }
+    named_bar_sync(1, 256);
+    if (tile_x) {
+      // x_proj partial of this tile's 128 channels: xacc[b][hd P + p] += sum_f u[b][f] W_x[hd P + p][f]
+      for (int mi = 0; mi * 16 < N; ++mi) {
+        uint32_t a[8][4];
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          ldmatrix_x4(a[ks], su + (mi * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * SU_LD + ks * 16 + (lane >> 4) * 8);
+#pragma unroll
+        for (int i = 0; i < XP_NT; ++i) {
+          const int p0 = (ew + 8 * i) * 8;
+          if (p0 >= P) continue;
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) mma_16816_bf16(d, a[ks], wf[i][ks][0], wf[i][ks][1]);
+          const int p = p0 + 2 * (lane & 3);
+          const int b = mi * 16 + lane / 4;
+          if (p < P) {
+            if (b < N) red_add_v2(e.xacc + (int64_t)b * ldx + hd * P + p, d[0], d[1]);
+            if (b + 8 < N) red_add_v2(e.xacc + (int64_t)(b + 8) * ldx + hd * P + p, d[2], d[3]);
+          }
+        }
+      }
+    }
+    named_bar_sync(1, 256);  // u tile free for the next tile
+  }
+}
+
+// Experiment-only timeline (cr.nomma & 8): per-CTA clock64 offsets of pipeline events.
+constexpr int kTraceSlots = 16, kTraceCtas = 1024;
+__device__ unsigned long long g_trace[kTraceCtas * kTraceSlots];
+#define TRACE(slot, val)                                                                   \
+  do {                                                                                     \
+    if ((cr.nomma & 8) && blockIdx.x < kTraceCtas) g_trace[blockIdx.x * kTraceSlots + (slot)] = (val); \
+  } while (0)
+
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_pf, int64_t lda, int K,
+                   int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_blk, int64_t lda, int K,
                    CtaRes cr, int a_blocked) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -222,10 +401,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const long long c_start = clock64();
+  if (threadIdx.x == 0) { TRACE(0, globaltimer()); TRACE(1, c_start); }
   pdl_trigger();
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
+    if (!a_blocked) tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -242,111 +423,180 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(2, clock64() - c_start);
 
   if (warp == 0) {
-    // A is the weight operand (swap-AB decode): stream this CTA's whole A range into L2 as long
-    // contiguous row segments (DRAM-friendly) while the predecessor kernel finishes
-    if (a_pf) {
-      int cur = ts.first(), mt, nt, kb0, kb1;
-      while (ts.next(cur, mt, nt, kb0, kb1)) {
-        const int c0 = kb0 * BK;
-        const int c1 = min(K, kb1 * BK);
-        if (c1 <= c0) continue;
-        for (int r = mt * BM + lane; r < min(M, mt * BM + BM); r += 32)
-          prefetch_l2(a_pf + (int64_t)r * lda + c0, (uint32_t)(c1 - c0) * 2);
-      }
-    }
-    pdl_wait();
     if (lane == 0) {
       // ---------------- TMA producer
-      int stage = 0;
+      const uint32_t stage_tx = (uint32_t)((cr.nomma & 2) ? BM : BM + BN) * BK * 2;  // per k-block
+      auto issue_a = [&](uint8_t* st, uint64_t* bar, int mt, int kb, int nk) {
+        if (a_blocked)  // A pre-tiled AND pre-swizzled: the nk blocks (mt, kb..kb+nk) are one
+          // contiguous run of nk x 16 KB whose bytes are already the SW128 smem image -> 1D bulk copy
+          bulk_load_evict_first(st, a_blk + ((int64_t)mt * ts.kb_total + kb) * (BM * BK), (uint32_t)nk * A_STAGE, bar);
+        else
+          for (int j = 0; j < nk; ++j) tma_load_2d(st + j * A_STAGE, &tmA, bar, (kb + j) * BK, mt * BM);
+      };
+      auto issue_b = [&](uint8_t* st, uint64_t* bar, int nt, int kb, int nk) {
+        if (!(cr.nomma & 2))
+          for (int j = 0; j < nk; ++j) tma_load_2d(st + BOFF + j * BSUB, &tmB, bar, (kb + j) * BK, nt * BN);
+      };
+      // A independent of the predecessor grid (weights): arm the first ring fill and issue its A
+      // loads BEFORE griddepcontrol.wait, so the weight stream starts while the predecessor drains.
+      int n_pre = 0;
+      if (cr.a_indep) {
+        int cur = ts.first(), mt, nt, kb0, kb1;
+        while (n_pre < STAGES && ts.next(cur, mt, nt, kb0, kb1))
+          for (int kb = kb0; kb < kb1 && n_pre < STAGES; kb += KBS, ++n_pre) {
+            const int nk = min(KBS, kb1 - kb);
+            mbar_arrive_expect_tx(&full[n_pre], (uint32_t)nk * stage_tx);
+            issue_a(ring + n_pre * SB, &full[n_pre], mt, kb, nk);
+          }
+      }
+      pdl_wait();
+      int stage = 0, g = 0;
       uint32_t ph = 0;
       int cur = ts.first(), mt, nt, kb0, kb1;
       while (ts.next(cur, mt, nt, kb0, kb1)) {
-        for (int kb = kb0; kb < kb1; kb += KBS) {
+        for (int kb = kb0; kb < kb1; kb += KBS, ++g) {
           const int nk = min(KBS, kb1 - kb);
-          mbar_wait(&empty[stage], ph ^ 1);
-          mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * (BM + BN) * BK * 2);
           uint8_t* st = ring + stage * SB;
-          if (a_blocked)  // A pre-tiled: block (mt, kb) is one contiguous 16 KB box
-            for (int j = 0; j < nk; ++j)
-              tma_load_3d(st + j * A_STAGE, &tmA, &full[stage], 0, 0, mt * ts.kb_total + kb + j);
-          else
-            for (int j = 0; j < nk; ++j) tma_load_2d(st + j * A_STAGE, &tmA, &full[stage], (kb + j) * BK, mt * BM);
-          for (int j = 0; j < nk; ++j) tma_load_2d(st + BOFF + j * BSUB, &tmB, &full[stage], (kb + j) * BK, nt * BN);
+          if (g >= n_pre) {
+            mbar_wait(&empty[stage], ph ^ 1);
+            if (kb == kb0) TRACE(3, clock64() - c_start);
+            mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * stage_tx);
+            issue_a(st, &full[stage], mt, kb, nk);
+          }
+          issue_b(st, &full[stage], nt, kb, nk);
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
       }
+    } else {
+      pdl_wait();
     }
   } else if (warp == 1) {
     pdl_wait();
-    if (lane == 0) {
-      // ---------------- MMA issuer (single thread)
-      const uint32_t idesc = umma_idesc_bf16(BM, BN);
-      int stage = 0;
-      uint32_t ph = 0;
-      int acc = 0;
-      uint32_t acc_ph = 0;
-      int cur = ts.first(), mt, nt, kb0, kb1;
-      while (ts.next(cur, mt, nt, kb0, kb1)) {
-        if (kb0 >= kb1) continue;
-        mbar_wait(&tempty[acc], acc_ph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + (uint32_t)(acc * cr.acc_stride);
-        for (int kb = kb0; kb < kb1; kb += KBS) {
-          const int nk = min(KBS, kb1 - kb);
-          mbar_wait(&full[stage], ph);
-          tc_fence_after();
-          const uint32_t s0 = smem_u32(ring + stage * SB);
-          for (int j = 0; j < nk; ++j) {
-            const uint32_t a0 = s0 + j * A_STAGE;
-            const uint32_t b0 = s0 + BOFF + j * BSUB;
-            if (!cr.nomma) {
-#pragma unroll
-              for (int k = 0; k < BK / 16; ++k) {
-                umma_bf16(d, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                          (kb > kb0 || j > 0 || k > 0) ? 1u : 0u);
-              }
-            }
-          }
-          umma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; ph ^= 1; }
-        }
-        umma_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
-      }
-    }
-  } else {
-    // ---------------- epilogue warps 2..9; TMEM lane group = warp % 4, column half = (warp-2)/4
-    pdl_wait();
-    const int eg = warp & 3;
-    const int half = (warp - 2) >> 2;
+    // ---------------- MMA issuer: the whole warp runs the (warp-uniform) schedule so the UMMA
+    // descriptors live in uniform registers; one elected lane issues the tcgen05.mma / commits.
+    // (A single-lane loop makes ptxas wrap every UMMA in a uniform-broadcast waterfall loop,
+    // ~100 cycles per instruction: that, not the tensor pipe, bounded skinny weight streams.)
+    const uint32_t idesc = umma_idesc_bf16(BM, BN);
+    const uint64_t ring_desc = umma_desc_sw128(smem_u32(ring));  // + (byte offset >> 4) addresses inside the ring
+    int stage = 0;
+    uint32_t ph = 0;
     int acc = 0;
     uint32_t acc_ph = 0;
     int cur = ts.first(), mt, nt, kb0, kb1;
     while (ts.next(cur, mt, nt, kb0, kb1)) {
       if (kb0 >= kb1) continue;
+      mbar_wait(&tempty[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + (uint32_t)(acc * cr.acc_stride);
+      const int na = tile_nacc(cr, kb0, kb1);
+      int slot = 0, ki = 0;  // partial accumulator of the next k-step; k-steps issued in this tile
+      for (int kb = kb0; kb < kb1; kb += KBS) {
+        const int nk = min(KBS, kb1 - kb);
+        mbar_wait(&full[stage], ph);
+        if (lane == 0 && kb == kb0) TRACE(4, clock64() - c_start);
+        if (lane == 0 && kb + KBS >= kb1) TRACE(5, clock64() - c_start);
+        tc_fence_after();
+        const uint64_t a_desc = ring_desc + (uint64_t)((stage * SB) >> 4);
+        const uint64_t b_desc = a_desc + (uint64_t)(BOFF >> 4);
+        if (elect_one()) {
+          if (!(cr.nomma & 1)) {
+            for (int j = 0; j < nk; ++j) {
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k) {
+                umma_bf16(d + (uint32_t)(slot * cr.slot_cols), a_desc + (uint64_t)((j * A_STAGE + k * 32) >> 4),
+                          b_desc + (uint64_t)((j * BSUB + k * 32) >> 4), idesc, ki >= na ? 1u : 0u);
+                ++ki;
+                if (++slot == na) slot = 0;
+              }
+            }
+          }
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; ph ^= 1; }
+      }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (lane == 0) TRACE(6, clock64() - c_start);
+      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+    }
+  } else {
+    // ---------------- epilogue warps 2..9; TMEM lane group = warp % 4, column half = (warp-2)/4
+    pdl_wait();
+    if (epi.zero && blockIdx.x == 0) {
+      const int64_t n4 = epi.nzero / 4;
+      for (int64_t i = threadIdx.x - 64; i < n4; i += kThreads - 64)
+        reinterpret_cast<float4*>(epi.zero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t i = 4 * n4 + threadIdx.x - 64; i < epi.nzero; i += kThreads - 64) epi.zero[i] = 0.f;
+    }
+    if (epi.kind == EPI_DECODE_INPROJ) {
+      decode_inproj_epilogue(epi, ts, M, N, tfull, tempty, tmem_base, cr,
+                             reinterpret_cast<__nv_bfloat16*>(smem + cr.ring + 512));
+      goto teardown;
+    }
+    {
+    const int eg = warp & 3;
+    const int half = (warp - 2) >> 2;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    int cur = ts.first(), mt, nt, kb0, kb1;
+    if (!(cr.nomma & 16) && lane == 0) {
+      // Touch the first output address now: a TLB miss on a store would otherwise stall the
+      // epilogue for microseconds after the weight stream (page walks queue behind it).
+      int c2 = cur, mt2, nt2, k0, k1;
+      if (ts.next(c2, mt2, nt2, k0, k1)) {
+        const int m = min(M - 1, mt2 * BM + eg * 32), n = min(N - 1, nt2 * BN);
+        const int64_t idx = epi.trans ? (int64_t)n * epi.ldc + m : (int64_t)m * epi.ldc + n;
+        const int esz = (epi.kind == EPI_STORE_BF16 || epi.kind == EPI_SOFTPLUS_BF16) ? 2 : 4;
+        touch_global(reinterpret_cast<const uint8_t*>(epi.C) + idx * esz);
+        if (epi.bias) touch_global(epi.bias + (epi.trans ? m : n));
+      }
+    }
+    while (ts.next(cur, mt, nt, kb0, kb1)) {
+      if (kb0 >= kb1) continue;
       mbar_wait(&tfull[acc], acc_ph);
+      if (threadIdx.x == 64) TRACE(7, clock64() - c_start);
       tc_fence_after();
       const int m0 = mt * BM + eg * 32;
       const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * cr.acc_stride);
-      for (int c = half; c < BN / 32; c += 2) {
+      const int na = tile_nacc(cr, kb0, kb1);
+      for (int c = half; c < (BN + 31) / 32; c += 2) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tbase + c * 32, r);
         tmem_ld_wait();
-        epi_chunk(epi, m0, nt * BN + c * 32, M, N, r);
+        for (int q = 1; q < na; ++q) {  // fold the interleaved partial accumulators
+          uint32_t r2[32];
+          tmem_ld_32x32b_x32(tbase + (uint32_t)(q * cr.slot_cols) + c * 32, r2);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
+        }
+        if ((cr.nomma & 8) && threadIdx.x == 64) {  // timestamp after the TMEM data has arrived
+          uint32_t dep;
+          asm volatile("add.u32 %0, %1, %2;" : "=r"(dep) : "r"(r[0]), "r"(r[31]));
+          TRACE(8, clock64() - c_start + (dep == 0x7f123456u ? 1 : 0));
+        }
+        if (!(cr.nomma & 4)) epi_chunk(epi, m0, nt * BN + c * 32, M, N, r);
       }
+      if (threadIdx.x == 64) TRACE(9, clock64() - c_start);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
+    }
   }
+teardown:
+  if (threadIdx.x == 0) TRACE(10, clock64() - c_start);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, cr.tmem_cols);
+    if (lane == 0) { TRACE(11, clock64() - c_start); TRACE(12, globaltimer()); }
   }
 }
 
@@ -380,30 +630,20 @@ bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int
   return r == CUDA_SUCCESS;
 }
 // Blocked ("pre-tiled") weight layout: block (r / 128, k / 64) of 128 x 64 bf16 stored as one
-// contiguous 16 KB row-major tile; blocks ordered row-tile-major.  TMA views it as a 3D tensor
-// {64, 128, n_blocks} so every box is one contiguous 16 KB read (sequential weight streams).
-bool make_map_blocked(CUtensorMap* map, const void* ptr, int64_t n_blocks) {
-  PFN_encodeTiled enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)BK, (cuuint64_t)BM, (cuuint64_t)n_blocks};
-  cuuint64_t strides[2] = {(cuuint64_t)(BK * 2), (cuuint64_t)(BK * BM * 2)};
-  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)BM, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
+// contiguous 16 KB tile, blocks ordered row-tile-major, and each tile stored in the SWIZZLE_128B
+// byte order UMMA reads from shared memory (16-B chunk j of row r at position j ^ (r % 8)).  A
+// weight-streaming decode GEMM then fetches KBS consecutive k-blocks as ONE 1D bulk copy with
+// no tensor-map address generation; the smem image is byte-identical to what a swizzling 2D
+// TMA load of the row-major matrix would produce.
 __global__ void pack_blocked_kernel(const __nv_bfloat16* __restrict__ w, int rows, int cols, int64_t ld,
                                     __nv_bfloat16* __restrict__ out, int kbt, int64_t n_vec) {
   // one thread per 16-B output vector (8 bf16); zero padding beyond rows / cols
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_vec; v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = v * 8;
-    const int64_t blk = e / (BM * BK);
-    const int within = (int)(e % (BM * BK));
-    const int r = (int)(blk / kbt) * BM + within / BK;
-    const int k = (int)(blk % kbt) * BK + within % BK;
+    const int64_t blk = v / (BM * BK / 8);
+    const int c = (int)(v % (BM * BK / 8));  // 16-B chunk within the tile: row c / 8, slot c % 8
+    const int rr = c >> 3;
+    const int r = (int)(blk / kbt) * BM + rr;
+    const int k = (int)(blk % kbt) * BK + (((c & 7) ^ (rr & 7)) << 3);
     uint4 val = make_uint4(0, 0, 0, 0);
     if (r < rows) {
       if (k + 8 <= cols && ((ld * 2) % 16 == 0)) {
@@ -431,6 +671,11 @@ cudaError_t pack_blocked(const __nv_bfloat16* w, int rows, int cols, int64_t ld,
   return cudaGetLastError();
 }
 
+cudaError_t gemm_trace_read(unsigned long long* host, int n) {
+  if (n > kTraceCtas * kTraceSlots) n = kTraceCtas * kTraceSlots;
+  return cudaMemcpyFromSymbol(host, g_trace, (size_t)n * sizeof(unsigned long long));
+}
+
 cudaError_t preload_gemm_tc() {
   cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
@@ -444,7 +689,7 @@ bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb) {
 }
 
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
-                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool prefetch_a,
+                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool a_indep,
                          const __nv_bfloat16* A_blocked) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   const int ksplit_in = ksplit;
@@ -452,7 +697,8 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   // 32-column chunks) covering N in as few tiles as possible
   int n_tiles = (N + BN_MAX - 1) / BN_MAX;
   int BN = (N + n_tiles - 1) / n_tiles;
-  BN = (BN + 31) / 32 * 32;
+  // (N <= 16: one 16-column UMMA tile -- decode batches -- halves the B operand and its smem)
+  BN = (BN <= 16 && kMinBN16) ? 16 : (BN + 31) / 32 * 32;
   n_tiles = (N + BN - 1) / BN;
   TileSched ts;
   ts.m_tiles = (M + BM - 1) / BM;
@@ -473,12 +719,13 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   if ((ts.ksplit > 1 || ts.streamk) && epi.kind != EPI_ATOMIC_F32) return cudaErrorInvalidValue;
 
   CUtensorMap ma, mb;
+  if (!make_map(&mb, B, N, K, ldb, BN)) return cudaErrorInvalidValue;
   if (A_blocked) {
-    if (!make_map_blocked(&ma, A_blocked, (int64_t)ts.m_tiles * ts.kb_total)) return cudaErrorInvalidValue;
+    if ((reinterpret_cast<uintptr_t>(A_blocked) & 127) != 0) return cudaErrorInvalidValue;
+    ma = mb;  // unused: A is fetched by 1D bulk copies
   } else if (!make_map(&ma, A, M, K, lda, BM)) {
     return cudaErrorInvalidValue;
   }
-  if (!make_map(&mb, B, N, K, ldb, BN)) return cudaErrorInvalidValue;
 
   static bool attr_set = false;
   if (!attr_set) {
@@ -495,6 +742,12 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   cr.acc_stride = BN_MAX;
   cr.tmem_cols = 512;
   cr.nomma = 0;
+  cr.a_indep = a_indep ? 1 : 0;
+  cr.slot_cols = (BN + 31) / 32 * 32;
+  cr.nacc = 1;  // measured: no gain from interleaved accumulators once the UMMA issue is warp-uniform
+  if (const char* env = getenv("SSM_GEMM_NACC")) cr.nacc = atoi(env);
+  if (cr.nacc < 1) cr.nacc = 1;
+  while (cr.nacc > 1 && cr.nacc * cr.slot_cols > cr.acc_stride) --cr.nacc;
   if (const char* env = getenv("SSM_GEMM_NOMMA")) cr.nomma = atoi(env);
   if (const char* env = getenv("SSM_GEMM_RING_KB")) {  // experiment: smaller CTA footprint
     cr.ring = atoi(env) * 1024;
@@ -502,9 +755,21 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     while (cols < 2 * BN) cols *= 2;
     cr.tmem_cols = cols;
     cr.acc_stride = cols / 2;
+    cr.nacc = 1;
   }
+  int extra = 0;
+  if (epi.kind == EPI_DECODE_INPROJ) {
+    // fused decode in_proj: one 32-column accumulator per tile, N <= 32 tokens, P <= 256 (even),
+    // tiles inside one head, window of <= 3 cached taps
+    if (!epi.trans || N > 32 || BN > 32 || epi.P > 8 * 8 * XP_NT || (epi.P & 1) || epi.K < 2 || epi.K > 4 ||
+        epi.cph % BM || M != 2 * epi.Ek || ts.ksplit != 1 || ts.streamk)
+      return cudaErrorInvalidValue;
+    extra = SU_BYTES;
+    cr.ring -= SU_BYTES;
+  }
+  if (epi.zero && (reinterpret_cast<uintptr_t>(epi.zero) & 15)) return cudaErrorInvalidValue;
   while (kbs > 1 && num_stages(BN, kbs, cr.ring) < 2) --kbs;
-  const int smem_bytes = 1024 + cr.ring + 512;
+  const int smem_bytes = 1024 + cr.ring + 512 + extra;
   int grid = ts.units < num_sms ? ts.units : num_sms;
   if (ts.streamk) {
     long long cap = num_sms;
@@ -513,7 +778,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     grid = (int)(W < cap ? W : cap);
   }
   { cudaError_t e_ = launch(gemm_tc_kernel, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi,
-                                      prefetch_a && !A_blocked && ((lda * 2) % 16 == 0) && (K % 8 == 0) ? A : nullptr,
+                                      A_blocked,
                                       lda, K, cr, A_blocked ? 1 : 0); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }

@@ -18,6 +18,7 @@ enum EpiKind : int {
   EPI_SOFTPLUS_F32 = 3,   // C f32  = softplus(acc + bias[feature])
   EPI_ADD_F32 = 4,        // C f32 += acc            (read-modify-write; ksplit must be 1)
   EPI_ATOMIC_F32 = 5,     // C f32 += acc atomically (split-K; C pre-initialised)
+  EPI_DECODE_INPROJ = 6,  // decode in_proj (swap-AB, bf16, N = batch <= 32), fused conv + x_proj; see below
 };
 
 struct Epilogue {
@@ -26,6 +27,22 @@ struct Epilogue {
   void* C;
   int64_t ldc;
   const float* bias;  // indexed by the output feature: n (trans=0) or m (trans=1)
+  // Any kind: CTA 0 zero-fills zero[0, nzero) floats (16-B aligned) before its first tile -- a
+  // buffer a LATER kernel accumulates into (saves a memset launch on the decode path).
+  float* zero;
+  int64_t nzero;
+  // EPI_DECODE_INPROJ (SURVEY.md §8 rows a1-a3 fused for one decode token).
+  // Output rows m are in_proj features: m < Ek are x channels -> causal conv step over the cached
+  // window cst + SiLU -> u (bf16 [N][Ek]) and the window shifted in place; Ek <= m < 2Ek are z
+  // -> C[n * ldc + m] (bf16).  The CTA then contracts its 128 u channels with the matching
+  // columns of W_x (mma.sync) and adds the partial x_proj [N][hl*P] into xacc (pre-zeroed).
+  void* cst;                  // [N][K-1][Ek] bf16
+  const float* cw;            // [Ek][K]
+  const float* cb;            // [Ek]
+  void* u;                    // [N][Ek] bf16
+  const void* wx;             // [hl*P][Ek] bf16 (block-diagonal over local heads)
+  float* xacc;                // [N][hl*P] fp32
+  int Ek, K, P, hl, cph;
 };
 
 struct Peers {
@@ -36,13 +53,15 @@ struct Peers {
 // tcgen05/TMEM/TMA bf16 GEMM: A [M,K] row stride lda, B [N,K] row stride ldb (elements).
 // ksplit > 1: data-parallel split-K; ksplit < 0: stream-K over all SMs (both need EPI_ATOMIC_F32).
 // Requires lda*2 % 16 == 0, ldb*2 % 16 == 0, 16-B aligned bases.
-// prefetch_a: A is a weight (independent of the predecessor kernel): bulk-prefetch each CTA's A
-// rows into L2 before griddepcontrol.wait.
+// a_indep: A is a weight (independent of the predecessor kernel): under PDL the producer issues
+// the first ring fill of A before griddepcontrol.wait.
 // A_blocked: optional copy of A in the blocked layout (pack_blocked); TMA then reads contiguous
 // 16 KB boxes (sequential weight streams for the decode GEMMs).
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
-                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool prefetch_a = false,
+                         int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool a_indep = false,
                          const __nv_bfloat16* A_blocked = nullptr);
+// experiment-only: copy the GEMM timeline buffer (16 u64 per CTA, SSM_GEMM_NOMMA bit 8)
+cudaError_t gemm_trace_read(unsigned long long* host, int n);
 size_t packed_blocked_bytes(int rows, int cols);
 cudaError_t pack_blocked(const __nv_bfloat16* w, int rows, int cols, int64_t ld, __nv_bfloat16* out, cudaStream_t s);
 bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb);

@@ -183,6 +183,12 @@ class TPMixer:
         L.call("ssm_tp_stats", self.handle, C.byref(a), C.byref(b))
         return {"allreduce": a.value, "bytes_sent": b.value}
 
+    def fused_calls(self):
+        """Decode calls that ran the fused in_proj (+conv +x_proj) kernel."""
+        n = C.c_int64()
+        L.call("ssm_tp_fused_calls", self.handle, C.byref(n))
+        return n.value
+
     def launches(self):
         n = C.c_int64()
         L.call("ssm_tp_launch_count", self.handle, C.byref(n))

@@ -34,4 +34,4 @@ e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1000 / 20 / nl
 print(f"{cfg} skip={os.environ.get('SSM_DEBUG_SKIP', '0')} skipnorm={os.environ.get('SSM_DEBUG_SKIP_NORM', '0')} "
-      f"pdl={os.environ.get('SSM_PDL', '0')} pack={os.environ.get('SSM_ABL_PACK', '1')}: {us:8.2f} us/layer  kernels/step={stack.graph_launches}", flush=True)
+      f"pdl={os.environ.get('SSM_PDL', '1')} pack={os.environ.get('SSM_ABL_PACK', '1')}: {us:8.2f} us/layer  kernels/step={stack.graph_launches}", flush=True)

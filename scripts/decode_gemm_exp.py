@@ -12,6 +12,10 @@ import synth  # noqa: E402
 from paper_2602_21144_b200 import TPMixer  # noqa: E402
 
 EXPS = [
+    ("packed nomma|noB", {"PACK": "1", "SSM_GEMM_NOMMA": "3"}, 1),
+    ("packed nomma|noB|noepi", {"PACK": "1", "SSM_GEMM_NOMMA": "7"}, 1),
+    ("packed noB", {"PACK": "1", "SSM_GEMM_NOMMA": "2"}, 1),
+    ("packed nomma", {"PACK": "1", "SSM_GEMM_NOMMA": "1"}, 1),
     ("packed kbs2", {"PACK": "1"}, 1),
     ("packed kbs1", {"PACK": "1", "SSM_GEMM_KBS": "1"}, 1),
     ("packed kbs4", {"PACK": "1", "SSM_GEMM_KBS": "4"}, 1),
@@ -22,7 +26,8 @@ EXPS = [
     ("nomma", {"SSM_GEMM_NOMMA": "1"}, 1),
     ("streamK148", {}, -1),
 ]
-SHAPES = {"in_proj": (16, 10240, 2560), "out_proj": (16, 2560, 5120)}
+SHAPES = {"in_proj": (16, 10240, 2560), "in_proj_K1280": (16, 10240, 1280), "in_proj_K640": (16, 10240, 640),
+          "out_proj": (16, 2560, 5120)}
 
 
 def main():

@@ -150,6 +150,29 @@ def test_mixer_tp1_bf16_prefill_decode(dims_name, pack):
     assert mx.stats()["allreduce"] == 0         # TP=1: no all-reduce (reading Q13)
 
 
+@pytest.mark.parametrize("B,dims_name", [(1, "med"), (16, "med"), (17, "med"), (32, "med"), (5, "med_zamba"),
+                                         (4, "med_falcon")])
+def test_fused_decode_inproj_matches_unfused_and_oracle(B, dims_name, monkeypatch):
+    """Decode in_proj with the conv step and x_proj fused into its epilogue (tokens split over
+    the two epilogue halves, x_proj partials accumulated into the state's zeroed buffer and
+    re-zeroed by out_proj) against the unfused kernel chain and the oracle, over several steps."""
+    dims = {"med": MED,
+            "med_falcon": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, bcdt_rmsnorm=True),
+            "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2)}[dims_name]
+    res = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("SSM_FUSE_DECODE", fuse)
+        gpu, ref, r0, st, st_ref, mx = _run_tp1(dims, "bf16", B, 40, 5, pack=True)
+        assert rel(gpu - r0, ref - r0) < TOL["bf16"], fuse
+        assert rel(st[1], st_ref[1]) < TOL["bf16"], fuse
+        assert rel(st[0], st_ref[0]) < TOL["bf16"], fuse
+        assert (mx.fused_calls() == 5) == (fuse == "1") and mx.fused_calls() in (0, 5)
+        res[fuse] = (gpu, st)
+    # same arithmetic up to the x_proj summation order: the two paths agree far inside the tolerance
+    assert rel(res["1"][0] - r0, res["0"][0] - r0) < 5e-3
+    np.testing.assert_array_equal(res["1"][1][0], res["0"][1][0])   # conv window: raw x values
+
+
 def test_mixer_chunked_prefill_matches_oracle_and_is_chunk_invariant():
     dims = MED
     g1, ref, res, st1, _, _ = _run_tp1(dims, "bf16", 2, 100, 0)
