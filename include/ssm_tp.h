@@ -149,7 +149,9 @@ ssm_status_t ssm_workspace_bytes(ssm_tp_t tp, int32_t batch, int32_t seqlen, siz
  *   conv window [batch][K-1][E_k] in cfg.dtype (raw x values, oldest first),
  *   h           [batch][E_k][N]   fp32.
  * ssm_state_bytes reports the two buffer sizes; ssm_state_alloc binds caller buffers of
- * at least those sizes and zero-fills them on `stream` (the prefill start state). */
+ * at least those sizes and zero-fills them on `stream` (the prefill start state).  The h
+ * buffer is h followed by library scratch of the fused decode path (x_proj accumulator,
+ * grid-barrier counter) that must stay zero/monotonic between calls: never write it. */
 ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, size_t* h_bytes);
 ssm_status_t ssm_state_alloc(ssm_tp_t tp, int32_t batch, void* conv_buf, size_t conv_bytes,
                              void* h_buf, size_t h_bytes, void* stream, ssm_state_t* out);

@@ -163,6 +163,17 @@ SSM_DEV void bulk_load_evict_first(void* smem_dst, const void* src, uint32_t byt
       : "memory");
 }
 
+// cp.async 16 B global -> shared (zero-fill when !pred)
+SSM_DEV void cp_async16(void* sdst, const void* gsrc, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(pred ? 16 : 0)
+               : "memory");
+}
+SSM_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+SSM_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05 / TMEM
 SSM_DEV void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
@@ -276,6 +287,13 @@ SSM_DEV uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 SSM_DEV void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+SSM_DEV uint64_t ld_acquire_gpu_u64(const unsigned long long* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Generic-proxy writes (made visible by an acquire) before subsequent async-proxy (TMA) reads.
+SSM_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 // Load one byte and discard it (address translation warm-up; result unused but not elided).
 SSM_DEV void touch_global(const void* p) {
   asm volatile("{\n.reg .u8 t;\nld.global.cg.u8 t, [%0];\n}" ::"l"(p) : "memory");

@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "dstep.cuh"
 
 namespace ssm {
 
@@ -374,6 +375,55 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
   }
 }
 
+// ---- decode-step job of the fused decode out_proj: epilogue warps 2-5 and 6-9 each run one
+// 128-thread decode-step unit at a time (named barriers 2 and 3), then all CTAs meet at a grid
+// barrier (monotonic 64-bit counter: generation = old / gridDim.x) so that every g row is
+// written before any CTA's TMA reads it.  Bounded wait (2 s): a broken co-residency assumption
+// produces wrong numbers and a printf instead of a hung GPU.
+constexpr int kJobIpt = 4;  // batch rows per thread in the decode-step job (16 rows per 128-thread unit)
+template <typename T, int N, bool FAST>
+__device__ void run_dstep_units(const DStepJob& j, float* smem_f) {
+  const int warp = threadIdx.x >> 5;
+  const int half = (warp - 2) >> 2;
+  const int htid = threadIdx.x - 64 - half * 128;
+  DStepArgs a{};
+  a.src_off = 0; a.ldp = j.ldp; a.rmsnorm = j.rmsnorm; a.eps = j.eps; a.u = j.u; a.z = j.z; a.ldz = j.ldz;
+  a.w_dt = j.w_dt; a.b_dt = j.b_dt; a.a_log = j.a_log; a.d_skip = j.d_skip; a.h = j.h; a.g = j.g;
+  a.batch = j.batch; a.Ek = j.Ek; a.R = j.R; a.cph = j.cph; a.zacc = nullptr;
+  Peers src{};
+  src.p[0] = const_cast<float*>(j.dbc);
+  constexpr int IPT = kJobIpt;
+  const int unit_floats = (int)(dstep_smem(j.R, N, (int)sizeof(T), IPT) / 4);
+  float* my = smem_f + half * unit_floats;
+  const int uc = (j.Ek + DS_CH - 1) / DS_CH, ub = (j.batch + DS_BB * IPT - 1) / (DS_BB * IPT);
+  for (int unit = blockIdx.x * 2 + half; unit < uc * ub; unit += gridDim.x * 2) {
+    dstep_unit<T, N, FAST, DS_THREADS, IPT>(a, src, 1, (unit % uc) * DS_CH, (unit / uc) * DS_BB * IPT, htid, my,
+                                            2 + half, false);
+    dstep_sync<DS_THREADS>(2 + half);  // unit smem reused by the next unit
+  }
+}
+
+__device__ __forceinline__ void run_dstep_job(const DStepJob& j, float* smem_f) {
+  if (j.N == 16) run_dstep_units<__nv_bfloat16, 16, true>(j, smem_f);
+  else run_dstep_units<__nv_bfloat16, 8, true>(j, smem_f);
+  named_bar_sync(1, 256);
+  if (threadIdx.x == 64) {
+    __threadfence();
+    const unsigned long long G = gridDim.x;
+    const unsigned long long old = atomicAdd(j.sync, 1ull);
+    const unsigned long long target = (old / G + 1) * G;
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire_gpu_u64(j.sync) < target) {
+      if (globaltimer() - t0 > 2000000000ull) {
+        printf("ssm: decode-step grid barrier timed out (CTA %d)\n", blockIdx.x);
+        break;
+      }
+    }
+    fence_proxy_async_global();
+  }
+  named_bar_sync(1, 256);
+}
+
 // Experiment-only timeline (cr.nomma & 8): per-CTA clock64 offsets of pipeline events.
 constexpr int kTraceSlots = 16, kTraceCtas = 1024;
 __device__ unsigned long long g_trace[kTraceCtas * kTraceSlots];
@@ -385,7 +435,7 @@ __device__ unsigned long long g_trace[kTraceCtas * kTraceSlots];
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_blk, int64_t lda, int K,
-                   CtaRes cr, int a_blocked) {
+                   CtaRes cr, int a_blocked, const DStepJob job) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int STAGES = num_stages(BN, KBS, cr.ring);
@@ -397,7 +447,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + MAX_STAGES;
   uint64_t* tfull = empty + MAX_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bready = tempty + 2;  // decode-step job done grid-wide: B (g) may be loaded
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -416,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 8);
     }
+    mbar_init(bready, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, cr.tmem_cols);
@@ -453,6 +505,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
       }
       pdl_wait();
+      if (job.enabled) {  // B = g is produced inside this grid (decode-step job + grid barrier)
+        mbar_wait(bready, 0);
+        fence_proxy_async_global();
+      }
       int stage = 0, g = 0;
       uint32_t ph = 0;
       int cur = ts.first(), mt, nt, kb0, kb1;
@@ -526,7 +582,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ---------------- epilogue warps 2..9; TMEM lane group = warp % 4, column half = (warp-2)/4
     pdl_wait();
-    if (epi.zero && blockIdx.x == 0) {
+    if (job.enabled) {
+      run_dstep_job(job, reinterpret_cast<float*>(smem + cr.ring + 512));
+      if (threadIdx.x == 64) mbar_arrive(bready);
+    }
+    if (epi.zero && blockIdx.x == 0) {  // (after the job: it may read the buffer being zeroed)
       const int64_t n4 = epi.nzero / 4;
       for (int64_t i = threadIdx.x - 64; i < n4; i += kThreads - 64)
         reinterpret_cast<float4*>(epi.zero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -690,8 +750,10 @@ bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb) {
 
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
                          int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool a_indep,
-                         const __nv_bfloat16* A_blocked) {
+                         const __nv_bfloat16* A_blocked, const DStepJob* job_in) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  DStepJob job{};
+  if (job_in) job = *job_in;
   const int ksplit_in = ksplit;
   // BN: multiple of 32 in [32, 256] (UMMA needs N % 16 == 0; the epilogue drains TMEM in
   // 32-column chunks) covering N in as few tiles as possible
@@ -768,6 +830,16 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     cr.ring -= SU_BYTES;
   }
   if (epi.zero && (reinterpret_cast<uintptr_t>(epi.zero) & 15)) return cudaErrorInvalidValue;
+  if (job.enabled) {
+    // B operand = g produced in-kernel: bf16 only, the decode-step smem of two units, one tile per
+    // CTA, all CTAs co-resident (grid <= SMs at 1 CTA/SM), decode-step shape limits
+    if (!job.bf16 || !job.sync || (job.N != 16 && job.N != 8) || epi.kind == EPI_DECODE_INPROJ ||
+        !dstep_supported(1, job.R, job.N, job.ldp, job.cph) || ts.units > num_sms)
+      return cudaErrorInvalidValue;
+    const int js = (int)((2 * dstep_smem(job.R, job.N, 2, kJobIpt) + 127) / 128 * 128);
+    extra += js;
+    cr.ring -= js;
+  }
   while (kbs > 1 && num_stages(BN, kbs, cr.ring) < 2) --kbs;
   const int smem_bytes = 1024 + cr.ring + 512 + extra;
   int grid = ts.units < num_sms ? ts.units : num_sms;
@@ -778,8 +850,8 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     grid = (int)(W < cap ? W : cap);
   }
   { cudaError_t e_ = launch(gemm_tc_kernel, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi,
-                                      A_blocked,
-                                      lda, K, cr, A_blocked ? 1 : 0); if (e_ != cudaSuccess) return e_; }
+                                      A_blocked, lda, K, cr, A_blocked ? 1 : 0, job);
+    if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 

@@ -49,6 +49,30 @@ struct Peers {
   void* p[kMaxTP];
 };
 
+// Decode step run inside the decode out_proj GEMM as the producer of its B operand g: the idle
+// epilogue warps of every CTA run decode-step units (dstep.cuh) while the weight stream starts,
+// then a grid-wide barrier (all CTAs co-resident: grid <= SMs, 1 CTA/SM) releases the B loads.
+struct DStepJob {
+  int enabled;
+  int bf16;
+  int N;                          // d_state (16 or 8)
+  const float* dbc;               // [batch][ldp] x_proj result (single source, no AR#1)
+  unsigned long long* sync;       // grid-barrier counter (monotonic; one per layer state)
+  // flattened DStepArgs fields
+  int ldp, rmsnorm;
+  float eps;
+  const void* u;
+  const void* z;
+  int64_t ldz;
+  const void* w_dt;
+  const float* b_dt;
+  const float* a_log;
+  const float* d_skip;
+  float* h;
+  void* g;
+  int batch, Ek, R, cph;
+};
+
 // ---- GEMM launchers (return cudaSuccess or the launch error) ----
 // tcgen05/TMEM/TMA bf16 GEMM: A [M,K] row stride lda, B [N,K] row stride ldb (elements).
 // ksplit > 1: data-parallel split-K; ksplit < 0: stream-K over all SMs (both need EPI_ATOMIC_F32).
@@ -59,7 +83,7 @@ struct Peers {
 // 16 KB boxes (sequential weight streams for the decode GEMMs).
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
                          int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool a_indep = false,
-                         const __nv_bfloat16* A_blocked = nullptr);
+                         const __nv_bfloat16* A_blocked = nullptr, const DStepJob* job = nullptr);
 // experiment-only: copy the GEMM timeline buffer (16 u64 per CTA, SSM_GEMM_NOMMA bit 8)
 cudaError_t gemm_trace_read(unsigned long long* host, int n);
 size_t packed_blocked_bytes(int rows, int cols);

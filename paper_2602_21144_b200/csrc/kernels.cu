@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "dstep.cuh"
 
 namespace ssm {
 namespace {
@@ -226,15 +227,6 @@ __global__ void __launch_bounds__(256) unpack_kernel(Peers src, int nsrc, int64_
 }
 
 // ---------------------------------------------------------------- selective scan (prefill)
-SSM_DEV void cp_async16(void* sdst, const void* gsrc, bool pred) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(pred ? 16 : 0)
-               : "memory");
-}
-SSM_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-SSM_DEV void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 constexpr int SC_THREADS = 128;  // channels per block
 
@@ -515,198 +507,17 @@ __global__ void __launch_bounds__(S3_THREADS) scan2_kernel(
 }
 
 // ---------------------------------------------------------------- decode step
-// One token per sequence: AR#1 fixed-order sum of the dbc partials (+ Falcon dt/B/C RMSNorm),
-// dt_proj + softplus, one scan step and the gate; h updated in place.  A block owns DS_CH
-// channels x DS_BB batch rows (one item per thread), so the grid has many small blocks that all
-// co-reside (no wave tail).  Decode is latency-bound: every global load of the kernel is issued
-// before any is consumed.
-constexpr int DS_CH = 32;
-constexpr int DS_BB = 4;
-constexpr int DS_THREADS = DS_CH * DS_BB;
-__host__ __device__ inline int dstep_rw(int R, int es) {
-  return es == 2 ? R + ((8 - R % 64) + 64) % 64 : R + ((4 - R % 32) + 32) % 32;
-}
-template <typename T, int N, bool FAST>
-__global__ void __launch_bounds__(DS_THREADS, 5) decode_step_kernel(
-    Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps, const T* __restrict__ u,
-    const T* __restrict__ z, int64_t ldz, const T* __restrict__ w_dt, const float* __restrict__ b_dt,
-    const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ h, T* __restrict__ g,
-    int batch, int Ek, int R, int ch_per_head, float* __restrict__ zacc) {
+// Body in dstep.cuh (shared with the out_proj GEMM, which can run it as its B-operand producer).
+template <typename T, int N, bool FAST, int IPT>
+__global__ void __launch_bounds__(DS_THREADS, IPT == 1 ? 5 : 3) decode_step_kernel(DStepArgs a, Peers src, int nsrc) {
   extern __shared__ __align__(16) float dsm[];
-  constexpr int V = 16 / sizeof(T);
-  const int P = R + 2 * N;
-  const int RW = dstep_rw(R, (int)sizeof(T));  // W_dt row stride (elements of T): 16-B aligned, and
-                                               // row-to-row bank shift of 4 words (conflict-free LDS.128)
-  const int P4 = (P + 3) & ~3;
-  T* sW = reinterpret_cast<T*>(dsm);      // [DS_CH][RW], storage type (converted on use)
-  float* sD = dsm + (DS_CH * RW * (int)sizeof(T) + 15) / 16 * 4;  // [DS_BB][P4] summed dbc rows
-  float* sA = sD + DS_BB * P4;            // [DS_CH][N]   A (log2e-scaled in FAST mode)
-  float* sS = sA + DS_CH * N;             // [DS_BB][3]   RMSNorm scales
-  const int tid = threadIdx.x;
-  const int c0 = blockIdx.x * DS_CH;
-  const int b0 = blockIdx.y * DS_BB;
-  const int hd = c0 / ch_per_head;
-  const int nb = min(DS_BB, batch - b0);
   pdl_trigger();
-
-  // ---- weights first (independent of the predecessor kernels): W_dt rows (cp.async, no
-  //      register staging), a_log
-  constexpr int AMAX = (DS_CH * N + DS_THREADS - 1) / DS_THREADS;
-  const int cpr = R / V;
-  const int nw = DS_CH * cpr;
-  for (int i = tid; i < nw; i += DS_THREADS) {
-    const int c = i / cpr, q = i % cpr;
-    const bool okw = c0 + c < Ek;
-    cp_async16(sW + c * RW + q * V, w_dt + (int64_t)(okw ? c0 + c : 0) * R + q * V, okw);
-  }
-  cp_async_commit();
-  float al[AMAX];
-#pragma unroll
-  for (int k = 0; k < AMAX; ++k) {
-    const int i = tid + k * DS_THREADS;
-    const int c = i / N, n = i % N;
-    al[k] = (i < DS_CH * N && c0 + c < Ek) ? a_log[(int64_t)(c0 + c) * N + n] : 0.f;
-  }
-  const int cc = tid % DS_CH, bl = tid / DS_CH;
-  const int d = c0 + cc, b = b0 + bl;
-  const bool ok = bl < nb && d < Ek;
-  const float bias = ok ? b_dt[d] : 0.f;
-  const float Dd = ok ? d_skip[d] : 0.f;
-  pdl_wait();  // everything below reads what the predecessor kernels produced
-  // ---- activations: dbc rows (first source), this thread's h row, u, z
-  const int p4 = P / 4;
-  const int nd = nb * p4;
-  constexpr int DMAX = 4;
-  float4 acc[DMAX];
-  const float* sp0 = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[0]) + src_off);
-#pragma unroll
-  for (int k = 0; k < DMAX; ++k) {
-    const int i = tid + k * DS_THREADS;
-    acc[k] = i < nd ? *reinterpret_cast<const float4*>(sp0 + (int64_t)(b0 + i / p4) * ldp + (int64_t)hd * P + 4 * (i % p4))
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  float hs[N];
-  float* hp = h + ((int64_t)(ok ? b : 0) * Ek + (ok ? d : 0)) * N;
-#pragma unroll
-  for (int n = 0; n < N; n += 4) {
-    const float4 t4 = ok ? *reinterpret_cast<const float4*>(hp + n) : make_float4(0.f, 0.f, 0.f, 0.f);
-    hs[n] = t4.x; hs[n + 1] = t4.y; hs[n + 2] = t4.z; hs[n + 3] = t4.w;
-  }
-  const float uu = ok ? io<T>::ld(u + (int64_t)b * Ek + d) : 0.f;
-  float zz = 0.f;
-  if (zacc) {
-    if (ok) { zz = zacc[(int64_t)b * ldz + d]; zacc[(int64_t)b * ldz + d] = 0.f; }
-  } else if (ok) {
-    zz = io<T>::ld(z + (int64_t)b * ldz + d);
-  }
-  // ---- consume into shared memory
-  for (int base = 0; base < nd; base += DMAX * DS_THREADS) {
-    if (base > 0) {
-#pragma unroll
-      for (int k = 0; k < DMAX; ++k) {
-        const int i = base + tid + k * DS_THREADS;
-        acc[k] = i < nd ? *reinterpret_cast<const float4*>(sp0 + (int64_t)(b0 + i / p4) * ldp + (int64_t)hd * P + 4 * (i % p4))
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-    for (int r = 1; r < nsrc; ++r) {  // fixed rank order (reading Q12)
-      const float* sp = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[r]) + src_off);
-      float4 ld[DMAX];
-#pragma unroll
-      for (int k = 0; k < DMAX; ++k) {
-        const int i = base + tid + k * DS_THREADS;
-        ld[k] = i < nd ? *reinterpret_cast<const float4*>(sp + (int64_t)(b0 + i / p4) * ldp + (int64_t)hd * P + 4 * (i % p4))
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int k = 0; k < DMAX; ++k) {
-        acc[k].x += ld[k].x; acc[k].y += ld[k].y; acc[k].z += ld[k].z; acc[k].w += ld[k].w;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < DMAX; ++k) {
-      const int i = base + tid + k * DS_THREADS;
-      if (i < nd) *reinterpret_cast<float4*>(sD + (i / p4) * P4 + 4 * (i % p4)) = acc[k];
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < AMAX; ++k) {
-    const int i = tid + k * DS_THREADS;
-    if (i < DS_CH * N) {
-      const float a = -expf(al[k]);
-      sA[i] = FAST ? a * 1.4426950408889634f : a;
-    }
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  if (rmsnorm) {  // weightless RMSNorm of dt_low, B, C per batch row (Falcon-Mamba, reading Q18)
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int r = warp; r < nb; r += DS_THREADS / 32) {
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-      for (int c = lane; c < P; c += 32) {
-        const float v = sD[r * P4 + c];
-        if (c < R) s0 = fmaf(v, v, s0);
-        else if (c < R + N) s1 = fmaf(v, v, s1);
-        else s2 = fmaf(v, v, s2);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      }
-      if (lane == 0) {
-        sS[r * 3 + 0] = 1.0f / sqrtf(s0 / (float)R + eps);
-        sS[r * 3 + 1] = 1.0f / sqrtf(s1 / (float)N + eps);
-        sS[r * 3 + 2] = 1.0f / sqrtf(s2 / (float)N + eps);
-      }
-    }
-    __syncthreads();
-  }
-  if (!ok) return;
-  // ---- compute: warp = one batch row, lane = channel
-  const T* wr = sW + cc * RW;
-  const float* xr = sD + bl * P4;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  for (int r = 0; r < R; r += V) {  // R % V == 0 (validated by the launcher)
-    float wv[V];
-    if constexpr (sizeof(T) == 2) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(wr + r);
-      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-      for (int j = 0; j < V / 2; ++j) { const float2 f = __bfloat1622float2(b2[j]); wv[2 * j] = f.x; wv[2 * j + 1] = f.y; }
-    } else {
-      const float4 f = *reinterpret_cast<const float4*>(wr + r);
-      wv[0] = f.x; wv[1] = f.y; wv[2] = f.z; wv[3] = f.w;
-    }
-#pragma unroll
-    for (int j = 0; j < V; j += 4) {
-      const float4 xv = *reinterpret_cast<const float4*>(xr + r + j);
-      s0 = fmaf(xv.x, wv[j], s0); s1 = fmaf(xv.y, wv[j + 1], s1); s2 = fmaf(xv.z, wv[j + 2], s2);
-      s3 = fmaf(xv.w, wv[j + 3], s3);
-    }
-  }
-  float dt = (s0 + s1) + (s2 + s3);
-  if (rmsnorm) dt *= sS[bl * 3 + 0];
-  const float de = softplus(dt + bias);
-  const float du = de * uu;
-  const float sBs = rmsnorm ? sS[bl * 3 + 1] : 1.f;
-  const float sCs = rmsnorm ? sS[bl * 3 + 2] : 1.f;
-  const float* Bt = xr + R;
-  const float* Ct = xr + R + N;
-  const float* Ac = sA + cc * N;
-  float y = 0.f;
-#pragma unroll
-  for (int n = 0; n < N; ++n) {
-    const float ab = FAST ? ex2_approx(de * Ac[n]) : expf(de * Ac[n]);
-    hs[n] = fmaf(ab, hs[n], du * (Bt[n] * sBs));
-    y = fmaf(Ct[n] * sCs, hs[n], y);
-  }
-#pragma unroll
-  for (int n = 0; n < N; n += 4) *reinterpret_cast<float4*>(hp + n) = make_float4(hs[n], hs[n + 1], hs[n + 2], hs[n + 3]);
-  y = fmaf(Dd, uu, y);
-  io<T>::st(g + (int64_t)b * Ek + d, y * silu<FAST>(zz));
+  dstep_unit<T, N, FAST, DS_THREADS, IPT>(a, src, nsrc, blockIdx.x * DS_CH, blockIdx.y * DS_BB * IPT, threadIdx.x, dsm,
+                                          -1, true);
 }
+// items (batch rows) per thread of the standalone decode-step kernel: 1 (640 blocks for B = 16)
+// or 4 (160 blocks, 4x fewer W_dt reads, every item's loads in flight at once); SSM_DSTEP_IPT
+const int g_dstep_ipt = [] { const char* e = getenv("SSM_DSTEP_IPT"); return e && atoi(e) == 4 ? 4 : 1; }();
 
 // ---------------------------------------------------------------- RMSNorm (glue)
 // One 128-thread block per row, the row cached in registers (<= 16 float4 per thread).
@@ -984,23 +795,14 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
   return scan_t<float, 8, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
 }
 
-static size_t dstep_smem(int R, int N, int es) {
-  const int P = R + 2 * N;
-  const int RW = dstep_rw(R, es), P4 = (P + 3) & ~3;
-  return (size_t)((DS_CH * RW * es + 15) / 16 * 16) + (size_t)(DS_BB * P4 + DS_CH * N + DS_BB * 3) * sizeof(float);
-}
-
 template <typename T, int N, bool F>
-static cudaError_t dstep_t(Peers src, int nsrc, int64_t off, int ldp, int rms, float eps, const void* u, const void* z,
-                           int64_t ldz, const void* w_dt, const float* b_dt, const float* a_log, const float* d_skip,
-                           float* h, void* g, int batch, int Ek, int R, int cph, float* zacc, cudaStream_t s) {
-  const size_t smem = dstep_smem(R, N, (int)sizeof(T));
-  dim3 grid((Ek + DS_CH - 1) / DS_CH, (batch + DS_BB - 1) / DS_BB);
-  { cudaError_t e_ = launch(decode_step_kernel<T, N, F>, grid, DS_THREADS, smem, s, src, nsrc, off, ldp, rms, eps,
-                            reinterpret_cast<const T*>(u), reinterpret_cast<const T*>(z), ldz,
-                            reinterpret_cast<const T*>(w_dt), b_dt, a_log, d_skip, h, reinterpret_cast<T*>(g), batch,
-                            Ek, R, cph, zacc);
-    if (e_ != cudaSuccess) return e_; }
+static cudaError_t dstep_t(const DStepArgs& a, Peers src, int nsrc, cudaStream_t s) {
+  const int ipt = g_dstep_ipt;
+  const size_t smem = dstep_smem(a.R, N, (int)sizeof(T), ipt);
+  dim3 grid((a.Ek + DS_CH - 1) / DS_CH, (a.batch + DS_BB * ipt - 1) / (DS_BB * ipt));
+  cudaError_t e_ = ipt == 4 ? launch(decode_step_kernel<T, N, F, 4>, grid, DS_THREADS, smem, s, a, src, nsrc)
+                            : launch(decode_step_kernel<T, N, F, 1>, grid, DS_THREADS, smem, s, a, src, nsrc);
+  if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
 }
 
@@ -1009,15 +811,13 @@ cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, i
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
                                int N, int ch_per_head, float* zacc, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
-  if (ch_per_head % DS_CH != 0) return cudaErrorInvalidValue;
-  if (N != 16 && N != 8) return cudaErrorInvalidValue;
-  const int es = bf16 ? 2 : 4;
-  if (dstep_smem(R, N, es) > 48 * 1024) return cudaErrorInvalidValue;
-  if ((R * es) % 16 || (R + 2 * N) % 4 || ldp % 4) return cudaErrorInvalidValue;
-#define DS_ARGS src, nsrc, src_off, ldp, rmsnorm, eps, u, z, ldz, w_dt, b_dt, a_log, d_skip, h, g, batch, Ek, R, ch_per_head, zacc, s
-  if (bf16) return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(DS_ARGS) : dstep_t<__nv_bfloat16, 8, true>(DS_ARGS);
-  return N == 16 ? dstep_t<float, 16, false>(DS_ARGS) : dstep_t<float, 8, false>(DS_ARGS);
-#undef DS_ARGS
+  if (!dstep_supported(bf16, R, N, ldp, ch_per_head) || nsrc < 1 || nsrc > kMaxTP) return cudaErrorInvalidValue;
+  DStepArgs a{};
+  a.src_off = src_off; a.ldp = ldp; a.rmsnorm = rmsnorm; a.eps = eps; a.u = u; a.z = z; a.ldz = ldz; a.w_dt = w_dt;
+  a.b_dt = b_dt; a.a_log = a_log; a.d_skip = d_skip; a.h = h; a.g = g; a.batch = batch; a.Ek = Ek; a.R = R;
+  a.cph = ch_per_head; a.zacc = zacc;
+  if (bf16) return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(a, src, nsrc, s) : dstep_t<__nv_bfloat16, 8, true>(a, src, nsrc, s);
+  return N == 16 ? dstep_t<float, 16, false>(a, src, nsrc, s) : dstep_t<float, 8, false>(a, src, nsrc, s);
 }
 
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
@@ -1077,8 +877,10 @@ cudaError_t preload_kernels() {
       (const void*)scan_kernel<float, 16, false>, (const void*)scan_kernel<float, 8, false>,
       (const void*)scan2_kernel<16, 0>, (const void*)scan2_kernel<16, 2>, (const void*)scan2_kernel<16, 4>,
       (const void*)scan2_kernel<16, 6>,
-      (const void*)decode_step_kernel<__nv_bfloat16, 16, true>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true>,
-      (const void*)decode_step_kernel<float, 16, false>, (const void*)decode_step_kernel<float, 8, false>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 1>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 1>,
+      (const void*)decode_step_kernel<float, 16, false, 1>, (const void*)decode_step_kernel<float, 8, false, 1>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 4>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 4>,
+      (const void*)decode_step_kernel<float, 16, false, 4>, (const void*)decode_step_kernel<float, 8, false, 4>,
       (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>,
       (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,
       (const void*)quantize_kernel<8>, (const void*)qar_reduce_kernel, (const void*)f32_reduce_kernel,

@@ -17,7 +17,7 @@ scanmicro) for v in "1 4" "2 0" "2 2" "2 4" "2 6"; do set -- $v; SSM_SCAN_VERSIO
 decexp) timeout 600 python scripts/decode_gemm_exp.py > gpurun_out/decexp_$TAG.txt 2>&1; cat gpurun_out/decexp_$TAG.txt ;;
 benchnopdl) SSM_PDL=0 timeout 900 python bench.py --no-cpu --no-e2e > gpurun_out/benchnopdl_$TAG.txt 2>&1; tail -1 gpurun_out/benchnopdl_$TAG.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('NOPDL', d['value'], d['ttft_ms'], d['tpot_ms'])" ;;
 decprof) timeout 600 python scripts/decode_profile.py > gpurun_out/decprof_$TAG.txt 2>&1; cat gpurun_out/decprof_$TAG.txt ;;
-ablate) (for m in 0 1 2 4 8 16 31; do SSM_DEBUG_SKIP=$m timeout 120 python scripts/decode_ablation.py; done; SSM_DEBUG_SKIP_NORM=1 timeout 120 python scripts/decode_ablation.py; SSM_DEBUG_SKIP=31 SSM_DEBUG_SKIP_NORM=1 timeout 120 python scripts/decode_ablation.py; SSM_PDL=0 timeout 120 python scripts/decode_ablation.py; SSM_FUSE_DECODE=0 timeout 120 python scripts/decode_ablation.py) > gpurun_out/ablate_$TAG.txt 2>&1; cat gpurun_out/ablate_$TAG.txt ;;
+ablate) (for m in 0 8 16 23 31; do SSM_DEBUG_SKIP=$m timeout 120 python scripts/decode_ablation.py; done; SSM_DEBUG_SKIP_NORM=1 timeout 120 python scripts/decode_ablation.py; SSM_DEBUG_SKIP=31 SSM_DEBUG_SKIP_NORM=1 timeout 120 python scripts/decode_ablation.py; SSM_PDL=0 timeout 120 python scripts/decode_ablation.py; SSM_FUSE_DECODE=0 timeout 120 python scripts/decode_ablation.py; echo dstep-fused-in-out_proj; SSM_FUSE_DSTEP=1 timeout 120 python scripts/decode_ablation.py) > gpurun_out/ablate_$TAG.txt 2>&1; cat gpurun_out/ablate_$TAG.txt ;;
 dstepfull) ARGS="--layers 2 --prompt 256 --decode 8 --steps 1 --warmup 1 --no-e2e --no-cpu"
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_step -s 4 -c 1 -o gpurun_out/dstep_$TAG python bench.py $ARGS > /dev/null 2>&1; ls gpurun_out/dstep_$TAG* ;;
 decinfull) ARGS="--layers 2 --prompt 256 --decode 8 --steps 1 --warmup 1 --no-e2e --no-cpu"

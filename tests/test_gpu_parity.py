@@ -160,17 +160,23 @@ def test_fused_decode_inproj_matches_unfused_and_oracle(B, dims_name, monkeypatc
             "med_falcon": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, bcdt_rmsnorm=True),
             "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2)}[dims_name]
     res = {}
-    for fuse in ("1", "0"):
+    for fuse, fuse_ds in (("1", "1"), ("1", "0"), ("0", "1"), ("0", "0")):
         monkeypatch.setenv("SSM_FUSE_DECODE", fuse)
+        monkeypatch.setenv("SSM_FUSE_DSTEP", fuse_ds)   # decode step inside the out_proj GEMM
         gpu, ref, r0, st, st_ref, mx = _run_tp1(dims, "bf16", B, 40, 5, pack=True)
-        assert rel(gpu - r0, ref - r0) < TOL["bf16"], fuse
-        assert rel(st[1], st_ref[1]) < TOL["bf16"], fuse
-        assert rel(st[0], st_ref[0]) < TOL["bf16"], fuse
+        tag = (fuse, fuse_ds)
+        assert rel(gpu - r0, ref - r0) < TOL["bf16"], tag
+        assert rel(st[1], st_ref[1]) < TOL["bf16"], tag
+        assert rel(st[0], st_ref[0]) < TOL["bf16"], tag
         assert (mx.fused_calls() == 5) == (fuse == "1") and mx.fused_calls() in (0, 5)
-        res[fuse] = (gpu, st)
-    # same arithmetic up to the x_proj summation order: the two paths agree far inside the tolerance
-    assert rel(res["1"][0] - r0, res["0"][0] - r0) < 5e-3
-    np.testing.assert_array_equal(res["1"][1][0], res["0"][1][0])   # conv window: raw x values
+        res[tag] = (gpu, st)
+    # same arithmetic up to the x_proj summation order: the paths agree far inside the tolerance
+    for tag in res:
+        assert rel(res[tag][0] - r0, res[("0", "0")][0] - r0) < 5e-3, tag
+        np.testing.assert_array_equal(res[tag][1][0], res[("0", "0")][1][0])   # conv window: raw x values
+    # the decode-step placement does not change the arithmetic (only atomic summation orders differ)
+    assert rel(res[("1", "1")][0] - r0, res[("1", "0")][0] - r0) < 1e-5
+    assert rel(res[("0", "1")][1][1], res[("0", "0")][1][1]) < 1e-5
 
 
 def test_mixer_chunked_prefill_matches_oracle_and_is_chunk_invariant():
