@@ -201,6 +201,39 @@ ssm_status_t ssm_packed_weight_bytes(int32_t rows, int32_t cols, size_t* bytes);
 ssm_status_t ssm_pack_weight(ssm_tp_t tp, const void* w, int32_t rows, int32_t cols, void* out, size_t out_bytes,
                              void* stream);
 
+/* ---- Persistent whole-stack decode (TP = 1) --------------------------------------------
+ * One decode token (seqlen 1) for `batch` sequences through n_layers pre-norm blocks
+ *   x = RMSNorm(residual) (weight 1, eps norm_eps; reading Q16);  residual += mixer_l(x)
+ * in ONE kernel launch (PAPER.md:276-280 decode from the cache; 545 TPOT is bound by memory
+ * bandwidth): the same arithmetic as n_layers x (ssm_rmsnorm + ssm_mixer_decode), with the
+ * layers' packed W_in / W_out streamed continuously through shared memory by a persistent
+ * grid of one CTA per SM (grid-wide barriers between the phases of a layer).
+ * Supported: SSM_BF16, tp_size 1, n_heads 1, d_state 16, 2 <= d_conv <= 4, batch <= 32,
+ * d_model % 128 == 0, d_inner % 64 == 0, dt_rank % 16 == 0, (dt_rank + 32) % 16 == 0;
+ * otherwise SSM_ERR_UNSUPPORTED (callers use the per-layer calls).
+ *
+ * ssm_stack_bytes: workspace bytes for (n_layers, batch).
+ * ssm_stack_bind: records the layers (w_in_pk and w_out_pk required: ssm_pack_weight) and
+ *   their states (allocated for this handle and batch) in the caller's workspace (>= the bytes
+ *   above, 256-B aligned, device memory that must outlive the binding), zero-fills it and
+ *   synchronises `stream`.  One bound stack per handle; binding again replaces it.  Errors:
+ *   SSM_ERR_UNSUPPORTED, SSM_ERR_ARG (NULL / small / misaligned), SSM_ERR_CACHE (state of
+ *   another handle or batch).
+ * ssm_stack_decode: enqueues the step on `stream`; residual [batch, D] fp32 in/out (16-B
+ *   aligned).  Graph-capturable (cooperative launch).  The workspace holds state between calls
+ *   (monotonic barrier counter, zeroed accumulators): never write it.
+ * ssm_stack_check: synchronises `stream`; SSM_ERR_PROTOCOL if a launch timed out at a grid
+ *   barrier or in the weight pipeline (the kernel then exits with garbage rather than hanging;
+ *   re-bind before the next call).
+ * ssm_stack_info: ring slots (1000 x 16-KB weight-tile slots + B-operand k-block slots per SM),
+ *   grid size and channels per CTA of the bound stack (diagnostics). */
+ssm_status_t ssm_stack_bytes(ssm_tp_t tp, int32_t n_layers, int32_t batch, size_t* ws_bytes);
+ssm_status_t ssm_stack_bind(ssm_tp_t tp, const ssm_layer_weights_t* layers, const ssm_state_t* states,
+                            int32_t n_layers, int32_t batch, void* ws, size_t ws_bytes, void* stream);
+ssm_status_t ssm_stack_decode(ssm_tp_t tp, void* ws, float* residual, float norm_eps, void* stream);
+ssm_status_t ssm_stack_check(ssm_tp_t tp, void* ws, void* stream);
+ssm_status_t ssm_stack_info(ssm_tp_t tp, int32_t* ring_slots, int32_t* grid, int32_t* ch_per_cta);
+
 /* Synchronise the stream and report device-side protocol errors (SSM_ERR_PROTOCOL). */
 ssm_status_t ssm_tp_check(ssm_tp_t tp, void* stream);
 
@@ -245,6 +278,9 @@ ssm_status_t ssm_dbg_gemm_ld(ssm_tp_t tp, const void* A, int64_t lda, const void
 ssm_status_t ssm_dbg_scan(ssm_tp_t tp, const void* u, const void* delta, const void* z, int32_t ldz,
                           const float* BC, const float* a_log, const float* d_skip, float* h,
                           void* g, int32_t batch, int32_t seqlen, void* stream);
+/* Experiment-only: device buffer (>= grid * n_layers * 32 u64, or NULL = off) that subsequent
+ * ssm_stack_decode launches fill with globaltimer stamps per CTA, layer and phase boundary. */
+ssm_status_t ssm_dbg_stack_trace(ssm_tp_t tp, void* buf, size_t bytes);
 /* Copy `capacity` u64 of the GEMM kernel's experiment timeline (16 per CTA: globaltimer at
  * entry, clock64 at entry, then clock64 offsets of pipeline events; written only when
  * SSM_GEMM_NOMMA has bit 8 set when the GEMM is launched).  Synchronises the device. */

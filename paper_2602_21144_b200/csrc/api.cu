@@ -46,6 +46,7 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 // Programmatic dependent launch for the decode path (SSM_PDL=0 disables).
 // Debug-only ablation knob (timing experiments): SSM_DEBUG_SKIP bitmask of decode kernels to
 // skip (1 in_proj, 2 conv, 4 x_proj, 8 decode_step, 16 out_proj).  Results are wrong when set.
+const int g_mk_dbg = [] { const char* e = getenv("SSM_MK_DBG"); return e ? atoi(e) : 0; }();
 const int g_dbg_skip = [] { const char* e = getenv("SSM_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
 
 // On by default for decode-sized launches: every kernel calls griddepcontrol.launch_dependents at
@@ -77,6 +78,14 @@ struct ssm_tp_s {
   int fuse_decode;        // fused decode in_proj (conv + x_proj in its epilogue); SSM_FUSE_DECODE=0 disables
   int64_t fused_calls;    // decode calls that took the fused path
   int fuse_dstep;         // decode step run inside the out_proj GEMM; SSM_FUSE_DSTEP=0 disables
+  // persistent whole-stack decode (ssm_stack_bind / ssm_stack_decode): the bound workspace
+  struct Stack {
+    void* ws = nullptr;
+    int n_layers = 0, batch = 0, bp = 0, ncmax = 0, ngrp = 0, ring = 0, nbr = 0, grid = 0;
+    size_t off_tab = 0, off_residT = 0, off_residB = 0, off_xzT = 0, off_dbcT = 0, off_ss = 0, off_ssP = 0,
+           off_gT = 0, off_cnt = 0, off_ep = 0, total = 0;
+    unsigned long long* trace = nullptr;  // experiment-only timeline buffer (ssm_dbg_stack_trace)
+  } stack;
   // timing probes: one slot per kernel kind
   struct ProbeSlot {
     int cap = 0, n = 0;
@@ -555,6 +564,7 @@ ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp
       pre = preload_kernels();
       if (pre == cudaSuccess) pre = preload_gemm_simt();
       if (pre == cudaSuccess) pre = preload_gemm_tc();
+      if (pre == cudaSuccess) pre = preload_decode_mk();
     });
     if (pre != cudaSuccess) {
       delete t;
@@ -832,6 +842,174 @@ ssm_status_t ssm_dbg_gemm_trace(uint64_t* out, int32_t capacity) {
   if (!out || capacity < 0) return fail(SSM_ERR_ARG, "NULL argument");
   CU(cudaDeviceSynchronize());
   CU(gemm_trace_read(reinterpret_cast<unsigned long long*>(out), capacity));
+  return SSM_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ persistent whole-stack decode
+namespace {
+// Workspace layout of a bound stack (256-B aligned pieces): header (barrier counter @0, error
+// word @64), layer table, residT [D][BP], xzT [2Ek][BP], dbcT [P][BP], ssP [grid][BP], gT [Ek][BP].
+ssm_status_t stack_plan(ssm_tp_s* t, int n_layers, int batch, ssm_tp_s::Stack* S, bool why) {
+  const ssm_config_t& c = t->cfg;
+  const int P = t->P, R = c.dt_rank, D = c.d_model, Ek = t->Ek;
+  auto no = [&](const char* m) { return why ? fail(SSM_ERR_UNSUPPORTED, "stack decode: %s", m) : SSM_ERR_UNSUPPORTED; };
+  if (!t->bf16) return no("bf16 only");
+  if (t->k != 1) return no("TP=1 only (the TP>1 decode runs per layer with the peer all-reduces)");
+  if (c.n_heads != 1) return no("one x_proj head only");
+  if (c.d_state != 16) return no("d_state 16 only");
+  if (c.d_conv < 2 || c.d_conv > 4) return no("2 <= d_conv <= 4");
+  if (batch < 1 || batch > 32) return no("1 <= batch <= 32");
+  if (n_layers < 1) return no("n_layers >= 1");
+  if (D % 128 || Ek % 64 || R % 16 || P % 16) return no("needs d_model % 128, d_inner % 64, dt_rank % 16, P % 16 == 0");
+  S->n_layers = n_layers;
+  S->batch = batch;
+  S->bp = batch <= 16 ? 16 : 32;
+  S->grid = t->num_sms;
+  S->ngrp = Ek / 16;
+  S->ncmax = (S->ngrp + S->grid - 1) / S->grid * 16;
+  if (S->ncmax > 128) return no("more than 128 channels per SM");
+  // B-operand slots: every unit of a phase (all its k-block copies in flight at once) when that
+  // leaves >= 4 weight-ring slots, else fewer
+  {
+    const int U1 = (2 * Ek / 128) * (D / 64), U4 = (D / 128) * (Ek / 64);
+    const int umax = ((U1 > U4 ? U1 : U4) + S->grid - 1) / S->grid;
+    S->nbr = umax < 1 ? 1 : umax;  // the B ring holds a whole phase (staged at once)
+    if (mk_ring_slots(S->bp, P, R, S->ncmax, S->nbr) < 4) return no("a phase's B operand does not fit in shared memory");
+  }
+  S->ring = mk_ring_slots(S->bp, P, R, S->ncmax, S->nbr);
+  if (S->ring < 3) return no("shared memory too small for the weight ring");
+  const int BP = S->bp;
+  const MkCnt cn = mk_cnt_layout(D, Ek);
+  size_t o = 256;
+  S->off_tab = o; o += al256((size_t)n_layers * sizeof(MkLayer));
+  S->off_residT = o; o += al256((size_t)D * BP * 4);
+  S->off_residB = o; o += al256((size_t)D * BP * 2);
+  S->off_xzT = o; o += al256((size_t)2 * Ek * BP * 4);
+  S->off_dbcT = o; o += al256((size_t)2 * P * BP * 4);
+  S->off_ss = o; o += al256((size_t)2 * BP * 4);
+  S->off_ssP = o; o += al256((size_t)S->grid * BP * 4);
+  S->off_gT = o; o += al256((size_t)Ek * BP * 2);
+  S->off_cnt = o; o += al256((size_t)cn.words * 4);
+  S->off_ep = o; o += al256((size_t)S->grid * 4);
+  S->total = o;
+  return SSM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+ssm_status_t ssm_stack_bytes(ssm_tp_t tp, int32_t n_layers, int32_t batch, size_t* ws_bytes) {
+  if (!tp || !ws_bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  ssm_tp_s::Stack S;
+  ssm_status_t st = stack_plan(tp, n_layers, batch, &S, true);
+  if (st != SSM_OK) return st;
+  *ws_bytes = S.total;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_stack_bind(ssm_tp_t tp, const ssm_layer_weights_t* layers, const ssm_state_t* states,
+                            int32_t n_layers, int32_t batch, void* ws, size_t ws_bytes, void* stream) {
+  if (!tp || !layers || !states || !ws) return fail(SSM_ERR_ARG, "NULL argument");
+  ssm_tp_s::Stack S;
+  ssm_status_t st = stack_plan(tp, n_layers, batch, &S, true);
+  if (st != SSM_OK) return st;
+  if (ws_bytes < S.total) return fail(SSM_ERR_ARG, "stack workspace too small (%zu < %zu B)", ws_bytes, S.total);
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(SSM_ERR_ARG, "stack workspace must be 256-B aligned");
+  MkLayer* tab = new (std::nothrow) MkLayer[n_layers];
+  if (!tab) return fail(SSM_ERR_ARG, "out of host memory");
+  for (int l = 0; l < n_layers; ++l) {
+    const ssm_layer_weights_t& w = layers[l];
+    ssm_state_s* sl = states[l];
+    if (!w.w_in_pk || !w.w_out_pk || !w.w_x || !w.w_dt || !w.conv_w || !w.conv_b || !w.b_dt || !w.a_log || !w.d_skip) {
+      delete[] tab;
+      return fail(SSM_ERR_ARG, "layer %d: NULL weight (the stack decode needs w_in_pk and w_out_pk)", l);
+    }
+    if (!sl || sl->owner != tp || sl->batch != batch) {
+      delete[] tab;
+      return fail(SSM_ERR_CACHE, "layer %d: state missing or bound to another handle/batch", l);
+    }
+    tab[l] = MkLayer{reinterpret_cast<const __nv_bfloat16*>(w.w_in_pk), reinterpret_cast<const __nv_bfloat16*>(w.w_out_pk),
+                     reinterpret_cast<const __nv_bfloat16*>(w.w_x), reinterpret_cast<const __nv_bfloat16*>(w.w_dt),
+                     w.conv_w, w.conv_b, w.b_dt, w.a_log, w.d_skip, reinterpret_cast<__nv_bfloat16*>(sl->conv), sl->h,
+                     nullptr};
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* W = reinterpret_cast<char*>(ws);
+  cudaError_t e = cudaMemsetAsync(ws, 0, S.total, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(W + S.off_tab, tab, (size_t)n_layers * sizeof(MkLayer), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  delete[] tab;
+  if (e != cudaSuccess) return fail(SSM_ERR_CUDA, "stack bind: %s", cudaGetErrorString(e));
+  S.ws = ws;
+  S.trace = tp->stack.trace;
+  tp->stack = S;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_stack_decode(ssm_tp_t tp, void* ws, float* residual, float norm_eps, void* stream) {
+  if (!tp || !ws || !residual) return fail(SSM_ERR_ARG, "NULL argument");
+  const ssm_tp_s::Stack& S = tp->stack;
+  if (ws != S.ws) return fail(SSM_ERR_ARG, "workspace is not the one bound by ssm_stack_bind");
+  if (reinterpret_cast<uintptr_t>(residual) & 15) return fail(SSM_ERR_ARG, "residual must be 16-B aligned");
+  char* W = reinterpret_cast<char*>(ws);
+  MkParams p{};
+  p.layers = reinterpret_cast<const MkLayer*>(W + S.off_tab);
+  p.n_layers = S.n_layers;
+  p.resid = residual;
+  p.residT = reinterpret_cast<float*>(W + S.off_residT);
+  p.residB = reinterpret_cast<__nv_bfloat16*>(W + S.off_residB);
+  p.xzT = reinterpret_cast<float*>(W + S.off_xzT);
+  p.dbcT = reinterpret_cast<float*>(W + S.off_dbcT);
+  p.ss = reinterpret_cast<float*>(W + S.off_ss);
+  p.ssP = reinterpret_cast<float*>(W + S.off_ssP);
+  p.gT = reinterpret_cast<__nv_bfloat16*>(W + S.off_gT);
+  p.cnt = reinterpret_cast<unsigned*>(W + S.off_cnt);
+  p.ep = reinterpret_cast<unsigned*>(W + S.off_ep);
+  p.bar = reinterpret_cast<unsigned long long*>(W);
+  p.err = reinterpret_cast<unsigned*>(W + 64);
+  p.B = S.batch;
+  p.D = tp->cfg.d_model;
+  p.Ek = tp->Ek;
+  p.R = tp->cfg.dt_rank;
+  p.P = tp->P;
+  p.K = tp->cfg.d_conv;
+  p.eps = norm_eps;
+  p.rmsnorm = tp->cfg.bcdt_rmsnorm;
+  p.rms_eps = tp->cfg.rms_eps;
+  p.ring = S.ring;
+  p.nbr = S.nbr;
+  p.ncmax = S.ncmax;
+  p.ngrp = S.ngrp;
+  p.trace = S.trace;
+  p.dbg = g_mk_dbg;
+  tp->launches++;
+  CU(launch_decode_mk(p, S.bp, S.grid, reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_stack_check(ssm_tp_t tp, void* ws, void* stream) {
+  if (!tp || !ws) return fail(SSM_ERR_ARG, "NULL argument");
+  CU(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+  uint32_t errw = 0;
+  CU(cudaMemcpy(&errw, reinterpret_cast<char*>(ws) + 64, 4, cudaMemcpyDeviceToHost));
+  if (errw) return fail(SSM_ERR_PROTOCOL, "stack decode: grid barrier / weight pipeline timed out (code %u)", errw);
+  return SSM_OK;
+}
+
+ssm_status_t ssm_dbg_stack_trace(ssm_tp_t tp, void* buf, size_t bytes) {
+  if (!tp) return fail(SSM_ERR_ARG, "NULL argument");
+  tp->stack.trace = reinterpret_cast<unsigned long long*>(buf);
+  (void)bytes;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_stack_info(ssm_tp_t tp, int32_t* ring_slots, int32_t* grid, int32_t* ch_per_cta) {
+  if (!tp || !ring_slots || !grid || !ch_per_cta) return fail(SSM_ERR_ARG, "NULL argument");
+  *ring_slots = tp->stack.ring * 1000 + tp->stack.nbr;
+  *grid = tp->stack.grid;
+  *ch_per_cta = tp->stack.ncmax;
   return SSM_OK;
 }
 

@@ -131,6 +131,67 @@ cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* o
 // (bounded; sets the error word on timeout).
 cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s);
 
+// ---- persistent whole-stack decode (decode_mk.cu) ----
+// One layer of the stack as the persistent decode kernel reads it (TP=1, bf16, one x_proj head).
+struct MkLayer {
+  const __nv_bfloat16* w_in_pk;   // pack_blocked(W_in [2Ek, D]): 128x64 tiles, row-tile-major
+  const __nv_bfloat16* w_out_pk;  // pack_blocked(W_out [D, Ek])
+  const __nv_bfloat16* w_x;       // [P, Ek]
+  const __nv_bfloat16* w_dt;      // [Ek, R]
+  const float* conv_w;            // [Ek, K]
+  const float* conv_b;            // [Ek]
+  const float* b_dt;              // [Ek]
+  const float* a_log;             // [Ek, 16]
+  const float* d_skip;            // [Ek]
+  __nv_bfloat16* conv;            // cache: conv window [batch][K-1][Ek]
+  float* h;                       // cache: h [batch][Ek][16]
+  void* pad;
+};
+struct MkParams {
+  const MkLayer* layers;
+  int n_layers;
+  float* resid;                   // [B][D] fp32, caller's residual (in/out)
+  float* residT;                  // [D][BP] fp32, the residual stream while the kernel runs
+  __nv_bfloat16* residB;          // bf16 copy of residT, K-major SW128 k-blocks [D/64][BP][64]: in_proj B
+  float* xzT;                     // [2Ek][BP] fp32 in_proj accumulators (zero between layers)
+  float* dbcT;                    // [2][P][BP] fp32 x_proj accumulators (double-buffered by epoch)
+  float* ss;                      // [2][BP] sums of squares of the residual rows (by epoch)
+  float* ssP;                     // [grid][BP] per-CTA sums of squares of the input residual
+  __nv_bfloat16* gT;              // gated scan output, K-major SW128 k-blocks [Ek/64][BP][64]: out_proj B
+  unsigned* cnt;                  // readiness counters (mk_cnt_layout), monotonic since bind
+  unsigned* ep;                   // [grid] layers completed since bind, per CTA
+  unsigned long long* bar;        // grid-barrier arrival counter (monotonic)
+  unsigned* err;                  // device error word (barrier / pipeline timeout)
+  int B, D, Ek, R, P, K;
+  float eps;                      // pre-norm RMSNorm eps (weight 1, reading Q16)
+  int rmsnorm;                    // Falcon dt/B/C RMSNorm (Q18)
+  float rms_eps;
+  int ring, nbr, ncmax, ngrp;     // weight-ring slots, B-ring slots, channels per CTA (max), groups
+  unsigned long long* trace;      // optional (NULL = off): [grid][n_layers][32] globaltimer stamps
+  int dbg;                        // experiment-only (SSM_MK_DBG)
+};
+// Counter block (u32 words, 32 B apart): cnt_x, cnt_fin, cnt_in[2Ek/128], rdy_g[Ek/64],
+// cnt_out[D/128], rdy_res[D/128].
+struct MkCnt {
+  int x, fin, in, g, out, res, words;
+};
+inline __host__ __device__ MkCnt mk_cnt_layout(int D, int Ek) {
+  MkCnt c{};
+  int o = 0;
+  c.x = o; o += 8;
+  c.fin = o; o += 8;
+  c.in = o; o += 8 * (2 * Ek / 128);
+  c.g = o; o += 8 * (Ek / 64);
+  c.out = o; o += 8 * (D / 128);
+  c.res = o; o += 8 * (D / 128);
+  c.words = o;
+  return c;
+}
+size_t mk_smem_bytes(int BP, int P, int R, int ncmax, int ring, int nbr);
+int mk_ring_slots(int BP, int P, int R, int ncmax, int nbr);
+cudaError_t launch_decode_mk(const MkParams& p, int BP, int grid, cudaStream_t s);
+cudaError_t preload_decode_mk();
+
 // Load every kernel eagerly (called once per process from ssm_tp_init when a device exists).
 cudaError_t preload_kernels();
 cudaError_t preload_gemm_simt();

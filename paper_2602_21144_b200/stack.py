@@ -7,6 +7,8 @@ from __future__ import annotations
 
 import os
 
+from ctypes import c_float as C_float
+
 import torch
 
 from . import _lib as L
@@ -48,7 +50,10 @@ class MixerStack:
     partial, torch.distributed all-reduces it in bf16, torch adds it to the residual)."""
 
     def __init__(self, mixer: TPMixer, layers: list, batch: int, max_chunk: int, flags=L.SSM_AR2_INT8,
-                 norm_eps=1e-5, nccl_group=None):
+                 norm_eps=1e-5, nccl_group=None, persistent=None):
+        """persistent: decode every token with ONE launch of the persistent whole-stack kernel
+        (ssm_stack_decode) when the library supports the configuration (TP=1, bf16, packed
+        weights, ...).  None = use it when supported; False = always per-layer calls."""
         self.mx, self.layers, self.batch, self.flags, self.eps = mixer, layers, batch, flags, norm_eps
         self.nccl = nccl_group if flags == L.SSM_AR2_EXTERNAL else None
         d = mixer.dims
@@ -62,6 +67,32 @@ class MixerStack:
             self.part = torch.empty((batch * max_chunk, d.d_model), dtype=torch.float32, device=mixer.device)
         self.graph = None
         self.graph_launches = 0
+        self.stack_ws = None
+        if persistent is not False and self.nccl is None:
+            self._bind_persistent(required=bool(persistent))
+
+    def _bind_persistent(self, required=False):
+        import ctypes as C
+        from .mixer import _ptr, _stream
+        nl = len(self.layers)
+        nb = C.c_size_t()
+        rc = L.LIB.ssm_stack_bytes(self.mx.handle, nl, self.batch, C.byref(nb))
+        packed = all(lw.struct.w_in_pk and lw.struct.w_out_pk for lw in self.layers)
+        if rc != 0 or not packed:
+            if required:
+                raise L.SSMError(rc or 8, "ssm_stack_bytes", L.LIB.ssm_last_error().decode() if rc else
+                                 "layers are not packed (LayerWeights.pack)")
+            return
+        self._layer_arr = (L.ssm_layer_weights_t * nl)(*[lw.struct for lw in self.layers])
+        self._state_arr = (C.c_void_p * nl)(*[st.handle.value for st in self.states])
+        self.stack_ws = torch.zeros(nb.value, dtype=torch.uint8, device=self.mx.device)
+        L.call("ssm_stack_bind", self.mx.handle, C.cast(self._layer_arr, C.c_void_p), C.cast(self._state_arr, C.c_void_p), nl, self.batch,
+               _ptr(self.stack_ws), nb.value, _stream(None))
+
+    def stack_check(self, stream=None):
+        from .mixer import _ptr, _stream
+        if self.stack_ws is not None:
+            L.call("ssm_stack_check", self.mx.handle, _ptr(self.stack_ws), _stream(stream))
 
     def reset(self, stream=None):
         for s in self.states:
@@ -80,6 +111,11 @@ class MixerStack:
 
     def decode_step(self, res_t, stream=None):
         """res_t: [batch, D] fp32, updated in place through all layers."""
+        if self.stack_ws is not None:
+            from .mixer import _ptr, _stream
+            L.call("ssm_stack_decode", self.mx.handle, _ptr(self.stack_ws), _ptr(res_t), C_float(self.eps),
+                   _stream(stream))
+            return
         skip_norm = _DEBUG_SKIP_NORM
         for lw, st in zip(self.layers, self.states):
             if not skip_norm:

@@ -83,3 +83,85 @@ extern "C" int probe_bulk(const void* p, long long bytes, int grid, int S, int C
     bulk_stream<<<grid, 32, sm, s>>>((const char*)p, bytes, S, CH, sink);
     return (int)cudaGetLastError();
 }
+
+// Burst probe: each CTA issues `n` bulk copies of `ch` bytes (all in flight at once, one mbarrier),
+// waits for all, `reps` times.  Time per burst tells whether TMA bulk copies overlap.
+extern "C" __global__ void bulk_burst(const char* __restrict__ p, long long span, int n, int ch, int reps,
+                                      int issuers, int* sink) {
+    extern __shared__ __align__(128) char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    char* buf = smem + 1024;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    const char* src = p + ((long long)blockIdx.x * n * ch) % (span - (long long)n * ch);
+    for (int r = 0; r < reps; ++r) {
+        if (threadIdx.x == 0) mbar_expect(bar, (unsigned)(n * ch));
+        __syncwarp();
+        if (threadIdx.x < issuers) {
+            for (int i = threadIdx.x; i < n; i += issuers)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        (unsigned)__cvta_generic_to_shared(buf + (size_t)i * ch)),
+                    "l"(src + (long long)i * ch), "r"(ch), "r"((unsigned)__cvta_generic_to_shared(bar))
+                    : "memory");
+        }
+        if (threadIdx.x == 0) mbar_wait(bar, r & 1);
+        __syncwarp();
+    }
+    if (buf[0] == 123 && buf[1] == 45) sink[0] = 1;
+}
+
+extern "C" int probe_burst(const void* p, long long span, int grid, int n, int ch, int reps, int issuers, int* sink,
+                           cudaStream_t s) {
+    int sm = 1024 + n * ch;
+    cudaFuncSetAttribute(bulk_burst, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    bulk_burst<<<grid, 32, sm, s>>>((const char*)p, span, n, ch, reps, issuers, sink);
+    return (int)cudaGetLastError();
+}
+
+// mbarrier try_wait cost on an already-completed phase (cycles per call), and elect/syncwarp cost
+extern "C" __global__ void mbar_cost(long long* out, int iters) {
+    __shared__ uint64_t bar[4];
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+        long long t0 = clock64();
+        unsigned okc = 0;
+        for (int i = 0; i < iters; ++i) {
+            unsigned ok;
+            asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+                         : "=r"(ok) : "r"(a), "r"(0u) : "memory");
+            okc += ok;
+        }
+        long long t1 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            unsigned ok;
+            asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+                         : "=r"(ok) : "r"(a), "r"(0u) : "memory");
+            okc += ok;
+        }
+        long long t2 = clock64();
+        unsigned long long g0, g1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+        for (int i = 0; i < iters; ++i) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+        }
+        long long t3 = clock64();
+        out[0] = (t1 - t0) / iters;
+        out[1] = (t2 - t1) / iters;
+        out[2] = (t3 - t2) / iters;
+        out[3] = okc;
+    }
+}
+extern "C" int probe_mbar(long long* out, int iters, cudaStream_t s) {
+    mbar_cost<<<1, 32, 0, s>>>(out, iters);
+    return (int)cudaGetLastError();
+}
