@@ -53,7 +53,9 @@ class MixerStack:
                  norm_eps=1e-5, nccl_group=None, persistent=None):
         """persistent: decode every token with ONE launch of the persistent whole-stack kernel
         (ssm_stack_decode) when the library supports the configuration (TP=1, bf16, packed
-        weights, ...).  None = use it when supported; False = always per-layer calls."""
+        weights, ...).  True = required; False = per-layer calls; None = the environment's
+        SSM_PERSISTENT_DECODE=1 opts in (default off: measured slower than the per-layer graph,
+        DESIGN.md §6c)."""
         self.mx, self.layers, self.batch, self.flags, self.eps = mixer, layers, batch, flags, norm_eps
         self.nccl = nccl_group if flags == L.SSM_AR2_EXTERNAL else None
         d = mixer.dims
@@ -68,8 +70,11 @@ class MixerStack:
         self.graph = None
         self.graph_launches = 0
         self.stack_ws = None
-        if persistent is not False and self.nccl is None:
-            self._bind_persistent(required=bool(persistent))
+        required = bool(persistent)
+        if persistent is None:
+            persistent = os.environ.get("SSM_PERSISTENT_DECODE") == "1"
+        if persistent and self.nccl is None:
+            self._bind_persistent(required=required)
 
     def _bind_persistent(self, required=False):
         import ctypes as C

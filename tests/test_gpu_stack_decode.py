@@ -124,5 +124,6 @@ def test_stack_decode_unsupported_configs_raise():
     dims = synth.MixerDims(d_model=256, d_inner=512, dt_rank=16)
     lw = LayerWeights(dims, prep_weights(dims, 0, "bf16"), 1, 0, "bf16")
     assert MixerStack(mx, [lw], 4, 4).stack_ws is None
+    assert MixerStack(mx, [lw], 4, 4, persistent=None).stack_ws is None  # opt-in only
     with pytest.raises(L.SSMError):
         MixerStack(mx, [lw], 4, 4, persistent=True)
