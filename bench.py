@@ -148,8 +148,14 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_baseline(dims, n_layers, prompt=512, decode=8):
-    dt, toks = oracle_sample(dims, prompt, decode)
+def cpu_baseline(dims, n_layers, prompt=512, decode=8, target_s=12.0):
+    """Oracle on a bounded sample: one layer, batch 1, prompt + decode tokens, scaled by a power
+    of two (after a calibration run) so the timed sample takes about target_s seconds of CPU."""
+    dt, toks = oracle_sample(dims, prompt, decode)  # calibration
+    if dt < target_s:
+        f = 2 ** max(0, math.ceil(math.log2(target_s / max(dt, 1e-3))))
+        prompt, decode = prompt * min(f, 256), decode * min(f, 256)
+        dt, toks = oracle_sample(dims, prompt, decode)
     per_layer = toks / dt
     return {"value": per_layer / n_layers, "unit": "tokens/s", "cores": blas_threads() or len(os.sched_getaffinity(0)),
             "affinity_cores": len(os.sched_getaffinity(0)), "cpu": cpu_model(), "kind": "oracle",

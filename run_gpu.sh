@@ -38,3 +38,6 @@ esac
 case " $* " in *" mbar "*)
   timeout 120 python scripts/mbar_probe.py 2>&1 | tail -2 ;;
 esac
+case " $* " in *" mkfull "*)
+  SSM_PERSISTENT_DECODE=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_mk -c 1 -o gpurun_out/mk_full_$TAG python scripts/stack_trace.py mamba2.8b 16 > gpurun_out/mk_full_$TAG.log 2>&1; tail -2 gpurun_out/mk_full_$TAG.log; ls gpurun_out/ | grep mk_full ;;
+esac
