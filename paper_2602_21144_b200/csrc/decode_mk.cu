@@ -48,6 +48,7 @@ constexpr int MK_N = 16;                       // d_state
 constexpr int MK_KH = 3;                       // decode-step items per thread with loads issued early
 constexpr uint64_t MK_TIMEOUT_NS = 4000000000ull;  // 4 s: a decode token takes ~1 ms
 constexpr float LOG2E = 1.4426950408889634f;
+__device__ int g_mk_testwait = 1;  // experiment switch: mbarrier.test_wait (1) or try_wait (0) polling
 
 struct MkLayout {
   uint32_t ring, bars, bring, wx, wdt, sd, sdl, su, sub, sdt, sa2, sbdt, sdsk, scb, scw, sal, sconv, srs, sns, red,
@@ -168,9 +169,20 @@ SSM_DEV bool mk_poll(const unsigned* p, uint32_t target, unsigned* err, uint64_t
 }
 
 // mbarrier wait that gives up (and raises the error word) instead of hanging the GPU.
+// Non-blocking probe of an mbarrier phase (mbarrier.test_wait never suspends the thread).
+SSM_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 SSM_DEV bool mk_wait(uint64_t* bar, uint32_t parity, unsigned* err, uint64_t t0) {
   uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
+  while (!((g_mk_testwait) ? mbar_test_wait(bar, parity) : mbar_try_wait(bar, parity))) {
     if (n > 4) __nanosleep(64);  // long waits: leave the issue slots to the working warps
     if ((++n & 255u) == 0u) {
       if (mk_err(err)) return false;
@@ -186,30 +198,47 @@ SSM_DEV bool mk_wait(uint64_t* bar, uint32_t parity, unsigned* err, uint64_t t0)
 // Warp-wide wait: one lane polls the mbarrier (32 pollers per warp would crowd the SM's
 // synchronisation unit that also services the producers' arrivals), the warp then converges.
 SSM_DEV void mk_wait_warp(uint64_t* bar, uint32_t parity, unsigned* err, uint64_t t0) {
-  if ((threadIdx.x & 31) == 0) mk_wait(bar, parity, err, t0);
-  __syncwarp();
+  // every lane probes (converged): a lone polling lane with its warp parked at __syncwarp crawls
+  uint32_t n = 0;
+  while (!__all_sync(0xffffffffu, mbar_test_wait(bar, parity))) {
+    if (n > 4) __nanosleep(32);
+    if ((++n & 255u) == 0u) {
+      if (mk_err(err)) return;
+      if (globaltimer() - t0 > MK_TIMEOUT_NS) {
+        if ((threadIdx.x & 31) == 0) atomicExch(err, 2u);
+        return;
+      }
+    }
+  }
 }
 
 // Grid-wide barrier of the consumer warps (kernel start only).  Monotonic arrival counter: this
 // CTA's arrival `old` belongs to round old / grid -- no reset between launches.
 SSM_DEV void mk_grid_sync(unsigned long long* bar, unsigned* err, uint64_t t0) {
   named_bar_sync(1, MK_CONSUMERS);
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned long long G = gridDim.x;
-    const unsigned long long old = atomicAdd(bar, 1ull);
-    const unsigned long long target = (old / G + 1ull) * G;
+  if (threadIdx.x < 32) {  // warp 0 arrives and polls, converged (lane 0 alone would crawl)
+    unsigned long long target = 0;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned long long G = gridDim.x;
+      const unsigned long long old = atomicAdd(bar, 1ull);
+      target = (old / G + 1ull) * G;
+    }
+    target = __shfl_sync(0xffffffffu, target, 0);
     uint32_t n = 0;
-    while (ld_acquire_gpu_u64(bar) < target) {
+    while (true) {
+      const bool done = threadIdx.x == 0 ? ld_acquire_gpu_u64(bar) >= target : true;
+      if (__all_sync(0xffffffffu, done)) break;
       if ((++n & 63u) == 0u) {
-        if (mk_err(err)) break;
-        if (globaltimer() - t0 > MK_TIMEOUT_NS) {
-          atomicExch(err, 1u);
+        const bool bad = mk_err(err) || globaltimer() - t0 > MK_TIMEOUT_NS;
+        if (__any_sync(0xffffffffu, bad)) {
+          if (threadIdx.x == 0) atomicExch(err, 1u);
           break;
         }
       }
     }
-    __threadfence();
+    if (threadIdx.x == 0) __threadfence();
+    __syncwarp();
   }
   named_bar_sync(1, MK_CONSUMERS);
 }
@@ -279,16 +308,28 @@ SSM_DEV void mk_epi(const Rings& rg, uint32_t& tc, int ub, int ue, int nkb, floa
 // here; the 256 consumer threads have all loads in flight at once.)
 template <int BP>
 SSM_DEV void mk_stage_b(unsigned char* smem, const MkLayout& L, const Rings& rg, uint32_t& bitc, int ub, int ue,
-                        int nkb, const __nv_bfloat16* src, unsigned* err, uint64_t t0) {
+                        int nkb, const __nv_bfloat16* src, unsigned* err, uint64_t t0, int dbg = 0,
+                        unsigned long long* dbg_tr = nullptr) {
   const int tid = threadIdx.x;
   const int n = ue - ub;
   if (n <= 0) return;
   constexpr int PPT = BP * 128 / 16;  // 16-B pieces per k-block tile
-  if (tid == 0)
-    for (int j = 0; j < n; ++j) {  // slot free: the MMAs of its previous use completed
+  if (tid < 32 && !(dbg & 256)) {
+    // slots free (the MMAs of their previous use completed): warp 0 probes up to 32 slots at once
+    // and stays converged (a lone polling lane with its warp parked at a barrier crawled)
+    const unsigned long long tw = clock64();
+    unsigned long long tries = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + (int)tid;
       const uint32_t b = bitc + j;
-      mk_wait(&rg.bempty[b % rg.nbr], ((b / rg.nbr) & 1u) ^ 1u, err, t0);
+      bool ok = j >= n;
+      while (!__all_sync(0xffffffffu, ok)) {
+        if (!ok) ok = mbar_test_wait(&rg.bempty[b % rg.nbr], ((b / rg.nbr) & 1u) ^ 1u);
+        ++tries;
+      }
     }
+    if (dbg_tr && tid == 0) { dbg_tr[0] = clock64() - tw; dbg_tr[1] = tries; }
+  }
   named_bar_sync(1, MK_CONSUMERS);
   const int tot = n * PPT;
   for (int q0 = tid; q0 < tot; q0 += 8 * MK_CONSUMERS) {
@@ -313,8 +354,8 @@ SSM_DEV void mk_stage_b(unsigned char* smem, const MkLayout& L, const Rings& rg,
   }
   fence_proxy_async();  // generic smem writes -> tcgen05.mma (async proxy) reads
   named_bar_sync(1, MK_CONSUMERS);
-  if (tid == 0)
-    for (int j = 0; j < n; ++j) mbar_arrive(&rg.bfull[(bitc + j) % rg.nbr]);
+  if (tid < 32)
+    for (int j = tid; j < n; j += 32) mbar_arrive(&rg.bfull[(bitc + j) % rg.nbr]);
   bitc += n;
 }
 
@@ -372,37 +413,46 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const MkParams
   unsigned* cnt = p.cnt;
   const uint32_t bsz = mk_bsz(BP);
 
-  if (warp == MK_WPROD) {  // ---------------- weight stream
-    if (lane == 0 && !(p.dbg & 2)) {
+  if (warp == MK_WPROD) {  // ---------------- weight stream (warp-uniform; lane 0 issues)
+    if (!(p.dbg & 2)) {
       const bool pf = !(p.dbg & 4);
       // L2 prefetches about one phase ahead of the ring (W_out(l) while the ring fills with
       // W_in(l); W_in(l+1) while it fills with W_out(l)): HBM keeps streaming through the
       // latency-bound phases; the ring then refills from L2.
       const size_t in_lo = (size_t)u0 * MK_TILE, in_bytes = (size_t)(u1 - u0) * MK_TILE;
       const size_t out_lo = (size_t)v0 * MK_TILE, out_bytes = (size_t)(v1 - v0) * MK_TILE;
-      if (p.n_layers > 0 && pf) mk_prefetch(p.layers[0].w_in_pk, in_lo, in_bytes);
+      const bool ld = lane == 0;
+      if (p.n_layers > 0 && pf && ld) mk_prefetch(p.layers[0].w_in_pk, in_lo, in_bytes);
       uint32_t it = 0;
       for (int l = 0; l < p.n_layers; ++l) {
         const MkLayer& Ly = p.layers[l];
-        mk_stamp(p, l, 12);
-        if (pf) mk_prefetch(Ly.w_out_pk, out_lo, out_bytes);
+        if (ld) mk_stamp(p, l, 12);
+        if (pf && ld) mk_prefetch(Ly.w_out_pk, out_lo, out_bytes);
         if (nc > 0)  // the decode step's h rows: into L2 now, read in phase B
-          for (int b = 0; b < B; ++b) prefetch_l2(Ly.h + ((int64_t)b * Ek + c0) * MK_N, (uint32_t)nc * MK_N * 4);
+          for (int b = lane; b < B; b += 32) prefetch_l2(Ly.h + ((int64_t)b * Ek + c0) * MK_N, (uint32_t)nc * MK_N * 4);
         for (int u = u0; u < u1; ++u, ++it) {
           const int s = it % p.ring;
-          if (!mk_wait(&rg.empty[s], ((it / p.ring) & 1u) ^ 1u, p.err, t0)) return;
-          mbar_arrive_expect_tx(&rg.full[s], MK_TILE);
-          bulk_load_evict_first(smem + L.ring + (size_t)s * MK_TILE,
-                                reinterpret_cast<const char*>(Ly.w_in_pk) + (int64_t)u * MK_TILE, MK_TILE, &rg.full[s]);
+          mk_wait_warp(&rg.empty[s], ((it / p.ring) & 1u) ^ 1u, p.err, t0);
+          if (mk_err(p.err)) return;
+          if (ld) {
+            mbar_arrive_expect_tx(&rg.full[s], MK_TILE);
+            bulk_load_evict_first(smem + L.ring + (size_t)s * MK_TILE,
+                                  reinterpret_cast<const char*>(Ly.w_in_pk) + (int64_t)u * MK_TILE, MK_TILE, &rg.full[s]);
+          }
+          __syncwarp();
         }
-        mk_stamp(p, l, 13);
-        if (l + 1 < p.n_layers && pf) mk_prefetch(p.layers[l + 1].w_in_pk, in_lo, in_bytes);
+        if (ld) mk_stamp(p, l, 13);
+        if (l + 1 < p.n_layers && pf && ld) mk_prefetch(p.layers[l + 1].w_in_pk, in_lo, in_bytes);
         for (int v = v0; v < v1; ++v, ++it) {
           const int s = it % p.ring;
-          if (!mk_wait(&rg.empty[s], ((it / p.ring) & 1u) ^ 1u, p.err, t0)) return;
-          mbar_arrive_expect_tx(&rg.full[s], MK_TILE);
-          bulk_load_evict_first(smem + L.ring + (size_t)s * MK_TILE,
-                                reinterpret_cast<const char*>(Ly.w_out_pk) + (int64_t)v * MK_TILE, MK_TILE, &rg.full[s]);
+          mk_wait_warp(&rg.empty[s], ((it / p.ring) & 1u) ^ 1u, p.err, t0);
+          if (mk_err(p.err)) return;
+          if (ld) {
+            mbar_arrive_expect_tx(&rg.full[s], MK_TILE);
+            bulk_load_evict_first(smem + L.ring + (size_t)s * MK_TILE,
+                                  reinterpret_cast<const char*>(Ly.w_out_pk) + (int64_t)v * MK_TILE, MK_TILE, &rg.full[s]);
+          }
+          __syncwarp();
         }
       }
     }
@@ -453,8 +503,10 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const MkParams
             if (!(p.dbg & 16)) umma_bf16(rg.tmem + (uint32_t)(buf * 32), ad + (uint64_t)(ks * 2), bd + (uint64_t)(ks * 2), idesc,
                       (first && ks == 0) ? 0u : 1u);
           const unsigned long long q1_ = clock64();
-          umma_commit(&rg.empty[s]);
-          umma_commit(&rg.bempty[bs]);
+          if (!(p.dbg & 256)) {
+            umma_commit(&rg.empty[s]);
+            umma_commit(&rg.bempty[bs]);
+          }
           const unsigned long long q2_ = clock64();
           w_mma += q1_ - q0_;
           w_com += q2_ - q1_;
@@ -574,7 +626,8 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const MkParams
     }
     cp_async_commit();
     if (st0) mk_stamp(p, l, 1);
-    mk_stage_b<BP>(smem, L, rg, bitc, u0, u1, nkb1, (p.dbg & 32) ? Ly.w_in_pk : p.residB, p.err, t0);
+    mk_stage_b<BP>(smem, L, rg, bitc, u0, u1, nkb1, (p.dbg & 32) ? Ly.w_in_pk : p.residB, p.err, t0, p.dbg,
+                   p.trace ? p.trace + ((size_t)cta * p.n_layers + l) * 32 + 28 : nullptr);
     if (st0) mk_stamp(p, l, 23);
     mk_epi<BP>(rg, tc, u0, u1, nkb1, p.xzT, p.err, t0, [&](int) {});
     if (st0) mk_stamp(p, l, 2);
@@ -825,7 +878,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) decode_mk_kernel(const MkParams
 
     // ================= phase D: out_proj (a8) + residual add (a9, TP=1) + row-tile finalisation
     const bool last_layer = l + 1 == p.n_layers;
-    mk_stage_b<BP>(smem, L, rg, bitc, v0, v1, nkb4, p.gT, p.err, t0);
+    mk_stage_b<BP>(smem, L, rg, bitc, v0, v1, nkb4, p.gT, p.err, t0, p.dbg);
     if (st0) mk_stamp(p, l, 22);
     mk_epi<BP>(rg, tc, v0, v1, nkb4, p.residT, p.err, t0, [&](int rt) {
       if (!(p.dbg & 8)) __threadfence();  // this thread's partials of residual row tile rt are performed

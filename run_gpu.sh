@@ -24,7 +24,7 @@ case " $* " in *" mktime "*)
   timeout 300 python scripts/stack_decode_time.py mamba2.8b 64 > gpurun_out/mk_time_$TAG.txt 2>&1; tail -4 gpurun_out/mk_time_$TAG.txt ;;
 esac
 case " $* " in *" mkdbg "*)
-  for d in 0; do echo "SSM_MK_DBG=$d"; SSM_MK_DBG=$d timeout 300 python scripts/stack_trace.py mamba2.8b 16 2>&1 | tail -22; done > gpurun_out/mk_dbg_$TAG.txt 2>&1; cat gpurun_out/mk_dbg_$TAG.txt ;;
+  for d in 0 2; do echo "SSM_MK_DBG=$d"; SSM_MK_DBG=$d timeout 300 python scripts/stack_trace.py mamba2.8b 16 2>&1 | tail -22; done > gpurun_out/mk_dbg_$TAG.txt 2>&1; cat gpurun_out/mk_dbg_$TAG.txt ;;
 esac
 case " $* " in *" mkncu "*)
   for d in 0 4; do SSM_MK_DBG=$d timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:decode_mk -c 2 python scripts/stack_trace.py mamba2.8b 16 > gpurun_out/mk_ncu_${d}_$TAG.txt 2>&1; echo "DBG=$d"; grep -E "dram__|gpu__time|lts__" gpurun_out/mk_ncu_${d}_$TAG.txt | tail -5; done ;;
@@ -40,4 +40,7 @@ case " $* " in *" mbar "*)
 esac
 case " $* " in *" mkfull "*)
   SSM_PERSISTENT_DECODE=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_mk -c 1 -o gpurun_out/mk_full_$TAG python scripts/stack_trace.py mamba2.8b 16 > gpurun_out/mk_full_$TAG.log 2>&1; tail -2 gpurun_out/mk_full_$TAG.log; ls gpurun_out/ | grep mk_full ;;
+esac
+case " $* " in *" commitprobe "*)
+  timeout 120 python scripts/commit_probe.py 2>&1 | tail -2 ;;
 esac

@@ -71,3 +71,4 @@ for k, nm in ((30, "A: MMA wait weights"), (31, "A: MMA wait B"), (26, "D: MMA w
 for k, nm in ((10, "A: MMA issue (elected lane)"), (11, "A: issue+commit+syncwarp"), (14, "A: MMA loop total")):
     d = acc[:, 1:, k] / 1965.0
     print(f"  {nm:28s} median {np.median(d):7.2f} us (clock64)")
+print("  A staging bempty waits: %.2f us (clock64), failed try_waits median %d" % (np.median(acc[:, 1:, 28]) / 1965.0, np.median(acc[:, 1:, 29])))

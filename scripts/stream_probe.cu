@@ -165,3 +165,60 @@ extern "C" int probe_mbar(long long* out, int iters, cudaStream_t s) {
     mbar_cost<<<1, 32, 0, s>>>(out, iters);
     return (int)cudaGetLastError();
 }
+
+// Does an mbarrier last arrived by tcgen05.commit cost more to probe than one arrived by a thread?
+extern "C" __global__ void commit_probe(long long* out, int mode) {
+    __shared__ __align__(8) uint64_t bar[32];
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 32; ++i) mbar_init(bar + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"((unsigned)__cvta_generic_to_shared(&tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    __syncthreads();
+    if (threadIdx.x == 32) {
+        for (int i = 0; i < 22; ++i) {
+            unsigned a = (unsigned)__cvta_generic_to_shared(bar + i);
+            if (mode == 1)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(a) : "memory");
+            else
+                asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(a) : "memory");
+        }
+    }
+    // wait (thread 0) until the last one completed, then time 22 probes of completed phases
+    if (threadIdx.x == 0) {
+        unsigned a = (unsigned)__cvta_generic_to_shared(bar + 21);
+        unsigned ok = 0;
+        while (!ok) asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a) : "memory");
+        long long t0 = clock64();
+        unsigned c = 0;
+        for (int i = 0; i < 22; ++i) {
+            unsigned a2 = (unsigned)__cvta_generic_to_shared(bar + i);
+            asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a2) : "memory");
+            c += ok;
+        }
+        long long t1 = clock64();
+        for (int i = 0; i < 22; ++i) {
+            unsigned a2 = (unsigned)__cvta_generic_to_shared(bar + i);
+            asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a2) : "memory");
+            c += ok;
+        }
+        long long t2 = clock64();
+        out[mode * 4 + 0] = t1 - t0;
+        out[mode * 4 + 1] = t2 - t1;
+        out[mode * 4 + 2] = c;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tslot));
+    }
+}
+extern "C" int probe_commit(long long* out, cudaStream_t s) {
+    commit_probe<<<1, 128, 0, s>>>(out, 0);
+    commit_probe<<<1, 128, 0, s>>>(out, 1);
+    return (int)cudaGetLastError();
+}
