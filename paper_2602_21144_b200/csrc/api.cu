@@ -53,6 +53,9 @@ const int g_dbg_skip = [] { const char* e = getenv("SSM_DEBUG_SKIP"); return e ?
 // entry and griddepcontrol.wait before touching memory a predecessor writes, so a successor's
 // launch and prologue overlap the predecessor's tail (measured 45.3 -> 42.2 us per Mamba-2.8B
 // decode layer with the fused in_proj).  SSM_PDL=0 disables.
+// Decode GEMMs with fewer tiles than SMs use the spare SMs to L2-prefetch the next weight stream
+// (SSM_L2_PREFETCH=1 enables; off by default: the decode GEMMs are not HBM-bound, r01 profiles).
+const bool g_l2_prefetch = [] { const char* e = getenv("SSM_L2_PREFETCH"); return e && atoi(e) != 0; }();  // measured: no gain (profiles)
 const bool g_pdl_enabled = [] { const char* e = getenv("SSM_PDL"); return !e || atoi(e) != 0; }();
 struct PdlScope {
   bool prev;
@@ -329,6 +332,10 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       e.hl = hl;
       e.cph = t->cph;
       if (!oacc) { e.zero = odst; e.nzero = nD; }  // out_proj partial target (AR#2 follows)
+      if (g_l2_prefetch) {  // spare SMs: this layer's W_out into L2 for the out_proj two kernels on
+        e.pf = w->w_out_pk ? w->w_out_pk : w->w_out;
+        e.pf_bytes = (int64_t)D * Ek * 2;
+      }
       CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, e, s, true, w->w_in_pk));
     } else if (swap)
       CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s, true, w->w_in_pk));

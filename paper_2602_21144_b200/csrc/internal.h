@@ -31,6 +31,11 @@ struct Epilogue {
   // buffer a LATER kernel accumulates into (saves a memset launch on the decode path).
   float* zero;
   int64_t nzero;
+  // Any kind: a weight range the NEXT kernel streams.  When set, the GEMM launches on every SM and
+  // the CTAs without a tile (the decode GEMMs have fewer tiles than SMs) issue L2 prefetches of
+  // [pf, pf + pf_bytes) and exit: HBM time the tile CTAs leave idle fetches the successor's weights.
+  const void* pf;
+  int64_t pf_bytes;
   // EPI_DECODE_INPROJ (SURVEY.md §8 rows a1-a3 fused for one decode token).
   // Output rows m are in_proj features: m < Ek are x channels -> causal conv step over the cached
   // window cst + SiLU -> u (bf16 [N][Ek]) and the window shifted in place; Ek <= m < 2Ek are z

@@ -8,7 +8,7 @@ smoke) timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke_$TAG.txt 2
 bench) timeout 900 python bench.py > gpurun_out/bench_$TAG.txt 2>&1; tail -1 gpurun_out/bench_$TAG.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('BENCH', d['value'], d['ttft_ms'], d['tpot_ms'], d['roofline']['frac'], d['clocks'])" ;;
 benchq) timeout 900 python bench.py --no-cpu --no-e2e $BARGS > gpurun_out/benchq_$TAG.txt 2>&1; tail -1 gpurun_out/benchq_$TAG.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('BENCHQ', d['value'], d['ttft_ms'], d['tpot_ms'], d['roofline']['frac'])" ;;
 ncu) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --layers 2 --prompt 2048 --decode 8 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_launch_$TAG.log 2>&1; tail -1 gpurun_out/ncu_launch_$TAG.log ;;
-ablate) (for m in 0 8 16 23 31; do SSM_DEBUG_SKIP=$m timeout 120 python scripts/decode_ablation.py; done; SSM_FUSE_DECODE=0 timeout 120 python scripts/decode_ablation.py; echo dstep-fused-in-out_proj; SSM_FUSE_DSTEP=1 timeout 120 python scripts/decode_ablation.py) > gpurun_out/ablate_$TAG.txt 2>&1; cat gpurun_out/ablate_$TAG.txt ;;
+ablate) (for m in 0 1 8 16 24 25 31; do SSM_DEBUG_SKIP=$m timeout 120 python scripts/decode_ablation.py; done; SSM_DEBUG_SKIP_NORM=1 timeout 120 python scripts/decode_ablation.py; SSM_PDL=0 timeout 120 python scripts/decode_ablation.py) > gpurun_out/ablate_$TAG.txt 2>&1; cat gpurun_out/ablate_$TAG.txt ;;
 micro) timeout 600 python scripts/gemm_micro.py > gpurun_out/micro_$TAG.txt 2>&1; cat gpurun_out/micro_$TAG.txt ;;
 decexp) timeout 600 python scripts/decode_gemm_exp.py > gpurun_out/decexp_$TAG.txt 2>&1; cat gpurun_out/decexp_$TAG.txt ;;
 esac
@@ -43,4 +43,10 @@ case " $* " in *" mkfull "*)
 esac
 case " $* " in *" commitprobe "*)
   timeout 120 python scripts/commit_probe.py 2>&1 | tail -2 ;;
+esac
+case " $* " in *" pfab "*)
+  (for v in 1 0; do SSM_L2_PREFETCH=$v timeout 120 python scripts/decode_ablation.py; SSM_L2_PREFETCH=$v SSM_DEBUG_SKIP=24 timeout 120 python scripts/decode_ablation.py; SSM_L2_PREFETCH=$v SSM_DEBUG_SKIP=8 timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/pfab_$TAG.txt 2>&1; cat gpurun_out/pfab_$TAG.txt ;;
+esac
+case " $* " in *" kbsab "*)
+  (for k in 2 3 4 6; do SSM_GEMM_KBS=$k timeout 120 python scripts/decode_ablation.py; SSM_GEMM_KBS=$k SSM_DEBUG_SKIP=24 timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/kbsab_$TAG.txt 2>&1; cat gpurun_out/kbsab_$TAG.txt ;;
 esac
