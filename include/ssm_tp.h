@@ -177,6 +177,30 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
                               const void* x_in, float* residual, int32_t batch,
                               uint32_t flags, void* workspace, size_t ws_bytes, void* stream);
 
+/* ---- Decode chain (TP = 1): the pre-norm RMSNorm folded into the neighbouring kernels --------
+ * A stack step x = RMSNorm(residual) (weight 1, eps norm_eps; reading Q16); residual += mixer(x)
+ * repeated over layers, without a separate norm kernel per layer: the per-row factor 1/rms
+ * factors out of the in_proj contraction (PAPER.md:152-154 is linear in x), so
+ *   ssm_decode_chain_begin: x_out = bf16(residual) (NOT normalised) and the per-row sums of
+ *     squares into the workspace (once per token, before the first layer);
+ *   ssm_mixer_decode_chained: one decode layer whose in_proj takes that un-normalised x_io and
+ *     scales its accumulators by 1/rms; its out_proj (split-K atomics into `residual`) ends with
+ *     the last contributor of every residual tile writing bf16(residual') into x_io and the new
+ *     sums of squares -- the next layer's inputs.  Same arithmetic as ssm_rmsnorm +
+ *     ssm_mixer_decode up to bf16 rounding order.  x_io [batch, D] bf16 in/out; the workspace
+ *     (>= ssm_workspace_bytes(batch, 1)) carries the chain state between the calls of one token:
+ *     pass the same one to every call.
+ * ssm_decode_chain_supported: *ok = 1 when the configuration qualifies (TP=1, bf16, no AR#1,
+ *   the fused decode in_proj: batch <= 32, P <= 256 even, 2 <= K <= 4, 128 | channels per head,
+ *   d_model % 128 == 0; w may be NULL).  ssm_mixer_decode_chained returns SSM_ERR_UNSUPPORTED
+ *   otherwise. */
+ssm_status_t ssm_decode_chain_supported(ssm_tp_t tp, const ssm_layer_weights_t* w, int32_t batch, int32_t* ok);
+ssm_status_t ssm_decode_chain_begin(ssm_tp_t tp, const float* residual, void* x_out, int32_t batch, void* workspace,
+                                    size_t ws_bytes, void* stream);
+ssm_status_t ssm_mixer_decode_chained(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, void* x_io,
+                                      float* residual, int32_t batch, float norm_eps, void* workspace,
+                                      size_t ws_bytes, void* stream);
+
 /* Quantised all-reduce of n fp32 values (n % qar_block == 0), rows of D = d_model:
  * every rank quantises its partial per block (s = amax/127, q = rint(o/s) clamped to
  * +-127), exchanges int8 codes + fp32 scales peer-to-peer, and forms

@@ -117,7 +117,7 @@ size_t sync_offset(const ssm_tp_s* t, int batch) {
 }
 
 struct WsLayout {
-  size_t xz, u, dbc, dlow, bc, delta, g, part, total;
+  size_t xz, u, dbc, dlow, bc, delta, g, part, css, ccnt, total;
 };
 
 WsLayout ws_layout(const ssm_tp_s* t, int64_t M) {
@@ -133,6 +133,8 @@ WsLayout ws_layout(const ssm_tp_s* t, int64_t M) {
   L.delta = take(M * t->Ek * es);
   L.g = take(M * t->Ek * es);
   L.part = take(t->k > 1 ? M * t->cfg.d_model * 4 : 0);
+  L.css = take(M * 4);                                     // decode chain: per-row sums of squares
+  L.ccnt = take(M > 0 ? ((size_t)t->cfg.d_model / 128 + 1) * 4 : 0);  // decode chain: out_proj tile counters
   L.total = off;
   return L;
 }
@@ -248,7 +250,8 @@ Peers group_peers(const ssm_tp_s* t, int gsize) {
 
 // One mixer layer. decode: seqlen == 1 path with in-place state update.
 ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* st, const void* x_in, float* residual,
-                       int batch, int seqlen, uint32_t flags, void* ws, bool decode, cudaStream_t s) {
+                       int batch, int seqlen, uint32_t flags, void* ws, bool decode, cudaStream_t s,
+                       bool chain = false, float norm_eps = 0.f) {
   const ssm_config_t& c = t->cfg;
   const int64_t M = (int64_t)batch * seqlen;
   const int D = c.d_model, Ek = t->Ek, R = c.dt_rank, N = c.d_state, K = c.d_conv, P = t->P, hl = t->hloc;
@@ -315,6 +318,9 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   const bool fuse = swap && !ar1 && t->fuse_decode && batch <= 32 && P <= 256 && P % 2 == 0 && K >= 2 && K <= 4 &&
                     t->cph % 128 == 0 && !(skip & 7) &&
                     gemm_tc_supported(w->w_in, D, x_in, D);
+  float* css = reinterpret_cast<float*>(W + L.css);
+  int* ccnt = reinterpret_cast<int*>(W + L.ccnt);
+  if (chain && (!fuse || skip || t->k != 1)) return fail(SSM_ERR_UNSUPPORTED, "decode chain needs the fused TP=1 decode path");
   if (!(skip & 1)) {
     Probe pr(t, decode ? SSM_PROBE_IN_PROJ_DECODE : SSM_PROBE_IN_PROJ, s);
     if (fuse) {
@@ -332,6 +338,11 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       e.hl = hl;
       e.cph = t->cph;
       if (!oacc) { e.zero = odst; e.nzero = nD; }  // out_proj partial target (AR#2 follows)
+      if (chain) {  // x_in = bf16(residual) un-normalised; the pre-norm's 1/rms applied here
+        e.ss = css;
+        e.ss_scale = 1.0f / (float)D;
+        e.ss_eps = norm_eps;
+      }
       if (g_l2_prefetch) {  // spare SMs: this layer's W_out into L2 for the out_proj two kernels on
         e.pf = w->w_out_pk ? w->w_out_pk : w->w_out;
         e.pf_bytes = (int64_t)D * Ek * 2;
@@ -424,7 +435,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->launches++;
     CU(launch_decode_step(bf, dsrc, nsrc, doff, hl * P, c.bcdt_rmsnorm, c.rms_eps, u,
                           reinterpret_cast<char*>(xz) + Ek * es, 2 * Ek, w->w_dt, w->b_dt, w->a_log, w->d_skip, st->h,
-                          g, batch, Ek, R, N, t->cph, nullptr, s));
+                          g, batch, Ek, R, N, t->cph, nullptr, s, chain ? css : nullptr));
     }
   } else {
     // (a4) unpack dt_low / B / C; (a5) dt_proj + softplus; (a6)+(a7) scan, D skip, gate
@@ -456,6 +467,12 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     if (swap) {
       Epilogue e = epi(EPI_ATOMIC_F32, 1, odst, D);
       if (fuse) { e.zero = xacc; e.nzero = (int64_t)batch * hl * P; }  // re-arm the x_proj accumulator
+      if (chain) {  // last contributor of each residual tile: next layer's bf16 B operand + sums of squares
+        e.fin_cnt = ccnt;
+        e.fin_x = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(x_in));
+        e.fin_ldx = D;
+        e.fin_ss = css;
+      }
       CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, e, s, true, w->w_out_pk, fuse_ds ? &job : nullptr));
     }
     else
@@ -710,6 +727,43 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
   PdlScope pdl(g_pdl_enabled);
   return run_layer(tp, w, st, x_in, residual, batch, 1, flags, workspace, true,
                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+ssm_status_t ssm_decode_chain_supported(ssm_tp_t tp, const ssm_layer_weights_t* w, int32_t batch, int32_t* ok) {
+  if (!tp || !ok) return fail(SSM_ERR_ARG, "NULL argument");
+  const ssm_config_t& c = tp->cfg;
+  *ok = tp->k == 1 && tp->bf16 && tp->ar1_group == 1 && tp->fuse_decode && batch >= 1 && batch <= 32 &&
+        (c.dt_rank + 2 * c.d_state) <= 256 && (c.dt_rank + 2 * c.d_state) % 2 == 0 && c.d_conv >= 2 && c.d_conv <= 4 &&
+        tp->cph % 128 == 0 && c.d_model % 128 == 0 && !g_dbg_skip && (!w || gemm_tc_supported(w->w_in, c.d_model, w->w_in, c.d_model));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_decode_chain_begin(ssm_tp_t tp, const float* residual, void* x_out, int32_t batch, void* workspace,
+                                    size_t ws_bytes, void* stream) {
+  if (!tp || !residual || !x_out || !workspace) return fail(SSM_ERR_ARG, "NULL argument");
+  if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
+  const WsLayout L = ws_layout(tp, batch);
+  if (ws_bytes < L.total) return fail(SSM_ERR_ARG, "workspace too small");
+  char* W = reinterpret_cast<char*>(workspace);
+  tp->launches++;
+  PdlScope pdl(g_pdl_enabled);
+  CU(launch_chain_begin(residual, reinterpret_cast<__nv_bfloat16*>(x_out), reinterpret_cast<float*>(W + L.css),
+                        reinterpret_cast<int*>(W + L.ccnt), tp->cfg.d_model / 128 + 1, batch, tp->cfg.d_model,
+                        reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_mixer_decode_chained(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, void* x_io,
+                                      float* residual, int32_t batch, float norm_eps, void* workspace,
+                                      size_t ws_bytes, void* stream) {
+  ssm_status_t s = check_call(tp, w, st, x_io, residual, batch, 1, 0, workspace, ws_bytes);
+  if (s != SSM_OK) return s;
+  int32_t ok = 0;
+  ssm_decode_chain_supported(tp, w, batch, &ok);
+  if (!ok) return fail(SSM_ERR_UNSUPPORTED, "decode chain: needs TP=1, bf16, the fused decode in_proj shape limits");
+  PdlScope pdl(g_pdl_enabled);
+  return run_layer(tp, w, st, x_io, residual, batch, 1, 0, workspace, true, reinterpret_cast<cudaStream_t>(stream),
+                   true, norm_eps);
 }
 
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {

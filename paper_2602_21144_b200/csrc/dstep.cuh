@@ -32,6 +32,8 @@ struct DStepArgs {
   void* g;               // [batch][Ek] out
   int batch, Ek, R, cph;
   float* zacc;           // optional fp32 z accumulator (read then zeroed)
+  float* zero_ss;        // optional: [batch] floats zeroed by unit (0, 0) once the predecessor finished
+  int h_late;            // experiment (SSM_DSTEP_HLATE=1): load h after griddepcontrol.wait
 };
 
 // W_dt row stride (elements): 16-B aligned, and a 4-word bank shift from row to row (conflict-free LDS.128)
@@ -102,7 +104,26 @@ SSM_DEV void dstep_unit(const DStepArgs& a, const Peers& src, int nsrc, int c0, 
   const bool okd = d < Ek;
   const float bias = okd ? a.b_dt[d] : 0.f;
   const float Dd = okd ? a.d_skip[d] : 0.f;
+  // the items' h rows: owner data of this kernel (the previous token's step), independent of the
+  // predecessor kernels -- in flight before griddepcontrol.wait
+  float hs[IPT][N];
+  auto load_h = [&]() {
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+      const int bi = bl + DS_BB * it;
+      const bool ok = bi < nb && okd;
+      const float* hp = a.h + ((int64_t)(ok ? b0 + bi : 0) * Ek + (ok ? d : 0)) * N;
+#pragma unroll
+      for (int n = 0; n < N; n += 4) {
+        const float4 t4 = ok ? *reinterpret_cast<const float4*>(hp + n) : make_float4(0.f, 0.f, 0.f, 0.f);
+        hs[it][n] = t4.x; hs[it][n + 1] = t4.y; hs[it][n + 2] = t4.z; hs[it][n + 3] = t4.w;
+      }
+    }
+  };
+  if (!a.h_late) load_h();
   if (with_pdl_wait) pdl_wait();  // everything below reads what the predecessor kernels produced
+  if (a.h_late) load_h();
+  if (a.zero_ss && c0 == 0 && b0 == 0 && tid < batch) a.zero_ss[tid] = 0.f;  // (its reader was the predecessor)
   // ---- activations: dbc rows (first source), the items' h rows, u, z -- all loads in flight
   const int p4 = P / 4;
   const int nd = nb * p4;
@@ -122,18 +143,11 @@ SSM_DEV void dstep_unit(const DStepArgs& a, const Peers& src, int nsrc, int c0, 
                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  float hs[IPT][N];
   float uu[IPT], zz[IPT];
 #pragma unroll
   for (int it = 0; it < IPT; ++it) {
     const int bi = bl + DS_BB * it;
     const bool ok = bi < nb && okd;
-    const float* hp = a.h + ((int64_t)(ok ? b0 + bi : 0) * Ek + (ok ? d : 0)) * N;
-#pragma unroll
-    for (int n = 0; n < N; n += 4) {
-      const float4 t4 = ok ? *reinterpret_cast<const float4*>(hp + n) : make_float4(0.f, 0.f, 0.f, 0.f);
-      hs[it][n] = t4.x; hs[it][n + 1] = t4.y; hs[it][n + 2] = t4.z; hs[it][n + 3] = t4.w;
-    }
     uu[it] = ok ? io<T>::ld(reinterpret_cast<const T*>(a.u) + (int64_t)(b0 + bi) * Ek + d) : 0.f;
     zz[it] = 0.f;
     if (a.zacc) {

@@ -286,6 +286,12 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
         }
       }
     }
+    float rsc[16];  // decode chain: the pre-norm's 1/rms of each token row (1 otherwise)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int b = half * 16 + q;
+      rsc[q] = (e.ss && b < N) ? rsqrtf(__ldcg(e.ss + b) * e.ss_scale + e.ss_eps) : 1.f;
+    }
     // ---- accumulator: 16 token columns of this warp's 32 feature rows
     mbar_wait(&tfull[acc], acc_ph);
     tc_fence_after();
@@ -313,7 +319,7 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
         const int b = half * 16 + q;
         float uq = 0.f;
         if (b < N) {
-          const float x = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[q])));
+          const float x = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[q]) * rsc[q]));
           float a = bias;
 #pragma unroll
           for (int j = 0; j < 3; ++j)
@@ -341,7 +347,7 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           const int b = half * 16 + q;
-          if (b < N) C[(int64_t)b * e.ldc] = __float2bfloat16_rn(__uint_as_float(r[q]));
+          if (b < N) C[(int64_t)b * e.ldc] = __float2bfloat16_rn(__uint_as_float(r[q]) * rsc[q]);
         }
       }
 #pragma unroll
@@ -407,21 +413,86 @@ __device__ __forceinline__ void run_dstep_job(const DStepJob& j, float* smem_f) 
   if (j.N == 16) run_dstep_units<__nv_bfloat16, 16, true>(j, smem_f);
   else run_dstep_units<__nv_bfloat16, 8, true>(j, smem_f);
   named_bar_sync(1, 256);
-  if (threadIdx.x == 64) {
-    __threadfence();
-    const unsigned long long G = gridDim.x;
-    const unsigned long long old = atomicAdd(j.sync, 1ull);
-    const unsigned long long target = (old / G + 1) * G;
+  if ((threadIdx.x >> 5) == 2) {  // warp 2 arrives and polls converged (a lone lane would crawl)
+    unsigned long long target = 0;
+    if (threadIdx.x == 64) {
+      __threadfence();
+      const unsigned long long G = gridDim.x;
+      const unsigned long long old = atomicAdd(j.sync, 1ull);
+      target = (old / G + 1) * G;
+    }
+    target = __shfl_sync(0xffffffffu, target, 0);
     const uint64_t t0 = globaltimer();
-    while (ld_acquire_gpu_u64(j.sync) < target) {
+    while (!__all_sync(0xffffffffu, threadIdx.x != 64 || ld_acquire_gpu_u64(j.sync) >= target)) {
       if (globaltimer() - t0 > 2000000000ull) {
-        printf("ssm: decode-step grid barrier timed out (CTA %d)\n", blockIdx.x);
+        if (threadIdx.x == 64) printf("ssm: decode-step grid barrier timed out (CTA %d)\n", blockIdx.x);
         break;
       }
     }
-    fence_proxy_async_global();
+    if (threadIdx.x == 64) fence_proxy_async_global();
+    __syncwarp();
   }
   named_bar_sync(1, 256);
+}
+
+// Decode-chain finaliser of the split-K out_proj (see Epilogue::fin_cnt): run by the 8 epilogue
+// warps after this CTA's atomics for output tile mt.  The last of the fin_need contributions
+// reads the final residual tile back (128 d-columns x N rows), writes its bf16 copy (the next
+// layer's in_proj B operand) and adds its per-row sums of squares (the next pre-norm).
+__device__ __forceinline__ void chain_finalise(const Epilogue& e, int mt, int M, int N, float* scratch) {
+  // scratch: 257 floats of dynamic shared memory carved from the ring (no static __shared__: the
+  // kernel's dynamic allocation is already at the opt-in limit)
+  float (*s_red)[32] = reinterpret_cast<float (*)[32]>(scratch);
+  volatile int& s_last = *reinterpret_cast<volatile int*>(scratch + 256);
+  const int et = threadIdx.x - 64;  // 0..255
+  const int warp = et >> 5, lane = et & 31;
+  // bar.sync makes every epilogue thread's atomics performed relative to thread 0; its gpu-scope
+  // fence then publishes them (cumulativity) before the counter increment
+  named_bar_sync(4, 256);
+  if (et == 0) {
+    __threadfence();
+    const int old = atomicAdd(e.fin_cnt + mt, 1);
+    const bool last = old + 1 == e.fin_need;
+    if (last) e.fin_cnt[mt] = 0;  // all contributions in: reset for the next call
+    s_last = last;
+    __threadfence();
+  }
+  named_bar_sync(4, 256);
+  if (!s_last) return;
+  const float* R = reinterpret_cast<const float*>(e.C);
+  const int m = mt * BM + (et & (BM - 1));
+  float acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+  if (m < M) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int n = (et >> 7) + 2 * j;  // threads 0-127: even rows, 128-255: odd rows
+      if (n < N) {
+        const float v = __ldcg(R + (int64_t)n * e.ldc + m);
+        e.fin_x[(int64_t)n * e.fin_ldx + m] = __float2bfloat16_rn(v);
+        acc[j] = v * v;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s_red[warp][j] = acc[j];
+  named_bar_sync(4, 256);
+  if (et < 32) {
+    const int j = et & 15, half = et >> 4;  // row n = half + 2 j, summed over the 4 warps of that half
+    const int n = half + 2 * j;
+    if (n < N) {
+      const float t = s_red[half * 4 + 0][j] + s_red[half * 4 + 1][j] + s_red[half * 4 + 2][j] + s_red[half * 4 + 3][j];
+      atomicAdd(e.fin_ss + n, t);
+    }
+  }
+  named_bar_sync(4, 256);  // s_red reused by the next tile
 }
 
 // Experiment-only timeline (cr.nomma & 8): per-CTA clock64 offsets of pipeline events.
@@ -665,6 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      if (epi.fin_cnt) chain_finalise(epi, mt, M, N, reinterpret_cast<float*>(smem + cr.ring + 512));
     }
     }
   }
@@ -851,6 +923,10 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     cr.ring -= SU_BYTES;
   }
   if (epi.zero && (reinterpret_cast<uintptr_t>(epi.zero) & 15)) return cudaErrorInvalidValue;
+  if (epi.fin_cnt) {  // decode-chain finaliser scratch (257 floats) after the barrier area
+    extra += 2048;
+    cr.ring -= 2048;
+  }
   if (job.enabled) {
     // B operand = g produced in-kernel: bf16 only, the decode-step smem of two units, one tile per
     // CTA, all CTAs co-resident (grid <= SMs at 1 CTA/SM), decode-step shape limits
@@ -871,7 +947,12 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     const long long W = (long long)ts.units * ts.kb_total;
     grid = (int)(W < cap ? W : cap);
   }
-  { cudaError_t e_ = launch(gemm_tc_kernel, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi,
+  Epilogue epi2 = epi;
+  if (epi2.fin_cnt) {  // decode-chain finaliser: contributions per output m-tile
+    if (ts.streamk || epi2.kind != EPI_ATOMIC_F32 || !epi2.trans || BM != 128) return cudaErrorInvalidValue;
+    epi2.fin_need = ts.ksplit * ts.n_tiles;
+  }
+  { cudaError_t e_ = launch(gemm_tc_kernel, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi2,
                                       A_blocked, lda, K, cr, A_blocked ? 1 : 0, job);
     if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();

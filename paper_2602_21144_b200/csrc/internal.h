@@ -36,6 +36,20 @@ struct Epilogue {
   // [pf, pf + pf_bytes) and exit: HBM time the tile CTAs leave idle fetches the successor's weights.
   const void* pf;
   int64_t pf_bytes;
+  // Decode chain (TP = 1; ssm_mixer_decode_chained): the pre-norm RMSNorm of every layer folded
+  // into the GEMMs around it.  in_proj: the B operand is bf16(residual) un-normalised and each
+  // accumulator column n is scaled by rsqrt(ss[n] * ss_scale + ss_eps) (the per-row 1/rms factors
+  // out of the contraction).  out_proj (split-K atomics into the residual): the last contributor
+  // of an output tile (counter fin_cnt[m-tile], fin_need contributions, reset by the last) writes
+  // bf16 of the final residual tile into fin_x [N][fin_ldx] (the next layer's B operand) and adds
+  // the tile's per-row sums of squares into fin_ss.
+  const float* ss;
+  float ss_scale, ss_eps;
+  int* fin_cnt;
+  int fin_need;
+  __nv_bfloat16* fin_x;
+  int64_t fin_ldx;
+  float* fin_ss;
   // EPI_DECODE_INPROJ (SURVEY.md §8 rows a1-a3 fused for one decode token).
   // Output rows m are in_proj features: m < Ek are x channels -> causal conv step over the cached
   // window cst + SiLU -> u (bf16 [N][Ek]) and the window shifted in place; Ek <= m < 2Ek are z
@@ -122,9 +136,13 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
 cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
                                const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
-                               int N, int ch_per_head, float* zacc, cudaStream_t s);
+                               int N, int ch_per_head, float* zacc, cudaStream_t s, float* zero_ss = nullptr);
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
                            cudaStream_t s);
+// Decode chain start: x = bf16(residual) (un-normalised), ss[b] = sum_d residual[b][d]^2, and the
+// out_proj finaliser counters zeroed.  residual [M][D] fp32.
+cudaError_t launch_chain_begin(const float* x, __nv_bfloat16* y, float* ss, int* cnt, int ncnt, int64_t M, int D,
+                               cudaStream_t s);
 // int8 quantisation of n fp32 values in blocks of blk: q [n] int8, scale [n/blk] f32.
 cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float* scale, cudaStream_t s);
 // out (+)= sum_r s_r q_r over k sources (fixed order 0..k-1).

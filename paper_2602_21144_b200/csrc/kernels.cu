@@ -809,15 +809,55 @@ static cudaError_t dstep_t(const DStepArgs& a, Peers src, int nsrc, cudaStream_t
 cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
                                const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
-                               int N, int ch_per_head, float* zacc, cudaStream_t s) {
+                               int N, int ch_per_head, float* zacc, cudaStream_t s, float* zero_ss) {
   if (batch <= 0) return cudaSuccess;
   if (!dstep_supported(bf16, R, N, ldp, ch_per_head) || nsrc < 1 || nsrc > kMaxTP) return cudaErrorInvalidValue;
   DStepArgs a{};
   a.src_off = src_off; a.ldp = ldp; a.rmsnorm = rmsnorm; a.eps = eps; a.u = u; a.z = z; a.ldz = ldz; a.w_dt = w_dt;
   a.b_dt = b_dt; a.a_log = a_log; a.d_skip = d_skip; a.h = h; a.g = g; a.batch = batch; a.Ek = Ek; a.R = R;
-  a.cph = ch_per_head; a.zacc = zacc;
+  a.cph = ch_per_head; a.zacc = zacc; a.zero_ss = zero_ss;
+  static const int h_late = [] { const char* e = getenv("SSM_DSTEP_HLATE"); return e ? atoi(e) : 0; }();
+  a.h_late = h_late;
   if (bf16) return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(a, src, nsrc, s) : dstep_t<__nv_bfloat16, 8, true>(a, src, nsrc, s);
   return N == 16 ? dstep_t<float, 16, false>(a, src, nsrc, s) : dstep_t<float, 8, false>(a, src, nsrc, s);
+}
+
+// Decode chain start (see internal.h): one 128-thread block per row; block 0 also zeroes the
+// out_proj finaliser counters.
+__global__ void __launch_bounds__(128) chain_begin_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                                          float* __restrict__ ss, int* __restrict__ cnt, int ncnt,
+                                                          int D) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[4];
+  const int64_t row = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (row == 0)
+    for (int i = tid; i < ncnt; i += 128) cnt[i] = 0;
+  float s2 = 0.f;
+  for (int i = tid; i < D / 4; i += 128) {
+    const float4 v = reinterpret_cast<const float4*>(x + row * D)[i];
+    s2 = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, s2))));
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(y + row * D)[i] = pk;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  if ((tid & 31) == 0) red[tid >> 5] = s2;
+  __syncthreads();
+  if (tid == 0) ss[row] = red[0] + red[1] + red[2] + red[3];
+}
+
+cudaError_t launch_chain_begin(const float* x, __nv_bfloat16* y, float* ss, int* cnt, int ncnt, int64_t M, int D,
+                               cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if (D % 4) return cudaErrorInvalidValue;
+  cudaError_t e_ = launch(chain_begin_kernel, (unsigned)M, 128, 0, s, x, y, ss, cnt, ncnt, D);
+  if (e_ != cudaSuccess) return e_;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
@@ -881,7 +921,7 @@ cudaError_t preload_kernels() {
       (const void*)decode_step_kernel<float, 16, false, 1>, (const void*)decode_step_kernel<float, 8, false, 1>,
       (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 4>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 4>,
       (const void*)decode_step_kernel<float, 16, false, 4>, (const void*)decode_step_kernel<float, 8, false, 4>,
-      (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>,
+      (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>, (const void*)chain_begin_kernel,
       (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,
       (const void*)quantize_kernel<8>, (const void*)qar_reduce_kernel, (const void*)f32_reduce_kernel,
       (const void*)peer_barrier_kernel};

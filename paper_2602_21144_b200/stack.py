@@ -70,6 +70,13 @@ class MixerStack:
         self.graph = None
         self.graph_launches = 0
         self.stack_ws = None
+        self.chain = False  # per-layer decode with the pre-norm folded into the GEMMs (ssm_mixer_decode_chained)
+        # opt-in (SSM_DECODE_CHAIN=1): measured slower than the norm kernel it removes
+        if self.nccl is None and os.environ.get("SSM_DECODE_CHAIN", "0") == "1" and layers:
+            import ctypes as C
+            ok = C.c_int32(0)
+            L.call("ssm_decode_chain_supported", mixer.handle, C.byref(layers[0].struct), batch, C.byref(ok))
+            self.chain = bool(ok.value)
         required = bool(persistent)
         if persistent is None:
             persistent = os.environ.get("SSM_PERSISTENT_DECODE") == "1"
@@ -120,6 +127,16 @@ class MixerStack:
             from .mixer import _ptr, _stream
             L.call("ssm_stack_decode", self.mx.handle, _ptr(self.stack_ws), _ptr(res_t), C_float(self.eps),
                    _stream(stream))
+            return
+        if self.chain:
+            import ctypes as C
+            from .mixer import _ptr, _stream
+            L.call("ssm_decode_chain_begin", self.mx.handle, _ptr(res_t), _ptr(self.xbuf_dec), self.batch,
+                   _ptr(self.ws_dec), self.ws_dec.numel(), _stream(stream))
+            for lw, st in zip(self.layers, self.states):
+                L.call("ssm_mixer_decode_chained", self.mx.handle, C.byref(lw.struct), st.handle, _ptr(self.xbuf_dec),
+                       _ptr(res_t), self.batch, C.c_float(self.eps), _ptr(self.ws_dec), self.ws_dec.numel(),
+                       _stream(stream))
             return
         skip_norm = _DEBUG_SKIP_NORM
         for lw, st in zip(self.layers, self.states):

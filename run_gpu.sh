@@ -50,3 +50,12 @@ esac
 case " $* " in *" kbsab "*)
   (for k in 2 3 4 6; do SSM_GEMM_KBS=$k timeout 120 python scripts/decode_ablation.py; SSM_GEMM_KBS=$k SSM_DEBUG_SKIP=24 timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/kbsab_$TAG.txt 2>&1; cat gpurun_out/kbsab_$TAG.txt ;;
 esac
+case " $* " in *" dsfuse "*)
+  (for v in 0 1; do SSM_FUSE_DSTEP=$v timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/dsfuse_$TAG.txt 2>&1; cat gpurun_out/dsfuse_$TAG.txt ;;
+esac
+case " $* " in *" chainab "*)
+  (for v in 1 0; do SSM_DECODE_CHAIN=$v timeout 120 python scripts/decode_ablation.py; done; SSM_DEBUG_SKIP=24 timeout 120 python scripts/decode_ablation.py) > gpurun_out/chainab_$TAG.txt 2>&1; cat gpurun_out/chainab_$TAG.txt ;;
+esac
+case " $* " in *" hlate "*)
+  (for v in 0 1 0 1; do SSM_DSTEP_HLATE=$v timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/hlate_$TAG.txt 2>&1; cat gpurun_out/hlate_$TAG.txt ;;
+esac

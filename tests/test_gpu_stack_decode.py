@@ -127,3 +127,31 @@ def test_stack_decode_unsupported_configs_raise():
     assert MixerStack(mx, [lw], 4, 4, persistent=None).stack_ws is None  # opt-in only
     with pytest.raises(L.SSMError):
         MixerStack(mx, [lw], 4, 4, persistent=True)
+
+
+def test_decode_chain_prenorm_folded_vs_oracle(monkeypatch):
+    """Opt-in decode chain (ssm_decode_chain_begin + ssm_mixer_decode_chained): the pre-norm's
+    1/rms applied inside the in_proj epilogue and the next layer's bf16 input written by the
+    out_proj's last contributor per tile; checked over graph-replayed tokens against the oracle."""
+    monkeypatch.setenv("SSM_DECODE_CHAIN", "1")
+    dims = synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_layers=3)
+    B, L_in, T = 8, 6, 6
+    ws = [prep_weights(dims, l, "bf16") for l in range(3)]
+    g = torch.Generator().manual_seed(11)
+    res0 = torch.randn(B, L_in + T, dims.d_model, generator=g, dtype=torch.float64).float().double()
+    mx = TPMixer(dims, "bf16")
+    lws = [LayerWeights(dims, w, 1, 0, "bf16").pack(mx) for w in ws]
+    st = MixerStack(mx, lws, B, L_in, L.SSM_AR2_INT8, persistent=False)
+    assert st.chain
+    st.prefill_chunk(res0[:, :L_in].float().cuda().contiguous().view(B * L_in, -1))
+    rt = torch.empty(B, dims.d_model, device="cuda")
+    gr = st.capture_decode(rt, warmup=False)
+    outs = []
+    for t in range(L_in, L_in + T):
+        rt.copy_(res0[:, t].float().cuda())
+        gr.replay()
+        outs.append(rt.cpu().clone())
+    ref, _ = M.model_forward(dims, [np64(w) for w in ws], res0.numpy())
+    r0 = res0.numpy()
+    got = torch.stack(outs, 1).double().numpy()
+    assert rel(got - r0[:, L_in:], ref[:, L_in:] - r0[:, L_in:]) < TOL["bf16"]
