@@ -55,6 +55,12 @@ const int g_dbg_skip = [] { const char* e = getenv("SSM_DEBUG_SKIP"); return e ?
 // decode layer with the fused in_proj).  SSM_PDL=0 disables.
 // Decode GEMMs with fewer tiles than SMs use the spare SMs to L2-prefetch the next weight stream
 // (SSM_L2_PREFETCH=1 enables; off by default: the decode GEMMs are not HBM-bound, r01 profiles).
+// SSM_DSTEP_PF=1: the decode-step kernel bulk-prefetches this layer's W_out into L2 (HBM idle there)
+// SSM_INPROJ_SK=1: the fused decode in_proj runs stream-K over all SMs instead of one CTA per
+// 128-row tile (measured slower: 58 vs 40 us per Mamba-2.8B decode layer; the weight stream of
+// the one-tile-per-CTA kernel already runs at ~6.1 TB/s, profiles/r01_gemm_timeline_34.txt)
+const bool g_inproj_sk = [] { const char* e = getenv("SSM_INPROJ_SK"); return e && atoi(e) != 0; }();
+const bool g_dstep_pf = [] { const char* e = getenv("SSM_DSTEP_PF"); return e && atoi(e) != 0; }();
 const bool g_l2_prefetch = [] { const char* e = getenv("SSM_L2_PREFETCH"); return e && atoi(e) != 0; }();  // measured: no gain (profiles)
 const bool g_pdl_enabled = [] { const char* e = getenv("SSM_PDL"); return !e || atoi(e) != 0; }();
 struct PdlScope {
@@ -114,6 +120,15 @@ size_t xacc_offset(const ssm_tp_s* t, int batch) {
 // ... then the grid-barrier counter of the fused decode-step + out_proj kernel (u64, monotonic).
 size_t sync_offset(const ssm_tp_s* t, int batch) {
   return xacc_offset(t, batch) + al256((size_t)batch * t->hloc * t->P * 4);
+}
+// ... then the stream-K accumulator of the fused decode in_proj [2E_k/128][batch][128] fp32 and its
+// per-tile counters (all-zero between calls; the last contributor of a tile re-zeroes its part).
+size_t sk_offset(const ssm_tp_s* t, int batch) { return sync_offset(t, batch) + 256; }
+size_t sk_cnt_offset(const ssm_tp_s* t, int batch) {
+  return sk_offset(t, batch) + al256((size_t)2 * t->Ek * batch * 4);
+}
+size_t h_total_bytes(const ssm_tp_s* t, int batch) {
+  return sk_cnt_offset(t, batch) + al256((size_t)(2 * t->Ek / 128 + 1) * 4);
 }
 
 struct WsLayout {
@@ -343,11 +358,17 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
         e.ss_scale = 1.0f / (float)D;
         e.ss_eps = norm_eps;
       }
+      int ks_in = 1;
+      if (g_inproj_sk && (2 * Ek) % 128 == 0) {  // stream-K over all SMs (80 row tiles < 148 SMs)
+        e.sk_acc = reinterpret_cast<float*>(reinterpret_cast<char*>(st->h) + sk_offset(t, batch));
+        e.sk_cnt = reinterpret_cast<int*>(reinterpret_cast<char*>(st->h) + sk_cnt_offset(t, batch));
+        ks_in = -1;
+      }
       if (g_l2_prefetch) {  // spare SMs: this layer's W_out into L2 for the out_proj two kernels on
         e.pf = w->w_out_pk ? w->w_out_pk : w->w_out;
         e.pf_bytes = (int64_t)D * Ek * 2;
       }
-      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, e, s, true, w->w_in_pk));
+      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, ks_in, e, s, true, w->w_in_pk));
     } else if (swap)
       CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s, true, w->w_in_pk));
     else
@@ -435,7 +456,8 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->launches++;
     CU(launch_decode_step(bf, dsrc, nsrc, doff, hl * P, c.bcdt_rmsnorm, c.rms_eps, u,
                           reinterpret_cast<char*>(xz) + Ek * es, 2 * Ek, w->w_dt, w->b_dt, w->a_log, w->d_skip, st->h,
-                          g, batch, Ek, R, N, t->cph, nullptr, s, chain ? css : nullptr));
+                          g, batch, Ek, R, N, t->cph, nullptr, s, chain ? css : nullptr,
+                          g_dstep_pf && swap ? (w->w_out_pk ? w->w_out_pk : w->w_out) : nullptr, (int64_t)D * Ek * (int64_t)es));
     }
   } else {
     // (a4) unpack dt_low / B / C; (a5) dt_proj + softplus; (a6)+(a7) scan, D skip, gate
@@ -662,7 +684,7 @@ ssm_status_t ssm_state_bytes(ssm_tp_t tp, int32_t batch, size_t* conv_bytes, siz
   if (!tp || !conv_bytes || !h_bytes) return fail(SSM_ERR_ARG, "NULL argument");
   if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
   *conv_bytes = (size_t)batch * (tp->cfg.d_conv - 1) * tp->Ek * tp->es;
-  *h_bytes = sync_offset(tp, batch) + 256;
+  *h_bytes = h_total_bytes(tp, batch);
   return SSM_OK;
 }
 

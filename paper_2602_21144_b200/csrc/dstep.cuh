@@ -34,6 +34,8 @@ struct DStepArgs {
   float* zacc;           // optional fp32 z accumulator (read then zeroed)
   float* zero_ss;        // optional: [batch] floats zeroed by unit (0, 0) once the predecessor finished
   int h_late;            // experiment (SSM_DSTEP_HLATE=1): load h after griddepcontrol.wait
+  const void* pf;        // optional: the successor GEMM's weights, bulk-prefetched into L2 by the blocks
+  int64_t pf_bytes;      //   (weights do not depend on activations; HBM is idle during this kernel)
 };
 
 // W_dt row stride (elements): 16-B aligned, and a 4-word bank shift from row to row (conflict-free LDS.128)

@@ -62,6 +62,12 @@ struct Epilogue {
   const void* wx;             // [hl*P][Ek] bf16 (block-diagonal over local heads)
   float* xacc;                // [N][hl*P] fp32
   int Ek, K, P, hl, cph;
+  // Stream-K fused decode in_proj (sk_acc != NULL): the (tile, k-block) space is cut evenly over
+  // all SMs; a CTA holding part of a tile adds its partial accumulator into sk_acc
+  // [m_tiles][N][128] fp32 (all-zero between calls) and bumps sk_cnt[m-tile]; the last of the
+  // tile's contributors reads the sum back, re-zeroes it and runs the conv / x_proj epilogue.
+  float* sk_acc;
+  int* sk_cnt;
 };
 
 struct Peers {
@@ -136,7 +142,8 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
 cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
                                const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
-                               int N, int ch_per_head, float* zacc, cudaStream_t s, float* zero_ss = nullptr);
+                               int N, int ch_per_head, float* zacc, cudaStream_t s, float* zero_ss = nullptr,
+                               const void* pf = nullptr, int64_t pf_bytes = 0);
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
                            cudaStream_t s);
 // Decode chain start: x = bf16(residual) (un-normalised), ss[b] = sum_d residual[b][d]^2, and the

@@ -512,6 +512,16 @@ template <typename T, int N, bool FAST, int IPT>
 __global__ void __launch_bounds__(DS_THREADS, IPT == 1 ? 5 : 3) decode_step_kernel(DStepArgs a, Peers src, int nsrc) {
   extern __shared__ __align__(16) float dsm[];
   pdl_trigger();
+  if (a.pf && threadIdx.x < 32) {  // this block's slice of the successor's weights into L2
+    const int nb = (int)(gridDim.x * gridDim.y), j = (int)(blockIdx.y * gridDim.x + blockIdx.x);
+    const int64_t per = ((a.pf_bytes + nb - 1) / nb + 15) & ~int64_t(15);
+    const int64_t lo = (int64_t)j * per, hi = lo + per < a.pf_bytes ? lo + per : a.pf_bytes;
+    const char* base = reinterpret_cast<const char*>(a.pf);
+    for (int64_t o = lo + (int64_t)threadIdx.x * 16384; o < hi; o += 32 * 16384) {
+      const int64_t n = hi - o < 16384 ? hi - o : 16384;
+      if (n >= 16) prefetch_l2(base + o, (uint32_t)(n & ~int64_t(15)));
+    }
+  }
   dstep_unit<T, N, FAST, DS_THREADS, IPT>(a, src, nsrc, blockIdx.x * DS_CH, blockIdx.y * DS_BB * IPT, threadIdx.x, dsm,
                                           -1, true);
 }
@@ -809,7 +819,8 @@ static cudaError_t dstep_t(const DStepArgs& a, Peers src, int nsrc, cudaStream_t
 cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
                                const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
-                               int N, int ch_per_head, float* zacc, cudaStream_t s, float* zero_ss) {
+                               int N, int ch_per_head, float* zacc, cudaStream_t s, float* zero_ss,
+                               const void* pf, int64_t pf_bytes) {
   if (batch <= 0) return cudaSuccess;
   if (!dstep_supported(bf16, R, N, ldp, ch_per_head) || nsrc < 1 || nsrc > kMaxTP) return cudaErrorInvalidValue;
   DStepArgs a{};
@@ -818,6 +829,8 @@ cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, i
   a.cph = ch_per_head; a.zacc = zacc; a.zero_ss = zero_ss;
   static const int h_late = [] { const char* e = getenv("SSM_DSTEP_HLATE"); return e ? atoi(e) : 0; }();
   a.h_late = h_late;
+  a.pf = pf;
+  a.pf_bytes = pf ? pf_bytes : 0;
   if (bf16) return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(a, src, nsrc, s) : dstep_t<__nv_bfloat16, 8, true>(a, src, nsrc, s);
   return N == 16 ? dstep_t<float, 16, false>(a, src, nsrc, s) : dstep_t<float, 8, false>(a, src, nsrc, s);
 }

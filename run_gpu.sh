@@ -59,3 +59,22 @@ esac
 case " $* " in *" hlate "*)
   (for v in 0 1 0 1; do SSM_DSTEP_HLATE=$v timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/hlate_$TAG.txt 2>&1; cat gpurun_out/hlate_$TAG.txt ;;
 esac
+case " $* " in *" l2floor "*)
+  (for v in 0 1; do SSM_DSTEP_PF=$v timeout 200 python scripts/l2_floor.py; done; SSM_DEBUG_SKIP=8 timeout 200 python scripts/l2_floor.py; SSM_DEBUG_SKIP=16 timeout 200 python scripts/l2_floor.py) > gpurun_out/l2floor_$TAG.txt 2>&1; cat gpurun_out/l2floor_$TAG.txt ;;
+esac
+case " $* " in *" skab "*)
+  (for v in 1 0 1 0; do SSM_INPROJ_SK=$v timeout 120 python scripts/decode_ablation.py; done; SSM_INPROJ_SK=1 SSM_DEBUG_SKIP=24 timeout 120 python scripts/decode_ablation.py; SSM_INPROJ_SK=1 SSM_DSTEP_PF=1 timeout 120 python scripts/decode_ablation.py) > gpurun_out/skab_$TAG.txt 2>&1; cat gpurun_out/skab_$TAG.txt ;;
+esac
+case " $* " in *" skprof "*)
+  (for v in 0 1; do echo "SK=$v"; SSM_INPROJ_SK=$v timeout 200 python scripts/decode_profile.py; SSM_INPROJ_SK=$v SSM_PDL=0 timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/skprof_$TAG.txt 2>&1; cat gpurun_out/skprof_$TAG.txt ;;
+esac
+case " $* " in *" skprobe "*)
+  timeout 200 python scripts/sk_probe.py > gpurun_out/skprobe_$TAG.txt 2>&1; cat gpurun_out/skprobe_$TAG.txt ;;
+esac
+case " $* " in *" coab "*)
+  (timeout 120 python scripts/decode_ablation.py; SSM_DSTEP_IPT=4 timeout 120 python scripts/decode_ablation.py;
+   for r in 192 160 128; do echo "ring $r"; SSM_GEMM_RING_KB=$r timeout 120 python scripts/decode_ablation.py; SSM_DSTEP_IPT=4 SSM_GEMM_RING_KB=$r timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/coab_$TAG.txt 2>&1; cat gpurun_out/coab_$TAG.txt ;;
+esac
+case " $* " in *" ringab "*)
+  (for r in 0 192 176 160 144 112; do echo "dec ring $r"; SSM_DEC_RING_KB=$r timeout 120 python scripts/decode_ablation.py; done; echo "160+pf"; SSM_DSTEP_PF=1 timeout 120 python scripts/decode_ablation.py; echo "160 skip24"; SSM_DEBUG_SKIP=24 timeout 120 python scripts/decode_ablation.py; echo "160 skip8"; SSM_DEBUG_SKIP=8 timeout 120 python scripts/decode_ablation.py; echo "160 skip16"; SSM_DEBUG_SKIP=16 timeout 120 python scripts/decode_ablation.py) > gpurun_out/ringab_$TAG.txt 2>&1; cat gpurun_out/ringab_$TAG.txt ;;
+esac
