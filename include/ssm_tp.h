@@ -72,7 +72,13 @@ enum {
   SSM_AR2_EXTERNAL = 0x4,  /* no AR#2: `residual` receives this rank's fp32 partial out_proj
                               (overwritten, not added) so the caller can all-reduce it itself
                               (the NCCL baseline arm)                                            */
-  SSM_QAR_ACCUMULATE = 0x10 /* ssm_qallreduce: out += result instead of out = result            */
+  SSM_AR2_FP16 = 0x8,      /* AR#2 = the paper's FP32 -> FP16 wire: each rank
+                              casts its fp32 partial to fp16 (IEEE RNE), exchanges it peer-to-peer,
+                              and every rank forms sum_{r=0..k-1} fl32(h_r) in fp32, left to right
+                              in rank order (reading Q21); the paper-literal ablation arm        */
+  SSM_QAR_ACCUMULATE = 0x10, /* ssm_qallreduce: out += result instead of out = result           */
+  SSM_QAR_FP16 = 0x20       /* ssm_qallreduce: fp16 wire (as SSM_AR2_FP16) instead of int8 blocks;
+                              n % 8 == 0                                                         */
 };
 
 enum { SSM_COMM_VIRTUAL = 0x1 }; /* ssm_comm_t.flags: all peer buffers live on THIS device
@@ -163,7 +169,7 @@ ssm_status_t ssm_state_free(ssm_state_t st);
  *   x_in     [batch*seqlen, D] cfg.dtype, replicated on all ranks (block input after the pre-norm)
  *   residual [batch*seqlen, D] fp32, replicated; residual += mixer(x_in)
  *            (with SSM_AR2_EXTERNAL: residual := this rank's partial out_proj)
- *   flags    SSM_AR2_INT8 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL (ignored when tp_size == 1)
+ *   flags    SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL (ignored when tp_size == 1)
  *   workspace >= ssm_workspace_bytes(batch, seqlen) bytes of device memory, 256-B aligned.
  * Errors: SSM_ERR_CACHE if st was allocated for another handle or batch;
  *         SSM_ERR_ARG if the symmetric buffer is too small for batch*seqlen tokens. */
@@ -206,7 +212,8 @@ ssm_status_t ssm_mixer_decode_chained(ssm_tp_t tp, const ssm_layer_weights_t* w,
  * +-127), exchanges int8 codes + fp32 scales peer-to-peer, and forms
  * out = sum_{r=0..k-1} s_r q_r in fixed rank order in fp32 (bitwise identical on all
  * ranks).  out may alias partial.  tp_size == 1: out = partial (no quantisation).
- * flags: SSM_QAR_ACCUMULATE.  Error bound per element: sum_r s_r / 2. */
+ * flags: SSM_QAR_ACCUMULATE, SSM_QAR_FP16.  Error bound per element: sum_r s_r / 2 (int8);
+ * sum_r (|o_r| 2^-11 + 2^-25) + the fp32 additions (fp16 wire). */
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n,
                             uint32_t flags, void* stream);
 

@@ -75,3 +75,39 @@ def northstar_bound(partials, block):
         amaxes.append(np.max(np.abs(o.reshape(o.shape[:-1] + (n // block, block))), axis=-1))
     m = np.max(np.stack(amaxes), axis=0)
     return np.repeat(k * m / 254.0, block, axis=-1)
+
+
+# ---------------------------------------------------------------------------------------------
+# FP16-wire all-reduce: the paper's own quantisation (§4.4, "quantizing the
+# communicated tensors to a lower-precision representation (FP16, from FP32) for transfer and
+# reduction, and then dequantizing them back"; "we quantize from the default FP32
+# precision to FP16").  Readings (Q21): the cast is IEEE round-to-nearest-even
+# (overflow -> inf, as the cast defines); the one-shot schedule reduces the k fp16 values in
+# fp32, fixed rank order 0..k-1 (acc = fl32(h_0); acc = fl32(acc + fl32(h_r))), and the fp32
+# sum is added to the fp32 residual (Q9).  Every step is an IEEE-defined operation, so the GPU
+# must reproduce it bit for bit.
+
+def fp16_cast(o):
+    """fl16(o) with round-to-nearest-even (numpy's float32 -> float16 cast)."""
+    return np.asarray(o, dtype=np.float32).astype(np.float16)
+
+
+def fp16_allreduce(partials):
+    """partials: k float32 arrays.  Returns the float32 sum of the fp16-cast partials formed
+    left to right in fp32 (fixed rank order), and the fp16 wire arrays."""
+    wire = [fp16_cast(o) for o in partials]
+    acc = wire[0].astype(np.float32)
+    for h in wire[1:]:
+        acc = (acc + h.astype(np.float32)).astype(np.float32)
+    return acc, wire
+
+
+def fp16_error_bound(partials):
+    """Per element: sum_r (|o_r| 2^-11 + 2^-25) (cast error: half an fp16 ulp, relative 2^-11
+    in the normal range, absolute 2^-25 in the subnormal range) + the fp32 additions
+    ((k-1) roundings of at most 2^-24 |partial sum| each, bounded via sum_r |o_r| (1 + 2^-11))."""
+    a = np.sum([np.abs(np.asarray(o, dtype=np.float64)) for o in partials], axis=0)
+    k = len(partials)
+    cast = a * 2.0 ** -11 + k * 2.0 ** -25
+    adds = (k - 1) * 2.0 ** -24 * (a * (1 + 2.0 ** -11) + k * 2.0 ** -25)
+    return cast + adds

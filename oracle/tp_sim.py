@@ -5,7 +5,7 @@ Channel splitter (§4.2) and packed-parameter placement
 (PAPER.md:306-311): AR#1 on the SSM-parameter projection, AR#2 at the
 residual boundary.  Reduction order is fixed 0..k-1 (Q12).
 Readings: A/D row-sharded (C4), B/C taken from AR#1's full vector (C5),
-AR#1 unquantised (Q3), AR#2 exact or int8 (qar_ref, Q6-Q9).
+AR#1 unquantised (Q3), AR#2 exact, int8 (qar_ref, Q6-Q9) or the paper's fp16 wire (Q21).
 Zamba heads (Q17): channel d belongs to head d // (E/H); AR#1 sums only over
 the ranks that own channels of a head.
 """
@@ -153,6 +153,9 @@ def tp_mixer_forward(dims, w, x_in, residual, k, states=None, ar2="exact", block
             total = total + partial_out[r]
     elif ar2 == "int8":
         total, _, _ = qar_ref.qallreduce([p.astype(np.float32) for p in partial_out], block)
+    elif ar2 == "fp16":                            # the paper's FP32 -> FP16 wire
+        total, _ = qar_ref.fp16_allreduce([p.astype(np.float32) for p in partial_out])
+        total = total.astype(np.float64)
     else:
         raise ValueError(ar2)
     if k > 1:

@@ -56,6 +56,13 @@ const int g_dbg_skip = [] { const char* e = getenv("SSM_DEBUG_SKIP"); return e ?
 // Decode GEMMs with fewer tiles than SMs use the spare SMs to L2-prefetch the next weight stream
 // (SSM_L2_PREFETCH=1 enables; off by default: the decode GEMMs are not HBM-bound, r01 profiles).
 // SSM_DSTEP_PF=1: the decode-step kernel bulk-prefetches this layer's W_out into L2 (HBM idle there)
+// SSM_OUT_LOCAL=1: the decode step runs inside a channel-owned out_proj (DStepJob::local) instead
+// of its own kernel before the split-K out_proj.  Measured slower (48-73 vs 38.6 us per
+// Mamba-2.8B decode layer over Q in {1,2,4,8}: 256 threads per SM run the latency-bound step)
+const bool g_out_local = [] { const char* e = getenv("SSM_OUT_LOCAL"); return e && atoi(e) != 0; }();
+// channel-owned out_proj shape: SSM_OUT_Q m-groups per k-split of SSM_OUT_KBS 64-channel k-blocks
+const int g_out_q = [] { const char* e = getenv("SSM_OUT_Q"); return e ? atoi(e) : 4; }();
+const int g_out_kbs = [] { const char* e = getenv("SSM_OUT_KBS"); return e ? atoi(e) : 4; }();
 // SSM_INPROJ_SK=1: the fused decode in_proj runs stream-K over all SMs instead of one CTA per
 // 128-row tile (measured slower: 58 vs 40 us per Mamba-2.8B decode layer; the weight stream of
 // the one-tile-per-CTA kernel already runs at ~6.1 TB/s, profiles/r01_gemm_timeline_34.txt)
@@ -127,8 +134,12 @@ size_t sk_offset(const ssm_tp_s* t, int batch) { return sync_offset(t, batch) + 
 size_t sk_cnt_offset(const ssm_tp_s* t, int batch) {
   return sk_offset(t, batch) + al256((size_t)2 * t->Ek * batch * 4);
 }
-size_t h_total_bytes(const ssm_tp_s* t, int batch) {
+// ... then the channel-owned out_proj's group-barrier counters (u64 per k-split, monotonic)
+size_t grp_offset(const ssm_tp_s* t, int batch) {
   return sk_cnt_offset(t, batch) + al256((size_t)(2 * t->Ek / 128 + 1) * 4);
+}
+size_t h_total_bytes(const ssm_tp_s* t, int batch) {
+  return grp_offset(t, batch) + al256((size_t)(t->Ek / 64 + 1) * 8);
 }
 
 struct WsLayout {
@@ -302,7 +313,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->ar_count++;
     t->bytes_sent += M * hl * P * 4;
   }
-  enum { OUT_RESID, OUT_EXTERNAL, OUT_FP32, OUT_INT8 } omode;
+  enum { OUT_RESID, OUT_EXTERNAL, OUT_FP32, OUT_INT8, OUT_FP16 } omode;
   float* odst;
   if (t->k == 1) {
     omode = OUT_RESID;
@@ -310,6 +321,10 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   } else if (flags & SSM_AR2_EXTERNAL) {
     omode = OUT_EXTERNAL;
     odst = residual;
+  } else if (flags & SSM_AR2_FP16) {
+    omode = OUT_FP16;
+    ep2 = ++t->epoch;
+    odst = part;
   } else if (flags & SSM_AR2_FP32) {
     omode = OUT_FP32;
     ep2 = ++t->epoch;
@@ -424,8 +439,14 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   // Decode step fused into the out_proj GEMM (its epilogue warps produce g, grid barrier, then the
   // B loads): needs one dbc source, real (not virtual) ranks so all CTAs can be co-resident.
   DStepJob job{};
-  const bool fuse_ds = swap && t->fuse_dstep && nsrc == 1 && !(t->flags & SSM_COMM_VIRTUAL) &&
-                       dstep_supported(1, R, N, hl * P, t->cph) && !(skip & 24) && gemm_tc_supported(w->w_out, Ek, g, Ek);
+  // Channel-owned out_proj (opt-in, SSM_OUT_LOCAL=1): Q CTAs per k-split run the decode step of
+  // the split's channels, meet at a group barrier, then their out_proj partials (no grid barrier,
+  // no separate decode-step kernel).
+  const bool local_ds = swap && g_out_local && fuse && nsrc == 1 && dstep_supported(1, R, N, hl * P, t->cph) &&
+                        g_out_q >= 1 && g_out_kbs >= 1 && (g_out_kbs * 64) % (32 * g_out_q) == 0 &&
+                        !(skip & 24) && !chain && gemm_tc_supported(w->w_out, Ek, g, Ek);
+  const bool fuse_ds = local_ds || (swap && t->fuse_dstep && nsrc == 1 && !(t->flags & SSM_COMM_VIRTUAL) &&
+                       dstep_supported(1, R, N, hl * P, t->cph) && !(skip & 24) && gemm_tc_supported(w->w_out, Ek, g, Ek));
   if (fuse_ds) {
     job.enabled = 1;
     job.bf16 = 1;
@@ -448,6 +469,12 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     job.Ek = Ek;
     job.R = R;
     job.cph = t->cph;
+    if (local_ds) {
+      job.local = g_out_q;
+      job.rd_cnt = reinterpret_cast<int*>(reinterpret_cast<char*>(st->h) + sync_offset(t, batch) + 64);
+      job.ndbc = (int64_t)batch * hl * P;
+      job.grp_cnt = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(st->h) + grp_offset(t, batch));
+    }
   }
   if (decode) {
     if (!(skip & 8) && !fuse_ds) {
@@ -488,14 +515,16 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     Probe pr(t, SSM_PROBE_OUT_PROJ, s);
     if (swap) {
       Epilogue e = epi(EPI_ATOMIC_F32, 1, odst, D);
-      if (fuse) { e.zero = xacc; e.nzero = (int64_t)batch * hl * P; }  // re-arm the x_proj accumulator
+      // re-arm the x_proj accumulator (channel-owned mode: its last reader does)
+      if (fuse && !local_ds) { e.zero = xacc; e.nzero = (int64_t)batch * hl * P; }
       if (chain) {  // last contributor of each residual tile: next layer's bf16 B operand + sums of squares
         e.fin_cnt = ccnt;
         e.fin_x = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(x_in));
         e.fin_ldx = D;
         e.fin_ss = css;
       }
-      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, e, s, true, w->w_out_pk, fuse_ds ? &job : nullptr));
+      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, local_ds ? ((Ek + 63) / 64 + g_out_kbs - 1) / g_out_kbs : ks_o, e, s, true, w->w_out_pk,
+              fuse_ds ? &job : nullptr));
     }
     else
       CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D), s));
@@ -508,6 +537,14 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->launches += 2;
     CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
     CU(launch_f32_reduce(t->peers, t->k, half_off(ep2), nD, residual, 1, s));
+  } else if (omode == OUT_FP16) {  // the paper's FP32 -> FP16 wire
+    Probe pr(t, SSM_PROBE_AR2, s);
+    t->launches += 3;
+    CU(launch_f16_cast(part, nD, own_half(ep2), s));
+    t->ar_count++;
+    t->bytes_sent += nD * 2;
+    CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
+    CU(launch_f16_reduce(t->peers, t->k, half_off(ep2), nD, residual, 1, s));
   } else if (omode == OUT_INT8) {
     Probe pr(t, SSM_PROBE_AR2, s);
     int8_t* q = reinterpret_cast<int8_t*>(own_half(ep2));
@@ -536,9 +573,10 @@ ssm_status_t check_call(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* 
   if (!x_in || !residual) return fail(SSM_ERR_ARG, "x_in/residual is NULL");
   if ((reinterpret_cast<uintptr_t>(x_in) | reinterpret_cast<uintptr_t>(residual)) & 15)
     return fail(SSM_ERR_ARG, "x_in/residual must be 16-B aligned");
-  if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL))
+  if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL))
     return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
-  const int nmode = !!(flags & SSM_AR2_INT8) + !!(flags & SSM_AR2_FP32) + !!(flags & SSM_AR2_EXTERNAL);
+  const int nmode = !!(flags & SSM_AR2_INT8) + !!(flags & SSM_AR2_FP16) + !!(flags & SSM_AR2_FP32) +
+                    !!(flags & SSM_AR2_EXTERNAL);
   if (nmode > 1) return fail(SSM_ERR_ARG, "at most one AR#2 mode flag");
   const int64_t M = (int64_t)batch * seqlen;
   const WsLayout L = ws_layout(t, M);
@@ -790,7 +828,7 @@ ssm_status_t ssm_mixer_decode_chained(ssm_tp_t tp, const ssm_layer_weights_t* w,
 
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
   if (!tp || !partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
-  if (flags & ~(uint32_t)SSM_QAR_ACCUMULATE) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  if (flags & ~(uint32_t)(SSM_QAR_ACCUMULATE | SSM_QAR_FP16)) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
   const int blk = tp->cfg.qar_block;
   if (n % blk) return fail(SSM_ERR_DIM, "n=%zu not a multiple of qar_block=%d", n, blk);
   if ((reinterpret_cast<uintptr_t>(partial) | reinterpret_cast<uintptr_t>(out)) & 15)
@@ -803,6 +841,20 @@ ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_
     one.p[0] = const_cast<float*>(partial);
     tp->launches++;
     CU(launch_f32_reduce(one, 1, 0, (int64_t)n, out, acc, s));
+    return SSM_OK;
+  }
+  if (flags & SSM_QAR_FP16) {  // the paper's fp16 wire
+    if (n % 8) return fail(SSM_ERR_DIM, "n=%zu not a multiple of 8 (fp16 wire)", n);
+    if (n * 2 > half_bytes(tp)) return fail(SSM_ERR_ARG, "symmetric buffer too small for n=%zu", n);
+    const uint32_t ep = ++tp->epoch;
+    const size_t half = half_bytes(tp);
+    char* own = reinterpret_cast<char*>(tp->peers.p[tp->rank]) + kSigBytes + (ep & 1) * half;
+    tp->launches += 3;
+    CU(launch_f16_cast(partial, (int64_t)n, own, s));
+    tp->ar_count++;
+    tp->bytes_sent += n * 2;
+    CU(launch_peer_barrier(tp->peers, tp->rank, tp->k, s));
+    CU(launch_f16_reduce(tp->peers, tp->k, (int64_t)(kSigBytes + (ep & 1) * half), (int64_t)n, out, acc, s));
     return SSM_OK;
   }
   const size_t need = al256(n) + n / blk * 4;

@@ -145,21 +145,28 @@ SSM_DEV void dstep_unit(const DStepArgs& a, const Peers& src, int nsrc, int c0, 
                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  float uu[IPT], zz[IPT];
+  // u and z: every item's loads issued back to back with no branch between them (raw bits; the
+  // conversion happens after the shared-memory barrier below), so their latencies overlap each
+  // other and the dbc copy instead of adding up
+  T ur[IPT], zr[IPT];
+  float zz[IPT];
 #pragma unroll
   for (int it = 0; it < IPT; ++it) {
     const int bi = bl + DS_BB * it;
     const bool ok = bi < nb && okd;
-    uu[it] = ok ? io<T>::ld(reinterpret_cast<const T*>(a.u) + (int64_t)(b0 + bi) * Ek + d) : 0.f;
+    const int64_t row = ok ? b0 + bi : b0;
+    const int dd = okd ? d : c0;
+    ur[it] = reinterpret_cast<const T*>(a.u)[row * Ek + dd];
+    if (!a.zacc) zr[it] = reinterpret_cast<const T*>(a.z)[row * a.ldz + dd];
+  }
+#pragma unroll
+  for (int it = 0; it < IPT; ++it) {
     zz[it] = 0.f;
-    if (a.zacc) {
-      if (ok) {
-        float* zp = a.zacc + (int64_t)(b0 + bi) * a.ldz + d;
-        zz[it] = *zp;
-        *zp = 0.f;
-      }
-    } else if (ok) {
-      zz[it] = io<T>::ld(reinterpret_cast<const T*>(a.z) + (int64_t)(b0 + bi) * a.ldz + d);
+    const int bi = bl + DS_BB * it;
+    if (a.zacc && bi < nb && okd) {
+      float* zp = a.zacc + (int64_t)(b0 + bi) * a.ldz + d;
+      zz[it] = *zp;
+      *zp = 0.f;
     }
   }
   // ---- consume into shared memory; partials of the other sources added in fixed rank order
@@ -200,6 +207,13 @@ SSM_DEV void dstep_unit(const DStepArgs& a, const Peers& src, int nsrc, int c0, 
   }
   cp_async_wait<0>();
   dstep_sync<NT>(bar_id);
+  float uu[IPT];
+#pragma unroll
+  for (int it = 0; it < IPT; ++it) {
+    const bool ok = bl + DS_BB * it < nb && okd;
+    uu[it] = ok ? io<T>::ld(&ur[it]) : 0.f;
+    if (!a.zacc) zz[it] = ok ? io<T>::ld(&zr[it]) : 0.f;
+  }
   if (a.rmsnorm) {  // weightless RMSNorm of dt_low, B, C per batch row (Falcon-Mamba, reading Q18)
     const int warp = tid >> 5, lane = tid & 31;
     for (int r = warp; r < nb; r += NT / 32) {

@@ -61,8 +61,19 @@ constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 
 // the head of the next, so partial tiles are combined by the atomic epilogue.
 struct TileSched {
   int m_tiles, n_tiles, kb_total, kbs, ksplit, units, streamk;
+  int kown;  // channel-owned (Q = kown m-groups): CTA i = (k-split i / Q, tiles i % Q + Q j); grid = ksplit * Q
   // iterate segments (mt, nt, kb0, kb1) of this CTA; returns false when done
   __device__ bool next(int& cursor, int& mt, int& nt, int& kb0, int& kb1) const {
+    if (kown) {
+      const int t = (int)blockIdx.x % kown + kown * cursor;
+      if (t >= m_tiles * n_tiles) return false;
+      ++cursor;
+      nt = t % n_tiles;
+      mt = t / n_tiles;
+      kb0 = (int)blockIdx.x / kown * kbs;
+      kb1 = min(kb_total, kb0 + kbs);
+      return true;
+    }
     if (!streamk) {
       const int u = cursor;
       if (u >= units) return false;
@@ -87,7 +98,7 @@ struct TileSched {
     cursor = (int)(pos + (kb1 - kb0));
     return true;
   }
-  __device__ int first() const { return streamk ? -1 : (int)blockIdx.x; }
+  __device__ int first() const { return streamk ? -1 : kown ? 0 : (int)blockIdx.x; }
   // stream-K: number of CTAs whose ranges intersect tile t (ranges are non-empty: W >= gridDim.x)
   __device__ int contributors(int t) const {
     const long long W = (long long)m_tiles * n_tiles * kb_total, G = gridDim.x;
@@ -447,6 +458,80 @@ __device__ void run_dstep_units(const DStepJob& j, float* smem_f) {
   }
 }
 
+// Channel-owned mode (DStepJob::local): the decode step for this CTA's channels only, then the
+// B operand (g of those channels) is published to the CTA's own TMA loads; the last CTA to have
+// consumed dbc re-zeroes it.  Units of 32 channels x 16 batch rows, alternating over the two
+// 128-thread halves of the epilogue warps.
+template <typename T, int N, bool FAST>
+__device__ void run_dstep_local_units(const DStepJob& j, float* smem_f, int c_lo, int c_hi) {
+  const int warp = threadIdx.x >> 5;
+  const int half = (warp - 2) >> 2;
+  const int htid = threadIdx.x - 64 - half * 128;
+  DStepArgs a{};
+  a.src_off = 0; a.ldp = j.ldp; a.rmsnorm = j.rmsnorm; a.eps = j.eps; a.u = j.u; a.z = j.z; a.ldz = j.ldz;
+  a.w_dt = j.w_dt; a.b_dt = j.b_dt; a.a_log = j.a_log; a.d_skip = j.d_skip; a.h = j.h; a.g = j.g;
+  a.batch = j.batch; a.Ek = j.Ek; a.R = j.R; a.cph = j.cph; a.zacc = nullptr;
+  Peers src{};
+  src.p[0] = const_cast<float*>(j.dbc);
+  constexpr int IPT = kJobIpt;
+  const int unit_floats = (int)(dstep_smem(j.R, N, (int)sizeof(T), IPT) / 4);
+  float* my = smem_f + half * unit_floats;
+  const int uc = (c_hi - c_lo + DS_CH - 1) / DS_CH, ub = (j.batch + DS_BB * IPT - 1) / (DS_BB * IPT);
+  for (int unit = half; unit < uc * ub; unit += 2) {
+    dstep_unit<T, N, FAST, DS_THREADS, IPT>(a, src, 1, c_lo + (unit % uc) * DS_CH, (unit / uc) * DS_BB * IPT, htid, my,
+                                            2 + half, false);
+    dstep_sync<DS_THREADS>(2 + half);  // unit smem reused by the next unit
+  }
+}
+
+__device__ __forceinline__ void run_dstep_local(const DStepJob& j, float* smem_f, const TileSched& ts,
+                                                volatile int* s_flag) {
+  const int Q = ts.kown, sl = (int)blockIdx.x / Q, q = (int)blockIdx.x % Q;
+  const int w = ts.kbs * BK / Q;  // channels of this CTA's share of the split (multiple of 32)
+  const int c_lo = sl * ts.kbs * BK + q * w;
+  const int c_hi = min(j.Ek, c_lo + w);
+  if (c_lo < c_hi) {
+    if (j.N == 16) run_dstep_local_units<__nv_bfloat16, 16, true>(j, smem_f, c_lo, c_hi);
+    else run_dstep_local_units<__nv_bfloat16, 8, true>(j, smem_f, c_lo, c_hi);
+  }
+  fence_proxy_async_global();  // this thread's g stores -> the async proxy (the group's TMA B loads)
+  named_bar_sync(1, 256);
+  if ((threadIdx.x >> 5) == 2) {  // warp 2: group barrier (converged polling) + dbc reader count
+    int last = 0;
+    unsigned long long target = 0;
+    if (threadIdx.x == 64) {
+      __threadfence();
+      const int old = atomicAdd(j.rd_cnt, 1);
+      last = old + 1 == (int)gridDim.x;
+      if (last) *j.rd_cnt = 0;
+      if (Q > 1) {
+        const unsigned long long o2 = atomicAdd(j.grp_cnt + sl, 1ull);
+        target = (o2 / Q + 1) * Q;
+      }
+    }
+    if (Q > 1) {
+      target = __shfl_sync(0xffffffffu, target, 0);
+      const uint64_t t0 = globaltimer();
+      while (!__all_sync(0xffffffffu, threadIdx.x != 64 || ld_acquire_gpu_u64(j.grp_cnt + sl) >= target)) {
+        if (globaltimer() - t0 > 2000000000ull) {
+          if (threadIdx.x == 64) printf("ssm: out_proj group barrier timed out (CTA %d)\n", blockIdx.x);
+          break;
+        }
+      }
+    }
+    if (threadIdx.x == 64) {
+      fence_proxy_async_global();
+      *s_flag = last;
+    }
+    __syncwarp();
+  }
+  named_bar_sync(1, 256);
+  if (*s_flag) {  // every CTA has read dbc into its shared memory: re-arm it for the next token
+    float* z = const_cast<float*>(j.dbc);
+    for (int64_t i = threadIdx.x - 64; i < j.ndbc; i += 256) z[i] = 0.f;
+  }
+}
+
 __device__ __forceinline__ void run_dstep_job(const DStepJob& j, float* smem_f) {
   if (j.N == 16) run_dstep_units<__nv_bfloat16, 16, true>(j, smem_f);
   else run_dstep_units<__nv_bfloat16, 8, true>(j, smem_f);
@@ -711,7 +796,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- epilogue warps 2..9; TMEM lane group = warp % 4, column half = (warp-2)/4
     pdl_wait();
     if (job.enabled) {
-      run_dstep_job(job, reinterpret_cast<float*>(smem + cr.ring + 512));
+      if (job.local) {
+        const int js = (int)((2 * dstep_smem(job.R, job.N, 2, kJobIpt) + 127) / 128 * 128);
+        run_dstep_local(job, reinterpret_cast<float*>(smem + cr.ring + 512), ts,
+                        reinterpret_cast<volatile int*>(smem + cr.ring + 512 + js));
+      } else {
+        run_dstep_job(job, reinterpret_cast<float*>(smem + cr.ring + 512));
+      }
       if (threadIdx.x == 64) mbar_arrive(bready);
     }
     if (epi.zero && blockIdx.x == 0) {  // (after the job: it may read the buffer being zeroed)
@@ -901,6 +992,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   ts.ksplit = (ts.kb_total + ts.kbs - 1) / ts.kbs;
   ts.units = ts.m_tiles * ts.n_tiles * ts.ksplit;
   ts.streamk = 0;
+  ts.kown = (job_in && job_in->enabled && job_in->local > 0) ? job_in->local : 0;
   if (ksplit_in < 0) {  // stream-K over all SMs (atomic epilogue)
     ts.streamk = 1;
     ts.ksplit = 1;
@@ -948,9 +1040,12 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   // weight / state loads issued before griddepcontrol.wait) can be co-resident on the SM.
   // Measured 40.4 -> 37.7 us per Mamba-2.8B decode layer; the stream rate is unchanged.
   static const int dec_ring_kb = [] { const char* e = getenv("SSM_DEC_RING_KB"); return e ? atoi(e) : 160; }();
+  static const int out_ring_kb = [] { const char* e = getenv("SSM_OUT_RING_KB"); return e ? atoi(e) : -1; }();
   const char* ring_env = getenv("SSM_GEMM_RING_KB");
-  if (ring_env || (BN <= 32 && dec_ring_kb > 0 && !job.enabled)) {  // smaller CTA footprint
-    cr.ring = (ring_env ? atoi(ring_env) : dec_ring_kb) * 1024;
+  int dec_kb = dec_ring_kb;
+  if (out_ring_kb >= 0 && epi.kind == EPI_ATOMIC_F32) dec_kb = out_ring_kb;  // experiment: split-K decode GEMMs
+  if (ring_env || (BN <= 32 && dec_kb > 0 && !job.enabled)) {  // smaller CTA footprint
+    cr.ring = (ring_env ? atoi(ring_env) : dec_kb) * 1024;
     int cols = 32;
     while (cols < 2 * BN) cols *= 2;
     cr.tmem_cols = cols;
@@ -975,16 +1070,24 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   if (job.enabled) {
     // B operand = g produced in-kernel: bf16 only, the decode-step smem of two units, one tile per
     // CTA, all CTAs co-resident (grid <= SMs at 1 CTA/SM), decode-step shape limits
-    if (!job.bf16 || !job.sync || (job.N != 16 && job.N != 8) || epi.kind == EPI_DECODE_INPROJ ||
-        !dstep_supported(1, job.R, job.N, job.ldp, job.cph) || ts.units > num_sms)
+    if (!job.bf16 || (job.N != 16 && job.N != 8) || epi.kind == EPI_DECODE_INPROJ ||
+        !dstep_supported(1, job.R, job.N, job.ldp, job.cph))
       return cudaErrorInvalidValue;
-    const int js = (int)((2 * dstep_smem(job.R, job.N, 2, kJobIpt) + 127) / 128 * 128);
+    if (job.local) {  // channel-owned: each CTA's share of a split is whole 32-channel units
+      if (!job.rd_cnt || (job.local > 1 && !job.grp_cnt) || (ts.kbs * BK) % (DS_CH * job.local) || ts.streamk ||
+          epi.zero)
+        return cudaErrorInvalidValue;
+    } else if (!job.sync || ts.units > num_sms) {
+      return cudaErrorInvalidValue;
+    }
+    const int js = (int)((2 * dstep_smem(job.R, job.N, 2, kJobIpt) + 127) / 128 * 128) + (job.local ? 128 : 0);
     extra += js;
     cr.ring -= js;
   }
   while (kbs > 1 && num_stages(BN, kbs, cr.ring) < 2) --kbs;
   const int smem_bytes = 1024 + cr.ring + 512 + extra;
   int grid = ts.units < num_sms ? ts.units : num_sms;
+  if (ts.kown) grid = ts.ksplit * ts.kown;  // Q CTAs per channel range
   if (epi.pf && epi.pf_bytes > 0 && !ts.streamk && ts.units < num_sms && !job.enabled) grid = num_sms;  // spare CTAs prefetch
   if (ts.streamk) {
     long long cap = num_sms;

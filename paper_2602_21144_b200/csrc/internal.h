@@ -96,6 +96,19 @@ struct DStepJob {
   float* h;
   void* g;
   int batch, Ek, R, cph;
+  // local != 0: channel-owned mode.  CTA i owns the k-block range (the d_inner channels) of split
+  // i and runs every output m-tile for it; its epilogue warps first run the decode step for
+  // exactly those channels (the step is channel-local, so no grid barrier), then the CTA's B
+  // operand g is loaded.  h and g are written by their owner CTA only.  The dbc rows every CTA
+  // reads are re-zeroed (for the next token's fused in_proj) by the last CTA to finish reading
+  // them (counter rd_cnt, reset by that CTA).
+  // local = Q >= 1 m-groups: CTA i = (k-split i / Q, m-group i % Q) runs the m-tiles q, q + Q, ...
+  // of its split; the split's channels are divided over its Q CTAs for the decode step, which then
+  // meet at a group barrier (grp_cnt[split], monotonic) before loading g of the whole split.
+  int local;
+  int* rd_cnt;
+  int64_t ndbc;  // floats of dbc to re-zero (batch * ldp)
+  unsigned long long* grp_cnt;
 };
 
 // ---- GEMM launchers (return cudaSuccess or the launch error) ----
@@ -156,6 +169,8 @@ cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float
 cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, int64_t n, int blk, float* out,
                               int accumulate, cudaStream_t s);
 cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s);
+cudaError_t launch_f16_cast(const float* x, int64_t n, void* out, cudaStream_t s);
+cudaError_t launch_f16_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s);
 // Cross-rank barrier: advance this rank's device-side epoch counter, write it into slot[rank]
 // of every peer's signal area, wait for all peers' slots in our own area to reach it
 // (bounded; sets the error word on timeout).

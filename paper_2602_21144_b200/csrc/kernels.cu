@@ -233,7 +233,7 @@ constexpr int SC_THREADS = 128;  // channels per block
 // One thread per (batch row, channel); N states in registers; tiles of u, delta, z
 // (bf16 or fp32) and B||C (fp32) staged through shared memory with cp.async double
 // buffering.  h_t = exp(delta A) h_{t-1} + delta B_t u_t;  y = <C_t, h_t> + D u;  g = y SiLU(z).
-template <typename T, int N, bool FAST>
+template <typename T, int N, bool FAST, int NP = 0>
 __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ u, int64_t ldu,
                                                           const T* __restrict__ dl, int64_t ldd,
                                                           const T* __restrict__ z, int64_t ldz,
@@ -333,8 +333,9 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
             const float4 b4 = B4[q], c4 = C4[q];
             const float2 dA0 = fmul2(de2, A2[2 * q]);
             const float2 dA1 = fmul2(de2, A2[2 * q + 1]);
-            const float2 a0 = make_float2(ex2_approx(dA0.x), ex2_approx(dA0.y));
-            const float2 a1 = make_float2(ex2_approx(dA1.x), ex2_approx(dA1.y));
+            // NP of the N states' exponentials on the FMA pipe (exp2_poly2), the rest on MUFU
+            const float2 a0 = (4 * q + 2 <= N - NP) ? make_float2(ex2_approx(dA0.x), ex2_approx(dA0.y)) : exp2_poly2(dA0);
+            const float2 a1 = (4 * q + 4 <= N - NP) ? make_float2(ex2_approx(dA1.x), ex2_approx(dA1.y)) : exp2_poly2(dA1);
             h2[2 * q] = ffma2(a0, h2[2 * q], fmul2(du2, make_float2(b4.x, b4.y)));
             h2[2 * q + 1] = ffma2(a1, h2[2 * q + 1], fmul2(du2, make_float2(b4.z, b4.w)));
             ya = ffma2(make_float2(c4.x, c4.y), h2[2 * q], ya);
@@ -653,6 +654,46 @@ __global__ void f32_reduce_kernel(Peers src, int k, int64_t off, int64_t n4, flo
   *o = acc;
 }
 
+// ---------------------------------------------------------------- fp16-wire all-reduce
+// Cast: 8 fp32 -> 8 fp16 per thread (cvt.rn.f16x2.f32: IEEE round-to-nearest-even, overflow -> inf).
+__global__ void f16_cast_kernel(const float* __restrict__ x, int64_t n8, __half* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  const float4 a = reinterpret_cast<const float4*>(x)[2 * i];
+  const float4 b = reinterpret_cast<const float4*>(x)[2 * i + 1];
+  __half2 h[4] = {__floats2half2_rn(a.x, a.y), __floats2half2_rn(a.z, a.w), __floats2half2_rn(b.x, b.y),
+                  __floats2half2_rn(b.z, b.w)};
+  reinterpret_cast<uint4*>(out)[i] = *reinterpret_cast<const uint4*>(h);
+}
+// Reduce: acc = fl32(h_0); acc = acc + fl32(h_r) for r = 1..k-1 (fixed order: bitwise-identical
+// replicas, Q12); out = out + acc (accumulate) or acc.
+__global__ void f16_reduce_kernel(Peers src, int k, int64_t off, int64_t n8, float* __restrict__ out, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  float acc[8];
+  for (int r = 0; r < k; ++r) {
+    const uint4 raw = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(src.p[r]) + off)[i];
+    const __half2* h = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(h[j]);
+      if (r == 0) { acc[2 * j] = f.x; acc[2 * j + 1] = f.y; }
+      else { acc[2 * j] = acc[2 * j] + f.x; acc[2 * j + 1] = acc[2 * j + 1] + f.y; }
+    }
+  }
+  float4* o = reinterpret_cast<float4*>(out) + 2 * i;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    float4 v = accumulate ? o[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    v.x = v.x + acc[4 * q]; v.y = v.y + acc[4 * q + 1]; v.z = v.z + acc[4 * q + 2]; v.w = v.w + acc[4 * q + 3];
+    o[q] = v;
+  }
+}
+
 // ---------------------------------------------------------------- cross-rank barrier
 // Signal area at the head of every symmetric buffer: uint32 slot[8] (slot[p] = last epoch
 // rank p announced to us), uint32 error word at +64 B, uint32 epoch counter at +128 B.
@@ -710,6 +751,8 @@ cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const fl
 // channel on the FMA-pipe exp2), read once per process
 static int g_scan_version = [] { const char* e = getenv("SSM_SCAN_VERSION"); return e ? atoi(e) : 1; }();
 static int g_scan_npoly = [] { const char* e = getenv("SSM_SCAN_NPOLY"); return e ? atoi(e) : 4; }();
+// states per channel on the FMA-pipe exp2 in the 1-channel kernel (bf16, N = 16): 0, 2, 4 or 6
+static int g_scan_np1 = [] { const char* e = getenv("SSM_SCAN_NP1"); return e ? atoi(e) : 0; }();
 
 // ==================================================================== launchers
 cudaError_t launch_conv1d_silu(int bf16, const void* xz, int64_t ldxz, const void* cs, const float* cw,
@@ -767,12 +810,12 @@ cudaError_t launch_unpack(int bf16, Peers src, int nsrc, int64_t off, int M, int
   return cudaGetLastError();
 }
 
-template <typename T, int N, bool F>
+template <typename T, int N, bool F, int NP = 0>
 static cudaError_t scan_t(const void* u, int64_t ldu, const void* dl, int64_t ldd, const void* z, int64_t ldz,
                           const float* BC, int64_t ldbc, const float* a_log, const float* d_skip, float* h,
                           int64_t hbs, void* g, int64_t ldg, int batch, int L, int nch, cudaStream_t s) {
   dim3 grid((nch + SC_THREADS - 1) / SC_THREADS, batch);
-  { cudaError_t e_ = launch(scan_kernel<T, N, F>, grid, SC_THREADS, 0, s, 
+  { cudaError_t e_ = launch(scan_kernel<T, N, F, NP>, grid, SC_THREADS, 0, s, 
       reinterpret_cast<const T*>(u), ldu, reinterpret_cast<const T*>(dl), ldd, reinterpret_cast<const T*>(z), ldz, BC,
       ldbc, a_log, d_skip, h, hbs, reinterpret_cast<T*>(g), ldg, L, nch); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
@@ -794,6 +837,13 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
     else { cudaError_t e_ = launch(scan2_kernel<16, 6>, grid, S3_THREADS, 0, s, S2A); if (e_ != cudaSuccess) return e_; }
 #undef S2A
     return cudaGetLastError();
+  }
+  if (bf16 && fast && N == 16 && g_scan_np1 > 0) {
+#define S1A u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s
+    if (g_scan_np1 == 2) return scan_t<__nv_bfloat16, 16, true, 2>(S1A);
+    if (g_scan_np1 == 4) return scan_t<__nv_bfloat16, 16, true, 4>(S1A);
+    return scan_t<__nv_bfloat16, 16, true, 6>(S1A);
+#undef S1A
   }
   if (bf16) {
     if (N == 16) return fast ? scan_t<__nv_bfloat16, 16, true>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s)
@@ -906,6 +956,22 @@ cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, in
   return cudaGetLastError();
 }
 
+cudaError_t launch_f16_cast(const float* x, int64_t n, void* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n % 8) return cudaErrorInvalidValue;
+  const int64_t n8 = n / 8;
+  { cudaError_t e_ = launch(f16_cast_kernel, (int)((n8 + 255) / 256), 256, 0, s, x, n8, reinterpret_cast<__half*>(out)); if (e_ != cudaSuccess) return e_; }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_f16_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n % 8) return cudaErrorInvalidValue;
+  const int64_t n8 = n / 8;
+  { cudaError_t e_ = launch(f16_reduce_kernel, (int)((n8 + 255) / 256), 256, 0, s, src, k, off, n8, out, accumulate); if (e_ != cudaSuccess) return e_; }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const int64_t n4 = n / 4;
@@ -937,6 +1003,7 @@ cudaError_t preload_kernels() {
       (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>, (const void*)chain_begin_kernel,
       (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,
       (const void*)quantize_kernel<8>, (const void*)qar_reduce_kernel, (const void*)f32_reduce_kernel,
+      (const void*)f16_cast_kernel, (const void*)f16_reduce_kernel,
       (const void*)peer_barrier_kernel};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);

@@ -78,3 +78,21 @@ esac
 case " $* " in *" ringab "*)
   (for r in 0 192 176 160 144 112; do echo "dec ring $r"; SSM_DEC_RING_KB=$r timeout 120 python scripts/decode_ablation.py; done; echo "160+pf"; SSM_DSTEP_PF=1 timeout 120 python scripts/decode_ablation.py; echo "160 skip24"; SSM_DEBUG_SKIP=24 timeout 120 python scripts/decode_ablation.py; echo "160 skip8"; SSM_DEBUG_SKIP=8 timeout 120 python scripts/decode_ablation.py; echo "160 skip16"; SSM_DEBUG_SKIP=16 timeout 120 python scripts/decode_ablation.py) > gpurun_out/ringab_$TAG.txt 2>&1; cat gpurun_out/ringab_$TAG.txt ;;
 esac
+case " $* " in *" fuseab "*)
+  (echo base; timeout 120 python scripts/decode_ablation.py; echo fuse_dstep; SSM_FUSE_DSTEP=1 timeout 120 python scripts/decode_ablation.py; echo chain; SSM_DECODE_CHAIN=1 timeout 120 python scripts/decode_ablation.py; echo chain+fuse; SSM_DECODE_CHAIN=1 SSM_FUSE_DSTEP=1 timeout 120 python scripts/decode_ablation.py; echo persistent; SSM_PERSISTENT_DECODE=1 timeout 120 python scripts/decode_ablation.py) > gpurun_out/fuseab_$TAG.txt 2>&1; cat gpurun_out/fuseab_$TAG.txt ;;
+esac
+case " $* " in *" outab "*)
+  (for r in 160 128 96 64 48; do echo "out ring $r"; SSM_OUT_RING_KB=$r timeout 120 python scripts/decode_ablation.py; done; echo "out 96 ipt4"; SSM_OUT_RING_KB=96 SSM_DSTEP_IPT=4 timeout 120 python scripts/decode_ablation.py; echo "in 176 out 96"; SSM_DEC_RING_KB=176 SSM_OUT_RING_KB=96 timeout 120 python scripts/decode_ablation.py) > gpurun_out/outab_$TAG.txt 2>&1; cat gpurun_out/outab_$TAG.txt ;;
+esac
+case " $* " in *" scanab "*)
+  (for v in 0 2 4 6 0 4; do SSM_SCAN_NP1=$v SSM_SCAN_NPOLY=$v timeout 120 python scripts/scan_micro.py; done; SSM_SCAN_VERSION=2 SSM_SCAN_NPOLY=4 timeout 120 python scripts/scan_micro.py) > gpurun_out/scanab_$TAG.txt 2>&1; cat gpurun_out/scanab_$TAG.txt ;;
+esac
+case " $* " in *" roof "*)
+  timeout 300 python scripts/kernel_rooflines.py --json gpurun_out/rooflines_$TAG.json > gpurun_out/rooflines_$TAG.txt 2>&1; cat gpurun_out/rooflines_$TAG.txt ;;
+esac
+case " $* " in *" localab "*)
+  (for v in 1 0 1 0; do SSM_OUT_LOCAL=$v timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/localab_$TAG.txt 2>&1; cat gpurun_out/localab_$TAG.txt ;;
+esac
+case " $* " in *" qab "*)
+  (for qk in "4 4" "2 2" "8 8" "1 1" "4 2" "8 4"; do set -- $qk; echo "Q=$1 KBS=$2"; SSM_OUT_Q=$1 SSM_OUT_KBS=$2 timeout 120 python scripts/decode_ablation.py; done; echo "off"; SSM_OUT_LOCAL=0 timeout 120 python scripts/decode_ablation.py; echo "Q4K4 gemmkbs1"; SSM_GEMM_KBS=1 timeout 120 python scripts/decode_ablation.py) > gpurun_out/qab_$TAG.txt 2>&1; cat gpurun_out/qab_$TAG.txt ;;
+esac

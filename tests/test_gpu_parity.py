@@ -294,6 +294,41 @@ def test_virtual_qallreduce_codes_bitexact_and_bound(k):
     assert np.all(np.abs(got - exact) <= Q.northstar_bound(list(parts.numpy()), 128) * (1 + 1e-5) + 1e-7)
 
 
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_virtual_fp16_allreduce_bitexact(k):
+    """The paper's FP32 -> FP16 wire: wire bytes and the fp32 rank-order sum
+    equal the oracle bit for bit; the error stays within the fp16 bound."""
+    dims = MED
+    n = 6 * dims.d_model
+    parts = synth.partials(k, n, seed=200 + k)
+    grp = VirtualGroup(dims, k, "bf16", 64)
+    outs = [torch.empty(n, device="cuda") for _ in range(k)]
+    dev_parts = [parts[r].cuda() for r in range(k)]
+    grp.run(lambda r, mx, s: mx.qallreduce(dev_parts[r], outs[r], stream=s, fp16=True))
+    ref, wire = Q.fp16_allreduce(list(parts.numpy()))
+    half = ((grp.bufs[0].numel() - 256) // 2) & ~255
+    for r in range(k):
+        base = 256 + half  # epoch 1 -> half 1
+        h = grp.bufs[r][base:base + 2 * n].cpu().view(torch.float16).numpy()
+        np.testing.assert_array_equal(h.view(np.uint16), wire[r].view(np.uint16))
+    for r in range(k):
+        np.testing.assert_array_equal(outs[r].cpu().numpy(), ref)
+    exact = parts.double().sum(0).numpy()
+    assert np.all(np.abs(outs[0].cpu().double().numpy() - exact) <= Q.fp16_error_bound(list(parts.numpy())))
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_virtual_tp_mixer_fp16_ar2_vs_oracle(k):
+    dims = MED
+    outs, w, x, res, grp, sts = _tp_virtual(dims, "bf16", k, 2, 40, 4, L.SSM_AR2_FP16)
+    for r in range(1, k):
+        assert torch.equal(outs[r], outs[0])
+    ref, _ = M.mixer_forward(dims, np64(w), x.numpy(), res.numpy())
+    resn = res.numpy()
+    assert rel(outs[0].double().numpy() - resn, ref - resn) < TOL["bf16"]
+    assert grp.mixers[0].stats()["allreduce"] == 2 * (1 + 4)
+
+
 def test_rmsnorm_kernel():
     dims = MED
     mx = TPMixer(dims, "fp32")

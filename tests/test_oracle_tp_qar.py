@@ -154,3 +154,87 @@ def test_tp_int8_ar2_within_bound():
     d = np.abs(q8[0] - ex[0])
     assert d.max() > 0
     assert d.max() / np.abs(ex[0] - res.numpy()).max() < 2 * k / 254 + 1e-6
+
+
+# ---------------------------------------------------------------- FP16-wire all-reduce
+def _golden_fp16():
+    path = os.path.join(os.path.dirname(__file__), "golden", "fp16_cast.txt")
+    rows = []
+    for line in open(path):
+        if line.startswith("#") or not line.strip():
+            continue
+        a, b = line.split()[:2]
+        rows.append((float(a), float(b)))
+    return rows
+
+
+def test_fp16_cast_golden():
+    """Hand-derived binary16 RNE cases (ties to even, overflow midpoint, subnormal ties)."""
+    import warnings
+    for a, b in _golden_fp16():
+        assert np.float32(a) == a, "golden inputs are exact fp32 values"
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            got = float(Q.fp16_cast(np.array([a], dtype=np.float32))[0])
+        assert got == b, (a, got, b)
+
+
+def test_fp16_cast_matches_torch_half():
+    """A second library's IEEE cast (torch CPU .half()) agrees element for element."""
+    import torch
+    rng = np.random.default_rng(5)
+    o = (rng.standard_normal(4096) * np.exp(rng.uniform(-20, 10, 4096))).astype(np.float32)
+    ref = torch.from_numpy(o).half().float().numpy()
+    np.testing.assert_array_equal(Q.fp16_cast(o).astype(np.float32), ref)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_fp16_allreduce_exact_when_representable(k):
+    """Partials that are fp16-exact with an fp32-exact sum: the result is the exact sum."""
+    rng = np.random.default_rng(k)
+    parts = [(rng.integers(-2048, 2048, 512) * 2.0 ** -10).astype(np.float32) for _ in range(k)]
+    got, wire = Q.fp16_allreduce(parts)
+    exact = np.sum([p.astype(np.float64) for p in parts], axis=0)
+    np.testing.assert_array_equal(got.astype(np.float64), exact)
+    for w, p in zip(wire, parts):
+        np.testing.assert_array_equal(w.astype(np.float32), p)
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_fp16_allreduce_within_bound(k):
+    rng = np.random.default_rng(100 + k)
+    parts = [(rng.standard_normal(8192) * np.exp(rng.uniform(-12, 4, 8192))).astype(np.float32) for _ in range(k)]
+    got, _ = Q.fp16_allreduce(parts)
+    exact = np.sum([p.astype(np.float64) for p in parts], axis=0)
+    err = np.abs(got.astype(np.float64) - exact)
+    bound = Q.fp16_error_bound(parts)
+    assert np.all(err <= bound)
+    assert np.max(err / bound) > 0.25  # the bound is not vacuous
+
+
+def test_fp16_allreduce_rank_order_and_k1():
+    """k = 1 is the cast itself; the fp32 reduction runs left to right in rank order."""
+    o = np.array([1.00146484375, 0.1, -3.0], dtype=np.float32)
+    got, _ = Q.fp16_allreduce([o])
+    np.testing.assert_array_equal(got, np.array([1.001953125, 0.0999755859375, -3.0], dtype=np.float32))
+    # 2048 + 2^-13 + 2^-13 in fp32 (ulp(2048) = 2^-12): left to right each add is a tie that
+    # rounds to even (2048) -- the order is part of the definition; (b + b) + a would be exact
+    a = np.array([2048.0], dtype=np.float32)          # fp16-exact
+    b = np.array([2 ** -13], dtype=np.float32)        # fp16-exact (normal)
+    got, _ = Q.fp16_allreduce([a, b, b])
+    assert got[0] == np.float32(2048.0)
+    got, _ = Q.fp16_allreduce([b, b, a])
+    assert got[0] == np.float32(2048.0 + 2 ** -12)
+
+
+def test_tp_fp16_ar2_within_bound():
+    """TP=2 mixer with the paper's fp16 AR#2 stays within the fp16 bound of the exact TP result."""
+    dims = synth.CONFIGS["tiny"]
+    w = {k_: v.numpy() for k_, v in synth.layer_weights(dims, 0).items()}
+    x, res = synth.activations(2, 16, dims.d_model)
+    x, res = x.numpy(), res.numpy()
+    exact, _, _ = T.tp_mixer_forward(dims, w, x, res, 2, ar2="exact")
+    f16, _, _ = T.tp_mixer_forward(dims, w, x, res, 2, ar2="fp16")
+    d = np.abs(f16[0] - exact[0])
+    assert d.max() > 0  # it did quantise
+    assert d.max() <= 2 * 2.0 ** -11 * np.abs(exact[0] - res).max() + 1e-6
