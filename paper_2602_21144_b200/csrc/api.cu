@@ -784,7 +784,9 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
   ssm_status_t s = check_call(tp, w, st, x_in, residual, batch, 1, flags, workspace, ws_bytes);
   if (s != SSM_OK) return s;
   if (batch == 0) return SSM_OK;
-  PdlScope pdl(g_pdl_enabled);
+  // no PDL across virtual ranks: early-launched dependents of one rank's stream would hold the SMs
+  // the other ranks' kernels need to reach the shared barrier
+  PdlScope pdl(g_pdl_enabled && !(tp->flags & SSM_COMM_VIRTUAL));
   return run_layer(tp, w, st, x_in, residual, batch, 1, flags, workspace, true,
                    reinterpret_cast<cudaStream_t>(stream));
 }
@@ -874,8 +876,9 @@ ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_
 
 ssm_status_t ssm_rmsnorm(ssm_tp_t tp, const float* residual, const float* weight, float eps, void* x_out, int64_t M,
                          void* stream) {
-  PdlScope pdl(g_pdl_enabled && M <= 256);  // decode-sized rows: overlap with the neighbours
   if (!tp || !residual || !x_out) return fail(SSM_ERR_ARG, "NULL argument");
+  // decode-sized rows: overlap with the neighbours (not across virtual ranks, see ssm_mixer_decode)
+  PdlScope pdl(g_pdl_enabled && M <= 256 && !(tp->flags & SSM_COMM_VIRTUAL));
   if ((reinterpret_cast<uintptr_t>(residual) | reinterpret_cast<uintptr_t>(weight) | reinterpret_cast<uintptr_t>(x_out)) & 15)
     return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
   tp->launches++;

@@ -96,3 +96,7 @@ esac
 case " $* " in *" qab "*)
   (for qk in "4 4" "2 2" "8 8" "1 1" "4 2" "8 4"; do set -- $qk; echo "Q=$1 KBS=$2"; SSM_OUT_Q=$1 SSM_OUT_KBS=$2 timeout 120 python scripts/decode_ablation.py; done; echo "off"; SSM_OUT_LOCAL=0 timeout 120 python scripts/decode_ablation.py; echo "Q4K4 gemmkbs1"; SSM_GEMM_KBS=1 timeout 120 python scripts/decode_ablation.py) > gpurun_out/qab_$TAG.txt 2>&1; cat gpurun_out/qab_$TAG.txt ;;
 esac
+case " $* " in *" agree "*)
+  timeout 300 python -m pytest tests/test_gpu_agreement.py -q -x -p no:cacheprovider 2>&1 | tail -15
+  timeout 1200 python scripts/agreement.py > gpurun_out/agreement_$TAG.jsonl 2> gpurun_out/agreement_$TAG.err; cat gpurun_out/agreement_$TAG.jsonl; tail -5 gpurun_out/agreement_$TAG.err ;;
+esac

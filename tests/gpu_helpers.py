@@ -54,32 +54,4 @@ def oracle_state_from_gpu_layout(conv, h):
     return conv.float().cpu().double().permute(0, 2, 1).numpy(), h.cpu().double().numpy()
 
 
-class VirtualGroup:
-    """k virtual TP ranks on one GPU: same-device symmetric buffers, one stream per rank
-    (SSM_COMM_VIRTUAL).  Exercises the real peer-to-peer kernels and flag protocol."""
-
-    def __init__(self, dims, k, dtype, max_tokens, qar_block=128):
-        self.k = k
-        cfg = L.make_config(dims, dtype, qar_block)
-        nbytes = L.comm_bytes(cfg, k, max_tokens)
-        self.bufs = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(k)]
-        ptrs = [b.data_ptr() for b in self.bufs]
-        self.mixers = [TPMixer(dims, dtype, rank=r, tp_size=k, peer_bufs=ptrs, buf_bytes=nbytes, virtual=True,
-                               qar_block=qar_block) for r in range(k)]
-        self.streams = [torch.cuda.Stream() for _ in range(k)]
-        torch.cuda.synchronize()
-
-    def run(self, fn):
-        """fn(rank, mixer, stream) enqueues rank r's work on its own stream."""
-        ev = torch.cuda.Event()
-        ev.record()
-        for r in range(self.k):
-            self.streams[r].wait_event(ev)
-        for r in range(self.k):
-            with torch.cuda.stream(self.streams[r]):
-                fn(r, self.mixers[r], self.streams[r])
-        for s in self.streams:
-            torch.cuda.current_stream().wait_stream(s)
-        torch.cuda.synchronize()
-        for r in range(self.k):
-            self.mixers[r].check(self.streams[r])
+from paper_2602_21144_b200.virtual import VirtualGroup  # noqa: E402,F401  (moved into the package)
