@@ -100,3 +100,12 @@ case " $* " in *" agree "*)
   timeout 300 python -m pytest tests/test_gpu_agreement.py -q -x -p no:cacheprovider 2>&1 | tail -15
   timeout 1200 python scripts/agreement.py > gpurun_out/agreement_$TAG.jsonl 2> gpurun_out/agreement_$TAG.err; cat gpurun_out/agreement_$TAG.jsonl; tail -5 gpurun_out/agreement_$TAG.err ;;
 esac
+case " $* " in *" cacheab "*)
+  timeout 900 python scripts/ablation_cache.py > gpurun_out/cacheab_$TAG.json 2> gpurun_out/cacheab_$TAG.err; cat gpurun_out/cacheab_$TAG.json; tail -3 gpurun_out/cacheab_$TAG.err ;;
+esac
+case " $* " in *" convab "*)
+  (for v in 1 0; do SSM_CONV_V2=$v timeout 300 python scripts/kernel_rooflines.py --layers 2 | grep -E "conv|row"; done) > gpurun_out/convab_$TAG.txt 2>&1; cat gpurun_out/convab_$TAG.txt ;;
+esac
+case " $* " in *" convncu "*)
+  for v in 1 0; do SSM_CONV_V2=$v timeout 600 ncu --set full --clock-control none -k regex:conv1d_silu -s 1 -c 1 -o gpurun_out/conv${v}_$TAG python bench.py --layers 2 --prompt 2048 --decode 2 --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1; done; ls gpurun_out/ | grep conv ;;
+esac
