@@ -77,8 +77,16 @@ enum {
                               and every rank forms sum_{r=0..k-1} fl32(h_r) in fp32, left to right
                               in rank order (reading Q21); the paper-literal ablation arm        */
   SSM_QAR_ACCUMULATE = 0x10, /* ssm_qallreduce: out += result instead of out = result           */
-  SSM_QAR_FP16 = 0x20       /* ssm_qallreduce: fp16 wire (as SSM_AR2_FP16) instead of int8 blocks;
+  SSM_QAR_FP16 = 0x20,      /* ssm_qallreduce: fp16 wire (as SSM_AR2_FP16) instead of int8 blocks;
                               n % 8 == 0                                                         */
+  SSM_QAR_TWOSHOT = 0x40,   /* int8 schedule (reading Q6): shared per-block scales (amax max over
+                              ranks), exact int16 reduce-scatter of the codes, all-gather of the
+                              sums; wire (k-1)/k (n + 2n) B per rank instead of (k-1) n; bound
+                              k max_r amax_r / 254.  ssm_qallreduce: selects it (n % (16 k) == 0);
+                              mixer calls: forces it for SSM_AR2_INT8                           */
+  SSM_QAR_ONESHOT = 0x80    /* mixer calls: force the one-shot int8 schedule.  Default for
+                              SSM_AR2_INT8: two-shot when tp_size >= 4 and the call has >= 64
+                              tokens (prefill), one-shot otherwise (decode, k = 2)               */
 };
 
 enum { SSM_COMM_VIRTUAL = 0x1 }; /* ssm_comm_t.flags: all peer buffers live on THIS device

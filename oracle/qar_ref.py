@@ -111,3 +111,34 @@ def fp16_error_bound(partials):
     cast = a * 2.0 ** -11 + k * 2.0 ** -25
     adds = (k - 1) * 2.0 ** -24 * (a * (1 + 2.0 ** -11) + k * 2.0 ** -25)
     return cast + adds
+
+
+# ---------------------------------------------------------------------------------------------
+# Two-shot int8 schedule with SHARED per-block scales (DESIGN.md §3 Q6):
+#   A_b   = max_r amax_{r,b}                   (exact in fp32)
+#   s_b   = fl32(A_b / 127)                     (IEEE fp32 division)
+#   q_r   = clamp(rint_even(fl32(o_r / s_b)), -127, 127)   (0 when s_b = 0)
+#   Q     = sum_r q_r                           (exact integer, |Q| <= 127 k: int16 on the wire)
+#   out   = fl32(s_b * Q)
+# bound |out - sum_r o_r| <= k s_b / 2 (+ the final fp32 rounding) <= k A_b / 254: the north_star's
+# k * max|x| / 254 with max over ranks.  The reduce-scatter / all-gather split is a data movement
+# choice that does not change these values.
+
+def qallreduce_twoshot(partials, block):
+    """partials: k float32 arrays [..., n].  Returns (out float32, codes list, scales float32)."""
+    ps = [np.asarray(o, dtype=np.float32) for o in partials]
+    n = ps[0].shape[-1]
+    assert n % block == 0
+    shp = ps[0].shape[:-1] + (n // block, block)
+    A = np.max(np.stack([np.max(np.abs(o.reshape(shp)), axis=-1) for o in ps]), axis=0)
+    s = (A / np.float32(127.0)).astype(np.float32)
+    safe = np.where(s == 0, np.float32(1.0), s).astype(np.float32)
+    codes = []
+    Q = np.zeros(shp, dtype=np.int64)
+    for o in ps:                                   # rank order irrelevant: integer sum
+        q = np.clip(np.rint((o.reshape(shp) / safe[..., None]).astype(np.float32)), -127, 127)
+        q = np.where(s[..., None] == 0, 0, q).astype(np.int64)
+        codes.append(q.reshape(ps[0].shape).astype(np.int8))
+        Q += q
+    out = (s[..., None] * Q.astype(np.float32)).astype(np.float32)
+    return out.reshape(ps[0].shape), codes, s

@@ -545,6 +545,16 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->bytes_sent += nD * 2;
     CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
     CU(launch_f16_reduce(t->peers, t->k, half_off(ep2), nD, residual, 1, s));
+  } else if (omode == OUT_INT8 && (flags & SSM_QAR_TWOSHOT ||
+                                    (!(flags & SSM_QAR_ONESHOT) && t->k >= 4 && M >= 64)) &&
+             nD % (16 * t->k) == 0 &&
+             2 * al256((size_t)nD / c.qar_block * 4) + al256(nD) + 2 * (size_t)nD / t->k <= half_bytes(t)) {
+    // two-shot schedule with shared scales (reading Q6): (k-1)/k 3n B on the wire instead of (k-1) n
+    Probe pr(t, SSM_PROBE_AR2, s);
+    t->launches += 7;
+    t->ar_count++;
+    t->bytes_sent += (nD + 2 * nD / t->k) * (t->k - 1) / t->k + nD / c.qar_block * 4;
+    CU(launch_qar_twoshot(t->peers, t->rank, t->k, half_off(ep2), part, nD, c.qar_block, residual, 1, s));
   } else if (omode == OUT_INT8) {
     Probe pr(t, SSM_PROBE_AR2, s);
     int8_t* q = reinterpret_cast<int8_t*>(own_half(ep2));
@@ -573,8 +583,11 @@ ssm_status_t check_call(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* 
   if (!x_in || !residual) return fail(SSM_ERR_ARG, "x_in/residual is NULL");
   if ((reinterpret_cast<uintptr_t>(x_in) | reinterpret_cast<uintptr_t>(residual)) & 15)
     return fail(SSM_ERR_ARG, "x_in/residual must be 16-B aligned");
-  if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL))
+  if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL | SSM_QAR_TWOSHOT |
+                          SSM_QAR_ONESHOT))
     return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  if ((flags & SSM_QAR_TWOSHOT) && (flags & SSM_QAR_ONESHOT))
+    return fail(SSM_ERR_ARG, "SSM_QAR_TWOSHOT and SSM_QAR_ONESHOT are exclusive");
   const int nmode = !!(flags & SSM_AR2_INT8) + !!(flags & SSM_AR2_FP16) + !!(flags & SSM_AR2_FP32) +
                     !!(flags & SSM_AR2_EXTERNAL);
   if (nmode > 1) return fail(SSM_ERR_ARG, "at most one AR#2 mode flag");
@@ -830,7 +843,8 @@ ssm_status_t ssm_mixer_decode_chained(ssm_tp_t tp, const ssm_layer_weights_t* w,
 
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
   if (!tp || !partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
-  if (flags & ~(uint32_t)(SSM_QAR_ACCUMULATE | SSM_QAR_FP16)) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  if (flags & ~(uint32_t)(SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_TWOSHOT))
+    return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
   const int blk = tp->cfg.qar_block;
   if (n % blk) return fail(SSM_ERR_DIM, "n=%zu not a multiple of qar_block=%d", n, blk);
   if ((reinterpret_cast<uintptr_t>(partial) | reinterpret_cast<uintptr_t>(out)) & 15)
@@ -843,6 +857,18 @@ ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_
     one.p[0] = const_cast<float*>(partial);
     tp->launches++;
     CU(launch_f32_reduce(one, 1, 0, (int64_t)n, out, acc, s));
+    return SSM_OK;
+  }
+  if (flags & SSM_QAR_TWOSHOT) {  // shared-scale two-shot int8 (reading Q6)
+    if (n % (16 * (size_t)tp->k) || blk % 16) return fail(SSM_ERR_DIM, "n=%zu not a multiple of 16*tp_size", n);
+    if (2 * al256(n / blk * 4) + al256(n) + 2 * n / tp->k > half_bytes(tp))
+      return fail(SSM_ERR_ARG, "symmetric buffer too small for n=%zu", n);
+    const uint32_t ep = ++tp->epoch;
+    tp->launches += 7;
+    tp->ar_count++;
+    tp->bytes_sent += (n + 2 * n / tp->k) * (tp->k - 1) / tp->k + n / blk * 4;
+    CU(launch_qar_twoshot(tp->peers, tp->rank, tp->k, (int64_t)(kSigBytes + (ep & 1) * half_bytes(tp)), partial,
+                          (int64_t)n, blk, out, acc, s));
     return SSM_OK;
   }
   if (flags & SSM_QAR_FP16) {  // the paper's fp16 wire

@@ -170,6 +170,8 @@ cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, in
                               int accumulate, cudaStream_t s);
 cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s);
 cudaError_t launch_f16_cast(const float* x, int64_t n, void* out, cudaStream_t s);
+cudaError_t launch_qar_twoshot(Peers peers, int rank, int k, int64_t off, const float* x, int64_t n, int blk,
+                               float* out, int accumulate, cudaStream_t s);
 cudaError_t launch_f16_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s);
 // Cross-rank barrier: advance this rank's device-side epoch counter, write it into slot[rank]
 // of every peer's signal area, wait for all peers' slots in our own area to reach it

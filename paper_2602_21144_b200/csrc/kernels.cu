@@ -727,6 +727,97 @@ __global__ void f32_reduce_kernel(Peers src, int k, int64_t off, int64_t n4, flo
   *o = acc;
 }
 
+// ---------------------------------------------------------------- two-shot int8 all-reduce (reading Q6)
+// Shared per-block scales, so codes of different ranks add exactly:
+//   (1) amax_r[b] -> own buffer; barrier
+//   (2) s[b] = fl32(max_r amax_r[b] / 127); q_r = clamp(rint(fl32(o_r / s)), +-127) -> own buffer; barrier
+//   (3) reduce-scatter: rank j sums the k codes of its shard exactly (int16, |sum| <= 127 k); barrier
+//   (4) all-gather: out[i] (+)= fl32(s[b] * sum_j[i]) read from the shard's owner.
+// Wire per rank: (k-1)/k n B of int8 codes + (k-1)/k 2n B of int16 sums (+ scales) vs (k-1) n B
+// one-shot.  Error <= k s / 2 <= k max_r amax_r / 254 per element (the north_star bound).
+template <int VPL>
+__global__ void amax_kernel(const float* __restrict__ x, int64_t nblocks, float* __restrict__ amax) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t blk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (blk >= nblocks) return;
+  const float* xb = x + blk * 32 * VPL + lane * VPL;
+  float am = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) am = fmaxf(am, fabsf(xb[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  if (lane == 0) amax[blk] = am;
+}
+
+template <int VPL>
+__global__ void quant_shared_kernel(const float* __restrict__ x, int64_t nblocks, Peers src, int k, int64_t amax_off,
+                                    int8_t* __restrict__ q, float* __restrict__ scale) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t blk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (blk >= nblocks) return;
+  float A = 0.f;
+  for (int r = 0; r < k; ++r)
+    A = fmaxf(A, reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[r]) + amax_off)[blk]);
+  const float s = __fdiv_rn(A, 127.0f);
+  const float* xb = x + blk * 32 * VPL + lane * VPL;
+  int8_t* qb = q + blk * 32 * VPL + lane * VPL;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    int c = 0;
+    if (s != 0.f) c = max(-127, min(127, __float2int_rn(__fdiv_rn(xb[i], s))));
+    qb[i] = (int8_t)c;
+  }
+  if (lane == 0) scale[blk] = s;
+}
+
+__global__ void rs16_kernel(Peers src, int k, int64_t q_off, int64_t lo, int64_t n16, int16_t* __restrict__ sums) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // 16-element group of this rank's shard
+  if (i >= n16) return;
+  int acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0;
+  for (int r = 0; r < k; ++r) {
+    const int4 qv = *reinterpret_cast<const int4*>(reinterpret_cast<const char*>(src.p[r]) + q_off + lo + i * 16);
+    const int8_t* qq = reinterpret_cast<const int8_t*>(&qv);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] += qq[j];
+  }
+  int16_t o[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) o[j] = (int16_t)acc[j];
+  reinterpret_cast<int4*>(sums + i * 16)[0] = reinterpret_cast<const int4*>(o)[0];
+  reinterpret_cast<int4*>(sums + i * 16)[1] = reinterpret_cast<const int4*>(o)[1];
+}
+
+__global__ void ag16_kernel(Peers src, int64_t sum_off, int64_t shard, int64_t n16, const float* __restrict__ scale,
+                            int blk, float* __restrict__ out, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n16) return;
+  const int64_t e0 = i * 16;
+  const int j = (int)(e0 / shard);  // owner of this 16-element group (shard % 16 == 0)
+  const int16_t* sp = reinterpret_cast<const int16_t*>(reinterpret_cast<const char*>(src.p[j]) + sum_off) + (e0 - (int64_t)j * shard);
+  int16_t qv[16];
+  reinterpret_cast<int4*>(qv)[0] = reinterpret_cast<const int4*>(sp)[0];
+  reinterpret_cast<int4*>(qv)[1] = reinterpret_cast<const int4*>(sp)[1];
+  const float s = scale[e0 / blk];  // blk % 16 == 0: one block per group
+  float4* o = reinterpret_cast<float4*>(out + e0);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float4 v = accumulate ? o[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    v.x = v.x + s * (float)qv[4 * q]; v.y = v.y + s * (float)qv[4 * q + 1];
+    v.z = v.z + s * (float)qv[4 * q + 2]; v.w = v.w + s * (float)qv[4 * q + 3];
+    o[q] = v;
+  }
+}
+
 // ---------------------------------------------------------------- fp16-wire all-reduce
 // Cast: 8 fp32 -> 8 fp16 per thread (cvt.rn.f16x2.f32: IEEE round-to-nearest-even, overflow -> inf).
 __global__ void f16_cast_kernel(const float* __restrict__ x, int64_t n8, __half* __restrict__ out) {
@@ -1057,6 +1148,46 @@ cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, in
   return cudaGetLastError();
 }
 
+// Two-shot int8 all-reduce (reading Q6).  Layout in every rank's buffer half at byte offset `off`:
+// amax [n/blk] f32 | scale [n/blk] f32 | codes [n] i8 | sums [n/k] i16 (each 256-B aligned).
+cudaError_t launch_qar_twoshot(Peers peers, int rank, int k, int64_t off, const float* x, int64_t n, int blk,
+                               float* out, int accumulate, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n % (16 * k) || n % blk || blk % 16) return cudaErrorInvalidValue;
+  const int64_t nb = n / blk;
+  auto a256 = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+  const int64_t o_amax = off, o_scale = o_amax + a256(nb * 4), o_q = o_scale + a256(nb * 4), o_sum = o_q + a256(n);
+  char* own = reinterpret_cast<char*>(peers.p[rank]);
+  const int blocks = (int)((nb * 32 + 255) / 256);
+  cudaError_t e_ = cudaSuccess;
+#define QTS(VPL)                                                                                              \
+  e_ = launch(amax_kernel<VPL>, blocks, 256, 0, s, x, nb, reinterpret_cast<float*>(own + o_amax));           \
+  if (e_ != cudaSuccess) return e_;                                                                           \
+  if ((e_ = launch_peer_barrier(peers, rank, k, s)) != cudaSuccess) return e_;                               \
+  e_ = launch(quant_shared_kernel<VPL>, blocks, 256, 0, s, x, nb, peers, k, o_amax,                           \
+              reinterpret_cast<int8_t*>(own + o_q), reinterpret_cast<float*>(own + o_scale));                 \
+  if (e_ != cudaSuccess) return e_;
+  switch (blk) {
+    case 32: QTS(1) break;
+    case 64: QTS(2) break;
+    case 128: QTS(4) break;
+    case 256: QTS(8) break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef QTS
+  if ((e_ = launch_peer_barrier(peers, rank, k, s)) != cudaSuccess) return e_;
+  const int64_t shard = n / k, s16 = shard / 16;
+  e_ = launch(rs16_kernel, (int)((s16 + 255) / 256), 256, 0, s, peers, k, o_q, (int64_t)rank * shard, s16,
+              reinterpret_cast<int16_t*>(own + o_sum));
+  if (e_ != cudaSuccess) return e_;
+  if ((e_ = launch_peer_barrier(peers, rank, k, s)) != cudaSuccess) return e_;
+  const int64_t n16 = n / 16;
+  e_ = launch(ag16_kernel, (int)((n16 + 255) / 256), 256, 0, s, peers, o_sum, shard, n16,
+              reinterpret_cast<const float*>(own + o_scale), blk, out, accumulate);
+  if (e_ != cudaSuccess) return e_;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_f16_cast(const float* x, int64_t n, void* out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   if (n % 8) return cudaErrorInvalidValue;
@@ -1104,7 +1235,8 @@ cudaError_t preload_kernels() {
       (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>, (const void*)chain_begin_kernel,
       (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,
       (const void*)quantize_kernel<8>, (const void*)qar_reduce_kernel, (const void*)f32_reduce_kernel,
-      (const void*)f16_cast_kernel, (const void*)f16_reduce_kernel,
+      (const void*)f16_cast_kernel, (const void*)f16_reduce_kernel, (const void*)amax_kernel<4>,
+      (const void*)quant_shared_kernel<4>, (const void*)rs16_kernel, (const void*)ag16_kernel,
       (const void*)peer_barrier_kernel};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);

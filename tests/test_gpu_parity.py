@@ -317,6 +317,43 @@ def test_virtual_fp16_allreduce_bitexact(k):
     assert np.all(np.abs(outs[0].cpu().double().numpy() - exact) <= Q.fp16_error_bound(list(parts.numpy())))
 
 
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_virtual_qallreduce_twoshot_bitexact(k):
+    """Two-shot shared-scale int8 schedule (reading Q6): codes, scales and the result equal the
+    oracle bit for bit on every rank; error within k max|x| / 254."""
+    dims = MED
+    n = 6 * dims.d_model
+    parts = synth.partials(k, n, seed=300 + k)
+    grp = VirtualGroup(dims, k, "bf16", 64)
+    outs = [torch.empty(n, device="cuda") for _ in range(k)]
+    dev_parts = [parts[r].cuda() for r in range(k)]
+    grp.run(lambda r, mx, s: mx.qallreduce(dev_parts[r], outs[r], stream=s, twoshot=True))
+    ref, codes, scales = Q.qallreduce_twoshot(list(parts.numpy()), 128)
+    half = ((grp.bufs[0].numel() - 256) // 2) & ~255
+    a256 = lambda b: (b + 255) // 256 * 256
+    nb = n // 128
+    for r in range(k):
+        base = 256 + half  # epoch 1 -> half 1: amax | scale | codes | sums
+        sc = grp.bufs[r][base + a256(4 * nb):base + a256(4 * nb) + 4 * nb].cpu().view(torch.float32).numpy()
+        q = grp.bufs[r][base + 2 * a256(4 * nb):base + 2 * a256(4 * nb) + n].cpu().view(torch.int8).numpy()
+        np.testing.assert_array_equal(sc, scales)
+        np.testing.assert_array_equal(q, codes[r])
+        np.testing.assert_array_equal(outs[r].cpu().numpy(), ref)
+    exact = parts.double().sum(0).numpy()
+    assert np.all(np.abs(outs[0].cpu().double().numpy() - exact) <= Q.northstar_bound(list(parts.numpy()), 128) * (1 + 1e-5))
+
+
+@pytest.mark.parametrize("k,sched", [(4, L.SSM_QAR_TWOSHOT), (4, L.SSM_QAR_ONESHOT), (8, 0)])
+def test_virtual_tp_mixer_int8_schedules_vs_oracle(k, sched):
+    dims = MED
+    outs, w, x, res, grp, sts = _tp_virtual(dims, "bf16", k, 2, 40, 4, L.SSM_AR2_INT8 | sched)
+    for r in range(1, k):
+        assert torch.equal(outs[r], outs[0])
+    ref, _ = M.mixer_forward(dims, np64(w), x.numpy(), res.numpy())
+    resn = res.numpy()
+    assert rel(outs[0].double().numpy() - resn, ref - resn) < TOL["bf16"]
+
+
 @pytest.mark.parametrize("k", [2, 4])
 def test_virtual_tp_mixer_fp16_ar2_vs_oracle(k):
     dims = MED

@@ -238,3 +238,38 @@ def test_tp_fp16_ar2_within_bound():
     d = np.abs(f16[0] - exact[0])
     assert d.max() > 0  # it did quantise
     assert d.max() <= 2 * 2.0 ** -11 * np.abs(exact[0] - res).max() + 1e-6
+
+
+# ---------------------------------------------------------------- two-shot shared-scale int8 (Q6)
+def test_twoshot_golden():
+    rows = [list(map(float, l.split())) for l in open(os.path.join(os.path.dirname(__file__), "golden", "qar_twoshot.txt"))
+            if l.strip() and not l.startswith("#")]
+    o0, o1, want, wantQ = (np.array(r, dtype=np.float32) for r in rows)
+    out, codes, s = Q.qallreduce_twoshot([o0, o1], 4)
+    assert float(s[0]) == 0.0625
+    np.testing.assert_array_equal(codes[0].astype(np.int64) + codes[1].astype(np.int64), wantQ.astype(np.int64))
+    np.testing.assert_array_equal(out, want)
+
+
+def test_twoshot_k1_equals_oneshot():
+    """k = 1: the shared scale is the rank's own scale, so the codes equal the one-shot codes."""
+    rng = np.random.default_rng(11)
+    o = (rng.standard_normal(1024) * np.exp(rng.uniform(-3, 3, 1024))).astype(np.float32)
+    out, codes, s = Q.qallreduce_twoshot([o], 128)
+    q1, s1 = Q.quantize_blocks(o, 128)
+    np.testing.assert_array_equal(codes[0], q1)
+    np.testing.assert_array_equal(s, s1)
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_twoshot_within_northstar_bound(k):
+    rng = np.random.default_rng(40 + k)
+    parts = [(rng.standard_normal(4096) * np.exp(rng.uniform(-2, 2, 4096))).astype(np.float32) for _ in range(k)]
+    out, codes, s = Q.qallreduce_twoshot(parts, 128)
+    exact = np.sum([p.astype(np.float64) for p in parts], axis=0)
+    err = np.abs(out.astype(np.float64) - exact)
+    bound = Q.northstar_bound(parts, 128)
+    assert np.all(err <= bound * (1 + 1e-6) + 1e-30)
+    assert np.max(err / bound) > 0.2                 # not vacuous
+    for q in codes:
+        assert q.min() >= -127 and q.max() <= 127
