@@ -215,6 +215,15 @@ ssm_status_t ssm_mixer_decode_chained(ssm_tp_t tp, const ssm_layer_weights_t* w,
                                       float* residual, int32_t batch, float norm_eps, void* workspace,
                                       size_t ws_bytes, void* stream);
 
+/* Decode step of one layer WITH its pre-norm (reading Q16: weightless RMSNorm, eps norm_eps):
+ * x_scratch [batch, d_model] bf16 receives RMSNorm(residual) and is the in_proj input; then as
+ * ssm_mixer_decode (residual += mixer(x)).  On the fused TP=1 decode path the norm runs inside the
+ * in_proj kernel (its epilogue warps write the B operand before releasing its loads: one launch
+ * fewer per layer); otherwise the standalone ssm_rmsnorm kernel runs first.  bf16 handles only. */
+ssm_status_t ssm_mixer_decode_prenorm(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, void* x_scratch,
+                                      float* residual, int32_t batch, float norm_eps, uint32_t flags,
+                                      void* workspace, size_t ws_bytes, void* stream);
+
 /* Quantised all-reduce of n fp32 values (n % qar_block == 0), rows of D = d_model:
  * every rank quantises its partial per block (s = amax/127, q = rint(o/s) clamped to
  * +-127), exchanges int8 codes + fp32 scales peer-to-peer, and forms

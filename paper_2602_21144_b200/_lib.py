@@ -87,6 +87,8 @@ def _load():
         "ssm_decode_chain_supported": (st, [vp, vp, i32, P(i32)]),
         "ssm_decode_chain_begin": (st, [vp, vp, vp, i32, vp, sz, vp]),
         "ssm_mixer_decode_chained": (st, [vp, P(ssm_layer_weights_t), vp, vp, vp, i32, C.c_float, vp, sz, vp]),
+        "ssm_mixer_decode_prenorm": (st, [vp, P(ssm_layer_weights_t), vp, vp, vp, i32, C.c_float, C.c_uint32, vp, sz,
+                                          vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -102,7 +104,7 @@ EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "s
             "ssm_tp_launch_count", "ssm_tp_fused_calls", "ssm_tp_probe", "ssm_tp_probe_read", "ssm_packed_weight_bytes", "ssm_pack_weight",
             "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld", "ssm_dbg_scan", "ssm_dbg_gemm_trace",
             "ssm_stack_bytes", "ssm_stack_bind", "ssm_stack_decode", "ssm_stack_check", "ssm_stack_info", "ssm_dbg_stack_trace",
-            "ssm_decode_chain_supported", "ssm_decode_chain_begin", "ssm_mixer_decode_chained"]
+            "ssm_decode_chain_supported", "ssm_decode_chain_begin", "ssm_mixer_decode_chained", "ssm_mixer_decode_prenorm"]
 PROBE = {"in_proj": 1, "conv": 2, "x_proj": 3, "dt_proj": 4, "scan": 5, "out_proj": 6, "ar2": 7, "decode_step": 8,
          "in_proj_decode": 9}
 

@@ -277,7 +277,7 @@ Peers group_peers(const ssm_tp_s* t, int gsize) {
 // One mixer layer. decode: seqlen == 1 path with in-place state update.
 ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* st, const void* x_in, float* residual,
                        int batch, int seqlen, uint32_t flags, void* ws, bool decode, cudaStream_t s,
-                       bool chain = false, float norm_eps = 0.f) {
+                       bool chain = false, float norm_eps = 0.f, bool prenorm = false) {
   const ssm_config_t& c = t->cfg;
   const int64_t M = (int64_t)batch * seqlen;
   const int D = c.d_model, Ek = t->Ek, R = c.dt_rank, N = c.d_state, K = c.d_conv, P = t->P, hl = t->hloc;
@@ -351,6 +351,11 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   float* css = reinterpret_cast<float*>(W + L.css);
   int* ccnt = reinterpret_cast<int*>(W + L.ccnt);
   if (chain && (!fuse || skip || t->k != 1)) return fail(SSM_ERR_UNSUPPORTED, "decode chain needs the fused TP=1 decode path");
+  if (prenorm && !fuse) {  // no fused in_proj: the standalone pre-norm kernel, then the layer
+    t->launches++;
+    CU(launch_rmsnorm(1, residual, nullptr, norm_eps, const_cast<void*>(x_in), M, D, s));
+    prenorm = false;
+  }
   if (!(skip & 1)) {
     Probe pr(t, decode ? SSM_PROBE_IN_PROJ_DECODE : SSM_PROBE_IN_PROJ, s);
     if (fuse) {
@@ -368,6 +373,11 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       e.hl = hl;
       e.cph = t->cph;
       if (!oacc) { e.zero = odst; e.nzero = nD; }  // out_proj partial target (AR#2 follows)
+      if (prenorm) {  // x_in = RMSNorm(residual) written by the in_proj kernel itself
+        e.nres = residual;
+        e.nres_eps = norm_eps;
+        e.nx = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(x_in));
+      }
       if (chain) {  // x_in = bf16(residual) un-normalised; the pre-norm's 1/rms applied here
         e.ss = css;
         e.ss_scale = 1.0f / (float)D;
@@ -802,6 +812,18 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
   PdlScope pdl(g_pdl_enabled && !(tp->flags & SSM_COMM_VIRTUAL));
   return run_layer(tp, w, st, x_in, residual, batch, 1, flags, workspace, true,
                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+ssm_status_t ssm_mixer_decode_prenorm(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, void* x_scratch,
+                                      float* residual, int32_t batch, float norm_eps, uint32_t flags, void* workspace,
+                                      size_t ws_bytes, void* stream) {
+  ssm_status_t s = check_call(tp, w, st, x_scratch, residual, batch, 1, flags, workspace, ws_bytes);
+  if (s != SSM_OK) return s;
+  if (!tp->bf16) return fail(SSM_ERR_UNSUPPORTED, "ssm_mixer_decode_prenorm: bf16 handles only");
+  if (batch == 0) return SSM_OK;
+  PdlScope pdl(g_pdl_enabled && !(tp->flags & SSM_COMM_VIRTUAL));
+  return run_layer(tp, w, st, x_scratch, residual, batch, 1, flags, workspace, true,
+                   reinterpret_cast<cudaStream_t>(stream), false, norm_eps, true);
 }
 
 ssm_status_t ssm_decode_chain_supported(ssm_tp_t tp, const ssm_layer_weights_t* w, int32_t batch, int32_t* ok) {

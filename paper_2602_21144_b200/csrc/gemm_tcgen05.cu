@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
     pdl_wait();
-    if (job.enabled) {  // B = g is produced inside this grid (decode-step job + grid barrier)
+    if (job.enabled || epi.nres) {  // B produced inside this grid (decode-step job / pre-norm)
       mbar_wait(bready, 0);
       if (leader) fence_proxy_async_global();
     }
@@ -810,6 +810,59 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t i = threadIdx.x - 64; i < n4; i += kThreads - 64)
         reinterpret_cast<float4*>(epi.zero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int64_t i = 4 * n4 + threadIdx.x - 64; i < epi.nzero; i += kThreads - 64) epi.zero[i] = 0.f;
+    }
+    if (epi.nres) {
+      // pre-norm of the N residual rows -> the bf16 B operand (global; identical in every CTA)
+      // the warp's rows are handled together, 8 x 16-B loads per row in flight per lane per chunk
+      const int et = threadIdx.x - 64, w8 = et >> 5;
+      constexpr int RW = 4, CH = 8;  // rows per warp (N <= 32), float4 per lane per chunk
+      float ss[RW];
+#pragma unroll
+      for (int r = 0; r < RW; ++r) ss[r] = 0.f;
+      const int nv = K / 4;
+      for (int base = 0; base < nv; base += 32 * CH) {
+        float4 v[RW][CH];
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const int row = w8 + 8 * r, i = base + lane + 32 * c;
+            v[r][c] = (row < N && i < nv) ? reinterpret_cast<const float4*>(epi.nres + (int64_t)row * K)[i]
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            ss[r] = fmaf(v[r][c].x, v[r][c].x, ss[r]); ss[r] = fmaf(v[r][c].y, v[r][c].y, ss[r]);
+            ss[r] = fmaf(v[r][c].z, v[r][c].z, ss[r]); ss[r] = fmaf(v[r][c].w, v[r][c].w, ss[r]);
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss[r] += __shfl_xor_sync(0xffffffffu, ss[r], o);
+        ss[r] = 1.0f / sqrtf(ss[r] / (float)K + epi.nres_eps);
+      }
+      for (int base = 0; base < K / 8; base += 32 * CH / 2) {  // second pass: L1-resident rows
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+          for (int c = 0; c < CH / 2; ++c) {
+            const int row = w8 + 8 * r, i = base + lane + 32 * c;
+            if (row < N && i < K / 8) {
+              const float4* xr = reinterpret_cast<const float4*>(epi.nres + (int64_t)row * K);
+              const float4 a = xr[2 * i], b = xr[2 * i + 1];
+              const float rs = ss[r];
+              __nv_bfloat162 h[4] = {__floats2bfloat162_rn(a.x * rs, a.y * rs), __floats2bfloat162_rn(a.z * rs, a.w * rs),
+                                     __floats2bfloat162_rn(b.x * rs, b.y * rs), __floats2bfloat162_rn(b.z * rs, b.w * rs)};
+              reinterpret_cast<uint4*>(epi.nx + (int64_t)row * K)[i] = *reinterpret_cast<const uint4*>(h);
+            }
+          }
+      }
+      fence_proxy_async_global();  // these generic stores -> this CTA's TMA loads of B
+      named_bar_sync(1, 256);
+      if (threadIdx.x == 64) mbar_arrive(bready);
     }
     if (epi.kind == EPI_DECODE_INPROJ) {
       decode_inproj_epilogue(epi, ts, M, N, tfull, tempty, tmem_base, cr,
@@ -1063,6 +1116,9 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     cr.ring -= SU_BYTES + 128;
   }
   if (epi.zero && (reinterpret_cast<uintptr_t>(epi.zero) & 15)) return cudaErrorInvalidValue;
+  if (epi.nres && (epi.kind != EPI_DECODE_INPROJ || K % 8 || epi.nx != B || job.enabled || N > 32 ||
+                   (reinterpret_cast<uintptr_t>(epi.nres) & 15)))
+    return cudaErrorInvalidValue;
   if (epi.fin_cnt) {  // decode-chain finaliser scratch (257 floats) after the barrier area
     extra += 2048;
     cr.ring -= 2048;

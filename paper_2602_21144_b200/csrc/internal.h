@@ -68,6 +68,12 @@ struct Epilogue {
   // tile's contributors reads the sum back, re-zeroes it and runs the conv / x_proj epilogue.
   float* sk_acc;
   int* sk_cnt;
+  // EPI_DECODE_INPROJ pre-norm (nres != NULL): the epilogue warps first write the B operand
+  // itself, B[n][:] = bf16(nres[n][:] / sqrt(mean(nres[n][:]^2) + nres_eps)) (the layer's weightless
+  // pre-norm RMSNorm, reading Q16; every CTA writes the same values), then release the B loads.
+  const float* nres;
+  float nres_eps;
+  __nv_bfloat16* nx;
 };
 
 struct Peers {

@@ -70,6 +70,11 @@ class MixerStack:
         self.graph = None
         self.graph_launches = 0
         self.stack_ws = None
+        # opt-in (SSM_PRENORM=1): the pre-norm computed inside the fused decode in_proj
+        # (ssm_mixer_decode_prenorm).  Measured slower: 44.6 vs 38.0 us per Mamba-2.8B decode layer
+        # -- 80 CTAs re-reading the same 164 KB of residual rows from L2 cost more than the 16-block
+        # norm kernel they replace
+        self.prenorm = mixer.dtype == "bf16" and os.environ.get("SSM_PRENORM", "0") == "1"
         self.chain = False  # per-layer decode with the pre-norm folded into the GEMMs (ssm_mixer_decode_chained)
         # opt-in (SSM_DECODE_CHAIN=1): measured slower than the norm kernel it removes
         if self.nccl is None and os.environ.get("SSM_DECODE_CHAIN", "0") == "1" and layers:
@@ -137,6 +142,14 @@ class MixerStack:
                 L.call("ssm_mixer_decode_chained", self.mx.handle, C.byref(lw.struct), st.handle, _ptr(self.xbuf_dec),
                        _ptr(res_t), self.batch, C.c_float(self.eps), _ptr(self.ws_dec), self.ws_dec.numel(),
                        _stream(stream))
+            return
+        if self.prenorm and self.nccl is None and not _DEBUG_SKIP_NORM:
+            import ctypes as C
+            from .mixer import _ptr, _stream
+            for lw, st in zip(self.layers, self.states):
+                L.call("ssm_mixer_decode_prenorm", self.mx.handle, C.byref(lw.struct), st.handle, _ptr(self.xbuf_dec),
+                       _ptr(res_t), self.batch, C.c_float(self.eps), self.flags, _ptr(self.ws_dec),
+                       self.ws_dec.numel(), _stream(stream))
             return
         skip_norm = _DEBUG_SKIP_NORM
         for lw, st in zip(self.layers, self.states):

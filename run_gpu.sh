@@ -109,3 +109,6 @@ esac
 case " $* " in *" convncu "*)
   for v in 1 0; do SSM_CONV_V2=$v timeout 600 ncu --set full --clock-control none -k regex:conv1d_silu -s 1 -c 1 -o gpurun_out/conv${v}_$TAG python bench.py --layers 2 --prompt 2048 --decode 2 --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1; done; ls gpurun_out/ | grep conv ;;
 esac
+case " $* " in *" pnab "*)
+  (for v in 1 0 1 0; do SSM_PRENORM=$v timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/pnab_$TAG.txt 2>&1; cat gpurun_out/pnab_$TAG.txt ;;
+esac

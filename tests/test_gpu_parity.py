@@ -419,3 +419,42 @@ def test_virtual_tp_stack_prefill_then_graph_decode(k, mode):
     r0 = res0.numpy()
     assert rel(got_pre - r0[:, :L_in], ref[:, :L_in] - r0[:, :L_in]) < TOL["bf16"]
     assert rel(got_dec - r0[:, L_in:], ref[:, L_in:] - r0[:, L_in:]) < TOL["bf16"]
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_stack_decode_prenorm_in_inproj_matches_separate_norm(graph):
+    """ssm_mixer_decode_prenorm (the pre-norm written by the fused in_proj kernel itself) against
+    the separate rmsnorm kernel + ssm_mixer_decode, TP=1 two-layer stack, eager and graph decode."""
+    from paper_2602_21144_b200.stack import MixerStack
+    dims = synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_layers=2)
+    B, L_in, L_out = 4, 12, 5
+    ws = [prep_weights(dims, l, "bf16") for l in range(2)]
+    g = torch.Generator().manual_seed(8)
+    res0 = torch.randn(B, L_in + L_out, dims.d_model, generator=g, dtype=torch.float64)
+    outs = {}
+    for pn in (False, True):
+        mx = TPMixer(dims, "bf16")
+        st = MixerStack(mx, [LayerWeights(dims, w, 1, 0, "bf16") for w in ws], B, L_in)
+        st.prenorm = pn
+        pre = res0[:, :L_in].float().cuda().contiguous().view(B * L_in, -1)
+        st.prefill_chunk(pre)
+        rt = torch.empty(B, dims.d_model, device="cuda")
+        gr = st.capture_decode(rt) if graph else None
+        if graph:  # the capture's warm-up step advanced the state: redo the prefill
+            st.reset()
+            pre = res0[:, :L_in].float().cuda().contiguous().view(B * L_in, -1)
+            st.prefill_chunk(pre)
+        seq = []
+        for t in range(L_in, L_in + L_out):
+            rt.copy_(res0[:, t].float().cuda())
+            if graph:
+                gr.replay()
+            else:
+                st.decode_step(rt)
+            seq.append(rt.clone())
+        torch.cuda.synchronize()
+        outs[pn] = torch.stack(seq, 1).cpu().double().numpy()
+        if pn:
+            assert mx.fused_calls() > 0
+    r0 = res0[:, L_in:].numpy()
+    assert rel(outs[True] - r0, outs[False] - r0) < 5e-3
