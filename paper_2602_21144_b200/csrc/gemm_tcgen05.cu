@@ -114,7 +114,8 @@ __device__ __forceinline__ int tile_nacc(const CtaRes& cr, int kb0, int kb1) { r
 // Epilogue for one warp's 32 x 32 chunk: lane = row m0 + lane, columns n0..n0+31, stored
 // straight from registers (staging through shared memory would compete with the UMMA operand
 // reads for smem bandwidth in the MMA-bound projections).
-__device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int M, int N, uint32_t (&r)[32]) {
+__device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int M, int N, uint32_t (&r)[32],
+                                          const float* bpre = nullptr) {
   const int kind = e.kind;
   const int m = m0 + threadIdx.x % 32;
   if (m >= M) return;
@@ -123,7 +124,10 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
   if (kind == EPI_SOFTPLUS_BF16 || kind == EPI_SOFTPLUS_F32) {
     float bb[32];
-    if (e.trans) {
+    if (bpre) {  // bias chunk loaded by the caller before the TMEM load (latencies overlap)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bb[j] = bpre[j];
+    } else if (e.trans) {
       const float b0 = e.bias[m];
 #pragma unroll
       for (int j = 0; j < 32; ++j) bb[j] = b0;
@@ -897,6 +901,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int na = tile_nacc(cr, kb0, kb1);
       for (int c = half; c < (BN + 31) / 32; c += 2) {
         uint32_t r[32];
+        const int nc = nt * BN + c * 32;
+        float bpre[32];
+        const bool pre = (epi.kind == EPI_SOFTPLUS_BF16 || epi.kind == EPI_SOFTPLUS_F32) && !epi.trans &&
+                         nc + 32 <= N && ((reinterpret_cast<uintptr_t>(epi.bias + nc) & 15) == 0);
+        if (pre) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 t4 = reinterpret_cast<const float4*>(epi.bias + nc)[q];
+            bpre[4 * q] = t4.x; bpre[4 * q + 1] = t4.y; bpre[4 * q + 2] = t4.z; bpre[4 * q + 3] = t4.w;
+          }
+        }
         tmem_ld_32x32b_x32(tbase + c * 32, r);
         tmem_ld_wait();
         for (int q = 1; q < na; ++q) {  // fold the interleaved partial accumulators
@@ -911,7 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("add.u32 %0, %1, %2;" : "=r"(dep) : "r"(r[0]), "r"(r[31]));
           TRACE(8, clock64() - c_start + (dep == 0x7f123456u ? 1 : 0));
         }
-        if (!(cr.nomma & 4)) epi_chunk(epi, m0, nt * BN + c * 32, M, N, r);
+        if (!(cr.nomma & 4)) epi_chunk(epi, m0, nt * BN + c * 32, M, N, r, pre ? bpre : nullptr);
       }
       if (threadIdx.x == 64) TRACE(9, clock64() - c_start);
       tc_fence_before();

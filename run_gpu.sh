@@ -112,3 +112,8 @@ esac
 case " $* " in *" pnab "*)
   (for v in 1 0 1 0; do SSM_PRENORM=$v timeout 120 python scripts/decode_ablation.py; done) > gpurun_out/pnab_$TAG.txt 2>&1; cat gpurun_out/pnab_$TAG.txt ;;
 esac
+case " $* " in *" gemmncu "*)
+  A="--layers 1 --prompt 2048 --decode 0 --steps 1 --warmup 0 --no-e2e --no-cpu"
+  timeout 300 python bench.py $A > gpurun_out/gemmncu_bench_$TAG.txt 2>&1; tail -c 300 gpurun_out/gemmncu_bench_$TAG.txt
+  for i in 2 3; do timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s $i -c 1 -o gpurun_out/pgemm${i}_$TAG python bench.py $A > /dev/null 2>&1; done; ls gpurun_out | grep pgemm ;;
+esac
