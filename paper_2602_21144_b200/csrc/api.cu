@@ -345,7 +345,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   // Fused decode (no AR#1 between x_proj and the scan): the in_proj epilogue also runs the conv
   // step (a2) and adds its x_proj partial (a3) into the state's zeroed accumulator.
   float* xacc = reinterpret_cast<float*>(reinterpret_cast<char*>(st->h) + xacc_offset(t, batch));
-  const bool fuse = swap && !ar1 && t->fuse_decode && batch <= 32 && P <= 256 && P % 2 == 0 && K >= 2 && K <= 4 &&
+  const bool fuse = swap && !ar1 && t->fuse_decode && batch <= 32 && P <= 320 && P % 2 == 0 && K >= 2 && K <= 4 &&
                     t->cph % 128 == 0 && !(skip & 7) &&
                     gemm_tc_supported(w->w_in, D, x_in, D);
   float* css = reinterpret_cast<float*>(W + L.css);
@@ -830,7 +830,7 @@ ssm_status_t ssm_decode_chain_supported(ssm_tp_t tp, const ssm_layer_weights_t* 
   if (!tp || !ok) return fail(SSM_ERR_ARG, "NULL argument");
   const ssm_config_t& c = tp->cfg;
   *ok = tp->k == 1 && tp->bf16 && tp->ar1_group == 1 && tp->fuse_decode && batch >= 1 && batch <= 32 &&
-        (c.dt_rank + 2 * c.d_state) <= 256 && (c.dt_rank + 2 * c.d_state) % 2 == 0 && c.d_conv >= 2 && c.d_conv <= 4 &&
+        (c.dt_rank + 2 * c.d_state) <= 320 && (c.dt_rank + 2 * c.d_state) % 2 == 0 && c.d_conv >= 2 && c.d_conv <= 4 &&
         tp->cph % 128 == 0 && c.d_model % 128 == 0 && !g_dbg_skip && (!w || gemm_tc_supported(w->w_in, c.d_model, w->w_in, c.d_model));
   return SSM_OK;
 }

@@ -252,7 +252,7 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
 // batch columns [16 half, 16 half + 16) (half = w / 4), so a CTA covers N <= 32 decode tokens.
 constexpr int SU_LD = 136;                       // u tile row pitch (bf16): conflict-free ldmatrix
 constexpr int SU_BYTES = 32 * SU_LD * 2;         // u tile [32 tokens][128 channels] bf16
-constexpr int XP_NT = 4;                         // x_proj n-tiles (8 outputs) per warp: P <= 256
+constexpr int XP_NT = 5;                         // x_proj n-tiles (8 outputs) per warp: P <= 320 (Zamba: 264)
 
 __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const TileSched& ts, int M, int N,
                                                        uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
@@ -1122,7 +1122,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   }
   int extra = 0;
   if (epi.kind == EPI_DECODE_INPROJ) {
-    // fused decode in_proj: one 32-column accumulator per tile, N <= 32 tokens, P <= 256 (even),
+    // fused decode in_proj: one 32-column accumulator per tile, N <= 32 tokens, P <= 320 (even),
     // tiles inside one head, window of <= 3 cached taps
     if (!epi.trans || N > 32 || BN > 32 || epi.P > 8 * 8 * XP_NT || (epi.P & 1) || epi.K < 2 || epi.K > 4 ||
         epi.cph % BM || M != 2 * epi.Ek || ts.ksplit != 1 || (ts.streamk && (!epi.sk_acc || !epi.sk_cnt)))

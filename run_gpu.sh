@@ -117,3 +117,6 @@ case " $* " in *" gemmncu "*)
   timeout 300 python bench.py $A > gpurun_out/gemmncu_bench_$TAG.txt 2>&1; tail -c 300 gpurun_out/gemmncu_bench_$TAG.txt
   for i in 2 3; do timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s $i -c 1 -o gpurun_out/pgemm${i}_$TAG python bench.py $A > /dev/null 2>&1; done; ls gpurun_out | grep pgemm ;;
 esac
+case " $* " in *" zamba "*)
+  timeout 900 python bench.py --config zamba7b --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/zamba_$TAG.txt 2>&1; tail -1 gpurun_out/zamba_$TAG.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('ZAMBA', d['value'], d['ttft_ms'], d['tpot_ms'], d['roofline']['kernel'], d['roofline']['frac'])" ;;
+esac

@@ -151,14 +151,16 @@ def test_mixer_tp1_bf16_prefill_decode(dims_name, pack):
 
 
 @pytest.mark.parametrize("B,dims_name", [(1, "med"), (16, "med"), (17, "med"), (32, "med"), (5, "med_zamba"),
-                                         (4, "med_falcon")])
+                                         (4, "med_falcon"), (16, "med_zamba_wide")])
 def test_fused_decode_inproj_matches_unfused_and_oracle(B, dims_name, monkeypatch):
     """Decode in_proj with the conv step and x_proj fused into its epilogue (tokens split over
     the two epilogue halves, x_proj partials accumulated into the state's zeroed buffer and
     re-zeroed by out_proj) against the unfused kernel chain and the oracle, over several steps."""
     dims = {"med": MED,
             "med_falcon": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, bcdt_rmsnorm=True),
-            "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2)}[dims_name]
+            "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2),
+            # P = dt_rank + 2 d_state = 272 > 256 (Zamba-7B: 264): the fused path's widest x_proj
+            "med_zamba_wide": synth.MixerDims(d_model=256, d_inner=512, dt_rank=240, n_heads=2)}[dims_name]
     res = {}
     for fuse, fuse_ds in (("1", "1"), ("1", "0"), ("0", "1"), ("0", "0")):
         monkeypatch.setenv("SSM_FUSE_DECODE", fuse)
