@@ -120,3 +120,9 @@ esac
 case " $* " in *" zamba "*)
   timeout 900 python bench.py --config zamba7b --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/zamba_$TAG.txt 2>&1; tail -1 gpurun_out/zamba_$TAG.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('ZAMBA', d['value'], d['ttft_ms'], d['tpot_ms'], d['roofline']['kernel'], d['roofline']['frac'])" ;;
 esac
+case " $* " in *" falcon "*)
+  timeout 900 python bench.py --config falcon7b --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/falcon_$TAG.txt 2>&1; tail -1 gpurun_out/falcon_$TAG.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('FALCON', d['value'], d['ttft_ms'], d['tpot_ms'], d['roofline']['kernel'], d['roofline']['frac'])" ;;
+esac
+case " $* " in *" splitab "*)
+  (for v in 0 1 0 1; do SSM_SCAN_SPLIT=$v timeout 120 python scripts/scan_micro.py; done; SSM_SCAN_SPLIT=1 timeout 300 python -m pytest tests -m gpu -q -x -k "scan or prefill or chunk" -p no:cacheprovider 2>&1 | tail -2) > gpurun_out/splitab_$TAG.txt 2>&1; cat gpurun_out/splitab_$TAG.txt ;;
+esac
