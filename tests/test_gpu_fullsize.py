@@ -64,3 +64,13 @@ def test_falcon7b_layer_chunked_sampled_rows():
 def test_zamba7b_layer_two_heads_sampled_rows():
     # Zamba-7B Mamba layer shapes (d_model 3712, dt_rank 232, 2 x_proj heads) at TP=1
     _run(synth.CONFIGS["zamba7b"], 4, 384, 2, rows=(2,))
+
+
+def test_falcon7b_decode_bench_batch_sampled_rows():
+    # the decode launch configuration bench.py times for Falcon-Mamba-7B: batch 32 through the
+    # fused decode in_proj (P = 288 x_proj outputs per token) and the decode step
+    _run(synth.CONFIGS["falcon7b"], synth.WORKLOADS["falcon7b"]["batch"], 64, 4, rows=(0, 31))
+
+
+def test_zamba7b_decode_bench_batch_sampled_rows():
+    _run(synth.CONFIGS["zamba7b"], synth.WORKLOADS["zamba7b"]["batch"], 64, 4, rows=(0, 15))
