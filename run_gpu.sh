@@ -126,3 +126,9 @@ esac
 case " $* " in *" splitab "*)
   (for v in 0 1 0 1; do SSM_SCAN_SPLIT=$v timeout 120 python scripts/scan_micro.py; done; SSM_SCAN_SPLIT=1 timeout 300 python -m pytest tests -m gpu -q -x -k "scan or prefill or chunk" -p no:cacheprovider 2>&1 | tail -2) > gpurun_out/splitab_$TAG.txt 2>&1; cat gpurun_out/splitab_$TAG.txt ;;
 esac
+case " $* " in *" tl "*)
+  timeout 300 python scripts/decode_timeline.py 8 > gpurun_out/timeline_$TAG.txt 2>&1; cat gpurun_out/timeline_$TAG.txt | tail -45 ;;
+esac
+case " $* " in *" fsab "*)
+  (for v in 1 0 1 0; do SSM_FLAG_SYNC=$v timeout 120 python scripts/decode_ablation.py; done; SSM_PRENORM=0 timeout 120 python scripts/decode_ablation.py; timeout 120 python scripts/decode_timeline.py 4 | tail -22) > gpurun_out/fsab_$TAG.txt 2>&1; cat gpurun_out/fsab_$TAG.txt ;;
+esac
