@@ -132,3 +132,6 @@ esac
 case " $* " in *" fsab "*)
   (for v in 1 0 1 0; do SSM_FLAG_SYNC=$v timeout 120 python scripts/decode_ablation.py; done; SSM_PRENORM=0 timeout 120 python scripts/decode_ablation.py; timeout 120 python scripts/decode_timeline.py 4 | tail -22) > gpurun_out/fsab_$TAG.txt 2>&1; cat gpurun_out/fsab_$TAG.txt ;;
 esac
+case " $* " in *" xcab "*)
+  (for v in 1 2 4 1 2 4; do SSM_XACC_COPIES=$v timeout 120 python scripts/decode_ablation.py | sed "s/^/copies=$v /"; done; SSM_XACC_COPIES=4 timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "fused or stack" -p no:cacheprovider 2>&1 | tail -2) > gpurun_out/xcab_$TAG.txt 2>&1; cat gpurun_out/xcab_$TAG.txt ;;
+esac
