@@ -640,10 +640,19 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ 
     if (k < nv) {
       float4 ww = make_float4(1.f, 1.f, 1.f, 1.f);
       if (w) ww = reinterpret_cast<const float4*>(w)[k];
-      io<T>::st(yr + 4 * k, v[i].x * rs * ww.x);
-      io<T>::st(yr + 4 * k + 1, v[i].y * rs * ww.y);
-      io<T>::st(yr + 4 * k + 2, v[i].z * rs * ww.z);
-      io<T>::st(yr + 4 * k + 3, v[i].w * rs * ww.w);
+      if constexpr (sizeof(T) == 2) {  // one 8-B store of 4 bf16
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(v[i].x * rs * ww.x, v[i].y * rs * ww.y);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(v[i].z * rs * ww.z, v[i].w * rs * ww.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+        reinterpret_cast<uint2*>(yr)[k] = pk;
+      } else {
+        io<T>::st(yr + 4 * k, v[i].x * rs * ww.x);
+        io<T>::st(yr + 4 * k + 1, v[i].y * rs * ww.y);
+        io<T>::st(yr + 4 * k + 2, v[i].z * rs * ww.z);
+        io<T>::st(yr + 4 * k + 3, v[i].w * rs * ww.w);
+      }
     }
   }
 }
