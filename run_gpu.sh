@@ -135,3 +135,6 @@ esac
 case " $* " in *" xcab "*)
   (for v in 1 2 4 1 2 4; do SSM_XACC_COPIES=$v timeout 120 python scripts/decode_ablation.py | sed "s/^/copies=$v /"; done; SSM_XACC_COPIES=4 timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "fused or stack" -p no:cacheprovider 2>&1 | tail -2) > gpurun_out/xcab_$TAG.txt 2>&1; cat gpurun_out/xcab_$TAG.txt ;;
 esac
+case " $* " in *" splitpf "*)
+  (for v in 1 0 1 0; do SSM_PREFILL_SPLIT=$v timeout 600 python bench.py --no-cpu --no-e2e --decode 8 --steps 3 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('split=$v', 'ttft', round(d['ttft_ms'],1), 'tpot', round(d['tpot_ms'],3))"; done; SSM_GEMM_TRIM_RING=0 SSM_PREFILL_SPLIT=0 timeout 600 python bench.py --no-cpu --no-e2e --decode 8 --steps 3 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('notrim nosplit ttft', round(d['ttft_ms'],1))") > gpurun_out/splitpf_$TAG.txt 2>&1; cat gpurun_out/splitpf_$TAG.txt ;;
+esac
