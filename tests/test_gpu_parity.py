@@ -460,3 +460,45 @@ def test_stack_decode_prenorm_in_inproj_matches_separate_norm(graph):
             assert mx.fused_calls() > 0
     r0 = res0[:, L_in:].numpy()
     assert rel(outs[True] - r0, outs[False] - r0) < 5e-3
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_degenerate_softplus_linear_branch_and_full_decay(dtype, monkeypatch):
+    """Degenerate regimes of the method (reading Q2): dt_proj bias so large that
+    softplus takes its linear branch (v > 20) and decays exp(dt A) underflow to 0 (h forgets
+    everything each step), plus a zero-bias half where softplus(v) ~ ln 2 -- prefill and decode
+    against the oracle."""
+    dims = synth.CONFIGS["tiny"] if dtype == "fp32" else MED
+    B, L_in, L_out = 2, 24, 3
+    w = prep_weights(dims, 0, dtype)
+    E = dims.d_inner
+    w["b_dt"] = w["b_dt"].clone()
+    w["b_dt"][: E // 2] = 25.0                 # softplus linear branch, decay exp(-25 e^{A_log}) -> 0
+    w["b_dt"][E // 2:] = 0.0
+    x, res = prep_acts(B, L_in + L_out, dims, dtype, seed=5)
+    mx = TPMixer(dims, dtype)
+    lw = LayerWeights(dims, w, dtype=dtype)
+    st = State(mx, B)
+    xi = to_dev(x[:, :L_in], dtype).view(B * L_in, -1)
+    r = res[:, :L_in].float().cuda().contiguous().view(B * L_in, -1)
+    mx.prefill(lw, st, xi, r)
+    outs = [r.view(B, L_in, -1)]
+    for t in range(L_in, L_in + L_out):
+        rt = res[:, t].float().cuda().contiguous()
+        mx.decode(lw, st, to_dev(x[:, t], dtype), rt)
+        outs.append(rt.view(B, 1, -1))
+    torch.cuda.synchronize()
+    gpu = torch.cat([o.cpu() for o in outs], 1).double().numpy()
+    ref, st_ref = M.mixer_forward(dims, np64(w), x.numpy(), res.numpy())
+    resn = res.numpy()
+    assert rel(gpu - resn, ref - resn) < TOL[dtype]
+    _, h = oracle_state_from_gpu_layout(st.conv, st.h)
+    assert rel(h, st_ref[1]) < TOL[dtype]
+
+
+def test_long_prompt_64k_single_chunk():
+    """The cfg5 prompt length (65536 tokens, the longest sequence the bench runs) as ONE prefill
+    call of 2 x 65536 = 131072 rows, then two decode steps, against the oracle (narrow channels so
+    the fp64 oracle stays quick; the scan carries its state across all 65536 steps)."""
+    import test_gpu_fullsize as F
+    F._run(MED, 2, 65536, 2, rows=(0, 1))
