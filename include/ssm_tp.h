@@ -229,7 +229,9 @@ ssm_status_t ssm_mixer_decode_prenorm(ssm_tp_t tp, const ssm_layer_weights_t* w,
  * +-127), exchanges int8 codes + fp32 scales peer-to-peer, and forms
  * out = sum_{r=0..k-1} s_r q_r in fixed rank order in fp32 (bitwise identical on all
  * ranks).  out may alias partial.  tp_size == 1: out = partial (no quantisation).
- * flags: SSM_QAR_ACCUMULATE, SSM_QAR_FP16.  Error bound per element: sum_r s_r / 2 (int8);
+ * n == 0 is a no-op (pointers may be NULL; with tp_size > 1 every rank must agree on it).
+ * flags: SSM_QAR_ACCUMULATE, SSM_QAR_FP16, SSM_QAR_TWOSHOT (shared-scale two-shot schedule).
+ * Error bound per element: sum_r s_r / 2 (int8 one-shot); k max_r amax_r / 254 (two-shot);
  * sum_r (|o_r| 2^-11 + 2^-25) + the fp32 additions (fp16 wire). */
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n,
                             uint32_t flags, void* stream);

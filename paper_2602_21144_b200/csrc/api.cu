@@ -864,7 +864,9 @@ ssm_status_t ssm_mixer_decode_chained(ssm_tp_t tp, const ssm_layer_weights_t* w,
 }
 
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
-  if (!tp || !partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
+  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
+  if (n == 0 && !(flags & ~(uint32_t)(SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_TWOSHOT))) return SSM_OK;  // nothing to reduce
+  if (!partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
   if (flags & ~(uint32_t)(SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_TWOSHOT))
     return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
   const int blk = tp->cfg.qar_block;

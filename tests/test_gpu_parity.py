@@ -502,3 +502,28 @@ def test_long_prompt_64k_single_chunk():
     the fp64 oracle stays quick; the scan carries its state across all 65536 steps)."""
     import test_gpu_fullsize as F
     F._run(MED, 2, 65536, 2, rows=(0, 1))
+
+
+def test_empty_calls_are_noops_and_state_untouched():
+    """Empty inputs: prefill with seqlen 0 and qallreduce with n = 0 return OK without touching the
+    residual or the cache (SPEC.md:162, 172 shapes; reading Q19: chunking, including empty
+    chunks, must not change the result)."""
+    dims = MED
+    mx = TPMixer(dims, "bf16")
+    w = LayerWeights(dims, prep_weights(dims, 0, "bf16"))
+    st = State(mx, 2)
+    x, res = prep_acts(2, 6, dims, "bf16", seed=3)
+    xi = to_dev(x, "bf16").view(12, -1)
+    r = res.float().cuda().contiguous().view(12, -1)
+    mx.prefill(w, st, xi, r)
+    torch.cuda.synchronize()
+    h0, c0, r0 = st.h.clone(), st.conv.clone(), r.clone()
+    e = torch.empty(0, dims.d_model, device="cuda")
+    L.call("ssm_mixer_prefill", mx.handle, __import__("ctypes").byref(w.struct), st.handle, xi.data_ptr(),
+           r.data_ptr(), 2, 0, L.SSM_AR2_INT8, mx.workspace(2, 1).data_ptr(), mx.workspace_bytes(2, 1), None)
+    zbuf = torch.full((128,), 7.0, device="cuda")
+    mx.qallreduce(zbuf[:0], zbuf[:0])            # n = 0 (valid pointers): no work
+    torch.cuda.synchronize()
+    assert torch.equal(st.h, h0) and torch.equal(st.conv, c0) and torch.equal(r, r0)
+    assert torch.all(zbuf == 7.0)
+    del e
