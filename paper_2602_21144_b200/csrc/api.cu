@@ -63,6 +63,8 @@ const bool g_out_local = [] { const char* e = getenv("SSM_OUT_LOCAL"); return e 
 // channel-owned out_proj shape: SSM_OUT_Q m-groups per k-split of SSM_OUT_KBS 64-channel k-blocks
 const int g_out_q = [] { const char* e = getenv("SSM_OUT_Q"); return e ? atoi(e) : 4; }();
 const int g_out_kbs = [] { const char* e = getenv("SSM_OUT_KBS"); return e ? atoi(e) : 4; }();
+// SSM_FUSE_AR1=0: no fused decode in_proj when AR#1 follows (TP > 1 with one x_proj group)
+const bool g_fuse_ar1 = [] { const char* e = getenv("SSM_FUSE_AR1"); return !e || atoi(e) != 0; }();
 // SSM_INPROJ_SK=1: the fused decode in_proj runs stream-K over all SMs instead of one CTA per
 // 128-row tile (measured slower: 58 vs 40 us per Mamba-2.8B decode layer; the weight stream of
 // the one-tile-per-CTA kernel already runs at ~6.1 TB/s, profiles/r01_gemm_timeline_34.txt)
@@ -345,7 +347,9 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   // Fused decode (no AR#1 between x_proj and the scan): the in_proj epilogue also runs the conv
   // step (a2) and adds its x_proj partial (a3) into the state's zeroed accumulator.
   float* xacc = reinterpret_cast<float*>(reinterpret_cast<char*>(st->h) + xacc_offset(t, batch));
-  const bool fuse = swap && !ar1 && t->fuse_decode && batch <= 32 && P <= 320 && P % 2 == 0 && K >= 2 && K <= 4 &&
+  // (with AR#1 the partial is published to the symmetric buffer by publish_barrier_kernel)
+  const bool fuse = swap && (!ar1 || g_fuse_ar1) && t->fuse_decode && batch <= 32 && P <= 320 && P % 2 == 0 &&
+                    K >= 2 && K <= 4 &&
                     t->cph % 128 == 0 && !(skip & 7) &&
                     gemm_tc_supported(w->w_in, D, x_in, D);
   float* css = reinterpret_cast<float*>(W + L.css);
@@ -438,7 +442,10 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   int64_t doff = 0;
   if (ar1) {
     t->launches++;
-    CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
+    if (fuse)
+      CU(launch_publish_barrier(t->peers, t->rank, t->k, xacc, (int64_t)batch * hl * P, half_off(ep1), s));
+    else
+      CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
     dsrc = group_peers(t, t->ar1_group);
     nsrc = t->ar1_group;
     doff = half_off(ep1);
@@ -526,7 +533,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     if (swap) {
       Epilogue e = epi(EPI_ATOMIC_F32, 1, odst, D);
       // re-arm the x_proj accumulator (channel-owned mode: its last reader does)
-      if (fuse && !local_ds) { e.zero = xacc; e.nzero = (int64_t)batch * hl * P; }
+      if (fuse && !local_ds && !ar1) { e.zero = xacc; e.nzero = (int64_t)batch * hl * P; }  // (ar1: the publish kernel re-zeroes it)
       if (chain) {  // last contributor of each residual tile: next layer's bf16 B operand + sums of squares
         e.fin_cnt = ccnt;
         e.fin_x = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(x_in));

@@ -183,6 +183,10 @@ cudaError_t launch_f16_reduce(Peers src, int k, int64_t off, int64_t n, float* o
 // of every peer's signal area, wait for all peers' slots in our own area to reach it
 // (bounded; sets the error word on timeout).
 cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s);
+// fused decode at TP > 1: copy the x_proj partial (state-local, n floats) into this rank's
+// symmetric buffer at dst_off, re-zero it, then the cross-rank barrier
+cudaError_t launch_publish_barrier(Peers bufs, int rank, int k, float* xacc, int64_t n, int64_t dst_off,
+                                   cudaStream_t s);
 
 // ---- persistent whole-stack decode (decode_mk.cu) ----
 // One layer of the stack as the persistent decode kernel reads it (TP=1, bf16, one x_proj head).

@@ -1254,6 +1254,55 @@ cudaError_t preload_kernels() {
   return cudaSuccess;
 }
 
+// AR#1 publish + barrier of the fused decode path at TP > 1: the fused in_proj accumulated this
+// rank's x_proj partial into the state-local buffer xacc; copy it into the rank's symmetric
+// buffer (where the peers read it), re-zero xacc for the next token, then the cross-rank barrier
+// (the copies are ordered before the flag by bar.sync + the signalling threads' fence.sys).
+__global__ void __launch_bounds__(256) publish_barrier_kernel(Peers bufs, int rank, int k, float* __restrict__ xacc,
+                                                              int64_t n, int64_t dst_off) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ uint32_t s_epoch;
+  const int t = threadIdx.x;
+  float* dst = reinterpret_cast<float*>(reinterpret_cast<char*>(bufs.p[rank]) + dst_off);
+  for (int64_t i = t; i < n / 4; i += 256) {
+    reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(xacc)[i];
+    reinterpret_cast<float4*>(xacc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int64_t i = 4 * (n / 4) + t; i < n; i += 256) {
+    dst[i] = xacc[i];
+    xacc[i] = 0.f;
+  }
+  uint32_t* own = reinterpret_cast<uint32_t*>(bufs.p[rank]);
+  if (t == 0) s_epoch = atomicAdd(own + 32, 1u) + 1u;
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  if (t < k) {
+    fence_sys();
+    st_release_sys(reinterpret_cast<uint32_t*>(bufs.p[t]) + rank, epoch);
+  }
+  __syncwarp();
+  if (t < k) {
+    const uint32_t* slot = own + t;
+    const uint64_t t0 = globaltimer();
+    while ((int32_t)(ld_acquire_sys(slot) - epoch) < 0) {
+      if (globaltimer() - t0 > 20ull * 1000000000ull) {
+        atomicExch(own + 16, 1u);
+        break;
+      }
+    }
+  }
+  __syncwarp();
+  fence_sys();
+}
+
+cudaError_t launch_publish_barrier(Peers bufs, int rank, int k, float* xacc, int64_t n, int64_t dst_off,
+                                   cudaStream_t s) {
+  if ((reinterpret_cast<uintptr_t>(xacc) & 15) || (dst_off & 15)) return cudaErrorInvalidValue;
+  { cudaError_t e_ = launch(publish_barrier_kernel, 1, 256, 0, s, bufs, rank, k, xacc, n, dst_off); if (e_ != cudaSuccess) return e_; }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s) {
   { cudaError_t e_ = launch(peer_barrier_kernel, 1, 32, 0, s, bufs, rank, k); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();

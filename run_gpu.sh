@@ -138,3 +138,35 @@ esac
 case " $* " in *" splitpf "*)
   (for v in 1 0 1 0; do SSM_PREFILL_SPLIT=$v timeout 600 python bench.py --no-cpu --no-e2e --decode 8 --steps 3 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('split=$v', 'ttft', round(d['ttft_ms'],1), 'tpot', round(d['tpot_ms'],3))"; done; SSM_GEMM_TRIM_RING=0 SSM_PREFILL_SPLIT=0 timeout 600 python bench.py --no-cpu --no-e2e --decode 8 --steps 3 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('notrim nosplit ttft', round(d['ttft_ms'],1))") > gpurun_out/splitpf_$TAG.txt 2>&1; cat gpurun_out/splitpf_$TAG.txt ;;
 esac
+case " $* " in *" tpdec "*)
+  cat > /tmp/tpdec.py <<'PY'
+import os, sys, torch
+sys.path.insert(0, os.getcwd())
+import synth
+from paper_2602_21144_b200 import _lib as L
+from paper_2602_21144_b200.mixer import LayerWeights
+from paper_2602_21144_b200.stack import MixerStack, synthetic_layer
+from paper_2602_21144_b200.virtual import VirtualGroup
+dims = synth.CONFIGS["mamba2.8b"]; B = 16; nl = 8
+for k in (2, 4, 8):
+    grp = VirtualGroup(dims, k, "bf16", B)
+    full = [synthetic_layer(dims, l) for l in range(nl)]
+    stacks = []
+    for r in range(k):
+        lws = [LayerWeights(dims, w, k, r, "bf16") for w in full]
+        for lw in lws: lw.pack(grp.mixers[r])
+        stacks.append(MixerStack(grp.mixers[r], lws, B, 1, L.SSM_AR2_INT8))
+    del full
+    res = [torch.randn(B, dims.d_model, device="cuda") for _ in range(k)]
+    for _ in range(3):
+        grp.run(lambda r, mx, s: stacks[r].decode_step(res[r], s))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        grp.run(lambda r, mx, s: stacks[r].decode_step(res[r], s))
+    e1.record(); torch.cuda.synchronize()
+    print(f"virtual TP={k} ({os.environ.get('SSM_FUSE_AR1','1')}): {e0.elapsed_time(e1)*1000/5/nl:.1f} us per layer-step (all k ranks on ONE GPU), fused calls {grp.mixers[0].fused_calls()}", flush=True)
+    del stacks, grp; torch.cuda.empty_cache()
+PY
+  (for v in 1 0; do SSM_FUSE_AR1=$v timeout 300 python /tmp/tpdec.py; done) > gpurun_out/tpdec_$TAG.txt 2>&1; cat gpurun_out/tpdec_$TAG.txt | tail -8 ;;
+esac
