@@ -340,7 +340,8 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   // decode GEMMs (swap-AB): split-K with the fp32 atomic epilogue so the few weight-row tiles
   // spread over the SMs (measured best: ~1 unit per SM, <= 32 splits)
   const int ks_x = swap ? split_for(t, hl * P, Ek) : 1;
-  const int ks_o = swap ? split_for(t, D, Ek) : 1;
+  static const int ks_o_env = [] { const char* e = getenv("SSM_OUT_KS"); return e ? atoi(e) : 0; }();
+  const int ks_o = swap ? (ks_o_env > 0 ? ks_o_env : split_for(t, D, Ek)) : 1;
 
   // (a1) in_proj, column-parallel: xz = x_in W_in,r^T   [M, 2E_k]
   const int skip = decode ? g_dbg_skip : 0;
