@@ -52,6 +52,8 @@ struct CtaRes {
                      // epilogue: independent MMA chains for skinny N, where one chain is MMA-latency bound
   int slot_cols;     // TMEM columns per partial accumulator (>= BN, multiple of 32)
 };
+// SSM_GEMM_VARIANTS=0: every GEMM on the all-paths kernel instantiation
+const bool g_gemm_variants = [] { const char* e = getenv("SSM_GEMM_VARIANTS"); return !e || atoi(e) != 0; }();
 const bool kMinBN16 = [] { const char* e = getenv("SSM_GEMM_BN16"); return !e || atoi(e) != 0; }();
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane group)
 
@@ -110,6 +112,18 @@ struct TileSched {
 
 // partial accumulators actually written for a tile of (kb1 - kb0) k-blocks (4 UMMA k-steps each)
 __device__ __forceinline__ int tile_nacc(const CtaRes& cr, int kb0, int kb1) { return min(cr.nacc, 4 * (kb1 - kb0)); }
+
+// The only epilogue of the VAR 2 kernel: C[n * ldc + m] += acc atomically (swap-AB split-K).
+__device__ __forceinline__ void epi_chunk_atomic_trans(const Epilogue& e, int m0, int n0, int M, int N,
+                                                       uint32_t (&r)[32]) {
+  const int m = m0 + threadIdx.x % 32;
+  if (m >= M) return;
+  const int nv = min(32, N - n0);
+  float* C = reinterpret_cast<float*>(e.C) + (int64_t)n0 * e.ldc + m;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < nv) atomicAdd(C + (int64_t)j * e.ldc, __uint_as_float(r[j]));
+}
 
 // Epilogue for one warp's 32 x 32 chunk: lane = row m0 + lane, columns n0..n0+31, stored
 // straight from registers (staging through shared memory would compete with the UMMA operand
@@ -630,6 +644,10 @@ __device__ unsigned long long g_trace[kTraceCtas * kTraceSlots];
     if ((cr.nomma & 8) && blockIdx.x < kTraceCtas) g_trace[blockIdx.x * kTraceSlots + (slot)] = (val); \
   } while (0)
 
+// VAR: 0 = every path (prefill GEMMs, experiments); 1 = the fused decode in_proj only; 2 = skinny
+// swap-AB split-K GEMMs with the atomic epilogue only (decode out_proj / x_proj).  The decode
+// variants are separate kernels so their register allocation is not set by paths they never run.
+template <int VAR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_blk, int64_t lda, int K,
@@ -799,7 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ---------------- epilogue warps 2..9; TMEM lane group = warp % 4, column half = (warp-2)/4
     pdl_wait();
-    if (job.enabled) {
+    if (VAR == 0 && job.enabled) {
       if (job.local) {
         const int js = (int)((2 * dstep_smem(job.R, job.N, 2, kJobIpt) + 127) / 128 * 128);
         run_dstep_local(job, reinterpret_cast<float*>(smem + cr.ring + 512), ts,
@@ -815,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         reinterpret_cast<float4*>(epi.zero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int64_t i = 4 * n4 + threadIdx.x - 64; i < epi.nzero; i += kThreads - 64) epi.zero[i] = 0.f;
     }
-    if (epi.nres) {
+    if (VAR == 0 && epi.nres) {
       // pre-norm of the N residual rows -> the bf16 B operand (global; identical in every CTA)
       // the warp's rows are handled together, 8 x 16-B loads per row in flight per lane per chunk
       const int et = threadIdx.x - 64, w8 = et >> 5;
@@ -868,11 +886,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar_sync(1, 256);
       if (threadIdx.x == 64) mbar_arrive(bready);
     }
-    if (epi.kind == EPI_DECODE_INPROJ) {
+    if (VAR == 1 || (VAR == 0 && epi.kind == EPI_DECODE_INPROJ)) {
       decode_inproj_epilogue(epi, ts, M, N, tfull, tempty, tmem_base, cr,
                              reinterpret_cast<__nv_bfloat16*>(smem + cr.ring + 512));
       goto teardown;
     }
+    if constexpr (VAR != 1)
     {
     const int eg = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -926,14 +945,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("add.u32 %0, %1, %2;" : "=r"(dep) : "r"(r[0]), "r"(r[31]));
           TRACE(8, clock64() - c_start + (dep == 0x7f123456u ? 1 : 0));
         }
-        if (!(cr.nomma & 4)) epi_chunk(epi, m0, nt * BN + c * 32, M, N, r, pre ? bpre : nullptr);
+        if (!(cr.nomma & 4)) {
+          if constexpr (VAR == 2) epi_chunk_atomic_trans(epi, m0, nt * BN + c * 32, M, N, r);
+          else epi_chunk(epi, m0, nt * BN + c * 32, M, N, r, pre ? bpre : nullptr);
+        }
       }
       if (threadIdx.x == 64) TRACE(9, clock64() - c_start);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
-      if (epi.fin_cnt) chain_finalise(epi, mt, M, N, reinterpret_cast<float*>(smem + cr.ring + 512));
+      if (VAR == 0 && epi.fin_cnt) chain_finalise(epi, mt, M, N, reinterpret_cast<float*>(smem + cr.ring + 512));
     }
     }
   }
@@ -1025,10 +1047,13 @@ cudaError_t gemm_trace_read(unsigned long long* host, int n) {
 }
 
 cudaError_t preload_gemm_tc() {
-  cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
   cudaFuncAttributes a;
-  return cudaFuncGetAttributes(&a, (const void*)gemm_tc_kernel);
+  for (const void* f : {(const void*)gemm_tc_kernel<0>, (const void*)gemm_tc_kernel<1>, (const void*)gemm_tc_kernel<2>}) {
+    if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess) return e;
+    if ((e = cudaFuncGetAttributes(&a, f)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb) {
@@ -1081,7 +1106,9 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
 
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -1171,7 +1198,14 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     if (ts.streamk || epi2.kind != EPI_ATOMIC_F32 || !epi2.trans || BM != 128) return cudaErrorInvalidValue;
     epi2.fin_need = ts.ksplit * ts.n_tiles;
   }
-  { cudaError_t e_ = launch(gemm_tc_kernel, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi2,
+  // kernel variant (see gemm_tc_kernel): decode GEMMs on their own instantiations
+  int var = 0;
+  if (g_gemm_variants && !job.enabled && !epi2.fin_cnt && !epi2.nres && !epi2.pf && !ts.streamk) {
+    if (epi2.kind == EPI_DECODE_INPROJ) var = 1;
+    else if (epi2.kind == EPI_ATOMIC_F32 && epi2.trans && BN <= 32) var = 2;
+  }
+  auto kfn = var == 1 ? gemm_tc_kernel<1> : var == 2 ? gemm_tc_kernel<2> : gemm_tc_kernel<0>;
+  { cudaError_t e_ = launch(kfn, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi2,
                                       A_blocked, lda, K, cr, A_blocked ? 1 : 0, job);
     if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
