@@ -268,6 +268,7 @@ constexpr int SU_LD = 136;                       // u tile row pitch (bf16): con
 constexpr int SU_BYTES = 32 * SU_LD * 2;         // u tile [32 tokens][128 channels] bf16
 constexpr int XP_NT = 5;                         // x_proj n-tiles (8 outputs) per warp: P <= 320 (Zamba: 264)
 
+template <int XPN = XP_NT>  // x_proj n-tiles per warp: P <= 64 XPN
 __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const TileSched& ts, int M, int N,
                                                        uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
                                                        const CtaRes& cr, __nv_bfloat16* su) {
@@ -307,11 +308,11 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
             if (j < K - 1) win[j][q / 2] |= (uint32_t)cs16[((int64_t)b * (K - 1) + j) * Ek + f] << (16 * (q & 1));
       }
     }
-    uint32_t wf[XP_NT][8][2];  // W_x B-fragments: rows p = 8 nt + lane / 4, cols f0 + 16 ks + 2 (lane % 4) (+8)
+    uint32_t wf[XPN][8][2];  // W_x B-fragments: rows p = 8 nt + lane / 4, cols f0 + 16 ks + 2 (lane % 4) (+8)
     const int hd = f0 / e.cph;
     if (tile_x) {
 #pragma unroll
-      for (int i = 0; i < XP_NT; ++i) {
+      for (int i = 0; i < XPN; ++i) {
         const int p = (ew + 8 * i) * 8 + lane / 4;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
@@ -429,7 +430,7 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
         for (int ks = 0; ks < 8; ++ks)
           ldmatrix_x4(a[ks], su + (mi * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * SU_LD + ks * 16 + (lane >> 4) * 8);
 #pragma unroll
-        for (int i = 0; i < XP_NT; ++i) {
+        for (int i = 0; i < XPN; ++i) {
           const int p0 = (ew + 8 * i) * 8;
           if (p0 >= P) continue;
           float d[4] = {0.f, 0.f, 0.f, 0.f};
@@ -647,7 +648,7 @@ __device__ unsigned long long g_trace[kTraceCtas * kTraceSlots];
 // VAR: 0 = every path (prefill GEMMs, experiments); 1 = the fused decode in_proj only; 2 = skinny
 // swap-AB split-K GEMMs with the atomic epilogue only (decode out_proj / x_proj).  The decode
 // variants are separate kernels so their register allocation is not set by paths they never run.
-template <int VAR>
+template <int VAR, int XPN = XP_NT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_blk, int64_t lda, int K,
@@ -887,8 +888,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 64) mbar_arrive(bready);
     }
     if (VAR == 1 || (VAR == 0 && epi.kind == EPI_DECODE_INPROJ)) {
-      decode_inproj_epilogue(epi, ts, M, N, tfull, tempty, tmem_base, cr,
-                             reinterpret_cast<__nv_bfloat16*>(smem + cr.ring + 512));
+      decode_inproj_epilogue<XPN>(epi, ts, M, N, tfull, tempty, tmem_base, cr,
+                                  reinterpret_cast<__nv_bfloat16*>(smem + cr.ring + 512));
       goto teardown;
     }
     if constexpr (VAR != 1)
@@ -1049,7 +1050,8 @@ cudaError_t gemm_trace_read(unsigned long long* host, int n) {
 cudaError_t preload_gemm_tc() {
   cudaError_t e = cudaSuccess;
   cudaFuncAttributes a;
-  for (const void* f : {(const void*)gemm_tc_kernel<0>, (const void*)gemm_tc_kernel<1>, (const void*)gemm_tc_kernel<2>}) {
+  for (const void* f : {(const void*)gemm_tc_kernel<0>, (const void*)gemm_tc_kernel<1>, (const void*)gemm_tc_kernel<1, 3>,
+                        (const void*)gemm_tc_kernel<1, 4>, (const void*)gemm_tc_kernel<2>}) {
     if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess) return e;
     if ((e = cudaFuncGetAttributes(&a, f)) != cudaSuccess) return e;
   }
@@ -1108,6 +1110,8 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -1204,7 +1208,8 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     if (epi2.kind == EPI_DECODE_INPROJ) var = 1;
     else if (epi2.kind == EPI_ATOMIC_F32 && epi2.trans && BN <= 32) var = 2;
   }
-  auto kfn = var == 1 ? gemm_tc_kernel<1> : var == 2 ? gemm_tc_kernel<2> : gemm_tc_kernel<0>;
+  auto kfn = var == 2 ? gemm_tc_kernel<2> : gemm_tc_kernel<0>;
+  if (var == 1) kfn = epi2.P <= 64 * 3 ? gemm_tc_kernel<1, 3> : epi2.P <= 64 * 4 ? gemm_tc_kernel<1, 4> : gemm_tc_kernel<1>;
   { cudaError_t e_ = launch(kfn, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi2,
                                       A_blocked, lda, K, cr, A_blocked ? 1 : 0, job);
     if (e_ != cudaSuccess) return e_; }
