@@ -56,6 +56,10 @@ struct CtaRes {
 const bool g_gemm_variants = [] { const char* e = getenv("SSM_GEMM_VARIANTS"); return !e || atoi(e) != 0; }();
 const bool kMinBN16 = [] { const char* e = getenv("SSM_GEMM_BN16"); return !e || atoi(e) != 0; }();
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane group)
+// threads of a kernel variant: the skinny atomic variant (VAR 2, BN <= 32: one 32-column chunk, so
+// only the first epilogue half ever works) runs 4 epilogue warps -- a smaller CTA that fits next
+// to the decode-step blocks it follows
+constexpr int var_threads(int var) { return var == 2 ? 192 : kThreads; }
 
 // Work decomposition.  Data-parallel mode: unit u = (k-split, m-tile, n-tile), CTAs stride
 // over units.  Stream-K mode (streamk != 0): the linearised (tile, k-block) space is cut into
@@ -649,7 +653,7 @@ __device__ unsigned long long g_trace[kTraceCtas * kTraceSlots];
 // swap-AB split-K GEMMs with the atomic epilogue only (decode out_proj / x_proj).  The decode
 // variants are separate kernels so their register allocation is not set by paths they never run.
 template <int VAR, int XPN = XP_NT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(var_threads(VAR), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_blk, int64_t lda, int K,
                    CtaRes cr, int a_blocked, const DStepJob job) {
@@ -696,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);
+      mbar_init(&tempty[i], (var_threads(VAR) - 64) / 32);
     }
     mbar_init(bready, 1);
     fence_barrier_init();
@@ -830,9 +834,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (epi.zero && blockIdx.x == 0) {  // (after the job: it may read the buffer being zeroed)
       const int64_t n4 = epi.nzero / 4;
-      for (int64_t i = threadIdx.x - 64; i < n4; i += kThreads - 64)
+      for (int64_t i = threadIdx.x - 64; i < n4; i += var_threads(VAR) - 64)
         reinterpret_cast<float4*>(epi.zero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int64_t i = 4 * n4 + threadIdx.x - 64; i < epi.nzero; i += kThreads - 64) epi.zero[i] = 0.f;
+      for (int64_t i = 4 * n4 + threadIdx.x - 64; i < epi.nzero; i += var_threads(VAR) - 64) epi.zero[i] = 0.f;
     }
     if (VAR == 0 && epi.nres) {
       // pre-norm of the N residual rows -> the bf16 B operand (global; identical in every CTA)
@@ -923,7 +927,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         const int nc = nt * BN + c * 32;
         float bpre[32];
-        const bool pre = (epi.kind == EPI_SOFTPLUS_BF16 || epi.kind == EPI_SOFTPLUS_F32) && !epi.trans &&
+        const bool pre = VAR == 0 && (epi.kind == EPI_SOFTPLUS_BF16 || epi.kind == EPI_SOFTPLUS_F32) && !epi.trans &&
                          nc + 32 <= N && ((reinterpret_cast<uintptr_t>(epi.bias + nc) & 15) == 0);
         if (pre) {
 #pragma unroll
@@ -1210,7 +1214,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   }
   auto kfn = var == 2 ? gemm_tc_kernel<2> : gemm_tc_kernel<0>;
   if (var == 1) kfn = epi2.P <= 64 * 3 ? gemm_tc_kernel<1, 3> : epi2.P <= 64 * 4 ? gemm_tc_kernel<1, 4> : gemm_tc_kernel<1>;
-  { cudaError_t e_ = launch(kfn, grid, kThreads, smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi2,
+  { cudaError_t e_ = launch(kfn, grid, var_threads(var), smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi2,
                                       A_blocked, lda, K, cr, A_blocked ? 1 : 0, job);
     if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
