@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(S3_THREADS) scan2_kernel(
 // ---------------------------------------------------------------- decode step
 // Body in dstep.cuh (shared with the out_proj GEMM, which can run it as its B-operand producer).
 template <typename T, int N, bool FAST, int IPT>
-__global__ void __launch_bounds__(DS_THREADS, IPT == 1 ? 5 : 3) decode_step_kernel(DStepArgs a, Peers src, int nsrc) {
+__global__ void __launch_bounds__(DS_THREADS, IPT == 1 ? 5 : IPT == 2 ? 4 : 3) decode_step_kernel(DStepArgs a, Peers src, int nsrc) {
   extern __shared__ __align__(16) float dsm[];
   pdl_trigger();
   if (a.pf && threadIdx.x < 32) {  // this block's slice of the successor's weights into L2
@@ -601,7 +601,11 @@ __global__ void __launch_bounds__(DS_THREADS, IPT == 1 ? 5 : 3) decode_step_kern
 }
 // items (batch rows) per thread of the standalone decode-step kernel: 1 (640 blocks for B = 16)
 // or 4 (160 blocks, 4x fewer W_dt reads, every item's loads in flight at once); SSM_DSTEP_IPT
-const int g_dstep_ipt = [] { const char* e = getenv("SSM_DSTEP_IPT"); return e && atoi(e) == 4 ? 4 : 1; }();
+const int g_dstep_ipt = [] {
+  const char* e = getenv("SSM_DSTEP_IPT");
+  const int v = e ? atoi(e) : 1;
+  return v == 4 ? 4 : v == 2 ? 2 : 1;
+}();
 
 // ---------------------------------------------------------------- RMSNorm (glue)
 // One 128-thread block per row, the row cached in registers (<= 16 float4 per thread).
@@ -1062,6 +1066,7 @@ static cudaError_t dstep_t(const DStepArgs& a, Peers src, int nsrc, cudaStream_t
   const size_t smem = dstep_smem(a.R, N, (int)sizeof(T), ipt);
   dim3 grid((a.Ek + DS_CH - 1) / DS_CH, (a.batch + DS_BB * ipt - 1) / (DS_BB * ipt));
   cudaError_t e_ = ipt == 4 ? launch(decode_step_kernel<T, N, F, 4>, grid, DS_THREADS, smem, s, a, src, nsrc)
+                 : ipt == 2 ? launch(decode_step_kernel<T, N, F, 2>, grid, DS_THREADS, smem, s, a, src, nsrc)
                             : launch(decode_step_kernel<T, N, F, 1>, grid, DS_THREADS, smem, s, a, src, nsrc);
   if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
