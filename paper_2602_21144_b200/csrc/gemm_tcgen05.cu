@@ -52,6 +52,8 @@ struct CtaRes {
                      // epilogue: independent MMA chains for skinny N, where one chain is MMA-latency bound
   int slot_cols;     // TMEM columns per partial accumulator (>= BN, multiple of 32)
 };
+// SSM_GEMM_PREFILL_VAR=0: the prefill GEMMs stay on the all-paths instantiation
+const int g_gemm_prefill_var = [] { const char* e = getenv("SSM_GEMM_PREFILL_VAR"); return e ? atoi(e) : 1; }();
 // SSM_GEMM_VARIANTS=0: every GEMM on the all-paths kernel instantiation
 const bool g_gemm_variants = [] { const char* e = getenv("SSM_GEMM_VARIANTS"); return !e || atoi(e) != 0; }();
 const bool kMinBN16 = [] { const char* e = getenv("SSM_GEMM_BN16"); return !e || atoi(e) != 0; }();
@@ -60,6 +62,10 @@ constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 
 // only the first epilogue half ever works) runs 4 epilogue warps -- a smaller CTA that fits next
 // to the decode-step blocks it follows
 constexpr int var_threads(int var) { return var == 2 ? 192 : kThreads; }
+// VAR 4..7: prefill GEMMs with one fixed (non-transposed) epilogue kind each
+constexpr int var_kind(int var) {
+  return var == 4 ? EPI_STORE_BF16 : var == 5 ? EPI_ADD_F32 : var == 6 ? EPI_SOFTPLUS_BF16 : var == 7 ? EPI_STORE_F32 : -1;
+}
 
 // Work decomposition.  Data-parallel mode: unit u = (k-split, m-tile, n-tile), CTAs stride
 // over units.  Stream-K mode (streamk != 0): the linearised (tile, k-block) space is cut into
@@ -132,9 +138,10 @@ __device__ __forceinline__ void epi_chunk_atomic_trans(const Epilogue& e, int m0
 // Epilogue for one warp's 32 x 32 chunk: lane = row m0 + lane, columns n0..n0+31, stored
 // straight from registers (staging through shared memory would compete with the UMMA operand
 // reads for smem bandwidth in the MMA-bound projections).
+template <int FK = -1>  // FK >= 0: the epilogue kind is fixed at compile time (other paths pruned)
 __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int M, int N, uint32_t (&r)[32],
                                           const float* bpre = nullptr) {
-  const int kind = e.kind;
+  const int kind = FK >= 0 ? FK : e.kind;
   const int m = m0 + threadIdx.x % 32;
   if (m >= M) return;
   float v[32];
@@ -927,7 +934,7 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         uint32_t r[32];
         const int nc = nt * BN + c * 32;
         float bpre[32];
-        const bool pre = VAR == 0 && (epi.kind == EPI_SOFTPLUS_BF16 || epi.kind == EPI_SOFTPLUS_F32) && !epi.trans &&
+        const bool pre = (VAR == 0 || VAR == 6) && (epi.kind == EPI_SOFTPLUS_BF16 || epi.kind == EPI_SOFTPLUS_F32) && !epi.trans &&
                          nc + 32 <= N && ((reinterpret_cast<uintptr_t>(epi.bias + nc) & 15) == 0);
         if (pre) {
 #pragma unroll
@@ -952,7 +959,7 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         }
         if (!(cr.nomma & 4)) {
           if constexpr (VAR == 2) epi_chunk_atomic_trans(epi, m0, nt * BN + c * 32, M, N, r);
-          else epi_chunk(epi, m0, nt * BN + c * 32, M, N, r, pre ? bpre : nullptr);
+          else epi_chunk<var_kind(VAR)>(epi, m0, nt * BN + c * 32, M, N, r, pre ? bpre : nullptr);
         }
       }
       if (threadIdx.x == 64) TRACE(9, clock64() - c_start);
@@ -1055,7 +1062,8 @@ cudaError_t preload_gemm_tc() {
   cudaError_t e = cudaSuccess;
   cudaFuncAttributes a;
   for (const void* f : {(const void*)gemm_tc_kernel<0>, (const void*)gemm_tc_kernel<1>, (const void*)gemm_tc_kernel<1, 3>,
-                        (const void*)gemm_tc_kernel<1, 4>, (const void*)gemm_tc_kernel<2>}) {
+                        (const void*)gemm_tc_kernel<1, 4>, (const void*)gemm_tc_kernel<2>, (const void*)gemm_tc_kernel<4>,
+                        (const void*)gemm_tc_kernel<5>, (const void*)gemm_tc_kernel<6>, (const void*)gemm_tc_kernel<7>}) {
     if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess) return e;
     if ((e = cudaFuncGetAttributes(&a, f)) != cudaSuccess) return e;
   }
@@ -1117,6 +1125,10 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -1211,8 +1223,17 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   if (g_gemm_variants && !job.enabled && !epi2.fin_cnt && !epi2.nres && !epi2.pf && !ts.streamk) {
     if (epi2.kind == EPI_DECODE_INPROJ) var = 1;
     else if (epi2.kind == EPI_ATOMIC_F32 && epi2.trans && BN <= 32) var = 2;
+    else if (!epi2.trans && g_gemm_prefill_var) {
+      // fixed-kind prefill variants: only the softplus one (dt_proj) measured faster (249 -> 230 us);
+      // the in_proj / out_proj ones measured 2-3% slower than the all-paths kernel, x_proj equal
+      var = epi2.kind == EPI_SOFTPLUS_BF16 ? 6 : 0;
+      if (g_gemm_prefill_var > 1)  // (experiment: every fixed-kind variant)
+        var = epi2.kind == EPI_STORE_BF16 ? 4 : epi2.kind == EPI_ADD_F32 ? 5 : epi2.kind == EPI_SOFTPLUS_BF16 ? 6
+            : epi2.kind == EPI_STORE_F32 ? 7 : 0;
+    }
   }
-  auto kfn = var == 2 ? gemm_tc_kernel<2> : gemm_tc_kernel<0>;
+  auto kfn = var == 2 ? gemm_tc_kernel<2> : var == 4 ? gemm_tc_kernel<4> : var == 5 ? gemm_tc_kernel<5>
+           : var == 6 ? gemm_tc_kernel<6> : var == 7 ? gemm_tc_kernel<7> : gemm_tc_kernel<0>;
   if (var == 1) kfn = epi2.P <= 64 * 3 ? gemm_tc_kernel<1, 3> : epi2.P <= 64 * 4 ? gemm_tc_kernel<1, 4> : gemm_tc_kernel<1>;
   { cudaError_t e_ = launch(kfn, grid, var_threads(var), smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi2,
                                       A_blocked, lda, K, cr, A_blocked ? 1 : 0, job);

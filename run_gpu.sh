@@ -170,3 +170,6 @@ for k in (2, 4, 8):
 PY
   (for v in 1 0; do SSM_FUSE_AR1=$v timeout 300 python /tmp/tpdec.py; done) > gpurun_out/tpdec_$TAG.txt 2>&1; cat gpurun_out/tpdec_$TAG.txt | tail -8 ;;
 esac
+case " $* " in *" pvar "*)
+  (for v in 1 0; do SSM_GEMM_PREFILL_VAR=$v timeout 300 python scripts/kernel_rooflines.py --layers 2 | grep -E "prefill" | sed "s/^/pvar=$v /"; done; for v in 1 0 1 0; do SSM_GEMM_PREFILL_VAR=$v timeout 600 python bench.py --no-cpu --no-e2e --decode 16 --steps 3 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('pvar=$v ttft', round(d['ttft_ms'],1))"; done) > gpurun_out/pvar_$TAG.txt 2>&1; cat gpurun_out/pvar_$TAG.txt ;;
+esac
