@@ -193,9 +193,29 @@ def run_reference(args, dims, wl, n_layers):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------- ranks
+def launch_ranks(args):
+    """`--gpus N` (N > 1) run WITHOUT torchrun: re-exec this script under torch.distributed.run with
+    N ranks on this node (one process per GPU).  Fails loudly when the node has fewer GPUs."""
+    import socket
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but this node has {n} CUDA device(s)\n")
+        sys.exit(2)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 # ---------------------------------------------------------------------------- main
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        launch_ranks(args)
     import synth
     dims = synth.CONFIGS["mamba2.8b" if args.config == "mamba2.8b-long" else args.config]
     wl = dict(synth.WORKLOADS[args.config])
@@ -213,6 +233,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (TP degree = number of ranks)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -270,9 +292,8 @@ def main():
         # (probe_graph, replayed right after the timed region): event nodes in the timed graph
         # itself would cost ~0.7 ms per step.  The probe slots stay full after this capture, so
         # the timed graph below gets no event nodes.
-        if stack.stack_ws is None:
-            probe_graph = stack.capture_decode(res_t, probes=[("in_proj_decode", n_layers)])
-        graph = stack.capture_decode(res_t, warmup=stack.stack_ws is not None)
+        probe_graph = stack.capture_decode(res_t, probes=[("in_proj_decode", n_layers)])
+        graph = stack.capture_decode(res_t, warmup=False)
 
     def step(timers=None):
         stack.reset()
@@ -286,7 +307,7 @@ def main():
             timers[1].record()
         for j in range(Ld):
             res_t.copy_(dec_in[j])
-            graph.replay()
+            stack.replay(graph)
             dec_out[j].copy_(res_t)
         if timers is not None:
             timers[2].record()
@@ -315,22 +336,10 @@ def main():
         barrier()
     pre_ms = mx.probe_read("in_proj")          # prefill in_proj launches of the timed steps
     dec_ms_launch = []
-    mk_ms = []
-    if Ld > 0 and stack.stack_ws is not None:
-        # persistent decode: the graph holds exactly one kernel (decode_mk_kernel); time launches
-        # with events on the launching stream, continuing from the timed state
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(16)]
-        for j, (e0, e1) in enumerate(evs):
-            res_t.copy_(dec_in[j % Ld])
-            e0.record()
-            graph.replay()
-            e1.record()
-        torch.cuda.synchronize()
-        mk_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
-    elif Ld > 0:
+    if Ld > 0:
         for j in range(min(Ld, 8)):  # probe graph: same decode step, continuing from the timed state
             res_t.copy_(dec_in[j])
-            probe_graph.replay()
+            stack.replay(probe_graph)
             dec_ms_launch += mx.probe_read("in_proj_decode")   # one per layer
     mx.probe("in_proj", 0)
     prefill_launches = mx.launches() - launches0
@@ -419,24 +428,6 @@ def main():
             "work_per_launch": (f"W_in 2E_k*D bf16 + x_in + z + u + conv window r/w + W_x + x_proj acc = {byts:.3e} B "
                                 "(in_proj with the conv step and x_proj fused into its epilogue)") if fused
                                else f"W_in 2E_k*D bf16 + x_in + xz = {byts:.3e} B",
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-    if mk_ms:
-        avg = statistics.median(mk_ms)
-        P = dims.dt_rank + 2 * dims.d_state
-        K, N = dims.d_conv, dims.d_state
-        per_layer = (2 * Ek * D + D * Ek + P * Ek + Ek * dims.dt_rank) * 2 \
-            + Ek * (K + 1 + 1 + N + 1) * 4 \
-            + 2 * B * Ek * N * 4 + 2 * B * (K - 1) * Ek * 2
-        byts = n_layers * per_layer + 2 * B * D * 4
-        peak = peaks.get("hbm_gbs", 6535.1)
-        ach = byts / (avg / 1000) / 1e9
-        roofs["decode_persistent"] = {
-            "kernel": "decode_mk_kernel (persistent whole-stack decode, one launch per token)", "bound": "hbm",
-            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "traffic": traffic.get("decode_persistent"), "launch_ms": avg, "launches": len(mk_ms),
-            "step_share_ms": avg * Ld,
-            "work_per_launch": (f"all {n_layers} layers: W_in+W_out+W_x+W_dt bf16, per-channel vectors fp32, "
-                                f"h read+write fp32, conv window read+write bf16, residual in/out = {byts:.4e} B"),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     roof = max(roofs.values(), key=lambda r: r["step_share_ms"]) if roofs else None
     roof_other = [r for r in roofs.values() if r is not roof]

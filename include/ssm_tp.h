@@ -84,9 +84,13 @@ enum {
                               sums; wire (k-1)/k (n + 2n) B per rank instead of (k-1) n; bound
                               k max_r amax_r / 254.  ssm_qallreduce: selects it (n % (16 k) == 0);
                               mixer calls: forces it for SSM_AR2_INT8                           */
-  SSM_QAR_ONESHOT = 0x80    /* mixer calls: force the one-shot int8 schedule.  Default for
+  SSM_QAR_ONESHOT = 0x80,   /* mixer calls: force the one-shot int8 schedule.  Default for
                               SSM_AR2_INT8: two-shot when tp_size >= 4 and the call has >= 64
                               tokens (prefill), one-shot otherwise (decode, k = 2)               */
+  SSM_DECODE_UNFUSED = 0x100 /* ssm_mixer_decode: run the plain kernel chain (in_proj GEMM, conv
+                              step, x_proj GEMM, decode step, out_proj) instead of the fused
+                              in_proj (+conv step +x_proj epilogue); same arithmetic, used to
+                              cross-check the fused kernel                                        */
 };
 
 enum { SSM_COMM_VIRTUAL = 0x1 }; /* ssm_comm_t.flags: all peer buffers live on THIS device
@@ -191,39 +195,6 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
                               const void* x_in, float* residual, int32_t batch,
                               uint32_t flags, void* workspace, size_t ws_bytes, void* stream);
 
-/* ---- Decode chain (TP = 1): the pre-norm RMSNorm folded into the neighbouring kernels --------
- * A stack step x = RMSNorm(residual) (weight 1, eps norm_eps; reading Q16); residual += mixer(x)
- * repeated over layers, without a separate norm kernel per layer: the per-row factor 1/rms
- * factors out of the in_proj contraction (PAPER.md:152-154 is linear in x), so
- *   ssm_decode_chain_begin: x_out = bf16(residual) (NOT normalised) and the per-row sums of
- *     squares into the workspace (once per token, before the first layer);
- *   ssm_mixer_decode_chained: one decode layer whose in_proj takes that un-normalised x_io and
- *     scales its accumulators by 1/rms; its out_proj (split-K atomics into `residual`) ends with
- *     the last contributor of every residual tile writing bf16(residual') into x_io and the new
- *     sums of squares -- the next layer's inputs.  Same arithmetic as ssm_rmsnorm +
- *     ssm_mixer_decode up to bf16 rounding order.  x_io [batch, D] bf16 in/out; the workspace
- *     (>= ssm_workspace_bytes(batch, 1)) carries the chain state between the calls of one token:
- *     pass the same one to every call.
- * ssm_decode_chain_supported: *ok = 1 when the configuration qualifies (TP=1, bf16, no AR#1,
- *   the fused decode in_proj: batch <= 32, P <= 256 even, 2 <= K <= 4, 128 | channels per head,
- *   d_model % 128 == 0; w may be NULL).  ssm_mixer_decode_chained returns SSM_ERR_UNSUPPORTED
- *   otherwise. */
-ssm_status_t ssm_decode_chain_supported(ssm_tp_t tp, const ssm_layer_weights_t* w, int32_t batch, int32_t* ok);
-ssm_status_t ssm_decode_chain_begin(ssm_tp_t tp, const float* residual, void* x_out, int32_t batch, void* workspace,
-                                    size_t ws_bytes, void* stream);
-ssm_status_t ssm_mixer_decode_chained(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, void* x_io,
-                                      float* residual, int32_t batch, float norm_eps, void* workspace,
-                                      size_t ws_bytes, void* stream);
-
-/* Decode step of one layer WITH its pre-norm (reading Q16: weightless RMSNorm, eps norm_eps):
- * x_scratch [batch, d_model] bf16 receives RMSNorm(residual) and is the in_proj input; then as
- * ssm_mixer_decode (residual += mixer(x)).  On the fused TP=1 decode path the norm runs inside the
- * in_proj kernel (its epilogue warps write the B operand before releasing its loads: one launch
- * fewer per layer); otherwise the standalone ssm_rmsnorm kernel runs first.  bf16 handles only. */
-ssm_status_t ssm_mixer_decode_prenorm(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, void* x_scratch,
-                                      float* residual, int32_t batch, float norm_eps, uint32_t flags,
-                                      void* workspace, size_t ws_bytes, void* stream);
-
 /* Quantised all-reduce of n fp32 values (n % qar_block == 0), rows of D = d_model:
  * every rank quantises its partial per block (s = amax/127, q = rint(o/s) clamped to
  * +-127), exchanges int8 codes + fp32 scales peer-to-peer, and forms
@@ -251,39 +222,6 @@ ssm_status_t ssm_packed_weight_bytes(int32_t rows, int32_t cols, size_t* bytes);
 ssm_status_t ssm_pack_weight(ssm_tp_t tp, const void* w, int32_t rows, int32_t cols, void* out, size_t out_bytes,
                              void* stream);
 
-/* ---- Persistent whole-stack decode (TP = 1) --------------------------------------------
- * One decode token (seqlen 1) for `batch` sequences through n_layers pre-norm blocks
- *   x = RMSNorm(residual) (weight 1, eps norm_eps; reading Q16);  residual += mixer_l(x)
- * in ONE kernel launch (PAPER.md:276-280 decode from the cache; 545 TPOT is bound by memory
- * bandwidth): the same arithmetic as n_layers x (ssm_rmsnorm + ssm_mixer_decode), with the
- * layers' packed W_in / W_out streamed continuously through shared memory by a persistent
- * grid of one CTA per SM (grid-wide barriers between the phases of a layer).
- * Supported: SSM_BF16, tp_size 1, n_heads 1, d_state 16, 2 <= d_conv <= 4, batch <= 32,
- * d_model % 128 == 0, d_inner % 64 == 0, dt_rank % 16 == 0, (dt_rank + 32) % 16 == 0;
- * otherwise SSM_ERR_UNSUPPORTED (callers use the per-layer calls).
- *
- * ssm_stack_bytes: workspace bytes for (n_layers, batch).
- * ssm_stack_bind: records the layers (w_in_pk and w_out_pk required: ssm_pack_weight) and
- *   their states (allocated for this handle and batch) in the caller's workspace (>= the bytes
- *   above, 256-B aligned, device memory that must outlive the binding), zero-fills it and
- *   synchronises `stream`.  One bound stack per handle; binding again replaces it.  Errors:
- *   SSM_ERR_UNSUPPORTED, SSM_ERR_ARG (NULL / small / misaligned), SSM_ERR_CACHE (state of
- *   another handle or batch).
- * ssm_stack_decode: enqueues the step on `stream`; residual [batch, D] fp32 in/out (16-B
- *   aligned).  Graph-capturable (cooperative launch).  The workspace holds state between calls
- *   (monotonic barrier counter, zeroed accumulators): never write it.
- * ssm_stack_check: synchronises `stream`; SSM_ERR_PROTOCOL if a launch timed out at a grid
- *   barrier or in the weight pipeline (the kernel then exits with garbage rather than hanging;
- *   re-bind before the next call).
- * ssm_stack_info: ring slots (1000 x 16-KB weight-tile slots + B-operand k-block slots per SM),
- *   grid size and channels per CTA of the bound stack (diagnostics). */
-ssm_status_t ssm_stack_bytes(ssm_tp_t tp, int32_t n_layers, int32_t batch, size_t* ws_bytes);
-ssm_status_t ssm_stack_bind(ssm_tp_t tp, const ssm_layer_weights_t* layers, const ssm_state_t* states,
-                            int32_t n_layers, int32_t batch, void* ws, size_t ws_bytes, void* stream);
-ssm_status_t ssm_stack_decode(ssm_tp_t tp, void* ws, float* residual, float norm_eps, void* stream);
-ssm_status_t ssm_stack_check(ssm_tp_t tp, void* ws, void* stream);
-ssm_status_t ssm_stack_info(ssm_tp_t tp, int32_t* ring_slots, int32_t* grid, int32_t* ch_per_cta);
-
 /* Synchronise the stream and report device-side protocol errors (SSM_ERR_PROTOCOL). */
 ssm_status_t ssm_tp_check(ssm_tp_t tp, void* stream);
 
@@ -292,10 +230,20 @@ ssm_status_t ssm_tp_check(ssm_tp_t tp, void* stream);
 ssm_status_t ssm_tp_stats(ssm_tp_t tp, int64_t* allreduce_count, int64_t* bytes_sent);
 
 /* Decode calls of this handle that ran the fused in_proj kernel (conv step and x_proj in the
- * GEMM epilogue; taken for bf16 when no AR#1 separates x_proj from the scan, batch <= 32,
- * P <= 256 and even, 2 <= K <= 4, 128 | channels per head; SSM_FUSE_DECODE=0 in the
- * environment at ssm_tp_init disables it).  The other decode calls run the unfused chain. */
+ * GEMM epilogue; taken for bf16 when batch <= 32, P <= 320 and even, 2 <= K <= 4, 128 |
+ * channels per head, and SSM_DECODE_UNFUSED is not set).  The other decode calls run the
+ * unfused chain. */
 ssm_status_t ssm_tp_fused_calls(ssm_tp_t tp, int64_t* calls);
+
+/* Collective epoch of the handle: the number of collectives (all-reduces and barriers) this rank
+ * has enqueued.  Collective e exchanges through half (e & 1) of the symmetric buffers, so two
+ * consecutive collectives always use different halves.  A CUDA graph captured with the epoch at
+ * parity p must be replayed with the epoch at parity p (its halves are fixed at capture);
+ * ssm_tp_barrier realigns it. */
+ssm_status_t ssm_tp_epoch(ssm_tp_t tp, uint32_t* epoch);
+/* Cross-rank barrier with no payload (a collective: every rank calls it in the same order);
+ * advances the epoch by one.  No-op (epoch unchanged) at tp_size == 1. */
+ssm_status_t ssm_tp_barrier(ssm_tp_t tp, void* stream);
 
 /* Kernel launches enqueued by this handle since creation (for bench.py gpu_launches). */
 ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches);
@@ -328,13 +276,6 @@ ssm_status_t ssm_dbg_gemm_ld(ssm_tp_t tp, const void* A, int64_t lda, const void
 ssm_status_t ssm_dbg_scan(ssm_tp_t tp, const void* u, const void* delta, const void* z, int32_t ldz,
                           const float* BC, const float* a_log, const float* d_skip, float* h,
                           void* g, int32_t batch, int32_t seqlen, void* stream);
-/* Experiment-only: device buffer (>= grid * n_layers * 32 u64, or NULL = off) that subsequent
- * ssm_stack_decode launches fill with globaltimer stamps per CTA, layer and phase boundary. */
-ssm_status_t ssm_dbg_stack_trace(ssm_tp_t tp, void* buf, size_t bytes);
-/* Copy `capacity` u64 of the GEMM kernel's experiment timeline (16 per CTA: globaltimer at
- * entry, clock64 at entry, then clock64 offsets of pipeline events; written only when
- * SSM_GEMM_NOMMA has bit 8 set when the GEMM is launched).  Synchronises the device. */
-ssm_status_t ssm_dbg_gemm_trace(uint64_t* out, int32_t capacity);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libssmtp.so")
 SSM_BF16, SSM_FP32 = 0, 1
 SSM_AR2_INT8, SSM_AR2_FP32, SSM_AR2_EXTERNAL, SSM_AR2_FP16 = 0x1, 0x2, 0x4, 0x8
 SSM_QAR_ACCUMULATE, SSM_QAR_FP16, SSM_QAR_TWOSHOT, SSM_QAR_ONESHOT = 0x10, 0x20, 0x40, 0x80
+SSM_DECODE_UNFUSED = 0x100
 SSM_COMM_VIRTUAL = 0x1
 
 STATUS = {0: "SSM_OK", 1: "SSM_ERR_ARG", 2: "SSM_ERR_DIM", 3: "SSM_ERR_SHARD", 4: "SSM_ERR_RANK",
@@ -68,6 +69,8 @@ def _load():
         "ssm_tp_check": (st, [vp, vp]),
         "ssm_tp_stats": (st, [vp, P(i64), P(i64)]),
         "ssm_tp_launch_count": (st, [vp, P(i64)]),
+        "ssm_tp_epoch": (st, [vp, P(C.c_uint32)]),
+        "ssm_tp_barrier": (st, [vp, vp]),
         "ssm_tp_fused_calls": (st, [vp, P(i64)]),
         "ssm_tp_probe": (st, [vp, i32, i32]),
         "ssm_tp_probe_read": (st, [vp, i32, P(C.c_float), i32, P(i32)]),
@@ -77,18 +80,6 @@ def _load():
         "ssm_dbg_gemm_packed": (st, [vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]),
         "ssm_dbg_gemm_ld": (st, [vp, vp, i64, vp, i64, vp, i32, i32, i32, i32, i32, vp]),
         "ssm_dbg_scan": (st, [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, i32, vp]),
-        "ssm_dbg_gemm_trace": (st, [vp, i32]),
-        "ssm_stack_bytes": (st, [vp, i32, i32, P(sz)]),
-        "ssm_stack_bind": (st, [vp, vp, vp, i32, i32, vp, sz, vp]),
-        "ssm_stack_decode": (st, [vp, vp, vp, C.c_float, vp]),
-        "ssm_stack_check": (st, [vp, vp, vp]),
-        "ssm_stack_info": (st, [vp, P(i32), P(i32), P(i32)]),
-        "ssm_dbg_stack_trace": (st, [vp, vp, sz]),
-        "ssm_decode_chain_supported": (st, [vp, vp, i32, P(i32)]),
-        "ssm_decode_chain_begin": (st, [vp, vp, vp, i32, vp, sz, vp]),
-        "ssm_mixer_decode_chained": (st, [vp, P(ssm_layer_weights_t), vp, vp, vp, i32, C.c_float, vp, sz, vp]),
-        "ssm_mixer_decode_prenorm": (st, [vp, P(ssm_layer_weights_t), vp, vp, vp, i32, C.c_float, C.c_uint32, vp, sz,
-                                          vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -100,11 +91,10 @@ def _load():
 LIB = _load()
 EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "ssm_comm_bytes", "ssm_workspace_bytes",
             "ssm_state_bytes", "ssm_state_alloc", "ssm_state_reset", "ssm_state_free", "ssm_mixer_prefill",
-            "ssm_mixer_decode", "ssm_qallreduce", "ssm_rmsnorm", "ssm_tp_check", "ssm_tp_stats",
-            "ssm_tp_launch_count", "ssm_tp_fused_calls", "ssm_tp_probe", "ssm_tp_probe_read", "ssm_packed_weight_bytes", "ssm_pack_weight",
-            "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld", "ssm_dbg_scan", "ssm_dbg_gemm_trace",
-            "ssm_stack_bytes", "ssm_stack_bind", "ssm_stack_decode", "ssm_stack_check", "ssm_stack_info", "ssm_dbg_stack_trace",
-            "ssm_decode_chain_supported", "ssm_decode_chain_begin", "ssm_mixer_decode_chained", "ssm_mixer_decode_prenorm"]
+            "ssm_mixer_decode", "ssm_qallreduce", "ssm_rmsnorm", "ssm_tp_check", "ssm_tp_stats", "ssm_tp_epoch",
+            "ssm_tp_barrier", "ssm_tp_launch_count", "ssm_tp_fused_calls", "ssm_tp_probe", "ssm_tp_probe_read",
+            "ssm_packed_weight_bytes", "ssm_pack_weight", "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld",
+            "ssm_dbg_scan"]
 PROBE = {"in_proj": 1, "conv": 2, "x_proj": 3, "dt_proj": 4, "scan": 5, "out_proj": 6, "ar2": 7, "decode_step": 8,
          "in_proj_decode": 9}
 

@@ -43,35 +43,11 @@ ssm_status_t fail(ssm_status_t code, const char* fmt, ...) {
 
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// Programmatic dependent launch for the decode path (SSM_PDL=0 disables).
-// Debug-only ablation knob (timing experiments): SSM_DEBUG_SKIP bitmask of decode kernels to
-// skip (1 in_proj, 2 conv, 4 x_proj, 8 decode_step, 16 out_proj).  Results are wrong when set.
-const int g_mk_dbg = [] { const char* e = getenv("SSM_MK_DBG"); return e ? atoi(e) : 0; }();
-const int g_dbg_skip = [] { const char* e = getenv("SSM_DEBUG_SKIP"); return e ? atoi(e) : 0; }();
-
-// On by default for decode-sized launches: every kernel calls griddepcontrol.launch_dependents at
-// entry and griddepcontrol.wait before touching memory a predecessor writes, so a successor's
-// launch and prologue overlap the predecessor's tail (measured 45.3 -> 42.2 us per Mamba-2.8B
-// decode layer with the fused in_proj).  SSM_PDL=0 disables.
-// Decode GEMMs with fewer tiles than SMs use the spare SMs to L2-prefetch the next weight stream
-// (SSM_L2_PREFETCH=1 enables; off by default: the decode GEMMs are not HBM-bound, r01 profiles).
-// SSM_DSTEP_PF=1: the decode-step kernel bulk-prefetches this layer's W_out into L2 (HBM idle there)
-// SSM_OUT_LOCAL=1: the decode step runs inside a channel-owned out_proj (DStepJob::local) instead
-// of its own kernel before the split-K out_proj.  Measured slower (48-73 vs 38.6 us per
-// Mamba-2.8B decode layer over Q in {1,2,4,8}: 256 threads per SM run the latency-bound step)
-const bool g_out_local = [] { const char* e = getenv("SSM_OUT_LOCAL"); return e && atoi(e) != 0; }();
-// channel-owned out_proj shape: SSM_OUT_Q m-groups per k-split of SSM_OUT_KBS 64-channel k-blocks
-const int g_out_q = [] { const char* e = getenv("SSM_OUT_Q"); return e ? atoi(e) : 4; }();
-const int g_out_kbs = [] { const char* e = getenv("SSM_OUT_KBS"); return e ? atoi(e) : 4; }();
-// SSM_FUSE_AR1=0: no fused decode in_proj when AR#1 follows (TP > 1 with one x_proj group)
-const bool g_fuse_ar1 = [] { const char* e = getenv("SSM_FUSE_AR1"); return !e || atoi(e) != 0; }();
-// SSM_INPROJ_SK=1: the fused decode in_proj runs stream-K over all SMs instead of one CTA per
-// 128-row tile (measured slower: 58 vs 40 us per Mamba-2.8B decode layer; the weight stream of
-// the one-tile-per-CTA kernel already runs at ~6.1 TB/s, profiles/r01_gemm_timeline_34.txt)
-const bool g_inproj_sk = [] { const char* e = getenv("SSM_INPROJ_SK"); return e && atoi(e) != 0; }();
-const bool g_dstep_pf = [] { const char* e = getenv("SSM_DSTEP_PF"); return e && atoi(e) != 0; }();
-const bool g_l2_prefetch = [] { const char* e = getenv("SSM_L2_PREFETCH"); return e && atoi(e) != 0; }();  // measured: no gain (profiles)
-const bool g_pdl_enabled = [] { const char* e = getenv("SSM_PDL"); return !e || atoi(e) != 0; }();
+// Programmatic dependent launch on the decode path: every kernel calls
+// griddepcontrol.launch_dependents at entry and griddepcontrol.wait before touching memory a
+// predecessor writes, so a successor's launch and prologue overlap the predecessor's tail
+// (measured 45.3 -> 42.2 us per Mamba-2.8B decode layer with the fused in_proj).  Off across
+// virtual ranks (see ssm_mixer_decode).
 struct PdlScope {
   bool prev;
   explicit PdlScope(bool on) : prev(ssm::t_launch_pdl) { ssm::t_launch_pdl = on; }
@@ -93,17 +69,7 @@ struct ssm_tp_s {
   uint32_t epoch;
   int64_t ar_count, bytes_sent, launches;
   int num_sms;
-  int fuse_decode;        // fused decode in_proj (conv + x_proj in its epilogue); SSM_FUSE_DECODE=0 disables
-  int64_t fused_calls;    // decode calls that took the fused path
-  int fuse_dstep;         // decode step run inside the out_proj GEMM; SSM_FUSE_DSTEP=0 disables
-  // persistent whole-stack decode (ssm_stack_bind / ssm_stack_decode): the bound workspace
-  struct Stack {
-    void* ws = nullptr;
-    int n_layers = 0, batch = 0, bp = 0, ncmax = 0, ngrp = 0, ring = 0, nbr = 0, grid = 0;
-    size_t off_tab = 0, off_residT = 0, off_residB = 0, off_xzT = 0, off_dbcT = 0, off_ss = 0, off_ssP = 0,
-           off_gT = 0, off_cnt = 0, off_ep = 0, total = 0;
-    unsigned long long* trace = nullptr;  // experiment-only timeline buffer (ssm_dbg_stack_trace)
-  } stack;
+  int64_t fused_calls;    // decode calls that took the fused in_proj (+conv step +x_proj) path
   // timing probes: one slot per kernel kind
   struct ProbeSlot {
     int cap = 0, n = 0;
@@ -122,30 +88,17 @@ namespace {
 
 // The h buffer of a state is h [batch][E_k][N] fp32 followed by the fused decode path's x_proj
 // accumulator [batch][hloc*P] fp32, which is all-zero between decode calls: the decode in_proj
-// adds into it, decode_step reads it, out_proj's CTA 0 zeroes it again.
+// adds into it, decode_step reads it, out_proj's CTA 0 zeroes it again (at TP > 1 the AR#1
+// publish kernel copies it out and re-zeroes it).
 size_t xacc_offset(const ssm_tp_s* t, int batch) {
   return al256((size_t)batch * t->Ek * t->cfg.d_state * 4);
 }
-// ... then the grid-barrier counter of the fused decode-step + out_proj kernel (u64, monotonic).
-size_t sync_offset(const ssm_tp_s* t, int batch) {
-  return xacc_offset(t, batch) + al256((size_t)batch * t->hloc * t->P * 4);
-}
-// ... then the stream-K accumulator of the fused decode in_proj [2E_k/128][batch][128] fp32 and its
-// per-tile counters (all-zero between calls; the last contributor of a tile re-zeroes its part).
-size_t sk_offset(const ssm_tp_s* t, int batch) { return sync_offset(t, batch) + 256; }
-size_t sk_cnt_offset(const ssm_tp_s* t, int batch) {
-  return sk_offset(t, batch) + al256((size_t)2 * t->Ek * batch * 4);
-}
-// ... then the channel-owned out_proj's group-barrier counters (u64 per k-split, monotonic)
-size_t grp_offset(const ssm_tp_s* t, int batch) {
-  return sk_cnt_offset(t, batch) + al256((size_t)(2 * t->Ek / 128 + 1) * 4);
-}
 size_t h_total_bytes(const ssm_tp_s* t, int batch) {
-  return grp_offset(t, batch) + al256((size_t)(t->Ek / 64 + 1) * 8);
+  return xacc_offset(t, batch) + al256((size_t)batch * t->hloc * t->P * 4);
 }
 
 struct WsLayout {
-  size_t xz, u, dbc, dlow, bc, delta, g, part, css, ccnt, total;
+  size_t xz, u, dbc, dlow, bc, delta, g, part, total;
 };
 
 WsLayout ws_layout(const ssm_tp_s* t, int64_t M) {
@@ -161,8 +114,6 @@ WsLayout ws_layout(const ssm_tp_s* t, int64_t M) {
   L.delta = take(M * t->Ek * es);
   L.g = take(M * t->Ek * es);
   L.part = take(t->k > 1 ? M * t->cfg.d_model * 4 : 0);
-  L.css = take(M * 4);                                     // decode chain: per-row sums of squares
-  L.ccnt = take(M > 0 ? ((size_t)t->cfg.d_model / 128 + 1) * 4 : 0);  // decode chain: out_proj tile counters
   L.total = off;
   return L;
 }
@@ -212,13 +163,12 @@ ssm_status_t validate_cfg(const ssm_config_t* c, int k) {
 
 cudaError_t gemm(ssm_tp_s* t, const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
                  int ksplit, const Epilogue& e, cudaStream_t s, bool a_is_weight = false,
-                 const void* a_blocked = nullptr, const DStepJob* job = nullptr) {
+                 const void* a_blocked = nullptr) {
   t->launches++;
   if (t->bf16 && gemm_tc_supported(A, lda, B, ldb))
     return gemm_tc_bf16(reinterpret_cast<const __nv_bfloat16*>(A), lda, reinterpret_cast<const __nv_bfloat16*>(B),
                         ldb, M, N, K, ksplit, e, t->num_sms, s, a_is_weight && t_launch_pdl,
-                        reinterpret_cast<const __nv_bfloat16*>(a_blocked), job);
-  if (job) return cudaErrorInvalidValue;
+                        reinterpret_cast<const __nv_bfloat16*>(a_blocked));
   return gemm_simt(A, lda, B, ldb, t->bf16, M, N, K, ksplit, e, s);
 }
 
@@ -278,8 +228,7 @@ Peers group_peers(const ssm_tp_s* t, int gsize) {
 
 // One mixer layer. decode: seqlen == 1 path with in-place state update.
 ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* st, const void* x_in, float* residual,
-                       int batch, int seqlen, uint32_t flags, void* ws, bool decode, cudaStream_t s,
-                       bool chain = false, float norm_eps = 0.f, bool prenorm = false) {
+                       int batch, int seqlen, uint32_t flags, void* ws, bool decode, cudaStream_t s) {
   const ssm_config_t& c = t->cfg;
   const int64_t M = (int64_t)batch * seqlen;
   const int D = c.d_model, Ek = t->Ek, R = c.dt_rank, N = c.d_state, K = c.d_conv, P = t->P, hl = t->hloc;
@@ -306,6 +255,10 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
 
   const int64_t nD = M * D;
   // Collective epochs and destinations, fixed up front in execution order (AR#1 then AR#2).
+  // Double buffering: collective e uses half e & 1.  A rank may write its half for collective e
+  // only after its barrier of collective e - 1 has passed (every peer has then finished reading
+  // the same half for collective e - 2), so no symmetric half is written before this layer's
+  // first barrier except by the collective that barrier belongs to.
   const bool ar1 = t->ar1_group > 1;
   uint32_t ep1 = 0, ep2 = 0;
   float* xdst = dbc;
@@ -330,7 +283,10 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   } else if (flags & SSM_AR2_FP32) {
     omode = OUT_FP32;
     ep2 = ++t->epoch;
-    odst = reinterpret_cast<float*>(own_half(ep2));
+    // decode: the split-K out_proj accumulates into the zeroed local partial (zeroed before this
+    // layer's AR#1 barrier: it cannot be the symmetric half), copied over by the publish kernel;
+    // prefill: stored straight into the half (the out_proj runs after the AR#1 barrier)
+    odst = swap ? part : reinterpret_cast<float*>(own_half(ep2));
   } else {
     omode = OUT_INT8;
     ep2 = ++t->epoch;
@@ -340,28 +296,16 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   // decode GEMMs (swap-AB): split-K with the fp32 atomic epilogue so the few weight-row tiles
   // spread over the SMs (measured best: ~1 unit per SM, <= 32 splits)
   const int ks_x = swap ? split_for(t, hl * P, Ek) : 1;
-  static const int ks_o_env = [] { const char* e = getenv("SSM_OUT_KS"); return e ? atoi(e) : 0; }();
-  const int ks_o = swap ? (ks_o_env > 0 ? ks_o_env : split_for(t, D, Ek)) : 1;
+  const int ks_o = swap ? split_for(t, D, Ek) : 1;
 
   // (a1) in_proj, column-parallel: xz = x_in W_in,r^T   [M, 2E_k]
-  const int skip = decode ? g_dbg_skip : 0;
-  // Fused decode (no AR#1 between x_proj and the scan): the in_proj epilogue also runs the conv
-  // step (a2) and adds its x_proj partial (a3) into the state's zeroed accumulator.
+  // Fused decode: the in_proj epilogue also runs the conv step (a2) and adds its x_proj partial
+  // (a3) into the state's zeroed accumulator (at TP > 1 published to the symmetric buffer by
+  // publish_barrier_kernel, which is also AR#1's barrier).
   float* xacc = reinterpret_cast<float*>(reinterpret_cast<char*>(st->h) + xacc_offset(t, batch));
-  // (with AR#1 the partial is published to the symmetric buffer by publish_barrier_kernel)
-  const bool fuse = swap && (!ar1 || g_fuse_ar1) && t->fuse_decode && batch <= 32 && P <= 320 && P % 2 == 0 &&
-                    K >= 2 && K <= 4 &&
-                    t->cph % 128 == 0 && !(skip & 7) &&
-                    gemm_tc_supported(w->w_in, D, x_in, D);
-  float* css = reinterpret_cast<float*>(W + L.css);
-  int* ccnt = reinterpret_cast<int*>(W + L.ccnt);
-  if (chain && (!fuse || skip || t->k != 1)) return fail(SSM_ERR_UNSUPPORTED, "decode chain needs the fused TP=1 decode path");
-  if (prenorm && !fuse) {  // no fused in_proj: the standalone pre-norm kernel, then the layer
-    t->launches++;
-    CU(launch_rmsnorm(1, residual, nullptr, norm_eps, const_cast<void*>(x_in), M, D, s));
-    prenorm = false;
-  }
-  if (!(skip & 1)) {
+  const bool fuse = swap && !(flags & SSM_DECODE_UNFUSED) && batch <= 32 && P <= 320 && P % 2 == 0 && K >= 2 &&
+                    K <= 4 && t->cph % 128 == 0 && gemm_tc_supported(w->w_in, D, x_in, D);
+  {
     Probe pr(t, decode ? SSM_PROBE_IN_PROJ_DECODE : SSM_PROBE_IN_PROJ, s);
     if (fuse) {
       t->fused_calls++;
@@ -377,28 +321,8 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       e.P = P;
       e.hl = hl;
       e.cph = t->cph;
-      if (!oacc) { e.zero = odst; e.nzero = nD; }  // out_proj partial target (AR#2 follows)
-      if (prenorm) {  // x_in = RMSNorm(residual) written by the in_proj kernel itself
-        e.nres = residual;
-        e.nres_eps = norm_eps;
-        e.nx = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(x_in));
-      }
-      if (chain) {  // x_in = bf16(residual) un-normalised; the pre-norm's 1/rms applied here
-        e.ss = css;
-        e.ss_scale = 1.0f / (float)D;
-        e.ss_eps = norm_eps;
-      }
-      int ks_in = 1;
-      if (g_inproj_sk && (2 * Ek) % 128 == 0) {  // stream-K over all SMs (80 row tiles < 148 SMs)
-        e.sk_acc = reinterpret_cast<float*>(reinterpret_cast<char*>(st->h) + sk_offset(t, batch));
-        e.sk_cnt = reinterpret_cast<int*>(reinterpret_cast<char*>(st->h) + sk_cnt_offset(t, batch));
-        ks_in = -1;
-      }
-      if (g_l2_prefetch) {  // spare SMs: this layer's W_out into L2 for the out_proj two kernels on
-        e.pf = w->w_out_pk ? w->w_out_pk : w->w_out;
-        e.pf_bytes = (int64_t)D * Ek * 2;
-      }
-      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, ks_in, e, s, true, w->w_in_pk));
+      if (!oacc) { e.zero = odst; e.nzero = nD; }  // out_proj partial target (local workspace)
+      CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, e, s, true, w->w_in_pk));
     } else if (swap)
       CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s, true, w->w_in_pk));
     else
@@ -406,7 +330,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   }
 
   // (a2) conv1d + SiLU, rank-local; conv window of the cache updated
-  if (decode && !(skip & 2) && !fuse) {
+  if (decode && !fuse) {
     // split-K targets of x_proj / out_proj are zeroed by the conv kernel (one launch fewer)
     float* z0 = nullptr;
     int64_t n0 = 0;
@@ -428,7 +352,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   }
 
   // (a3) x_proj partial [M, hloc*P] fp32, straight into the symmetric buffer when AR#1 follows
-  if (!(skip & 4) && !fuse) {
+  if (!fuse) {
     Probe pr(t, SSM_PROBE_X_PROJ, s);
     if (swap)
       CU(gemm(t, w->w_x, Ek, u, Ek, hl * P, (int)M, Ek, ks_x,
@@ -454,56 +378,13 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     dsrc.p[0] = fuse ? xacc : dbc;
   }
 
-  // Decode step fused into the out_proj GEMM (its epilogue warps produce g, grid barrier, then the
-  // B loads): needs one dbc source, real (not virtual) ranks so all CTAs can be co-resident.
-  DStepJob job{};
-  // Channel-owned out_proj (opt-in, SSM_OUT_LOCAL=1): Q CTAs per k-split run the decode step of
-  // the split's channels, meet at a group barrier, then their out_proj partials (no grid barrier,
-  // no separate decode-step kernel).
-  const bool local_ds = swap && g_out_local && fuse && nsrc == 1 && dstep_supported(1, R, N, hl * P, t->cph) &&
-                        g_out_q >= 1 && g_out_kbs >= 1 && (g_out_kbs * 64) % (32 * g_out_q) == 0 &&
-                        !(skip & 24) && !chain && gemm_tc_supported(w->w_out, Ek, g, Ek);
-  const bool fuse_ds = local_ds || (swap && t->fuse_dstep && nsrc == 1 && !(t->flags & SSM_COMM_VIRTUAL) &&
-                       dstep_supported(1, R, N, hl * P, t->cph) && !(skip & 24) && gemm_tc_supported(w->w_out, Ek, g, Ek));
-  if (fuse_ds) {
-    job.enabled = 1;
-    job.bf16 = 1;
-    job.N = N;
-    job.dbc = reinterpret_cast<const float*>(dsrc.p[0]);
-    job.sync = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(st->h) + sync_offset(t, batch));
-    job.ldp = hl * P;
-    job.rmsnorm = c.bcdt_rmsnorm;
-    job.eps = c.rms_eps;
-    job.u = u;
-    job.z = reinterpret_cast<char*>(xz) + Ek * es;
-    job.ldz = 2 * Ek;
-    job.w_dt = w->w_dt;
-    job.b_dt = w->b_dt;
-    job.a_log = w->a_log;
-    job.d_skip = w->d_skip;
-    job.h = st->h;
-    job.g = g;
-    job.batch = batch;
-    job.Ek = Ek;
-    job.R = R;
-    job.cph = t->cph;
-    if (local_ds) {
-      job.local = g_out_q;
-      job.rd_cnt = reinterpret_cast<int*>(reinterpret_cast<char*>(st->h) + sync_offset(t, batch) + 64);
-      job.ndbc = (int64_t)batch * hl * P;
-      job.grp_cnt = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(st->h) + grp_offset(t, batch));
-    }
-  }
   if (decode) {
-    if (!(skip & 8) && !fuse_ds) {
     // (a4)-(a7) decode: AR#1 sum + unpack + dt_proj + softplus + scan step + gate, one kernel
     Probe pr(t, SSM_PROBE_DECODE_STEP, s);
     t->launches++;
     CU(launch_decode_step(bf, dsrc, nsrc, doff, hl * P, c.bcdt_rmsnorm, c.rms_eps, u,
                           reinterpret_cast<char*>(xz) + Ek * es, 2 * Ek, w->w_dt, w->b_dt, w->a_log, w->d_skip, st->h,
-                          g, batch, Ek, R, N, t->cph, nullptr, s, chain ? css : nullptr,
-                          g_dstep_pf && swap ? (w->w_out_pk ? w->w_out_pk : w->w_out) : nullptr, (int64_t)D * Ek * (int64_t)es));
-    }
+                          g, batch, Ek, R, N, t->cph, nullptr, s));
   } else {
     // (a4) unpack dt_low / B / C; (a5) dt_proj + softplus; (a6)+(a7) scan, D skip, gate
     t->launches++;
@@ -529,23 +410,16 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   }
 
   // (a8) out_proj, row-parallel partial (TP=1: added straight into the fp32 residual)
-  if (!(skip & 16)) {
+  {
     Probe pr(t, SSM_PROBE_OUT_PROJ, s);
     if (swap) {
       Epilogue e = epi(EPI_ATOMIC_F32, 1, odst, D);
-      // re-arm the x_proj accumulator (channel-owned mode: its last reader does)
-      if (fuse && !local_ds && !ar1) { e.zero = xacc; e.nzero = (int64_t)batch * hl * P; }  // (ar1: the publish kernel re-zeroes it)
-      if (chain) {  // last contributor of each residual tile: next layer's bf16 B operand + sums of squares
-        e.fin_cnt = ccnt;
-        e.fin_x = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(x_in));
-        e.fin_ldx = D;
-        e.fin_ss = css;
-      }
-      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, local_ds ? ((Ek + 63) / 64 + g_out_kbs - 1) / g_out_kbs : ks_o, e, s, true, w->w_out_pk,
-              fuse_ds ? &job : nullptr));
-    }
-    else
+      // re-arm the x_proj accumulator (at TP > 1 the publish kernel re-zeroes it)
+      if (fuse && !ar1) { e.zero = xacc; e.nzero = (int64_t)batch * hl * P; }
+      CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, e, s, true, w->w_out_pk));
+    } else {
       CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D), s));
+    }
   }
   // (a9) AR#2 at the residual boundary
   if (omode == OUT_FP32) {
@@ -553,7 +427,10 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->ar_count++;
     t->bytes_sent += nD * 4;
     t->launches += 2;
-    CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
+    if (swap)  // local partial -> own half (re-zeroing the partial), then the barrier
+      CU(launch_publish_barrier(t->peers, t->rank, t->k, part, nD, half_off(ep2), s));
+    else
+      CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
     CU(launch_f32_reduce(t->peers, t->k, half_off(ep2), nD, residual, 1, s));
   } else if (omode == OUT_FP16) {  // the paper's FP32 -> FP16 wire
     Probe pr(t, SSM_PROBE_AR2, s);
@@ -602,7 +479,7 @@ ssm_status_t check_call(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* 
   if ((reinterpret_cast<uintptr_t>(x_in) | reinterpret_cast<uintptr_t>(residual)) & 15)
     return fail(SSM_ERR_ARG, "x_in/residual must be 16-B aligned");
   if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL | SSM_QAR_TWOSHOT |
-                          SSM_QAR_ONESHOT))
+                          SSM_QAR_ONESHOT | SSM_DECODE_UNFUSED))
     return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
   if ((flags & SSM_QAR_TWOSHOT) && (flags & SSM_QAR_ONESHOT))
     return fail(SSM_ERR_ARG, "SSM_QAR_TWOSHOT and SSM_QAR_ONESHOT are exclusive");
@@ -662,14 +539,6 @@ ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp
   t->bf16 = cfg->dtype == SSM_BF16;
   t->es = t->bf16 ? 2 : 4;
   t->epoch = 0;
-  {
-    const char* e = getenv("SSM_FUSE_DECODE");
-    t->fuse_decode = e ? atoi(e) != 0 : 1;
-    // off by default: measured 45.9 vs 39.4 us per Mamba-2.8B decode layer (the job has 8 warps per
-    // SM where the standalone kernel has 20, and the decode step is latency-bound); SSM_FUSE_DSTEP=1
-    const char* e2 = getenv("SSM_FUSE_DSTEP");
-    t->fuse_dstep = e2 ? atoi(e2) != 0 : 0;
-  }
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) {
     t->num_sms = sms;
@@ -679,7 +548,6 @@ ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp
       pre = preload_kernels();
       if (pre == cudaSuccess) pre = preload_gemm_simt();
       if (pre == cudaSuccess) pre = preload_gemm_tc();
-      if (pre == cudaSuccess) pre = preload_decode_mk();
     });
     if (pre != cudaSuccess) {
       delete t;
@@ -817,58 +685,9 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
   if (batch == 0) return SSM_OK;
   // no PDL across virtual ranks: early-launched dependents of one rank's stream would hold the SMs
   // the other ranks' kernels need to reach the shared barrier
-  PdlScope pdl(g_pdl_enabled && !(tp->flags & SSM_COMM_VIRTUAL));
+  PdlScope pdl(!(tp->flags & SSM_COMM_VIRTUAL));
   return run_layer(tp, w, st, x_in, residual, batch, 1, flags, workspace, true,
                    reinterpret_cast<cudaStream_t>(stream));
-}
-
-ssm_status_t ssm_mixer_decode_prenorm(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, void* x_scratch,
-                                      float* residual, int32_t batch, float norm_eps, uint32_t flags, void* workspace,
-                                      size_t ws_bytes, void* stream) {
-  ssm_status_t s = check_call(tp, w, st, x_scratch, residual, batch, 1, flags, workspace, ws_bytes);
-  if (s != SSM_OK) return s;
-  if (!tp->bf16) return fail(SSM_ERR_UNSUPPORTED, "ssm_mixer_decode_prenorm: bf16 handles only");
-  if (batch == 0) return SSM_OK;
-  PdlScope pdl(g_pdl_enabled && !(tp->flags & SSM_COMM_VIRTUAL));
-  return run_layer(tp, w, st, x_scratch, residual, batch, 1, flags, workspace, true,
-                   reinterpret_cast<cudaStream_t>(stream), false, norm_eps, true);
-}
-
-ssm_status_t ssm_decode_chain_supported(ssm_tp_t tp, const ssm_layer_weights_t* w, int32_t batch, int32_t* ok) {
-  if (!tp || !ok) return fail(SSM_ERR_ARG, "NULL argument");
-  const ssm_config_t& c = tp->cfg;
-  *ok = tp->k == 1 && tp->bf16 && tp->ar1_group == 1 && tp->fuse_decode && batch >= 1 && batch <= 32 &&
-        (c.dt_rank + 2 * c.d_state) <= 320 && (c.dt_rank + 2 * c.d_state) % 2 == 0 && c.d_conv >= 2 && c.d_conv <= 4 &&
-        tp->cph % 128 == 0 && c.d_model % 128 == 0 && !g_dbg_skip && (!w || gemm_tc_supported(w->w_in, c.d_model, w->w_in, c.d_model));
-  return SSM_OK;
-}
-
-ssm_status_t ssm_decode_chain_begin(ssm_tp_t tp, const float* residual, void* x_out, int32_t batch, void* workspace,
-                                    size_t ws_bytes, void* stream) {
-  if (!tp || !residual || !x_out || !workspace) return fail(SSM_ERR_ARG, "NULL argument");
-  if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
-  const WsLayout L = ws_layout(tp, batch);
-  if (ws_bytes < L.total) return fail(SSM_ERR_ARG, "workspace too small");
-  char* W = reinterpret_cast<char*>(workspace);
-  tp->launches++;
-  PdlScope pdl(g_pdl_enabled);
-  CU(launch_chain_begin(residual, reinterpret_cast<__nv_bfloat16*>(x_out), reinterpret_cast<float*>(W + L.css),
-                        reinterpret_cast<int*>(W + L.ccnt), tp->cfg.d_model / 128 + 1, batch, tp->cfg.d_model,
-                        reinterpret_cast<cudaStream_t>(stream)));
-  return SSM_OK;
-}
-
-ssm_status_t ssm_mixer_decode_chained(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, void* x_io,
-                                      float* residual, int32_t batch, float norm_eps, void* workspace,
-                                      size_t ws_bytes, void* stream) {
-  ssm_status_t s = check_call(tp, w, st, x_io, residual, batch, 1, 0, workspace, ws_bytes);
-  if (s != SSM_OK) return s;
-  int32_t ok = 0;
-  ssm_decode_chain_supported(tp, w, batch, &ok);
-  if (!ok) return fail(SSM_ERR_UNSUPPORTED, "decode chain: needs TP=1, bf16, the fused decode in_proj shape limits");
-  PdlScope pdl(g_pdl_enabled);
-  return run_layer(tp, w, st, x_io, residual, batch, 1, 0, workspace, true, reinterpret_cast<cudaStream_t>(stream),
-                   true, norm_eps);
 }
 
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
@@ -936,7 +755,7 @@ ssm_status_t ssm_rmsnorm(ssm_tp_t tp, const float* residual, const float* weight
                          void* stream) {
   if (!tp || !residual || !x_out) return fail(SSM_ERR_ARG, "NULL argument");
   // decode-sized rows: overlap with the neighbours (not across virtual ranks, see ssm_mixer_decode)
-  PdlScope pdl(g_pdl_enabled && M <= 256 && !(tp->flags & SSM_COMM_VIRTUAL));
+  PdlScope pdl(M <= 256 && !(tp->flags & SSM_COMM_VIRTUAL));
   if ((reinterpret_cast<uintptr_t>(residual) | reinterpret_cast<uintptr_t>(weight) | reinterpret_cast<uintptr_t>(x_out)) & 15)
     return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
   tp->launches++;
@@ -965,6 +784,22 @@ ssm_status_t ssm_tp_stats(ssm_tp_t tp, int64_t* allreduce_count, int64_t* bytes_
 ssm_status_t ssm_tp_fused_calls(ssm_tp_t tp, int64_t* calls) {
   if (!tp || !calls) return fail(SSM_ERR_ARG, "NULL argument");
   *calls = tp->fused_calls;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_epoch(ssm_tp_t tp, uint32_t* epoch) {
+  if (!tp || !epoch) return fail(SSM_ERR_ARG, "NULL argument");
+  *epoch = tp->epoch;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_tp_barrier(ssm_tp_t tp, void* stream) {
+  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
+  if (tp->k == 1) return SSM_OK;
+  ++tp->epoch;
+  tp->launches++;
+  PdlScope pdl(!(tp->flags & SSM_COMM_VIRTUAL));
+  CU(launch_peer_barrier(tp->peers, tp->rank, tp->k, reinterpret_cast<cudaStream_t>(stream)));
   return SSM_OK;
 }
 
@@ -1034,179 +869,5 @@ ssm_status_t ssm_dbg_scan(ssm_tp_t tp, const void* u, const void* delta, const v
   return SSM_OK;
 }
 
-ssm_status_t ssm_dbg_gemm_trace(uint64_t* out, int32_t capacity) {
-  if (!out || capacity < 0) return fail(SSM_ERR_ARG, "NULL argument");
-  CU(cudaDeviceSynchronize());
-  CU(gemm_trace_read(reinterpret_cast<unsigned long long*>(out), capacity));
-  return SSM_OK;
-}
-
 }  // extern "C"
 
-// ------------------------------------------------------------------ persistent whole-stack decode
-namespace {
-// Workspace layout of a bound stack (256-B aligned pieces): header (barrier counter @0, error
-// word @64), layer table, residT [D][BP], xzT [2Ek][BP], dbcT [P][BP], ssP [grid][BP], gT [Ek][BP].
-ssm_status_t stack_plan(ssm_tp_s* t, int n_layers, int batch, ssm_tp_s::Stack* S, bool why) {
-  const ssm_config_t& c = t->cfg;
-  const int P = t->P, R = c.dt_rank, D = c.d_model, Ek = t->Ek;
-  auto no = [&](const char* m) { return why ? fail(SSM_ERR_UNSUPPORTED, "stack decode: %s", m) : SSM_ERR_UNSUPPORTED; };
-  if (!t->bf16) return no("bf16 only");
-  if (t->k != 1) return no("TP=1 only (the TP>1 decode runs per layer with the peer all-reduces)");
-  if (c.n_heads != 1) return no("one x_proj head only");
-  if (c.d_state != 16) return no("d_state 16 only");
-  if (c.d_conv < 2 || c.d_conv > 4) return no("2 <= d_conv <= 4");
-  if (batch < 1 || batch > 32) return no("1 <= batch <= 32");
-  if (n_layers < 1) return no("n_layers >= 1");
-  if (D % 128 || Ek % 64 || R % 16 || P % 16) return no("needs d_model % 128, d_inner % 64, dt_rank % 16, P % 16 == 0");
-  S->n_layers = n_layers;
-  S->batch = batch;
-  S->bp = batch <= 16 ? 16 : 32;
-  S->grid = t->num_sms;
-  S->ngrp = Ek / 16;
-  S->ncmax = (S->ngrp + S->grid - 1) / S->grid * 16;
-  if (S->ncmax > 128) return no("more than 128 channels per SM");
-  // B-operand slots: every unit of a phase (all its k-block copies in flight at once) when that
-  // leaves >= 4 weight-ring slots, else fewer
-  {
-    const int U1 = (2 * Ek / 128) * (D / 64), U4 = (D / 128) * (Ek / 64);
-    const int umax = ((U1 > U4 ? U1 : U4) + S->grid - 1) / S->grid;
-    S->nbr = umax < 1 ? 1 : umax;  // the B ring holds a whole phase (staged at once)
-    if (mk_ring_slots(S->bp, P, R, S->ncmax, S->nbr) < 4) return no("a phase's B operand does not fit in shared memory");
-  }
-  S->ring = mk_ring_slots(S->bp, P, R, S->ncmax, S->nbr);
-  if (S->ring < 3) return no("shared memory too small for the weight ring");
-  const int BP = S->bp;
-  const MkCnt cn = mk_cnt_layout(D, Ek);
-  size_t o = 256;
-  S->off_tab = o; o += al256((size_t)n_layers * sizeof(MkLayer));
-  S->off_residT = o; o += al256((size_t)D * BP * 4);
-  S->off_residB = o; o += al256((size_t)D * BP * 2);
-  S->off_xzT = o; o += al256((size_t)2 * Ek * BP * 4);
-  S->off_dbcT = o; o += al256((size_t)2 * P * BP * 4);
-  S->off_ss = o; o += al256((size_t)2 * BP * 4);
-  S->off_ssP = o; o += al256((size_t)S->grid * BP * 4);
-  S->off_gT = o; o += al256((size_t)Ek * BP * 2);
-  S->off_cnt = o; o += al256((size_t)cn.words * 4);
-  S->off_ep = o; o += al256((size_t)S->grid * 4);
-  S->total = o;
-  return SSM_OK;
-}
-}  // namespace
-
-extern "C" {
-
-ssm_status_t ssm_stack_bytes(ssm_tp_t tp, int32_t n_layers, int32_t batch, size_t* ws_bytes) {
-  if (!tp || !ws_bytes) return fail(SSM_ERR_ARG, "NULL argument");
-  ssm_tp_s::Stack S;
-  ssm_status_t st = stack_plan(tp, n_layers, batch, &S, true);
-  if (st != SSM_OK) return st;
-  *ws_bytes = S.total;
-  return SSM_OK;
-}
-
-ssm_status_t ssm_stack_bind(ssm_tp_t tp, const ssm_layer_weights_t* layers, const ssm_state_t* states,
-                            int32_t n_layers, int32_t batch, void* ws, size_t ws_bytes, void* stream) {
-  if (!tp || !layers || !states || !ws) return fail(SSM_ERR_ARG, "NULL argument");
-  ssm_tp_s::Stack S;
-  ssm_status_t st = stack_plan(tp, n_layers, batch, &S, true);
-  if (st != SSM_OK) return st;
-  if (ws_bytes < S.total) return fail(SSM_ERR_ARG, "stack workspace too small (%zu < %zu B)", ws_bytes, S.total);
-  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(SSM_ERR_ARG, "stack workspace must be 256-B aligned");
-  MkLayer* tab = new (std::nothrow) MkLayer[n_layers];
-  if (!tab) return fail(SSM_ERR_ARG, "out of host memory");
-  for (int l = 0; l < n_layers; ++l) {
-    const ssm_layer_weights_t& w = layers[l];
-    ssm_state_s* sl = states[l];
-    if (!w.w_in_pk || !w.w_out_pk || !w.w_x || !w.w_dt || !w.conv_w || !w.conv_b || !w.b_dt || !w.a_log || !w.d_skip) {
-      delete[] tab;
-      return fail(SSM_ERR_ARG, "layer %d: NULL weight (the stack decode needs w_in_pk and w_out_pk)", l);
-    }
-    if (!sl || sl->owner != tp || sl->batch != batch) {
-      delete[] tab;
-      return fail(SSM_ERR_CACHE, "layer %d: state missing or bound to another handle/batch", l);
-    }
-    tab[l] = MkLayer{reinterpret_cast<const __nv_bfloat16*>(w.w_in_pk), reinterpret_cast<const __nv_bfloat16*>(w.w_out_pk),
-                     reinterpret_cast<const __nv_bfloat16*>(w.w_x), reinterpret_cast<const __nv_bfloat16*>(w.w_dt),
-                     w.conv_w, w.conv_b, w.b_dt, w.a_log, w.d_skip, reinterpret_cast<__nv_bfloat16*>(sl->conv), sl->h,
-                     nullptr};
-  }
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  char* W = reinterpret_cast<char*>(ws);
-  cudaError_t e = cudaMemsetAsync(ws, 0, S.total, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(W + S.off_tab, tab, (size_t)n_layers * sizeof(MkLayer), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  delete[] tab;
-  if (e != cudaSuccess) return fail(SSM_ERR_CUDA, "stack bind: %s", cudaGetErrorString(e));
-  S.ws = ws;
-  S.trace = tp->stack.trace;
-  tp->stack = S;
-  return SSM_OK;
-}
-
-ssm_status_t ssm_stack_decode(ssm_tp_t tp, void* ws, float* residual, float norm_eps, void* stream) {
-  if (!tp || !ws || !residual) return fail(SSM_ERR_ARG, "NULL argument");
-  const ssm_tp_s::Stack& S = tp->stack;
-  if (ws != S.ws) return fail(SSM_ERR_ARG, "workspace is not the one bound by ssm_stack_bind");
-  if (reinterpret_cast<uintptr_t>(residual) & 15) return fail(SSM_ERR_ARG, "residual must be 16-B aligned");
-  char* W = reinterpret_cast<char*>(ws);
-  MkParams p{};
-  p.layers = reinterpret_cast<const MkLayer*>(W + S.off_tab);
-  p.n_layers = S.n_layers;
-  p.resid = residual;
-  p.residT = reinterpret_cast<float*>(W + S.off_residT);
-  p.residB = reinterpret_cast<__nv_bfloat16*>(W + S.off_residB);
-  p.xzT = reinterpret_cast<float*>(W + S.off_xzT);
-  p.dbcT = reinterpret_cast<float*>(W + S.off_dbcT);
-  p.ss = reinterpret_cast<float*>(W + S.off_ss);
-  p.ssP = reinterpret_cast<float*>(W + S.off_ssP);
-  p.gT = reinterpret_cast<__nv_bfloat16*>(W + S.off_gT);
-  p.cnt = reinterpret_cast<unsigned*>(W + S.off_cnt);
-  p.ep = reinterpret_cast<unsigned*>(W + S.off_ep);
-  p.bar = reinterpret_cast<unsigned long long*>(W);
-  p.err = reinterpret_cast<unsigned*>(W + 64);
-  p.B = S.batch;
-  p.D = tp->cfg.d_model;
-  p.Ek = tp->Ek;
-  p.R = tp->cfg.dt_rank;
-  p.P = tp->P;
-  p.K = tp->cfg.d_conv;
-  p.eps = norm_eps;
-  p.rmsnorm = tp->cfg.bcdt_rmsnorm;
-  p.rms_eps = tp->cfg.rms_eps;
-  p.ring = S.ring;
-  p.nbr = S.nbr;
-  p.ncmax = S.ncmax;
-  p.ngrp = S.ngrp;
-  p.trace = S.trace;
-  p.dbg = g_mk_dbg;
-  tp->launches++;
-  CU(launch_decode_mk(p, S.bp, S.grid, reinterpret_cast<cudaStream_t>(stream)));
-  return SSM_OK;
-}
-
-ssm_status_t ssm_stack_check(ssm_tp_t tp, void* ws, void* stream) {
-  if (!tp || !ws) return fail(SSM_ERR_ARG, "NULL argument");
-  CU(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
-  uint32_t errw = 0;
-  CU(cudaMemcpy(&errw, reinterpret_cast<char*>(ws) + 64, 4, cudaMemcpyDeviceToHost));
-  if (errw) return fail(SSM_ERR_PROTOCOL, "stack decode: grid barrier / weight pipeline timed out (code %u)", errw);
-  return SSM_OK;
-}
-
-ssm_status_t ssm_dbg_stack_trace(ssm_tp_t tp, void* buf, size_t bytes) {
-  if (!tp) return fail(SSM_ERR_ARG, "NULL argument");
-  tp->stack.trace = reinterpret_cast<unsigned long long*>(buf);
-  (void)bytes;
-  return SSM_OK;
-}
-
-ssm_status_t ssm_stack_info(ssm_tp_t tp, int32_t* ring_slots, int32_t* grid, int32_t* ch_per_cta) {
-  if (!tp || !ring_slots || !grid || !ch_per_cta) return fail(SSM_ERR_ARG, "NULL argument");
-  *ring_slots = tp->stack.ring * 1000 + tp->stack.nbr;
-  *grid = tp->stack.grid;
-  *ch_per_cta = tp->stack.ncmax;
-  return SSM_OK;
-}
-
-}  // extern "C"

@@ -53,26 +53,6 @@ SSM_DEV float2 fadd2(float2 a, float2 b) {
       : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
   return *reinterpret_cast<float2*>(&d);
 }
-// 2^x for x <= 0 on the FMA pipe (no MUFU): x = j + f, j = rint(x) via the 1.5*2^23 magic
-// add, f in [-0.5, 0.5], 2^f by a degree-5 near-minimax polynomial (max rel. error 2.3e-7,
-// the same order as ex2.approx.f32), 2^j applied by adding j to the exponent bits.
-// Used to move part of the scan's exponentials off the MUFU pipe (FlashAttention-4 style).
-SSM_DEV float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -125.f);
-  x.y = fmaxf(x.y, -125.f);
-  const float2 magic = make_float2(12582912.f, 12582912.f);
-  const float2 t = fadd2(x, magic);
-  const float2 jf = fadd2(t, make_float2(-12582912.f, -12582912.f));
-  const float2 f = ffma2(jf, make_float2(-1.f, -1.f), x);
-  float2 p = ffma2(f, make_float2(0.00132764654699713f, 0.00132764654699713f),
-                   make_float2(0.009675541892647743f, 0.009675541892647743f));
-  p = ffma2(p, f, make_float2(0.05550713464617729f, 0.05550713464617729f));
-  p = ffma2(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
-  p = ffma2(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
-  p = ffma2(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
 // SiLU with a single MUFU op: v * sigmoid(v) = 0.5 v (1 + tanh(v/2))  (bf16 mode; the tanh.approx
 // error ~2^-11 is below bf16 output rounding)
 SSM_DEV float silu_tanh(float v) {

@@ -4,8 +4,7 @@
 // scan step (Q1) with h updated in place, D skip and the SiLU(z) gate.
 //
 // The work unit is DS_CH channels x DS_BB batch rows, one (b, d) item per thread of a 128-thread
-// group.  Used by decode_step_kernel (one unit per block) and by the out_proj GEMM, whose idle
-// epilogue warps run the units as the producer of the GEMM's B operand g (gemm_tcgen05.cu).
+// group, one unit per block of decode_step_kernel (kernels.cu).
 #pragma once
 #include "common.cuh"
 #include "internal.h"
@@ -32,10 +31,6 @@ struct DStepArgs {
   void* g;               // [batch][Ek] out
   int batch, Ek, R, cph;
   float* zacc;           // optional fp32 z accumulator (read then zeroed)
-  float* zero_ss;        // optional: [batch] floats zeroed by unit (0, 0) once the predecessor finished
-  int h_late;            // experiment (SSM_DSTEP_HLATE=1): load h after griddepcontrol.wait
-  const void* pf;        // optional: the successor GEMM's weights, bulk-prefetched into L2 by the blocks
-  int64_t pf_bytes;      //   (weights do not depend on activations; HBM is idle during this kernel)
 };
 
 // W_dt row stride (elements): 16-B aligned, and a 4-word bank shift from row to row (conflict-free LDS.128)
@@ -106,10 +101,13 @@ SSM_DEV void dstep_unit(const DStepArgs& a, const Peers& src, int nsrc, int c0, 
   const bool okd = d < Ek;
   const float bias = okd ? a.b_dt[d] : 0.f;
   const float Dd = okd ? a.d_skip[d] : 0.f;
-  // the items' h rows: owner data of this kernel (the previous token's step), independent of the
-  // predecessor kernels -- in flight before griddepcontrol.wait
+  // the items' h rows, written by the previous token's decode step: that kernel is only a
+  // transitive predecessor (PDL guarantees the completion of the immediate predecessor grid
+  // alone, and every kernel of the chain triggers its dependents at entry), so h is read after
+  // griddepcontrol.wait, which returns once the whole chain up to this kernel has completed
+  if (with_pdl_wait) pdl_wait();  // everything below reads what the predecessor kernels produced
   float hs[IPT][N];
-  auto load_h = [&]() {
+  {
 #pragma unroll
     for (int it = 0; it < IPT; ++it) {
       const int bi = bl + DS_BB * it;
@@ -121,11 +119,7 @@ SSM_DEV void dstep_unit(const DStepArgs& a, const Peers& src, int nsrc, int c0, 
         hs[it][n] = t4.x; hs[it][n + 1] = t4.y; hs[it][n + 2] = t4.z; hs[it][n + 3] = t4.w;
       }
     }
-  };
-  if (!a.h_late) load_h();
-  if (with_pdl_wait) pdl_wait();  // everything below reads what the predecessor kernels produced
-  if (a.h_late) load_h();
-  if (a.zero_ss && c0 == 0 && b0 == 0 && tid < batch) a.zero_ss[tid] = 0.f;  // (its reader was the predecessor)
+  }
   // ---- activations: dbc rows (first source), the items' h rows, u, z -- all loads in flight
   const int p4 = P / 4;
   const int nd = nb * p4;

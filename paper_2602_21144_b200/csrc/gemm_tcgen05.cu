@@ -18,12 +18,12 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
-#include <cstdlib>
+
 #include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
-#include "dstep.cuh"
+
 
 namespace ssm {
 
@@ -46,82 +46,34 @@ struct CtaRes {
   int ring;          // bytes of the stage ring
   int tmem_cols;     // power of two >= 32
   int acc_stride;    // columns per accumulator
-  int nomma;         // experiment knob (bits): 1 skip the MMAs, 2 skip the B loads, 4 skip the epilogue
   int a_indep;       // A (weights) does not depend on the predecessor grid: first ring fill before the PDL wait
-  int nacc;          // interleaved partial accumulators per tile (k-step i -> slot i % nacc), summed by the
-                     // epilogue: independent MMA chains for skinny N, where one chain is MMA-latency bound
-  int slot_cols;     // TMEM columns per partial accumulator (>= BN, multiple of 32)
 };
-// SSM_GEMM_PREFILL_VAR=0: the prefill GEMMs stay on the all-paths instantiation
-const int g_gemm_prefill_var = [] { const char* e = getenv("SSM_GEMM_PREFILL_VAR"); return e ? atoi(e) : 1; }();
-// SSM_GEMM_VARIANTS=0: every GEMM on the all-paths kernel instantiation
-const bool g_gemm_variants = [] { const char* e = getenv("SSM_GEMM_VARIANTS"); return !e || atoi(e) != 0; }();
-const bool kMinBN16 = [] { const char* e = getenv("SSM_GEMM_BN16"); return !e || atoi(e) != 0; }();
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane group)
 // threads of a kernel variant: the skinny atomic variant (VAR 2, BN <= 32: one 32-column chunk, so
 // only the first epilogue half ever works) runs 4 epilogue warps -- a smaller CTA that fits next
 // to the decode-step blocks it follows
 constexpr int var_threads(int var) { return var == 2 ? 192 : kThreads; }
-// VAR 4..7: prefill GEMMs with one fixed (non-transposed) epilogue kind each
-constexpr int var_kind(int var) {
-  return var == 4 ? EPI_STORE_BF16 : var == 5 ? EPI_ADD_F32 : var == 6 ? EPI_SOFTPLUS_BF16 : var == 7 ? EPI_STORE_F32 : -1;
-}
+// VAR 6: the prefill dt_proj with its softplus(+bias) epilogue fixed at compile time
+constexpr int var_kind(int var) { return var == 6 ? EPI_SOFTPLUS_BF16 : -1; }
 
-// Work decomposition.  Data-parallel mode: unit u = (k-split, m-tile, n-tile), CTAs stride
-// over units.  Stream-K mode (streamk != 0): the linearised (tile, k-block) space is cut into
-// gridDim.x equal contiguous ranges, one per CTA; a range may cover the tail of one tile and
-// the head of the next, so partial tiles are combined by the atomic epilogue.
+// Work decomposition: unit u = (k-split, m-tile, n-tile), CTAs stride over units.
 struct TileSched {
-  int m_tiles, n_tiles, kb_total, kbs, ksplit, units, streamk;
-  int kown;  // channel-owned (Q = kown m-groups): CTA i = (k-split i / Q, tiles i % Q + Q j); grid = ksplit * Q
-  // iterate segments (mt, nt, kb0, kb1) of this CTA; returns false when done
+  int m_tiles, n_tiles, kb_total, kbs, ksplit, units;
+  // iterate units (mt, nt, kb0, kb1) of this CTA; returns false when done
   __device__ bool next(int& cursor, int& mt, int& nt, int& kb0, int& kb1) const {
-    if (kown) {
-      const int t = (int)blockIdx.x % kown + kown * cursor;
-      if (t >= m_tiles * n_tiles) return false;
-      ++cursor;
-      nt = t % n_tiles;
-      mt = t / n_tiles;
-      kb0 = (int)blockIdx.x / kown * kbs;
-      kb1 = min(kb_total, kb0 + kbs);
-      return true;
-    }
-    if (!streamk) {
-      const int u = cursor;
-      if (u >= units) return false;
-      cursor += gridDim.x;
-      nt = u % n_tiles;
-      const int rest = u / n_tiles;
-      mt = rest % m_tiles;
-      const int ks = rest / m_tiles;
-      kb0 = ks * kbs;
-      kb1 = min(kb_total, kb0 + kbs);
-      return true;
-    }
-    const long long W = (long long)m_tiles * n_tiles * kb_total;
-    const long long end = W * (blockIdx.x + 1) / gridDim.x;
-    long long pos = cursor < 0 ? W * blockIdx.x / gridDim.x : (long long)cursor;
-    if (pos >= end) return false;
-    const int tile = (int)(pos / kb_total);
-    kb0 = (int)(pos % kb_total);
-    kb1 = (int)min((long long)kb_total, kb0 + (end - pos));
-    nt = tile % n_tiles;
-    mt = tile / n_tiles;
-    cursor = (int)(pos + (kb1 - kb0));
+    const int u = cursor;
+    if (u >= units) return false;
+    cursor += gridDim.x;
+    nt = u % n_tiles;
+    const int rest = u / n_tiles;
+    mt = rest % m_tiles;
+    const int ks = rest / m_tiles;
+    kb0 = ks * kbs;
+    kb1 = min(kb_total, kb0 + kbs);
     return true;
   }
-  __device__ int first() const { return streamk ? -1 : kown ? 0 : (int)blockIdx.x; }
-  // stream-K: number of CTAs whose ranges intersect tile t (ranges are non-empty: W >= gridDim.x)
-  __device__ int contributors(int t) const {
-    const long long W = (long long)m_tiles * n_tiles * kb_total, G = gridDim.x;
-    const long long p0 = (long long)t * kb_total, p1 = p0 + kb_total - 1;
-    const long long c0 = ((p0 + 1) * G + W - 1) / W - 1, c1 = ((p1 + 1) * G + W - 1) / W - 1;
-    return (int)(c1 - c0 + 1);
-  }
+  __device__ int first() const { return (int)blockIdx.x; }
 };
-
-// partial accumulators actually written for a tile of (kb1 - kb0) k-blocks (4 UMMA k-steps each)
-__device__ __forceinline__ int tile_nacc(const CtaRes& cr, int kb0, int kb1) { return min(cr.nacc, 4 * (kb1 - kb0)); }
 
 // The only epilogue of the VAR 2 kernel: C[n * ldc + m] += acc atomically (swap-AB split-K).
 __device__ __forceinline__ void epi_chunk_atomic_trans(const Epilogue& e, int m0, int n0, int M, int N,
@@ -334,12 +286,6 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
         }
       }
     }
-    float rsc[16];  // decode chain: the pre-norm's 1/rms of each token row (1 otherwise)
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int b = half * 16 + q;
-      rsc[q] = (e.ss && b < N) ? rsqrtf(__ldcg(e.ss + b) * e.ss_scale + e.ss_eps) : 1.f;
-    }
     // ---- accumulator: 16 token columns of this warp's 32 feature rows
     mbar_wait(&tfull[acc], acc_ph);
     tc_fence_after();
@@ -347,48 +293,10 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
     const uint32_t tb = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * cr.acc_stride + half * 16);
     tmem_ld_32x32b_x16(tb, r);
     tmem_ld_wait();
-    for (int q = 1; q < tile_nacc(cr, kb0, kb1); ++q) {  // fold the interleaved partial accumulators
-      uint32_t r2[16];
-      tmem_ld_32x32b_x16(tb + (uint32_t)(q * cr.slot_cols), r2);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
-    }
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM consumed: the MMA warp may reuse it
     if (++acc == 2) { acc = 0; acc_ph ^= 1; }
-
-    if (ts.streamk && !(kb0 == 0 && kb1 == ts.kb_total)) {
-      // stream-K partial tile: add into the shared accumulator; the last contributor finishes
-      const int need = ts.contributors(mt);
-      float* sk = e.sk_acc + ((int64_t)mt * N) * BM + (f - f0);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int b = half * 16 + q;
-        if (b < N) red_add_f32(sk + (int64_t)b * BM, __uint_as_float(r[q]));
-      }
-      volatile int& s_last = *reinterpret_cast<volatile int*>(su + 32 * SU_LD);
-      named_bar_sync(1, 256);  // every epilogue thread's adds performed relative to thread 64
-      if (threadIdx.x == 64) {
-        __threadfence();
-        const int old = atomicAdd(e.sk_cnt + mt, 1);
-        const bool last = old + 1 == need;
-        if (last) e.sk_cnt[mt] = 0;  // all contributions in: re-armed for the next call
-        s_last = last;
-        __threadfence();
-      }
-      named_bar_sync(1, 256);
-      if (!s_last) continue;
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int b = half * 16 + q;
-        if (b < N) {
-          r[q] = __float_as_uint(__ldcg(sk + (int64_t)b * BM));
-          sk[(int64_t)b * BM] = 0.f;
-        }
-      }
-    }
 
     __nv_bfloat16* su_col = su + (f - f0);
     if (is_x) {
@@ -398,7 +306,7 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
         const int b = half * 16 + q;
         float uq = 0.f;
         if (b < N) {
-          const float x = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[q]) * rsc[q]));
+          const float x = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[q])));
           float a = bias;
 #pragma unroll
           for (int j = 0; j < 3; ++j)
@@ -426,7 +334,7 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           const int b = half * 16 + q;
-          if (b < N) C[(int64_t)b * e.ldc] = __float2bfloat16_rn(__uint_as_float(r[q]) * rsc[q]);
+          if (b < N) C[(int64_t)b * e.ldc] = __float2bfloat16_rn(__uint_as_float(r[q]));
         }
       }
 #pragma unroll
@@ -460,210 +368,15 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
   }
 }
 
-// ---- decode-step job of the fused decode out_proj: epilogue warps 2-5 and 6-9 each run one
-// 128-thread decode-step unit at a time (named barriers 2 and 3), then all CTAs meet at a grid
-// barrier (monotonic 64-bit counter: generation = old / gridDim.x) so that every g row is
-// written before any CTA's TMA reads it.  Bounded wait (2 s): a broken co-residency assumption
-// produces wrong numbers and a printf instead of a hung GPU.
-constexpr int kJobIpt = 4;  // batch rows per thread in the decode-step job (16 rows per 128-thread unit)
-template <typename T, int N, bool FAST>
-__device__ void run_dstep_units(const DStepJob& j, float* smem_f) {
-  const int warp = threadIdx.x >> 5;
-  const int half = (warp - 2) >> 2;
-  const int htid = threadIdx.x - 64 - half * 128;
-  DStepArgs a{};
-  a.src_off = 0; a.ldp = j.ldp; a.rmsnorm = j.rmsnorm; a.eps = j.eps; a.u = j.u; a.z = j.z; a.ldz = j.ldz;
-  a.w_dt = j.w_dt; a.b_dt = j.b_dt; a.a_log = j.a_log; a.d_skip = j.d_skip; a.h = j.h; a.g = j.g;
-  a.batch = j.batch; a.Ek = j.Ek; a.R = j.R; a.cph = j.cph; a.zacc = nullptr;
-  Peers src{};
-  src.p[0] = const_cast<float*>(j.dbc);
-  constexpr int IPT = kJobIpt;
-  const int unit_floats = (int)(dstep_smem(j.R, N, (int)sizeof(T), IPT) / 4);
-  float* my = smem_f + half * unit_floats;
-  const int uc = (j.Ek + DS_CH - 1) / DS_CH, ub = (j.batch + DS_BB * IPT - 1) / (DS_BB * IPT);
-  for (int unit = blockIdx.x * 2 + half; unit < uc * ub; unit += gridDim.x * 2) {
-    dstep_unit<T, N, FAST, DS_THREADS, IPT>(a, src, 1, (unit % uc) * DS_CH, (unit / uc) * DS_BB * IPT, htid, my,
-                                            2 + half, false);
-    dstep_sync<DS_THREADS>(2 + half);  // unit smem reused by the next unit
-  }
-}
-
-// Channel-owned mode (DStepJob::local): the decode step for this CTA's channels only, then the
-// B operand (g of those channels) is published to the CTA's own TMA loads; the last CTA to have
-// consumed dbc re-zeroes it.  Units of 32 channels x 16 batch rows, alternating over the two
-// 128-thread halves of the epilogue warps.
-template <typename T, int N, bool FAST>
-__device__ void run_dstep_local_units(const DStepJob& j, float* smem_f, int c_lo, int c_hi) {
-  const int warp = threadIdx.x >> 5;
-  const int half = (warp - 2) >> 2;
-  const int htid = threadIdx.x - 64 - half * 128;
-  DStepArgs a{};
-  a.src_off = 0; a.ldp = j.ldp; a.rmsnorm = j.rmsnorm; a.eps = j.eps; a.u = j.u; a.z = j.z; a.ldz = j.ldz;
-  a.w_dt = j.w_dt; a.b_dt = j.b_dt; a.a_log = j.a_log; a.d_skip = j.d_skip; a.h = j.h; a.g = j.g;
-  a.batch = j.batch; a.Ek = j.Ek; a.R = j.R; a.cph = j.cph; a.zacc = nullptr;
-  Peers src{};
-  src.p[0] = const_cast<float*>(j.dbc);
-  constexpr int IPT = kJobIpt;
-  const int unit_floats = (int)(dstep_smem(j.R, N, (int)sizeof(T), IPT) / 4);
-  float* my = smem_f + half * unit_floats;
-  const int uc = (c_hi - c_lo + DS_CH - 1) / DS_CH, ub = (j.batch + DS_BB * IPT - 1) / (DS_BB * IPT);
-  for (int unit = half; unit < uc * ub; unit += 2) {
-    dstep_unit<T, N, FAST, DS_THREADS, IPT>(a, src, 1, c_lo + (unit % uc) * DS_CH, (unit / uc) * DS_BB * IPT, htid, my,
-                                            2 + half, false);
-    dstep_sync<DS_THREADS>(2 + half);  // unit smem reused by the next unit
-  }
-}
-
-__device__ __forceinline__ void run_dstep_local(const DStepJob& j, float* smem_f, const TileSched& ts,
-                                                volatile int* s_flag) {
-  const int Q = ts.kown, sl = (int)blockIdx.x / Q, q = (int)blockIdx.x % Q;
-  const int w = ts.kbs * BK / Q;  // channels of this CTA's share of the split (multiple of 32)
-  const int c_lo = sl * ts.kbs * BK + q * w;
-  const int c_hi = min(j.Ek, c_lo + w);
-  if (c_lo < c_hi) {
-    if (j.N == 16) run_dstep_local_units<__nv_bfloat16, 16, true>(j, smem_f, c_lo, c_hi);
-    else run_dstep_local_units<__nv_bfloat16, 8, true>(j, smem_f, c_lo, c_hi);
-  }
-  fence_proxy_async_global();  // this thread's g stores -> the async proxy (the group's TMA B loads)
-  named_bar_sync(1, 256);
-  if ((threadIdx.x >> 5) == 2) {  // warp 2: group barrier (converged polling) + dbc reader count
-    int last = 0;
-    unsigned long long target = 0;
-    if (threadIdx.x == 64) {
-      __threadfence();
-      const int old = atomicAdd(j.rd_cnt, 1);
-      last = old + 1 == (int)gridDim.x;
-      if (last) *j.rd_cnt = 0;
-      if (Q > 1) {
-        const unsigned long long o2 = atomicAdd(j.grp_cnt + sl, 1ull);
-        target = (o2 / Q + 1) * Q;
-      }
-    }
-    if (Q > 1) {
-      target = __shfl_sync(0xffffffffu, target, 0);
-      const uint64_t t0 = globaltimer();
-      while (!__all_sync(0xffffffffu, threadIdx.x != 64 || ld_acquire_gpu_u64(j.grp_cnt + sl) >= target)) {
-        if (globaltimer() - t0 > 2000000000ull) {
-          if (threadIdx.x == 64) printf("ssm: out_proj group barrier timed out (CTA %d)\n", blockIdx.x);
-          break;
-        }
-      }
-    }
-    if (threadIdx.x == 64) {
-      fence_proxy_async_global();
-      *s_flag = last;
-    }
-    __syncwarp();
-  }
-  named_bar_sync(1, 256);
-  if (*s_flag) {  // every CTA has read dbc into its shared memory: re-arm it for the next token
-    float* z = const_cast<float*>(j.dbc);
-    for (int64_t i = threadIdx.x - 64; i < j.ndbc; i += 256) z[i] = 0.f;
-  }
-}
-
-__device__ __forceinline__ void run_dstep_job(const DStepJob& j, float* smem_f) {
-  if (j.N == 16) run_dstep_units<__nv_bfloat16, 16, true>(j, smem_f);
-  else run_dstep_units<__nv_bfloat16, 8, true>(j, smem_f);
-  named_bar_sync(1, 256);
-  if ((threadIdx.x >> 5) == 2) {  // warp 2 arrives and polls converged (a lone lane would crawl)
-    unsigned long long target = 0;
-    if (threadIdx.x == 64) {
-      __threadfence();
-      const unsigned long long G = gridDim.x;
-      const unsigned long long old = atomicAdd(j.sync, 1ull);
-      target = (old / G + 1) * G;
-    }
-    target = __shfl_sync(0xffffffffu, target, 0);
-    const uint64_t t0 = globaltimer();
-    while (!__all_sync(0xffffffffu, threadIdx.x != 64 || ld_acquire_gpu_u64(j.sync) >= target)) {
-      if (globaltimer() - t0 > 2000000000ull) {
-        if (threadIdx.x == 64) printf("ssm: decode-step grid barrier timed out (CTA %d)\n", blockIdx.x);
-        break;
-      }
-    }
-    if (threadIdx.x == 64) fence_proxy_async_global();
-    __syncwarp();
-  }
-  named_bar_sync(1, 256);
-}
-
-// Decode-chain finaliser of the split-K out_proj (see Epilogue::fin_cnt): run by the 8 epilogue
-// warps after this CTA's atomics for output tile mt.  The last of the fin_need contributions
-// reads the final residual tile back (128 d-columns x N rows), writes its bf16 copy (the next
-// layer's in_proj B operand) and adds its per-row sums of squares (the next pre-norm).
-__device__ __forceinline__ void chain_finalise(const Epilogue& e, int mt, int M, int N, float* scratch) {
-  // scratch: 257 floats of dynamic shared memory carved from the ring (no static __shared__: the
-  // kernel's dynamic allocation is already at the opt-in limit)
-  float (*s_red)[32] = reinterpret_cast<float (*)[32]>(scratch);
-  volatile int& s_last = *reinterpret_cast<volatile int*>(scratch + 256);
-  const int et = threadIdx.x - 64;  // 0..255
-  const int warp = et >> 5, lane = et & 31;
-  // bar.sync makes every epilogue thread's atomics performed relative to thread 0; its gpu-scope
-  // fence then publishes them (cumulativity) before the counter increment
-  named_bar_sync(4, 256);
-  if (et == 0) {
-    __threadfence();
-    const int old = atomicAdd(e.fin_cnt + mt, 1);
-    const bool last = old + 1 == e.fin_need;
-    if (last) e.fin_cnt[mt] = 0;  // all contributions in: reset for the next call
-    s_last = last;
-    __threadfence();
-  }
-  named_bar_sync(4, 256);
-  if (!s_last) return;
-  const float* R = reinterpret_cast<const float*>(e.C);
-  const int m = mt * BM + (et & (BM - 1));
-  float acc[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-  if (m < M) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int n = (et >> 7) + 2 * j;  // threads 0-127: even rows, 128-255: odd rows
-      if (n < N) {
-        const float v = __ldcg(R + (int64_t)n * e.ldc + m);
-        e.fin_x[(int64_t)n * e.fin_ldx + m] = __float2bfloat16_rn(v);
-        acc[j] = v * v;
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-  }
-  if (lane == 0)
-#pragma unroll
-    for (int j = 0; j < 16; ++j) s_red[warp][j] = acc[j];
-  named_bar_sync(4, 256);
-  if (et < 32) {
-    const int j = et & 15, half = et >> 4;  // row n = half + 2 j, summed over the 4 warps of that half
-    const int n = half + 2 * j;
-    if (n < N) {
-      const float t = s_red[half * 4 + 0][j] + s_red[half * 4 + 1][j] + s_red[half * 4 + 2][j] + s_red[half * 4 + 3][j];
-      atomicAdd(e.fin_ss + n, t);
-    }
-  }
-  named_bar_sync(4, 256);  // s_red reused by the next tile
-}
-
-// Experiment-only timeline (cr.nomma & 8): per-CTA clock64 offsets of pipeline events.
-constexpr int kTraceSlots = 16, kTraceCtas = 1024;
-__device__ unsigned long long g_trace[kTraceCtas * kTraceSlots];
-#define TRACE(slot, val)                                                                   \
-  do {                                                                                     \
-    if ((cr.nomma & 8) && blockIdx.x < kTraceCtas) g_trace[blockIdx.x * kTraceSlots + (slot)] = (val); \
-  } while (0)
-
-// VAR: 0 = every path (prefill GEMMs, experiments); 1 = the fused decode in_proj only; 2 = skinny
-// swap-AB split-K GEMMs with the atomic epilogue only (decode out_proj / x_proj).  The decode
-// variants are separate kernels so their register allocation is not set by paths they never run.
+// VAR: 0 = every path (prefill GEMMs); 1 = the fused decode in_proj only; 2 = skinny swap-AB
+// split-K GEMMs with the atomic epilogue only (decode out_proj / x_proj); 6 = prefill dt_proj
+// (softplus epilogue).  The decode variants are separate kernels so their register allocation is
+// not set by paths they never run.
 template <int VAR, int XPN = XP_NT>
 __global__ void __launch_bounds__(var_threads(VAR), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_blk, int64_t lda, int K,
-                   CtaRes cr, int a_blocked, const DStepJob job) {
+                   CtaRes cr, int a_blocked) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int STAGES = num_stages(BN, KBS, cr.ring);
@@ -675,28 +388,11 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
   uint64_t* empty = full + MAX_STAGES;
   uint64_t* tfull = empty + MAX_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* bready = tempty + 2;  // decode-step job done grid-wide: B (g) may be loaded
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const long long c_start = clock64();
-  if (threadIdx.x == 0) { TRACE(0, globaltimer()); TRACE(1, c_start); }
   pdl_trigger();
-  if (epi.pf && (int)blockIdx.x >= (ts.streamk ? (int)gridDim.x : ts.units)) {
-    // spare CTA: L2 prefetch of its slice of the successor's weights, then exit
-    const int nspare = (int)gridDim.x - ts.units, j = (int)blockIdx.x - ts.units;
-    const int64_t per = ((epi.pf_bytes + nspare - 1) / nspare + 15) & ~int64_t(15);
-    const int64_t lo = (int64_t)j * per, hi = lo + per < epi.pf_bytes ? lo + per : epi.pf_bytes;
-    if (threadIdx.x < 32) {
-      const char* base = reinterpret_cast<const char*>(epi.pf);
-      for (int64_t o = lo + (int64_t)threadIdx.x * 65536; o < hi; o += 32 * 65536) {
-        const int64_t n = hi - o < 65536 ? hi - o : 65536;
-        prefetch_l2(base + o, (uint32_t)(n & ~int64_t(15)));
-      }
-    }
-    return;
-  }
 
   if (warp == 0 && lane == 0) {
     if (!a_blocked) tma_prefetch_desc(&tmA);
@@ -709,7 +405,6 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], (var_threads(VAR) - 64) / 32);
     }
-    mbar_init(bready, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, cr.tmem_cols);
@@ -717,14 +412,13 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) TRACE(2, clock64() - c_start);
 
   if (warp == 0) {
     // ---------------- TMA producer.  The whole warp runs the (warp-uniform) schedule and waits;
     // lane 0 alone issues the copies.  (With lane 0 looping alone while lanes 1-31 sat at the
     // teardown barrier, every iteration of the producer loop measured ~0.2-0.45 us.)
     const bool leader = lane == 0;
-    const uint32_t stage_tx = (uint32_t)((cr.nomma & 2) ? BM : BM + BN) * BK * 2;  // per k-block
+    const uint32_t stage_tx = (uint32_t)(BM + BN) * BK * 2;  // per k-block
     auto issue_a = [&](uint8_t* st, uint64_t* bar, int mt, int kb, int nk) {
       if (a_blocked)  // A pre-tiled AND pre-swizzled: the nk blocks (mt, kb..kb+nk) are one
         // contiguous run of nk x 16 KB whose bytes are already the SW128 smem image -> 1D bulk copy
@@ -733,8 +427,7 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         for (int j = 0; j < nk; ++j) tma_load_2d(st + j * A_STAGE, &tmA, bar, (kb + j) * BK, mt * BM);
     };
     auto issue_b = [&](uint8_t* st, uint64_t* bar, int nt, int kb, int nk) {
-      if (!(cr.nomma & 2))
-        for (int j = 0; j < nk; ++j) tma_load_2d(st + BOFF + j * BSUB, &tmB, bar, (kb + j) * BK, nt * BN);
+      for (int j = 0; j < nk; ++j) tma_load_2d(st + BOFF + j * BSUB, &tmB, bar, (kb + j) * BK, nt * BN);
     };
     // A independent of the predecessor grid (weights): arm the first ring fill and issue its A
     // loads BEFORE griddepcontrol.wait, so the weight stream starts while the predecessor drains.
@@ -752,10 +445,6 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
     }
     __syncwarp();
     pdl_wait();
-    if (job.enabled || epi.nres) {  // B produced inside this grid (decode-step job / pre-norm)
-      mbar_wait(bready, 0);
-      if (leader) fence_proxy_async_global();
-    }
     int stage = 0, g = 0;
     uint32_t ph = 0;
     int cur = ts.first(), mt, nt, kb0, kb1;
@@ -766,7 +455,6 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         if (g >= n_pre) {
           mbar_wait(&empty[stage], ph ^ 1);
           if (leader) {
-            if (kb == kb0) TRACE(3, clock64() - c_start);
             mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * stage_tx);
             issue_a(st, &full[stage], mt, kb, nk);
           }
@@ -794,27 +482,18 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
       mbar_wait(&tempty[acc], acc_ph ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + (uint32_t)(acc * cr.acc_stride);
-      const int na = tile_nacc(cr, kb0, kb1);
-      int slot = 0, ki = 0;  // partial accumulator of the next k-step; k-steps issued in this tile
       for (int kb = kb0; kb < kb1; kb += KBS) {
         const int nk = min(KBS, kb1 - kb);
         mbar_wait(&full[stage], ph);
-        if (lane == 0 && kb == kb0) TRACE(4, clock64() - c_start);
-        if (lane == 0 && kb + KBS >= kb1) TRACE(5, clock64() - c_start);
         tc_fence_after();
         const uint64_t a_desc = ring_desc + (uint64_t)((stage * SB) >> 4);
         const uint64_t b_desc = a_desc + (uint64_t)(BOFF >> 4);
         if (elect_one()) {
-          if (!(cr.nomma & 1)) {
-            for (int j = 0; j < nk; ++j) {
+          for (int j = 0; j < nk; ++j) {
 #pragma unroll
-              for (int k = 0; k < BK / 16; ++k) {
-                umma_bf16(d + (uint32_t)(slot * cr.slot_cols), a_desc + (uint64_t)((j * A_STAGE + k * 32) >> 4),
-                          b_desc + (uint64_t)((j * BSUB + k * 32) >> 4), idesc, ki >= na ? 1u : 0u);
-                ++ki;
-                if (++slot == na) slot = 0;
-              }
-            }
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16(d, a_desc + (uint64_t)((j * A_STAGE + k * 32) >> 4), b_desc + (uint64_t)((j * BSUB + k * 32) >> 4),
+                        idesc, (kb > kb0 || j > 0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
         }
@@ -823,162 +502,74 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
       }
       if (elect_one()) umma_commit(&tfull[acc]);
       __syncwarp();
-      if (lane == 0) TRACE(6, clock64() - c_start);
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
   } else {
     // ---------------- epilogue warps 2..9; TMEM lane group = warp % 4, column half = (warp-2)/4
     pdl_wait();
-    if (VAR == 0 && job.enabled) {
-      if (job.local) {
-        const int js = (int)((2 * dstep_smem(job.R, job.N, 2, kJobIpt) + 127) / 128 * 128);
-        run_dstep_local(job, reinterpret_cast<float*>(smem + cr.ring + 512), ts,
-                        reinterpret_cast<volatile int*>(smem + cr.ring + 512 + js));
-      } else {
-        run_dstep_job(job, reinterpret_cast<float*>(smem + cr.ring + 512));
-      }
-      if (threadIdx.x == 64) mbar_arrive(bready);
-    }
-    if (epi.zero && blockIdx.x == 0) {  // (after the job: it may read the buffer being zeroed)
+    if (epi.zero && blockIdx.x == 0) {
       const int64_t n4 = epi.nzero / 4;
       for (int64_t i = threadIdx.x - 64; i < n4; i += var_threads(VAR) - 64)
         reinterpret_cast<float4*>(epi.zero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int64_t i = 4 * n4 + threadIdx.x - 64; i < epi.nzero; i += var_threads(VAR) - 64) epi.zero[i] = 0.f;
     }
-    if (VAR == 0 && epi.nres) {
-      // pre-norm of the N residual rows -> the bf16 B operand (global; identical in every CTA)
-      // the warp's rows are handled together, 8 x 16-B loads per row in flight per lane per chunk
-      const int et = threadIdx.x - 64, w8 = et >> 5;
-      constexpr int RW = 4, CH = 8;  // rows per warp (N <= 32), float4 per lane per chunk
-      float ss[RW];
-#pragma unroll
-      for (int r = 0; r < RW; ++r) ss[r] = 0.f;
-      const int nv = K / 4;
-      for (int base = 0; base < nv; base += 32 * CH) {
-        float4 v[RW][CH];
-#pragma unroll
-        for (int r = 0; r < RW; ++r)
-#pragma unroll
-          for (int c = 0; c < CH; ++c) {
-            const int row = w8 + 8 * r, i = base + lane + 32 * c;
-            v[r][c] = (row < N && i < nv) ? reinterpret_cast<const float4*>(epi.nres + (int64_t)row * K)[i]
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-        for (int r = 0; r < RW; ++r)
-#pragma unroll
-          for (int c = 0; c < CH; ++c) {
-            ss[r] = fmaf(v[r][c].x, v[r][c].x, ss[r]); ss[r] = fmaf(v[r][c].y, v[r][c].y, ss[r]);
-            ss[r] = fmaf(v[r][c].z, v[r][c].z, ss[r]); ss[r] = fmaf(v[r][c].w, v[r][c].w, ss[r]);
-          }
-      }
-#pragma unroll
-      for (int r = 0; r < RW; ++r) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ss[r] += __shfl_xor_sync(0xffffffffu, ss[r], o);
-        ss[r] = 1.0f / sqrtf(ss[r] / (float)K + epi.nres_eps);
-      }
-      for (int base = 0; base < K / 8; base += 32 * CH / 2) {  // second pass: L1-resident rows
-#pragma unroll
-        for (int r = 0; r < RW; ++r)
-#pragma unroll
-          for (int c = 0; c < CH / 2; ++c) {
-            const int row = w8 + 8 * r, i = base + lane + 32 * c;
-            if (row < N && i < K / 8) {
-              const float4* xr = reinterpret_cast<const float4*>(epi.nres + (int64_t)row * K);
-              const float4 a = xr[2 * i], b = xr[2 * i + 1];
-              const float rs = ss[r];
-              __nv_bfloat162 h[4] = {__floats2bfloat162_rn(a.x * rs, a.y * rs), __floats2bfloat162_rn(a.z * rs, a.w * rs),
-                                     __floats2bfloat162_rn(b.x * rs, b.y * rs), __floats2bfloat162_rn(b.z * rs, b.w * rs)};
-              reinterpret_cast<uint4*>(epi.nx + (int64_t)row * K)[i] = *reinterpret_cast<const uint4*>(h);
-            }
-          }
-      }
-      fence_proxy_async_global();  // these generic stores -> this CTA's TMA loads of B
-      named_bar_sync(1, 256);
-      if (threadIdx.x == 64) mbar_arrive(bready);
-    }
-    if (VAR == 1 || (VAR == 0 && epi.kind == EPI_DECODE_INPROJ)) {
+    if constexpr (VAR == 1) {
       decode_inproj_epilogue<XPN>(epi, ts, M, N, tfull, tempty, tmem_base, cr,
                                   reinterpret_cast<__nv_bfloat16*>(smem + cr.ring + 512));
-      goto teardown;
-    }
-    if constexpr (VAR != 1)
-    {
-    const int eg = warp & 3;
-    const int half = (warp - 2) >> 2;
-    int acc = 0;
-    uint32_t acc_ph = 0;
-    int cur = ts.first(), mt, nt, kb0, kb1;
-    if (!(cr.nomma & 16) && lane == 0) {
-      // Touch the first output address now: a TLB miss on a store would otherwise stall the
-      // epilogue for microseconds after the weight stream (page walks queue behind it).
-      int c2 = cur, mt2, nt2, k0, k1;
-      if (ts.next(c2, mt2, nt2, k0, k1)) {
-        const int m = min(M - 1, mt2 * BM + eg * 32), n = min(N - 1, nt2 * BN);
-        const int64_t idx = epi.trans ? (int64_t)n * epi.ldc + m : (int64_t)m * epi.ldc + n;
-        const int esz = (epi.kind == EPI_STORE_BF16 || epi.kind == EPI_SOFTPLUS_BF16) ? 2 : 4;
-        touch_global(reinterpret_cast<const uint8_t*>(epi.C) + idx * esz);
-        if (epi.bias) touch_global(epi.bias + (epi.trans ? m : n));
+    } else {
+      const int eg = warp & 3;
+      const int half = (warp - 2) >> 2;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      int cur = ts.first(), mt, nt, kb0, kb1;
+      if (lane == 0) {
+        // Touch the first output address now: a TLB miss on a store would otherwise stall the
+        // epilogue for microseconds after the weight stream (page walks queue behind it).
+        int c2 = cur, mt2, nt2, k0, k1;
+        if (ts.next(c2, mt2, nt2, k0, k1)) {
+          const int m = min(M - 1, mt2 * BM + eg * 32), n = min(N - 1, nt2 * BN);
+          const int64_t idx = epi.trans ? (int64_t)n * epi.ldc + m : (int64_t)m * epi.ldc + n;
+          const int esz = (epi.kind == EPI_STORE_BF16 || epi.kind == EPI_SOFTPLUS_BF16) ? 2 : 4;
+          touch_global(reinterpret_cast<const uint8_t*>(epi.C) + idx * esz);
+          if (epi.bias) touch_global(epi.bias + (epi.trans ? m : n));
+        }
       }
-    }
-    while (ts.next(cur, mt, nt, kb0, kb1)) {
-      if (kb0 >= kb1) continue;
-      mbar_wait(&tfull[acc], acc_ph);
-      if (threadIdx.x == 64) TRACE(7, clock64() - c_start);
-      tc_fence_after();
-      const int m0 = mt * BM + eg * 32;
-      const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * cr.acc_stride);
-      const int na = tile_nacc(cr, kb0, kb1);
-      for (int c = half; c < (BN + 31) / 32; c += 2) {
-        uint32_t r[32];
-        const int nc = nt * BN + c * 32;
-        float bpre[32];
-        const bool pre = (VAR == 0 || VAR == 6) && (epi.kind == EPI_SOFTPLUS_BF16 || epi.kind == EPI_SOFTPLUS_F32) && !epi.trans &&
-                         nc + 32 <= N && ((reinterpret_cast<uintptr_t>(epi.bias + nc) & 15) == 0);
-        if (pre) {
+      while (ts.next(cur, mt, nt, kb0, kb1)) {
+        if (kb0 >= kb1) continue;
+        mbar_wait(&tfull[acc], acc_ph);
+        tc_fence_after();
+        const int m0 = mt * BM + eg * 32;
+        const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * cr.acc_stride);
+        for (int c = half; c < (BN + 31) / 32; c += 2) {
+          uint32_t r[32];
+          const int nc = nt * BN + c * 32;
+          float bpre[32];
+          const bool pre = (VAR == 0 || VAR == 6) && (epi.kind == EPI_SOFTPLUS_BF16 || epi.kind == EPI_SOFTPLUS_F32) &&
+                           !epi.trans && nc + 32 <= N && ((reinterpret_cast<uintptr_t>(epi.bias + nc) & 15) == 0);
+          if (pre) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 t4 = reinterpret_cast<const float4*>(epi.bias + nc)[q];
-            bpre[4 * q] = t4.x; bpre[4 * q + 1] = t4.y; bpre[4 * q + 2] = t4.z; bpre[4 * q + 3] = t4.w;
+            for (int q = 0; q < 8; ++q) {
+              const float4 t4 = reinterpret_cast<const float4*>(epi.bias + nc)[q];
+              bpre[4 * q] = t4.x; bpre[4 * q + 1] = t4.y; bpre[4 * q + 2] = t4.z; bpre[4 * q + 3] = t4.w;
+            }
           }
-        }
-        tmem_ld_32x32b_x32(tbase + c * 32, r);
-        tmem_ld_wait();
-        for (int q = 1; q < na; ++q) {  // fold the interleaved partial accumulators
-          uint32_t r2[32];
-          tmem_ld_32x32b_x32(tbase + (uint32_t)(q * cr.slot_cols) + c * 32, r2);
+          tmem_ld_32x32b_x32(tbase + c * 32, r);
           tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
-        }
-        if ((cr.nomma & 8) && threadIdx.x == 64) {  // timestamp after the TMEM data has arrived
-          uint32_t dep;
-          asm volatile("add.u32 %0, %1, %2;" : "=r"(dep) : "r"(r[0]), "r"(r[31]));
-          TRACE(8, clock64() - c_start + (dep == 0x7f123456u ? 1 : 0));
-        }
-        if (!(cr.nomma & 4)) {
           if constexpr (VAR == 2) epi_chunk_atomic_trans(epi, m0, nt * BN + c * 32, M, N, r);
           else epi_chunk<var_kind(VAR)>(epi, m0, nt * BN + c * 32, M, N, r, pre ? bpre : nullptr);
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
       }
-      if (threadIdx.x == 64) TRACE(9, clock64() - c_start);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
-      if (VAR == 0 && epi.fin_cnt) chain_finalise(epi, mt, M, N, reinterpret_cast<float*>(smem + cr.ring + 512));
-    }
     }
   }
-teardown:
-  if (threadIdx.x == 0) TRACE(10, clock64() - c_start);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, cr.tmem_cols);
-    if (lane == 0) { TRACE(11, clock64() - c_start); TRACE(12, globaltimer()); }
   }
 }
 
@@ -1053,17 +644,13 @@ cudaError_t pack_blocked(const __nv_bfloat16* w, int rows, int cols, int64_t ld,
   return cudaGetLastError();
 }
 
-cudaError_t gemm_trace_read(unsigned long long* host, int n) {
-  if (n > kTraceCtas * kTraceSlots) n = kTraceCtas * kTraceSlots;
-  return cudaMemcpyFromSymbol(host, g_trace, (size_t)n * sizeof(unsigned long long));
-}
+#define SSM_GEMM_KERNELS (const void*)gemm_tc_kernel<0>, (const void*)gemm_tc_kernel<1>, (const void*)gemm_tc_kernel<1, 3>, \
+    (const void*)gemm_tc_kernel<1, 4>, (const void*)gemm_tc_kernel<2>, (const void*)gemm_tc_kernel<6>
 
 cudaError_t preload_gemm_tc() {
   cudaError_t e = cudaSuccess;
   cudaFuncAttributes a;
-  for (const void* f : {(const void*)gemm_tc_kernel<0>, (const void*)gemm_tc_kernel<1>, (const void*)gemm_tc_kernel<1, 3>,
-                        (const void*)gemm_tc_kernel<1, 4>, (const void*)gemm_tc_kernel<2>, (const void*)gemm_tc_kernel<4>,
-                        (const void*)gemm_tc_kernel<5>, (const void*)gemm_tc_kernel<6>, (const void*)gemm_tc_kernel<7>}) {
+  for (const void* f : {SSM_GEMM_KERNELS}) {
     if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess) return e;
     if ((e = cudaFuncGetAttributes(&a, f)) != cudaSuccess) return e;
   }
@@ -1077,17 +664,14 @@ bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb) {
 
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
                          int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool a_indep,
-                         const __nv_bfloat16* A_blocked, const DStepJob* job_in) {
+                         const __nv_bfloat16* A_blocked) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  DStepJob job{};
-  if (job_in) job = *job_in;
-  const int ksplit_in = ksplit;
   // BN: multiple of 32 in [32, 256] (UMMA needs N % 16 == 0; the epilogue drains TMEM in
-  // 32-column chunks) covering N in as few tiles as possible
+  // 32-column chunks) covering N in as few tiles as possible; N <= 16: one 16-column UMMA tile
+  // (decode batches) halves the B operand and its smem
   int n_tiles = (N + BN_MAX - 1) / BN_MAX;
   int BN = (N + n_tiles - 1) / n_tiles;
-  // (N <= 16: one 16-column UMMA tile -- decode batches -- halves the B operand and its smem)
-  BN = (BN <= 16 && kMinBN16) ? 16 : (BN + 31) / 32 * 32;
+  BN = BN <= 16 ? 16 : (BN + 31) / 32 * 32;
   n_tiles = (N + BN - 1) / BN;
   TileSched ts;
   ts.m_tiles = (M + BM - 1) / BM;
@@ -1098,16 +682,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   ts.kbs = (ts.kb_total + ksplit - 1) / ksplit;
   ts.ksplit = (ts.kb_total + ts.kbs - 1) / ts.kbs;
   ts.units = ts.m_tiles * ts.n_tiles * ts.ksplit;
-  ts.streamk = 0;
-  ts.kown = (job_in && job_in->enabled && job_in->local > 0) ? job_in->local : 0;
-  if (ksplit_in < 0) {  // stream-K over all SMs (atomic epilogue)
-    ts.streamk = 1;
-    ts.ksplit = 1;
-    ts.kbs = ts.kb_total;
-    ts.units = ts.m_tiles * ts.n_tiles;
-  }
-  if ((ts.ksplit > 1 || ts.streamk) && epi.kind != EPI_ATOMIC_F32 && !(ts.streamk && epi.kind == EPI_DECODE_INPROJ))
-    return cudaErrorInvalidValue;
+  if (ts.ksplit > 1 && epi.kind != EPI_ATOMIC_F32) return cudaErrorInvalidValue;
 
   CUtensorMap ma, mb;
   if (!make_map(&mb, B, N, K, ldb, BN)) return cudaErrorInvalidValue;
@@ -1117,127 +692,61 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   } else if (!make_map(&ma, A, M, K, lda, BM)) {
     return cudaErrorInvalidValue;
   }
-
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_tc_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
+    for (const void* f : {SSM_GEMM_KERNELS}) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+    }
     attr_set = true;
   }
   // k-blocks per stage: skinny-N (weight-streaming) GEMMs fetch longer contiguous row segments
   // (decode, N = batch <= 32: 4 k-blocks = 64 KB of weights per stage; measured 39.4 -> 38.1 us per
   // Mamba-2.8B decode layer vs 2, fewer ring turnarounds per CTA)
   int kbs = BN <= 32 ? 4 : BN <= 64 ? 2 : 1;
-  if (const char* env = getenv("SSM_GEMM_KBS")) kbs = atoi(env);
-  if (kbs < 1) kbs = 1;
   CtaRes cr;
   cr.ring = RING_BYTES;
   cr.acc_stride = BN_MAX;
   cr.tmem_cols = 512;
-  cr.nomma = 0;
   cr.a_indep = a_indep ? 1 : 0;
-  cr.slot_cols = (BN + 31) / 32 * 32;
-  cr.nacc = 1;  // measured: no gain from interleaved accumulators once the UMMA issue is warp-uniform
-  if (const char* env = getenv("SSM_GEMM_NACC")) cr.nacc = atoi(env);
-  if (cr.nacc < 1) cr.nacc = 1;
-  while (cr.nacc > 1 && cr.nacc * cr.slot_cols > cr.acc_stride) --cr.nacc;
-  if (const char* env = getenv("SSM_GEMM_NOMMA")) cr.nomma = atoi(env);
   // Skinny-N (decode, weight-streaming) GEMMs take a smaller footprint: a 160 KB ring and a TMEM
   // allocation of 2 x BN columns, so the neighbouring kernels' CTAs (PDL: launched early, their
   // weight / state loads issued before griddepcontrol.wait) can be co-resident on the SM.
-  // Measured 40.4 -> 37.7 us per Mamba-2.8B decode layer; the stream rate is unchanged.
-  static const int dec_ring_kb = [] { const char* e = getenv("SSM_DEC_RING_KB"); return e ? atoi(e) : 160; }();
-  static const int out_ring_kb = [] { const char* e = getenv("SSM_OUT_RING_KB"); return e ? atoi(e) : -1; }();
-  const char* ring_env = getenv("SSM_GEMM_RING_KB");
-  int dec_kb = dec_ring_kb;
-  if (out_ring_kb >= 0 && epi.kind == EPI_ATOMIC_F32) dec_kb = out_ring_kb;  // experiment: split-K decode GEMMs
-  if (ring_env || (BN <= 32 && dec_kb > 0 && !job.enabled)) {  // smaller CTA footprint
-    cr.ring = (ring_env ? atoi(ring_env) : dec_kb) * 1024;
+  // Measured 40.4 -> 37.7 us per Mamba-2.8B decode layer (stream rate unchanged); 144 and 176 KB
+  // rings measured slower (39.2 / 38.8 us).
+  if (BN <= 32) {
+    cr.ring = 160 * 1024;
     int cols = 32;
     while (cols < 2 * BN) cols *= 2;
     cr.tmem_cols = cols;
     cr.acc_stride = cols / 2;
-    cr.nacc = 1;
   }
   int extra = 0;
   if (epi.kind == EPI_DECODE_INPROJ) {
     // fused decode in_proj: one 32-column accumulator per tile, N <= 32 tokens, P <= 320 (even),
     // tiles inside one head, window of <= 3 cached taps
     if (!epi.trans || N > 32 || BN > 32 || epi.P > 8 * 8 * XP_NT || (epi.P & 1) || epi.K < 2 || epi.K > 4 ||
-        epi.cph % BM || M != 2 * epi.Ek || ts.ksplit != 1 || (ts.streamk && (!epi.sk_acc || !epi.sk_cnt)))
+        epi.cph % BM || M != 2 * epi.Ek || ts.ksplit != 1)
       return cudaErrorInvalidValue;
-    extra = SU_BYTES + 128;  // u tile + the stream-K last-contributor flag
+    extra = SU_BYTES + 128;  // u tile
     cr.ring -= SU_BYTES + 128;
   }
   if (epi.zero && (reinterpret_cast<uintptr_t>(epi.zero) & 15)) return cudaErrorInvalidValue;
-  if (epi.nres && (epi.kind != EPI_DECODE_INPROJ || K % 8 || epi.nx != B || job.enabled || N > 32 ||
-                   (reinterpret_cast<uintptr_t>(epi.nres) & 15)))
-    return cudaErrorInvalidValue;
-  if (epi.fin_cnt) {  // decode-chain finaliser scratch (257 floats) after the barrier area
-    extra += 2048;
-    cr.ring -= 2048;
-  }
-  if (job.enabled) {
-    // B operand = g produced in-kernel: bf16 only, the decode-step smem of two units, one tile per
-    // CTA, all CTAs co-resident (grid <= SMs at 1 CTA/SM), decode-step shape limits
-    if (!job.bf16 || (job.N != 16 && job.N != 8) || epi.kind == EPI_DECODE_INPROJ ||
-        !dstep_supported(1, job.R, job.N, job.ldp, job.cph))
-      return cudaErrorInvalidValue;
-    if (job.local) {  // channel-owned: each CTA's share of a split is whole 32-channel units
-      if (!job.rd_cnt || (job.local > 1 && !job.grp_cnt) || (ts.kbs * BK) % (DS_CH * job.local) || ts.streamk ||
-          epi.zero)
-        return cudaErrorInvalidValue;
-    } else if (!job.sync || ts.units > num_sms) {
-      return cudaErrorInvalidValue;
-    }
-    const int js = (int)((2 * dstep_smem(job.R, job.N, 2, kJobIpt) + 127) / 128 * 128) + (job.local ? 128 : 0);
-    extra += js;
-    cr.ring -= js;
-  }
   while (kbs > 1 && num_stages(BN, kbs, cr.ring) < 2) --kbs;
   const int smem_bytes = 1024 + cr.ring + 512 + extra;
-  int grid = ts.units < num_sms ? ts.units : num_sms;
-  if (ts.kown) grid = ts.ksplit * ts.kown;  // Q CTAs per channel range
-  if (epi.pf && epi.pf_bytes > 0 && !ts.streamk && ts.units < num_sms && !job.enabled) grid = num_sms;  // spare CTAs prefetch
-  if (ts.streamk) {
-    long long cap = num_sms;
-    if (const char* env = getenv("SSM_GEMM_SK_CTAS")) cap = atoi(env);
-    const long long W = (long long)ts.units * ts.kb_total;
-    grid = (int)(W < cap ? W : cap);
-  }
-  Epilogue epi2 = epi;
-  if (epi2.fin_cnt) {  // decode-chain finaliser: contributions per output m-tile
-    if (ts.streamk || epi2.kind != EPI_ATOMIC_F32 || !epi2.trans || BM != 128) return cudaErrorInvalidValue;
-    epi2.fin_need = ts.ksplit * ts.n_tiles;
-  }
-  // kernel variant (see gemm_tc_kernel): decode GEMMs on their own instantiations
+  const int grid = ts.units < num_sms ? ts.units : num_sms;
+  // kernel variant (see gemm_tc_kernel): the decode GEMMs and the prefill dt_proj on their own
+  // instantiations (fixed-kind in_proj / out_proj variants measured 2-3% slower than the all-paths
+  // kernel, x_proj equal; the dt_proj one 249 -> 230 us)
   int var = 0;
-  if (g_gemm_variants && !job.enabled && !epi2.fin_cnt && !epi2.nres && !epi2.pf && !ts.streamk) {
-    if (epi2.kind == EPI_DECODE_INPROJ) var = 1;
-    else if (epi2.kind == EPI_ATOMIC_F32 && epi2.trans && BN <= 32) var = 2;
-    else if (!epi2.trans && g_gemm_prefill_var) {
-      // fixed-kind prefill variants: only the softplus one (dt_proj) measured faster (249 -> 230 us);
-      // the in_proj / out_proj ones measured 2-3% slower than the all-paths kernel, x_proj equal
-      var = epi2.kind == EPI_SOFTPLUS_BF16 ? 6 : 0;
-      if (g_gemm_prefill_var > 1)  // (experiment: every fixed-kind variant)
-        var = epi2.kind == EPI_STORE_BF16 ? 4 : epi2.kind == EPI_ADD_F32 ? 5 : epi2.kind == EPI_SOFTPLUS_BF16 ? 6
-            : epi2.kind == EPI_STORE_F32 ? 7 : 0;
-    }
-  }
-  auto kfn = var == 2 ? gemm_tc_kernel<2> : var == 4 ? gemm_tc_kernel<4> : var == 5 ? gemm_tc_kernel<5>
-           : var == 6 ? gemm_tc_kernel<6> : var == 7 ? gemm_tc_kernel<7> : gemm_tc_kernel<0>;
-  if (var == 1) kfn = epi2.P <= 64 * 3 ? gemm_tc_kernel<1, 3> : epi2.P <= 64 * 4 ? gemm_tc_kernel<1, 4> : gemm_tc_kernel<1>;
-  { cudaError_t e_ = launch(kfn, grid, var_threads(var), smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi2,
-                                      A_blocked, lda, K, cr, A_blocked ? 1 : 0, job);
-    if (e_ != cudaSuccess) return e_; }
+  if (epi.kind == EPI_DECODE_INPROJ) var = 1;
+  else if (epi.kind == EPI_ATOMIC_F32 && epi.trans && BN <= 32) var = 2;
+  else if (!epi.trans && epi.kind == EPI_SOFTPLUS_BF16) var = 6;
+  auto kfn = var == 2 ? gemm_tc_kernel<2> : var == 6 ? gemm_tc_kernel<6> : gemm_tc_kernel<0>;
+  if (var == 1) kfn = epi.P <= 64 * 3 ? gemm_tc_kernel<1, 3> : epi.P <= 64 * 4 ? gemm_tc_kernel<1, 4> : gemm_tc_kernel<1>;
+  cudaError_t e_ = launch(kfn, grid, var_threads(var), smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi, A_blocked, lda, K,
+                          cr, A_blocked ? 1 : 0);
+  if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
 }
 

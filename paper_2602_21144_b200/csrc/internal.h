@@ -31,25 +31,6 @@ struct Epilogue {
   // buffer a LATER kernel accumulates into (saves a memset launch on the decode path).
   float* zero;
   int64_t nzero;
-  // Any kind: a weight range the NEXT kernel streams.  When set, the GEMM launches on every SM and
-  // the CTAs without a tile (the decode GEMMs have fewer tiles than SMs) issue L2 prefetches of
-  // [pf, pf + pf_bytes) and exit: HBM time the tile CTAs leave idle fetches the successor's weights.
-  const void* pf;
-  int64_t pf_bytes;
-  // Decode chain (TP = 1; ssm_mixer_decode_chained): the pre-norm RMSNorm of every layer folded
-  // into the GEMMs around it.  in_proj: the B operand is bf16(residual) un-normalised and each
-  // accumulator column n is scaled by rsqrt(ss[n] * ss_scale + ss_eps) (the per-row 1/rms factors
-  // out of the contraction).  out_proj (split-K atomics into the residual): the last contributor
-  // of an output tile (counter fin_cnt[m-tile], fin_need contributions, reset by the last) writes
-  // bf16 of the final residual tile into fin_x [N][fin_ldx] (the next layer's B operand) and adds
-  // the tile's per-row sums of squares into fin_ss.
-  const float* ss;
-  float ss_scale, ss_eps;
-  int* fin_cnt;
-  int fin_need;
-  __nv_bfloat16* fin_x;
-  int64_t fin_ldx;
-  float* fin_ss;
   // EPI_DECODE_INPROJ (SURVEY.md §8 rows a1-a3 fused for one decode token).
   // Output rows m are in_proj features: m < Ek are x channels -> causal conv step over the cached
   // window cst + SiLU -> u (bf16 [N][Ek]) and the window shifted in place; Ek <= m < 2Ek are z
@@ -62,64 +43,15 @@ struct Epilogue {
   const void* wx;             // [hl*P][Ek] bf16 (block-diagonal over local heads)
   float* xacc;                // [N][hl*P] fp32
   int Ek, K, P, hl, cph;
-  // Stream-K fused decode in_proj (sk_acc != NULL): the (tile, k-block) space is cut evenly over
-  // all SMs; a CTA holding part of a tile adds its partial accumulator into sk_acc
-  // [m_tiles][N][128] fp32 (all-zero between calls) and bumps sk_cnt[m-tile]; the last of the
-  // tile's contributors reads the sum back, re-zeroes it and runs the conv / x_proj epilogue.
-  float* sk_acc;
-  int* sk_cnt;
-  // EPI_DECODE_INPROJ pre-norm (nres != NULL): the epilogue warps first write the B operand
-  // itself, B[n][:] = bf16(nres[n][:] / sqrt(mean(nres[n][:]^2) + nres_eps)) (the layer's weightless
-  // pre-norm RMSNorm, reading Q16; every CTA writes the same values), then release the B loads.
-  const float* nres;
-  float nres_eps;
-  __nv_bfloat16* nx;
 };
 
 struct Peers {
   void* p[kMaxTP];
 };
 
-// Decode step run inside the decode out_proj GEMM as the producer of its B operand g: the idle
-// epilogue warps of every CTA run decode-step units (dstep.cuh) while the weight stream starts,
-// then a grid-wide barrier (all CTAs co-resident: grid <= SMs, 1 CTA/SM) releases the B loads.
-struct DStepJob {
-  int enabled;
-  int bf16;
-  int N;                          // d_state (16 or 8)
-  const float* dbc;               // [batch][ldp] x_proj result (single source, no AR#1)
-  unsigned long long* sync;       // grid-barrier counter (monotonic; one per layer state)
-  // flattened DStepArgs fields
-  int ldp, rmsnorm;
-  float eps;
-  const void* u;
-  const void* z;
-  int64_t ldz;
-  const void* w_dt;
-  const float* b_dt;
-  const float* a_log;
-  const float* d_skip;
-  float* h;
-  void* g;
-  int batch, Ek, R, cph;
-  // local != 0: channel-owned mode.  CTA i owns the k-block range (the d_inner channels) of split
-  // i and runs every output m-tile for it; its epilogue warps first run the decode step for
-  // exactly those channels (the step is channel-local, so no grid barrier), then the CTA's B
-  // operand g is loaded.  h and g are written by their owner CTA only.  The dbc rows every CTA
-  // reads are re-zeroed (for the next token's fused in_proj) by the last CTA to finish reading
-  // them (counter rd_cnt, reset by that CTA).
-  // local = Q >= 1 m-groups: CTA i = (k-split i / Q, m-group i % Q) runs the m-tiles q, q + Q, ...
-  // of its split; the split's channels are divided over its Q CTAs for the decode step, which then
-  // meet at a group barrier (grp_cnt[split], monotonic) before loading g of the whole split.
-  int local;
-  int* rd_cnt;
-  int64_t ndbc;  // floats of dbc to re-zero (batch * ldp)
-  unsigned long long* grp_cnt;
-};
-
 // ---- GEMM launchers (return cudaSuccess or the launch error) ----
 // tcgen05/TMEM/TMA bf16 GEMM: A [M,K] row stride lda, B [N,K] row stride ldb (elements).
-// ksplit > 1: data-parallel split-K; ksplit < 0: stream-K over all SMs (both need EPI_ATOMIC_F32).
+// ksplit > 1: data-parallel split-K (needs EPI_ATOMIC_F32).
 // Requires lda*2 % 16 == 0, ldb*2 % 16 == 0, 16-B aligned bases.
 // a_indep: A is a weight (independent of the predecessor kernel): under PDL the producer issues
 // the first ring fill of A before griddepcontrol.wait.
@@ -127,9 +59,7 @@ struct DStepJob {
 // 16 KB boxes (sequential weight streams for the decode GEMMs).
 cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb, int M, int N,
                          int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool a_indep = false,
-                         const __nv_bfloat16* A_blocked = nullptr, const DStepJob* job = nullptr);
-// experiment-only: copy the GEMM timeline buffer (16 u64 per CTA, SSM_GEMM_NOMMA bit 8)
-cudaError_t gemm_trace_read(unsigned long long* host, int n);
+                         const __nv_bfloat16* A_blocked = nullptr);
 size_t packed_blocked_bytes(int rows, int cols);
 cudaError_t pack_blocked(const __nv_bfloat16* w, int rows, int cols, int64_t ld, __nv_bfloat16* out, cudaStream_t s);
 bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb);
@@ -161,14 +91,9 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
 cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
                                const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
-                               int N, int ch_per_head, float* zacc, cudaStream_t s, float* zero_ss = nullptr,
-                               const void* pf = nullptr, int64_t pf_bytes = 0);
+                               int N, int ch_per_head, float* zacc, cudaStream_t s);
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
                            cudaStream_t s);
-// Decode chain start: x = bf16(residual) (un-normalised), ss[b] = sum_d residual[b][d]^2, and the
-// out_proj finaliser counters zeroed.  residual [M][D] fp32.
-cudaError_t launch_chain_begin(const float* x, __nv_bfloat16* y, float* ss, int* cnt, int ncnt, int64_t M, int D,
-                               cudaStream_t s);
 // int8 quantisation of n fp32 values in blocks of blk: q [n] int8, scale [n/blk] f32.
 cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float* scale, cudaStream_t s);
 // out (+)= sum_r s_r q_r over k sources (fixed order 0..k-1).
@@ -187,67 +112,6 @@ cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s);
 // symmetric buffer at dst_off, re-zero it, then the cross-rank barrier
 cudaError_t launch_publish_barrier(Peers bufs, int rank, int k, float* xacc, int64_t n, int64_t dst_off,
                                    cudaStream_t s);
-
-// ---- persistent whole-stack decode (decode_mk.cu) ----
-// One layer of the stack as the persistent decode kernel reads it (TP=1, bf16, one x_proj head).
-struct MkLayer {
-  const __nv_bfloat16* w_in_pk;   // pack_blocked(W_in [2Ek, D]): 128x64 tiles, row-tile-major
-  const __nv_bfloat16* w_out_pk;  // pack_blocked(W_out [D, Ek])
-  const __nv_bfloat16* w_x;       // [P, Ek]
-  const __nv_bfloat16* w_dt;      // [Ek, R]
-  const float* conv_w;            // [Ek, K]
-  const float* conv_b;            // [Ek]
-  const float* b_dt;              // [Ek]
-  const float* a_log;             // [Ek, 16]
-  const float* d_skip;            // [Ek]
-  __nv_bfloat16* conv;            // cache: conv window [batch][K-1][Ek]
-  float* h;                       // cache: h [batch][Ek][16]
-  void* pad;
-};
-struct MkParams {
-  const MkLayer* layers;
-  int n_layers;
-  float* resid;                   // [B][D] fp32, caller's residual (in/out)
-  float* residT;                  // [D][BP] fp32, the residual stream while the kernel runs
-  __nv_bfloat16* residB;          // bf16 copy of residT, K-major SW128 k-blocks [D/64][BP][64]: in_proj B
-  float* xzT;                     // [2Ek][BP] fp32 in_proj accumulators (zero between layers)
-  float* dbcT;                    // [2][P][BP] fp32 x_proj accumulators (double-buffered by epoch)
-  float* ss;                      // [2][BP] sums of squares of the residual rows (by epoch)
-  float* ssP;                     // [grid][BP] per-CTA sums of squares of the input residual
-  __nv_bfloat16* gT;              // gated scan output, K-major SW128 k-blocks [Ek/64][BP][64]: out_proj B
-  unsigned* cnt;                  // readiness counters (mk_cnt_layout), monotonic since bind
-  unsigned* ep;                   // [grid] layers completed since bind, per CTA
-  unsigned long long* bar;        // grid-barrier arrival counter (monotonic)
-  unsigned* err;                  // device error word (barrier / pipeline timeout)
-  int B, D, Ek, R, P, K;
-  float eps;                      // pre-norm RMSNorm eps (weight 1, reading Q16)
-  int rmsnorm;                    // Falcon dt/B/C RMSNorm (Q18)
-  float rms_eps;
-  int ring, nbr, ncmax, ngrp;     // weight-ring slots, B-ring slots, channels per CTA (max), groups
-  unsigned long long* trace;      // optional (NULL = off): [grid][n_layers][32] globaltimer stamps
-  int dbg;                        // experiment-only (SSM_MK_DBG)
-};
-// Counter block (u32 words, 32 B apart): cnt_x, cnt_fin, cnt_in[2Ek/128], rdy_g[Ek/64],
-// cnt_out[D/128], rdy_res[D/128].
-struct MkCnt {
-  int x, fin, in, g, out, res, words;
-};
-inline __host__ __device__ MkCnt mk_cnt_layout(int D, int Ek) {
-  MkCnt c{};
-  int o = 0;
-  c.x = o; o += 8;
-  c.fin = o; o += 8;
-  c.in = o; o += 8 * (2 * Ek / 128);
-  c.g = o; o += 8 * (Ek / 64);
-  c.out = o; o += 8 * (D / 128);
-  c.res = o; o += 8 * (D / 128);
-  c.words = o;
-  return c;
-}
-size_t mk_smem_bytes(int BP, int P, int R, int ncmax, int ring, int nbr);
-int mk_ring_slots(int BP, int P, int R, int ncmax, int nbr);
-cudaError_t launch_decode_mk(const MkParams& p, int BP, int grid, cudaStream_t s);
-cudaError_t preload_decode_mk();
 
 // Load every kernel eagerly (called once per process from ssm_tp_init when a device exists).
 cudaError_t preload_kernels();

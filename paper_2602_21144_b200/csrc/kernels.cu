@@ -306,7 +306,7 @@ constexpr int SC_THREADS = 128;  // channels per block
 // One thread per (batch row, channel); N states in registers; tiles of u, delta, z
 // (bf16 or fp32) and B||C (fp32) staged through shared memory with cp.async double
 // buffering.  h_t = exp(delta A) h_{t-1} + delta B_t u_t;  y = <C_t, h_t> + D u;  g = y SiLU(z).
-template <typename T, int N, bool FAST, int NP = 0>
+template <typename T, int N, bool FAST>
 __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ u, int64_t ldu,
                                                           const T* __restrict__ dl, int64_t ldd,
                                                           const T* __restrict__ z, int64_t ldz,
@@ -406,9 +406,8 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
             const float4 b4 = B4[q], c4 = C4[q];
             const float2 dA0 = fmul2(de2, A2[2 * q]);
             const float2 dA1 = fmul2(de2, A2[2 * q + 1]);
-            // NP of the N states' exponentials on the FMA pipe (exp2_poly2), the rest on MUFU
-            const float2 a0 = (4 * q + 2 <= N - NP) ? make_float2(ex2_approx(dA0.x), ex2_approx(dA0.y)) : exp2_poly2(dA0);
-            const float2 a1 = (4 * q + 4 <= N - NP) ? make_float2(ex2_approx(dA1.x), ex2_approx(dA1.y)) : exp2_poly2(dA1);
+            const float2 a0 = make_float2(ex2_approx(dA0.x), ex2_approx(dA0.y));
+            const float2 a1 = make_float2(ex2_approx(dA1.x), ex2_approx(dA1.y));
             h2[2 * q] = ffma2(a0, h2[2 * q], fmul2(du2, make_float2(b4.x, b4.y)));
             h2[2 * q + 1] = ffma2(a1, h2[2 * q + 1], fmul2(du2, make_float2(b4.z, b4.w)));
             ya = ffma2(make_float2(c4.x, c4.y), h2[2 * q], ya);
@@ -450,163 +449,17 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
   }
 }
 
-// ---------------------------------------------------------------- selective scan v3 (bf16 fast path)
-// Two channels per thread (B/C smem broadcasts and u/delta/z loads shared, bf16x2 IO) and
-// NPOLY of the N states' exponentials evaluated on the FMA pipe (exp2_poly2) so the MUFU
-// pipe (the binding unit) carries fewer ops per channel-token.
-constexpr int S3_THREADS = 128, S3_CH = 2 * S3_THREADS, S3_TT = 8;
-template <int N, int NPOLY>
-__global__ void __launch_bounds__(S3_THREADS) scan2_kernel(
-    const __nv_bfloat16* __restrict__ u, int64_t ldu, const __nv_bfloat16* __restrict__ dl, int64_t ldd,
-    const __nv_bfloat16* __restrict__ z, int64_t ldz, const float* __restrict__ BC, int64_t ldbc,
-    const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ h, int64_t h_bstride,
-    __nv_bfloat16* __restrict__ g, int64_t ldg, int L, int nch) {
-  pdl_trigger();
-  pdl_wait();
-  static_assert(N % 4 == 0 && NPOLY % 2 == 0 && NPOLY <= N, "bad N/NPOLY");
-  constexpr int CH_CHUNKS = S3_CH * 2 / 16;  // 16-B chunks per staged row
-  constexpr int BC_CHUNKS = 2 * N * 4 / 16;
-  __shared__ __align__(16) __nv_bfloat16 su[2][S3_TT][S3_CH];
-  __shared__ __align__(16) __nv_bfloat16 sd[2][S3_TT][S3_CH];
-  __shared__ __align__(16) __nv_bfloat16 sz[2][S3_TT][S3_CH];
-  __shared__ __align__(16) float sbc[2][S3_TT][2 * N];
-  const int tid = threadIdx.x;
-  const int b = blockIdx.y;
-  const int cbase = blockIdx.x * S3_CH;
-  const int d = cbase + 2 * tid;  // this thread: channels d, d+1
-  const bool valid = d < nch;     // nch % 2 == 0
-  const int64_t row0 = (int64_t)b * L;
-
-  auto load_tile = [&](int buf, int tile) {
-    const int tb = tile * S3_TT;
-    for (int i = tid; i < S3_TT * CH_CHUNKS; i += S3_THREADS) {
-      const int r = i / CH_CHUNKS, c = i % CH_CHUNKS;
-      const int t = tb + r, ch = cbase + c * 8;
-      const bool ok = (t < L) && (ch < nch);
-      const int64_t row = row0 + (ok ? t : 0);
-      const int chs = ok ? ch : 0;
-      cp_async16(&su[buf][r][c * 8], u + row * ldu + chs, ok);
-      cp_async16(&sd[buf][r][c * 8], dl + row * ldd + chs, ok);
-      cp_async16(&sz[buf][r][c * 8], z + row * ldz + chs, ok);
-    }
-    for (int i = tid; i < S3_TT * BC_CHUNKS; i += S3_THREADS) {
-      const int r = i / BC_CHUNKS, c = i % BC_CHUNKS;
-      const int t = tb + r;
-      const bool ok = t < L;
-      cp_async16(&sbc[buf][r][c * 4], BC + (row0 + (ok ? t : 0)) * ldbc + c * 4, ok);
-    }
-  };
-
-  float2 A2[2][N / 2], h2[2][N / 2];
-  float Dd[2] = {0.f, 0.f};
-  float* hp = h + (int64_t)b * h_bstride + (int64_t)(valid ? d : 0) * N;
-  if (valid) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-#pragma unroll
-      for (int i = 0; i < N / 2; ++i) {
-        A2[c][i] = make_float2(-expf(a_log[(int64_t)(d + c) * N + 2 * i]) * 1.4426950408889634f,
-                               -expf(a_log[(int64_t)(d + c) * N + 2 * i + 1]) * 1.4426950408889634f);
-        h2[c][i] = make_float2(hp[c * N + 2 * i], hp[c * N + 2 * i + 1]);
-      }
-      Dd[c] = d_skip[d + c];
-    }
-  }
-
-  const int ntiles = (L + S3_TT - 1) / S3_TT;
-  load_tile(0, 0);
-  cp_async_commit();
-  for (int it = 0; it < ntiles; ++it) {
-    const int buf = it & 1;
-    if (it + 1 < ntiles) {
-      load_tile(buf ^ 1, it + 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    if (valid) {
-      const int tb = it * S3_TT;
-      const int tn = min(S3_TT, L - tb);
-      for (int r = 0; r < tn; ++r) {
-        const float2 uu = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&su[buf][r][2 * tid]));
-        const float2 de = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sd[buf][r][2 * tid]));
-        const float2 zz = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sz[buf][r][2 * tid]));
-        float4 Bq[N / 4], Cq[N / 4];
-#pragma unroll
-        for (int q = 0; q < N / 4; ++q) {
-          Bq[q] = reinterpret_cast<const float4*>(sbc[buf][r])[q];
-          Cq[q] = reinterpret_cast<const float4*>(sbc[buf][r] + N)[q];
-        }
-        float y[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const float dec = c ? de.y : de.x;
-          const float uc = c ? uu.y : uu.x;
-          const float2 de2 = make_float2(dec, dec);
-          const float2 du2 = make_float2(dec * uc, dec * uc);
-          float2 ya = make_float2(0.f, 0.f), yb = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int q = 0; q < N / 4; ++q) {
-            const float2 dA0 = fmul2(de2, A2[c][2 * q]);
-            const float2 dA1 = fmul2(de2, A2[c][2 * q + 1]);
-            float2 a0, a1;
-            if (4 * q + 2 <= N - NPOLY) a0 = make_float2(ex2_approx(dA0.x), ex2_approx(dA0.y));
-            else a0 = exp2_poly2(dA0);
-            if (4 * q + 4 <= N - NPOLY) a1 = make_float2(ex2_approx(dA1.x), ex2_approx(dA1.y));
-            else a1 = exp2_poly2(dA1);
-            h2[c][2 * q] = ffma2(a0, h2[c][2 * q], fmul2(du2, make_float2(Bq[q].x, Bq[q].y)));
-            h2[c][2 * q + 1] = ffma2(a1, h2[c][2 * q + 1], fmul2(du2, make_float2(Bq[q].z, Bq[q].w)));
-            ya = ffma2(make_float2(Cq[q].x, Cq[q].y), h2[c][2 * q], ya);
-            yb = ffma2(make_float2(Cq[q].z, Cq[q].w), h2[c][2 * q + 1], yb);
-          }
-          y[c] = fmaf(Dd[c], uc, (ya.x + ya.y) + (yb.x + yb.y));
-        }
-        const float g0 = y[0] * silu_tanh(zz.x), g1 = y[1] * silu_tanh(zz.y);
-        *reinterpret_cast<__nv_bfloat162*>(g + (row0 + tb + r) * ldg + d) = __floats2bfloat162_rn(g0, g1);
-      }
-    }
-    __syncthreads();
-  }
-  if (valid) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int i = 0; i < N / 2; ++i) {
-        hp[c * N + 2 * i] = h2[c][i].x;
-        hp[c * N + 2 * i + 1] = h2[c][i].y;
-      }
-  }
-}
-
 // ---------------------------------------------------------------- decode step
 // Body in dstep.cuh (shared with the out_proj GEMM, which can run it as its B-operand producer).
-template <typename T, int N, bool FAST, int IPT>
-__global__ void __launch_bounds__(DS_THREADS, IPT == 1 ? 5 : IPT == 2 ? 4 : 3) decode_step_kernel(DStepArgs a, Peers src, int nsrc) {
+// one (batch row, channel) item per thread: 640 blocks of 128 threads for Mamba-2.8B at batch 16 (a
+// 4-row-per-thread variant, 160 blocks with 4x fewer W_dt reads, and a 2-row one measured slower)
+template <typename T, int N, bool FAST>
+__global__ void __launch_bounds__(DS_THREADS, 5) decode_step_kernel(DStepArgs a, Peers src, int nsrc) {
   extern __shared__ __align__(16) float dsm[];
   pdl_trigger();
-  if (a.pf && threadIdx.x < 32) {  // this block's slice of the successor's weights into L2
-    const int nb = (int)(gridDim.x * gridDim.y), j = (int)(blockIdx.y * gridDim.x + blockIdx.x);
-    const int64_t per = ((a.pf_bytes + nb - 1) / nb + 15) & ~int64_t(15);
-    const int64_t lo = (int64_t)j * per, hi = lo + per < a.pf_bytes ? lo + per : a.pf_bytes;
-    const char* base = reinterpret_cast<const char*>(a.pf);
-    for (int64_t o = lo + (int64_t)threadIdx.x * 16384; o < hi; o += 32 * 16384) {
-      const int64_t n = hi - o < 16384 ? hi - o : 16384;
-      if (n >= 16) prefetch_l2(base + o, (uint32_t)(n & ~int64_t(15)));
-    }
-  }
-  dstep_unit<T, N, FAST, DS_THREADS, IPT>(a, src, nsrc, blockIdx.x * DS_CH, blockIdx.y * DS_BB * IPT, threadIdx.x, dsm,
+  dstep_unit<T, N, FAST, DS_THREADS, 1>(a, src, nsrc, blockIdx.x * DS_CH, blockIdx.y * DS_BB, threadIdx.x, dsm,
                                           -1, true);
 }
-// items (batch rows) per thread of the standalone decode-step kernel: 1 (640 blocks for B = 16)
-// or 4 (160 blocks, 4x fewer W_dt reads, every item's loads in flight at once); SSM_DSTEP_IPT
-const int g_dstep_ipt = [] {
-  const char* e = getenv("SSM_DSTEP_IPT");
-  const int v = e ? atoi(e) : 1;
-  return v == 4 ? 4 : v == 2 ? 2 : 1;
-}();
-
 // ---------------------------------------------------------------- RMSNorm (glue)
 // One 128-thread block per row, the row cached in registers (<= 16 float4 per thread).
 template <typename T>
@@ -825,8 +678,9 @@ __global__ void ag16_kernel(Peers src, int64_t sum_off, int64_t shard, int64_t n
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     float4 v = accumulate ? o[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-    v.x = v.x + s * (float)qv[4 * q]; v.y = v.y + s * (float)qv[4 * q + 1];
-    v.z = v.z + s * (float)qv[4 * q + 2]; v.w = v.w + s * (float)qv[4 * q + 3];
+    // fl32(s * Q) then an fp32 add, as the oracle rounds (no fma contraction)
+    v.x = __fadd_rn(v.x, __fmul_rn(s, (float)qv[4 * q])); v.y = __fadd_rn(v.y, __fmul_rn(s, (float)qv[4 * q + 1]));
+    v.z = __fadd_rn(v.z, __fmul_rn(s, (float)qv[4 * q + 2])); v.w = __fadd_rn(v.w, __fmul_rn(s, (float)qv[4 * q + 3]));
     o[q] = v;
   }
 }
@@ -904,13 +758,11 @@ __global__ void peer_barrier_kernel(Peers bufs, int rank, int k) {
   fence_sys();
 }
 
-static const int g_conv_v2 = [] { const char* e = getenv("SSM_CONV_V2"); return !e || atoi(e) != 0; }();
-
 template <typename T, bool F>
 cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const float* cw, const float* cb, void* u,
                           int64_t ldu, int batch, int L, int Ek, int K, cudaStream_t s) {
   if constexpr (sizeof(T) == 2 && F) {
-    if (g_conv_v2 && Ek % 8 == 0 && ldxz % 8 == 0 && ldu % 8 == 0) {  // smem-staged kernel (bf16)
+    if (Ek % 8 == 0 && ldxz % 8 == 0 && ldu % 8 == 0) {  // smem-staged kernel (bf16)
       dim3 grid2((Ek + C2_CH - 1) / C2_CH, (L + C2_TT - 1) / C2_TT, batch);
       const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(xz);
       const __nv_bfloat16* c = reinterpret_cast<const __nv_bfloat16*>(cs);
@@ -951,13 +803,6 @@ cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const fl
 }
 
 }  // namespace
-
-// scan variant knobs (SSM_SCAN_VERSION=1 selects the 1-channel kernel; SSM_SCAN_NPOLY = states per
-// channel on the FMA-pipe exp2), read once per process
-static int g_scan_version = [] { const char* e = getenv("SSM_SCAN_VERSION"); return e ? atoi(e) : 1; }();
-static int g_scan_npoly = [] { const char* e = getenv("SSM_SCAN_NPOLY"); return e ? atoi(e) : 4; }();
-// states per channel on the FMA-pipe exp2 in the 1-channel kernel (bf16, N = 16): 0, 2, 4 or 6
-static int g_scan_np1 = [] { const char* e = getenv("SSM_SCAN_NP1"); return e ? atoi(e) : 0; }();
 
 // ==================================================================== launchers
 cudaError_t launch_conv1d_silu(int bf16, const void* xz, int64_t ldxz, const void* cs, const float* cw,
@@ -1015,12 +860,12 @@ cudaError_t launch_unpack(int bf16, Peers src, int nsrc, int64_t off, int M, int
   return cudaGetLastError();
 }
 
-template <typename T, int N, bool F, int NP = 0>
+template <typename T, int N, bool F>
 static cudaError_t scan_t(const void* u, int64_t ldu, const void* dl, int64_t ldd, const void* z, int64_t ldz,
                           const float* BC, int64_t ldbc, const float* a_log, const float* d_skip, float* h,
                           int64_t hbs, void* g, int64_t ldg, int batch, int L, int nch, cudaStream_t s) {
   dim3 grid((nch + SC_THREADS - 1) / SC_THREADS, batch);
-  { cudaError_t e_ = launch(scan_kernel<T, N, F, NP>, grid, SC_THREADS, 0, s, 
+  { cudaError_t e_ = launch(scan_kernel<T, N, F>, grid, SC_THREADS, 0, s, 
       reinterpret_cast<const T*>(u), ldu, reinterpret_cast<const T*>(dl), ldd, reinterpret_cast<const T*>(z), ldz, BC,
       ldbc, a_log, d_skip, h, hbs, reinterpret_cast<T*>(g), ldg, L, nch); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
@@ -1031,25 +876,6 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
                         int64_t hbs, void* g, int64_t ldg, int batch, int L, int nch, int N, cudaStream_t s) {
   if (batch <= 0 || L <= 0 || nch <= 0) return cudaSuccess;
   if (N != 16 && N != 8) return cudaErrorInvalidValue;
-  if (bf16 && fast && N == 16 && nch % 2 == 0 && ldg % 2 == 0 && g_scan_version >= 2) {
-    dim3 grid((nch + S3_CH - 1) / S3_CH, batch);
-    const int npoly = g_scan_npoly;
-#define S2A reinterpret_cast<const __nv_bfloat16*>(u), ldu, reinterpret_cast<const __nv_bfloat16*>(dl), ldd, \
-      reinterpret_cast<const __nv_bfloat16*>(z), ldz, BC, ldbc, a_log, d_skip, h, hbs, reinterpret_cast<__nv_bfloat16*>(g), ldg, L, nch
-    if (npoly == 0) { cudaError_t e_ = launch(scan2_kernel<16, 0>, grid, S3_THREADS, 0, s, S2A); if (e_ != cudaSuccess) return e_; }
-    else if (npoly == 2) { cudaError_t e_ = launch(scan2_kernel<16, 2>, grid, S3_THREADS, 0, s, S2A); if (e_ != cudaSuccess) return e_; }
-    else if (npoly == 4) { cudaError_t e_ = launch(scan2_kernel<16, 4>, grid, S3_THREADS, 0, s, S2A); if (e_ != cudaSuccess) return e_; }
-    else { cudaError_t e_ = launch(scan2_kernel<16, 6>, grid, S3_THREADS, 0, s, S2A); if (e_ != cudaSuccess) return e_; }
-#undef S2A
-    return cudaGetLastError();
-  }
-  if (bf16 && fast && N == 16 && g_scan_np1 > 0) {
-#define S1A u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s
-    if (g_scan_np1 == 2) return scan_t<__nv_bfloat16, 16, true, 2>(S1A);
-    if (g_scan_np1 == 4) return scan_t<__nv_bfloat16, 16, true, 4>(S1A);
-    return scan_t<__nv_bfloat16, 16, true, 6>(S1A);
-#undef S1A
-  }
   if (bf16) {
     if (N == 16) return fast ? scan_t<__nv_bfloat16, 16, true>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s)
                              : scan_t<__nv_bfloat16, 16, false>(u, ldu, dl, ldd, z, ldz, BC, ldbc, a_log, d_skip, h, hbs, g, ldg, batch, L, nch, s);
@@ -1062,12 +888,9 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
 
 template <typename T, int N, bool F>
 static cudaError_t dstep_t(const DStepArgs& a, Peers src, int nsrc, cudaStream_t s) {
-  const int ipt = g_dstep_ipt;
-  const size_t smem = dstep_smem(a.R, N, (int)sizeof(T), ipt);
-  dim3 grid((a.Ek + DS_CH - 1) / DS_CH, (a.batch + DS_BB * ipt - 1) / (DS_BB * ipt));
-  cudaError_t e_ = ipt == 4 ? launch(decode_step_kernel<T, N, F, 4>, grid, DS_THREADS, smem, s, a, src, nsrc)
-                 : ipt == 2 ? launch(decode_step_kernel<T, N, F, 2>, grid, DS_THREADS, smem, s, a, src, nsrc)
-                            : launch(decode_step_kernel<T, N, F, 1>, grid, DS_THREADS, smem, s, a, src, nsrc);
+  const size_t smem = dstep_smem(a.R, N, (int)sizeof(T), 1);
+  dim3 grid((a.Ek + DS_CH - 1) / DS_CH, (a.batch + DS_BB - 1) / DS_BB);
+  cudaError_t e_ = launch(decode_step_kernel<T, N, F>, grid, DS_THREADS, smem, s, a, src, nsrc);
   if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
 }
@@ -1075,58 +898,15 @@ static cudaError_t dstep_t(const DStepArgs& a, Peers src, int nsrc, cudaStream_t
 cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, int ldp, int rmsnorm, float eps,
                                const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
-                               int N, int ch_per_head, float* zacc, cudaStream_t s, float* zero_ss,
-                               const void* pf, int64_t pf_bytes) {
+                               int N, int ch_per_head, float* zacc, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   if (!dstep_supported(bf16, R, N, ldp, ch_per_head) || nsrc < 1 || nsrc > kMaxTP) return cudaErrorInvalidValue;
   DStepArgs a{};
   a.src_off = src_off; a.ldp = ldp; a.rmsnorm = rmsnorm; a.eps = eps; a.u = u; a.z = z; a.ldz = ldz; a.w_dt = w_dt;
   a.b_dt = b_dt; a.a_log = a_log; a.d_skip = d_skip; a.h = h; a.g = g; a.batch = batch; a.Ek = Ek; a.R = R;
-  a.cph = ch_per_head; a.zacc = zacc; a.zero_ss = zero_ss;
-  static const int h_late = [] { const char* e = getenv("SSM_DSTEP_HLATE"); return e ? atoi(e) : 0; }();
-  a.h_late = h_late;
-  a.pf = pf;
-  a.pf_bytes = pf ? pf_bytes : 0;
+  a.cph = ch_per_head; a.zacc = zacc;
   if (bf16) return N == 16 ? dstep_t<__nv_bfloat16, 16, true>(a, src, nsrc, s) : dstep_t<__nv_bfloat16, 8, true>(a, src, nsrc, s);
   return N == 16 ? dstep_t<float, 16, false>(a, src, nsrc, s) : dstep_t<float, 8, false>(a, src, nsrc, s);
-}
-
-// Decode chain start (see internal.h): one 128-thread block per row; block 0 also zeroes the
-// out_proj finaliser counters.
-__global__ void __launch_bounds__(128) chain_begin_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
-                                                          float* __restrict__ ss, int* __restrict__ cnt, int ncnt,
-                                                          int D) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float red[4];
-  const int64_t row = blockIdx.x;
-  const int tid = threadIdx.x;
-  if (row == 0)
-    for (int i = tid; i < ncnt; i += 128) cnt[i] = 0;
-  float s2 = 0.f;
-  for (int i = tid; i < D / 4; i += 128) {
-    const float4 v = reinterpret_cast<const float4*>(x + row * D)[i];
-    s2 = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, s2))));
-    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-    reinterpret_cast<uint2*>(y + row * D)[i] = pk;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-  if ((tid & 31) == 0) red[tid >> 5] = s2;
-  __syncthreads();
-  if (tid == 0) ss[row] = red[0] + red[1] + red[2] + red[3];
-}
-
-cudaError_t launch_chain_begin(const float* x, __nv_bfloat16* y, float* ss, int* cnt, int ncnt, int64_t M, int D,
-                               cudaStream_t s) {
-  if (M <= 0) return cudaSuccess;
-  if (D % 4) return cudaErrorInvalidValue;
-  cudaError_t e_ = launch(chain_begin_kernel, (unsigned)M, 128, 0, s, x, y, ss, cnt, ncnt, D);
-  if (e_ != cudaSuccess) return e_;
-  return cudaGetLastError();
 }
 
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
@@ -1240,13 +1020,10 @@ cudaError_t preload_kernels() {
       (const void*)scan_kernel<__nv_bfloat16, 16, true>, (const void*)scan_kernel<__nv_bfloat16, 16, false>,
       (const void*)scan_kernel<__nv_bfloat16, 8, true>, (const void*)scan_kernel<__nv_bfloat16, 8, false>,
       (const void*)scan_kernel<float, 16, false>, (const void*)scan_kernel<float, 8, false>,
-      (const void*)scan2_kernel<16, 0>, (const void*)scan2_kernel<16, 2>, (const void*)scan2_kernel<16, 4>,
-      (const void*)scan2_kernel<16, 6>,
-      (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 1>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 1>,
-      (const void*)decode_step_kernel<float, 16, false, 1>, (const void*)decode_step_kernel<float, 8, false, 1>,
-      (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 4>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 4>,
-      (const void*)decode_step_kernel<float, 16, false, 4>, (const void*)decode_step_kernel<float, 8, false, 4>,
-      (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>, (const void*)chain_begin_kernel,
+      (const void*)conv1d_silu_v2_kernel<2>, (const void*)conv1d_silu_v2_kernel<3>, (const void*)conv1d_silu_v2_kernel<4>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 16, true>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true>,
+      (const void*)decode_step_kernel<float, 16, false>, (const void*)decode_step_kernel<float, 8, false>,
+      (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>,
       (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,
       (const void*)quantize_kernel<8>, (const void*)qar_reduce_kernel, (const void*)f32_reduce_kernel,
       (const void*)f16_cast_kernel, (const void*)f16_reduce_kernel, (const void*)amax_kernel<4>,

@@ -185,6 +185,16 @@ class TPMixer:
         L.call("ssm_tp_stats", self.handle, C.byref(a), C.byref(b))
         return {"allreduce": a.value, "bytes_sent": b.value}
 
+    def epoch(self):
+        """Collectives enqueued so far (ssm_tp_epoch); collective e uses symmetric half e & 1."""
+        e = C.c_uint32()
+        L.call("ssm_tp_epoch", self.handle, C.byref(e))
+        return e.value
+
+    def barrier(self, stream=None):
+        """Payload-free cross-rank barrier (a collective); advances the epoch by one at TP > 1."""
+        L.call("ssm_tp_barrier", self.handle, _stream(stream))
+
     def fused_calls(self):
         """Decode calls that ran the fused in_proj (+conv +x_proj) kernel."""
         n = C.c_int64()

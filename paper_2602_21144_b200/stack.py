@@ -5,16 +5,10 @@ launched through libssmtp's C ABI; PyTorch provides memory, streams and the grap
 """
 from __future__ import annotations
 
-import os
-
-from ctypes import c_float as C_float
-
 import torch
 
 from . import _lib as L
-
-_DEBUG_SKIP_NORM = os.environ.get("SSM_DEBUG_SKIP_NORM") == "1"  # timing ablations only
-from .mixer import LayerWeights, State, TPMixer
+from .mixer import LayerWeights, State, TPMixer  # noqa: F401
 
 
 def synthetic_layer(dims, layer, seed=1000, device="cuda"):
@@ -45,17 +39,12 @@ def synthetic_layer(dims, layer, seed=1000, device="cuda"):
 
 
 class MixerStack:
-    """flags: SSM_AR2_INT8 / SSM_AR2_FP32 (the library's peer-to-peer AR#2), or SSM_AR2_EXTERNAL
-    with nccl_group set: the NCCL bf16 all-reduce BASELINE arm (library writes the rank's fp32
-    partial, torch.distributed all-reduces it in bf16, torch adds it to the residual)."""
+    """flags: SSM_AR2_INT8 / SSM_AR2_FP16 / SSM_AR2_FP32 (the library's peer-to-peer AR#2), or
+    SSM_AR2_EXTERNAL with nccl_group set: the NCCL bf16 all-reduce BASELINE arm (library writes the
+    rank's fp32 partial, torch.distributed all-reduces it in bf16, torch adds it to the residual)."""
 
     def __init__(self, mixer: TPMixer, layers: list, batch: int, max_chunk: int, flags=L.SSM_AR2_INT8,
-                 norm_eps=1e-5, nccl_group=None, persistent=None):
-        """persistent: decode every token with ONE launch of the persistent whole-stack kernel
-        (ssm_stack_decode) when the library supports the configuration (TP=1, bf16, packed
-        weights, ...).  True = required; False = per-layer calls; None = the environment's
-        SSM_PERSISTENT_DECODE=1 opts in (default off: measured slower than the per-layer graph,
-        DESIGN.md §6c)."""
+                 norm_eps=1e-5, nccl_group=None):
         self.mx, self.layers, self.batch, self.flags, self.eps = mixer, layers, batch, flags, norm_eps
         self.nccl = nccl_group if flags == L.SSM_AR2_EXTERNAL else None
         d = mixer.dims
@@ -69,47 +58,7 @@ class MixerStack:
             self.part = torch.empty((batch * max_chunk, d.d_model), dtype=torch.float32, device=mixer.device)
         self.graph = None
         self.graph_launches = 0
-        self.stack_ws = None
-        # opt-in (SSM_PRENORM=1): the pre-norm computed inside the fused decode in_proj
-        # (ssm_mixer_decode_prenorm).  Measured slower: 44.6 vs 38.0 us per Mamba-2.8B decode layer
-        # -- 80 CTAs re-reading the same 164 KB of residual rows from L2 cost more than the 16-block
-        # norm kernel they replace
-        self.prenorm = mixer.dtype == "bf16" and os.environ.get("SSM_PRENORM", "0") == "1"
-        self.chain = False  # per-layer decode with the pre-norm folded into the GEMMs (ssm_mixer_decode_chained)
-        # opt-in (SSM_DECODE_CHAIN=1): measured slower than the norm kernel it removes
-        if self.nccl is None and os.environ.get("SSM_DECODE_CHAIN", "0") == "1" and layers:
-            import ctypes as C
-            ok = C.c_int32(0)
-            L.call("ssm_decode_chain_supported", mixer.handle, C.byref(layers[0].struct), batch, C.byref(ok))
-            self.chain = bool(ok.value)
-        required = bool(persistent)
-        if persistent is None:
-            persistent = os.environ.get("SSM_PERSISTENT_DECODE") == "1"
-        if persistent and self.nccl is None:
-            self._bind_persistent(required=required)
-
-    def _bind_persistent(self, required=False):
-        import ctypes as C
-        from .mixer import _ptr, _stream
-        nl = len(self.layers)
-        nb = C.c_size_t()
-        rc = L.LIB.ssm_stack_bytes(self.mx.handle, nl, self.batch, C.byref(nb))
-        packed = all(lw.struct.w_in_pk and lw.struct.w_out_pk for lw in self.layers)
-        if rc != 0 or not packed:
-            if required:
-                raise L.SSMError(rc or 8, "ssm_stack_bytes", L.LIB.ssm_last_error().decode() if rc else
-                                 "layers are not packed (LayerWeights.pack)")
-            return
-        self._layer_arr = (L.ssm_layer_weights_t * nl)(*[lw.struct for lw in self.layers])
-        self._state_arr = (C.c_void_p * nl)(*[st.handle.value for st in self.states])
-        self.stack_ws = torch.zeros(nb.value, dtype=torch.uint8, device=self.mx.device)
-        L.call("ssm_stack_bind", self.mx.handle, C.cast(self._layer_arr, C.c_void_p), C.cast(self._state_arr, C.c_void_p), nl, self.batch,
-               _ptr(self.stack_ws), nb.value, _stream(None))
-
-    def stack_check(self, stream=None):
-        from .mixer import _ptr, _stream
-        if self.stack_ws is not None:
-            L.call("ssm_stack_check", self.mx.handle, _ptr(self.stack_ws), _stream(stream))
+        self._graph_parity = 0
 
     def reset(self, stream=None):
         for s in self.states:
@@ -128,33 +77,8 @@ class MixerStack:
 
     def decode_step(self, res_t, stream=None):
         """res_t: [batch, D] fp32, updated in place through all layers."""
-        if self.stack_ws is not None:
-            from .mixer import _ptr, _stream
-            L.call("ssm_stack_decode", self.mx.handle, _ptr(self.stack_ws), _ptr(res_t), C_float(self.eps),
-                   _stream(stream))
-            return
-        if self.chain:
-            import ctypes as C
-            from .mixer import _ptr, _stream
-            L.call("ssm_decode_chain_begin", self.mx.handle, _ptr(res_t), _ptr(self.xbuf_dec), self.batch,
-                   _ptr(self.ws_dec), self.ws_dec.numel(), _stream(stream))
-            for lw, st in zip(self.layers, self.states):
-                L.call("ssm_mixer_decode_chained", self.mx.handle, C.byref(lw.struct), st.handle, _ptr(self.xbuf_dec),
-                       _ptr(res_t), self.batch, C.c_float(self.eps), _ptr(self.ws_dec), self.ws_dec.numel(),
-                       _stream(stream))
-            return
-        if self.prenorm and self.nccl is None and not _DEBUG_SKIP_NORM:
-            import ctypes as C
-            from .mixer import _ptr, _stream
-            for lw, st in zip(self.layers, self.states):
-                L.call("ssm_mixer_decode_prenorm", self.mx.handle, C.byref(lw.struct), st.handle, _ptr(self.xbuf_dec),
-                       _ptr(res_t), self.batch, C.c_float(self.eps), self.flags, _ptr(self.ws_dec),
-                       self.ws_dec.numel(), _stream(stream))
-            return
-        skip_norm = _DEBUG_SKIP_NORM
         for lw, st in zip(self.layers, self.states):
-            if not skip_norm:
-                self.mx.rmsnorm(res_t, self.xbuf_dec, None, self.eps, stream)
+            self.mx.rmsnorm(res_t, self.xbuf_dec, None, self.eps, stream)
             if self.nccl is None:
                 self.mx.decode(lw, st, self.xbuf_dec, res_t, self.flags, self.ws_dec, stream)
             else:
@@ -172,8 +96,10 @@ class MixerStack:
     def capture_decode(self, res_t, probes=(), warmup=True):
         """Capture one decode step over all layers into a CUDA graph reading/writing res_t.
         The decode path is graph-safe: no host sync, fixed pointers; the all-reduce epoch
-        counters live in device memory and advance on every replay, and each step issues an
-        even number of collectives so the double-buffer halves alternate across replays."""
+        counters live in device memory and advance on every replay.  The symmetric-buffer halves
+        of the captured collectives are fixed, so the graph must be replayed with the handle's
+        epoch at the parity it had at capture (replay() realigns it with a barrier), and one step
+        must issue an even number of collectives so that back-to-back replays alternate halves."""
         if warmup:  # one eager step first (attribute setup outside capture); callers driving several
             s = torch.cuda.Stream()  # virtual ranks on one device do their warm-ups themselves
             s.wait_stream(torch.cuda.current_stream())
@@ -186,10 +112,23 @@ class MixerStack:
         g = torch.cuda.CUDAGraph()
         before = self.mx.launches()
         ar_before = self.mx.stats()["allreduce"]
+        self._graph_parity = self.mx.epoch() & 1
+        e0 = self.mx.epoch()
         with torch.cuda.graph(g):
             self.decode_step(res_t)
         self.graph_launches = self.mx.launches() - before
-        if (self.mx.stats()["allreduce"] - ar_before) % 2:
+        if (self.mx.epoch() - e0) % 2:
             raise RuntimeError("odd number of collectives per decode step: double-buffer halves would not alternate")
+        del ar_before
         self.graph = g
         return g
+
+    def align_epoch(self, stream=None):
+        """Before replaying the decode graph: if eager collectives since the capture (a prefill)
+        left the epoch at the other parity, one payload-free barrier restores it."""
+        if self.mx.tp_size > 1 and (self.mx.epoch() & 1) != self._graph_parity:
+            self.mx.barrier(stream)
+
+    def replay(self, graph=None, stream=None):
+        self.align_epoch(stream)
+        (graph or self.graph).replay()

@@ -37,7 +37,6 @@ SHAPES = {
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--kbs", default="1,2")
     p.add_argument("--only", default="")
     a = p.parse_args()
     mx = TPMixer(synth.CONFIGS["tiny"], "bf16")
@@ -49,8 +48,7 @@ def main():
         W = [torch.randn(N, K, device="cuda").to(torch.bfloat16) for _ in range(copies)]
         X = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         C = torch.empty(M, N, device="cuda")
-        for kbs in a.kbs.split(","):
-            os.environ["SSM_GEMM_KBS"] = kbs
+        for kbs in ("auto",):
             reps = 24 if swap else 4
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())

@@ -1,8 +1,6 @@
 #!/usr/bin/env python
 """Microbenchmark of the prefill scan kernel on Mamba-2.8B shapes (GPU only).
-Variant knobs are environment variables read by libssmtp at load time
-(SSM_SCAN_VERSION, SSM_SCAN_NPOLY), so run one variant per process:
-    SSM_SCAN_NPOLY=4 python scripts/scan_micro.py [--tp 1] [--batch 16] [--seqlen 2048]
+    python scripts/scan_micro.py [--tp 1] [--batch 16] [--seqlen 2048]
 """
 import argparse
 import os
@@ -49,8 +47,7 @@ def main():
     ms = e0.elapsed_time(e1) / reps
     chtok = B * L * E
     byts = chtok * 8 + B * L * 2 * N * 4
-    print(f"scan tp={a.tp} B={B} L={L} E_k={E} version={os.environ.get('SSM_SCAN_VERSION', '2')} "
-          f"npoly={os.environ.get('SSM_SCAN_NPOLY', '4')}: {ms * 1000:8.1f} us  "
+    print(f"scan tp={a.tp} B={B} L={L} E_k={E}: {ms * 1000:8.1f} us  "
           f"{chtok / ms / 1e6:8.1f} Gch-tok/s  {byts / ms / 1e6:8.1f} GB/s", flush=True)
 
 
