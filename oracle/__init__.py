@@ -18,10 +18,14 @@ Modules:
   tp_sim     channel splitter + the two-all-reduce TP mixer, ranks simulated
              in-process.
 
+  agreement_ref  Table 1's agreement metrics, straight-line.
+
 Pins (tests/test_oracle_*.py): SPEC.md worked examples (closed forms),
 scipy.signal.lfilter on constant-parameter scans, torch conv1d, a pure-Python
 brute-force recurrence, HF transformers MambaMixer/FalconMambaMixer/
-ZambaMambaMixer slow paths in float64, cache/prefix invariants, and the
-hand-worked int8 block example in tests/golden/qar_block.txt.
-No function here is "parity unpinned".
+ZambaMambaMixer slow paths in float64, the pre-norm stack (model_forward)
+against chained HF MambaBlocks in float64 (eps-sensitive scale), cache/prefix
+invariants, the hand-worked int8 blocks (tests/golden/qar_block.txt,
+qar_twoshot.txt) and the closed-form bounds' hand values
+(tests/golden/qar_bounds.txt: northstar_bound, fp16_error_bound).
 """

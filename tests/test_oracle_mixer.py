@@ -194,3 +194,48 @@ def test_channel_permutation_equivariance_of_ssm_path():
     yp, hp = M.scan_full(u[:, :, p], dl[:, :, p], A[p], Bm, Cm, Dv[p], np.zeros((Bsz, E, N)))
     np.testing.assert_array_equal(yp, y[:, :, p])
     np.testing.assert_array_equal(hp, h[:, p])
+
+
+def _hf_block(dims, w, eps):
+    """HF MambaBlock (pre-norm RMSNorm -> MambaMixer -> residual add) in float64, norm weight 1."""
+    from transformers import MambaConfig
+    from transformers.models.mamba.modeling_mamba import MambaBlock
+    m = _hf_mamba(dims, w)
+    cfg = MambaConfig(hidden_size=dims.d_model, intermediate_size=dims.d_inner, state_size=dims.d_state,
+                      conv_kernel=dims.d_conv, time_step_rank=dims.dt_rank, use_bias=False, use_conv_bias=True,
+                      hidden_act="silu", use_mambapy=False, layer_norm_epsilon=eps, residual_in_fp32=False)
+    prev = torch.get_default_dtype()
+    torch.set_default_dtype(torch.float64)
+    try:
+        blk = MambaBlock(cfg, layer_idx=0).eval()
+    finally:
+        torch.set_default_dtype(prev)
+    blk.mixer = m
+    with torch.no_grad():
+        blk.norm.weight.fill_(1.0)
+    return blk
+
+
+@pytest.mark.parametrize("scale", [1.0, 3e-3])
+def test_model_forward_matches_hf_mamba_blocks(scale):
+    """oracle.model_forward (the pre-norm stack of reading Q16: residual += mixer(RMSNorm(residual)),
+    eps 1e-5, RMSNorm weight 1, residual carried in float64) against two chained HF MambaBlocks in
+    float64 (residual_in_fp32=False so no cast).  At scale 3e-3 the residual's mean square (~1e-5)
+    is of the order of eps, so a wrong eps, a post-norm order or a residual swap all fail."""
+    warnings.filterwarnings("ignore")
+    dims = _tiny(n_layers=2)
+    ws = [synth.layer_weights(dims, l) for l in range(2)]
+    _, res = synth.activations(2, 24, dims.d_model, seed=17)
+    res = res * scale
+    with torch.no_grad():
+        h = res.clone()
+        for l in range(2):
+            h = _hf_block(dims, ws[l], 1e-5)(h)
+    hf = h.numpy()
+    mine, _ = M.model_forward(dims, [_np(w) for w in ws], res.numpy(), norm_eps=1e-5)
+    d_hf, d_mine = hf - res.numpy(), mine - res.numpy()
+    # HF casts A, B, u to fp32 inside the mixer (modeling_mamba.py slow path) -> ~1e-7, not bits
+    assert np.abs(d_mine - d_hf).max() / np.abs(d_hf).max() < 2e-6
+    # the pins bite: eps 1e-6 (Falcon's mixer eps) instead of 1e-5 is far outside the tolerance
+    wrong, _ = M.model_forward(dims, [_np(w) for w in ws], res.numpy(), norm_eps=1e-6)
+    assert np.abs((wrong - res.numpy()) - d_hf).max() / np.abs(d_hf).max() > (1e-3 if scale < 1 else 1e-7)

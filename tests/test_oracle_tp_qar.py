@@ -273,3 +273,42 @@ def test_twoshot_within_northstar_bound(k):
     assert np.max(err / bound) > 0.2                 # not vacuous
     for q in codes:
         assert q.min() >= -127 and q.max() <= 127
+
+
+def _bounds_golden():
+    vals = {}
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "qar_bounds.txt")):
+        if line.strip() and not line.startswith("#"):
+            key, *rest = line.split()
+            vals[key] = [float(v) for v in rest]
+    return vals
+
+
+def test_northstar_bound_golden():
+    """northstar_bound = k max_r amax / 254 exactly on the hand-worked blocks (a bound constant of
+    127, a missing k or a mean instead of a max fails)."""
+    g = _bounds_golden()
+    rows = [np.array(list(map(float, l.split())), np.float32)
+            for l in open(os.path.join(os.path.dirname(__file__), "golden", "qar_twoshot.txt"))
+            if l.strip() and not l.startswith("#")]
+    b2 = Q.northstar_bound([rows[0], rows[1]], 4)
+    np.testing.assert_array_equal(b2, np.full(4, g["northstar_k2"][0]))
+    o = np.array([7.9375, 0.03125, -0.09375, 0.15625], np.float32)
+    b1 = Q.northstar_bound([o], 4)
+    np.testing.assert_array_equal(b1, np.full(4, g["northstar_k1"][0]))
+    q, s = Q.quantize_blocks(o[None], 4)
+    np.testing.assert_array_equal(Q.error_bound([s], 4)[0], b1)        # = s / 2 here
+    err = np.abs(Q.dequantize_blocks(q, s, 4)[0] - o)
+    assert np.sum(err == b1) == 3                                      # attained (tight)
+
+
+def test_fp16_error_bound_golden():
+    g = _bounds_golden()
+    want = sum(2.0 ** e for e in g["fp16_k2_exponents"])
+    got = Q.fp16_error_bound([np.array([1.0], np.float32), np.array([3.0], np.float32)])
+    assert got[0] == want
+    o = np.array(g["fp16_tie_input"], np.float32)
+    got, _ = Q.fp16_allreduce([o])
+    err = abs(float(got[0]) - float(o[0]))
+    assert err == g["fp16_tie_error"][0]
+    assert err <= Q.fp16_error_bound([o])[0] <= err * (1 + 2.0 ** -10)   # attained up to 2^-25
