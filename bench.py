@@ -34,8 +34,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="mamba2.8b", choices=["mamba2.8b", "falcon7b", "zamba7b", "mamba2.8b-long"])
-    p.add_argument("--ar2", default="int8", choices=["int8", "fp16", "fp32", "nccl"],
-                   help="AR#2: int8 / fp32 peer-to-peer (library), or nccl = NCCL bf16 all-reduce baseline arm")
+    p.add_argument("--ar2", default="int8", choices=["int8", "fp16", "bf16", "fp32", "nccl"],
+                   help="AR#2: int8 / fp16 / bf16 / fp32 peer-to-peer (library), or nccl = NCCL bf16 all-reduce "
+                        "baseline arm")
     p.add_argument("--prompt", type=int, default=0, help="override prompt length (smoke runs only)")
     p.add_argument("--decode", type=int, default=-1, help="override decode length (smoke runs only)")
     p.add_argument("--layers", type=int, default=0, help="override layer count (smoke runs only)")
@@ -250,7 +251,8 @@ def main():
     while B * chunk > 65536 and chunk % 2 == 0:
         chunk //= 2
     n_chunks = math.ceil(Lp / chunk)
-    flags = {"int8": L.SSM_AR2_INT8, "fp16": L.SSM_AR2_FP16, "fp32": L.SSM_AR2_FP32, "nccl": L.SSM_AR2_EXTERNAL}[args.ar2]
+    flags = {"int8": L.SSM_AR2_INT8, "fp16": L.SSM_AR2_FP16, "bf16": L.SSM_AR2_BF16, "fp32": L.SSM_AR2_FP32,
+             "nccl": L.SSM_AR2_EXTERNAL}[args.ar2]
 
     peer_bufs, nbytes, symm = None, 0, None
     if k > 1:

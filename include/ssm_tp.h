@@ -87,10 +87,16 @@ enum {
   SSM_QAR_ONESHOT = 0x80,   /* mixer calls: force the one-shot int8 schedule.  Default for
                               SSM_AR2_INT8: two-shot when tp_size >= 4 and the call has >= 64
                               tokens (prefill), one-shot otherwise (decode, k = 2)               */
-  SSM_DECODE_UNFUSED = 0x100 /* ssm_mixer_decode: run the plain kernel chain (in_proj GEMM, conv
+  SSM_DECODE_UNFUSED = 0x100, /* ssm_mixer_decode: run the plain kernel chain (in_proj GEMM, conv
                               step, x_proj GEMM, decode step, out_proj) instead of the fused
                               in_proj (+conv step +x_proj epilogue); same arithmetic, used to
                               cross-check the fused kernel                                        */
+  SSM_AR2_BF16 = 0x200,     /* AR#2 = custom bf16 wire (SURVEY.md §8(d) "custom bf16" arm, the
+                              unquantised-16-bit baseline the int8 AR is compared with, PAPER.md
+                              591-610): each rank casts its fp32 partial to bf16 (RNE), exchanges
+                              it peer-to-peer, and every rank sums the k bf16 values in fp32 left
+                              to right in rank order, added to the fp32 residual                 */
+  SSM_QAR_BF16 = 0x400      /* ssm_qallreduce: bf16 wire (as SSM_AR2_BF16); n % 8 == 0           */
 };
 
 enum { SSM_COMM_VIRTUAL = 0x1 }; /* ssm_comm_t.flags: all peer buffers live on THIS device

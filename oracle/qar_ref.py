@@ -114,6 +114,41 @@ def fp16_error_bound(partials):
 
 
 # ---------------------------------------------------------------------------------------------
+# bf16-wire all-reduce: the custom bf16 arm of SURVEY.md §8(d) ("AR#2 in {NCCL bf16, custom bf16,
+# int8}"), the unquantised 16-bit baseline the paper's Table 1 compares quantisation against
+# (PAPER.md:591-610).  Same one-shot schedule and fp32 reduction as the fp16 wire; the cast is
+# bfloat16 round-to-nearest-even (8 significant bits, fp32's exponent range, so no overflow for
+# finite fp32 inputs except the last binade rounding up to inf).
+
+def bf16_cast(o):
+    """fl_bf16(o), RNE, returned as the float32 values (bfloat16 = the top 16 bits of binary32):
+    add 0x7FFF plus the lowest kept bit to the 32-bit pattern, then clear the low 16 bits."""
+    u = np.asarray(o, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    r = ((u + 0x7FFF + lsb) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
+def bf16_allreduce(partials):
+    """partials: k float32 arrays.  Returns the float32 sum of the bf16-cast partials formed left
+    to right in fp32 (fixed rank order), and the bf16 wire values (as float32)."""
+    wire = [bf16_cast(o) for o in partials]
+    acc = wire[0].astype(np.float32)
+    for h in wire[1:]:
+        acc = (acc + h).astype(np.float32)
+    return acc, wire
+
+
+def bf16_error_bound(partials):
+    """Per element: sum_r |o_r| 2^-8 (RNE cast: half a bf16 ulp; 8 significant bits, so the unit
+    roundoff is 2^-8; the fp32 subnormal range is ignored) + (k-1) roundings of the fp32 adds,
+    each <= 2^-24 sum_r |o_r| (1 + 2^-8)."""
+    a = np.sum([np.abs(np.asarray(o, dtype=np.float64)) for o in partials], axis=0)
+    k = len(partials)
+    return a * 2.0 ** -8 + (k - 1) * 2.0 ** -24 * a * (1 + 2.0 ** -8)
+
+
+# ---------------------------------------------------------------------------------------------
 # Two-shot int8 schedule with SHARED per-block scales (SURVEY.md §8(c) Q6, DESIGN.md §3 Q6):
 #   A_b   = max_r amax_{r,b}                   (exact in fp32)
 #   s_b   = fl32(A_b / 127)                     (IEEE fp32 division)

@@ -156,6 +156,9 @@ def tp_mixer_forward(dims, w, x_in, residual, k, states=None, ar2="exact", block
     elif ar2 == "fp16":                            # the paper's FP32 -> FP16 wire
         total, _ = qar_ref.fp16_allreduce([p.astype(np.float32) for p in partial_out])
         total = total.astype(np.float64)
+    elif ar2 == "bf16":                            # the custom bf16 wire
+        total, _ = qar_ref.bf16_allreduce([p.astype(np.float32) for p in partial_out])
+        total = total.astype(np.float64)
     else:
         raise ValueError(ar2)
     if k > 1:

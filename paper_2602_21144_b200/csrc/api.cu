@@ -268,7 +268,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->ar_count++;
     t->bytes_sent += M * hl * P * 4;
   }
-  enum { OUT_RESID, OUT_EXTERNAL, OUT_FP32, OUT_INT8, OUT_FP16 } omode;
+  enum { OUT_RESID, OUT_EXTERNAL, OUT_FP32, OUT_INT8, OUT_W16 } omode;
   float* odst;
   if (t->k == 1) {
     omode = OUT_RESID;
@@ -276,8 +276,8 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   } else if (flags & SSM_AR2_EXTERNAL) {
     omode = OUT_EXTERNAL;
     odst = residual;
-  } else if (flags & SSM_AR2_FP16) {
-    omode = OUT_FP16;
+  } else if (flags & (SSM_AR2_FP16 | SSM_AR2_BF16)) {
+    omode = OUT_W16;
     ep2 = ++t->epoch;
     odst = part;
   } else if (flags & SSM_AR2_FP32) {
@@ -432,14 +432,15 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     else
       CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
     CU(launch_f32_reduce(t->peers, t->k, half_off(ep2), nD, residual, 1, s));
-  } else if (omode == OUT_FP16) {  // the paper's FP32 -> FP16 wire
+  } else if (omode == OUT_W16) {  // the paper's FP32 -> FP16 wire or the bf16 arm
     Probe pr(t, SSM_PROBE_AR2, s);
+    const int wbf = (flags & SSM_AR2_BF16) ? 1 : 0;
     t->launches += 3;
-    CU(launch_f16_cast(part, nD, own_half(ep2), s));
+    CU(launch_w16_cast(wbf, part, nD, own_half(ep2), s));
     t->ar_count++;
     t->bytes_sent += nD * 2;
     CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
-    CU(launch_f16_reduce(t->peers, t->k, half_off(ep2), nD, residual, 1, s));
+    CU(launch_w16_reduce(wbf, t->peers, t->k, half_off(ep2), nD, residual, 1, s));
   } else if (omode == OUT_INT8 && (flags & SSM_QAR_TWOSHOT ||
                                     (!(flags & SSM_QAR_ONESHOT) && t->k >= 4 && M >= 64)) &&
              nD % (16 * t->k) == 0 &&
@@ -478,12 +479,12 @@ ssm_status_t check_call(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* 
   if (!x_in || !residual) return fail(SSM_ERR_ARG, "x_in/residual is NULL");
   if ((reinterpret_cast<uintptr_t>(x_in) | reinterpret_cast<uintptr_t>(residual)) & 15)
     return fail(SSM_ERR_ARG, "x_in/residual must be 16-B aligned");
-  if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL | SSM_QAR_TWOSHOT |
-                          SSM_QAR_ONESHOT | SSM_DECODE_UNFUSED))
+  if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_BF16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL |
+                          SSM_QAR_TWOSHOT | SSM_QAR_ONESHOT | SSM_DECODE_UNFUSED))
     return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
   if ((flags & SSM_QAR_TWOSHOT) && (flags & SSM_QAR_ONESHOT))
     return fail(SSM_ERR_ARG, "SSM_QAR_TWOSHOT and SSM_QAR_ONESHOT are exclusive");
-  const int nmode = !!(flags & SSM_AR2_INT8) + !!(flags & SSM_AR2_FP16) + !!(flags & SSM_AR2_FP32) +
+  const int nmode = !!(flags & SSM_AR2_INT8) + !!(flags & SSM_AR2_FP16) + !!(flags & SSM_AR2_BF16) + !!(flags & SSM_AR2_FP32) +
                     !!(flags & SSM_AR2_EXTERNAL);
   if (nmode > 1) return fail(SSM_ERR_ARG, "at most one AR#2 mode flag");
   const int64_t M = (int64_t)batch * seqlen;
@@ -692,10 +693,11 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
 
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
   if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
-  if (n == 0 && !(flags & ~(uint32_t)(SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_TWOSHOT))) return SSM_OK;  // nothing to reduce
+  const uint32_t known = SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_BF16 | SSM_QAR_TWOSHOT;
+  if (n == 0 && !(flags & ~known)) return SSM_OK;  // nothing to reduce
   if (!partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
-  if (flags & ~(uint32_t)(SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_TWOSHOT))
-    return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  if (flags & ~known) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  if ((flags & SSM_QAR_FP16) && (flags & SSM_QAR_BF16)) return fail(SSM_ERR_ARG, "SSM_QAR_FP16 and SSM_QAR_BF16 are exclusive");
   const int blk = tp->cfg.qar_block;
   if (n % blk) return fail(SSM_ERR_DIM, "n=%zu not a multiple of qar_block=%d", n, blk);
   if ((reinterpret_cast<uintptr_t>(partial) | reinterpret_cast<uintptr_t>(out)) & 15)
@@ -722,18 +724,19 @@ ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_
                           (int64_t)n, blk, out, acc, s));
     return SSM_OK;
   }
-  if (flags & SSM_QAR_FP16) {  // the paper's fp16 wire
+  if (flags & (SSM_QAR_FP16 | SSM_QAR_BF16)) {  // the paper's fp16 wire / the bf16 arm
+    const int wbf = (flags & SSM_QAR_BF16) ? 1 : 0;
     if (n % 8) return fail(SSM_ERR_DIM, "n=%zu not a multiple of 8 (fp16 wire)", n);
     if (n * 2 > half_bytes(tp)) return fail(SSM_ERR_ARG, "symmetric buffer too small for n=%zu", n);
     const uint32_t ep = ++tp->epoch;
     const size_t half = half_bytes(tp);
     char* own = reinterpret_cast<char*>(tp->peers.p[tp->rank]) + kSigBytes + (ep & 1) * half;
     tp->launches += 3;
-    CU(launch_f16_cast(partial, (int64_t)n, own, s));
+    CU(launch_w16_cast(wbf, partial, (int64_t)n, own, s));
     tp->ar_count++;
     tp->bytes_sent += n * 2;
     CU(launch_peer_barrier(tp->peers, tp->rank, tp->k, s));
-    CU(launch_f16_reduce(tp->peers, tp->k, (int64_t)(kSigBytes + (ep & 1) * half), (int64_t)n, out, acc, s));
+    CU(launch_w16_reduce(wbf, tp->peers, tp->k, (int64_t)(kSigBytes + (ep & 1) * half), (int64_t)n, out, acc, s));
     return SSM_OK;
   }
   const size_t need = al256(n) + n / blk * 4;

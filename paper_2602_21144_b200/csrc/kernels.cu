@@ -685,22 +685,37 @@ __global__ void ag16_kernel(Peers src, int64_t sum_off, int64_t shard, int64_t n
   }
 }
 
-// ---------------------------------------------------------------- fp16-wire all-reduce
-// Cast: 8 fp32 -> 8 fp16 per thread (cvt.rn.f16x2.f32: IEEE round-to-nearest-even, overflow -> inf).
-__global__ void f16_cast_kernel(const float* __restrict__ x, int64_t n8, __half* __restrict__ out) {
+// ---------------------------------------------------------------- 16-bit-wire all-reduces
+// fp16 (the paper's FP32 -> FP16 wire) and bf16 (the custom bf16 arm, SURVEY.md
+// §8(d)): cast 8 fp32 -> 8 16-bit values per thread (cvt.rn: IEEE round-to-nearest-even; fp16
+// overflow -> inf), exchanged one-shot, then summed in fp32.
+template <typename H> struct Wire16;
+template <> struct Wire16<__half> {
+  SSM_DEV static uint32_t pack(float a, float b) { __half2 h = __floats2half2_rn(a, b); return *reinterpret_cast<uint32_t*>(&h); }
+  SSM_DEV static float2 unpack(uint32_t w) { return __half22float2(*reinterpret_cast<const __half2*>(&w)); }
+};
+template <> struct Wire16<__nv_bfloat16> {
+  SSM_DEV static uint32_t pack(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  SSM_DEV static float2 unpack(uint32_t w) { return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w)); }
+};
+template <typename H>
+__global__ void w16_cast_kernel(const float* __restrict__ x, int64_t n8, uint4* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n8) return;
   const float4 a = reinterpret_cast<const float4*>(x)[2 * i];
   const float4 b = reinterpret_cast<const float4*>(x)[2 * i + 1];
-  __half2 h[4] = {__floats2half2_rn(a.x, a.y), __floats2half2_rn(a.z, a.w), __floats2half2_rn(b.x, b.y),
-                  __floats2half2_rn(b.z, b.w)};
-  reinterpret_cast<uint4*>(out)[i] = *reinterpret_cast<const uint4*>(h);
+  out[i] = make_uint4(Wire16<H>::pack(a.x, a.y), Wire16<H>::pack(a.z, a.w), Wire16<H>::pack(b.x, b.y),
+                      Wire16<H>::pack(b.z, b.w));
 }
 // Reduce: acc = fl32(h_0); acc = acc + fl32(h_r) for r = 1..k-1 (fixed order: bitwise-identical
 // replicas, Q12); out = out + acc (accumulate) or acc.
-__global__ void f16_reduce_kernel(Peers src, int k, int64_t off, int64_t n8, float* __restrict__ out, int accumulate) {
+template <typename H>
+__global__ void w16_reduce_kernel(Peers src, int k, int64_t off, int64_t n8, float* __restrict__ out, int accumulate) {
   pdl_trigger();
   pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -708,10 +723,10 @@ __global__ void f16_reduce_kernel(Peers src, int k, int64_t off, int64_t n8, flo
   float acc[8];
   for (int r = 0; r < k; ++r) {
     const uint4 raw = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(src.p[r]) + off)[i];
-    const __half2* h = reinterpret_cast<const __half2*>(&raw);
+    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float2 f = __half22float2(h[j]);
+      const float2 f = Wire16<H>::unpack(w[j]);
       if (r == 0) { acc[2 * j] = f.x; acc[2 * j + 1] = f.y; }
       else { acc[2 * j] = acc[2 * j] + f.x; acc[2 * j + 1] = acc[2 * j + 1] + f.y; }
     }
@@ -982,19 +997,26 @@ cudaError_t launch_qar_twoshot(Peers peers, int rank, int k, int64_t off, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_f16_cast(const float* x, int64_t n, void* out, cudaStream_t s) {
+cudaError_t launch_w16_cast(int bf16, const float* x, int64_t n, void* out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   if (n % 8) return cudaErrorInvalidValue;
   const int64_t n8 = n / 8;
-  { cudaError_t e_ = launch(f16_cast_kernel, (int)((n8 + 255) / 256), 256, 0, s, x, n8, reinterpret_cast<__half*>(out)); if (e_ != cudaSuccess) return e_; }
+  const int blocks = (int)((n8 + 255) / 256);
+  cudaError_t e_ = bf16 ? launch(w16_cast_kernel<__nv_bfloat16>, blocks, 256, 0, s, x, n8, reinterpret_cast<uint4*>(out))
+                        : launch(w16_cast_kernel<__half>, blocks, 256, 0, s, x, n8, reinterpret_cast<uint4*>(out));
+  if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
 }
 
-cudaError_t launch_f16_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s) {
+cudaError_t launch_w16_reduce(int bf16, Peers src, int k, int64_t off, int64_t n, float* out, int accumulate,
+                              cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   if (n % 8) return cudaErrorInvalidValue;
   const int64_t n8 = n / 8;
-  { cudaError_t e_ = launch(f16_reduce_kernel, (int)((n8 + 255) / 256), 256, 0, s, src, k, off, n8, out, accumulate); if (e_ != cudaSuccess) return e_; }
+  const int blocks = (int)((n8 + 255) / 256);
+  cudaError_t e_ = bf16 ? launch(w16_reduce_kernel<__nv_bfloat16>, blocks, 256, 0, s, src, k, off, n8, out, accumulate)
+                        : launch(w16_reduce_kernel<__half>, blocks, 256, 0, s, src, k, off, n8, out, accumulate);
+  if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
 }
 
@@ -1026,7 +1048,8 @@ cudaError_t preload_kernels() {
       (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>,
       (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,
       (const void*)quantize_kernel<8>, (const void*)qar_reduce_kernel, (const void*)f32_reduce_kernel,
-      (const void*)f16_cast_kernel, (const void*)f16_reduce_kernel, (const void*)amax_kernel<4>,
+      (const void*)w16_cast_kernel<__half>, (const void*)w16_reduce_kernel<__half>,
+      (const void*)w16_cast_kernel<__nv_bfloat16>, (const void*)w16_reduce_kernel<__nv_bfloat16>, (const void*)amax_kernel<4>,
       (const void*)quant_shared_kernel<4>, (const void*)rs16_kernel, (const void*)ag16_kernel,
       (const void*)peer_barrier_kernel};
   for (const void* f : fns) {

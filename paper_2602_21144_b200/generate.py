@@ -77,11 +77,11 @@ class TPLanguageModel:
         return torch.stack(toks, 1), torch.stack(logits, 0)
 
 
-def agreement_study(dims, n_layers, vocab, k_list, batch, prompt_len, n_out, seed=0, arms=("int8", "fp16")):
+def agreement_study(dims, n_layers, vocab, k_list, batch, prompt_len, n_out, seed=0, arms=("int8", "fp16", "bf16")):
     """Reference arm: exact fp32 all-reduce at each k (and TP=1).  Every arm is teacher-forced with
     the reference arm's tokens; returns a list of result dicts."""
     from .agreement import topk_agreement
-    flags = {"fp32": L.SSM_AR2_FP32, "int8": L.SSM_AR2_INT8, "fp16": L.SSM_AR2_FP16}
+    flags = {"fp32": L.SSM_AR2_FP32, "int8": L.SSM_AR2_INT8, "fp16": L.SSM_AR2_FP16, "bf16": L.SSM_AR2_BF16}
     layers = [synthetic_layer(dims, l) for l in range(n_layers)]
     g = torch.Generator(device="cuda").manual_seed(seed)
     emb = torch.randn(vocab, dims.d_model, generator=g, device="cuda").to(torch.bfloat16)

@@ -21,6 +21,7 @@ def test_agreement_study_small():
     assert by[(2, "fp32")]["top1"] >= 0.95
     assert by[(2, "fp16")]["top1"] >= 0.9
     assert by[(2, "int8")]["top1"] >= 0.8
+    assert by[(2, "bf16")]["top1"] >= 0.8
 
 
 def test_greedy_generation_deterministic_and_cache_equals_rescan():

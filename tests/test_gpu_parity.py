@@ -314,6 +314,55 @@ def test_virtual_fp16_allreduce_bitexact(k):
 
 
 @pytest.mark.parametrize("k", [2, 4, 8])
+def test_virtual_bf16_allreduce_bitexact(k):
+    """The custom bf16 wire: wire bytes and the fp32 rank-order sum equal the oracle bit for bit;
+    the error stays within the bf16 bound."""
+    dims = MED
+    n = 6 * dims.d_model
+    parts = synth.partials(k, n, seed=250 + k)
+    grp = VirtualGroup(dims, k, "bf16", 64)
+    outs = [torch.empty(n, device="cuda") for _ in range(k)]
+    dev_parts = [parts[r].cuda() for r in range(k)]
+    grp.run(lambda r, mx, s: mx.qallreduce(dev_parts[r], outs[r], stream=s, bf16=True))
+    ref, wire = Q.bf16_allreduce(list(parts.numpy()))
+    half = ((grp.bufs[0].numel() - 256) // 2) & ~255
+    for r in range(k):
+        base = 256 + half  # epoch 1 -> half 1
+        h = grp.bufs[r][base:base + 2 * n].cpu().view(torch.int16).numpy().view(np.uint16)
+        np.testing.assert_array_equal(h, (wire[r].view(np.uint32) >> 16).astype(np.uint16))
+    for r in range(k):
+        np.testing.assert_array_equal(outs[r].cpu().numpy(), ref)
+    exact = parts.double().sum(0).numpy()
+    assert np.all(np.abs(outs[0].cpu().double().numpy() - exact) <= Q.bf16_error_bound(list(parts.numpy())))
+
+
+@pytest.mark.parametrize("k,arm", [(2, "twoshot"), (4, "twoshot"), (8, "twoshot"), (4, "fp16"), (4, "bf16")])
+def test_virtual_allreduce_accumulate_bitexact(k, arm):
+    """SSM_QAR_ACCUMULATE (the mixer's mode: the result is added to the fp32 residual): out =
+    fl32(residual + result), the result rounded as the oracle rounds it (fl32(s * Q) for the
+    two-shot all-gather: no fma contraction with the residual add)."""
+    dims = MED
+    n = 6 * dims.d_model
+    parts = synth.partials(k, n, seed=400 + k)
+    g = torch.Generator().manual_seed(k)
+    res0 = (torch.randn(n, generator=g) * 3).float()
+    grp = VirtualGroup(dims, k, "bf16", 64)
+    outs = [res0.clone().cuda() for _ in range(k)]
+    dev_parts = [parts[r].cuda() for r in range(k)]
+    kw = {"twoshot": dict(twoshot=True), "fp16": dict(fp16=True), "bf16": dict(bf16=True)}[arm]
+    grp.run(lambda r, mx, s: mx.qallreduce(dev_parts[r], outs[r], accumulate=True, stream=s, **kw))
+    if arm == "twoshot":
+        ref, _, _ = Q.qallreduce_twoshot(list(parts.numpy()), 128)
+    elif arm == "fp16":
+        ref, _ = Q.fp16_allreduce(list(parts.numpy()))
+    else:
+        ref, _ = Q.bf16_allreduce(list(parts.numpy()))
+    want = (res0.numpy() + ref).astype(np.float32)
+    for r in range(k):
+        np.testing.assert_array_equal(outs[r].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
 def test_virtual_qallreduce_twoshot_bitexact(k):
     """Two-shot shared-scale int8 schedule (reading Q6): codes, scales and the result equal the
     oracle bit for bit on every rank; error within k max|x| / 254."""
@@ -351,9 +400,11 @@ def test_virtual_tp_mixer_int8_schedules_vs_oracle(k, sched):
 
 
 @pytest.mark.parametrize("k", [2, 4])
-def test_virtual_tp_mixer_fp16_ar2_vs_oracle(k):
+@pytest.mark.parametrize("wire", ["fp16", "bf16"])
+def test_virtual_tp_mixer_w16_ar2_vs_oracle(k, wire):
     dims = MED
-    outs, w, x, res, grp, sts = _tp_virtual(dims, "bf16", k, 2, 40, 4, L.SSM_AR2_FP16)
+    flags = L.SSM_AR2_FP16 if wire == "fp16" else L.SSM_AR2_BF16
+    outs, w, x, res, grp, sts = _tp_virtual(dims, "bf16", k, 2, 40, 4, flags)
     for r in range(1, k):
         assert torch.equal(outs[r], outs[0])
     ref, _ = M.mixer_forward(dims, np64(w), x.numpy(), res.numpy())

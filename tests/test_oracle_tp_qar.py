@@ -312,3 +312,54 @@ def test_fp16_error_bound_golden():
     err = abs(float(got[0]) - float(o[0]))
     assert err == g["fp16_tie_error"][0]
     assert err <= Q.fp16_error_bound([o])[0] <= err * (1 + 2.0 ** -10)   # attained up to 2^-25
+
+
+# ---------------------------------------------------------------- bf16-wire all-reduce (custom bf16 arm)
+def test_bf16_cast_golden():
+    """Hand-derived bfloat16 RNE cases (ties to even at several exponents)."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "bf16_cast.txt")
+    n = 0
+    for line in open(path):
+        if line.startswith("#") or not line.strip():
+            continue
+        a, b = (float(v) for v in line.split()[:2])
+        got = float(Q.bf16_cast(np.array([a], dtype=np.float32))[0])
+        assert got == b, (a, got, b)
+        n += 1
+    assert n == 8
+
+
+def test_bf16_cast_matches_torch_bfloat16():
+    """A second library's cast (torch CPU .bfloat16()) agrees element for element."""
+    import torch
+    rng = np.random.default_rng(6)
+    o = (rng.standard_normal(8192) * np.exp(rng.uniform(-40, 40, 8192))).astype(np.float32)
+    ref = torch.from_numpy(o).bfloat16().float().numpy()
+    np.testing.assert_array_equal(Q.bf16_cast(o), ref)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_bf16_allreduce_exact_and_bound(k):
+    rng = np.random.default_rng(200 + k)
+    parts = [(rng.integers(-128, 128, 512) * 2.0 ** -6).astype(np.float32) for _ in range(k)]
+    got, wire = Q.bf16_allreduce(parts)                      # bf16-exact partials, exact sums
+    np.testing.assert_array_equal(got.astype(np.float64), np.sum([p.astype(np.float64) for p in parts], axis=0))
+    parts = [(rng.standard_normal(8192) * np.exp(rng.uniform(-8, 8, 8192))).astype(np.float32) for _ in range(k)]
+    got, _ = Q.bf16_allreduce(parts)
+    exact = np.sum([p.astype(np.float64) for p in parts], axis=0)
+    err = np.abs(got.astype(np.float64) - exact)
+    bound = Q.bf16_error_bound(parts)
+    assert np.all(err <= bound)
+    assert np.max(err / bound) > 0.25                        # not vacuous
+
+
+def test_tp_bf16_ar2_within_bound():
+    dims = synth.CONFIGS["tiny"]
+    w = {k_: v.numpy() for k_, v in synth.layer_weights(dims, 0).items()}
+    x, res = synth.activations(2, 16, dims.d_model)
+    x, res = x.numpy(), res.numpy()
+    exact, _, _ = T.tp_mixer_forward(dims, w, x, res, 2, ar2="exact")
+    b16, _, _ = T.tp_mixer_forward(dims, w, x, res, 2, ar2="bf16")
+    d = np.abs(b16[0] - exact[0])
+    assert d.max() > 0
+    assert d.max() <= 2 * 2.0 ** -8 * np.abs(exact[0] - res).max() + 1e-6
