@@ -201,6 +201,15 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
                               const void* x_in, float* residual, int32_t batch,
                               uint32_t flags, void* workspace, size_t ws_bytes, void* stream);
 
+/* One pre-norm block of decode (PAPER.md:277-280 with the glue of reading Q16):
+ *   residual += mixer(RMSNorm(residual))      (RMSNorm weight 1, eps norm_eps)
+ * i.e. ssm_rmsnorm + ssm_mixer_decode with x_in in the workspace (the rmsnorm kernel, then the
+ * decode kernels; graph-capturable).  residual [batch, D] fp32 in/out, 16-B aligned; workspace >=
+ * ssm_workspace_bytes(batch, 1).  Errors as ssm_mixer_decode. */
+ssm_status_t ssm_mixer_decode_block(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, float* residual,
+                                    int32_t batch, float norm_eps, uint32_t flags, void* workspace, size_t ws_bytes,
+                                    void* stream);
+
 /* Quantised all-reduce of n fp32 values (n % qar_block == 0), rows of D = d_model:
  * every rank quantises its partial per block (s = amax/127, q = rint(o/s) clamped to
  * +-127), exchanges int8 codes + fp32 scales peer-to-peer, and forms

@@ -98,7 +98,7 @@ size_t h_total_bytes(const ssm_tp_s* t, int batch) {
 }
 
 struct WsLayout {
-  size_t xz, u, dbc, dlow, bc, delta, g, part, total;
+  size_t xz, u, dbc, dlow, bc, delta, g, part, xn, total;
 };
 
 WsLayout ws_layout(const ssm_tp_s* t, int64_t M) {
@@ -114,6 +114,7 @@ WsLayout ws_layout(const ssm_tp_s* t, int64_t M) {
   L.delta = take(M * t->Ek * es);
   L.g = take(M * t->Ek * es);
   L.part = take(t->k > 1 ? M * t->cfg.d_model * 4 : 0);
+  L.xn = take(M * t->cfg.d_model * es);                  // pre-norm output (ssm_mixer_decode_block)
   L.total = off;
   return L;
 }
@@ -227,8 +228,11 @@ Peers group_peers(const ssm_tp_s* t, int gsize) {
 }
 
 // One mixer layer. decode: seqlen == 1 path with in-place state update.
+// norm_res != NULL (decode blocks): x_in = RMSNorm(norm_res) (weight 1, eps norm_eps; reading
+// Q16) first, by the rmsnorm kernel.
 ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* st, const void* x_in, float* residual,
-                       int batch, int seqlen, uint32_t flags, void* ws, bool decode, cudaStream_t s) {
+                       int batch, int seqlen, uint32_t flags, void* ws, bool decode, cudaStream_t s,
+                       const float* norm_res = nullptr, float norm_eps = 0.f) {
   const ssm_config_t& c = t->cfg;
   const int64_t M = (int64_t)batch * seqlen;
   const int D = c.d_model, Ek = t->Ek, R = c.dt_rank, N = c.d_state, K = c.d_conv, P = t->P, hl = t->hloc;
@@ -305,6 +309,10 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   float* xacc = reinterpret_cast<float*>(reinterpret_cast<char*>(st->h) + xacc_offset(t, batch));
   const bool fuse = swap && !(flags & SSM_DECODE_UNFUSED) && batch <= 32 && P <= 320 && P % 2 == 0 && K >= 2 &&
                     K <= 4 && t->cph % 128 == 0 && gemm_tc_supported(w->w_in, D, x_in, D);
+  if (norm_res) {
+    t->launches++;
+    CU(launch_rmsnorm(bf, norm_res, nullptr, norm_eps, const_cast<void*>(x_in), M, D, s));
+  }
   {
     Probe pr(t, decode ? SSM_PROBE_IN_PROJ_DECODE : SSM_PROBE_IN_PROJ, s);
     if (fuse) {
@@ -689,6 +697,19 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
   PdlScope pdl(!(tp->flags & SSM_COMM_VIRTUAL));
   return run_layer(tp, w, st, x_in, residual, batch, 1, flags, workspace, true,
                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+ssm_status_t ssm_mixer_decode_block(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, float* residual,
+                                    int32_t batch, float norm_eps, uint32_t flags, void* workspace, size_t ws_bytes,
+                                    void* stream) {
+  ssm_status_t s = check_call(tp, w, st, residual, residual, batch, 1, flags, workspace, ws_bytes);
+  if (s != SSM_OK) return s;
+  if (!(norm_eps >= 0.f)) return fail(SSM_ERR_ARG, "norm_eps must be >= 0");
+  if (batch == 0) return SSM_OK;
+  PdlScope pdl(!(tp->flags & SSM_COMM_VIRTUAL));
+  void* xn = reinterpret_cast<char*>(workspace) + ws_layout(tp, batch).xn;
+  return run_layer(tp, w, st, xn, residual, batch, 1, flags, workspace, true, reinterpret_cast<cudaStream_t>(stream),
+                   residual, norm_eps);
 }
 
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {

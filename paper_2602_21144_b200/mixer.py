@@ -167,6 +167,13 @@ class TPMixer:
         L.call("ssm_mixer_decode", self.handle, C.byref(w.struct), state.handle, _ptr(x_in), _ptr(residual), B, flags,
                _ptr(ws), ws.numel(), _stream(stream))
 
+    def decode_block(self, w, state, residual, norm_eps=1e-5, flags=L.SSM_AR2_INT8, workspace=None, stream=None):
+        """One pre-norm decode block: residual += mixer(RMSNorm(residual)) (ssm_mixer_decode_block)."""
+        B = state.batch
+        ws = workspace if workspace is not None else self.workspace(B, 1)
+        L.call("ssm_mixer_decode_block", self.handle, C.byref(w.struct), state.handle, _ptr(residual), B,
+               C.c_float(norm_eps), flags, _ptr(ws), ws.numel(), _stream(stream))
+
     def qallreduce(self, partial, out, accumulate=False, stream=None, fp16=False, twoshot=False, bf16=False):
         """fp16=True: the paper's FP32 -> FP16 wire (PAPER.md:357) instead of int8 blocks;
         bf16=True: the custom bf16 wire."""

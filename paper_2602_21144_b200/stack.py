@@ -59,6 +59,7 @@ class MixerStack:
         self.graph = None
         self.graph_launches = 0
         self._graph_parity = 0
+        self.dec_flags = 0   # extra decode flags (SSM_DECODE_UNFUSED: cross-checks)
 
     def reset(self, stream=None):
         for s in self.states:
@@ -76,12 +77,13 @@ class MixerStack:
                 self._nccl_layer(lambda p: self.mx.prefill(lw, st, x, p, self.flags, self.ws, stream), res)
 
     def decode_step(self, res_t, stream=None):
-        """res_t: [batch, D] fp32, updated in place through all layers."""
+        """res_t: [batch, D] fp32, updated in place through all layers (ssm_mixer_decode_block:
+        pre-norm RMSNorm, then the layer's decode kernels)."""
         for lw, st in zip(self.layers, self.states):
-            self.mx.rmsnorm(res_t, self.xbuf_dec, None, self.eps, stream)
             if self.nccl is None:
-                self.mx.decode(lw, st, self.xbuf_dec, res_t, self.flags, self.ws_dec, stream)
+                self.mx.decode_block(lw, st, res_t, self.eps, self.flags | self.dec_flags, self.ws_dec, stream)
             else:
+                self.mx.rmsnorm(res_t, self.xbuf_dec, None, self.eps, stream)
                 self._nccl_layer(lambda p: self.mx.decode(lw, st, self.xbuf_dec, p, self.flags, self.ws_dec, stream),
                                  res_t)
 

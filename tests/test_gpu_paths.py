@@ -115,3 +115,44 @@ def test_generation_harness_logits_vs_oracle(k, arm):
     # the oracle's top-1 matches the harness's at (nearly) every position
     agree = (got.argmax(-1) == want.argmax(-1)).mean()
     assert agree >= 0.9
+
+
+@pytest.mark.parametrize("dims_name,B", [("med", 1), ("med", 16), ("med", 17), ("med", 32), ("med_falcon", 8),
+                                         ("med_zamba", 16), ("med_zamba_wide", 4)])
+def test_decode_block_variants_vs_oracle(dims_name, B):
+    """ssm_mixer_decode_block through MixerStack (eager steps): the default path (fused in_proj for
+    batch <= 32) and SSM_DECODE_UNFUSED (plain kernel chain) match the fp64 pre-norm stack and each
+    other."""
+    dims = {"med": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_layers=2),
+            "med_falcon": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, bcdt_rmsnorm=True, n_layers=2),
+            "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2, n_layers=2),
+            "med_zamba_wide": synth.MixerDims(d_model=256, d_inner=512, dt_rank=232, n_heads=2, n_layers=2)}[dims_name]
+    L_in, L_out = 10, 4
+    fulls = [synthetic_layer(dims, l) for l in range(2)]
+    ws = [_host_weights(f) for f in fulls]
+    g = torch.Generator().manual_seed(31)
+    res0 = torch.randn(B, L_in + L_out, dims.d_model, generator=g, dtype=torch.float64).float()
+    r0 = res0.double().numpy()
+    ref, _ = M.model_forward(dims, ws, r0)
+    got = {}
+    for name, fl in (("default", 0), ("unfused", L.SSM_DECODE_UNFUSED)):
+        mx = TPMixer(dims, "bf16")
+        lws = [LayerWeights(dims, f, 1, 0, "bf16").pack(mx) for f in fulls]
+        stack = MixerStack(mx, lws, B, L_in, L.SSM_AR2_INT8)
+        stack.dec_flags = fl
+        pre = res0[:, :L_in].cuda().contiguous().view(B * L_in, -1)
+        stack.prefill_chunk(pre)
+        outs = []
+        rt = torch.empty(B, dims.d_model, device="cuda")
+        for t in range(L_in, L_in + L_out):
+            rt.copy_(res0[:, t].cuda())
+            stack.decode_step(rt)
+            outs.append(rt.cpu().clone())
+        torch.cuda.synchronize()
+        dec = torch.stack(outs, 1).double().numpy()
+        assert rel(dec - r0[:, L_in:], ref[:, L_in:] - r0[:, L_in:]) < TOL["bf16"], name
+        assert (mx.fused_calls() > 0) == (name != "unfused" and B <= 32)
+        got[name] = dec
+    d_ref = got["unfused"] - r0[:, L_in:]
+    for name in ("default",):
+        assert rel(got[name] - r0[:, L_in:], d_ref) < (1e-2 if dims.bcdt_rmsnorm else 5e-3), name
