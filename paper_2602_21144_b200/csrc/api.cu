@@ -297,6 +297,14 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     odst = part;
   }
   const bool oacc = omode == OUT_RESID;  // out_proj accumulates into its destination
+  // int8 AR#2 schedule (reading Q6): two-shot with shared scales for k >= 4 and >= 64 tokens
+  const bool twoshot = omode == OUT_INT8 &&
+                       (flags & SSM_QAR_TWOSHOT || (!(flags & SSM_QAR_ONESHOT) && t->k >= 4 && M >= 64)) &&
+                       nD % (16 * t->k) == 0 &&
+                       2 * al256((size_t)nD / c.qar_block * 4) + al256(nD) + 2 * (size_t)nD / t->k <= half_bytes(t);
+  // one-shot int8 at prefill: the out_proj epilogue quantises its TMEM accumulator straight into the
+  // symmetric buffer (codes + per-block scales; no fp32 partial in HBM, no quantize kernel)
+  const bool qfuse = omode == OUT_INT8 && !twoshot && !swap && bf && gemm_tc_supported(g, Ek, w->w_out, Ek);
   // decode GEMMs (swap-AB): split-K with the fp32 atomic epilogue so the few weight-row tiles
   // spread over the SMs (measured best: ~1 unit per SM, <= 32 splits)
   const int ks_x = swap ? split_for(t, hl * P, Ek) : 1;
@@ -425,6 +433,11 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       // re-arm the x_proj accumulator (at TP > 1 the publish kernel re-zeroes it)
       if (fuse && !ar1) { e.zero = xacc; e.nzero = (int64_t)batch * hl * P; }
       CU(gemm(t, w->w_out, Ek, g, Ek, D, (int)M, Ek, ks_o, e, s, true, w->w_out_pk));
+    } else if (qfuse) {
+      Epilogue e = epi(EPI_QUANT_I8, 0, own_half(ep2), D);
+      e.qs = reinterpret_cast<float*>(own_half(ep2) + al256(nD));
+      e.qblk = c.qar_block;
+      CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, e, s));
     } else {
       CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D), s));
     }
@@ -449,10 +462,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->bytes_sent += nD * 2;
     CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
     CU(launch_w16_reduce(wbf, t->peers, t->k, half_off(ep2), nD, residual, 1, s));
-  } else if (omode == OUT_INT8 && (flags & SSM_QAR_TWOSHOT ||
-                                    (!(flags & SSM_QAR_ONESHOT) && t->k >= 4 && M >= 64)) &&
-             nD % (16 * t->k) == 0 &&
-             2 * al256((size_t)nD / c.qar_block * 4) + al256(nD) + 2 * (size_t)nD / t->k <= half_bytes(t)) {
+  } else if (twoshot) {
     // two-shot schedule with shared scales (reading Q6): (k-1)/k 3n B on the wire instead of (k-1) n
     Probe pr(t, SSM_PROBE_AR2, s);
     t->launches += 7;
@@ -463,8 +473,8 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     Probe pr(t, SSM_PROBE_AR2, s);
     int8_t* q = reinterpret_cast<int8_t*>(own_half(ep2));
     float* sc = reinterpret_cast<float*>(own_half(ep2) + al256(nD));
-    t->launches += 3;
-    CU(launch_quantize(part, nD, c.qar_block, q, sc, s));
+    t->launches += qfuse ? 2 : 3;
+    if (!qfuse) CU(launch_quantize(part, nD, c.qar_block, q, sc, s));
     t->ar_count++;
     t->bytes_sent += nD + nD / c.qar_block * 4;
     CU(launch_peer_barrier(t->peers, t->rank, t->k, s));

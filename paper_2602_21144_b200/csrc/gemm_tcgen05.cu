@@ -53,8 +53,9 @@ constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 
 // only the first epilogue half ever works) runs 4 epilogue warps -- a smaller CTA that fits next
 // to the decode-step blocks it follows
 constexpr int var_threads(int var) { return var == 2 ? 192 : kThreads; }
-// VAR 6: the prefill dt_proj with its softplus(+bias) epilogue fixed at compile time
-constexpr int var_kind(int var) { return var == 6 ? EPI_SOFTPLUS_BF16 : -1; }
+// VAR 6: the prefill dt_proj with its softplus(+bias) epilogue fixed at compile time; VAR 7: the
+// prefill out_proj with the int8 quantisation epilogue (EPI_QUANT_I8)
+constexpr int var_kind(int var) { return var == 6 ? EPI_SOFTPLUS_BF16 : var == 7 ? EPI_QUANT_I8 : -1; }
 
 // Work decomposition: unit u = (k-split, m-tile, n-tile), CTAs stride over units.
 struct TileSched {
@@ -222,6 +223,60 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
         if (n0 + j < N) atomicAdd(C + j, v[j]);
     }
   }
+}
+
+// ---- EPI_QUANT_I8: int8 per-block quantisation of the out_proj partial in its TMEM drain -------
+// (§4.4; reading Q6-Q8.)  The tile's rows are the TMEM lanes, a
+// row's qblk-column block spans qblk / 32 chunks of 32 columns that the two epilogue halves drain
+// alternately, so the drain runs twice: pass 1 writes each chunk's amax to shared memory
+// (s_am [128 rows][8 chunks]), pass 2 re-reads the accumulator, forms s = fl32(amax / 127) of the
+// chunk's block and stores the 32 codes (two 16-B stores) -- the same IEEE operations as
+// quantize_kernel, so codes and scales equal the fp32-partial route bit for bit.
+__device__ __forceinline__ void quant_epilogue(const Epilogue& e, int m0, int n_base, int BN, int M, int N,
+                                               uint32_t tbase, float* s_am) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = (warp - 2) >> 2, eg = warp & 3;
+  const int row = eg * 32 + lane, m = m0 + lane;
+  const int nch = BN / 32, cpb = e.qblk / 32;
+  for (int c = half; c < nch; c += 2) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tbase + c * 32, r);
+    tmem_ld_wait();
+    float am = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) am = fmaxf(am, fabsf(__uint_as_float(r[j])));
+    s_am[row * 8 + c] = am;
+  }
+  named_bar_sync(1, 256);
+  for (int c = half; c < nch; c += 2) {
+    const int n0 = n_base + c * 32;
+    const int b0 = (c / cpb) * cpb;
+    float A = 0.f;
+    for (int j = 0; j < cpb; ++j) A = fmaxf(A, s_am[row * 8 + b0 + j]);
+    const float s = __fdiv_rn(A, 127.0f);
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tbase + c * 32, r);
+    tmem_ld_wait();
+    if (m < M && n0 < N) {
+      uint32_t pk[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          int code = 0;
+          if (s != 0.f) code = max(-127, min(127, __float2int_rn(__fdiv_rn(__uint_as_float(r[4 * q + j]), s))));
+          w |= (uint32_t)(code & 0xff) << (8 * j);
+        }
+        pk[q] = w;
+      }
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(e.C) + (int64_t)m * e.ldc + n0);
+      dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      if (c % cpb == 0) e.qs[(int64_t)m * (N / e.qblk) + n0 / e.qblk] = s;
+    }
+  }
+  named_bar_sync(1, 256);  // s_am reused by the next tile
 }
 
 // ---- EPI_DECODE_INPROJ: decode in_proj epilogue fused with the conv step and x_proj ----------
@@ -540,6 +595,14 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         tc_fence_after();
         const int m0 = mt * BM + eg * 32;
         const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * cr.acc_stride);
+        if constexpr (VAR == 7) {
+          quant_epilogue(epi, m0, nt * BN, BN, M, N, tbase, reinterpret_cast<float*>(smem + cr.ring + 512));
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+          continue;
+        }
         for (int c = half; c < (BN + 31) / 32; c += 2) {
           uint32_t r[32];
           const int nc = nt * BN + c * 32;
@@ -645,7 +708,8 @@ cudaError_t pack_blocked(const __nv_bfloat16* w, int rows, int cols, int64_t ld,
 }
 
 #define SSM_GEMM_KERNELS (const void*)gemm_tc_kernel<0>, (const void*)gemm_tc_kernel<1>, (const void*)gemm_tc_kernel<1, 3>, \
-    (const void*)gemm_tc_kernel<1, 4>, (const void*)gemm_tc_kernel<2>, (const void*)gemm_tc_kernel<6>
+    (const void*)gemm_tc_kernel<1, 4>, (const void*)gemm_tc_kernel<2>, (const void*)gemm_tc_kernel<6>, \
+    (const void*)gemm_tc_kernel<7>
 
 cudaError_t preload_gemm_tc() {
   cudaError_t e = cudaSuccess;
@@ -672,6 +736,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   int n_tiles = (N + BN_MAX - 1) / BN_MAX;
   int BN = (N + n_tiles - 1) / n_tiles;
   BN = BN <= 16 ? 16 : (BN + 31) / 32 * 32;
+  if (epi.kind == EPI_QUANT_I8 && epi.qblk > 0) BN = (BN + epi.qblk - 1) / epi.qblk * epi.qblk;  // whole blocks
   n_tiles = (N + BN - 1) / BN;
   TileSched ts;
   ts.m_tiles = (M + BM - 1) / BM;
@@ -731,6 +796,15 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     extra = SU_BYTES + 128;  // u tile
     cr.ring -= SU_BYTES + 128;
   }
+  if (epi.kind == EPI_QUANT_I8) {
+    // whole qblk blocks inside every tile, 16-B aligned code rows, <= 8 chunks of amax per row
+    if (epi.trans || ts.ksplit != 1 || !epi.qs || BN > 256 || BN % 32 || N % epi.qblk ||
+        !(epi.qblk == 32 || epi.qblk == 64 || epi.qblk == 128 || epi.qblk == 256) || BN % epi.qblk ||
+        epi.ldc % 16 || (reinterpret_cast<uintptr_t>(epi.C) & 15))
+      return cudaErrorInvalidValue;
+    extra = 128 * 8 * 4;  // s_am
+    cr.ring -= extra;
+  }
   if (epi.zero && (reinterpret_cast<uintptr_t>(epi.zero) & 15)) return cudaErrorInvalidValue;
   while (kbs > 1 && num_stages(BN, kbs, cr.ring) < 2) --kbs;
   const int smem_bytes = 1024 + cr.ring + 512 + extra;
@@ -742,7 +816,8 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   if (epi.kind == EPI_DECODE_INPROJ) var = 1;
   else if (epi.kind == EPI_ATOMIC_F32 && epi.trans && BN <= 32) var = 2;
   else if (!epi.trans && epi.kind == EPI_SOFTPLUS_BF16) var = 6;
-  auto kfn = var == 2 ? gemm_tc_kernel<2> : var == 6 ? gemm_tc_kernel<6> : gemm_tc_kernel<0>;
+  else if (epi.kind == EPI_QUANT_I8) var = 7;
+  auto kfn = var == 2 ? gemm_tc_kernel<2> : var == 6 ? gemm_tc_kernel<6> : var == 7 ? gemm_tc_kernel<7> : gemm_tc_kernel<0>;
   if (var == 1) kfn = epi.P <= 64 * 3 ? gemm_tc_kernel<1, 3> : epi.P <= 64 * 4 ? gemm_tc_kernel<1, 4> : gemm_tc_kernel<1>;
   cudaError_t e_ = launch(kfn, grid, var_threads(var), smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi, A_blocked, lda, K,
                           cr, A_blocked ? 1 : 0);

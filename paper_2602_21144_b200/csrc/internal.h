@@ -19,6 +19,10 @@ enum EpiKind : int {
   EPI_ADD_F32 = 4,        // C f32 += acc            (read-modify-write; ksplit must be 1)
   EPI_ATOMIC_F32 = 5,     // C f32 += acc atomically (split-K; C pre-initialised)
   EPI_DECODE_INPROJ = 6,  // decode in_proj (swap-AB, bf16, N = batch <= 32), fused conv + x_proj; see below
+  EPI_QUANT_I8 = 7,       // int8 per-block quantisation of the accumulator (prefill out_proj at TP > 1, the
+                          // one-shot AR#2 schedule): per qblk consecutive columns n of a row m, amax = max |acc|,
+                          // s = fl32(amax / 127), code = clamp(rint(fl32(acc / s)), +-127) (0 if s == 0) ->
+                          // C (int8 [M][ldc]), s -> qs[m * (N / qblk) + n / qblk]; trans = 0, N % qblk == 0
 };
 
 struct Epilogue {
@@ -31,6 +35,9 @@ struct Epilogue {
   // buffer a LATER kernel accumulates into (saves a memset launch on the decode path).
   float* zero;
   int64_t nzero;
+  // EPI_QUANT_I8: per-block scales and block size (32 | 64 | 128 | 256, dividing the tile width)
+  float* qs;
+  int qblk;
   // EPI_DECODE_INPROJ (SURVEY.md §8 rows a1-a3 fused for one decode token).
   // Output rows m are in_proj features: m < Ek are x channels -> causal conv step over the cached
   // window cst + SiLU -> u (bf16 [N][Ek]) and the window shifted in place; Ek <= m < 2Ek are z

@@ -537,3 +537,39 @@ def test_empty_calls_are_noops_and_state_untouched():
     assert torch.equal(st.h, h0) and torch.equal(st.conv, c0) and torch.equal(r, r0)
     assert torch.all(zbuf == 7.0)
     del e
+
+
+@pytest.mark.parametrize("k,qblk", [(2, 128), (4, 128), (2, 64)])
+def test_prefill_out_proj_quant_epilogue_bitexact(k, qblk):
+    """a8 fused: at prefill with the one-shot int8 schedule the out_proj epilogue quantises its TMEM
+    accumulator straight into the symmetric buffer.  Its codes and scales must equal qar_ref's
+    quantisation of the rank's fp32 partial (taken from the same prefill run with SSM_AR2_EXTERNAL,
+    which writes that partial instead) bit for bit (reading Q6-Q8)."""
+    dims = MED
+    B, Lp = 2, 40
+    w = prep_weights(dims, 0, "bf16")
+    x, res = prep_acts(B, Lp, dims, "bf16", seed=23)
+    n = B * Lp * dims.d_model
+    parts, codes, scales = [], [], []
+    for mode in ("external", "int8"):
+        grp = VirtualGroup(dims, k, "bf16", B * Lp, qar_block=qblk)
+        lws = [LayerWeights(dims, w, k, r, "bf16") for r in range(k)]
+        sts = [State(grp.mixers[r], B) for r in range(k)]
+        wsp = [grp.mixers[r].workspace(B, Lp) for r in range(k)]
+        xp = [to_dev(x, "bf16").view(B * Lp, -1) for _ in range(k)]
+        rp = [res.float().cuda().contiguous().view(B * Lp, -1) for _ in range(k)]
+        fl = L.SSM_AR2_EXTERNAL if mode == "external" else (L.SSM_AR2_INT8 | L.SSM_QAR_ONESHOT)
+        torch.cuda.synchronize()
+        grp.run(lambda r, mx, s: mx.prefill(lws[r], sts[r], xp[r], rp[r], flags=fl, workspace=wsp[r], stream=s))
+        if mode == "external":
+            parts = [rp[r].cpu().numpy().reshape(-1) for r in range(k)]
+        else:
+            # epochs: AR#1 = 1 (half 1), AR#2 = 2 (half 0): codes at 256, scales at 256 + align256(n)
+            for r in range(k):
+                codes.append(grp.bufs[r][256:256 + n].cpu().view(torch.int8).numpy())
+                so = 256 + (n + 255) // 256 * 256
+                scales.append(grp.bufs[r][so:so + 4 * (n // qblk)].cpu().view(torch.float32).numpy())
+    for r in range(k):
+        q_ref, s_ref = Q.quantize_blocks(parts[r].astype(np.float32), qblk)
+        np.testing.assert_array_equal(scales[r], s_ref.reshape(-1))
+        np.testing.assert_array_equal(codes[r], q_ref.reshape(-1))
