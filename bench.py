@@ -37,6 +37,9 @@ def parse():
     p.add_argument("--ar2", default="int8", choices=["int8", "fp16", "bf16", "fp32", "nccl"],
                    help="AR#2: int8 / fp16 / bf16 / fp32 peer-to-peer (library), or nccl = NCCL bf16 all-reduce "
                         "baseline arm")
+    p.add_argument("--tp-design", default="split", choices=["split", "naive"],
+                   help="split = the paper's channel splitter (2 all-reduces per block); naive = the naive sharding "
+                        "baseline (2 all-gathers + 2 all-reduces per block, PAPER.md:297), TP > 1 only")
     p.add_argument("--prompt", type=int, default=0, help="override prompt length (smoke runs only)")
     p.add_argument("--decode", type=int, default=-1, help="override decode length (smoke runs only)")
     p.add_argument("--layers", type=int, default=0, help="override layer count (smoke runs only)")
@@ -253,6 +256,9 @@ def main():
     n_chunks = math.ceil(Lp / chunk)
     flags = {"int8": L.SSM_AR2_INT8, "fp16": L.SSM_AR2_FP16, "bf16": L.SSM_AR2_BF16, "fp32": L.SSM_AR2_FP32,
              "nccl": L.SSM_AR2_EXTERNAL}[args.ar2]
+    naive = args.tp_design == "naive" and k > 1
+    if naive:
+        flags |= L.SSM_TP_NAIVE
 
     peer_bufs, nbytes, symm = None, 0, None
     if k > 1:
@@ -269,7 +275,7 @@ def main():
     layers = []
     for l in range(n_layers):
         full = synthetic_layer(dims, l, device=dev)
-        lw = LayerWeights(dims, full, k, rank, "bf16", dev)
+        lw = LayerWeights(dims, full, k, rank, "bf16", dev, naive=naive)
         if not args.no_pack:
             lw.pack(mx)  # pre-tiled copies of w_in / w_x / w_out for the decode weight streams
         layers.append(lw)
@@ -446,6 +452,7 @@ def main():
                 "config": {"workload": f"{args.config}: {n_layers} layers, d_model {dims.d_model}, batch {B}, "
                                        f"prompt {Lp} + {Ld} decode", "model": args.config, "global_batch": B,
                            "seq_len": Lp + Ld, "parallelism": f"tp{k}", "ar2": args.ar2 if k > 1 else "none",
+                           "tp_design": args.tp_design if k > 1 else "none",
                            "prefill_chunk": chunk, "packed_decode_weights": not args.no_pack,
                            "l2": "inputs larger than L2 (prompt residual "
                                                          f"{B * Lp * D * 4 / 1e6:.0f} MB > 126 MB)"},

@@ -96,7 +96,17 @@ enum {
                               591-610): each rank casts its fp32 partial to bf16 (RNE), exchanges
                               it peer-to-peer, and every rank sums the k bf16 values in fp32 left
                               to right in rank order, added to the fp32 residual                 */
-  SSM_QAR_BF16 = 0x400      /* ssm_qallreduce: bf16 wire (as SSM_AR2_BF16); n % 8 == 0           */
+  SSM_QAR_BF16 = 0x400,     /* ssm_qallreduce: bf16 wire (as SSM_AR2_BF16); n % 8 == 0           */
+  SSM_TP_NAIVE = 0x1000     /* mixer calls, tp_size > 1, n_heads == 1: the paper's NAIVE sharding
+                              baseline (§4.2 "the number of communication
+                              collectives can grow to four per block"): W_in split uniformly
+                              along its packed first extent (w_in_naive), so (i) the in_proj
+                              output is all-gathered to rebuild the packed [x ; z] activation,
+                              (ii) the conv output is all-gathered to rebuild the full-width
+                              layout, then (iii) AR#1 on the x_proj partial and (iv) AR#2 at the
+                              residual boundary, as in the channel-split design.  Same result;
+                              four collectives per block instead of two.  Workspace:
+                              ssm_workspace_bytes_flags(..., SSM_TP_NAIVE).  Ablation arm only. */
 };
 
 enum { SSM_COMM_VIRTUAL = 0x1 }; /* ssm_comm_t.flags: all peer buffers live on THIS device
@@ -145,6 +155,9 @@ typedef struct {
   const void* w_in_pk;
   const void* w_x_pk;
   const void* w_out_pk;
+  /* SSM_TP_NAIVE only: [2E/k, D] rows [r 2E/k, (r+1) 2E/k) of the PACKED W_in [x ; z] -- the
+   * uniform split along the first extent that ignores the packed field boundary */
+  const void* w_in_naive;
 } ssm_layer_weights_t;
 
 typedef struct ssm_tp_s* ssm_tp_t;
@@ -166,8 +179,10 @@ ssm_status_t ssm_tp_destroy(ssm_tp_t tp);
  * max_tokens (= batch*seqlen) tokens. */
 ssm_status_t ssm_comm_bytes(const ssm_config_t* cfg, int32_t tp_size, int64_t max_tokens, size_t* bytes);
 
-/* Bytes of the per-call workspace for (batch, seqlen). */
+/* Bytes of the per-call workspace for (batch, seqlen); _flags: for calls with these flags
+ * (SSM_TP_NAIVE needs the gathered full-width activations, M (3 d_inner) elements more). */
 ssm_status_t ssm_workspace_bytes(ssm_tp_t tp, int32_t batch, int32_t seqlen, size_t* bytes);
+ssm_status_t ssm_workspace_bytes_flags(ssm_tp_t tp, int32_t batch, int32_t seqlen, uint32_t flags, size_t* bytes);
 
 /* SSM cache of one layer on this rank:
  *   conv window [batch][K-1][E_k] in cfg.dtype (raw x values, oldest first),

@@ -165,3 +165,72 @@ def tp_mixer_forward(dims, w, x_in, residual, k, states=None, ar2="exact", block
         stats["allreduce"] += 1
     out = residual + total
     return [out.copy() for _ in range(k)], new_states, stats
+
+
+def tp_mixer_forward_naive(dims, w, x_in, residual, k, states=None, stats=None):
+    """The paper's NAIVE sharding baseline (§4.2): "the number of communication
+    collectives can grow to four per block because packed intermediate tensors must be repeatedly
+    reassembled" -- (i) after the input projection, (ii) around the convolution branch, (iii)
+    after the SSM-parameter projection, (iv) when merging the SSM output (the residual boundary).
+    Reading N1: W_in is split uniformly along its PACKED first extent (rank r owns
+    rows [r 2E/k, (r+1) 2E/k) of [x ; z], straddling the field boundary), so (i) is an all-gather
+    of the packed activation; the conv weights follow the channels, so (ii) is an all-gather of the
+    conv output back to the full-width layout; (iii) and (iv) are the all-reduces of the channel-
+    split design (x_proj and out_proj partials over the rank's channels).  One block, TP = k,
+    Mamba/Falcon (one x_proj head).  Returns (outs, states', stats) with stats["allgather"],
+    stats["allreduce"] and stats["elements"] (elements each rank contributes, summed over the
+    collectives)."""
+    x_in, residual = np.asarray(x_in, np.float64), np.asarray(residual, np.float64)
+    Bsz, L, D = x_in.shape
+    E, N, K, R = dims.d_inner, dims.d_state, dims.d_conv, dims.dt_rank
+    assert dims.n_heads == 1 and E % k == 0
+    Ek, wn = E // k, 2 * E // k
+    if stats is None:
+        stats = {"allreduce": 0, "allgather": 0, "elements": 0}
+    w_in = np.asarray(w["w_in"])
+    if states is None:
+        states = [M.zero_state(Bsz, Ek, N, K) for _ in range(k)]
+    # (i) uniform slices of the packed in_proj, all-gathered into the full [x ; z]
+    xz_parts = [x_in @ w_in[r * wn:(r + 1) * wn].T for r in range(k)]
+    xz = np.concatenate(xz_parts, axis=-1)
+    stats["allgather"] += 1
+    stats["elements"] += Bsz * L * wn
+    x_full, z_full = xz[..., :E], xz[..., E:]
+    shards = [shard_weights(dims, w, k, r) for r in range(k)]
+    # (ii) conv on the owned channels, all-gathered back to the full width
+    us, convs = [], []
+    for r in range(k):
+        s = shards[r]
+        xc, conv_new = M.causal_conv1d(x_full[..., r * Ek:(r + 1) * Ek], s["conv_w"], s["conv_b"], states[r][0])
+        us.append(M.silu(xc))
+        convs.append(conv_new)
+    u_full = np.concatenate(us, axis=-1)
+    stats["allgather"] += 1
+    stats["elements"] += Bsz * L * Ek
+    # (iii) x_proj partials over the owned channels of the gathered layout, all-reduced
+    wx = np.asarray(w["w_x"])[0]
+    dbc = None
+    for r in range(k):
+        p = u_full[..., r * Ek:(r + 1) * Ek] @ wx[:, r * Ek:(r + 1) * Ek].T
+        dbc = p if dbc is None else dbc + p
+    stats["allreduce"] += 1
+    stats["elements"] += Bsz * L * (R + 2 * N)
+    dt_low, Bm, Cm = M.split_ssm_params(dbc, R, N)
+    if dims.bcdt_rmsnorm:
+        dt_low = M.rmsnorm(dt_low, eps=dims.rms_eps)
+        Bm = M.rmsnorm(Bm, eps=dims.rms_eps)
+        Cm = M.rmsnorm(Cm, eps=dims.rms_eps)
+    # local dt_proj / scan / gate on the owned channels, (iv) out_proj partials all-reduced
+    total, new_states = None, []
+    for r in range(k):
+        s = shards[r]
+        delta = M.softplus(dt_low @ s["w_dt"].T + s["b_dt"])
+        y, h_new = M.scan_full(us[r], delta, -np.exp(s["a_log"]), Bm, Cm, s["d_skip"], states[r][1])
+        g = y * M.silu(z_full[..., r * Ek:(r + 1) * Ek])
+        p = g @ s["w_out"].T
+        total = p if total is None else total + p
+        new_states.append((convs[r], h_new))
+    stats["allreduce"] += 1
+    stats["elements"] += Bsz * L * D
+    out = residual + total
+    return [out.copy() for _ in range(k)], new_states, stats

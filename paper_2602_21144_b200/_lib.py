@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libssmtp.so")
 SSM_BF16, SSM_FP32 = 0, 1
 SSM_AR2_INT8, SSM_AR2_FP32, SSM_AR2_EXTERNAL, SSM_AR2_FP16 = 0x1, 0x2, 0x4, 0x8
 SSM_QAR_ACCUMULATE, SSM_QAR_FP16, SSM_QAR_TWOSHOT, SSM_QAR_ONESHOT = 0x10, 0x20, 0x40, 0x80
-SSM_DECODE_UNFUSED, SSM_AR2_BF16, SSM_QAR_BF16 = 0x100, 0x200, 0x400
+SSM_DECODE_UNFUSED, SSM_AR2_BF16, SSM_QAR_BF16, SSM_TP_NAIVE = 0x100, 0x200, 0x400, 0x1000
 SSM_COMM_VIRTUAL = 0x1
 
 STATUS = {0: "SSM_OK", 1: "SSM_ERR_ARG", 2: "SSM_ERR_DIM", 3: "SSM_ERR_SHARD", 4: "SSM_ERR_RANK",
@@ -41,7 +41,8 @@ class ssm_comm_t(C.Structure):
 class ssm_layer_weights_t(C.Structure):
     _fields_ = [("w_in", C.c_void_p), ("conv_w", C.c_void_p), ("conv_b", C.c_void_p), ("w_x", C.c_void_p),
                 ("w_dt", C.c_void_p), ("b_dt", C.c_void_p), ("a_log", C.c_void_p), ("d_skip", C.c_void_p),
-                ("w_out", C.c_void_p), ("w_in_pk", C.c_void_p), ("w_x_pk", C.c_void_p), ("w_out_pk", C.c_void_p)]
+                ("w_out", C.c_void_p), ("w_in_pk", C.c_void_p), ("w_x_pk", C.c_void_p), ("w_out_pk", C.c_void_p),
+                ("w_in_naive", C.c_void_p)]
 
 
 def _load():
@@ -58,6 +59,7 @@ def _load():
         "ssm_tp_destroy": (st, [vp]),
         "ssm_comm_bytes": (st, [P(ssm_config_t), i32, i64, P(sz)]),
         "ssm_workspace_bytes": (st, [vp, i32, i32, P(sz)]),
+        "ssm_workspace_bytes_flags": (st, [vp, i32, i32, C.c_uint32, P(sz)]),
         "ssm_state_bytes": (st, [vp, i32, P(sz), P(sz)]),
         "ssm_state_alloc": (st, [vp, i32, vp, sz, vp, sz, vp, P(vp)]),
         "ssm_state_reset": (st, [vp, vp]),
@@ -91,6 +93,7 @@ def _load():
 
 LIB = _load()
 EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "ssm_comm_bytes", "ssm_workspace_bytes",
+            "ssm_workspace_bytes_flags",
             "ssm_state_bytes", "ssm_state_alloc", "ssm_state_reset", "ssm_state_free", "ssm_mixer_prefill",
             "ssm_mixer_decode", "ssm_mixer_decode_block", "ssm_qallreduce", "ssm_rmsnorm", "ssm_tp_check", "ssm_tp_stats", "ssm_tp_epoch",
             "ssm_tp_barrier", "ssm_tp_launch_count", "ssm_tp_fused_calls", "ssm_tp_probe", "ssm_tp_probe_read",

@@ -98,10 +98,11 @@ size_t h_total_bytes(const ssm_tp_s* t, int batch) {
 }
 
 struct WsLayout {
-  size_t xz, u, dbc, dlow, bc, delta, g, part, xn, total;
+  size_t xz, u, dbc, dlow, bc, delta, g, part, xn, xzf, uf, total;
 };
 
-WsLayout ws_layout(const ssm_tp_s* t, int64_t M) {
+// naive: + the all-gathered full-width activations of the SSM_TP_NAIVE arm (xz [M][2E], u [M][E])
+WsLayout ws_layout(const ssm_tp_s* t, int64_t M, bool naive = false) {
   WsLayout L{};
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += al256(bytes); return o; };
@@ -115,6 +116,8 @@ WsLayout ws_layout(const ssm_tp_s* t, int64_t M) {
   L.g = take(M * t->Ek * es);
   L.part = take(t->k > 1 ? M * t->cfg.d_model * 4 : 0);
   L.xn = take(M * t->cfg.d_model * es);                  // pre-norm output (ssm_mixer_decode_block)
+  L.xzf = take(naive ? M * 2 * t->cfg.d_inner * es : 0);
+  L.uf = take(naive ? M * t->cfg.d_inner * es : 0);
   L.total = off;
   return L;
 }
@@ -126,7 +129,10 @@ size_t payload_bytes(const ssm_config_t* c, int k, int64_t M) {
   size_t ar1 = (size_t)M * hloc * P * 4;
   size_t ar2q = al256((size_t)M * c->d_model) + (size_t)M * (c->d_model / (c->qar_block > 0 ? c->qar_block : 128)) * 4;
   size_t ar2f = (size_t)M * c->d_model * 4;
+  const size_t es = c->dtype == SSM_BF16 ? 2 : 4;
+  size_t agn = (size_t)M * 2 * (c->d_inner / k) * es;  // SSM_TP_NAIVE all-gather slices (in_proj, conv)
   size_t m = ar1 > ar2q ? ar1 : ar2q;
+  if (agn > m) m = agn;
   return al256(m > ar2f ? m : ar2f);
 }
 
@@ -237,7 +243,8 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   const int64_t M = (int64_t)batch * seqlen;
   const int D = c.d_model, Ek = t->Ek, R = c.dt_rank, N = c.d_state, K = c.d_conv, P = t->P, hl = t->hloc;
   const int bf = t->bf16;
-  const WsLayout L = ws_layout(t, M);
+  const bool naive = (flags & SSM_TP_NAIVE) != 0;
+  const WsLayout L = ws_layout(t, M, naive);
   char* W = reinterpret_cast<char*>(ws);
   void* xz = W + L.xz;
   void* u = W + L.u;
@@ -264,6 +271,17 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   // the same half for collective e - 2), so no symmetric half is written before this layer's
   // first barrier except by the collective that barrier belongs to.
   const bool ar1 = t->ar1_group > 1;
+  // SSM_TP_NAIVE: two all-gathers first (in_proj output, conv output), then AR#1 and AR#2
+  const uint32_t ep_ag1 = naive ? ++t->epoch : 0, ep_ag2 = naive ? ++t->epoch : 0;
+  const int E = c.d_inner, wn = 2 * E / t->k;  // naive: packed in_proj rows per rank
+  if (naive) {
+    t->ar_count += 2;
+    t->bytes_sent += M * wn * es + M * Ek * es;
+  }
+  // packed [x ; z] activation: rank-local [M][2E_k] (channel split) or the gathered [M][2E] (naive)
+  char* xzb = naive ? W + L.xzf : reinterpret_cast<char*>(xz);
+  const int64_t ldxz = naive ? 2 * E : 2 * Ek;
+  const int64_t xoff = naive ? (int64_t)t->rank * Ek : 0, zoff = naive ? E + (int64_t)t->rank * Ek : Ek;
   uint32_t ep1 = 0, ep2 = 0;
   float* xdst = dbc;
   if (ar1) {
@@ -307,7 +325,9 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   const bool qfuse = omode == OUT_INT8 && !twoshot && !swap && bf && gemm_tc_supported(g, Ek, w->w_out, Ek);
   // decode GEMMs (swap-AB): split-K with the fp32 atomic epilogue so the few weight-row tiles
   // spread over the SMs (measured best: ~1 unit per SM, <= 32 splits)
-  const int ks_x = swap ? split_for(t, hl * P, Ek) : 1;
+  // (naive decode: no split-K for x_proj -- its zero-fill of the AR#1 half would precede the
+  // all-gather barrier of the same half's previous use)
+  const int ks_x = swap && !naive ? split_for(t, hl * P, Ek) : 1;
   const int ks_o = swap ? split_for(t, D, Ek) : 1;
 
   // (a1) in_proj, column-parallel: xz = x_in W_in,r^T   [M, 2E_k]
@@ -315,7 +335,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
   // (a3) into the state's zeroed accumulator (at TP > 1 published to the symmetric buffer by
   // publish_barrier_kernel, which is also AR#1's barrier).
   float* xacc = reinterpret_cast<float*>(reinterpret_cast<char*>(st->h) + xacc_offset(t, batch));
-  const bool fuse = swap && !(flags & SSM_DECODE_UNFUSED) && batch <= 32 && P <= 320 && P % 2 == 0 && K >= 2 &&
+  const bool fuse = swap && !naive && !(flags & SSM_DECODE_UNFUSED) && batch <= 32 && P <= 320 && P % 2 == 0 && K >= 2 &&
                     K <= 4 && t->cph % 128 == 0 && gemm_tc_supported(w->w_in, D, x_in, D);
   if (norm_res) {
     t->launches++;
@@ -339,11 +359,24 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       e.cph = t->cph;
       if (!oacc) { e.zero = odst; e.nzero = nD; }  // out_proj partial target (local workspace)
       CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, e, s, true, w->w_in_pk));
+    } else if (naive) {
+      // (i) this rank's uniform slice of the packed in_proj -> own half, barrier, all-gather of the
+      // full packed activation [x ; z] ("after the input projection")
+      char* dst = own_half(ep_ag1);
+      if (swap)
+        CU(gemm(t, w->w_in_naive, D, x_in, D, wn, (int)M, D, 1, epi(kst, 1, dst, wn), s, true));
+      else
+        CU(gemm(t, x_in, D, w->w_in_naive, D, (int)M, wn, D, 1, epi(kst, 0, dst, wn), s));
+      t->launches += 2;
+      CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
+      CU(launch_gather_cols(t->peers, t->k, half_off(ep_ag1), M, (int)(wn * es), xzb, ldxz * (int64_t)es, s));
     } else if (swap)
       CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s, true, w->w_in_pk));
     else
       CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, epi(kst, 0, xz, 2 * Ek), s));
   }
+  // naive: the conv output goes to this rank's half for the second all-gather
+  if (naive) u = own_half(ep_ag2);
 
   // (a2) conv1d + SiLU, rank-local; conv window of the cache updated
   if (decode && !fuse) {
@@ -358,23 +391,34 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     if ((n1 & 3) && n1) { CU(cudaMemsetAsync(z1, 0, n1 * 4, s)); n1 = 0; }
     Probe pr(t, SSM_PROBE_CONV, s);
     t->launches++;
-    CU(launch_conv_decode(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, Ek, K, z0, n0, z1, n1,
-                          nullptr, s));
+    CU(launch_conv_decode(bf, xzb + xoff * es, ldxz, st->conv, w->conv_w, w->conv_b, u, Ek, batch, Ek, K, z0, n0, z1,
+                          n1, nullptr, s));
   } else if (!decode) {
     Probe pr(t, SSM_PROBE_CONV, s);
     t->launches += 2;
-    CU(launch_conv1d_silu(bf, xz, 2 * Ek, st->conv, w->conv_w, w->conv_b, u, Ek, batch, seqlen, Ek, K, s));
-    CU(launch_conv_state_update(bf, xz, 2 * Ek, st->conv, batch, seqlen, Ek, K, s));
+    CU(launch_conv1d_silu(bf, xzb + xoff * es, ldxz, st->conv, w->conv_w, w->conv_b, u, Ek, batch, seqlen, Ek, K, s));
+    CU(launch_conv_state_update(bf, xzb + xoff * es, ldxz, st->conv, batch, seqlen, Ek, K, s));
+  }
+  // (ii) naive: barrier, all-gather of the full-width conv output ("around the
+  // convolution branch"); the x_proj partial then reads this rank's slice of the gathered layout
+  const void* ux = u;
+  int64_t ldux = Ek;
+  if (naive) {
+    t->launches += 2;
+    CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
+    CU(launch_gather_cols(t->peers, t->k, half_off(ep_ag2), M, (int)(Ek * es), W + L.uf, (int64_t)E * es, s));
+    ux = W + L.uf + xoff * es;
+    ldux = E;
   }
 
   // (a3) x_proj partial [M, hloc*P] fp32, straight into the symmetric buffer when AR#1 follows
   if (!fuse) {
     Probe pr(t, SSM_PROBE_X_PROJ, s);
     if (swap)
-      CU(gemm(t, w->w_x, Ek, u, Ek, hl * P, (int)M, Ek, ks_x,
-              epi(ks_x != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s, true, w->w_x_pk));
+      CU(gemm(t, w->w_x, Ek, ux, ldux, hl * P, (int)M, Ek, ks_x,
+              epi(ks_x != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s, true, naive ? nullptr : w->w_x_pk));
     else
-      CU(gemm(t, u, Ek, w->w_x, Ek, (int)M, hl * P, Ek, 1, epi(EPI_STORE_F32, 0, xdst, hl * P), s));
+      CU(gemm(t, ux, ldux, w->w_x, Ek, (int)M, hl * P, Ek, 1, epi(EPI_STORE_F32, 0, xdst, hl * P), s));
   }
 
   // (a4) AR#1: barrier, then the fixed-order sum is done by its consumer
@@ -398,9 +442,8 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     // (a4)-(a7) decode: AR#1 sum + unpack + dt_proj + softplus + scan step + gate, one kernel
     Probe pr(t, SSM_PROBE_DECODE_STEP, s);
     t->launches++;
-    CU(launch_decode_step(bf, dsrc, nsrc, doff, hl * P, c.bcdt_rmsnorm, c.rms_eps, u,
-                          reinterpret_cast<char*>(xz) + Ek * es, 2 * Ek, w->w_dt, w->b_dt, w->a_log, w->d_skip, st->h,
-                          g, batch, Ek, R, N, t->cph, nullptr, s));
+    CU(launch_decode_step(bf, dsrc, nsrc, doff, hl * P, c.bcdt_rmsnorm, c.rms_eps, u, xzb + zoff * es, ldxz, w->w_dt,
+                          w->b_dt, w->a_log, w->d_skip, st->h, g, batch, Ek, R, N, t->cph, nullptr, s));
   } else {
     // (a4) unpack dt_low / B / C; (a5) dt_proj + softplus; (a6)+(a7) scan, D skip, gate
     t->launches++;
@@ -419,7 +462,7 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       const int c0 = j * t->cph;
       t->launches++;
       CU(launch_scan(bf, bf, reinterpret_cast<char*>(u) + c0 * es, Ek, reinterpret_cast<char*>(delta) + c0 * es, Ek,
-                     reinterpret_cast<char*>(xz) + (Ek + c0) * es, 2 * Ek, BC + (size_t)j * M * 2 * N, 2 * N,
+                     xzb + (zoff + c0) * es, ldxz, BC + (size_t)j * M * 2 * N, 2 * N,
                      w->a_log + (size_t)c0 * N, w->d_skip + c0, st->h + (size_t)c0 * N, (int64_t)Ek * N,
                      reinterpret_cast<char*>(g) + c0 * es, Ek, batch, seqlen, t->cph, N, s));
     }
@@ -498,7 +541,7 @@ ssm_status_t check_call(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* 
   if ((reinterpret_cast<uintptr_t>(x_in) | reinterpret_cast<uintptr_t>(residual)) & 15)
     return fail(SSM_ERR_ARG, "x_in/residual must be 16-B aligned");
   if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_BF16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL |
-                          SSM_QAR_TWOSHOT | SSM_QAR_ONESHOT | SSM_DECODE_UNFUSED))
+                          SSM_QAR_TWOSHOT | SSM_QAR_ONESHOT | SSM_DECODE_UNFUSED | SSM_TP_NAIVE))
     return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
   if ((flags & SSM_QAR_TWOSHOT) && (flags & SSM_QAR_ONESHOT))
     return fail(SSM_ERR_ARG, "SSM_QAR_TWOSHOT and SSM_QAR_ONESHOT are exclusive");
@@ -506,7 +549,10 @@ ssm_status_t check_call(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* 
                     !!(flags & SSM_AR2_EXTERNAL);
   if (nmode > 1) return fail(SSM_ERR_ARG, "at most one AR#2 mode flag");
   const int64_t M = (int64_t)batch * seqlen;
-  const WsLayout L = ws_layout(t, M);
+  const bool naive = (flags & SSM_TP_NAIVE) != 0;
+  if (naive && (t->k < 2 || t->hloc != 1 || t->ar1_group < 2 || !w->w_in_naive))
+    return fail(SSM_ERR_UNSUPPORTED, "SSM_TP_NAIVE needs tp_size > 1, one x_proj head per rank and w_in_naive");
+  const WsLayout L = ws_layout(t, M, naive);
   if (M > 0 && (!ws || ws_bytes < L.total))
     return fail(SSM_ERR_ARG, "workspace %zu B < required %zu B", ws_bytes, L.total);
   if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(SSM_ERR_ARG, "workspace must be 256-B aligned");
@@ -633,6 +679,13 @@ ssm_status_t ssm_workspace_bytes(ssm_tp_t tp, int32_t batch, int32_t seqlen, siz
   if (!tp || !bytes) return fail(SSM_ERR_ARG, "NULL argument");
   if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
   *bytes = ws_layout(tp, (int64_t)batch * seqlen).total;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_workspace_bytes_flags(ssm_tp_t tp, int32_t batch, int32_t seqlen, uint32_t flags, size_t* bytes) {
+  if (!tp || !bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
+  *bytes = ws_layout(tp, (int64_t)batch * seqlen, (flags & SSM_TP_NAIVE) != 0).total;
   return SSM_OK;
 }
 

@@ -114,6 +114,10 @@ cudaError_t launch_w16_reduce(int bf16, Peers src, int k, int64_t off, int64_t n
                               cudaStream_t s);
 cudaError_t launch_qar_twoshot(Peers peers, int rank, int k, int64_t off, const float* x, int64_t n, int blk,
                                float* out, int accumulate, cudaStream_t s);
+// All-gather of column slices (naive TP arm): out[m][r * wbytes + j] = src_r[off + m * wbytes + j] for
+// every rank r < k, bytes j < wbytes (multiple of 16); out row stride ldo_bytes.
+cudaError_t launch_gather_cols(Peers src, int k, int64_t off, int64_t M, int wbytes, void* out, int64_t ldo_bytes,
+                               cudaStream_t s);
 // Cross-rank barrier: advance this rank's device-side epoch counter, write it into slot[rank]
 // of every peer's signal area, wait for all peers' slots in our own area to reach it
 // (bounded; sets the error word on timeout).

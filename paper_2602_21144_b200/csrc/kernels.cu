@@ -1030,6 +1030,8 @@ cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* o
 // Force-load every kernel of this translation unit (CUDA lazy loading would otherwise load
 // a kernel at its first launch, which can wait on a spinning peer barrier of another
 // virtual rank on the same device).
+__global__ void gather_cols_kernel(Peers src, int k, int64_t off, int64_t M, int wv, uint4* __restrict__ out,
+                                   int64_t ldo_v);
 cudaError_t preload_kernels() {
   cudaFuncAttributes a;
   const void* fns[] = {
@@ -1051,7 +1053,7 @@ cudaError_t preload_kernels() {
       (const void*)w16_cast_kernel<__half>, (const void*)w16_reduce_kernel<__half>,
       (const void*)w16_cast_kernel<__nv_bfloat16>, (const void*)w16_reduce_kernel<__nv_bfloat16>, (const void*)amax_kernel<4>,
       (const void*)quant_shared_kernel<4>, (const void*)rs16_kernel, (const void*)ag16_kernel,
-      (const void*)peer_barrier_kernel};
+      (const void*)peer_barrier_kernel, (const void*)gather_cols_kernel};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -1105,6 +1107,33 @@ cudaError_t launch_publish_barrier(Peers bufs, int rank, int k, float* xacc, int
                                    cudaStream_t s) {
   if ((reinterpret_cast<uintptr_t>(xacc) & 15) || (dst_off & 15)) return cudaErrorInvalidValue;
   { cudaError_t e_ = launch(publish_barrier_kernel, 1, 256, 0, s, bufs, rank, k, xacc, n, dst_off); if (e_ != cudaSuccess) return e_; }
+  return cudaGetLastError();
+}
+
+__global__ void gather_cols_kernel(Peers src, int k, int64_t off, int64_t M, int wv, uint4* __restrict__ out,
+                                   int64_t ldo_v) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t total = M * k * wv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / ((int64_t)k * wv);
+    const int rem = (int)(i % ((int64_t)k * wv));
+    const int r = rem / wv, j = rem % wv;
+    const uint4* sp = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(src.p[r]) + off);
+    out[m * ldo_v + (int64_t)r * wv + j] = sp[m * wv + j];
+  }
+}
+
+cudaError_t launch_gather_cols(Peers src, int k, int64_t off, int64_t M, int wbytes, void* out, int64_t ldo_bytes,
+                               cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if ((wbytes | ldo_bytes | off) & 15) return cudaErrorInvalidValue;
+  const int wv = wbytes / 16;
+  const int64_t total = M * k * wv;
+  const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  cudaError_t e_ = launch(gather_cols_kernel, blocks, 256, 0, s, src, k, off, M, wv, reinterpret_cast<uint4*>(out),
+                          ldo_bytes / 16);
+  if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
 }
 

@@ -44,7 +44,7 @@ class LayerWeights:
     x_proj is block-diagonal over the heads it touches.
     """
 
-    def __init__(self, dims, full, tp_size=1, rank=0, dtype="bf16", device="cuda"):
+    def __init__(self, dims, full, tp_size=1, rank=0, dtype="bf16", device="cuda", naive=False):
         lo, hi = channel_range(dims.d_inner, tp_size, rank)
         E, H = dims.d_inner, dims.n_heads
         Eh = E // H
@@ -72,6 +72,9 @@ class LayerWeights:
             "d_skip": dev(full["d_skip"][lo:hi], f32),
             "w_out": dev(full["w_out"][:, lo:hi], mat),
         }
+        if naive:  # the naive baseline's uniform split of the PACKED in_proj (SSM_TP_NAIVE)
+            wn = 2 * E // tp_size
+            self.tensors["w_in_naive"] = dev(full["w_in"][rank * wn:(rank + 1) * wn], mat)
         self.struct = L.ssm_layer_weights_t(**{k: v.data_ptr() for k, v in self.tensors.items()})
 
     def pack(self, mixer, stream=None):
@@ -145,13 +148,13 @@ class TPMixer:
             pass
 
     # ---- sizes
-    def workspace_bytes(self, batch, seqlen):
+    def workspace_bytes(self, batch, seqlen, flags=0):
         out = C.c_size_t()
-        L.call("ssm_workspace_bytes", self.handle, batch, seqlen, C.byref(out))
+        L.call("ssm_workspace_bytes_flags", self.handle, batch, seqlen, flags, C.byref(out))
         return out.value
 
-    def workspace(self, batch, seqlen):
-        n = self.workspace_bytes(batch, seqlen)
+    def workspace(self, batch, seqlen, flags=0):
+        n = self.workspace_bytes(batch, seqlen, flags)
         return torch.empty(max(n, 256), dtype=torch.uint8, device=self.device)
 
     # ---- compute

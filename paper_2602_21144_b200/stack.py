@@ -49,8 +49,8 @@ class MixerStack:
         self.nccl = nccl_group if flags == L.SSM_AR2_EXTERNAL else None
         d = mixer.dims
         dt = torch.bfloat16 if mixer.dtype == "bf16" else torch.float32
-        self.ws = mixer.workspace(batch, max_chunk)
-        self.ws_dec = mixer.workspace(batch, 1)
+        self.ws = mixer.workspace(batch, max_chunk, flags)
+        self.ws_dec = mixer.workspace(batch, 1, flags)
         self.xbuf = torch.empty((batch * max_chunk, d.d_model), dtype=dt, device=mixer.device)
         self.xbuf_dec = torch.empty((batch, d.d_model), dtype=dt, device=mixer.device)
         self.states = [State(mixer, batch) for _ in layers]

@@ -211,17 +211,17 @@ def test_api_errors_on_gpu():
 
 
 # ------------------------------------------------------------------ virtual TP (single GPU, k streams)
-def _tp_virtual(dims, dtype, k, B, L_in, L_out, flags, qar_block=128):
+def _tp_virtual(dims, dtype, k, B, L_in, L_out, flags, qar_block=128, naive=False):
     """All device inputs and workspaces are created BEFORE the ranks' work is enqueued:
     a pageable H2D copy or a cudaMalloc inside the enqueue loop can serialise against a
     spinning peer barrier of another virtual rank on the same device."""
     w = prep_weights(dims, 0, dtype)
     x, res = prep_acts(B, L_in + L_out, dims, dtype, seed=17)
     grp = VirtualGroup(dims, k, dtype, B * max(L_in, 1), qar_block)
-    lws = [LayerWeights(dims, w, k, r, dtype) for r in range(k)]
+    lws = [LayerWeights(dims, w, k, r, dtype, naive=naive) for r in range(k)]
     sts = [State(grp.mixers[r], B) for r in range(k)]
-    ws_p = [grp.mixers[r].workspace(B, L_in) for r in range(k)]
-    ws_d = [grp.mixers[r].workspace(B, 1) for r in range(k)]
+    ws_p = [grp.mixers[r].workspace(B, L_in, flags) for r in range(k)]
+    ws_d = [grp.mixers[r].workspace(B, 1, flags) for r in range(k)]
     xp = [to_dev(x[:, :L_in], dtype).view(B * L_in, -1) for _ in range(k)]
     rp = [res[:, :L_in].float().cuda().contiguous().view(B * L_in, -1) for _ in range(k)]
     xd = [[to_dev(x[:, t:t + 1], dtype).view(B, -1) for t in range(L_in, L_in + L_out)] for _ in range(k)]
@@ -573,3 +573,25 @@ def test_prefill_out_proj_quant_epilogue_bitexact(k, qblk):
         q_ref, s_ref = Q.quantize_blocks(parts[r].astype(np.float32), qblk)
         np.testing.assert_array_equal(scales[r], s_ref.reshape(-1))
         np.testing.assert_array_equal(codes[r], q_ref.reshape(-1))
+
+
+@pytest.mark.parametrize("k,dtype,ar2", [(2, "bf16", "int8"), (4, "bf16", "fp32"), (2, "fp32", "fp32")])
+def test_virtual_tp_naive_four_collectives_vs_oracle(k, dtype, ar2):
+    """NEXT-3 naive arm (SSM_TP_NAIVE): uniform split of the packed in_proj,
+    all-gather of the packed activation and of the conv output, then AR#1 and AR#2 -- four
+    collectives per block -- matches the oracle (tp_sim.tp_mixer_forward_naive == mixer_forward)
+    and replicates bitwise."""
+    dims = MED if dtype == "bf16" else synth.CONFIGS["tiny"]
+    flags = (L.SSM_AR2_INT8 if ar2 == "int8" else L.SSM_AR2_FP32) | L.SSM_TP_NAIVE
+    L_in, L_out = 24, 3
+    outs, w, x, res, grp, sts = _tp_virtual(dims, dtype, k, 2, L_in, L_out, flags, qar_block=min(128, dims.d_model),
+                                            naive=True)
+    for r in range(1, k):
+        assert torch.equal(outs[r], outs[0])
+    ref, st_ref = M.mixer_forward(dims, np64(w), x.numpy(), res.numpy())
+    resn = res.numpy()
+    tol = TOL[dtype] if ar2 != "int8" else TOL["bf16"]
+    assert rel(outs[0].double().numpy() - resn, ref - resn) < tol
+    h = np.concatenate([sts[r].h.cpu().double().numpy() for r in range(k)], 1)
+    assert rel(h, st_ref[1]) < tol
+    assert grp.mixers[0].stats()["allreduce"] == 4 * (1 + L_out)     # 2 all-gathers + 2 all-reduces per call

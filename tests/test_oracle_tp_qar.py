@@ -363,3 +363,28 @@ def test_tp_bf16_ar2_within_bound():
     d = np.abs(b16[0] - exact[0])
     assert d.max() > 0
     assert d.max() <= 2 * 2.0 ** -8 * np.abs(exact[0] - res).max() + 1e-6
+
+
+# ---------------------------------------------------------------- naive 4-collective baseline (§4.2)
+@pytest.mark.parametrize("k", [2, 4])
+def test_naive_tp_four_collectives_equals_single_rank(k):
+    """PAPER.md:297 ("can grow to four per block"), 306 ("lowers the required AllReduces from four
+    (under naive sharding) to two"): the naive arm computes the same block with 2 all-gathers + 2
+    all-reduces, moving strictly more data than the channel splitter's 2 all-reduces."""
+    dims = _tiny()
+    w = _np(synth.layer_weights(dims, 0))
+    x, res = synth.activations(2, 12, dims.d_model, seed=9)
+    ref, st_ref = M.mixer_forward(dims, w, x.numpy(), res.numpy())
+    outs, sts, st = T.tp_mixer_forward_naive(dims, w, x.numpy(), res.numpy(), k)
+    np.testing.assert_allclose(outs[0], ref, rtol=1e-12, atol=1e-12)
+    assert st["allgather"] == 2 and st["allreduce"] == 2
+    h = T.gather_state(sts)[1]
+    np.testing.assert_allclose(h, st_ref[1], rtol=1e-12, atol=1e-12)
+    _, _, st_opt = T.tp_mixer_forward(dims, w, x.numpy(), res.numpy(), k)
+    assert st_opt["allreduce"] == 2 and st_opt["allgather"] == 0
+    opt_elems = 2 * 12 * (dims.dt_rank + 2 * dims.d_state + dims.d_model)
+    assert st["elements"] > opt_elems
+    # the naive arm's in_proj split straddles the packed field boundary for every k (its rank 0 owns
+    # x rows only when k = 2, x and z rows of different channels otherwise) -- the §4.3 pitfall
+    wn = 2 * dims.d_inner // k
+    assert set(range(0, wn)) != set(T.in_proj_rows(dims.d_inner, k, 0))
