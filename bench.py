@@ -34,7 +34,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="mamba2.8b", choices=["mamba2.8b", "falcon7b", "zamba7b", "mamba2.8b-long"])
-    p.add_argument("--ar2", default="int8", choices=["int8", "fp16", "bf16", "fp32", "nccl"],
+    p.add_argument("--ar2", default="int8", choices=["int8", "int8-requant", "fp16", "bf16", "fp32", "nccl"],
                    help="AR#2: int8 / fp16 / bf16 / fp32 peer-to-peer (library), or nccl = NCCL bf16 all-reduce "
                         "baseline arm")
     p.add_argument("--tp-design", default="split", choices=["split", "naive"],
@@ -254,7 +254,7 @@ def main():
     while B * chunk > 65536 and chunk % 2 == 0:
         chunk //= 2
     n_chunks = math.ceil(Lp / chunk)
-    flags = {"int8": L.SSM_AR2_INT8, "fp16": L.SSM_AR2_FP16, "bf16": L.SSM_AR2_BF16, "fp32": L.SSM_AR2_FP32,
+    flags = {"int8": L.SSM_AR2_INT8, "int8-requant": L.SSM_AR2_INT8 | L.SSM_QAR_REQUANT, "fp16": L.SSM_AR2_FP16, "bf16": L.SSM_AR2_BF16, "fp32": L.SSM_AR2_FP32,
              "nccl": L.SSM_AR2_EXTERNAL}[args.ar2]
     naive = args.tp_design == "naive" and k > 1
     if naive:

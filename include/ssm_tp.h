@@ -97,7 +97,7 @@ enum {
                               it peer-to-peer, and every rank sums the k bf16 values in fp32 left
                               to right in rank order, added to the fp32 residual                 */
   SSM_QAR_BF16 = 0x400,     /* ssm_qallreduce: bf16 wire (as SSM_AR2_BF16); n % 8 == 0           */
-  SSM_TP_NAIVE = 0x1000     /* mixer calls, tp_size > 1, n_heads == 1: the paper's NAIVE sharding
+  SSM_TP_NAIVE = 0x1000,    /* mixer calls, tp_size > 1, n_heads == 1: the paper's NAIVE sharding
                               baseline (§4.2 "the number of communication
                               collectives can grow to four per block"): W_in split uniformly
                               along its packed first extent (w_in_naive), so (i) the in_proj
@@ -107,6 +107,13 @@ enum {
                               residual boundary, as in the channel-split design.  Same result;
                               four collectives per block instead of two.  Workspace:
                               ssm_workspace_bytes_flags(..., SSM_TP_NAIVE).  Ablation arm only. */
+  SSM_QAR_REQUANT = 0x2000  /* int8 schedule, LABELLED VARIANT (never the default; reading Q6):
+                              requantised two-shot -- per-rank scales as one-shot, the owner of
+                              each 1/k shard sums the k ranks' dequantised codes in fp32 (rank
+                              order) and requantises the sum with fresh per-block scales, then the
+                              requantised shards are all-gathered.  Wire 2 (k-1)/k n (1 + 4/blk) B
+                              per rank (k = 4: 1.55 n, 8: 1.80 n); bound 2 k max_r amax_r / 254.
+                              ssm_qallreduce and SSM_AR2_INT8 mixer calls; n % (k qar_block) == 0 */
 };
 
 enum { SSM_COMM_VIRTUAL = 0x1 }; /* ssm_comm_t.flags: all peer buffers live on THIS device

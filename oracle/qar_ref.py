@@ -177,3 +177,28 @@ def qallreduce_twoshot(partials, block):
         Q += q
     out = (s[..., None] * Q.astype(np.float32)).astype(np.float32)
     return out.reshape(ps[0].shape), codes, s
+
+
+# ---------------------------------------------------------------------------------------------
+# Requantised two-shot int8 schedule (a LABELLED variant, never the default):
+# every rank quantises its partial with its own per-block scales (as the one-shot scheme), the
+# owner of shard j dequantises and sums the k ranks' codes of its shard in fixed rank order in
+# fp32, RE-quantises that sum with a fresh per-block scale, and the requantised shard is all-gathered:
+#   S    = fl32(...fl32(fl32(s_0 q_0) + fl32(s_1 q_1)) ... + fl32(s_{k-1} q_{k-1}))
+#   q', s' = quantize_blocks(S);   out = fl32(s' q')
+# Wire per rank 2 (k-1)/k n (1 + 4/blk) B (k = 4: 1.55 n, k = 8: 1.80 n) at the price of a second
+# rounding: |out - sum_r o_r| <= sum_r s_r / 2 + s'/2 <= 2 k max_r amax_r / 254.
+
+def qallreduce_requant(partials, block):
+    """partials: k float32 arrays [..., n].  Returns (out float32, first-stage codes/scales lists,
+    requantised codes, requantised scales)."""
+    codes, scales, S = [], [], None
+    for o in partials:
+        q, s = quantize_blocks(np.asarray(o, dtype=np.float32), block)
+        codes.append(q)
+        scales.append(s)
+        d = (np.repeat(s, block, axis=-1) * q.astype(np.float32)).astype(np.float32)
+        S = d if S is None else (S + d).astype(np.float32)
+    q2, s2 = quantize_blocks(S, block)
+    out = (np.repeat(s2, block, axis=-1) * q2.astype(np.float32)).astype(np.float32)
+    return out, codes, scales, q2, s2

@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libssmtp.so")
 SSM_BF16, SSM_FP32 = 0, 1
 SSM_AR2_INT8, SSM_AR2_FP32, SSM_AR2_EXTERNAL, SSM_AR2_FP16 = 0x1, 0x2, 0x4, 0x8
 SSM_QAR_ACCUMULATE, SSM_QAR_FP16, SSM_QAR_TWOSHOT, SSM_QAR_ONESHOT = 0x10, 0x20, 0x40, 0x80
-SSM_DECODE_UNFUSED, SSM_AR2_BF16, SSM_QAR_BF16, SSM_TP_NAIVE = 0x100, 0x200, 0x400, 0x1000
+SSM_DECODE_UNFUSED, SSM_AR2_BF16, SSM_QAR_BF16, SSM_TP_NAIVE, SSM_QAR_REQUANT = 0x100, 0x200, 0x400, 0x1000, 0x2000
 SSM_COMM_VIRTUAL = 0x1
 
 STATUS = {0: "SSM_OK", 1: "SSM_ERR_ARG", 2: "SSM_ERR_DIM", 3: "SSM_ERR_SHARD", 4: "SSM_ERR_RANK",

@@ -315,14 +315,16 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     odst = part;
   }
   const bool oacc = omode == OUT_RESID;  // out_proj accumulates into its destination
-  // int8 AR#2 schedule (reading Q6): two-shot with shared scales for k >= 4 and >= 64 tokens
-  const bool twoshot = omode == OUT_INT8 &&
+  // int8 AR#2 schedule (reading Q6): two-shot with shared scales for k >= 4 and >= 64 tokens; the
+  // requantised two-shot only on request (labelled variant)
+  const bool requant = omode == OUT_INT8 && (flags & SSM_QAR_REQUANT) && nD % ((int64_t)t->k * c.qar_block) == 0;
+  const bool twoshot = omode == OUT_INT8 && !requant &&
                        (flags & SSM_QAR_TWOSHOT || (!(flags & SSM_QAR_ONESHOT) && t->k >= 4 && M >= 64)) &&
                        nD % (16 * t->k) == 0 &&
                        2 * al256((size_t)nD / c.qar_block * 4) + al256(nD) + 2 * (size_t)nD / t->k <= half_bytes(t);
   // one-shot int8 at prefill: the out_proj epilogue quantises its TMEM accumulator straight into the
   // symmetric buffer (codes + per-block scales; no fp32 partial in HBM, no quantize kernel)
-  const bool qfuse = omode == OUT_INT8 && !twoshot && !swap && bf && gemm_tc_supported(g, Ek, w->w_out, Ek);
+  const bool qfuse = omode == OUT_INT8 && !twoshot && !requant && !swap && bf && gemm_tc_supported(g, Ek, w->w_out, Ek);
   // decode GEMMs (swap-AB): split-K with the fp32 atomic epilogue so the few weight-row tiles
   // spread over the SMs (measured best: ~1 unit per SM, <= 32 splits)
   // (naive decode: no split-K for x_proj -- its zero-fill of the AR#1 half would precede the
@@ -505,6 +507,12 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->bytes_sent += nD * 2;
     CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
     CU(launch_w16_reduce(wbf, t->peers, t->k, half_off(ep2), nD, residual, 1, s));
+  } else if (requant) {  // requantised two-shot (labelled variant of reading Q6)
+    Probe pr(t, SSM_PROBE_AR2, s);
+    t->launches += 5;
+    t->ar_count++;
+    t->bytes_sent += 2 * (nD + nD / c.qar_block * 4) * (t->k - 1) / t->k;
+    CU(launch_qar_requant(t->peers, t->rank, t->k, half_off(ep2), part, nD, c.qar_block, residual, 1, s));
   } else if (twoshot) {
     // two-shot schedule with shared scales (reading Q6): (k-1)/k 3n B on the wire instead of (k-1) n
     Probe pr(t, SSM_PROBE_AR2, s);
@@ -541,7 +549,7 @@ ssm_status_t check_call(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* 
   if ((reinterpret_cast<uintptr_t>(x_in) | reinterpret_cast<uintptr_t>(residual)) & 15)
     return fail(SSM_ERR_ARG, "x_in/residual must be 16-B aligned");
   if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_BF16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL |
-                          SSM_QAR_TWOSHOT | SSM_QAR_ONESHOT | SSM_DECODE_UNFUSED | SSM_TP_NAIVE))
+                          SSM_QAR_TWOSHOT | SSM_QAR_ONESHOT | SSM_QAR_REQUANT | SSM_DECODE_UNFUSED | SSM_TP_NAIVE))
     return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
   if ((flags & SSM_QAR_TWOSHOT) && (flags & SSM_QAR_ONESHOT))
     return fail(SSM_ERR_ARG, "SSM_QAR_TWOSHOT and SSM_QAR_ONESHOT are exclusive");
@@ -777,7 +785,7 @@ ssm_status_t ssm_mixer_decode_block(ssm_tp_t tp, const ssm_layer_weights_t* w, s
 
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
   if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
-  const uint32_t known = SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_BF16 | SSM_QAR_TWOSHOT;
+  const uint32_t known = SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_BF16 | SSM_QAR_TWOSHOT | SSM_QAR_REQUANT;
   if (n == 0 && !(flags & ~known)) return SSM_OK;  // nothing to reduce
   if (!partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
   if (flags & ~known) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
@@ -794,6 +802,18 @@ ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_
     one.p[0] = const_cast<float*>(partial);
     tp->launches++;
     CU(launch_f32_reduce(one, 1, 0, (int64_t)n, out, acc, s));
+    return SSM_OK;
+  }
+  if (flags & SSM_QAR_REQUANT) {  // requantised two-shot int8 (labelled variant of reading Q6)
+    if (n % ((size_t)tp->k * blk) || blk % 16) return fail(SSM_ERR_DIM, "n=%zu not a multiple of tp_size*qar_block", n);
+    if (al256(n) + al256(n / blk * 4) + al256(n / tp->k) + n / tp->k / blk * 4 > half_bytes(tp))
+      return fail(SSM_ERR_ARG, "symmetric buffer too small for n=%zu", n);
+    const uint32_t ep = ++tp->epoch;
+    tp->launches += 5;
+    tp->ar_count++;
+    tp->bytes_sent += 2 * (n + n / blk * 4) * (tp->k - 1) / tp->k;
+    CU(launch_qar_requant(tp->peers, tp->rank, tp->k, (int64_t)(kSigBytes + (ep & 1) * half_bytes(tp)), partial,
+                          (int64_t)n, blk, out, acc, s));
     return SSM_OK;
   }
   if (flags & SSM_QAR_TWOSHOT) {  // shared-scale two-shot int8 (reading Q6)

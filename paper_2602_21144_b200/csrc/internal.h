@@ -107,6 +107,10 @@ cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float
 cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, int64_t n, int blk, float* out,
                               int accumulate, cudaStream_t s);
 cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s);
+// Requantised two-shot int8 (labelled variant of reading Q6): quantise, barrier, shard owner sums and
+// requantises, barrier, all-gather + dequantise; n % (k blk) == 0.
+cudaError_t launch_qar_requant(Peers peers, int rank, int k, int64_t off, const float* x, int64_t n, int blk,
+                               float* out, int accumulate, cudaStream_t s);
 // 16-bit wire: fp16 (bf16 == 0) or bf16 RNE cast of n fp32 values (n % 8 == 0), and the fixed-order
 // fp32 sum of the k ranks' 16-bit arrays.
 cudaError_t launch_w16_cast(int bf16, const float* x, int64_t n, void* out, cudaStream_t s);

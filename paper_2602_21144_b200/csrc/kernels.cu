@@ -685,6 +685,70 @@ __global__ void ag16_kernel(Peers src, int64_t sum_off, int64_t shard, int64_t n
   }
 }
 
+// ---------------------------------------------------------------- requantised two-shot int8 (labelled variant)
+// Stage 2 (shard owner): S = fl32 sum over ranks (fixed order) of fl32(s_r q_r), then per-block
+// requantisation (amax, s' = fl32(amax / 127), q' = clamp(rint(fl32(S / s')))) -- the operations of
+// qar_ref.qallreduce_requant.  One warp per block of blk = 32 VPL elements of this rank's shard.
+template <int VPL>
+__global__ void rq_reduce_kernel(Peers src, int k, int64_t q_off, int64_t s_off, int64_t lo, int64_t nb_shard,
+                                 int8_t* __restrict__ q2, float* __restrict__ s2) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= nb_shard) return;
+  constexpr int blk = 32 * VPL;
+  const int64_t e0 = lo + b * blk + lane * VPL, gb = lo / blk + b;
+  float acc[VPL];
+  for (int r = 0; r < k; ++r) {  // fixed rank order 0..k-1
+    const char* base = reinterpret_cast<const char*>(src.p[r]);
+    const float sr = reinterpret_cast<const float*>(base + s_off)[gb];
+    const int8_t* qr = reinterpret_cast<const int8_t*>(base + q_off) + e0;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const float d = __fmul_rn(sr, (float)qr[i]);
+      acc[i] = r == 0 ? d : __fadd_rn(acc[i], d);
+    }
+  }
+  float am = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) am = fmaxf(am, fabsf(acc[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  const float sp = __fdiv_rn(am, 127.0f);
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    int c = 0;
+    if (sp != 0.f) c = max(-127, min(127, __float2int_rn(__fdiv_rn(acc[i], sp))));
+    q2[b * blk + lane * VPL + i] = (int8_t)c;
+  }
+  if (lane == 0) s2[b] = sp;
+}
+
+// Stage 3 (all-gather): out[i] (+)= fl32(s'_o q'_o[i]) from the shard owner o = i / shard.
+__global__ void rq_gather_kernel(Peers src, int64_t q2_off, int64_t s2_off, int64_t shard, int64_t n16, int blk,
+                                 float* __restrict__ out, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n16) return;
+  const int64_t e0 = i * 16;
+  const int o = (int)(e0 / shard);
+  const char* base = reinterpret_cast<const char*>(src.p[o]);
+  const int64_t le = e0 - (int64_t)o * shard;
+  const int4 qv = *reinterpret_cast<const int4*>(base + q2_off + le);
+  const int8_t* qq = reinterpret_cast<const int8_t*>(&qv);
+  const float sp = reinterpret_cast<const float*>(base + s2_off)[le / blk];
+  float4* dst = reinterpret_cast<float4*>(out + e0);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float4 v = accumulate ? dst[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    v.x = __fadd_rn(v.x, __fmul_rn(sp, (float)qq[4 * q])); v.y = __fadd_rn(v.y, __fmul_rn(sp, (float)qq[4 * q + 1]));
+    v.z = __fadd_rn(v.z, __fmul_rn(sp, (float)qq[4 * q + 2])); v.w = __fadd_rn(v.w, __fmul_rn(sp, (float)qq[4 * q + 3]));
+    dst[q] = v;
+  }
+}
+
 // ---------------------------------------------------------------- 16-bit-wire all-reduces
 // fp16 (the paper's FP32 -> FP16 wire) and bf16 (the custom bf16 arm, SURVEY.md
 // §8(d)): cast 8 fp32 -> 8 16-bit values per thread (cvt.rn: IEEE round-to-nearest-even; fp16
@@ -1020,6 +1084,39 @@ cudaError_t launch_w16_reduce(int bf16, Peers src, int k, int64_t off, int64_t n
   return cudaGetLastError();
 }
 
+// Requantised two-shot (labelled variant).  Layout in every rank's half at byte offset `off`:
+// codes [n] i8 | scales [n/blk] f32 | requantised shard codes [n/k] i8 | shard scales [n/k/blk] f32.
+cudaError_t launch_qar_requant(Peers peers, int rank, int k, int64_t off, const float* x, int64_t n, int blk,
+                               float* out, int accumulate, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n % ((int64_t)k * blk) || blk % 16) return cudaErrorInvalidValue;
+  auto a256 = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+  const int64_t nb = n / blk, shard = n / k;
+  const int64_t o_q = off, o_s = o_q + a256(n), o_q2 = o_s + a256(nb * 4), o_s2 = o_q2 + a256(shard);
+  char* own = reinterpret_cast<char*>(peers.p[rank]);
+  cudaError_t e_ = launch_quantize(x, n, blk, reinterpret_cast<int8_t*>(own + o_q), reinterpret_cast<float*>(own + o_s), s);
+  if (e_ != cudaSuccess) return e_;
+  if ((e_ = launch_peer_barrier(peers, rank, k, s)) != cudaSuccess) return e_;
+  const int64_t nbs = shard / blk;
+  const int blocks = (int)((nbs * 32 + 255) / 256);
+#define RQR(VPL) e_ = launch(rq_reduce_kernel<VPL>, blocks, 256, 0, s, peers, k, o_q, o_s, (int64_t)rank * shard, nbs, \
+                             reinterpret_cast<int8_t*>(own + o_q2), reinterpret_cast<float*>(own + o_s2))
+  switch (blk) {
+    case 32: RQR(1); break;
+    case 64: RQR(2); break;
+    case 128: RQR(4); break;
+    case 256: RQR(8); break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef RQR
+  if (e_ != cudaSuccess) return e_;
+  if ((e_ = launch_peer_barrier(peers, rank, k, s)) != cudaSuccess) return e_;
+  const int64_t n16 = n / 16;
+  e_ = launch(rq_gather_kernel, (int)((n16 + 255) / 256), 256, 0, s, peers, o_q2, o_s2, shard, n16, blk, out, accumulate);
+  if (e_ != cudaSuccess) return e_;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const int64_t n4 = n / 4;
@@ -1053,7 +1150,9 @@ cudaError_t preload_kernels() {
       (const void*)w16_cast_kernel<__half>, (const void*)w16_reduce_kernel<__half>,
       (const void*)w16_cast_kernel<__nv_bfloat16>, (const void*)w16_reduce_kernel<__nv_bfloat16>, (const void*)amax_kernel<4>,
       (const void*)quant_shared_kernel<4>, (const void*)rs16_kernel, (const void*)ag16_kernel,
-      (const void*)peer_barrier_kernel, (const void*)gather_cols_kernel};
+      (const void*)peer_barrier_kernel, (const void*)gather_cols_kernel, (const void*)rq_reduce_kernel<1>,
+      (const void*)rq_reduce_kernel<2>, (const void*)rq_reduce_kernel<4>, (const void*)rq_reduce_kernel<8>,
+      (const void*)rq_gather_kernel};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;

@@ -177,12 +177,14 @@ class TPMixer:
         L.call("ssm_mixer_decode_block", self.handle, C.byref(w.struct), state.handle, _ptr(residual), B,
                C.c_float(norm_eps), flags, _ptr(ws), ws.numel(), _stream(stream))
 
-    def qallreduce(self, partial, out, accumulate=False, stream=None, fp16=False, twoshot=False, bf16=False):
+    def qallreduce(self, partial, out, accumulate=False, stream=None, fp16=False, twoshot=False, bf16=False,
+                   requant=False):
         """fp16=True: the paper's FP32 -> FP16 wire (PAPER.md:357) instead of int8 blocks;
-        bf16=True: the custom bf16 wire."""
+        bf16=True: the custom bf16 wire; twoshot / requant: the int8 two-shot schedules."""
         L.call("ssm_qallreduce", self.handle, _ptr(partial), _ptr(out), partial.numel(),
                (L.SSM_QAR_ACCUMULATE if accumulate else 0) | (L.SSM_QAR_FP16 if fp16 else 0) |
-               (L.SSM_QAR_BF16 if bf16 else 0) | (L.SSM_QAR_TWOSHOT if twoshot else 0), _stream(stream))
+               (L.SSM_QAR_BF16 if bf16 else 0) | (L.SSM_QAR_TWOSHOT if twoshot else 0) |
+               (L.SSM_QAR_REQUANT if requant else 0), _stream(stream))
 
     def rmsnorm(self, residual, out, weight=None, eps=1e-5, stream=None):
         L.call("ssm_rmsnorm", self.handle, _ptr(residual), _ptr(weight), C.c_float(eps), _ptr(out),

@@ -595,3 +595,42 @@ def test_virtual_tp_naive_four_collectives_vs_oracle(k, dtype, ar2):
     h = np.concatenate([sts[r].h.cpu().double().numpy() for r in range(k)], 1)
     assert rel(h, st_ref[1]) < tol
     assert grp.mixers[0].stats()["allreduce"] == 4 * (1 + L_out)     # 2 all-gathers + 2 all-reduces per call
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_virtual_qallreduce_requant_bitexact(k):
+    """Requantised two-shot (labelled variant, reading Q6): first-stage codes, the shard owners'
+    requantised codes/scales and the result equal qar_ref.qallreduce_requant bit for bit; error
+    within 2 k max|x| / 254."""
+    dims = MED
+    n = 6 * dims.d_model * k // 2 * 2
+    n -= n % (k * 128)
+    parts = synth.partials(k, n, seed=500 + k)
+    grp = VirtualGroup(dims, k, "bf16", 64)
+    outs = [torch.empty(n, device="cuda") for _ in range(k)]
+    dev_parts = [parts[r].cuda() for r in range(k)]
+    grp.run(lambda r, mx, s: mx.qallreduce(dev_parts[r], outs[r], stream=s, requant=True))
+    ref, codes, scales, q2, s2 = Q.qallreduce_requant(list(parts.numpy()), 128)
+    half = ((grp.bufs[0].numel() - 256) // 2) & ~255
+    a256 = lambda b: (b + 255) // 256 * 256
+    shard = n // k
+    for r in range(k):
+        base = 256 + half  # epoch 1 -> half 1: codes | scales | shard codes | shard scales
+        q = grp.bufs[r][base:base + n].cpu().view(torch.int8).numpy()
+        np.testing.assert_array_equal(q, codes[r])
+        o2 = base + a256(n) + a256(4 * (n // 128))
+        qs = grp.bufs[r][o2:o2 + shard].cpu().view(torch.int8).numpy()
+        np.testing.assert_array_equal(qs, q2[r * shard:(r + 1) * shard])
+        np.testing.assert_array_equal(outs[r].cpu().numpy(), ref)
+    exact = parts.double().sum(0).numpy()
+    assert np.all(np.abs(outs[0].cpu().double().numpy() - exact) <= 2 * Q.northstar_bound(list(parts.numpy()), 128) * (1 + 1e-5))
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_virtual_tp_mixer_requant_vs_oracle(k):
+    outs, w, x, res, grp, sts = _tp_virtual(MED, "bf16", k, 2, 40, 4, L.SSM_AR2_INT8 | L.SSM_QAR_REQUANT)
+    for r in range(1, k):
+        assert torch.equal(outs[r], outs[0])
+    ref, _ = M.mixer_forward(MED, np64(w), x.numpy(), res.numpy())
+    resn = res.numpy()
+    assert rel(outs[0].double().numpy() - resn, ref - resn) < TOL["bf16"]

@@ -388,3 +388,37 @@ def test_naive_tp_four_collectives_equals_single_rank(k):
     # x rows only when k = 2, x and z rows of different channels otherwise) -- the §4.3 pitfall
     wn = 2 * dims.d_inner // k
     assert set(range(0, wn)) != set(T.in_proj_rows(dims.d_inner, k, 0))
+
+
+# ---------------------------------------------------------------- requantised two-shot (labelled variant)
+def test_requant_golden():
+    rows = [list(map(float, l.split())) for l in open(os.path.join(os.path.dirname(__file__), "golden", "qar_requant.txt"))
+            if l.strip() and not l.startswith("#")]
+    o0, o1 = (np.array(r, dtype=np.float32) for r in rows[:2])
+    out, codes, scales, q2, s2 = Q.qallreduce_requant([o0, o1], 4)
+    np.testing.assert_array_equal(q2.astype(np.int64), np.array(rows[2], dtype=np.int64))
+    np.testing.assert_array_equal(out, np.array(rows[3], dtype=np.float32))
+    assert float(s2[0]) == rows[4][0]
+    np.testing.assert_array_equal(codes[1], np.array([127, 16, 1, -3], np.int8))
+
+
+def test_requant_k1_reproduces_oneshot():
+    """k = 1: the dequantised codes are multiples of s with the block maximum at 127 s, so the
+    requantisation returns the same codes and scale."""
+    rng = np.random.default_rng(12)
+    o = (rng.standard_normal(2048) * np.exp(rng.uniform(-3, 3, 2048))).astype(np.float32)
+    out, codes, scales, q2, s2 = Q.qallreduce_requant([o], 128)
+    np.testing.assert_array_equal(q2, codes[0])
+    np.testing.assert_array_equal(s2, scales[0])
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_requant_within_twice_northstar_bound(k):
+    rng = np.random.default_rng(70 + k)
+    parts = [(rng.standard_normal(4096) * np.exp(rng.uniform(-2, 2, 4096))).astype(np.float32) for _ in range(k)]
+    out, *_ = Q.qallreduce_requant(parts, 128)
+    exact = np.sum([p.astype(np.float64) for p in parts], axis=0)
+    err = np.abs(out.astype(np.float64) - exact)
+    bound = 2 * Q.northstar_bound(parts, 128)
+    assert np.all(err <= bound * (1 + 1e-6))
+    assert np.max(err / Q.northstar_bound(parts, 128)) > 0.5       # the second rounding shows
