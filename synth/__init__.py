@@ -124,3 +124,42 @@ def partials(k: int, n: int, seed: int = 7, scale: float = 1.0):
 def bf16_round(t: torch.Tensor) -> torch.Tensor:
     """Round to bf16 and back to float64 (input preparation for bf16-mode parity)."""
     return t.to(torch.bfloat16).to(torch.float64)
+
+
+# ---------------------------------------------------------------------------------------------
+# Zamba's shared transformer block (SURVEY.md §8(f) NEXT-1): dimensions and seeded weights.
+@dataclass(frozen=True)
+class AttnDims:
+    d_model: int            # D; the block's input is concat(h, h0): 2 D
+    n_heads: int            # H; head_dim = 2 D / H
+    intermediate: int       # MLP width I
+    eps: float = 1e-5
+
+    @property
+    def head_dim(self) -> int:
+        return 2 * self.d_model // self.n_heads
+
+
+# Zamba-7B (HF ZambaConfig defaults): hidden 3712, attention hidden 7424, 16 heads of 464, MLP 14848,
+# GELU, hybrid (shared-attention) layers at these indices of the 76
+ZAMBA7B_ATTN = AttnDims(d_model=3712, n_heads=16, intermediate=14848)
+ZAMBA7B_HYBRID_LAYERS = (2, 7, 13, 19, 25, 31, 37, 43, 49, 55, 61, 67, 73)
+
+
+def shared_block_weights(adims: AttnDims, seed: int = 3000, layer: int = 0) -> dict:
+    """Weights of the shared block (float64 CPU; nn.Linear [out, in]) plus one hybrid layer's
+    linear (seed + layer): RMSNorm weights 1 + N(0, 0.1) (so a dropped weight shows), the
+    projections U(+-1/sqrt(fan_in)), w_lin scaled by 1/4 (the block's output is added to the
+    Mamba layer's input)."""
+    g = torch.Generator().manual_seed(seed)
+    D, H, I = adims.d_model, adims.n_heads, adims.intermediate
+    A = 2 * D
+    w = {"norm1": 1.0 + 0.1 * torch.randn((A,), generator=g, dtype=torch.float64),
+         "w_q": _u(g, (A, A), 1.0 / math.sqrt(A)), "w_k": _u(g, (A, A), 1.0 / math.sqrt(A)),
+         "w_v": _u(g, (A, A), 1.0 / math.sqrt(A)), "w_o": _u(g, (D, A), 1.0 / math.sqrt(A)),
+         "norm2": 1.0 + 0.1 * torch.randn((D,), generator=g, dtype=torch.float64),
+         "w_g": _u(g, (I, D), 1.0 / math.sqrt(D)), "w_u": _u(g, (I, D), 1.0 / math.sqrt(D)),
+         "w_d": _u(g, (D, I), 1.0 / math.sqrt(I))}
+    g2 = torch.Generator().manual_seed(seed + 1 + layer)
+    w["w_lin"] = _u(g2, (D, D), 1.0 / math.sqrt(D)) / 4.0
+    return w
