@@ -107,13 +107,15 @@ enum {
                               residual boundary, as in the channel-split design.  Same result;
                               four collectives per block instead of two.  Workspace:
                               ssm_workspace_bytes_flags(..., SSM_TP_NAIVE).  Ablation arm only. */
-  SSM_QAR_REQUANT = 0x2000  /* int8 schedule, LABELLED VARIANT (never the default; reading Q6):
+  SSM_QAR_REQUANT = 0x2000, /* int8 schedule, LABELLED VARIANT (never the default; reading Q6):
                               requantised two-shot -- per-rank scales as one-shot, the owner of
                               each 1/k shard sums the k ranks' dequantised codes in fp32 (rank
                               order) and requantises the sum with fresh per-block scales, then the
                               requantised shards are all-gathered.  Wire 2 (k-1)/k n (1 + 4/blk) B
                               per rank (k = 4: 1.55 n, 8: 1.80 n); bound 2 k max_r amax_r / 254.
                               ssm_qallreduce and SSM_AR2_INT8 mixer calls; n % (k qar_block) == 0 */
+  SSM_QAR_FP32 = 0x4000     /* ssm_qallreduce: exact fp32 one-shot (no quantisation), fixed rank
+                              order; n % 4 == 0                                                  */
 };
 
 enum { SSM_COMM_VIRTUAL = 0x1 }; /* ssm_comm_t.flags: all peer buffers live on THIS device
@@ -231,6 +233,55 @@ ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_sta
 ssm_status_t ssm_mixer_decode_block(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, float* residual,
                                     int32_t batch, float norm_eps, uint32_t flags, void* workspace, size_t ws_bytes,
                                     void* stream);
+
+/* ---- Zamba's shared transformer block ------------------
+ * Zamba runs one shared attention + MLP block before its 13 "hybrid" Mamba layers (the public
+ * model definition, HF modeling_zamba.py: ZambaAttentionDecoderLayer + the hybrid layer's linear):
+ *   x = RMSNorm_1(concat(h, h0)); q, k, v = x W_qkv^T (H heads of d = 2 D / H, no rotary)
+ *   o = causal softmax(q k^T / sqrt(d / 2)) v over the KV cache; a = o W_o^T
+ *   y = RMSNorm_2(a); m = (GELU(y W_g^T) * y W_u^T) W_d^T; t = m W_lin^T
+ * and the hybrid layer's Mamba block then runs on RMSNorm(h + t) (ssm_rmsnorm_add) with residual h.
+ * Tensor parallel (reading Z1): rank r owns heads [r H/k, (r+1) H/k) and MLP columns
+ * [r I/k, (r+1) I/k) (column-parallel q/k/v and gate/up, row-parallel o and down, each followed by
+ * an all-reduce; W_lin replicated).  bf16 handles only; d_model = the handle's d_model. */
+typedef struct {
+  int32_t n_heads;        /* H (global)                                                       */
+  int32_t intermediate;   /* I (global)                                                       */
+  float eps;              /* both RMSNorms (Zamba: 1e-5)                                      */
+  int32_t max_seq;        /* KV cache capacity in tokens per sequence                         */
+} ssm_attn_config_t;
+typedef struct {          /* rank-local shards, bf16 matrices nn.Linear [out, in], fp32 vectors */
+  const float* norm1;     /* [2D]                                                             */
+  const void* w_qkv;      /* [3 (H/k) d, 2D]: rows q | k | v of the owned heads               */
+  const void* w_o;        /* [D, (H/k) d]                                                     */
+  const float* norm2;     /* [D]                                                              */
+  const void* w_gu;       /* [2 I/k, D]: rows gate | up of the owned MLP columns              */
+  const void* w_d;        /* [D, I/k]                                                         */
+  const void* w_lin;      /* [D, D] (replicated)                                              */
+} ssm_attn_weights_t;
+typedef struct ssm_kv_s* ssm_kv_t;
+/* KV cache of one shared-block application on this rank: caller-owned device buffer of
+ * ssm_kv_bytes (256-B header with the device-side length, then K and V [batch][max_seq][H/k][d]
+ * bf16); alloc binds and zero-fills it; reset empties it.  Calls append to it (prefill chunks,
+ * decode tokens); the length lives in device memory, so a captured decode graph keeps appending. */
+ssm_status_t ssm_kv_bytes(ssm_tp_t tp, const ssm_attn_config_t* acfg, int32_t batch, size_t* bytes);
+ssm_status_t ssm_kv_alloc(ssm_tp_t tp, const ssm_attn_config_t* acfg, int32_t batch, void* buf, size_t bytes,
+                          void* stream, ssm_kv_t* out);
+ssm_status_t ssm_kv_reset(ssm_kv_t kv, void* stream);
+ssm_status_t ssm_kv_free(ssm_kv_t kv);
+ssm_status_t ssm_attn_workspace_bytes(ssm_tp_t tp, const ssm_attn_config_t* acfg, int32_t batch, int32_t seqlen,
+                                      size_t* bytes);
+/* t_out [batch*seqlen, D] fp32 := the block applied to h, h0 [batch*seqlen, D] fp32 (row = b L + t);
+ * the call's K, V are appended to kv (SSM_ERR_PROTOCOL from ssm_tp_check if max_seq overflows).
+ * flags: the two all-reduces at TP > 1: SSM_AR2_FP32 (exact, default when 0), SSM_AR2_INT8,
+ * SSM_AR2_FP16, SSM_AR2_BF16.  Collective at TP > 1 (two all-reduces). */
+ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ssm_attn_weights_t* w, ssm_kv_t kv,
+                            const float* h, const float* h0, float* t_out, int32_t batch, int32_t seqlen,
+                            uint32_t flags, void* workspace, size_t ws_bytes, void* stream);
+/* x = RMSNorm(a + b) * weight (b may be NULL, weight may be NULL = ones), a, b fp32 [M, D] ->
+ * x [M, D] in the handle's dtype: the hybrid layer's Mamba pre-norm of h + t. */
+ssm_status_t ssm_rmsnorm_add(ssm_tp_t tp, const float* a, const float* b, const float* weight, float eps, void* x_out,
+                             int64_t M, void* stream);
 
 /* Quantised all-reduce of n fp32 values (n % qar_block == 0), rows of D = d_model:
  * every rank quantises its partial per block (s = amax/127, q = rint(o/s) clamped to

@@ -14,6 +14,7 @@ SSM_BF16, SSM_FP32 = 0, 1
 SSM_AR2_INT8, SSM_AR2_FP32, SSM_AR2_EXTERNAL, SSM_AR2_FP16 = 0x1, 0x2, 0x4, 0x8
 SSM_QAR_ACCUMULATE, SSM_QAR_FP16, SSM_QAR_TWOSHOT, SSM_QAR_ONESHOT = 0x10, 0x20, 0x40, 0x80
 SSM_DECODE_UNFUSED, SSM_AR2_BF16, SSM_QAR_BF16, SSM_TP_NAIVE, SSM_QAR_REQUANT = 0x100, 0x200, 0x400, 0x1000, 0x2000
+SSM_QAR_FP32 = 0x4000
 SSM_COMM_VIRTUAL = 0x1
 
 STATUS = {0: "SSM_OK", 1: "SSM_ERR_ARG", 2: "SSM_ERR_DIM", 3: "SSM_ERR_SHARD", 4: "SSM_ERR_RANK",
@@ -45,6 +46,15 @@ class ssm_layer_weights_t(C.Structure):
                 ("w_in_naive", C.c_void_p)]
 
 
+class ssm_attn_config_t(C.Structure):
+    _fields_ = [("n_heads", C.c_int32), ("intermediate", C.c_int32), ("eps", C.c_float), ("max_seq", C.c_int32)]
+
+
+class ssm_attn_weights_t(C.Structure):
+    _fields_ = [("norm1", C.c_void_p), ("w_qkv", C.c_void_p), ("w_o", C.c_void_p), ("norm2", C.c_void_p),
+                ("w_gu", C.c_void_p), ("w_d", C.c_void_p), ("w_lin", C.c_void_p)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libssmtp.so not built ({LIB_PATH}); run `python -m paper_2602_21144_b200.build`")
@@ -70,6 +80,14 @@ def _load():
         "ssm_qallreduce": (st, [vp, vp, vp, sz, C.c_uint32, vp]),
         "ssm_rmsnorm": (st, [vp, vp, vp, C.c_float, vp, i64, vp]),
         "ssm_tp_check": (st, [vp, vp]),
+        "ssm_rmsnorm_add": (st, [vp, vp, vp, vp, C.c_float, vp, i64, vp]),
+        "ssm_kv_bytes": (st, [vp, P(ssm_attn_config_t), i32, P(sz)]),
+        "ssm_kv_alloc": (st, [vp, P(ssm_attn_config_t), i32, vp, sz, vp, P(vp)]),
+        "ssm_kv_reset": (st, [vp, vp]),
+        "ssm_kv_free": (st, [vp]),
+        "ssm_attn_workspace_bytes": (st, [vp, P(ssm_attn_config_t), i32, i32, P(sz)]),
+        "ssm_attn_block": (st, [vp, P(ssm_attn_config_t), P(ssm_attn_weights_t), vp, vp, vp, vp, i32, i32, C.c_uint32,
+                                vp, sz, vp]),
         "ssm_tp_stats": (st, [vp, P(i64), P(i64)]),
         "ssm_tp_launch_count": (st, [vp, P(i64)]),
         "ssm_tp_epoch": (st, [vp, P(C.c_uint32)]),
@@ -98,7 +116,8 @@ EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "s
             "ssm_mixer_decode", "ssm_mixer_decode_block", "ssm_qallreduce", "ssm_rmsnorm", "ssm_tp_check", "ssm_tp_stats", "ssm_tp_epoch",
             "ssm_tp_barrier", "ssm_tp_launch_count", "ssm_tp_fused_calls", "ssm_tp_probe", "ssm_tp_probe_read",
             "ssm_packed_weight_bytes", "ssm_pack_weight", "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld",
-            "ssm_dbg_scan"]
+            "ssm_dbg_scan", "ssm_rmsnorm_add", "ssm_kv_bytes", "ssm_kv_alloc", "ssm_kv_reset", "ssm_kv_free",
+            "ssm_attn_workspace_bytes", "ssm_attn_block"]
 PROBE = {"in_proj": 1, "conv": 2, "x_proj": 3, "dt_proj": 4, "scan": 5, "out_proj": 6, "ar2": 7, "decode_step": 8,
          "in_proj_decode": 9}
 

@@ -84,6 +84,12 @@ struct ssm_state_s {
   float* h;
 };
 
+struct ssm_kv_s {
+  ssm_tp_s* owner;
+  int batch, max_seq, hk, d;
+  char* buf;  // header (int len @0, int err @4), K, V
+};
+
 namespace {
 
 // The h buffer of a state is h [batch][E_k][N] fp32 followed by the fused decode path's x_proj
@@ -621,6 +627,7 @@ ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp
       pre = preload_kernels();
       if (pre == cudaSuccess) pre = preload_gemm_simt();
       if (pre == cudaSuccess) pre = preload_gemm_tc();
+      if (pre == cudaSuccess) pre = preload_attn();
     });
     if (pre != cudaSuccess) {
       delete t;
@@ -785,7 +792,8 @@ ssm_status_t ssm_mixer_decode_block(ssm_tp_t tp, const ssm_layer_weights_t* w, s
 
 ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_t n, uint32_t flags, void* stream) {
   if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
-  const uint32_t known = SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_BF16 | SSM_QAR_TWOSHOT | SSM_QAR_REQUANT;
+  const uint32_t known = SSM_QAR_ACCUMULATE | SSM_QAR_FP16 | SSM_QAR_BF16 | SSM_QAR_TWOSHOT | SSM_QAR_REQUANT |
+                         SSM_QAR_FP32;
   if (n == 0 && !(flags & ~known)) return SSM_OK;  // nothing to reduce
   if (!partial || !out) return fail(SSM_ERR_ARG, "NULL argument");
   if (flags & ~known) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
@@ -802,6 +810,19 @@ ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_
     one.p[0] = const_cast<float*>(partial);
     tp->launches++;
     CU(launch_f32_reduce(one, 1, 0, (int64_t)n, out, acc, s));
+    return SSM_OK;
+  }
+  if (flags & SSM_QAR_FP32) {  // exact: partial -> own half, barrier, fixed-order fp32 sum
+    if (n % 4 || (reinterpret_cast<uintptr_t>(partial) & 15)) return fail(SSM_ERR_DIM, "n=%zu not a multiple of 4", n);
+    if (n * 4 > half_bytes(tp)) return fail(SSM_ERR_ARG, "symmetric buffer too small for n=%zu", n);
+    const uint32_t ep = ++tp->epoch;
+    const int64_t off = (int64_t)(kSigBytes + (ep & 1) * half_bytes(tp));
+    tp->launches += 2;
+    tp->ar_count++;
+    tp->bytes_sent += n * 4;
+    CU(cudaMemcpyAsync(reinterpret_cast<char*>(tp->peers.p[tp->rank]) + off, partial, n * 4, cudaMemcpyDeviceToDevice, s));
+    CU(launch_peer_barrier(tp->peers, tp->rank, tp->k, s));
+    CU(launch_f32_reduce(tp->peers, tp->k, off, (int64_t)n, out, acc, s));
     return SSM_OK;
   }
   if (flags & SSM_QAR_REQUANT) {  // requantised two-shot int8 (labelled variant of reading Q6)
@@ -973,6 +994,192 @@ ssm_status_t ssm_dbg_scan(ssm_tp_t tp, const void* u, const void* delta, const v
   tp->launches++;
   CU(launch_scan(tp->bf16, tp->bf16, u, Ek, delta, Ek, z, ldz, BC, 2 * N, a_log, d_skip, h, (int64_t)Ek * N, g, Ek,
                  batch, seqlen, Ek, N, reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_rmsnorm_add(ssm_tp_t tp, const float* a, const float* b, const float* weight, float eps, void* x_out,
+                             int64_t M, void* stream) {
+  if (!tp || !a || !x_out) return fail(SSM_ERR_ARG, "NULL argument");
+  if (!tp->bf16) return fail(SSM_ERR_UNSUPPORTED, "ssm_rmsnorm_add: bf16 handles only");
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(weight) |
+       reinterpret_cast<uintptr_t>(x_out)) & 15)
+    return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
+  PdlScope pdl(M <= 256 && !(tp->flags & SSM_COMM_VIRTUAL));
+  tp->launches++;
+  CU(launch_rmsnorm2(a, b, 1, weight, eps, reinterpret_cast<__nv_bfloat16*>(x_out), M, tp->cfg.d_model,
+                     reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+struct AttnDims {
+  int D, H, hk, d, I, ik;
+};
+ssm_status_t attn_dims(const ssm_tp_s* t, const ssm_attn_config_t* a, AttnDims* o) {
+  if (!a) return fail(SSM_ERR_ARG, "attention config is NULL");
+  if (!t->bf16) return fail(SSM_ERR_UNSUPPORTED, "shared attention block: bf16 handles only");
+  const int D = t->cfg.d_model, H = a->n_heads, I = a->intermediate;
+  if (H < 1 || (2 * D) % H || H % t->k || I < 1 || I % (8 * t->k) || a->max_seq < 1)
+    return fail(SSM_ERR_SHARD, "n_heads=%d / intermediate=%d do not split over tp_size=%d (2 d_model=%d)", H, I, t->k,
+                2 * D);
+  const int d = 2 * D / H;
+  if (!(d == 32 || d == 64 || d == 128 || d == 464) || D % 8)
+    return fail(SSM_ERR_UNSUPPORTED, "head_dim=%d (supported: 32, 64, 128, 464)", d);
+  *o = AttnDims{D, H, H / t->k, d, I, I / t->k};
+  return SSM_OK;
+}
+struct AttnWs {
+  size_t xa, qkv, o, a, y, gu, m, dd, mb, total;
+};
+AttnWs attn_ws(const AttnDims& z, int64_t M) {
+  AttnWs L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += al256(bytes); return o; };
+  L.xa = take(M * 2 * z.D * 2);
+  L.qkv = take(M * 3 * z.hk * z.d * 2);
+  L.o = take(M * z.hk * z.d * 2);
+  L.a = take(M * z.D * 4);
+  L.y = take(M * z.D * 2);
+  L.gu = take(M * 2 * z.ik * 2);
+  L.m = take(M * z.ik * 2);
+  L.dd = take(M * z.D * 4);
+  L.mb = take(M * z.D * 2);
+  L.total = off;
+  return L;
+}
+uint32_t attn_ar_flags(uint32_t flags) {
+  if (flags & SSM_AR2_INT8) return 0;
+  if (flags & SSM_AR2_FP16) return SSM_QAR_FP16;
+  if (flags & SSM_AR2_BF16) return SSM_QAR_BF16;
+  return SSM_QAR_FP32;
+}
+}  // namespace
+
+extern "C" {
+
+ssm_status_t ssm_kv_bytes(ssm_tp_t tp, const ssm_attn_config_t* acfg, int32_t batch, size_t* bytes) {
+  if (!tp || !bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  AttnDims z;
+  ssm_status_t st = attn_dims(tp, acfg, &z);
+  if (st != SSM_OK) return st;
+  if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
+  *bytes = 256 + 2 * al256((size_t)batch * acfg->max_seq * z.hk * z.d * 2);
+  return SSM_OK;
+}
+
+ssm_status_t ssm_kv_alloc(ssm_tp_t tp, const ssm_attn_config_t* acfg, int32_t batch, void* buf, size_t bytes,
+                          void* stream, ssm_kv_t* out) {
+  if (!out) return fail(SSM_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  size_t need = 0;
+  ssm_status_t st = ssm_kv_bytes(tp, acfg, batch, &need);
+  if (st != SSM_OK) return st;
+  if (!buf || bytes < need) return fail(SSM_ERR_ARG, "KV buffer NULL or too small (%zu < %zu B)", bytes, need);
+  if (reinterpret_cast<uintptr_t>(buf) & 255) return fail(SSM_ERR_ARG, "KV buffer must be 256-B aligned");
+  ssm_kv_s* kv = new (std::nothrow) ssm_kv_s();
+  if (!kv) return fail(SSM_ERR_ARG, "out of host memory");
+  AttnDims z;
+  attn_dims(tp, acfg, &z);
+  *kv = ssm_kv_s{tp, batch, acfg->max_seq, z.hk, z.d, reinterpret_cast<char*>(buf)};
+  if (cudaMemsetAsync(buf, 0, need, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess) {
+    delete kv;
+    return fail(SSM_ERR_CUDA, "zero-fill of the KV cache failed");
+  }
+  *out = kv;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_kv_reset(ssm_kv_t kv, void* stream) {
+  if (!kv) return fail(SSM_ERR_ARG, "kv is NULL");
+  CU(cudaMemsetAsync(kv->buf, 0, 256, reinterpret_cast<cudaStream_t>(stream)));   // length and error word
+  return SSM_OK;
+}
+
+ssm_status_t ssm_kv_free(ssm_kv_t kv) {
+  delete kv;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_attn_workspace_bytes(ssm_tp_t tp, const ssm_attn_config_t* acfg, int32_t batch, int32_t seqlen,
+                                      size_t* bytes) {
+  if (!tp || !bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  AttnDims z;
+  ssm_status_t st = attn_dims(tp, acfg, &z);
+  if (st != SSM_OK) return st;
+  if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
+  *bytes = attn_ws(z, (int64_t)batch * seqlen).total;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ssm_attn_weights_t* w, ssm_kv_t kv,
+                            const float* h, const float* h0, float* t_out, int32_t batch, int32_t seqlen,
+                            uint32_t flags, void* workspace, size_t ws_bytes, void* stream) {
+  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
+  AttnDims z;
+  ssm_status_t st = attn_dims(tp, acfg, &z);
+  if (st != SSM_OK) return st;
+  if (!w || !w->norm1 || !w->w_qkv || !w->w_o || !w->norm2 || !w->w_gu || !w->w_d || !w->w_lin)
+    return fail(SSM_ERR_ARG, "attention weights struct or one of its pointers is NULL");
+  if (!kv || kv->owner != tp) return fail(SSM_ERR_CACHE, "KV cache missing or bound to another handle");
+  if (kv->batch != batch || kv->max_seq != acfg->max_seq) return fail(SSM_ERR_CACHE, "KV cache batch/max_seq mismatch");
+  if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
+  if (!h || !h0 || !t_out) return fail(SSM_ERR_ARG, "h/h0/t_out is NULL");
+  if ((reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(h0) | reinterpret_cast<uintptr_t>(t_out)) & 15)
+    return fail(SSM_ERR_ARG, "h/h0/t_out must be 16-B aligned");
+  if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP16 | SSM_AR2_BF16 | SSM_AR2_FP32))
+    return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  const int64_t M = (int64_t)batch * seqlen;
+  if (M == 0) return SSM_OK;
+  const AttnWs L = attn_ws(z, M);
+  if (!workspace || ws_bytes < L.total) return fail(SSM_ERR_ARG, "workspace %zu B < required %zu B", ws_bytes, L.total);
+  if (reinterpret_cast<uintptr_t>(workspace) & 255) return fail(SSM_ERR_ARG, "workspace must be 256-B aligned");
+  if (tp->k > 1 && (size_t)M * z.D * 4 > half_bytes(tp))
+    return fail(SSM_ERR_ARG, "symmetric buffer too small for %lld tokens", (long long)M);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  PdlScope pdl(M <= 256 && !(tp->flags & SSM_COMM_VIRTUAL));
+  char* W = reinterpret_cast<char*>(workspace);
+  auto bf = [&](size_t off) { return reinterpret_cast<__nv_bfloat16*>(W + off); };
+  const int D = z.D, A2 = 2 * D, QW = z.hk * z.d;
+  int* len = reinterpret_cast<int*>(kv->buf);
+  int* err = len + 1;
+  __nv_bfloat16* Kc = reinterpret_cast<__nv_bfloat16*>(kv->buf + 256);
+  __nv_bfloat16* Vc = reinterpret_cast<__nv_bfloat16*>(kv->buf + 256 + al256((size_t)batch * kv->max_seq * QW * 2));
+  // x = RMSNorm_1(concat(h, h0)); q | k | v of the owned heads
+  tp->launches++;
+  CU(launch_rmsnorm2(h, h0, 0, w->norm1, acfg->eps, bf(L.xa), M, D, s));
+  CU(gemm(tp, bf(L.xa), A2, w->w_qkv, A2, (int)M, 3 * QW, A2, 1, epi(EPI_STORE_BF16, 0, bf(L.qkv), 3 * QW), s));
+  // K, V appended to the cache; causal attention over it; the cache length advanced
+  tp->launches += 3;
+  CU(launch_kv_append(bf(L.qkv), len, batch, seqlen, z.hk, z.d, kv->max_seq, Kc, Vc, err, s));
+  // (the attention reads *len after the append: it counts this call's rows once advanced, so
+  //  advance first and let the kernel take t0 = len - L)
+  CU(launch_kv_advance(len, seqlen, s));
+  CU(launch_attn(bf(L.qkv), len, Kc, Vc, batch, seqlen, z.hk, z.d, kv->max_seq, 1.0f / sqrtf((float)z.d / 2.0f),
+                 bf(L.o), s));
+  // a = o W_o^T (row-parallel partial), all-reduced at TP > 1
+  float* a = reinterpret_cast<float*>(W + L.a);
+  CU(gemm(tp, bf(L.o), QW, w->w_o, QW, (int)M, D, QW, 1, epi(EPI_STORE_F32, 0, a, D), s));
+  if (tp->k > 1) {
+    ssm_status_t r = ssm_qallreduce(tp, a, a, (size_t)M * D, attn_ar_flags(flags), stream);
+    if (r != SSM_OK) return r;
+  }
+  // y = RMSNorm_2(a); m = GELU(y W_g^T) * (y W_u^T); d = m W_d^T (partial), all-reduced
+  tp->launches += 2;
+  CU(launch_rmsnorm2(a, nullptr, 1, w->norm2, acfg->eps, bf(L.y), M, D, s));
+  CU(gemm(tp, bf(L.y), D, w->w_gu, D, (int)M, 2 * z.ik, D, 1, epi(EPI_STORE_BF16, 0, bf(L.gu), 2 * z.ik), s));
+  CU(launch_gelu_mul(bf(L.gu), M, z.ik, bf(L.m), s));
+  float* dd = reinterpret_cast<float*>(W + L.dd);
+  CU(gemm(tp, bf(L.m), z.ik, w->w_d, z.ik, (int)M, D, z.ik, 1, epi(EPI_STORE_F32, 0, dd, D), s));
+  if (tp->k > 1) {
+    ssm_status_t r = ssm_qallreduce(tp, dd, dd, (size_t)M * D, attn_ar_flags(flags), stream);
+    if (r != SSM_OK) return r;
+  }
+  // t = m W_lin^T (replicated)
+  tp->launches++;
+  CU(launch_cast_bf16(dd, M * D, bf(L.mb), s));
+  CU(gemm(tp, bf(L.mb), D, w->w_lin, D, (int)M, D, D, 1, epi(EPI_STORE_F32, 0, t_out, D), s));
   return SSM_OK;
 }
 

@@ -131,6 +131,24 @@ cudaError_t launch_peer_barrier(Peers bufs, int rank, int k, cudaStream_t s);
 cudaError_t launch_publish_barrier(Peers bufs, int rank, int k, float* xacc, int64_t n, int64_t dst_off,
                                    cudaStream_t s);
 
+// ---- Zamba shared transformer block (attn.cu) ----
+// mode 0: y = RMSNorm(concat(a, b)) * w over 2D columns; mode 1: y = RMSNorm(a + b) * w over D (b may
+// be NULL); w may be NULL (ones); y bf16.
+cudaError_t launch_rmsnorm2(const float* a, const float* b, int mode, const float* w, float eps, __nv_bfloat16* y,
+                            int64_t M, int D, cudaStream_t s);
+// K, V rows of qkv [batch*L][3 Hk d] -> cache [batch][Tmax][Hk][d] at the device-side length *len
+// (err = 1 and nothing written on overflow); kv_advance: *len += L (after the attention)
+cudaError_t launch_kv_append(const __nv_bfloat16* qkv, const int* len, int batch, int L, int Hk, int d, int Tmax,
+                             __nv_bfloat16* K, __nv_bfloat16* V, int* err, cudaStream_t s);
+cudaError_t launch_kv_advance(int* len, int L, cudaStream_t s);
+// causal attention of this call's queries (qkv) over the cache holding *len rows (this call's
+// included); out [batch*L][Hk d] bf16; d in {32, 64, 128, 464}
+cudaError_t launch_attn(const __nv_bfloat16* qkv, const int* len, const __nv_bfloat16* K, const __nv_bfloat16* V,
+                        int batch, int L, int Hk, int d, int Tmax, float scale, __nv_bfloat16* out, cudaStream_t s);
+cudaError_t launch_gelu_mul(const __nv_bfloat16* gu, int64_t M, int I, __nv_bfloat16* m, cudaStream_t s);
+cudaError_t launch_cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t s);
+cudaError_t preload_attn();
+
 // Load every kernel eagerly (called once per process from ssm_tp_init when a device exists).
 cudaError_t preload_kernels();
 cudaError_t preload_gemm_simt();

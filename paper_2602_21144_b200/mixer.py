@@ -190,6 +190,11 @@ class TPMixer:
         L.call("ssm_rmsnorm", self.handle, _ptr(residual), _ptr(weight), C.c_float(eps), _ptr(out),
                residual.numel() // self.dims.d_model, _stream(stream))
 
+    def rmsnorm_add(self, a, b, out, weight=None, eps=1e-5, stream=None):
+        """out = RMSNorm(a + b) * weight (b may be None): the hybrid layer's Mamba pre-norm."""
+        L.call("ssm_rmsnorm_add", self.handle, _ptr(a), _ptr(b), _ptr(weight), C.c_float(eps), _ptr(out),
+               a.numel() // self.dims.d_model, _stream(stream))
+
     def check(self, stream=None):
         L.call("ssm_tp_check", self.handle, _stream(stream))
 
