@@ -280,8 +280,16 @@ def main():
             lw.pack(mx)  # pre-tiled copies of w_in / w_x / w_out for the decode weight streams
         layers.append(lw)
         del full
+    hybrid = None
+    if args.config == "zamba7b":
+        # Zamba-7B: the shared attention + MLP block before its 13 hybrid layers
+        from paper_2602_21144_b200.attention import hybrid_config, synthetic_shared_block
+        hl = [li for li in synth.ZAMBA7B_HYBRID_LAYERS if li < n_layers]
+        blk_full, lins = synthetic_shared_block(synth.ZAMBA7B_ATTN, hl, device=dev)
+        hybrid = hybrid_config(synth.ZAMBA7B_ATTN, blk_full, lins, k, rank, Lp + max(Ld, 1) + 16, dev)
+        del blk_full, lins
     torch.cuda.empty_cache()
-    stack = MixerStack(mx, layers, B, chunk, flags, nccl_group=(dist.group.WORLD if k > 1 else None))
+    stack = MixerStack(mx, layers, B, chunk, flags, nccl_group=(dist.group.WORLD if k > 1 else None), hybrid=hybrid)
 
     # inputs: replicated on all ranks (same seed); larger than L2 (126 MB) -> no flush needed
     g = torch.Generator(device=dev).manual_seed(42)
@@ -310,11 +318,13 @@ def main():
         if timers is not None:
             timers[0].record()
         for c in range(n_chunks):
-            stack.prefill_chunk(work[c])
+            stack.prefill_chunk(work[c], h0=prompt_in[c])
         if timers is not None:
             timers[1].record()
         for j in range(Ld):
             res_t.copy_(dec_in[j])
+            if stack.hybrid:
+                stack.h0_dec.copy_(dec_in[j])
             stack.replay(graph)
             dec_out[j].copy_(res_t)
         if timers is not None:
@@ -449,8 +459,11 @@ def main():
         line = {"metric": "batch tokens/sec", "value": value, "unit": "tokens/s", "n_gpus": k, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": f"{args.config}: {n_layers} layers, d_model {dims.d_model}, batch {B}, "
-                                       f"prompt {Lp} + {Ld} decode", "model": args.config, "global_batch": B,
+                "config": {"workload": f"{args.config}: {n_layers} layers"
+                                       + (f" ({len(stack.hybrid)} hybrid: shared attention + MLP block first)"
+                                          if stack.hybrid else "")
+                                       + f", d_model {dims.d_model}, batch {B}, prompt {Lp} + {Ld} decode",
+                           "model": args.config, "global_batch": B,
                            "seq_len": Lp + Ld, "parallelism": f"tp{k}", "ar2": args.ar2 if k > 1 else "none",
                            "tp_design": args.tp_design if k > 1 else "none",
                            "prefill_chunk": chunk, "packed_decode_weights": not args.no_pack,

@@ -1155,7 +1155,7 @@ ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ss
   CU(launch_kv_append(bf(L.qkv), len, batch, seqlen, z.hk, z.d, kv->max_seq, Kc, Vc, err, s));
   // (the attention reads *len after the append: it counts this call's rows once advanced, so
   //  advance first and let the kernel take t0 = len - L)
-  CU(launch_kv_advance(len, seqlen, s));
+  CU(launch_kv_advance(len, seqlen, kv->max_seq, s));
   CU(launch_attn(bf(L.qkv), len, Kc, Vc, batch, seqlen, z.hk, z.d, kv->max_seq, 1.0f / sqrtf((float)z.d / 2.0f),
                  bf(L.o), s));
   // a = o W_o^T (row-parallel partial), all-reduced at TP > 1

@@ -99,10 +99,14 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, const in
   }
 }
 
-__global__ void kv_advance_kernel(int* len, int L) {
+__global__ void kv_advance_kernel(int* len, int L, int Tmax) {
   pdl_trigger();
   pdl_wait();
-  if (threadIdx.x == 0 && blockIdx.x == 0) *reinterpret_cast<volatile int*>(len) += L;
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    volatile int* v = reinterpret_cast<volatile int*>(len);
+    const int n = *v + L;
+    *v = n < Tmax ? n : Tmax;  // saturating (an overflowing append wrote nothing and set the error word)
+  }
 }
 
 // ---------------------------------------------------------------- causal flash attention
@@ -332,8 +336,8 @@ cudaError_t launch_kv_append(const __nv_bfloat16* qkv, const int* len, int batch
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_kv_advance(int* len, int L, cudaStream_t s) {
-  cudaError_t e = launch(kv_advance_kernel, 1, 32, 0, s, len, L);
+cudaError_t launch_kv_advance(int* len, int L, int Tmax, cudaStream_t s) {
+  cudaError_t e = launch(kv_advance_kernel, 1, 32, 0, s, len, L, Tmax);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

@@ -137,10 +137,10 @@ cudaError_t launch_publish_barrier(Peers bufs, int rank, int k, float* xacc, int
 cudaError_t launch_rmsnorm2(const float* a, const float* b, int mode, const float* w, float eps, __nv_bfloat16* y,
                             int64_t M, int D, cudaStream_t s);
 // K, V rows of qkv [batch*L][3 Hk d] -> cache [batch][Tmax][Hk][d] at the device-side length *len
-// (err = 1 and nothing written on overflow); kv_advance: *len += L (after the attention)
+// (err = 1 and nothing written on overflow); kv_advance: *len = min(*len + L, Tmax)
 cudaError_t launch_kv_append(const __nv_bfloat16* qkv, const int* len, int batch, int L, int Hk, int d, int Tmax,
                              __nv_bfloat16* K, __nv_bfloat16* V, int* err, cudaStream_t s);
-cudaError_t launch_kv_advance(int* len, int L, cudaStream_t s);
+cudaError_t launch_kv_advance(int* len, int L, int Tmax, cudaStream_t s);
 // causal attention of this call's queries (qkv) over the cache holding *len rows (this call's
 // included); out [batch*L][Hk d] bf16; d in {32, 64, 128, 464}
 cudaError_t launch_attn(const __nv_bfloat16* qkv, const int* len, const __nv_bfloat16* K, const __nv_bfloat16* V,

@@ -44,7 +44,11 @@ class MixerStack:
     rank's fp32 partial, torch.distributed all-reduces it in bf16, torch adds it to the residual)."""
 
     def __init__(self, mixer: TPMixer, layers: list, batch: int, max_chunk: int, flags=L.SSM_AR2_INT8,
-                 norm_eps=1e-5, nccl_group=None):
+                 norm_eps=1e-5, nccl_group=None, hybrid=None):
+        """hybrid: Zamba's shared transformer block as
+        dict(adims=synth.AttnDims, weights={layer index: attention.SharedBlockWeights}, max_seq=int):
+        before each listed layer the block runs on (residual, h0) into t, and that layer's Mamba
+        block takes RMSNorm(residual + t).  The calls then take h0 (the token embeddings)."""
         self.mx, self.layers, self.batch, self.flags, self.eps = mixer, layers, batch, flags, norm_eps
         self.nccl = nccl_group if flags == L.SSM_AR2_EXTERNAL else None
         d = mixer.dims
@@ -56,6 +60,16 @@ class MixerStack:
         self.states = [State(mixer, batch) for _ in layers]
         if self.nccl is not None:
             self.part = torch.empty((batch * max_chunk, d.d_model), dtype=torch.float32, device=mixer.device)
+        self.hybrid = {}
+        if hybrid:
+            from .attention import SharedBlock
+            shared_ws = None
+            for li, w in hybrid["weights"].items():
+                blk = SharedBlock(mixer, hybrid["adims"], batch, hybrid["max_seq"], max_chunk, workspaces=shared_ws)
+                shared_ws = (blk.ws, blk.ws_dec)      # one workspace pair for every hybrid layer
+                self.hybrid[li] = (w, blk)
+            self.t_buf = torch.empty((batch * max_chunk, d.d_model), device=mixer.device)
+            self.h0_dec = torch.zeros((batch, d.d_model), device=mixer.device)
         self.graph = None
         self.graph_launches = 0
         self._graph_parity = 0
@@ -64,13 +78,23 @@ class MixerStack:
     def reset(self, stream=None):
         for s in self.states:
             s.reset(stream)
+        for _, blk in self.hybrid.values():
+            blk.reset(stream)
 
-    def prefill_chunk(self, res, stream=None):
-        """res: [batch * Lc, D] fp32, this chunk's residual rows (row = b*Lc + t), updated in place."""
+    def prefill_chunk(self, res, stream=None, h0=None):
+        """res: [batch * Lc, D] fp32, this chunk's residual rows (row = b*Lc + t), updated in place;
+        h0: the chunk's token embeddings (Zamba hybrid layers)."""
         n = res.shape[0]
         x = self.xbuf[:n]
-        for lw, st in zip(self.layers, self.states):
-            self.mx.rmsnorm(res, x, None, self.eps, stream)
+        for li, (lw, st) in enumerate(zip(self.layers, self.states)):
+            if li in self.hybrid:
+                w, blk = self.hybrid[li]
+                t = self.t_buf[:n]
+                blk(w, res, h0, t, n // self.batch, self.flags & (L.SSM_AR2_INT8 | L.SSM_AR2_FP16 | L.SSM_AR2_BF16),
+                    stream)
+                self.mx.rmsnorm_add(res, t, x, None, self.eps, stream)
+            else:
+                self.mx.rmsnorm(res, x, None, self.eps, stream)
             if self.nccl is None:
                 self.mx.prefill(lw, st, x, res, self.flags, self.ws, stream)
             else:
@@ -78,8 +102,21 @@ class MixerStack:
 
     def decode_step(self, res_t, stream=None):
         """res_t: [batch, D] fp32, updated in place through all layers (ssm_mixer_decode_block:
-        pre-norm RMSNorm, then the layer's decode kernels)."""
-        for lw, st in zip(self.layers, self.states):
+        pre-norm RMSNorm, then the layer's decode kernels); Zamba hybrid layers read the token
+        embeddings from self.h0_dec."""
+        for li, (lw, st) in enumerate(zip(self.layers, self.states)):
+            if li in self.hybrid:
+                w, blk = self.hybrid[li]
+                t = self.t_buf[:self.batch]
+                blk(w, res_t, self.h0_dec, t, 1, self.flags & (L.SSM_AR2_INT8 | L.SSM_AR2_FP16 | L.SSM_AR2_BF16),
+                    stream)
+                self.mx.rmsnorm_add(res_t, t, self.xbuf_dec, None, self.eps, stream)
+                if self.nccl is None:
+                    self.mx.decode(lw, st, self.xbuf_dec, res_t, self.flags | self.dec_flags, self.ws_dec, stream)
+                else:
+                    self._nccl_layer(lambda p: self.mx.decode(lw, st, self.xbuf_dec, p, self.flags, self.ws_dec,
+                                                              stream), res_t)
+                continue
             if self.nccl is None:
                 self.mx.decode_block(lw, st, res_t, self.eps, self.flags | self.dec_flags, self.ws_dec, stream)
             else:
@@ -118,6 +155,8 @@ class MixerStack:
         e0 = self.mx.epoch()
         with torch.cuda.graph(g):
             self.decode_step(res_t)
+            if (self.mx.epoch() - e0) % 2:  # odd collective count (e.g. Zamba at TP = 2): one payload-free
+                self.mx.barrier()              # barrier keeps back-to-back replays alternating the halves
         self.graph_launches = self.mx.launches() - before
         if (self.mx.epoch() - e0) % 2:
             raise RuntimeError("odd number of collectives per decode step: double-buffer halves would not alternate")

@@ -94,3 +94,70 @@ def test_kv_overflow_reports_and_reset_empties():
     blk(w, x, x, t, 8)
     torch.cuda.synchronize()
     assert int(blk.kv_buf[0:4].view(torch.int32).cpu()[0]) == 8
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_zamba_hybrid_stack_prefill_graph_decode_vs_oracle(k):
+    """A Zamba-shaped stack (2 mixer heads; layer 1 of 3 is hybrid: the shared block runs on
+    (residual, h0) into t and the Mamba layer takes RMSNorm(residual + t)) through MixerStack: chunked
+    prefill, then CUDA-graph decode replays, against the fp64 composition of the oracles."""
+    from oracle import mixer_ref as M
+    from paper_2602_21144_b200 import LayerWeights
+    from paper_2602_21144_b200.attention import hybrid_config
+    from paper_2602_21144_b200.stack import MixerStack, synthetic_layer
+    from test_gpu_paths import _host_weights
+    dims = synth.MixerDims(d_model=128, d_inner=256, dt_rank=16, n_heads=2, n_layers=3)
+    adims = synth.AttnDims(d_model=128, n_heads=4, intermediate=256)
+    B, L_in, L_out, hyb = 2, 20, 3, 1
+    fulls = [synthetic_layer(dims, l) for l in range(3)]
+    blk = synth.shared_block_weights(adims)
+    lin = {hyb: blk["w_lin"]}
+    g = torch.Generator().manual_seed(3)
+    res0 = torch.randn(B, L_in + L_out, 128, generator=g, dtype=torch.float64).float()
+    h0 = torch.randn(B, L_in + L_out, 128, generator=g, dtype=torch.float64).float()
+    grp = VirtualGroup(dims, k, "bf16", B * L_in) if k > 1 else None
+    mixers = grp.mixers if k > 1 else [TPMixer(dims, "bf16")]
+    stacks = [MixerStack(mixers[r], [LayerWeights(dims, f, k, r, "bf16") for f in fulls], B, L_in, L.SSM_AR2_FP32,
+                         hybrid=hybrid_config(adims, blk, lin, k, r, L_in + L_out + 4)) for r in range(k)]
+    pre = [res0[:, :L_in].cuda().contiguous().view(B * L_in, -1) for _ in range(k)]
+    h0p = [h0[:, :L_in].cuda().contiguous().view(B * L_in, -1) for _ in range(k)]
+    rts = [torch.empty(B, 128, device="cuda") for _ in range(k)]
+    torch.cuda.synchronize()
+
+    def run(fn):
+        if grp is None:
+            fn(0, mixers[0], torch.cuda.current_stream())
+            torch.cuda.synchronize()
+        else:
+            grp.run(fn)
+    graphs = []
+    for r in range(k):
+        if grp is None:
+            graphs.append(stacks[r].capture_decode(rts[r]))
+        else:
+            with torch.cuda.stream(grp.streams[r]):
+                graphs.append(stacks[r].capture_decode(rts[r], warmup=False))
+    run(lambda r, mx, s: (stacks[r].reset(s), stacks[r].prefill_chunk(pre[r], s, h0=h0p[r])))
+    outs = []
+    for t in range(L_in, L_in + L_out):
+        for r in range(k):
+            rts[r].copy_(res0[:, t].cuda())
+            stacks[r].h0_dec.copy_(h0[:, t].cuda())
+        torch.cuda.synchronize()
+        run(lambda r, mx, s: stacks[r].replay(graphs[r], s))
+        outs.append(rts[0].cpu().clone())
+    ws = [_host_weights(f) for f in fulls]
+    hb = {kk: (synth.bf16_round(v) if kk.startswith("w_") else v.float().double()).numpy() for kk, v in blk.items()}
+    res = res0.double().numpy()
+    for l in range(3):
+        if l == hyb:
+            tt, _ = A.shared_block(adims, hb, res, h0.double().numpy())
+            x = M.rmsnorm(res + tt, None, 1e-5)
+        else:
+            x = M.rmsnorm(res, None, 1e-5)
+        res, _ = M.mixer_forward(dims, ws[l], x, res)
+    r0 = res0.double().numpy()
+    got_pre = pre[0].view(B, L_in, -1).cpu().double().numpy()
+    got_dec = torch.stack(outs, 1).double().numpy()
+    assert rel(got_pre - r0[:, :L_in], res[:, :L_in] - r0[:, :L_in]) < TOL["bf16"]
+    assert rel(got_dec - r0[:, L_in:], res[:, L_in:] - r0[:, L_in:]) < TOL["bf16"]
