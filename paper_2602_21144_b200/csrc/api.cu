@@ -1031,9 +1031,9 @@ ssm_status_t attn_dims(const ssm_tp_s* t, const ssm_attn_config_t* a, AttnDims* 
   return SSM_OK;
 }
 struct AttnWs {
-  size_t xa, qkv, o, a, y, gu, m, dd, mb, total;
+  size_t xa, qkv, o, a, y, gu, m, dd, mb, part, total;
 };
-AttnWs attn_ws(const AttnDims& z, int64_t M) {
+AttnWs attn_ws(const AttnDims& z, int64_t M, int batch = 0, int max_seq = 0) {
   AttnWs L{};
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += al256(bytes); return o; };
@@ -1046,6 +1046,8 @@ AttnWs attn_ws(const AttnDims& z, int64_t M) {
   L.m = take(M * z.ik * 2);
   L.dd = take(M * z.D * 4);
   L.mb = take(M * z.D * 2);
+  // decode (one token per sequence): the split-K attention's partials
+  L.part = take(batch > 0 && M == batch ? attn_dec_part_floats(batch, z.hk, z.d, max_seq) * 4 : 0);
   L.total = off;
   return L;
 }
@@ -1109,7 +1111,7 @@ ssm_status_t ssm_attn_workspace_bytes(ssm_tp_t tp, const ssm_attn_config_t* acfg
   ssm_status_t st = attn_dims(tp, acfg, &z);
   if (st != SSM_OK) return st;
   if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
-  *bytes = attn_ws(z, (int64_t)batch * seqlen).total;
+  *bytes = attn_ws(z, (int64_t)batch * seqlen, batch, acfg->max_seq).total;
   return SSM_OK;
 }
 
@@ -1132,7 +1134,7 @@ ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ss
     return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
   const int64_t M = (int64_t)batch * seqlen;
   if (M == 0) return SSM_OK;
-  const AttnWs L = attn_ws(z, M);
+  const AttnWs L = attn_ws(z, M, batch, acfg->max_seq);
   if (!workspace || ws_bytes < L.total) return fail(SSM_ERR_ARG, "workspace %zu B < required %zu B", ws_bytes, L.total);
   if (reinterpret_cast<uintptr_t>(workspace) & 255) return fail(SSM_ERR_ARG, "workspace must be 256-B aligned");
   if (tp->k > 1 && (size_t)M * z.D * 4 > half_bytes(tp))
@@ -1156,8 +1158,14 @@ ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ss
   // (the attention reads *len after the append: it counts this call's rows once advanced, so
   //  advance first and let the kernel take t0 = len - L)
   CU(launch_kv_advance(len, seqlen, kv->max_seq, s));
-  CU(launch_attn(bf(L.qkv), len, Kc, Vc, batch, seqlen, z.hk, z.d, kv->max_seq, 1.0f / sqrtf((float)z.d / 2.0f),
-                 bf(L.o), s));
+  const float ascale = 1.0f / sqrtf((float)z.d / 2.0f);
+  if (seqlen == 1) {  // decode: memory-bound split-K over the cached keys
+    tp->launches++;
+    CU(launch_attn_decode(bf(L.qkv), len, Kc, Vc, batch, z.hk, z.d, kv->max_seq, ascale,
+                          reinterpret_cast<float*>(W + L.part), bf(L.o), s));
+  } else {
+    CU(launch_attn(bf(L.qkv), len, Kc, Vc, batch, seqlen, z.hk, z.d, kv->max_seq, ascale, bf(L.o), s));
+  }
   // a = o W_o^T (row-parallel partial), all-reduced at TP > 1
   float* a = reinterpret_cast<float*>(W + L.a);
   CU(gemm(tp, bf(L.o), QW, w->w_o, QW, (int)M, D, QW, 1, epi(EPI_STORE_F32, 0, a, D), s));

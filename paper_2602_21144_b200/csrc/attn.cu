@@ -272,6 +272,153 @@ __global__ void __launch_bounds__(AT, 1) attn_kernel(const __nv_bfloat16* __rest
   }
 }
 
+// ---------------------------------------------------------------- decode attention (L = 1)
+// Memory-bound flash decoding: grid (splits, Hk, batch); a 128-thread CTA streams its slice of the
+// cache rows of one (b, head); each warp takes keys in groups of 4 (all of their K and V 16-B
+// chunks in flight together: a lane owns chunks lane and lane + 32 of a d-wide row), forms the
+// scores with a warp reduction and keeps an online softmax and its share of the output; the CTA
+// then merges its warps and writes a partial (max, sum, acc[d]) per split, merged by
+// attn_dec_combine_kernel.  d % 8 == 0, d <= 512.
+constexpr int DEC_THREADS = 128, DEC_G = 4;
+__global__ void __launch_bounds__(DEC_THREADS) attn_dec_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                                               const int* __restrict__ len,
+                                                               const __nv_bfloat16* __restrict__ Kc,
+                                                               const __nv_bfloat16* __restrict__ Vc, int Hk, int d,
+                                                               int Tmax, float scale_log2, int keys_per_split,
+                                                               float* __restrict__ part) {
+  pdl_trigger();
+  pdl_wait();
+  const int sp = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = *reinterpret_cast<const volatile int*>(len);
+  const int nch = d / 8;
+  const int k_lo = sp * keys_per_split, k_hi = min(T, k_lo + keys_per_split);
+  // q: a lane's two 16-B chunks (lane, lane + 32)
+  float q[2][8];
+  const __nv_bfloat16* qr = qkv + (int64_t)b * 3 * Hk * d + (int64_t)h * d;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int ch = lane + 32 * c;
+    uint4 raw = ch < nch ? reinterpret_cast<const uint4*>(qr)[ch] : make_uint4(0, 0, 0, 0);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h2[j]);
+      q[c][2 * j] = f.x * scale_log2;
+      q[c][2 * j + 1] = f.y * scale_log2;
+    }
+  }
+  float m = -INFINITY, l = 0.f, acc[2][8];
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[c][j] = 0.f;
+  const int64_t row_stride = (int64_t)Hk * d;
+  const __nv_bfloat16* Kb = Kc + ((int64_t)b * Tmax) * row_stride + (int64_t)h * d;
+  const __nv_bfloat16* Vb = Vc + ((int64_t)b * Tmax) * row_stride + (int64_t)h * d;
+  for (int k0 = k_lo + warp * DEC_G; k0 < k_hi; k0 += 4 * DEC_G) {
+    uint4 kr[DEC_G][2], vr[DEC_G][2];
+#pragma unroll
+    for (int g = 0; g < DEC_G; ++g)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int ch = lane + 32 * c;
+        const bool ok = k0 + g < k_hi && ch < nch;
+        kr[g][c] = ok ? reinterpret_cast<const uint4*>(Kb + (int64_t)(k0 + g) * row_stride)[ch] : make_uint4(0, 0, 0, 0);
+        vr[g][c] = ok ? reinterpret_cast<const uint4*>(Vb + (int64_t)(k0 + g) * row_stride)[ch] : make_uint4(0, 0, 0, 0);
+      }
+    float s[DEC_G];
+#pragma unroll
+    for (int g = 0; g < DEC_G; ++g) {
+      float a = 0.f;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kr[g][c]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(k2[j]);
+          a = fmaf(q[c][2 * j], f.x, fmaf(q[c][2 * j + 1], f.y, a));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      s[g] = k0 + g < k_hi ? a : -INFINITY;
+    }
+    float mn = m;
+#pragma unroll
+    for (int g = 0; g < DEC_G; ++g) mn = fmaxf(mn, s[g]);
+    const float alpha = m == -INFINITY ? 0.f : ex2_approx(m - mn);
+    l *= alpha;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[c][j] *= alpha;
+#pragma unroll
+    for (int g = 0; g < DEC_G; ++g) {
+      const float p = s[g] == -INFINITY ? 0.f : ex2_approx(s[g] - mn);
+      l += p;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vr[g][c]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(v2[j]);
+          acc[c][2 * j] = fmaf(p, f.x, acc[c][2 * j]);
+          acc[c][2 * j + 1] = fmaf(p, f.y, acc[c][2 * j + 1]);
+        }
+      }
+    }
+    m = mn;
+  }
+  // merge the 4 warps (shared memory), write the split's partial: [m, l, acc[d]]
+  __shared__ float s_m[4], s_l[4];
+  __shared__ float s_acc[4][512];
+  if (lane == 0) { s_m[warp] = m; s_l[warp] = l; }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int ch = lane + 32 * c;
+    if (ch < nch)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s_acc[warp][ch * 8 + j] = acc[c][j];
+  }
+  __syncthreads();
+  float M = fmaxf(fmaxf(s_m[0], s_m[1]), fmaxf(s_m[2], s_m[3]));
+  float w[4], Lt = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    w[i] = s_m[i] == -INFINITY ? 0.f : ex2_approx(s_m[i] - M);
+    Lt += w[i] * s_l[i];
+  }
+  float* pp = part + (((int64_t)b * Hk + h) * gridDim.x + sp) * (2 + d);
+  if (threadIdx.x == 0) { pp[0] = M; pp[1] = Lt; }
+  for (int i = threadIdx.x; i < d; i += DEC_THREADS)
+    pp[2 + i] = w[0] * s_acc[0][i] + w[1] * s_acc[1][i] + w[2] * s_acc[2][i] + w[3] * s_acc[3][i];
+}
+
+__global__ void attn_dec_combine_kernel(const float* __restrict__ part, int splits, int Hk, int d,
+                                        __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int h = blockIdx.x, b = blockIdx.y;
+  const float* pp = part + ((int64_t)b * Hk + h) * splits * (2 + d);
+  float M = -INFINITY;
+  for (int s = 0; s < splits; ++s) M = fmaxf(M, pp[s * (2 + d)]);
+  float Lt = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float ms = pp[s * (2 + d)];
+    Lt += ms == -INFINITY ? 0.f : ex2_approx(ms - M) * pp[s * (2 + d) + 1];
+  }
+  const float inv = Lt > 0.f ? 1.f / Lt : 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float o = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float ms = pp[s * (2 + d)];
+      if (ms != -INFINITY) o = fmaf(ex2_approx(ms - M), pp[s * (2 + d) + 2 + i], o);
+    }
+    out[((int64_t)b * Hk + h) * d + i] = __float2bfloat16_rn(o * inv);
+  }
+}
+
 // ---------------------------------------------------------------- MLP gate and cast
 // gu [M][2 I] bf16 (gate | up) -> m [M][I] bf16 = GELU(gate) * up, GELU(x) = x Phi(x) (erf form)
 __global__ void gelu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int64_t M, int I, __nv_bfloat16* __restrict__ m) {
@@ -369,6 +516,31 @@ cudaError_t launch_attn(const __nv_bfloat16* qkv, const int* len, const __nv_bfl
   }
 }
 
+// decode (L = 1): splits chosen so that ~3 CTAs per SM stream the cache; part: workspace of
+// batch * Hk * splits * (2 + d) floats (attn_dec_part_floats)
+int attn_dec_splits(int batch, int Hk, int Tmax) {
+  int sp = (3 * 148 + batch * Hk - 1) / (batch * Hk);
+  const int maxsp = (Tmax + 63) / 64;
+  if (sp > maxsp) sp = maxsp;
+  return sp < 1 ? 1 : sp;
+}
+size_t attn_dec_part_floats(int batch, int Hk, int d, int Tmax) {
+  return (size_t)batch * Hk * attn_dec_splits(batch, Hk, Tmax) * (2 + d);
+}
+cudaError_t launch_attn_decode(const __nv_bfloat16* qkv, const int* len, const __nv_bfloat16* K, const __nv_bfloat16* V,
+                               int batch, int Hk, int d, int Tmax, float scale, float* part, __nv_bfloat16* out,
+                               cudaStream_t s) {
+  if (batch <= 0) return cudaSuccess;
+  if (d % 8 || d > 512) return cudaErrorInvalidValue;
+  const int sp = attn_dec_splits(batch, Hk, Tmax);
+  const int kps = (Tmax + sp - 1) / sp;
+  cudaError_t e = launch(attn_dec_kernel, dim3(sp, Hk, batch), DEC_THREADS, 0, s, qkv, len, K, V, Hk, d, Tmax,
+                         scale * 1.4426950408889634f, kps, part);
+  if (e != cudaSuccess) return e;
+  e = launch(attn_dec_combine_kernel, dim3(Hk, batch), 128, 0, s, (const float*)part, sp, Hk, d, out);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 cudaError_t launch_gelu_mul(const __nv_bfloat16* gu, int64_t M, int I, __nv_bfloat16* m, cudaStream_t s) {
   if (I % 8) return cudaErrorInvalidValue;
   if (M <= 0) return cudaSuccess;
@@ -387,7 +559,8 @@ cudaError_t preload_attn() {
   cudaFuncAttributes a;
   for (const void* f : {(const void*)rmsnorm2_kernel, (const void*)kv_append_kernel, (const void*)kv_advance_kernel,
                         (const void*)attn_kernel<464>, (const void*)attn_kernel<32>, (const void*)attn_kernel<64>,
-                        (const void*)attn_kernel<128>, (const void*)gelu_mul_kernel, (const void*)cast_bf16_kernel}) {
+                        (const void*)attn_kernel<128>, (const void*)gelu_mul_kernel, (const void*)cast_bf16_kernel,
+                        (const void*)attn_dec_kernel, (const void*)attn_dec_combine_kernel}) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
   }

@@ -145,6 +145,13 @@ cudaError_t launch_kv_advance(int* len, int L, int Tmax, cudaStream_t s);
 // included); out [batch*L][Hk d] bf16; d in {32, 64, 128, 464}
 cudaError_t launch_attn(const __nv_bfloat16* qkv, const int* len, const __nv_bfloat16* K, const __nv_bfloat16* V,
                         int batch, int L, int Hk, int d, int Tmax, float scale, __nv_bfloat16* out, cudaStream_t s);
+// decode (L = 1) attention: split over the cached keys (flash decoding) + combine; part: workspace
+// of attn_dec_part_floats floats
+int attn_dec_splits(int batch, int Hk, int Tmax);
+size_t attn_dec_part_floats(int batch, int Hk, int d, int Tmax);
+cudaError_t launch_attn_decode(const __nv_bfloat16* qkv, const int* len, const __nv_bfloat16* K, const __nv_bfloat16* V,
+                               int batch, int Hk, int d, int Tmax, float scale, float* part, __nv_bfloat16* out,
+                               cudaStream_t s);
 cudaError_t launch_gelu_mul(const __nv_bfloat16* gu, int64_t M, int I, __nv_bfloat16* m, cudaStream_t s);
 cudaError_t launch_cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t s);
 cudaError_t preload_attn();
