@@ -163,3 +163,46 @@ def shared_block_weights(adims: AttnDims, seed: int = 3000, layer: int = 0) -> d
     g2 = torch.Generator().manual_seed(seed + 1 + layer)
     w["w_lin"] = _u(g2, (D, D), 1.0 / math.sqrt(D)) / 4.0
     return w
+
+
+# ---------------------------------------------------------------------------------------------
+# Mamba-2 (SSD) mixer: dimensions and seeded weights.
+@dataclass(frozen=True)
+class Mamba2Dims:
+    d_model: int
+    d_inner: int
+    d_state: int = 128
+    headdim: int = 64
+    n_groups: int = 1
+    d_conv: int = 4
+    eps: float = 1e-5
+    n_layers: int = 1
+
+    @property
+    def n_heads(self) -> int:
+        return self.d_inner // self.headdim
+
+
+# Mamba-2 2.7B (public config: d_model 2560, 64 layers, expand 2, d_state 128, headdim 64, 1 group)
+MAMBA2_2P7B = Mamba2Dims(d_model=2560, d_inner=5120, n_layers=64)
+
+
+def mamba2_weights(m2: Mamba2Dims, layer: int = 0, seed: int = 5000) -> dict:
+    """Full weights of one Mamba-2 mixer (float64 CPU; nn.Linear [out, in]); packed
+    w_in rows [z (E) | x (E) | B (G N) | C (G N) | dt (H)], Mamba-2 init ranges: projections
+    U(+-1/sqrt(fan_in)), conv U(+-1/sqrt(K)), dt_bias = softplus^-1(dt0) with dt0 log-uniform in
+    [1e-3, 1e-1], A_log = log U[1, 16] (+ jitter), D = 1, norm weight 1 + N(0, 0.1)."""
+    g = torch.Generator().manual_seed(seed + layer)
+    D, E, N, G, K = m2.d_model, m2.d_inner, m2.d_state, m2.n_groups, m2.d_conv
+    H = m2.n_heads
+    C = E + 2 * G * N
+    w = {"w_in": _u(g, (2 * E + 2 * G * N + H, D), 1.0 / math.sqrt(D)),
+         "conv_w": _u(g, (C, K), 1.0 / math.sqrt(K)), "conv_b": _u(g, (C,), 1.0 / math.sqrt(K))}
+    lo, hi = math.log(1e-3), math.log(1e-1)
+    dt0 = torch.exp(torch.rand((H,), generator=g, dtype=torch.float64) * (hi - lo) + lo)
+    w["dt_bias"] = dt0 + torch.log(-torch.expm1(-dt0))
+    w["a_log"] = torch.log(1.0 + 15.0 * torch.rand((H,), generator=g, dtype=torch.float64))
+    w["d_skip"] = torch.ones((H,), dtype=torch.float64)
+    w["norm_w"] = 1.0 + 0.1 * torch.randn((E,), generator=g, dtype=torch.float64)
+    w["w_out"] = _u(g, (D, E), 1.0 / math.sqrt(E)) / math.sqrt(2.0 * max(m2.n_layers, 1))
+    return w
