@@ -283,6 +283,46 @@ ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ss
 ssm_status_t ssm_rmsnorm_add(ssm_tp_t tp, const float* a, const float* b, const float* weight, float eps, void* x_out,
                              int64_t M, void* stream);
 
+/* ---- Mamba-2 (SSD) mixer under the same TP design ----
+ * Packed in_proj [z | x | B | C | dt], causal conv + SiLU over the x|B|C channels, the scalar-A-per-
+ * head selective scan h <- exp(dt A) h + dt x B, y = C.h + D x (d_state N, head dim P = 64),
+ * gated RMSNorm o = RMSNorm(y SiLU(z)) * w over d_inner (norm after the gate), out_proj.
+ * Tensor parallel (reading M1): rank r owns heads [r H/k, (r+1) H/k) (z, x, dt rows of W_in, their
+ * conv / dt_bias / A_log / D / norm entries, W_out columns); B and C (n_groups == 1) are replicated
+ * on every rank (their W_in rows and conv taps too) -- no all-reduce before the scan; the gated
+ * RMSNorm's per-token sum of squares is all-reduced (exact fp32, M floats), out_proj row-parallel
+ * -> AR#2 into the residual (flags: SSM_AR2_INT8 one-shot, SSM_AR2_FP32, SSM_AR2_FP16, SSM_AR2_BF16).
+ * The handle supplies d_model and the communicator; bf16 only. */
+typedef struct {
+  int32_t d_inner;        /* E (global)                                                       */
+  int32_t d_state;        /* N: 16, 64 or 128                                                 */
+  int32_t headdim;        /* P: 64                                                            */
+  int32_t n_groups;       /* G: 1 (B/C replicated over the ranks)                             */
+  int32_t d_conv;         /* K: 2..4                                                          */
+  float eps;              /* gated RMSNorm                                                    */
+} ssm_m2_config_t;
+typedef struct {          /* rank-local: E_k = E/k, H_k = H/k, C_k = E_k + 2 G N             */
+  const void* w_in;       /* [2 E_k + 2 G N + H_k, D] bf16: rows z_r | x_r | B | C | dt_r      */
+  const float* conv_w;    /* [C_k, K]: x channels of the rank, then B, C                       */
+  const float* conv_b;    /* [C_k]                                                           */
+  const float* dt_bias;   /* [H_k]                                                           */
+  const float* a_log;     /* [H_k]                                                           */
+  const float* d_skip;    /* [H_k]                                                           */
+  const float* norm_w;    /* [E_k]                                                           */
+  const void* w_out;      /* [D, E_k] bf16                                                    */
+} ssm_m2_weights_t;
+/* cache of one layer on this rank: conv window [batch][K-1][C_k] bf16, h [batch][H_k][P][N] fp32 */
+ssm_status_t ssm_m2_state_bytes(ssm_tp_t tp, const ssm_m2_config_t* cfg, int32_t batch, size_t* conv_bytes,
+                                size_t* h_bytes);
+ssm_status_t ssm_m2_workspace_bytes(ssm_tp_t tp, const ssm_m2_config_t* cfg, int32_t batch, int32_t seqlen,
+                                    size_t* bytes);
+/* residual [batch*seqlen, D] fp32 += mixer(x_in [batch*seqlen, D] bf16), row = b L + t; the cache
+ * carries across calls (prefill chunks, then seqlen == 1 decode).  Caller-owned state buffers
+ * (zero = empty cache).  Collective at TP > 1 (two all-reduces). */
+ssm_status_t ssm_m2_mixer(ssm_tp_t tp, const ssm_m2_config_t* cfg, const ssm_m2_weights_t* w, void* conv_state,
+                          float* h_state, const void* x_in, float* residual, int32_t batch, int32_t seqlen,
+                          uint32_t flags, void* workspace, size_t ws_bytes, void* stream);
+
 /* Quantised all-reduce of n fp32 values (n % qar_block == 0), rows of D = d_model:
  * every rank quantises its partial per block (s = amax/127, q = rint(o/s) clamped to
  * +-127), exchanges int8 codes + fp32 scales peer-to-peer, and forms

@@ -55,6 +55,16 @@ class ssm_attn_weights_t(C.Structure):
                 ("w_gu", C.c_void_p), ("w_d", C.c_void_p), ("w_lin", C.c_void_p)]
 
 
+class ssm_m2_config_t(C.Structure):
+    _fields_ = [("d_inner", C.c_int32), ("d_state", C.c_int32), ("headdim", C.c_int32), ("n_groups", C.c_int32),
+                ("d_conv", C.c_int32), ("eps", C.c_float)]
+
+
+class ssm_m2_weights_t(C.Structure):
+    _fields_ = [("w_in", C.c_void_p), ("conv_w", C.c_void_p), ("conv_b", C.c_void_p), ("dt_bias", C.c_void_p),
+                ("a_log", C.c_void_p), ("d_skip", C.c_void_p), ("norm_w", C.c_void_p), ("w_out", C.c_void_p)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libssmtp.so not built ({LIB_PATH}); run `python -m paper_2602_21144_b200.build`")
@@ -81,6 +91,10 @@ def _load():
         "ssm_rmsnorm": (st, [vp, vp, vp, C.c_float, vp, i64, vp]),
         "ssm_tp_check": (st, [vp, vp]),
         "ssm_rmsnorm_add": (st, [vp, vp, vp, vp, C.c_float, vp, i64, vp]),
+        "ssm_m2_state_bytes": (st, [vp, P(ssm_m2_config_t), i32, P(sz), P(sz)]),
+        "ssm_m2_workspace_bytes": (st, [vp, P(ssm_m2_config_t), i32, i32, P(sz)]),
+        "ssm_m2_mixer": (st, [vp, P(ssm_m2_config_t), P(ssm_m2_weights_t), vp, vp, vp, vp, i32, i32, C.c_uint32, vp,
+                              sz, vp]),
         "ssm_kv_bytes": (st, [vp, P(ssm_attn_config_t), i32, P(sz)]),
         "ssm_kv_alloc": (st, [vp, P(ssm_attn_config_t), i32, vp, sz, vp, P(vp)]),
         "ssm_kv_reset": (st, [vp, vp]),
@@ -117,7 +131,8 @@ EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "s
             "ssm_tp_barrier", "ssm_tp_launch_count", "ssm_tp_fused_calls", "ssm_tp_probe", "ssm_tp_probe_read",
             "ssm_packed_weight_bytes", "ssm_pack_weight", "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld",
             "ssm_dbg_scan", "ssm_rmsnorm_add", "ssm_kv_bytes", "ssm_kv_alloc", "ssm_kv_reset", "ssm_kv_free",
-            "ssm_attn_workspace_bytes", "ssm_attn_block"]
+            "ssm_attn_workspace_bytes", "ssm_attn_block", "ssm_m2_state_bytes", "ssm_m2_workspace_bytes",
+            "ssm_m2_mixer"]
 PROBE = {"in_proj": 1, "conv": 2, "x_proj": 3, "dt_proj": 4, "scan": 5, "out_proj": 6, "ar2": 7, "decode_step": 8,
          "in_proj_decode": 9}
 

@@ -628,6 +628,7 @@ ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp
       if (pre == cudaSuccess) pre = preload_gemm_simt();
       if (pre == cudaSuccess) pre = preload_gemm_tc();
       if (pre == cudaSuccess) pre = preload_attn();
+      if (pre == cudaSuccess) pre = preload_ssd();
     });
     if (pre != cudaSuccess) {
       delete t;
@@ -799,7 +800,8 @@ ssm_status_t ssm_qallreduce(ssm_tp_t tp, const float* partial, float* out, size_
   if (flags & ~known) return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
   if ((flags & SSM_QAR_FP16) && (flags & SSM_QAR_BF16)) return fail(SSM_ERR_ARG, "SSM_QAR_FP16 and SSM_QAR_BF16 are exclusive");
   const int blk = tp->cfg.qar_block;
-  if (n % blk) return fail(SSM_ERR_DIM, "n=%zu not a multiple of qar_block=%d", n, blk);
+  if (n % blk && !(flags & (SSM_QAR_FP32 | SSM_QAR_FP16 | SSM_QAR_BF16)))
+    return fail(SSM_ERR_DIM, "n=%zu not a multiple of qar_block=%d", n, blk);
   if ((reinterpret_cast<uintptr_t>(partial) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1193,3 +1195,145 @@ ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ss
 
 }  // extern "C"
 
+namespace {
+struct M2Dims {
+  int D, E, Ek, N, P, G, GN, H, Hk, K, Ck, Wp, ldp;
+};
+ssm_status_t m2_dims(const ssm_tp_s* t, const ssm_m2_config_t* c, M2Dims* o) {
+  if (!c) return fail(SSM_ERR_ARG, "Mamba-2 config is NULL");
+  if (!t->bf16) return fail(SSM_ERR_UNSUPPORTED, "Mamba-2 mixer: bf16 handles only");
+  if (c->headdim != 64 || !(c->d_state == 16 || c->d_state == 64 || c->d_state == 128) || c->n_groups != 1 ||
+      c->d_conv < 2 || c->d_conv > 4)
+    return fail(SSM_ERR_UNSUPPORTED, "Mamba-2: headdim 64, d_state 16/64/128, n_groups 1, 2 <= d_conv <= 4");
+  if (c->d_inner % c->headdim || (c->d_inner / c->headdim) % t->k)
+    return fail(SSM_ERR_SHARD, "Mamba-2: heads (%d) do not split over tp_size=%d", c->d_inner / c->headdim, t->k);
+  M2Dims z{};
+  z.D = t->cfg.d_model;
+  z.E = c->d_inner;
+  z.Ek = z.E / t->k;
+  z.N = c->d_state;
+  z.P = c->headdim;
+  z.G = c->n_groups;
+  z.GN = z.G * z.N;
+  z.H = z.E / z.P;
+  z.Hk = z.H / t->k;
+  z.K = c->d_conv;
+  z.Ck = z.Ek + 2 * z.GN;
+  z.Wp = 2 * z.Ek + 2 * z.GN + z.Hk;
+  z.ldp = (z.Wp + 7) / 8 * 8;  // 16-B rows for the conv kernels' vector loads
+  *o = z;
+  return SSM_OK;
+}
+struct M2Ws {
+  size_t proj, u, y, ss, o, part, total;
+};
+M2Ws m2_ws(const ssm_tp_s* t, const M2Dims& z, int64_t M) {
+  M2Ws L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += al256(bytes); return o; };
+  L.proj = take(M * z.ldp * 2);
+  L.u = take(M * z.Ck * 2);
+  L.y = take(M * z.Ek * 4);
+  L.ss = take(((M + 3) / 4 * 4) * 4);
+  L.o = take(M * z.Ek * 2);
+  L.part = take(t->k > 1 ? M * z.D * 4 : 0);
+  L.total = off;
+  return L;
+}
+}  // namespace
+
+extern "C" {
+
+ssm_status_t ssm_m2_state_bytes(ssm_tp_t tp, const ssm_m2_config_t* cfg, int32_t batch, size_t* conv_bytes,
+                                size_t* h_bytes) {
+  if (!tp || !conv_bytes || !h_bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  M2Dims z;
+  ssm_status_t st = m2_dims(tp, cfg, &z);
+  if (st != SSM_OK) return st;
+  if (batch < 1) return fail(SSM_ERR_DIM, "batch=%d", batch);
+  *conv_bytes = (size_t)batch * (z.K - 1) * z.Ck * 2;
+  *h_bytes = (size_t)batch * z.Hk * z.P * z.N * 4;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_m2_workspace_bytes(ssm_tp_t tp, const ssm_m2_config_t* cfg, int32_t batch, int32_t seqlen,
+                                    size_t* bytes) {
+  if (!tp || !bytes) return fail(SSM_ERR_ARG, "NULL argument");
+  M2Dims z;
+  ssm_status_t st = m2_dims(tp, cfg, &z);
+  if (st != SSM_OK) return st;
+  if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
+  *bytes = m2_ws(tp, z, (int64_t)batch * seqlen).total;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_m2_mixer(ssm_tp_t tp, const ssm_m2_config_t* cfg, const ssm_m2_weights_t* w, void* conv_state,
+                          float* h_state, const void* x_in, float* residual, int32_t batch, int32_t seqlen,
+                          uint32_t flags, void* workspace, size_t ws_bytes, void* stream) {
+  if (!tp) return fail(SSM_ERR_ARG, "tp is NULL");
+  M2Dims z;
+  ssm_status_t st = m2_dims(tp, cfg, &z);
+  if (st != SSM_OK) return st;
+  if (!w || !w->w_in || !w->conv_w || !w->conv_b || !w->dt_bias || !w->a_log || !w->d_skip || !w->norm_w || !w->w_out)
+    return fail(SSM_ERR_ARG, "Mamba-2 weights struct or one of its pointers is NULL");
+  if (!conv_state || !h_state || !x_in || !residual) return fail(SSM_ERR_ARG, "NULL state / input / residual");
+  if ((reinterpret_cast<uintptr_t>(conv_state) | reinterpret_cast<uintptr_t>(h_state) |
+       reinterpret_cast<uintptr_t>(x_in) | reinterpret_cast<uintptr_t>(residual)) & 15)
+    return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
+  if (batch < 0 || seqlen < 0) return fail(SSM_ERR_DIM, "negative batch/seqlen");
+  if (flags & ~(uint32_t)(SSM_AR2_INT8 | SSM_AR2_FP32 | SSM_AR2_FP16 | SSM_AR2_BF16))
+    return fail(SSM_ERR_ARG, "unknown flags 0x%x", flags);
+  const int64_t M = (int64_t)batch * seqlen;
+  if (M == 0) return SSM_OK;
+  const M2Ws L = m2_ws(tp, z, M);
+  if (!workspace || ws_bytes < L.total) return fail(SSM_ERR_ARG, "workspace %zu B < required %zu B", ws_bytes, L.total);
+  if (reinterpret_cast<uintptr_t>(workspace) & 255) return fail(SSM_ERR_ARG, "workspace must be 256-B aligned");
+  if (tp->k > 1 && (size_t)M * z.D * 4 > half_bytes(tp))
+    return fail(SSM_ERR_ARG, "symmetric buffer too small for %lld tokens", (long long)M);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  PdlScope pdl(seqlen == 1 && M <= 256 && !(tp->flags & SSM_COMM_VIRTUAL));
+  char* W = reinterpret_cast<char*>(workspace);
+  __nv_bfloat16* proj = reinterpret_cast<__nv_bfloat16*>(W + L.proj);
+  __nv_bfloat16* u = reinterpret_cast<__nv_bfloat16*>(W + L.u);
+  float* y = reinterpret_cast<float*>(W + L.y);
+  float* ss = reinterpret_cast<float*>(W + L.ss);
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(W + L.o);
+  // packed in_proj [z | x | B | C | dt] of the rank
+  CU(gemm(tp, x_in, z.D, w->w_in, z.D, (int)M, z.Wp, z.D, 1, epi(EPI_STORE_BF16, 0, proj, z.ldp), s));
+  // causal conv + SiLU over the x | B | C channels (window of the cache updated)
+  const __nv_bfloat16* xbc = proj + z.Ek;
+  if (seqlen == 1) {
+    tp->launches++;
+    CU(launch_conv_decode(1, xbc, z.ldp, conv_state, w->conv_w, w->conv_b, u, z.Ck, batch, z.Ck, z.K, nullptr, 0,
+                          nullptr, 0, nullptr, s));
+  } else {
+    tp->launches += 2;
+    CU(launch_conv1d_silu(1, xbc, z.ldp, conv_state, w->conv_w, w->conv_b, u, z.Ck, batch, seqlen, z.Ck, z.K, s));
+    CU(launch_conv_state_update(1, xbc, z.ldp, conv_state, batch, seqlen, z.Ck, z.K, s));
+  }
+  // scan (per head, per sequence); gate + the row's sum of squares; (TP > 1) all-reduce of the
+  // sums; normalise -> out_proj input
+  tp->launches += 3;
+  CU(launch_m2_scan(proj, z.ldp, 2 * z.Ek + 2 * z.GN, u, z.Ck, z.Ek, z.Ek + z.GN, z.H / z.G / tp->k > 0 ? z.Hk : 1,
+                    w->dt_bias, w->a_log, w->d_skip, h_state, y, z.Ek, batch, seqlen, z.Hk, z.P, z.N, s));
+  CU(launch_m2_gate_ss(y, z.Ek, proj, z.ldp, ss, M, s));
+  if (tp->k > 1) {
+    ssm_status_t r = ssm_qallreduce(tp, ss, ss, (size_t)((M + 3) / 4 * 4), SSM_QAR_FP32, stream);
+    if (r != SSM_OK) return r;
+  }
+  CU(launch_m2_norm_apply(y, z.Ek, ss, z.E, cfg->eps, w->norm_w, o, M, s));
+  // out_proj (row-parallel): TP = 1 straight into the residual, else partial + AR#2
+  if (tp->k == 1) {
+    CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, epi(EPI_ADD_F32, 0, residual, z.D), s));
+  } else {
+    float* part = reinterpret_cast<float*>(W + L.part);
+    CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, epi(EPI_STORE_F32, 0, part, z.D), s));
+    const uint32_t qf = (flags & SSM_AR2_FP32) ? SSM_QAR_FP32 : (flags & SSM_AR2_FP16) ? SSM_QAR_FP16
+                      : (flags & SSM_AR2_BF16) ? SSM_QAR_BF16 : 0;
+    ssm_status_t r = ssm_qallreduce(tp, part, residual, (size_t)M * z.D, qf | SSM_QAR_ACCUMULATE, stream);
+    if (r != SSM_OK) return r;
+  }
+  return SSM_OK;
+}
+
+}  // extern "C"

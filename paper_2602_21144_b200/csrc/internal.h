@@ -156,6 +156,17 @@ cudaError_t launch_gelu_mul(const __nv_bfloat16* gu, int64_t M, int I, __nv_bflo
 cudaError_t launch_cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t s);
 cudaError_t preload_attn();
 
+// ---- Mamba-2 (SSD) mixer (ssd.cu) ----
+cudaError_t launch_m2_scan(const __nv_bfloat16* proj, int64_t ldp, int dt_col, const __nv_bfloat16* u, int64_t ldu,
+                           int b_col, int c_col, int heads_per_group, const float* dt_bias, const float* a_log,
+                           const float* d_skip, float* hstate, float* y, int64_t ldy, int batch, int L, int Hk, int P,
+                           int N, cudaStream_t s);
+cudaError_t launch_m2_gate_ss(float* y, int Ek, const __nv_bfloat16* proj, int64_t ldp, float* ss, int64_t M,
+                              cudaStream_t s);
+cudaError_t launch_m2_norm_apply(const float* g, int Ek, const float* ss, int E, float eps, const float* w,
+                                 __nv_bfloat16* o, int64_t M, cudaStream_t s);
+cudaError_t preload_ssd();
+
 // Load every kernel eagerly (called once per process from ssm_tp_init when a device exists).
 cudaError_t preload_kernels();
 cudaError_t preload_gemm_simt();
