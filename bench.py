@@ -33,7 +33,8 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="mamba2.8b", choices=["mamba2.8b", "falcon7b", "zamba7b", "mamba2.8b-long"])
+    p.add_argument("--config", default="mamba2.8b",
+                   choices=["mamba2.8b", "falcon7b", "zamba7b", "mamba2.8b-long", "mamba2-2.7b"])
     p.add_argument("--ar2", default="int8", choices=["int8", "int8-requant", "fp16", "bf16", "fp32", "nccl"],
                    help="AR#2: int8 / fp16 / bf16 / fp32 peer-to-peer (library), or nccl = NCCL bf16 all-reduce "
                         "baseline arm")
@@ -221,8 +222,9 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
         launch_ranks(args)
     import synth
-    dims = synth.CONFIGS["mamba2.8b" if args.config == "mamba2.8b-long" else args.config]
-    wl = dict(synth.WORKLOADS[args.config])
+    mamba2 = args.config == "mamba2-2.7b"   # Mamba-2 (SSD) stack, SURVEY.md §8(f) NEXT-4 (not a BASELINE config)
+    dims = synth.CONFIGS["mamba2.8b" if args.config in ("mamba2.8b-long", "mamba2-2.7b") else args.config]
+    wl = dict(synth.WORKLOADS["mamba2.8b" if mamba2 else args.config])
     n_layers = args.layers or dims.n_layers
     if args.prompt:
         wl["prompt"] = args.prompt
@@ -273,7 +275,7 @@ def main():
         dist.barrier()
     mx = TPMixer(dims, "bf16", rank=rank, tp_size=k, peer_bufs=peer_bufs, buf_bytes=nbytes, device=dev)
     layers = []
-    for l in range(n_layers):
+    for l in range(0 if mamba2 else n_layers):
         full = synthetic_layer(dims, l, device=dev)
         lw = LayerWeights(dims, full, k, rank, "bf16", dev, naive=naive)
         if not args.no_pack:
@@ -289,7 +291,19 @@ def main():
         hybrid = hybrid_config(synth.ZAMBA7B_ATTN, blk_full, lins, k, rank, Lp + max(Ld, 1) + 16, dev)
         del blk_full, lins
     torch.cuda.empty_cache()
-    stack = MixerStack(mx, layers, B, chunk, flags, nccl_group=(dist.group.WORLD if k > 1 else None), hybrid=hybrid)
+    if mamba2:
+        from paper_2602_21144_b200.mamba2 import Mamba2Stack, Mamba2Weights, synthetic_mamba2_layer
+        m2 = synth.MAMBA2_2P7B
+        m2w = []
+        for l in range(n_layers):
+            full = synthetic_mamba2_layer(m2, l, device=dev)
+            m2w.append(Mamba2Weights(m2, full, k, rank, dev))
+            del full
+        torch.cuda.empty_cache()
+        stack = Mamba2Stack(mx, m2, m2w, B, chunk, flags if flags != L.SSM_AR2_EXTERNAL else L.SSM_AR2_INT8)
+    else:
+        stack = MixerStack(mx, layers, B, chunk, flags, nccl_group=(dist.group.WORLD if k > 1 else None),
+                           hybrid=hybrid)
 
     # inputs: replicated on all ranks (same seed); larger than L2 (126 MB) -> no flush needed
     g = torch.Generator(device=dev).manual_seed(42)
@@ -308,7 +322,7 @@ def main():
         # (probe_graph, replayed right after the timed region): event nodes in the timed graph
         # itself would cost ~0.7 ms per step.  The probe slots stay full after this capture, so
         # the timed graph below gets no event nodes.
-        probe_graph = stack.capture_decode(res_t, probes=[("in_proj_decode", n_layers)])
+        probe_graph = stack.capture_decode(res_t, probes=[] if mamba2 else [("in_proj_decode", n_layers)])
         graph = stack.capture_decode(res_t, warmup=False)
 
     def step(timers=None):
@@ -323,7 +337,7 @@ def main():
             timers[1].record()
         for j in range(Ld):
             res_t.copy_(dec_in[j])
-            if stack.hybrid:
+            if getattr(stack, "hybrid", None):
                 stack.h0_dec.copy_(dec_in[j])
             stack.replay(graph)
             dec_out[j].copy_(res_t)
@@ -461,7 +475,9 @@ def main():
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": f"{args.config}: {n_layers} layers"
                                        + (f" ({len(stack.hybrid)} hybrid: shared attention + MLP block first)"
-                                          if stack.hybrid else "")
+                                          if getattr(stack, "hybrid", None) else "")
+                                       + (" of the Mamba-2 (SSD) mixer, d_inner 5120, d_state 128, 80 heads"
+                                          if mamba2 else "")
                                        + f", d_model {dims.d_model}, batch {B}, prompt {Lp} + {Ld} decode",
                            "model": args.config, "global_batch": B,
                            "seq_len": Lp + Ld, "parallelism": f"tp{k}", "ar2": args.ar2 if k > 1 else "none",

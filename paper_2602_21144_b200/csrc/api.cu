@@ -1298,8 +1298,12 @@ ssm_status_t ssm_m2_mixer(ssm_tp_t tp, const ssm_m2_config_t* cfg, const ssm_m2_
   float* y = reinterpret_cast<float*>(W + L.y);
   float* ss = reinterpret_cast<float*>(W + L.ss);
   __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(W + L.o);
-  // packed in_proj [z | x | B | C | dt] of the rank
-  CU(gemm(tp, x_in, z.D, w->w_in, z.D, (int)M, z.Wp, z.D, 1, epi(EPI_STORE_BF16, 0, proj, z.ldp), s));
+  // packed in_proj [z | x | B | C | dt] of the rank (decode: swap-AB, the weights fill the MMA rows)
+  const bool swap = seqlen == 1 && batch <= 32;
+  if (swap)
+    CU(gemm(tp, w->w_in, z.D, x_in, z.D, z.Wp, (int)M, z.D, 1, epi(EPI_STORE_BF16, 1, proj, z.ldp), s, true));
+  else
+    CU(gemm(tp, x_in, z.D, w->w_in, z.D, (int)M, z.Wp, z.D, 1, epi(EPI_STORE_BF16, 0, proj, z.ldp), s));
   // causal conv + SiLU over the x | B | C channels (window of the cache updated)
   const __nv_bfloat16* xbc = proj + z.Ek;
   if (seqlen == 1) {
@@ -1322,12 +1326,23 @@ ssm_status_t ssm_m2_mixer(ssm_tp_t tp, const ssm_m2_config_t* cfg, const ssm_m2_
     if (r != SSM_OK) return r;
   }
   CU(launch_m2_norm_apply(y, z.Ek, ss, z.E, cfg->eps, w->norm_w, o, M, s));
-  // out_proj (row-parallel): TP = 1 straight into the residual, else partial + AR#2
+  // out_proj (row-parallel): TP = 1 straight into the residual, else partial + AR#2 (decode:
+  // swap-AB split-K with fp32 atomics)
   if (tp->k == 1) {
-    CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, epi(EPI_ADD_F32, 0, residual, z.D), s));
+    if (swap)
+      CU(gemm(tp, w->w_out, z.Ek, o, z.Ek, z.D, (int)M, z.Ek, split_for(tp, z.D, z.Ek),
+              epi(EPI_ATOMIC_F32, 1, residual, z.D), s, true));
+    else
+      CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, epi(EPI_ADD_F32, 0, residual, z.D), s));
   } else {
     float* part = reinterpret_cast<float*>(W + L.part);
-    CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, epi(EPI_STORE_F32, 0, part, z.D), s));
+    if (swap) {
+      CU(cudaMemsetAsync(part, 0, (size_t)M * z.D * 4, s));
+      CU(gemm(tp, w->w_out, z.Ek, o, z.Ek, z.D, (int)M, z.Ek, split_for(tp, z.D, z.Ek),
+              epi(EPI_ATOMIC_F32, 1, part, z.D), s, true));
+    } else {
+      CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, epi(EPI_STORE_F32, 0, part, z.D), s));
+    }
     const uint32_t qf = (flags & SSM_AR2_FP32) ? SSM_QAR_FP32 : (flags & SSM_AR2_FP16) ? SSM_QAR_FP16
                       : (flags & SSM_AR2_BF16) ? SSM_QAR_BF16 : 0;
     ssm_status_t r = ssm_qallreduce(tp, part, residual, (size_t)M * z.D, qf | SSM_QAR_ACCUMULATE, stream);

@@ -68,3 +68,86 @@ class Mamba2Mixer:
         ws = self.ws_dec if seqlen == 1 else self.ws
         L.call("ssm_m2_mixer", self.mx.handle, C.byref(self.cfg), C.byref(w.struct), _ptr(self.conv), _ptr(self.h),
                _ptr(x_in), _ptr(residual), self.batch, seqlen, flags, _ptr(ws), ws.numel(), _stream(stream))
+
+
+class Mamba2Stack:
+    """n_layers x [pre-norm RMSNorm (weight 1, reading Q16) -> Mamba-2 mixer -> fp32 residual] on one
+    TP rank: chunk-major prefill carrying the caches into CUDA-graph decode (as stack.MixerStack)."""
+
+    def __init__(self, mixer, m2, weights, batch, max_chunk, flags=L.SSM_AR2_INT8, norm_eps=1e-5):
+        self.mx, self.m2, self.weights, self.batch, self.flags, self.eps = mixer, m2, weights, batch, flags, norm_eps
+        self.layers = [Mamba2Mixer(mixer, m2, batch, max_chunk) for _ in weights]
+        ws, wd = self.layers[0].ws, self.layers[0].ws_dec           # one workspace pair for all layers
+        for lyr in self.layers[1:]:
+            lyr.ws, lyr.ws_dec = ws, wd
+        D = m2.d_model
+        self.xbuf = torch.empty((batch * max_chunk, D), dtype=torch.bfloat16, device=mixer.device)
+        self.xbuf_dec = torch.empty((batch, D), dtype=torch.bfloat16, device=mixer.device)
+        self.graph = None
+        self.graph_launches = 0
+        self._graph_parity = 0
+
+    def reset(self, stream=None):
+        for lyr in self.layers:
+            lyr.reset()
+
+    def prefill_chunk(self, res, stream=None, h0=None):
+        n = res.shape[0]
+        x = self.xbuf[:n]
+        for w, lyr in zip(self.weights, self.layers):
+            self.mx.rmsnorm(res, x, None, self.eps, stream)
+            lyr(w, x, res, n // self.batch, self.flags, stream)
+
+    def decode_step(self, res_t, stream=None):
+        for w, lyr in zip(self.weights, self.layers):
+            self.mx.rmsnorm(res_t, self.xbuf_dec, None, self.eps, stream)
+            lyr(w, self.xbuf_dec, res_t, 1, self.flags, stream)
+
+    def capture_decode(self, res_t, probes=(), warmup=True):
+        if warmup:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self.decode_step(res_t, s)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        before = self.mx.launches()
+        self._graph_parity = self.mx.epoch() & 1
+        e0 = self.mx.epoch()
+        with torch.cuda.graph(g):
+            self.decode_step(res_t)
+            if (self.mx.epoch() - e0) % 2:
+                self.mx.barrier()
+        self.graph_launches = self.mx.launches() - before
+        self.graph = g
+        return g
+
+    def replay(self, graph=None, stream=None):
+        if self.mx.tp_size > 1 and (self.mx.epoch() & 1) != self._graph_parity:
+            self.mx.barrier(stream)
+        (graph or self.graph).replay()
+
+
+def synthetic_mamba2_layer(m2, layer, seed=5000, device="cuda"):
+    """Full Mamba-2 layer weights generated ON the device (the recipe of synth.mamba2_weights) for
+    the full-depth bench."""
+    import math
+    g = torch.Generator(device=device).manual_seed(seed + layer)
+    D, E, N, G, K = m2.d_model, m2.d_inner, m2.d_state, m2.n_groups, m2.d_conv
+    H = m2.n_heads
+    Cd = E + 2 * G * N
+    f = dict(device=device, dtype=torch.float32)
+
+    def u(shape, bound):
+        return (torch.rand(shape, generator=g, **f) * 2 - 1) * bound
+    w = {"w_in": u((2 * E + 2 * G * N + H, D), 1 / math.sqrt(D)), "conv_w": u((Cd, K), 1 / math.sqrt(K)),
+         "conv_b": u((Cd,), 1 / math.sqrt(K))}
+    lo, hi = math.log(1e-3), math.log(1e-1)
+    dt0 = torch.exp(torch.rand((H,), generator=g, **f) * (hi - lo) + lo)
+    w["dt_bias"] = dt0 + torch.log(-torch.expm1(-dt0))
+    w["a_log"] = torch.log(1.0 + 15.0 * torch.rand((H,), generator=g, **f))
+    w["d_skip"] = torch.ones((H,), **f)
+    w["norm_w"] = 1.0 + 0.1 * torch.randn((E,), generator=g, **f)
+    w["w_out"] = u((D, E), 1 / math.sqrt(E)) / math.sqrt(2.0 * max(m2.n_layers, 1))
+    return w
