@@ -62,8 +62,10 @@ if __name__ == "__main__":
     i = 0
     while i < len(args):
         if args[i] == "--full":
-            full(args[i + 1])
-            i += 2
+            i += 1
+            while i < len(args) and args[i].endswith(".ncu-rep"):
+                full(args[i])
+                i += 1
         else:
             launches(args[i])
             i += 1
