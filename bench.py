@@ -49,6 +49,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-pack", action="store_true", help="decode streams the row-major weights (no pre-tiled copy)")
+    p.add_argument("--decode-impl", default="auto", choices=["auto", "persistent", "layer"],
+                   help="persistent = one cooperative launch per token for the whole stack (TP = 1, pure Mamba "
+                        "stacks); layer = the per-layer CUDA-graph decode (4 kernels per layer); auto = persistent "
+                        "where supported")
     return p.parse_args()
 
 
@@ -274,11 +278,15 @@ def main():
         symm = (buf, hdl)
         dist.barrier()
     mx = TPMixer(dims, "bf16", rank=rank, tp_size=k, peer_bufs=peer_bufs, buf_bytes=nbytes, device=dev)
+    want_persistent = (args.decode_impl != "layer" and k == 1 and not mamba2 and args.config != "zamba7b"
+                       and wl["batch"] <= 16)
+    if args.decode_impl == "persistent" and not want_persistent:
+        raise SystemExit("bench.py: --decode-impl persistent needs TP = 1, a pure Mamba stack and batch <= 16")
     layers = []
     for l in range(0 if mamba2 else n_layers):
         full = synthetic_layer(dims, l, device=dev)
         lw = LayerWeights(dims, full, k, rank, "bf16", dev, naive=naive)
-        if not args.no_pack:
+        if not args.no_pack and not want_persistent:
             lw.pack(mx)  # pre-tiled copies of w_in / w_x / w_out for the decode weight streams
         layers.append(lw)
         del full
@@ -304,6 +312,16 @@ def main():
     else:
         stack = MixerStack(mx, layers, B, chunk, flags, nccl_group=(dist.group.WORLD if k > 1 else None),
                            hybrid=hybrid)
+        if want_persistent:
+            try:
+                stack.persistent()
+            except L.SSMError as e:
+                if args.decode_impl == "persistent":
+                    raise
+                print(f"bench.py: persistent decode unsupported here ({e}); per-layer decode", file=sys.stderr)
+                for lw in layers:
+                    lw.pack(mx)
+    persistent = getattr(stack, "dstack", None) is not None
 
     # inputs: replicated on all ranks (same seed); larger than L2 (126 MB) -> no flush needed
     g = torch.Generator(device=dev).manual_seed(42)
@@ -322,7 +340,7 @@ def main():
         # (probe_graph, replayed right after the timed region): event nodes in the timed graph
         # itself would cost ~0.7 ms per step.  The probe slots stay full after this capture, so
         # the timed graph below gets no event nodes.
-        probe_graph = stack.capture_decode(res_t, probes=[] if mamba2 else [("in_proj_decode", n_layers)])
+        probe_graph = stack.capture_decode(res_t, probes=[] if (mamba2 or persistent) else [("in_proj_decode", n_layers)])
         graph = stack.capture_decode(res_t, warmup=False)
 
     def step(timers=None):
@@ -368,7 +386,19 @@ def main():
         barrier()
     pre_ms = mx.probe_read("in_proj")          # prefill in_proj launches of the timed steps
     dec_ms_launch = []
-    if Ld > 0:
+    stack_ms = []
+    if Ld > 0 and persistent:
+        # the persistent kernel is the whole decode step: CUDA events around single-kernel graph
+        # replays on the launching stream, continuing from the timed state
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(8)]
+        for j, (e0, e1) in enumerate(evs):
+            res_t.copy_(dec_in[j % Ld])
+            e0.record()
+            stack.replay(graph)
+            e1.record()
+        torch.cuda.synchronize()
+        stack_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    elif Ld > 0:
         for j in range(min(Ld, 8)):  # probe graph: same decode step, continuing from the timed state
             res_t.copy_(dec_in[j])
             stack.replay(probe_graph)
@@ -461,6 +491,24 @@ def main():
                                 "(in_proj with the conv step and x_proj fused into its epilogue)") if fused
                                else f"W_in 2E_k*D bf16 + x_in + xz = {byts:.3e} B",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    if stack_ms:
+        avg = statistics.mean(stack_ms)
+        P = dims.dt_rank + 2 * dims.d_state
+        E, K, N = dims.d_inner, dims.d_conv, dims.d_state
+        per_layer = (2 * E * D * 2 + D * E * 2 + P * E * 2 + E * dims.dt_rank * 2     # W_in, W_out, W_x, W_dt (bf16)
+                     + E * (K + 3 + N) * 4                                            # conv w/b, b_dt, D, A_log
+                     + 2 * B * E * N * 4 + 2 * B * (K - 1) * E * 2)                   # h and conv window r/w
+        byts = n_layers * per_layer + 2 * B * D * 4                                   # + residual in/out
+        peak = peaks.get("hbm_gbs", 6535.1)
+        ach = byts / (avg / 1000) / 1e9
+        roofs["decode_stack"] = {
+            "kernel": "decode_stack_kernel (persistent whole-stack decode, one launch per token)", "bound": "hbm",
+            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": traffic.get("decode_stack"), "launch_ms": avg, "launches": len(stack_ms),
+            "step_share_ms": avg * Ld,
+            "work_per_launch": (f"{n_layers} layers x (W_in + W_out + W_x + W_dt bf16 + per-channel vectors + h r/w "
+                                f"+ conv window r/w = {per_layer:.4e} B) + residual = {byts:.4e} B"),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     roof = max(roofs.values(), key=lambda r: r["step_share_ms"]) if roofs else None
     roof_other = [r for r in roofs.values() if r is not roof]
 
@@ -483,6 +531,7 @@ def main():
                            "seq_len": Lp + Ld, "parallelism": f"tp{k}", "ar2": args.ar2 if k > 1 else "none",
                            "tp_design": args.tp_design if k > 1 else "none",
                            "prefill_chunk": chunk, "packed_decode_weights": not args.no_pack,
+                           "decode_impl": "persistent" if persistent else "layer",
                            "l2": "inputs larger than L2 (prompt residual "
                                                          f"{B * Lp * D * 4 / 1e6:.0f} MB > 126 MB)"},
                 "ttft_ms": statistics.mean(ttft), "tpot_ms": statistics.mean(dec_ms) / max(Ld, 1),

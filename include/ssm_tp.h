@@ -234,6 +234,37 @@ ssm_status_t ssm_mixer_decode_block(ssm_tp_t tp, const ssm_layer_weights_t* w, s
                                     int32_t batch, float norm_eps, uint32_t flags, void* workspace, size_t ws_bytes,
                                     void* stream);
 
+/* ---- Persistent whole-stack decode at TP = 1 (§4.1) --------
+ * ONE cooperative launch per token runs n_layers pre-norm decode blocks,
+ *   for l in 0..n_layers-1:  residual += mixer_l(RMSNorm(residual))      (weight 1, eps norm_eps)
+ * with the mixer of PAPER.md:151-174 (§2.2) at L = 1 from each layer's cached state: in_proj,
+ * conv step + SiLU, x_proj, dt_proj + softplus, one scan step h = exp(dt A) h + dt B u (ZOH / Euler,
+ * reading Q1), y = C h + D u, gate SiLU(z), out_proj.  Same result as n_layers calls of
+ * ssm_mixer_decode_block up to rounding: the pre-norm's 1/rms is applied after the in_proj
+ * contraction (in_proj(bf16(r)) * rstd instead of in_proj(bf16(r * rstd)); reading Q22)
+ * and dt_low enters dt_proj in bf16.  Each SM streams its share of every layer's weights through a
+ * shared-memory ring; grid barriers separate in_proj | scan step | out_proj.
+ *   ssm_dstack_bytes:   bytes of the caller-owned device buffer for (n_layers, batch, ctas) (ctas = CTAs
+ *                       of the launch, one per SM; 0 = all SMs).
+ *   ssm_dstack_create:  binds `buf` (>= ssm_dstack_bytes, 256-B aligned): re-packs the layers' w_in,
+ *                       w_out, w_x, w_dt into MMA-fragment order inside buf (the originals are not
+ *                       referenced afterwards), keeps POINTERS to conv_w, conv_b, b_dt, a_log, d_skip and
+ *                       to the states' conv window and h (updated in place by every decode: the same
+ *                       caches ssm_mixer_prefill fills), zero-fills the scratch; synchronises `stream`.
+ *                       layers / states: n_layers entries (host arrays).  The handle owns no device memory.
+ *   ssm_dstack_decode:  residual [batch, D] fp32 (16-B aligned) in/out; graph-capturable (a cooperative
+ *                       kernel node).  Every state is advanced by one token.
+ * Errors: SSM_ERR_UNSUPPORTED unless tp_size 1, bf16, n_heads 1, d_state 16, batch <= 16, d_model % 128 == 0
+ * and <= 2816, d_inner % 128 == 0 and <= 5632, dt_rank % 16 == 0; SSM_ERR_CACHE for a state of another
+ * handle or batch; SSM_ERR_ARG for NULL pointers / a short or misaligned buffer / ctas > SMs. */
+typedef struct ssm_dstack_s* ssm_dstack_t;
+ssm_status_t ssm_dstack_bytes(ssm_tp_t tp, int32_t n_layers, int32_t batch, int32_t ctas, size_t* bytes);
+ssm_status_t ssm_dstack_create(ssm_tp_t tp, int32_t n_layers, const ssm_layer_weights_t* layers,
+                               const ssm_state_t* states, int32_t batch, float norm_eps, int32_t ctas, void* buf,
+                               size_t buf_bytes, void* stream, ssm_dstack_t* out);
+ssm_status_t ssm_dstack_decode(ssm_dstack_t ds, float* residual, void* stream);
+ssm_status_t ssm_dstack_destroy(ssm_dstack_t ds);
+
 /* ---- Zamba's shared transformer block ------------------
  * Zamba runs one shared attention + MLP block before its 13 "hybrid" Mamba layers (the public
  * model definition, HF modeling_zamba.py: ZambaAttentionDecoderLayer + the hybrid layer's linear):

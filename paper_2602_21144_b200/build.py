@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build", "libssmtp")
 LIB = os.path.join(HERE, "libssmtp.so")
-SOURCES = ["api.cu", "gemm_tcgen05.cu", "gemm_simt.cu", "kernels.cu", "attn.cu", "ssd.cu"]
+SOURCES = ["api.cu", "gemm_tcgen05.cu", "gemm_simt.cu", "kernels.cu", "attn.cu", "ssd.cu", "decode_stack.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]

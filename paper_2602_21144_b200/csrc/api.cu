@@ -10,6 +10,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/ssm_tp.h"
 #include "internal.h"
@@ -629,6 +630,7 @@ ssm_status_t ssm_tp_init(const ssm_config_t* cfg, const ssm_comm_t* comm, ssm_tp
       if (pre == cudaSuccess) pre = preload_gemm_tc();
       if (pre == cudaSuccess) pre = preload_attn();
       if (pre == cudaSuccess) pre = preload_ssd();
+      if (pre == cudaSuccess) pre = preload_decode_stack();
     });
     if (pre != cudaSuccess) {
       delete t;
@@ -1348,6 +1350,127 @@ ssm_status_t ssm_m2_mixer(ssm_tp_t tp, const ssm_m2_config_t* cfg, const ssm_m2_
     ssm_status_t r = ssm_qallreduce(tp, part, residual, (size_t)M * z.D, qf | SSM_QAR_ACCUMULATE, stream);
     if (r != SSM_OK) return r;
   }
+  return SSM_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- persistent whole-stack decode
+struct ssm_dstack_s {
+  ssm_tp_s* owner;
+  int L, batch, ctas;
+  float eps;
+  DsGeom g;
+  std::vector<DsLayer> table;  // host copy of the device layer table (source of the async upload)
+  DsLayer* table_dev;
+  uint8_t* scratch;
+};
+
+namespace {
+size_t al256z(size_t x) { return (x + 255) & ~size_t(255); }
+
+ssm_status_t dstack_geom(ssm_tp_s* t, int32_t n_layers, int32_t batch, int32_t ctas, DsGeom* g, size_t* bytes) {
+  if (!t) return fail(SSM_ERR_ARG, "tp is NULL");
+  const ssm_config_t& c = t->cfg;
+  if (t->k != 1 || !t->bf16 || c.n_heads != 1 || c.d_state != 16)
+    return fail(SSM_ERR_UNSUPPORTED, "persistent decode: tp_size 1, bf16, n_heads 1, d_state 16 only");
+  if (n_layers < 1 || batch < 1 || batch > 16) return fail(SSM_ERR_UNSUPPORTED, "persistent decode: n_layers >= 1, batch 1..16");
+  const int nc = ctas > 0 ? ctas : t->num_sms;
+  if (nc > t->num_sms) return fail(SSM_ERR_ARG, "ctas=%d > %d SMs (one CTA per SM)", nc, t->num_sms);
+  *g = ds_geometry(batch, c.d_model, c.d_inner, c.dt_rank, t->P, c.d_conv, nc);
+  if (!g->ok)
+    return fail(SSM_ERR_UNSUPPORTED, "persistent decode: shape not supported (d_model=%d d_inner=%d dt_rank=%d batch=%d ctas=%d)",
+                c.d_model, c.d_inner, c.dt_rank, batch, nc);
+  *bytes = al256z((size_t)n_layers * ds_packed_layer_bytes(c.d_model, c.d_inner, c.dt_rank, t->P)) +
+           al256z((size_t)n_layers * sizeof(DsLayer)) + al256z(g->scratch_bytes);
+  return SSM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+ssm_status_t ssm_dstack_bytes(ssm_tp_t tp, int32_t n_layers, int32_t batch, int32_t ctas, size_t* bytes) {
+  if (!bytes) return fail(SSM_ERR_ARG, "bytes is NULL");
+  DsGeom g;
+  return dstack_geom(tp, n_layers, batch, ctas, &g, bytes);
+}
+
+ssm_status_t ssm_dstack_create(ssm_tp_t tp, int32_t n_layers, const ssm_layer_weights_t* layers,
+                               const ssm_state_t* states, int32_t batch, float norm_eps, int32_t ctas, void* buf,
+                               size_t buf_bytes, void* stream, ssm_dstack_t* out) {
+  if (!out) return fail(SSM_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  DsGeom g;
+  size_t need = 0;
+  ssm_status_t st = dstack_geom(tp, n_layers, batch, ctas, &g, &need);
+  if (st != SSM_OK) return st;
+  if (!layers || !states) return fail(SSM_ERR_ARG, "layers/states is NULL");
+  if (!buf || buf_bytes < need) return fail(SSM_ERR_ARG, "buffer %zu B < required %zu B", buf_bytes, need);
+  if (reinterpret_cast<uintptr_t>(buf) & 255) return fail(SSM_ERR_ARG, "buffer must be 256-B aligned");
+  const int nc = ctas > 0 ? ctas : tp->num_sms;
+  if (ds_max_active(g.smem) < 1) return fail(SSM_ERR_CUDA, "persistent decode kernel cannot be resident (%d B smem)", g.smem);
+  const ssm_config_t& c = tp->cfg;
+  const int D = c.d_model, E = c.d_inner, R = c.dt_rank, P = tp->P;
+  for (int l = 0; l < n_layers; ++l) {
+    const ssm_layer_weights_t& w = layers[l];
+    if (!w.w_in || !w.w_out || !w.w_x || !w.w_dt || !w.conv_w || !w.conv_b || !w.b_dt || !w.a_log || !w.d_skip)
+      return fail(SSM_ERR_ARG, "layer %d: a weight pointer is NULL", l);
+    if (!states[l] || states[l]->owner != tp || states[l]->batch != batch)
+      return fail(SSM_ERR_CACHE, "layer %d: state missing, of another handle or of another batch", l);
+  }
+  ssm_dstack_s* ds = new (std::nothrow) ssm_dstack_s();
+  if (!ds) return fail(SSM_ERR_ARG, "out of host memory");
+  ds->owner = tp;
+  ds->L = n_layers;
+  ds->batch = batch;
+  ds->ctas = nc;
+  ds->eps = norm_eps;
+  ds->g = g;
+  ds->table.resize(n_layers);
+  uint8_t* p = reinterpret_cast<uint8_t*>(buf);
+  const size_t lb = ds_packed_layer_bytes(D, E, R, P);
+  uint8_t* packed = p;
+  ds->table_dev = reinterpret_cast<DsLayer*>(p + al256z((size_t)n_layers * lb));
+  ds->scratch = reinterpret_cast<uint8_t*>(ds->table_dev) + al256z((size_t)n_layers * sizeof(DsLayer));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  for (int l = 0; l < n_layers; ++l) {
+    const ssm_layer_weights_t& w = layers[l];
+    uint8_t* dst = packed + (size_t)l * lb;
+    cudaError_t e = ds_pack_layer(reinterpret_cast<const __nv_bfloat16*>(w.w_in), reinterpret_cast<const __nv_bfloat16*>(w.w_out),
+                                  reinterpret_cast<const __nv_bfloat16*>(w.w_x), reinterpret_cast<const __nv_bfloat16*>(w.w_dt),
+                                  D, E, R, P, dst, s);
+    if (e == cudaSuccess)
+      e = ds_fill_layer(&ds->table[l], dst, D, E, R, P, w.conv_w, w.conv_b, w.b_dt, w.a_log, w.d_skip, states[l]->conv,
+                        states[l]->h);
+    if (e != cudaSuccess) {
+      delete ds;
+      return fail(SSM_ERR_CUDA, "packing layer %d: %s", l, cudaGetErrorString(e));
+    }
+  }
+  if (cudaMemcpyAsync(ds->table_dev, ds->table.data(), (size_t)n_layers * sizeof(DsLayer), cudaMemcpyHostToDevice, s) !=
+          cudaSuccess ||
+      cudaMemsetAsync(ds->scratch, 0, g.scratch_bytes, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess) {
+    delete ds;
+    return fail(SSM_ERR_CUDA, "uploading the layer table: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  *out = ds;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_dstack_decode(ssm_dstack_t ds, float* residual, void* stream) {
+  if (!ds) return fail(SSM_ERR_ARG, "dstack is NULL");
+  if (!residual || (reinterpret_cast<uintptr_t>(residual) & 15)) return fail(SSM_ERR_ARG, "residual NULL or not 16-B aligned");
+  ssm_tp_s* t = ds->owner;
+  const ssm_config_t& c = t->cfg;
+  t->launches++;
+  CU(ds_launch(ds->table_dev, ds->L, ds->batch, c.d_model, c.d_inner, c.dt_rank, t->P, c.d_conv, ds->eps, c.bcdt_rmsnorm,
+               c.rms_eps, residual, ds->scratch, ds->g, ds->ctas, reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_dstack_destroy(ssm_dstack_t ds) {
+  delete ds;
   return SSM_OK;
 }
 

@@ -1,0 +1,835 @@
+// decode_stack.cu — persistent whole-stack decode at TP = 1: ONE cooperative launch per token runs
+// every layer's pre-norm + mixer decode step (SURVEY.md §8 rows a1-a7 at L = 1, a10, a11;
+// PAPER.md:276-287 §4.1 "decode from the cached state", §2.2 the mixer).
+//
+// Why a persistent kernel: a decode token is a weight stream (W_in 2E x D, W_out D x E, W_x, W_dt:
+// ~82 MB per Mamba-2.8B layer at batch 16) plus a latency-bound middle (conv step, x_proj reduction,
+// scan step).  The per-layer graph (4 kernels per layer) measured ~34 us per layer against a 14.5 us
+// HBM floor: ~10 us of kernel-boundary latency and an in_proj that streams on 80 of 148 SMs.
+// Here every SM streams its share of every layer's weights through one shared-memory ring that
+// runs ahead across phases and layers (weights never depend on activations), and the three
+// data-dependent steps are separated by grid barriers instead of kernel boundaries:
+//
+//   N0 (once): ss[b] = sum_d r[b][d]^2, xr = bf16(r) in MMA A-fragment order          | barrier
+//   per layer l:
+//   A  in_proj units (8 rows x D): xz = rstd[b] * (W_in bf16(r));  x rows -> conv step + SiLU -> u,
+//      window shift, x_proj partial (mma m16n8k8) -> red.add into xacc;  z rows -> z      | barrier
+//   B  channel groups: dt = softplus(W_dt dt_low + b_dt) (mma m16n8k16), h = exp(dt A) h + dt B u,
+//      y = C h + D u, g = y SiLU(z) -> g in A-fragment order; h written back            | barrier
+//   C  out_proj units (8 rows x E/4): r += W_out g (red.add); the last of a row group's four
+//      contributors re-reads the finished rows -> ss for the next pre-norm, xr = bf16(r) | barrier
+//
+// Pre-norm (reading Q16: RMSNorm, weight 1, eps): the norm is applied after the in_proj contraction,
+// xz[b] = rstd[b] * (W_in bf16(r[b])) -- the same product as W_in bf16(rstd[b] r[b]) up to where the
+// bf16 rounding of the GEMM input falls (reading Q22).
+//
+// CTA roles (512 threads, 1 CTA per SM): warps 0-10 "MMA warps" (mma.sync over bf16 fragments
+// pre-packed in global memory: weights stream in through the ring and are read with one LDS.128 per
+// lane per 32-wide k chunk; activations are register-resident A fragments), warps 11-14 "epilogue
+// warps" (cross-warp reduction of a unit's 8 partials, conv step / z store / x_proj / residual
+// update), warp 15 the producer (one lane issues cp.async.bulk copies of whole units into the ring).
+// Decode GEMMs at batch <= 16 are HBM-bound weight streams (16 flop per weight byte): the tensor
+// pipe of mma.sync is far from the bound, what matters is keeping every SM's stream fed.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace ssm {
+
+namespace {
+
+constexpr int kMW = 11;                     // MMA warps
+constexpr int kEW = 4;                      // epilogue warps
+constexpr int kThreads = (kMW + kEW + 1) * 32;  // + the producer warp: 16 warps, 128 registers per thread
+constexpr int kWork = (kMW + kEW) * 32;     // threads in grid barriers and phase B
+constexpr int kSlots = 8;                   // ring units in flight (mbarrier slots)
+constexpr int kMaxCA = 8;                   // phase A: 32-wide k chunks per MMA warp (D <= 2816)
+constexpr int kMaxCC = 4;                   // phase C: chunks per MMA warp per quarter (E <= 5632)
+constexpr int kMaxPT = 8;                   // x_proj 8-wide p tiles per epilogue warp (P <= 256)
+
+SSM_DEV void mma_1688_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a0), "r"(a1), "r"(b0));
+}
+SSM_DEV uint32_t ld_acquire_gpu_u32(const unsigned* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+SSM_DEV uint4 lds128(uint32_t addr) {  // shared-window address: LDS.128, not a generic load
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+SSM_DEV uint32_t pack_bf2(float lo, float hi) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+SSM_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__host__ __device__ inline int part(int n, int c, int nc) { return (int)(((long long)n * c) / nc); }
+
+// Byte offset of element (b, k) (b < 16) in an A-fragment buffer of an m16 x K bf16 operand:
+// 32-wide k chunk j = k / 32 occupies 1 KB; lane L holds 32 B = the m16n8k16 registers a0..a3 of
+// the chunk's first 16 k, then of its second 16 k (a0: row L/4, k 2(L%4)+{0,1}; a1: row +8; a2: k +8;
+// a3: both).  One lane loads its chunk with two 16-B loads.
+__host__ __device__ inline int afrag_off(int b, int k) {
+  const int j = k >> 5, kk32 = k & 31, half = kk32 >> 4, kk = kk32 & 15;
+  const int reg = (b >> 3) + 2 * (kk >> 3);
+  const int lane = (b & 7) * 4 + ((kk & 7) >> 1);
+  return j * 1024 + lane * 32 + half * 16 + reg * 4 + (kk & 1) * 2;
+}
+
+}  // namespace
+
+struct DsArgs {
+  const DsLayer* layers;
+  int L, B, D, E, R, P, K;
+  float eps;
+  int bcdt_rmsnorm;
+  float rms_eps;
+  float* r;                 // residual [B][D] fp32, updated in place through all layers
+  uint8_t* xr;              // A fragments of bf16(r): D/32 KB (rows >= B stay zero)
+  uint8_t* gf;              // A fragments of g: E/32 KB
+  __nv_bfloat16* u;         // [B][E]
+  __nv_bfloat16* z;         // [B][E]
+  float* xacc;              // [2][16][P]  (zero between uses)
+  float* ssb;               // [2][16]
+  unsigned* cnt;            // [D/8] out_proj contributor counters (zero between uses)
+  unsigned* bar;            // [2] grid-barrier counter, exit counter
+  int ring_bytes, nch_max;  // ring size; max phase-B channels per CTA
+  int off_sb, off_red, off_pb, off_ut, off_misc;
+};
+
+namespace {
+
+// Shared-memory carve-up: everything is an offset from the 1 KB-aligned base, recomputed from the
+// (constant-bank) kernel parameters at each use so no pointer stays live in a register.
+struct Smem {
+  uint8_t* base;
+  const DsArgs* a;
+  SSM_DEV uint8_t* ring() const { return base; }
+  SSM_DEV float* sh() const { return reinterpret_cast<float*>(base + a->off_sb); }                 // [B][nch_max][16]
+  SSM_DEV uint32_t* swdt() const { return reinterpret_cast<uint32_t*>(base + a->off_sb + a->B * a->nch_max * 64); }
+  SSM_DEV float* salog() const {                                                                    // [nch_max][16]
+    return reinterpret_cast<float*>(base + a->off_sb + a->B * a->nch_max * 64 + (a->nch_max / 8) * (a->R / 16) * 256);
+  }
+  SSM_DEV float* sbdt() const { return salog() + a->nch_max * 16; }
+  SSM_DEV float* sdsk() const { return sbdt() + a->nch_max; }
+  SSM_DEV float* sred() const { return reinterpret_cast<float*>(base + a->off_red); }              // [2][kMW][128]
+  SSM_DEV float* sdbc() const { return reinterpret_cast<float*>(base + a->off_pb); }               // [16][P]
+  SSM_DEV float* sdt() const { return sdbc() + 16 * a->P; }                                         // [16][nch_max]
+  SSM_DEV float* sA() const { return sdt() + 16 * a->nch_max; }                                      // [nch_max][16]
+  SSM_DEV __nv_bfloat16* utile() const { return reinterpret_cast<__nv_bfloat16*>(base + a->off_ut); }  // [2][16][8]
+  SSM_DEV uint64_t* full() const { return reinterpret_cast<uint64_t*>(base + a->off_misc); }     // [kSlots]
+  SSM_DEV uint64_t* empty() const { return full() + kSlots; }                                       // [kSlots]
+  SSM_DEV uint64_t* ready() const { return full() + 2 * kSlots; }                                   // [2]
+  SSM_DEV uint64_t* freeb() const { return full() + 2 * kSlots + 2; }                               // [2]
+  SSM_DEV uint64_t* mbB() const { return full() + 2 * kSlots + 4; }                                 // phase-B prefetch
+  SSM_DEV float* srstd() const { return reinterpret_cast<float*>(full() + 2 * kSlots + 5); }       // [16]
+  SSM_DEV float* sss() const { return srstd() + 16; }                                               // [16]
+  SSM_DEV int* slist() const { return reinterpret_cast<int*>(sss() + 16); }                        // [33]
+  SSM_DEV struct Pump* pump() const { return reinterpret_cast<struct Pump*>(base + a->off_misc + 512); }
+};
+
+// Grid barrier over the work threads of every CTA (the producer warp never joins): bar.sync, one
+// thread per CTA releases its arrival and spins on the counter with acquire loads.
+SSM_DEV void grid_sync(unsigned* bar, unsigned target) {
+  named_bar_sync(1, kWork);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire_gpu_u32(bar) < target) {
+    }
+    __threadfence();
+  }
+  named_bar_sync(1, kWork);
+}
+
+// Phase-B prefetch of layer l (h tile, W_dt fragments, A_log, b_dt, D for this CTA's channels):
+// one thread issues bulk copies that complete on mbB.
+SSM_DEV void issue_phase_b_prefetch(const DsArgs& a, const Smem& s, const DsLayer& ly, int gb0, int gb1) {
+  const int nch = 8 * (gb1 - gb0), d0 = 8 * gb0;
+  const uint32_t hb = (uint32_t)nch * 64, wb = (uint32_t)(gb1 - gb0) * (a.R / 16) * 256;
+  const uint32_t tot = (uint32_t)a.B * hb + wb + hb + 2u * nch * 4;
+  mbar_arrive_expect_tx(s.mbB(), tot);
+  if (nch == 0) return;  // (tiny shapes: a CTA without phase-B channels)
+  for (int b = 0; b < a.B; ++b)
+    bulk_g2s(s.sh() + (size_t)b * a.nch_max * 16, ly.h + ((size_t)b * a.E + d0) * 16, hb, s.mbB());
+  bulk_g2s(s.swdt(), ly.wdt + (size_t)gb0 * (a.R / 16) * 256, wb, s.mbB());
+  bulk_g2s(s.salog(), ly.a_log + (size_t)d0 * 16, hb, s.mbB());
+  bulk_g2s(s.sbdt(), ly.b_dt + d0, nch * 4, s.mbB());
+  bulk_g2s(s.sdsk(), ly.d_skip + d0, nch * 4, s.mbB());
+}
+
+// Finalise out_proj row group g8 (all four contributions landed): epilogue thread e = (b, n) reads
+// r[b][8 g8 + n], adds v^2 to the CTA's per-token sum, and writes bf16(v) into the A fragments.
+SSM_DEV void finalize_group(const DsArgs& a, const Smem& s, int g8, int e) {
+  const int b = e >> 3, n = e & 7;
+  const int k = 8 * g8 + n;
+  float v = 0.f;
+  if (b < a.B) v = __ldcg(a.r + (size_t)b * a.D + k);
+  float q = v * v;
+  q += __shfl_xor_sync(0xffffffffu, q, 1);
+  q += __shfl_xor_sync(0xffffffffu, q, 2);
+  q += __shfl_xor_sync(0xffffffffu, q, 4);
+  if (b < a.B) {
+    if (n == 0) atomicAdd(&s.sss()[b], q);
+    *reinterpret_cast<__nv_bfloat16*>(a.xr + afrag_off(b, k)) = __float2bfloat16_rn(v);
+  }
+}
+
+// Ring producer state (lane 0 of the producer warp).
+struct Pump {
+  long long issued, released;
+  int seq, oldest, nA, nC, ua0, uc0, szA, szC, total;
+};
+
+SSM_DEV int pump_size(const Pump& p, int q) { return q % (p.nA + p.nC) < p.nA ? p.szA : p.szC; }
+
+// Issue units while the ring has room; units <= `done` (already consumed by warp 0) may be waited for.
+__device__ __forceinline__ void pump_run(const DsArgs& a, const Smem& s, Pump* pp, int done) {
+  Pump p = *pp;
+  while (p.seq < p.total) {
+    const int sz = pump_size(p, p.seq);
+    bool stop = false;
+    while (p.seq - p.oldest >= kSlots || p.issued + sz - p.released > a.ring_bytes) {
+      if (p.oldest > done) { stop = true; break; }
+      mbar_wait(&s.empty()[p.oldest % kSlots], (p.oldest / kSlots) & 1);
+      p.released += pump_size(p, p.oldest);
+      ++p.oldest;
+    }
+    if (stop) break;
+    const int l = p.seq / (p.nA + p.nC), pos = p.seq % (p.nA + p.nC);
+    const DsLayer& ly = a.layers[l];
+    const uint8_t* src = pos < p.nA ? ly.wa + (size_t)(p.ua0 + pos) * sz : ly.wc + (size_t)(p.uc0 + pos - p.nA) * sz;
+    const int off = (int)(p.issued % a.ring_bytes);
+    uint64_t* fb = &s.full()[p.seq % kSlots];
+    mbar_arrive_expect_tx(fb, (uint32_t)sz);
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const int first = min(sz, a.ring_bytes - off);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(s.ring() + off)),
+        "l"(src), "r"(first), "r"(smem_u32(fb)), "l"(pol)
+        : "memory");
+    if (first < sz)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+              smem_u32(s.ring())),
+          "l"(src + first), "r"(sz - first), "r"(smem_u32(fb)), "l"(pol)
+          : "memory");
+    p.issued += sz;
+    ++p.seq;
+  }
+  *pp = p;
+}
+
+// Unit-sequence counters shared by the MMA and epilogue warps: ring unit index (mbarrier slot /
+// parity), reduction-buffer unit index, ring byte offset of the next unit.
+struct Ctr {
+  int seq, useq, roff;
+};
+
+// MMA warps over units [u0, u1) of a phase: activation A fragments register-resident (chunk j of the
+// unit's k range at frag + ((u / qdiv) * nch + j) KB, reloaded when u / qdiv changes; qdiv = 0: one
+// k range), weight B fragments from the ring, partial [16 x 8] -> the unit's reduction buffer.
+template <int MAXC>
+__device__ __noinline__ Ctr mma_units(const DsArgs& a, uint8_t* base, const uint8_t* frag, int nch, int qdiv,
+                                      int u0, int u1, int sz, Ctr ct) {
+  const Smem s{base, &a};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ring = smem_u32(s.ring());
+  // segments of units sharing one k range (qdiv = 0: all of them): the A fragments are loaded once
+  // per segment, so they stay in registers across the segment's units
+  for (int us = u0; us < u1;) {
+    const int q = qdiv ? us / qdiv : 0;
+    const int ue = qdiv ? min(u1, (q + 1) * qdiv) : u1;
+    uint32_t xa[MAXC][8];
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      const int j = min(warp + kMW * i, nch - 1);
+      const uint8_t* fp = frag + (size_t)(q * nch + j) * 1024 + lane * 32;
+      const uint4 v0 = __ldcg(reinterpret_cast<const uint4*>(fp));
+      const uint4 v1 = __ldcg(reinterpret_cast<const uint4*>(fp + 16));
+      xa[i][0] = v0.x; xa[i][1] = v0.y; xa[i][2] = v0.z; xa[i][3] = v0.w;
+      xa[i][4] = v1.x; xa[i][5] = v1.y; xa[i][6] = v1.z; xa[i][7] = v1.w;
+    }
+    for (int u = us; u < ue; ++u, ++ct.seq, ++ct.useq) {
+      const int slot = ct.seq % kSlots;
+      mbar_wait(&s.full()[slot], (ct.seq / kSlots) & 1);
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < MAXC; ++i) {
+        const int j = warp + kMW * i;
+        if (j < nch) {
+          int o = ct.roff + j * 512 + lane * 16;
+          if (o >= a.ring_bytes) o -= a.ring_bytes;
+          const uint4 w4 = lds128(ring + o);
+          const uint32_t a0[4] = {xa[i][0], xa[i][1], xa[i][2], xa[i][3]};
+          const uint32_t a1[4] = {xa[i][4], xa[i][5], xa[i][6], xa[i][7]};
+          mma_16816_bf16(acc, a0, w4.x, w4.y);
+          mma_16816_bf16(acc, a1, w4.z, w4.w);
+        }
+      }
+      mbar_arrive(&s.empty()[slot]);
+      mbar_wait(&s.freeb()[ct.useq & 1], ((ct.useq >> 1) & 1) ^ 1);
+      float* sp = s.sred() + (ct.useq & 1) * (kMW * 128) + warp * 128;
+      sp[lane] = acc[0]; sp[32 + lane] = acc[1]; sp[64 + lane] = acc[2]; sp[96 + lane] = acc[3];
+      mbar_arrive(&s.ready()[ct.useq & 1]);
+      ct.roff += sz;
+      if (ct.roff >= a.ring_bytes) ct.roff -= a.ring_bytes;
+    }
+    us = ue;
+  }
+  return ct;
+}
+
+// Epilogue thread e = (b = e / 8, n = e % 8): the unit's output element (token b, row n), summed over
+// the kMW partials in fixed warp order.
+SSM_DEV float reduce_unit(const Smem& s, int useq, int b, int n) {
+  const float* sp = s.sred() + (useq & 1) * (kMW * 128) + ((b >> 3) * 2 + (n & 1)) * 32 + (b & 7) * 4 + (n >> 1);
+  float v = 0.f;
+#pragma unroll
+  for (int w = 0; w < kMW; ++w) v += sp[w * 128];
+  return v;
+}
+
+// Phase A epilogue warps: z rows -> z; x rows -> conv step + SiLU -> u, window shift, x_proj partial.
+__device__ __noinline__ Ctr epi_units_a(const DsArgs& a, uint8_t* base, int l, int u0, int u1, Ctr ct) {
+  const Smem s{base, &a};
+  const DsLayer& ly = a.layers[l];
+  const int e = threadIdx.x - kMW * 32, ew = e >> 5, lane = threadIdx.x & 31;
+  const int b = e >> 3, n = e & 7;
+  const int B = a.B, E = a.E, P = a.P, K = a.K;
+  if (e < 16) s.srstd()[e] = rsqrtf(__ldcg(a.ssb + (l & 1) * 16 + e) / (float)a.D + a.eps);
+  named_bar_sync(2, kEW * 32);
+  const float rs = s.srstd()[b];
+  float xp[kMaxPT][4];
+#pragma unroll
+  for (int k = 0; k < kMaxPT; ++k) xp[k][0] = xp[k][1] = xp[k][2] = xp[k][3] = 0.f;
+  const int npt = P / 8;
+  int ux = 0;
+  for (int u = u0; u < u1; ++u, ++ct.seq, ++ct.useq) {
+    const bool is_x = (u & 1) == 0;
+    const int i = u >> 1, f = 8 * i + n;
+    // loads independent of the contraction, in flight while the unit streams
+    float cw[4] = {0.f, 0.f, 0.f, 0.f}, cb = 0.f;
+    uint32_t win[3] = {0u, 0u, 0u};
+    uint32_t wx[kMaxPT];
+    if (is_x) {
+      if (b < B) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < K) cw[j] = ly.conv_w[(size_t)f * K + j];
+        cb = ly.conv_b[f];
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (j < K - 1) win[j] = reinterpret_cast<const uint16_t*>(ly.cst)[((size_t)b * (K - 1) + j) * E + f];
+      }
+#pragma unroll
+      for (int k = 0; k < kMaxPT; ++k) {
+        const int t = ew + kEW * k;
+        wx[k] = t < npt ? ly.wxf[((size_t)i * npt + t) * 32 + lane] : 0u;
+      }
+    }
+    mbar_wait(&s.ready()[ct.useq & 1], (ct.useq >> 1) & 1);
+    float v = reduce_unit(s, ct.useq, b, n);
+    mbar_arrive(&s.freeb()[ct.useq & 1]);
+    v *= rs;
+    if (!is_x) {
+      if (b < B) a.z[(size_t)b * E + f] = __float2bfloat16_rn(v);
+      continue;
+    }
+    // causal conv step (tap K-1 = this token) + SiLU; the window shifts by one
+    const float x = __bfloat162float(__float2bfloat16_rn(v));
+    float acc = cb;
+    float wl = cw[1];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      if (j < K - 1) acc = fmaf(cw[j], __uint_as_float(win[j] << 16), acc);
+#pragma unroll
+    for (int j = 2; j < 4; ++j)
+      if (j == K - 1) wl = cw[j];
+    acc = fmaf(wl, x, acc);
+    const __nv_bfloat16 ub = __float2bfloat16_rn(silu<true>(acc));
+    __nv_bfloat16* ut = s.utile() + (ux & 1) * 128;
+    ut[b * 8 + n] = b < B ? ub : __float2bfloat16_rn(0.f);
+    if (b < B) {
+      a.u[(size_t)b * E + f] = ub;
+      uint16_t* cs = reinterpret_cast<uint16_t*>(ly.cst);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (j < K - 2) cs[((size_t)b * (K - 1) + j) * E + f] = (uint16_t)win[j + 1];
+      ly.cst[((size_t)b * (K - 1) + (K - 2)) * E + f] = __float2bfloat16_rn(x);
+    }
+    named_bar_sync(2, kEW * 32);
+    // x_proj partial of these 8 channels: xp[b][p] += sum_n u[b][n] W_x[p][8i + n]  (m16n8k8)
+    const uint32_t a0 = *reinterpret_cast<const uint32_t*>(ut + (lane >> 2) * 8 + 2 * (lane & 3));
+    const uint32_t a1 = *reinterpret_cast<const uint32_t*>(ut + ((lane >> 2) + 8) * 8 + 2 * (lane & 3));
+#pragma unroll
+    for (int k = 0; k < kMaxPT; ++k)
+      if (ew + kEW * k < npt) mma_1688_bf16(xp[k], a0, a1, wx[k]);
+    ++ux;
+  }
+  // this CTA's x_proj partials -> xacc (fp32 reductions)
+  float* xacc = a.xacc + (l & 1) * 16 * P;
+#pragma unroll
+  for (int k = 0; k < kMaxPT; ++k) {
+    const int t = ew + kEW * k;
+    if (t < npt) {
+      const int p = 8 * t + 2 * (lane & 3), br = lane >> 2;
+      if (br < B) red_add_v2(xacc + br * P + p, xp[k][0], xp[k][1]);
+      if (br + 8 < B) red_add_v2(xacc + (br + 8) * P + p, xp[k][2], xp[k][3]);
+    }
+  }
+  return ct;
+}
+
+// Phase C epilogue warps: r += the unit's partial (fp32 reductions); the fourth contributor of a row
+// group finalises it (ss for the next pre-norm, xr = bf16(r)) unless this is the last layer.
+__device__ __noinline__ Ctr epi_units_c(const DsArgs& a, uint8_t* base, int l, int u0, int u1, Ctr ct) {
+  const Smem s{base, &a};
+  const int e = threadIdx.x - kMW * 32, ew = e >> 5, lane = threadIdx.x & 31;
+  const int b = e >> 3, n = e & 7;
+  const int D = a.D;
+  unsigned res = 0u;
+  int ui = 0;
+  for (int u = u0; u < u1; ++u, ++ct.seq, ++ct.useq, ++ui) {
+    const int g8 = u % (D / 8);
+    mbar_wait(&s.ready()[ct.useq & 1], (ct.useq >> 1) & 1);
+    const float v = reduce_unit(s, ct.useq, b, n);
+    mbar_arrive(&s.freeb()[ct.useq & 1]);
+    if (b < a.B) red_add_f32(a.r + (size_t)b * D + 8 * g8 + n, v);
+    __threadfence();
+    named_bar_sync(2, kEW * 32);
+    // contributor count of the row group; the result is only inspected after the last unit
+    if (e == ui) res = atomicAdd(&a.cnt[g8], 1u);
+  }
+  const int nu = u1 - u0;
+  const bool last = e < nu && res == 3u;
+  if (last) a.cnt[(u0 + e) % (D / 8)] = 0u;
+  if (l + 1 < a.L) {
+    if (ew == 0) {
+      const unsigned m = __ballot_sync(0xffffffffu, last);
+      if (lane == 0) s.slist()[0] = __popc(m);
+      if (last) s.slist()[1 + __popc(m & ((1u << lane) - 1u))] = (u0 + lane) % (D / 8);
+    }
+    __threadfence();
+    named_bar_sync(2, kEW * 32);
+    const int nl = s.slist()[0];
+    for (int q = 0; q < nl; ++q) finalize_group(a, s, s.slist()[1 + q], e);
+    named_bar_sync(2, kEW * 32);
+    if (e < a.B) {
+      atomicAdd(&a.ssb[((l & 1) ^ 1) * 16 + e], s.sss()[e]);
+      s.sss()[e] = 0.f;
+    }
+  }
+  return ct;
+}
+
+// Phase B (all work threads): dt_proj + softplus + scan step + D skip + gate for this CTA's channels.
+__device__ __noinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, int gb0, int gb1) {
+  const Smem s{base, &a};
+  const DsLayer& ly = a.layers[l];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int B = a.B, E = a.E, P = a.P, R = a.R;
+  const int nch = 8 * (gb1 - gb0), d0 = 8 * gb0, ng = gb1 - gb0;
+  const float* xacc = a.xacc + (l & 1) * 16 * P;
+  if (blockIdx.x == 0 && tid < 16) a.ssb[((l & 1) ^ 1) * 16 + tid] = 0.f;
+  for (int i = tid; i < 16 * (P / 4); i += kWork) {
+    const int bb = i / (P / 4), q = i % (P / 4);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (bb < B) v = __ldcg(reinterpret_cast<const float4*>(xacc + bb * P) + q);
+    reinterpret_cast<float4*>(s.sdbc() + bb * P)[q] = v;
+  }
+  // this thread's items (b, ch): u and z loads in flight
+  const int nit = B * nch;
+  float uu0 = 0.f, zz0 = 0.f, uu1 = 0.f, zz1 = 0.f;
+  if (tid < nit) {
+    const int bb = tid / nch, ch = tid % nch;
+    uu0 = __bfloat162float(__ldcg(a.u + (size_t)bb * E + d0 + ch));
+    zz0 = __bfloat162float(__ldcg(a.z + (size_t)bb * E + d0 + ch));
+  }
+  if (tid + kWork < nit) {
+    const int bb = (tid + kWork) / nch, ch = (tid + kWork) % nch;
+    uu1 = __bfloat162float(__ldcg(a.u + (size_t)bb * E + d0 + ch));
+    zz1 = __bfloat162float(__ldcg(a.z + (size_t)bb * E + d0 + ch));
+  }
+  mbar_wait(s.mbB(), l & 1);
+  for (int i = tid; i < nch * 16; i += kWork) s.sA()[i] = -expf(s.salog()[i]) * 1.4426950408889634f;
+  named_bar_sync(1, kWork);
+  if (a.bcdt_rmsnorm) {  // weightless RMSNorm of dt_low, B, C per token (Falcon-Mamba, reading Q18)
+    for (int bb = warp; bb < B; bb += kMW + kEW) {
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+      for (int p = lane; p < P; p += 32) {
+        const float v = s.sdbc()[bb * P + p];
+        if (p < R) s0 = fmaf(v, v, s0);
+        else if (p < R + 16) s1 = fmaf(v, v, s1);
+        else s2 = fmaf(v, v, s2);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      const float r0 = 1.0f / sqrtf(s0 / (float)R + a.rms_eps), r1 = 1.0f / sqrtf(s1 / 16.f + a.rms_eps),
+                  r2 = 1.0f / sqrtf(s2 / 16.f + a.rms_eps);
+      __syncwarp();
+      for (int p = lane; p < P; p += 32) s.sdbc()[bb * P + p] *= (p < R ? r0 : p < R + 16 ? r1 : r2);
+    }
+    named_bar_sync(1, kWork);
+  }
+  // dt_proj on the tensor pipe: dt[b][ch] = sum_r dt_low[b][r] W_dt[ch][r] (m16n8k16, warp = 8 channels)
+  if (warp < ng) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int br = lane >> 2, kq = 2 * (lane & 3);
+    const uint2* wb = reinterpret_cast<const uint2*>(s.swdt()) + warp * (R / 16) * 32 + lane;
+#pragma unroll 2
+    for (int st = 0; st < R / 16; ++st) {
+      const float* r0 = s.sdbc() + br * P + 16 * st + kq;
+      const float* r1 = r0 + 8 * P;
+      const uint32_t af[4] = {pack_bf2(r0[0], r0[1]), pack_bf2(r1[0], r1[1]), pack_bf2(r0[8], r0[9]),
+                              pack_bf2(r1[8], r1[9])};
+      const uint2 w2 = wb[st * 32];
+      mma_16816_bf16(acc, af, w2.x, w2.y);
+    }
+    const int ch = 8 * warp + kq;
+    float* sdt = s.sdt();
+    sdt[br * a.nch_max + ch] = softplus(acc[0] + s.sbdt()[ch]);
+    sdt[br * a.nch_max + ch + 1] = softplus(acc[1] + s.sbdt()[ch + 1]);
+    sdt[(br + 8) * a.nch_max + ch] = softplus(acc[2] + s.sbdt()[ch]);
+    sdt[(br + 8) * a.nch_max + ch + 1] = softplus(acc[3] + s.sbdt()[ch + 1]);
+  }
+  named_bar_sync(1, kWork);
+#pragma unroll 1
+  for (int q = 0; q < 2; ++q) {  // (not unrolled: one item's 16 states live at a time)
+    const int it = tid + q * kWork;
+    const float uq = q == 0 ? uu0 : uu1, zq = q == 0 ? zz0 : zz1;
+    if (it < nit) {
+      const int bb = it / nch, ch = it % nch;
+      const float dt = s.sdt()[bb * a.nch_max + ch];
+      const float du = dt * uq;
+      const float* hp = s.sh() + ((size_t)bb * a.nch_max + ch) * 16;
+      const float* Ac = s.sA() + ch * 16;
+      const float* Bv = s.sdbc() + bb * P + R;
+      const float* Cv = Bv + 16;
+      float y = 0.f;
+      float* hg = ly.h + ((size_t)bb * E + d0 + ch) * 16;
+#pragma unroll
+      for (int nn = 0; nn < 16; nn += 4) {
+        const float4 h4 = *reinterpret_cast<const float4*>(hp + nn);
+        const float4 a4 = *reinterpret_cast<const float4*>(Ac + nn);
+        const float4 b4 = *reinterpret_cast<const float4*>(Bv + nn);
+        const float4 c4 = *reinterpret_cast<const float4*>(Cv + nn);
+        float4 o;  // h_t = exp(dt A) h_{t-1} + dt B_t u_t  (ZOH for A, Euler for B: reading Q1)
+        o.x = fmaf(ex2_approx(dt * a4.x), h4.x, du * b4.x);
+        o.y = fmaf(ex2_approx(dt * a4.y), h4.y, du * b4.y);
+        o.z = fmaf(ex2_approx(dt * a4.z), h4.z, du * b4.z);
+        o.w = fmaf(ex2_approx(dt * a4.w), h4.w, du * b4.w);
+        y = fmaf(c4.x, o.x, y); y = fmaf(c4.y, o.y, y); y = fmaf(c4.z, o.z, y); y = fmaf(c4.w, o.w, y);
+        *reinterpret_cast<float4*>(hg + nn) = o;
+      }
+      y = fmaf(s.sdsk()[ch], uq, y);
+      *reinterpret_cast<__nv_bfloat16*>(a.gf + afrag_off(bb, d0 + ch)) = __float2bfloat16_rn(y * silu<true>(zq));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) decode_stack_kernel(const __grid_constant__ DsArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const Smem s{base, &a};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c = blockIdx.x, nc = gridDim.x;
+  const int D = a.D, E = a.E;
+  const int UA = E / 4;                    // in_proj units (2E rows / 8)
+  const int UC = D / 2;                    // out_proj units (4 quarters x D/8)
+  const int ua0 = part(UA, c, nc), ua1 = part(UA, c + 1, nc);
+  const int uc0 = part(UC, c, nc), uc1 = part(UC, c + 1, nc);
+  const int gb0 = part(E / 8, c, nc), gb1 = part(E / 8, c + 1, nc);
+
+  if (tid == 0) {
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&s.full()[i], 1);
+      mbar_init(&s.empty()[i], kMW * 32);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s.ready()[i], kMW * 32);
+      mbar_init(&s.freeb()[i], kEW * 32);
+    }
+    mbar_init(s.mbB(), 1);
+    fence_barrier_init();
+  }
+  if (tid < 16) s.sss()[tid] = 0.f;
+  __syncthreads();
+
+  // ---------------- ring producer (warp kMW + kEW, lane 0): every layer's A units then C units of this
+  // CTA in order (cp.async.bulk, L2 evict-first), as far as ring space allows -- weights never
+  // depend on activations, so the stream runs ahead across phases, barriers and layers
+  if (warp == kMW + kEW) {
+    if (lane == 0) {
+      Pump* pump = s.pump();
+      Pump p{};
+      p.nA = ua1 - ua0; p.nC = uc1 - uc0; p.ua0 = ua0; p.uc0 = uc0; p.szA = 16 * D; p.szC = 4 * E;
+      p.total = a.L * (p.nA + p.nC);
+      *pump = p;
+      pump_run(a, s, pump, 0x7fffffff);
+    }
+    return;
+  }
+
+  // ---------------- work threads: MMA warps 0..kMW-1, epilogue warps kMW..kMW+kEW-1
+  const bool mw = warp < kMW;
+  unsigned nbar = 0;
+  Ctr ct{0, 0, 0};
+  if (tid == 0) issue_phase_b_prefetch(a, s, a.layers[0], gb0, gb1);
+
+  // ---- N0: ss and xr of the input residual (row groups of 8 columns, split over the CTAs)
+  if (!mw) {
+    const int g0 = part(D / 8, c, nc), g1 = part(D / 8, c + 1, nc);
+    for (int g = g0; g < g1; ++g) finalize_group(a, s, g, tid - kMW * 32);
+  }
+  named_bar_sync(1, kWork);
+  if (tid < a.B) {
+    atomicAdd(&a.ssb[tid], s.sss()[tid]);
+    s.sss()[tid] = 0.f;
+  }
+  grid_sync(a.bar, (++nbar) * nc);
+
+  for (int l = 0; l < a.L; ++l) {
+    const DsLayer& ly = a.layers[l];
+    // ---- A: in_proj + conv step + x_proj partial
+    if (mw) ct = mma_units<kMaxCA>(a, base, a.xr, D / 32, 0, ua0, ua1, 16 * D, ct);
+    else ct = epi_units_a(a, base, l, ua0, ua1, ct);
+    grid_sync(a.bar, (++nbar) * nc);
+    // ---- B: dt_proj + softplus + scan step + D skip + gate
+    phase_b(a, base, l, gb0, gb1);
+    grid_sync(a.bar, (++nbar) * nc);
+    // ---- C: out_proj (K quarters) -> residual
+    if (tid == 0 && l + 1 < a.L) issue_phase_b_prefetch(a, s, a.layers[l + 1], gb0, gb1);
+    if (c == 0) {
+      float* xacc = a.xacc + (l & 1) * 16 * a.P;
+      for (int i = tid; i < 16 * a.P; i += kWork) xacc[i] = 0.f;  // re-armed for layer l + 2
+      if (l + 1 == a.L && tid < 32) a.ssb[tid] = 0.f;             // both pre-norm sums zero for the next launch
+    }
+    if (mw) ct = mma_units<kMaxCC>(a, base, a.gf, E / 128, D / 8, uc0, uc1, 4 * E, ct);
+    else ct = epi_units_c(a, base, l, uc0, uc1, ct);
+    (void)ly;
+    if (l + 1 < a.L) grid_sync(a.bar, (++nbar) * nc);
+  }
+
+  // exit: the last CTA out resets the barrier counter for the next launch
+  named_bar_sync(1, kWork);
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(a.bar + 1, 1u) == (unsigned)nc - 1) {
+      atomicExch(a.bar, 0u);
+      atomicExch(a.bar + 1, 0u);
+    }
+  }
+  (void)lane;
+}
+
+// ---------------------------------------------------------------- weight packing (once per plan)
+// B fragments of an 8-row block over a 32-wide k chunk: lane L holds W[row0 + L/4][k0 + 2q + {0,1}],
+// [+8], [+16], [+24] (q = L % 4) = the m16n8k16 registers b0, b1 of two k16 steps.
+__device__ __forceinline__ uint4 bfrag8x32(const __nv_bfloat16* W, int64_t ld, int row, int k0, int lane) {
+  const int q = lane & 3;
+  const __nv_bfloat16* p = W + (int64_t)row * ld + k0 + 2 * q;
+  uint4 o;
+  o.x = *reinterpret_cast<const uint32_t*>(p);
+  o.y = *reinterpret_cast<const uint32_t*>(p + 8);
+  o.z = *reinterpret_cast<const uint32_t*>(p + 16);
+  o.w = *reinterpret_cast<const uint32_t*>(p + 24);
+  return o;
+}
+
+// in_proj [2E][D] -> units (x group i = 2i, z group i = 2i+1) of D/32 chunks
+__global__ void pack_wa_kernel(const __nv_bfloat16* __restrict__ w, int E, int D, uint4* __restrict__ out) {
+  const int64_t n = (int64_t)(E / 4) * (D / 32) * 32;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(v & 31);
+    const int64_t cu = v >> 5;
+    const int j = (int)(cu % (D / 32));
+    const int u = (int)(cu / (D / 32));
+    const int row = ((u & 1) ? E : 0) + 8 * (u >> 1) + (lane >> 2);
+    out[v] = bfrag8x32(w, D, row, 32 * j, lane);
+  }
+}
+// out_proj [D][E] -> units (quarter qq, row group g) = qq * D/8 + g of E/128 chunks
+__global__ void pack_wc_kernel(const __nv_bfloat16* __restrict__ w, int D, int E, uint4* __restrict__ out) {
+  const int64_t n = (int64_t)(D / 2) * (E / 128) * 32;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(v & 31);
+    const int64_t cu = v >> 5;
+    const int j = (int)(cu % (E / 128));
+    const int u = (int)(cu / (E / 128));
+    const int qq = u / (D / 8), g = u % (D / 8);
+    out[v] = bfrag8x32(w, E, 8 * g + (lane >> 2), qq * (E / 4) + 32 * j, lane);
+  }
+}
+// x_proj [P][E] -> [E/8][P/8][32] u32: {W_x[8t + L/4][8i + 2q], +1}
+__global__ void pack_wx_kernel(const __nv_bfloat16* __restrict__ w, int P, int E, uint32_t* __restrict__ out) {
+  const int64_t n = (int64_t)(E / 8) * (P / 8) * 32;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(v & 31);
+    const int t = (int)((v >> 5) % (P / 8));
+    const int i = (int)((v >> 5) / (P / 8));
+    out[v] = *reinterpret_cast<const uint32_t*>(w + (int64_t)(8 * t + (lane >> 2)) * E + 8 * i + 2 * (lane & 3));
+  }
+}
+// dt_proj [E][R] -> [E/8][R/16][32] x 8 B: {W_dt[8g + L/4][16s + 2q], +1, [+8], [+9]}
+__global__ void pack_wdt_kernel(const __nv_bfloat16* __restrict__ w, int E, int R, uint2* __restrict__ out) {
+  const int64_t n = (int64_t)(E / 8) * (R / 16) * 32;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(v & 31);
+    const int st = (int)((v >> 5) % (R / 16));
+    const int g = (int)((v >> 5) / (R / 16));
+    const __nv_bfloat16* p = w + (int64_t)(8 * g + (lane >> 2)) * R + 16 * st + 2 * (lane & 3);
+    out[v] = make_uint2(*reinterpret_cast<const uint32_t*>(p), *reinterpret_cast<const uint32_t*>(p + 8));
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+size_t ds_packed_layer_bytes(int D, int E, int R, int P) {
+  auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  return al((size_t)2 * E * D * 2) + al((size_t)D * E * 2) + al((size_t)E * P * 2) + al((size_t)E * R * 2);
+}
+
+DsGeom ds_geometry(int B, int D, int E, int R, int P, int K, int num_sms) {  // num_sms: grid size
+  DsGeom g{};
+  g.ok = B >= 1 && B <= 16 && D % 128 == 0 && D / 32 <= kMW * kMaxCA && E % 128 == 0 && E / 128 <= kMW * kMaxCC &&
+         R % 16 == 0 && P == R + 32 && P % 8 == 0 && P / 8 <= kEW * kMaxPT && K >= 2 && K <= 4 && num_sms >= 1;
+  const int gmax = (E / 8 + num_sms - 1) / num_sms;
+  g.nch_max = 8 * gmax;
+  auto al = [](int x) { return (x + 127) & ~127; };
+  const int sb = al(B * g.nch_max * 64) + al(gmax * (R / 16) * 256) + al(g.nch_max * 64) + al(g.nch_max * 4) * 2;
+  const int red = 2 * kMW * 128 * 4;
+  const int pbz = al(16 * P * 4) + al(16 * g.nch_max * 4) + al(g.nch_max * 16 * 4);
+  const int ut = 2 * 16 * 8 * 2;
+  const int misc = 512 + 128;  // mbarriers, rstd, ss, finalise list | pump state
+  const int fixed = sb + red + pbz + ut + misc;
+  const int budget = 227 * 1024 - 1024;  // dynamic smem minus the 1 KB alignment slack
+  int ring = (budget - fixed) / 4096 * 4096;
+  const int maxunit = 16 * D > 4 * E ? 16 * D : 4 * E;
+  if (ring < 2 * maxunit) g.ok = false;
+  if ((D / 2 + num_sms - 1) / num_sms > 32 || B * g.nch_max > 2 * kWork || gmax > kMW + kEW) g.ok = false;
+  g.ring_bytes = ring;
+  g.off_sb = ring;
+  g.off_red = g.off_sb + sb;
+  g.off_pb = g.off_red + red;
+  g.off_ut = g.off_pb + pbz;
+  g.off_misc = g.off_ut + ut;
+  g.smem = g.off_misc + misc + 1024;
+  g.scratch_bytes = (size_t)(D / 32) * 1024 + (size_t)(E / 32) * 1024 + 2 * (size_t)16 * E * 2 +
+                    (size_t)2 * 16 * P * 4 + 2 * 16 * 4 + (size_t)(D / 8) * 4 + 64;
+  return g;
+}
+
+cudaError_t ds_pack_layer(const __nv_bfloat16* w_in, const __nv_bfloat16* w_out, const __nv_bfloat16* w_x,
+                          const __nv_bfloat16* w_dt, int D, int E, int R, int P, uint8_t* dst, cudaStream_t s) {
+  auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  uint8_t* wa = dst;
+  uint8_t* wc = wa + al((size_t)2 * E * D * 2);
+  uint8_t* wx = wc + al((size_t)D * E * 2);
+  uint8_t* wd = wx + al((size_t)E * P * 2);
+  pack_wa_kernel<<<1184, 256, 0, s>>>(w_in, E, D, reinterpret_cast<uint4*>(wa));
+  pack_wc_kernel<<<1184, 256, 0, s>>>(w_out, D, E, reinterpret_cast<uint4*>(wc));
+  pack_wx_kernel<<<296, 256, 0, s>>>(w_x, P, E, reinterpret_cast<uint32_t*>(wx));
+  pack_wdt_kernel<<<296, 256, 0, s>>>(w_dt, E, R, reinterpret_cast<uint2*>(wd));
+  return cudaGetLastError();
+}
+
+cudaError_t ds_fill_layer(DsLayer* host_entry, const uint8_t* packed, int D, int E, int R, int P,
+                          const float* conv_w, const float* conv_b, const float* b_dt, const float* a_log,
+                          const float* d_skip, void* cst, float* h) {
+  auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+  DsLayer& ly = *host_entry;
+  ly.wa = packed;
+  ly.wc = packed + al((size_t)2 * E * D * 2);
+  ly.wxf = reinterpret_cast<const uint32_t*>(ly.wc + al((size_t)D * E * 2));
+  ly.wdt = reinterpret_cast<const uint8_t*>(ly.wxf) + al((size_t)E * P * 2);
+  ly.conv_w = conv_w;
+  ly.conv_b = conv_b;
+  ly.b_dt = b_dt;
+  ly.a_log = a_log;
+  ly.d_skip = d_skip;
+  ly.cst = reinterpret_cast<__nv_bfloat16*>(cst);
+  ly.h = h;
+  return cudaSuccess;
+}
+
+size_t ds_layer_entry_bytes() { return sizeof(DsLayer); }
+
+cudaError_t ds_launch(const DsLayer* layers_dev, int L, int B, int D, int E, int R, int P, int K, float eps,
+                      int bcdt_rmsnorm, float rms_eps, float* r, uint8_t* scratch, const DsGeom& g, int num_sms,
+                      cudaStream_t s) {
+  DsArgs a{};
+  a.layers = layers_dev;
+  a.L = L; a.B = B; a.D = D; a.E = E; a.R = R; a.P = P; a.K = K;
+  a.eps = eps;
+  a.bcdt_rmsnorm = bcdt_rmsnorm;
+  a.rms_eps = rms_eps;
+  a.r = r;
+  uint8_t* p = scratch;
+  a.xr = p; p += (size_t)(D / 32) * 1024;
+  a.gf = p; p += (size_t)(E / 32) * 1024;
+  a.u = reinterpret_cast<__nv_bfloat16*>(p); p += (size_t)16 * E * 2;
+  a.z = reinterpret_cast<__nv_bfloat16*>(p); p += (size_t)16 * E * 2;
+  a.xacc = reinterpret_cast<float*>(p); p += (size_t)2 * 16 * P * 4;
+  a.ssb = reinterpret_cast<float*>(p); p += 2 * 16 * 4;
+  a.cnt = reinterpret_cast<unsigned*>(p); p += (size_t)(D / 8) * 4;
+  a.bar = reinterpret_cast<unsigned*>(p);
+  a.ring_bytes = g.ring_bytes;
+  a.nch_max = g.nch_max;
+  a.off_sb = g.off_sb;
+  a.off_red = g.off_red;
+  a.off_pb = g.off_pb;
+  a.off_ut = g.off_ut;
+  a.off_misc = g.off_misc;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_stack_kernel, a);
+}
+
+cudaError_t preload_decode_stack() {
+  cudaError_t e = cudaFuncSetAttribute(decode_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  return cudaFuncGetAttributes(&fa, decode_stack_kernel);
+}
+
+int ds_max_active(int smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_stack_kernel, kThreads, smem) != cudaSuccess) return 0;
+  return n;
+}
+
+}  // namespace ssm

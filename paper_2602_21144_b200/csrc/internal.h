@@ -167,6 +167,40 @@ cudaError_t launch_m2_norm_apply(const float* g, int Ek, const float* ss, int E,
                                  __nv_bfloat16* o, int64_t M, cudaStream_t s);
 cudaError_t preload_ssd();
 
+
+// ---- persistent whole-stack decode at TP = 1 (decode_stack.cu) ----
+struct DsLayer {            // one layer's device pointers (array in the plan's device buffer)
+  const uint8_t* wa;        // in_proj units: 2E/8 units (x group i = unit 2i, z group i = unit 2i+1) x 16D B
+  const uint8_t* wc;        // out_proj units: 4 quarters x D/8 row groups x 4E B (quarter-major)
+  const uint32_t* wxf;      // x_proj B fragments [E/8][P/8][32] u32
+  const uint8_t* wdt;       // dt_proj B fragments [E/8][R/16][32] x 8 B
+  const float* conv_w;      // [E][K]
+  const float* conv_b;      // [E]
+  const float* b_dt;        // [E]
+  const float* a_log;       // [E][16]
+  const float* d_skip;      // [E]
+  __nv_bfloat16* cst;       // conv window [B][K-1][E]
+  float* h;                 // [B][E][16]
+};
+
+struct DsGeom {
+  bool ok;
+  int nch_max, ring_bytes, off_sb, off_red, off_pb, off_ut, off_misc, smem;
+  size_t scratch_bytes;
+};
+DsGeom ds_geometry(int B, int D, int E, int R, int P, int K, int num_ctas);
+size_t ds_packed_layer_bytes(int D, int E, int R, int P);
+cudaError_t ds_pack_layer(const __nv_bfloat16* w_in, const __nv_bfloat16* w_out, const __nv_bfloat16* w_x,
+                          const __nv_bfloat16* w_dt, int D, int E, int R, int P, uint8_t* dst, cudaStream_t s);
+cudaError_t ds_fill_layer(DsLayer* host_entry, const uint8_t* packed, int D, int E, int R, int P,
+                          const float* conv_w, const float* conv_b, const float* b_dt, const float* a_log,
+                          const float* d_skip, void* cst, float* h);
+cudaError_t ds_launch(const DsLayer* layers_dev, int L, int B, int D, int E, int R, int P, int K, float eps,
+                      int bcdt_rmsnorm, float rms_eps, float* r, uint8_t* scratch, const DsGeom& g, int num_ctas,
+                      cudaStream_t s);
+cudaError_t preload_decode_stack();
+int ds_max_active(int smem);
+
 // Load every kernel eagerly (called once per process from ssm_tp_init when a device exists).
 cudaError_t preload_kernels();
 cudaError_t preload_gemm_simt();

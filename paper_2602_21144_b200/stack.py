@@ -38,6 +38,42 @@ def synthetic_layer(dims, layer, seed=1000, device="cuda"):
     return w
 
 
+class DecodeStack:
+    """Persistent whole-stack decode at TP = 1 (ssm_dstack_*): one cooperative launch per token runs
+    every layer's pre-norm decode block (§4.1).  Owns the device buffer holding the
+    re-packed projection weights and the scratch; keeps the layers' small vectors and the states'
+    caches referenced (they must outlive it)."""
+
+    def __init__(self, mixer: TPMixer, layers: list, states: list, batch: int, norm_eps=1e-5, ctas=0,
+                 stream=None):
+        import ctypes as C
+        self.mx, self.batch = mixer, batch
+        n = len(layers)
+        nb = C.c_size_t()
+        L.call("ssm_dstack_bytes", mixer.handle, n, batch, ctas, C.byref(nb))
+        self.buf = torch.empty(nb.value, dtype=torch.uint8, device=mixer.device)
+        arr = (L.ssm_layer_weights_t * n)(*[lw.struct for lw in layers])
+        sts = (C.c_void_p * n)(*[st.handle.value for st in states])
+        self._keep = (layers, states)
+        self.handle = C.c_void_p()
+        s = stream if stream is not None else torch.cuda.current_stream()
+        L.call("ssm_dstack_create", mixer.handle, n, arr, sts, batch, C.c_float(norm_eps), ctas,
+               C.c_void_p(self.buf.data_ptr()), nb.value, C.c_void_p(s.cuda_stream), C.byref(self.handle))
+
+    def decode(self, res_t, stream=None):
+        """res_t: [batch, D] fp32, updated in place through all layers (one kernel launch)."""
+        import ctypes as C
+        s = stream if stream is not None else torch.cuda.current_stream()
+        L.call("ssm_dstack_decode", self.handle, C.c_void_p(res_t.data_ptr()), C.c_void_p(s.cuda_stream))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                L.LIB.ssm_dstack_destroy(self.handle)
+        except Exception:
+            pass
+
+
 class MixerStack:
     """flags: SSM_AR2_INT8 / SSM_AR2_FP16 / SSM_AR2_FP32 (the library's peer-to-peer AR#2), or
     SSM_AR2_EXTERNAL with nccl_group set: the NCCL bf16 all-reduce BASELINE arm (library writes the
@@ -74,6 +110,15 @@ class MixerStack:
         self.graph_launches = 0
         self._graph_parity = 0
         self.dec_flags = 0   # extra decode flags (SSM_DECODE_UNFUSED: cross-checks)
+        self.dstack = None   # DecodeStack: the persistent whole-stack decode (TP = 1), see persistent()
+
+    def persistent(self, ctas=0):
+        """Switch decode to the persistent whole-stack kernel (TP = 1, pure Mamba stacks); raises
+        SSMError(SSM_ERR_UNSUPPORTED) for shapes it does not cover."""
+        if self.hybrid or self.nccl is not None:
+            raise ValueError("persistent decode: pure Mamba stacks without the NCCL arm only")
+        self.dstack = DecodeStack(self.mx, self.layers, self.states, self.batch, self.eps, ctas)
+        return self
 
     def reset(self, stream=None):
         for s in self.states:
@@ -104,6 +149,9 @@ class MixerStack:
         """res_t: [batch, D] fp32, updated in place through all layers (ssm_mixer_decode_block:
         pre-norm RMSNorm, then the layer's decode kernels); Zamba hybrid layers read the token
         embeddings from self.h0_dec."""
+        if self.dstack is not None:
+            self.dstack.decode(res_t, stream)
+            return
         for li, (lw, st) in enumerate(zip(self.layers, self.states)):
             if li in self.hybrid:
                 w, blk = self.hybrid[li]
