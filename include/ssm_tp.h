@@ -264,6 +264,13 @@ ssm_status_t ssm_dstack_create(ssm_tp_t tp, int32_t n_layers, const ssm_layer_we
                                size_t buf_bytes, void* stream, ssm_dstack_t* out);
 ssm_status_t ssm_dstack_decode(ssm_dstack_t ds, float* residual, void* stream);
 ssm_status_t ssm_dstack_destroy(ssm_dstack_t ds);
+/* Test/profiling only: subsequent ssm_dstack_decode calls write a timeline into `trace` (device,
+ * ctas x n_layers x 32 u64 globaltimer stamps per CTA and layer: 0 layer start, 1 in_proj MMA done,
+ * 2 in_proj epilogue done, 3 after barrier, 4 scan step done, 5 after barrier, 6 out_proj MMA done,
+ * 7 out_proj epilogue done, 8 after barrier; 9 / 10 ns warp 0 waited for ring data in in_proj / out_proj;
+ * 11-13 scan-step sub-phases; 16+i / 24+i in_proj epilogue: unit i started / its partials ready).
+ * NULL switches it off. */
+ssm_status_t ssm_dbg_dstack_trace(ssm_dstack_t ds, void* trace);
 
 /* ---- Zamba's shared transformer block ------------------
  * Zamba runs one shared attention + MLP block before its 13 "hybrid" Mamba layers (the public

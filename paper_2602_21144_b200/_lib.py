@@ -119,6 +119,7 @@ def _load():
         "ssm_dstack_create": (st, [vp, i32, P(ssm_layer_weights_t), P(vp), i32, C.c_float, i32, vp, sz, vp, P(vp)]),
         "ssm_dstack_decode": (st, [vp, vp, vp]),
         "ssm_dstack_destroy": (st, [vp]),
+        "ssm_dbg_dstack_trace": (st, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -136,7 +137,8 @@ EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "s
             "ssm_packed_weight_bytes", "ssm_pack_weight", "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld",
             "ssm_dbg_scan", "ssm_rmsnorm_add", "ssm_kv_bytes", "ssm_kv_alloc", "ssm_kv_reset", "ssm_kv_free",
             "ssm_attn_workspace_bytes", "ssm_attn_block", "ssm_m2_state_bytes", "ssm_m2_workspace_bytes",
-            "ssm_m2_mixer", "ssm_dstack_bytes", "ssm_dstack_create", "ssm_dstack_decode", "ssm_dstack_destroy"]
+            "ssm_m2_mixer", "ssm_dstack_bytes", "ssm_dstack_create", "ssm_dstack_decode", "ssm_dstack_destroy",
+            "ssm_dbg_dstack_trace"]
 PROBE = {"in_proj": 1, "conv": 2, "x_proj": 3, "dt_proj": 4, "scan": 5, "out_proj": 6, "ar2": 7, "decode_step": 8,
          "in_proj_decode": 9}
 

@@ -1364,6 +1364,7 @@ struct ssm_dstack_s {
   std::vector<DsLayer> table;  // host copy of the device layer table (source of the async upload)
   DsLayer* table_dev;
   uint8_t* scratch;
+  unsigned long long* trace = nullptr;  // ssm_dbg_dstack_trace
 };
 
 namespace {
@@ -1465,7 +1466,13 @@ ssm_status_t ssm_dstack_decode(ssm_dstack_t ds, float* residual, void* stream) {
   const ssm_config_t& c = t->cfg;
   t->launches++;
   CU(ds_launch(ds->table_dev, ds->L, ds->batch, c.d_model, c.d_inner, c.dt_rank, t->P, c.d_conv, ds->eps, c.bcdt_rmsnorm,
-               c.rms_eps, residual, ds->scratch, ds->g, ds->ctas, reinterpret_cast<cudaStream_t>(stream)));
+               c.rms_eps, residual, ds->scratch, ds->g, ds->ctas, reinterpret_cast<cudaStream_t>(stream), ds->trace));
+  return SSM_OK;
+}
+
+ssm_status_t ssm_dbg_dstack_trace(ssm_dstack_t ds, void* trace) {
+  if (!ds) return fail(SSM_ERR_ARG, "dstack is NULL");
+  ds->trace = reinterpret_cast<unsigned long long*>(trace);
   return SSM_OK;
 }
 

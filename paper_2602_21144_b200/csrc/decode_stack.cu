@@ -10,14 +10,13 @@
 // runs ahead across phases and layers (weights never depend on activations), and the three
 // data-dependent steps are separated by grid barriers instead of kernel boundaries:
 //
-//   N0 (once): ss[b] = sum_d r[b][d]^2, xr = bf16(r) in MMA A-fragment order          | barrier
 //   per layer l:
-//   A  in_proj units (8 rows x D): xz = rstd[b] * (W_in bf16(r));  x rows -> conv step + SiLU -> u,
+//   A  every CTA reads the fp32 residual into bf16 A fragments and forms the RMSNorm statistic;
+//      in_proj units (8 rows x D): xz = rstd[b] * (W_in bf16(r));  x rows -> conv step + SiLU -> u,
 //      window shift, x_proj partial (mma m16n8k8) -> red.add into xacc;  z rows -> z      | barrier
 //   B  channel groups: dt = softplus(W_dt dt_low + b_dt) (mma m16n8k16), h = exp(dt A) h + dt B u,
 //      y = C h + D u, g = y SiLU(z) -> g in A-fragment order; h written back            | barrier
-//   C  out_proj units (8 rows x E/4): r += W_out g (red.add); the last of a row group's four
-//      contributors re-reads the finished rows -> ss for the next pre-norm, xr = bf16(r) | barrier
+//   C  out_proj units (8 rows x E/4): r += W_out g (red.add)                               | barrier
 //
 // Pre-norm (reading Q16: RMSNorm, weight 1, eps): the norm is applied after the in_proj contraction,
 // xz[b] = rstd[b] * (W_in bf16(r[b])) -- the same product as W_in bf16(rstd[b] r[b]) up to where the
@@ -32,6 +31,7 @@
 // pipe of mma.sync is far from the bound, what matters is keeping every SM's stream fed.
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -48,6 +48,7 @@ constexpr int kSlots = 8;                   // ring units in flight (mbarrier sl
 constexpr int kMaxCA = 8;                   // phase A: 32-wide k chunks per MMA warp (D <= 2816)
 constexpr int kMaxCC = 4;                   // phase C: chunks per MMA warp per quarter (E <= 5632)
 constexpr int kMaxPT = 8;                   // x_proj 8-wide p tiles per epilogue warp (P <= 256)
+constexpr int kMaxXU = 5;                   // in_proj x units (8 channels) per CTA
 
 SSM_DEV void mma_1688_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
   asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
@@ -75,18 +76,7 @@ SSM_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
                : "memory");
 }
 
-__host__ __device__ inline int part(int n, int c, int nc) { return (int)(((long long)n * c) / nc); }
-
-// Byte offset of element (b, k) (b < 16) in an A-fragment buffer of an m16 x K bf16 operand:
-// 32-wide k chunk j = k / 32 occupies 1 KB; lane L holds 32 B = the m16n8k16 registers a0..a3 of
-// the chunk's first 16 k, then of its second 16 k (a0: row L/4, k 2(L%4)+{0,1}; a1: row +8; a2: k +8;
-// a3: both).  One lane loads its chunk with two 16-B loads.
-__host__ __device__ inline int afrag_off(int b, int k) {
-  const int j = k >> 5, kk32 = k & 31, half = kk32 >> 4, kk = kk32 & 15;
-  const int reg = (b >> 3) + 2 * (kk >> 3);
-  const int lane = (b & 7) * 4 + ((kk & 7) >> 1);
-  return j * 1024 + lane * 32 + half * 16 + reg * 4 + (kk & 1) * 2;
-}
+__host__ __device__ inline int part(int n, int c, int nc) { return (n * c) / nc; }  // (n * c < 2^31 here)
 
 }  // namespace
 
@@ -97,15 +87,14 @@ struct DsArgs {
   int bcdt_rmsnorm;
   float rms_eps;
   float* r;                 // residual [B][D] fp32, updated in place through all layers
-  uint8_t* xr;              // A fragments of bf16(r): D/32 KB (rows >= B stay zero)
-  uint8_t* gf;              // A fragments of g: E/32 KB
+  __nv_bfloat16* g;         // gated output [16][E] (rows >= B stay zero)
   __nv_bfloat16* u;         // [B][E]
   __nv_bfloat16* z;         // [B][E]
   float* xacc;              // [2][16][P]  (zero between uses)
-  float* ssb;               // [2][16]
-  unsigned* cnt;            // [D/8] out_proj contributor counters (zero between uses)
   unsigned* bar;            // [2] grid-barrier counter, exit counter
   int ring_bytes, nch_max;  // ring size; max phase-B channels per CTA
+  unsigned long long* trace; // debug (ssm_dbg_dstack_trace): [grid][L][32] globaltimer stamps, or NULL
+  int max_inflight;          // ring units issued but not yet landed, at most
   int off_sb, off_red, off_pb, off_ut, off_misc;
 };
 
@@ -125,8 +114,8 @@ struct Smem {
   SSM_DEV float* sbdt() const { return salog() + a->nch_max * 16; }
   SSM_DEV float* sdsk() const { return sbdt() + a->nch_max; }
   SSM_DEV float* sred() const { return reinterpret_cast<float*>(base + a->off_red); }              // [2][kMW][128]
-  SSM_DEV float* sdbc() const { return reinterpret_cast<float*>(base + a->off_pb); }               // [16][P]
-  SSM_DEV float* sdt() const { return sdbc() + 16 * a->P; }                                         // [16][nch_max]
+  SSM_DEV float* sdbc() const { return reinterpret_cast<float*>(base + a->off_pb); }  // [16][P + 8] (bank shift per row)
+  SSM_DEV float* sdt() const { return sdbc() + 16 * (a->P + 8); }                                   // [16][nch_max]
   SSM_DEV float* sA() const { return sdt() + 16 * a->nch_max; }                                      // [nch_max][16]
   SSM_DEV __nv_bfloat16* utile() const { return reinterpret_cast<__nv_bfloat16*>(base + a->off_ut); }  // [2][16][8]
   SSM_DEV uint64_t* full() const { return reinterpret_cast<uint64_t*>(base + a->off_misc); }     // [kSlots]
@@ -134,22 +123,28 @@ struct Smem {
   SSM_DEV uint64_t* ready() const { return full() + 2 * kSlots; }                                   // [2]
   SSM_DEV uint64_t* freeb() const { return full() + 2 * kSlots + 2; }                               // [2]
   SSM_DEV uint64_t* mbB() const { return full() + 2 * kSlots + 4; }                                 // phase-B prefetch
-  SSM_DEV float* srstd() const { return reinterpret_cast<float*>(full() + 2 * kSlots + 5); }       // [16]
-  SSM_DEV float* sss() const { return srstd() + 16; }                                               // [16]
-  SSM_DEV int* slist() const { return reinterpret_cast<int*>(sss() + 16); }                        // [33]
-  SSM_DEV struct Pump* pump() const { return reinterpret_cast<struct Pump*>(base + a->off_misc + 512); }
+  SSM_DEV uint64_t* mbX() const { return full() + 2 * kSlots + 5; }                                 // phase-A prefetch
+  SSM_DEV uint64_t* mbSS() const { return full() + 2 * kSlots + 6; }                                // pre-norm partials
+  SSM_DEV float* ssp() const { return reinterpret_cast<float*>(full() + 2 * kSlots + 7); }         // [kMW][16]
+  SSM_DEV struct Pump* pump() const { return reinterpret_cast<struct Pump*>(base + a->off_misc + 1024); }
+  // phase-A epilogue operands of this CTA's x units (aliasing the phase-B scratch, free during C and A):
+  // W_x B fragments [kMaxXU][P/8][32] u32, conv taps [kMaxXU * 8][K], conv bias [kMaxXU * 8], windows
+  // [kMaxXU][16 b][3 j][8 n] bf16
+  SSM_DEV uint32_t* sxw() const { return reinterpret_cast<uint32_t*>(base + a->off_pb); }
+  SSM_DEV float* sxcw() const { return reinterpret_cast<float*>(base + a->off_pb + kMaxXU * a->P * 16); }
+  SSM_DEV float* sxcb() const { return sxcw() + kMaxXU * 8 * 4; }
+  SSM_DEV uint16_t* sxwin() const { return reinterpret_cast<uint16_t*>(sxcb() + kMaxXU * 8); }
 };
 
-// Grid barrier over the work threads of every CTA (the producer warp never joins): bar.sync, one
-// thread per CTA releases its arrival and spins on the counter with acquire loads.
+// Grid barrier over the work threads of every CTA (the producer warp never joins): bar.sync, then one
+// thread per CTA releases its arrival and spins on the counter with acquire loads (bar.sync orders
+// the CTA's other threads' writes before that release).
 SSM_DEV void grid_sync(unsigned* bar, unsigned target) {
   named_bar_sync(1, kWork);
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     while (ld_acquire_gpu_u32(bar) < target) {
     }
-    __threadfence();
   }
   named_bar_sync(1, kWork);
 }
@@ -170,44 +165,53 @@ SSM_DEV void issue_phase_b_prefetch(const DsArgs& a, const Smem& s, const DsLaye
   bulk_g2s(s.sdsk(), ly.d_skip + d0, nch * 4, s.mbB());
 }
 
-// Finalise out_proj row group g8 (all four contributions landed): epilogue thread e = (b, n) reads
-// r[b][8 g8 + n], adds v^2 to the CTA's per-token sum, and writes bf16(v) into the A fragments.
-SSM_DEV void finalize_group(const DsArgs& a, const Smem& s, int g8, int e) {
-  const int b = e >> 3, n = e & 7;
-  const int k = 8 * g8 + n;
-  float v = 0.f;
-  if (b < a.B) v = __ldcg(a.r + (size_t)b * a.D + k);
-  float q = v * v;
-  q += __shfl_xor_sync(0xffffffffu, q, 1);
-  q += __shfl_xor_sync(0xffffffffu, q, 2);
-  q += __shfl_xor_sync(0xffffffffu, q, 4);
-  if (b < a.B) {
-    if (n == 0) atomicAdd(&s.sss()[b], q);
-    *reinterpret_cast<__nv_bfloat16*>(a.xr + afrag_off(b, k)) = __float2bfloat16_rn(v);
+// Phase-A prefetch of layer l (W_x fragments, conv taps and bias of this CTA's x groups [gx0, gx1)):
+// one thread issues bulk copies that complete on mbX.
+SSM_DEV void issue_phase_a_prefetch(const DsArgs& a, const Smem& s, const DsLayer& ly, int gx0, int gx1) {
+  const int ng = gx1 - gx0;
+  const uint32_t wb = (uint32_t)ng * (a.P / 8) * 128, cwb = (uint32_t)ng * 8 * a.K * 4, cbb = (uint32_t)ng * 32;
+  mbar_arrive_expect_tx(s.mbX(), wb + cwb + cbb);
+  if (ng == 0) return;
+  bulk_g2s(s.sxw(), ly.wxf + (size_t)gx0 * (a.P / 8) * 32, wb, s.mbX());
+  bulk_g2s(s.sxcw(), ly.conv_w + (size_t)gx0 * 8 * a.K, cwb, s.mbX());
+  bulk_g2s(s.sxcb(), ly.conv_b + (size_t)gx0 * 8, cbb, s.mbX());
+}
+
+// The cached conv windows of this CTA's x groups (16-B rows of 8 channels per (group, b, tap)) ->
+// sxwin by cp.async from the epilogue threads (waited for at the start of the layer's phase A).
+SSM_DEV void issue_window_prefetch(const DsArgs& a, const Smem& s, const DsLayer& ly, int gx0, int gx1, int e) {
+  const int B = a.B, K = a.K;
+  const uint16_t* cst = reinterpret_cast<const uint16_t*>(ly.cst);
+  for (int q = e; q < (gx1 - gx0) * B * (K - 1); q += kEW * 32) {
+    const int xi = q / (B * (K - 1)), r = q % (B * (K - 1)), bb = r / (K - 1), j = r % (K - 1);
+    cp_async16(s.sxwin() + ((xi * 16 + bb) * 3 + j) * 8, cst + ((size_t)bb * (K - 1) + j) * a.E + 8 * (gx0 + xi), true);
   }
+  cp_async_commit();
 }
 
 // Ring producer state (lane 0 of the producer warp).
 struct Pump {
   long long issued, released;
-  int seq, oldest, nA, nC, ua0, uc0, szA, szC, total;
+  int seq, oldest, landed, nA, nC, ua0, uc0, szA, szC, total;
 };
 
 SSM_DEV int pump_size(const Pump& p, int q) { return q % (p.nA + p.nC) < p.nA ? p.szA : p.szC; }
 
-// Issue units while the ring has room; units <= `done` (already consumed by warp 0) may be waited for.
-__device__ __forceinline__ void pump_run(const DsArgs& a, const Smem& s, Pump* pp, int done) {
+// Issue units while the ring has room (waiting for the oldest unit's release when it has none).
+__device__ __forceinline__ void pump_run(const DsArgs& a, const Smem& s, Pump* pp) {
   Pump p = *pp;
   while (p.seq < p.total) {
     const int sz = pump_size(p, p.seq);
-    bool stop = false;
     while (p.seq - p.oldest >= kSlots || p.issued + sz - p.released > a.ring_bytes) {
-      if (p.oldest > done) { stop = true; break; }
       mbar_wait(&s.empty()[p.oldest % kSlots], (p.oldest / kSlots) & 1);
       p.released += pump_size(p, p.oldest);
       ++p.oldest;
     }
-    if (stop) break;
+    // bounded bytes in flight: deep TMA queues delay every other memory access of the step
+    while (p.seq - p.landed >= a.max_inflight) {
+      mbar_wait(&s.full()[p.landed % kSlots], (p.landed / kSlots) & 1);
+      ++p.landed;
+    }
     const int l = p.seq / (p.nA + p.nC), pos = p.seq % (p.nA + p.nC);
     const DsLayer& ly = a.layers[l];
     const uint8_t* src = pos < p.nA ? ly.wa + (size_t)(p.ua0 + pos) * sz : ly.wc + (size_t)(p.uc0 + pos - p.nA) * sz;
@@ -234,61 +238,119 @@ __device__ __forceinline__ void pump_run(const DsArgs& a, const Smem& s, Pump* p
   *pp = p;
 }
 
+// Debug timeline: slot k of (CTA, layer) <- globaltimer (one thread per stamp; NULL trace = off).
+SSM_DEV void stamp(const DsArgs& a, int l, int k) {
+  if (a.trace) a.trace[((size_t)blockIdx.x * a.L + l) * 32 + k] = globaltimer();
+}
+
 // Unit-sequence counters shared by the MMA and epilogue warps: ring unit index (mbarrier slot /
 // parity), reduction-buffer unit index, ring byte offset of the next unit.
 struct Ctr {
   int seq, useq, roff;
 };
 
-// MMA warps over units [u0, u1) of a phase: activation A fragments register-resident (chunk j of the
-// unit's k range at frag + ((u / qdiv) * nch + j) KB, reloaded when u / qdiv changes; qdiv = 0: one
-// k range), weight B fragments from the ring, partial [16 x 8] -> the unit's reduction buffer.
+// The MMA warps' unit loop: weight B fragments from the ring (one LDS.128 per lane per 32-wide chunk),
+// activation A fragments in registers, partial [16 x 8] -> the unit's reduction buffer.
 template <int MAXC>
-__device__ __noinline__ Ctr mma_units(const DsArgs& a, uint8_t* base, const uint8_t* frag, int nch, int qdiv,
-                                      int u0, int u1, int sz, Ctr ct) {
-  const Smem s{base, &a};
+SSM_DEV Ctr unit_loop(const DsArgs& a, const Smem& s, const uint32_t (&xa)[MAXC][8], int nch, int u0, int u1, int sz,
+                      Ctr ct) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t ring = smem_u32(s.ring());
-  // segments of units sharing one k range (qdiv = 0: all of them): the A fragments are loaded once
-  // per segment, so they stay in registers across the segment's units
-  for (int us = u0; us < u1;) {
-    const int q = qdiv ? us / qdiv : 0;
-    const int ue = qdiv ? min(u1, (q + 1) * qdiv) : u1;
-    uint32_t xa[MAXC][8];
+  for (int u = u0; u < u1; ++u, ++ct.seq, ++ct.useq) {
+    const int slot = ct.seq % kSlots;
+    mbar_wait(&s.full()[slot], (ct.seq / kSlots) & 1);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) {
-      const int j = min(warp + kMW * i, nch - 1);
-      const uint8_t* fp = frag + (size_t)(q * nch + j) * 1024 + lane * 32;
-      const uint4 v0 = __ldcg(reinterpret_cast<const uint4*>(fp));
-      const uint4 v1 = __ldcg(reinterpret_cast<const uint4*>(fp + 16));
-      xa[i][0] = v0.x; xa[i][1] = v0.y; xa[i][2] = v0.z; xa[i][3] = v0.w;
-      xa[i][4] = v1.x; xa[i][5] = v1.y; xa[i][6] = v1.z; xa[i][7] = v1.w;
-    }
-    for (int u = us; u < ue; ++u, ++ct.seq, ++ct.useq) {
-      const int slot = ct.seq % kSlots;
-      mbar_wait(&s.full()[slot], (ct.seq / kSlots) & 1);
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int i = 0; i < MAXC; ++i) {
-        const int j = warp + kMW * i;
-        if (j < nch) {
-          int o = ct.roff + j * 512 + lane * 16;
-          if (o >= a.ring_bytes) o -= a.ring_bytes;
-          const uint4 w4 = lds128(ring + o);
-          const uint32_t a0[4] = {xa[i][0], xa[i][1], xa[i][2], xa[i][3]};
-          const uint32_t a1[4] = {xa[i][4], xa[i][5], xa[i][6], xa[i][7]};
-          mma_16816_bf16(acc, a0, w4.x, w4.y);
-          mma_16816_bf16(acc, a1, w4.z, w4.w);
-        }
+      const int j = warp + kMW * i;
+      if (j < nch) {
+        int o = ct.roff + j * 512 + lane * 16;
+        if (o >= a.ring_bytes) o -= a.ring_bytes;
+        const uint4 w4 = lds128(ring + o);
+        const uint32_t a0[4] = {xa[i][0], xa[i][1], xa[i][2], xa[i][3]};
+        const uint32_t a1[4] = {xa[i][4], xa[i][5], xa[i][6], xa[i][7]};
+        mma_16816_bf16(acc, a0, w4.x, w4.y);
+        mma_16816_bf16(acc, a1, w4.z, w4.w);
       }
-      mbar_arrive(&s.empty()[slot]);
-      mbar_wait(&s.freeb()[ct.useq & 1], ((ct.useq >> 1) & 1) ^ 1);
-      float* sp = s.sred() + (ct.useq & 1) * (kMW * 128) + warp * 128;
-      sp[lane] = acc[0]; sp[32 + lane] = acc[1]; sp[64 + lane] = acc[2]; sp[96 + lane] = acc[3];
-      mbar_arrive(&s.ready()[ct.useq & 1]);
-      ct.roff += sz;
-      if (ct.roff >= a.ring_bytes) ct.roff -= a.ring_bytes;
     }
+    mbar_arrive(&s.empty()[slot]);
+    mbar_wait(&s.freeb()[ct.useq & 1], ((ct.useq >> 1) & 1) ^ 1);
+    float* sp = s.sred() + (ct.useq & 1) * (kMW * 128) + warp * 128;
+    sp[lane] = acc[0]; sp[32 + lane] = acc[1]; sp[64 + lane] = acc[2]; sp[96 + lane] = acc[3];
+    mbar_arrive(&s.ready()[ct.useq & 1]);
+    ct.roff += sz;
+    if (ct.roff >= a.ring_bytes) ct.roff -= a.ring_bytes;
+  }
+  return ct;
+}
+
+// Phase A, MMA warps: A fragments = bf16(r) straight from the fp32 residual (this warp's 32-wide k
+// chunks j = warp + kMW i of all 16 rows; rows >= B zero) plus the warp's share of the pre-norm sum
+// of squares per token -> ssp[warp][b] (the CTA's warps together cover all of D, so every CTA forms
+// the full RMSNorm statistic itself).
+__device__ __forceinline__ Ctr mma_units_a(const DsArgs& a, uint8_t* base, int l, int u0, int u1, Ctr ct) {
+  const Smem s{base, &a};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b0 = lane >> 2, b1 = b0 + 8, q2 = 2 * (lane & 3);
+  const int D = a.D, nch = D / 32;
+  const bool v0 = b0 < a.B, v1 = b1 < a.B;
+  const float* r0 = a.r + (size_t)b0 * D;
+  const float* r1 = a.r + (size_t)b1 * D;
+  uint32_t xa[kMaxCA][8];
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxCA; ++i) {
+    const int j = min(warp + kMW * i, nch - 1);
+    const bool in = warp + kMW * i < nch;
+    const int k = 32 * j + 4 * q2;   // this lane's 8 consecutive k of the chunk (permuted fragments)
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 p0 = (in && v0) ? __ldcg(reinterpret_cast<const float4*>(r0 + k)) : z4;
+    const float4 p1 = (in && v0) ? __ldcg(reinterpret_cast<const float4*>(r0 + k + 4)) : z4;
+    const float4 p2 = (in && v1) ? __ldcg(reinterpret_cast<const float4*>(r1 + k)) : z4;
+    const float4 p3 = (in && v1) ? __ldcg(reinterpret_cast<const float4*>(r1 + k + 4)) : z4;
+    s0 = fmaf(p0.x, p0.x, fmaf(p0.y, p0.y, fmaf(p0.z, p0.z, fmaf(p0.w, p0.w, s0))));
+    s0 = fmaf(p1.x, p1.x, fmaf(p1.y, p1.y, fmaf(p1.z, p1.z, fmaf(p1.w, p1.w, s0))));
+    s1 = fmaf(p2.x, p2.x, fmaf(p2.y, p2.y, fmaf(p2.z, p2.z, fmaf(p2.w, p2.w, s1))));
+    s1 = fmaf(p3.x, p3.x, fmaf(p3.y, p3.y, fmaf(p3.z, p3.z, fmaf(p3.w, p3.w, s1))));
+    // k16 step 0: a0 (row b0, elements 0-1), a1 (row b1, 0-1), a2 (row b0, 2-3), a3 (row b1, 2-3);
+    // k16 step 1: the same with elements 4-7
+    xa[i][0] = pack_bf2(p0.x, p0.y); xa[i][1] = pack_bf2(p2.x, p2.y);
+    xa[i][2] = pack_bf2(p0.z, p0.w); xa[i][3] = pack_bf2(p2.z, p2.w);
+    xa[i][4] = pack_bf2(p1.x, p1.y); xa[i][5] = pack_bf2(p3.x, p3.y);
+    xa[i][6] = pack_bf2(p1.z, p1.w); xa[i][7] = pack_bf2(p3.z, p3.w);
+  }
+  s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+  s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+  s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+  s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+  if ((lane & 3) == 0) {
+    s.ssp()[warp * 16 + b0] = s0;
+    s.ssp()[warp * 16 + b1] = s1;
+  }
+  mbar_arrive(s.mbSS());
+  return unit_loop<kMaxCA>(a, s, xa, nch, u0, u1, 16 * D, ct);
+}
+
+// Phase C, MMA warps: A fragments of g for the quarter of E each unit covers (u / (D/8)), loaded per
+// run of units sharing a quarter.
+__device__ __forceinline__ Ctr mma_units_c(const DsArgs& a, uint8_t* base, int l, int u0, int u1, Ctr ct) {
+  const Smem s{base, &a};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = a.E / 128, qdiv = a.D / 8;
+  for (int us = u0; us < u1;) {
+    const int q = us / qdiv;
+    const int ue = min(u1, (q + 1) * qdiv);
+    uint32_t xa[kMaxCC][8];
+#pragma unroll
+    for (int i = 0; i < kMaxCC; ++i) {
+      const int j = min(warp + kMW * i, nch - 1);
+      const int k = q * (a.E / 4) + 32 * j + 8 * (lane & 3);   // 8 consecutive channels (permuted fragments)
+      const uint4 v0 = __ldcg(reinterpret_cast<const uint4*>(a.g + (size_t)(lane >> 2) * a.E + k));
+      const uint4 v1 = __ldcg(reinterpret_cast<const uint4*>(a.g + (size_t)((lane >> 2) + 8) * a.E + k));
+      xa[i][0] = v0.x; xa[i][1] = v1.x; xa[i][2] = v0.y; xa[i][3] = v1.y;
+      xa[i][4] = v0.z; xa[i][5] = v1.z; xa[i][6] = v0.w; xa[i][7] = v1.w;
+    }
+    ct = unit_loop<kMaxCC>(a, s, xa, nch, us, ue, 4 * a.E, ct);
     us = ue;
   }
   return ct;
@@ -305,15 +367,25 @@ SSM_DEV float reduce_unit(const Smem& s, int useq, int b, int n) {
 }
 
 // Phase A epilogue warps: z rows -> z; x rows -> conv step + SiLU -> u, window shift, x_proj partial.
-__device__ __noinline__ Ctr epi_units_a(const DsArgs& a, uint8_t* base, int l, int u0, int u1, Ctr ct) {
+__device__ __forceinline__ Ctr epi_units_a(const DsArgs& a, uint8_t* base, int l, int u0, int u1, Ctr ct) {
   const Smem s{base, &a};
-  const DsLayer& ly = a.layers[l];
   const int e = threadIdx.x - kMW * 32, ew = e >> 5, lane = threadIdx.x & 31;
   const int b = e >> 3, n = e & 7;
   const int B = a.B, E = a.E, P = a.P, K = a.K;
-  if (e < 16) s.srstd()[e] = rsqrtf(__ldcg(a.ssb + (l & 1) * 16 + e) / (float)a.D + a.eps);
+  const int gx0 = (u0 + 1) >> 1;
+  // the layer's pointers in registers (stores below may alias the layer table as far as the compiler knows)
+  __nv_bfloat16* const cst = a.layers[l].cst;
+  __nv_bfloat16* const uo = a.u;
+  __nv_bfloat16* const zo = a.z;
+  // RMSNorm statistic of the pre-norm (reading Q16, weight 1): 1 / sqrt(mean_d r[b][d]^2 + eps)
+  mbar_wait(s.mbSS(), l & 1);
+  float ss = 0.f;
+#pragma unroll
+  for (int w = 0; w < kMW; ++w) ss += s.ssp()[w * 16 + b];
+  const float rs = rsqrtf(ss / (float)a.D + a.eps);
+  mbar_wait(s.mbX(), l & 1);
+  cp_async_wait<0>();
   named_bar_sync(2, kEW * 32);
-  const float rs = s.srstd()[b];
   float xp[kMaxPT][4];
 #pragma unroll
   for (int k = 0; k < kMaxPT; ++k) xp[k][0] = xp[k][1] = xp[k][2] = xp[k][3] = 0.f;
@@ -321,64 +393,41 @@ __device__ __noinline__ Ctr epi_units_a(const DsArgs& a, uint8_t* base, int l, i
   int ux = 0;
   for (int u = u0; u < u1; ++u, ++ct.seq, ++ct.useq) {
     const bool is_x = (u & 1) == 0;
-    const int i = u >> 1, f = 8 * i + n;
-    // loads independent of the contraction, in flight while the unit streams
-    float cw[4] = {0.f, 0.f, 0.f, 0.f}, cb = 0.f;
-    uint32_t win[3] = {0u, 0u, 0u};
-    uint32_t wx[kMaxPT];
-    if (is_x) {
-      if (b < B) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < K) cw[j] = ly.conv_w[(size_t)f * K + j];
-        cb = ly.conv_b[f];
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (j < K - 1) win[j] = reinterpret_cast<const uint16_t*>(ly.cst)[((size_t)b * (K - 1) + j) * E + f];
-      }
-#pragma unroll
-      for (int k = 0; k < kMaxPT; ++k) {
-        const int t = ew + kEW * k;
-        wx[k] = t < npt ? ly.wxf[((size_t)i * npt + t) * 32 + lane] : 0u;
-      }
-    }
+    const int i = u >> 1, f = 8 * i + n, xi = i - gx0;
+    if (e == 0 && u - u0 < 8) stamp(a, l, 16 + (u - u0));
     mbar_wait(&s.ready()[ct.useq & 1], (ct.useq >> 1) & 1);
+    if (e == 0 && u - u0 < 8) stamp(a, l, 24 + (u - u0));
     float v = reduce_unit(s, ct.useq, b, n);
     mbar_arrive(&s.freeb()[ct.useq & 1]);
     v *= rs;
     if (!is_x) {
-      if (b < B) a.z[(size_t)b * E + f] = __float2bfloat16_rn(v);
+      if (b < B) zo[(size_t)b * E + f] = __float2bfloat16_rn(v);
       continue;
     }
     // causal conv step (tap K-1 = this token) + SiLU; the window shifts by one
+    const float* cw = s.sxcw() + (xi * 8 + n) * K;
+    const uint16_t* wn = s.sxwin() + (xi * 16 + b) * 24 + n;
     const float x = __bfloat162float(__float2bfloat16_rn(v));
-    float acc = cb;
-    float wl = cw[1];
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      if (j < K - 1) acc = fmaf(cw[j], __uint_as_float(win[j] << 16), acc);
-#pragma unroll
-    for (int j = 2; j < 4; ++j)
-      if (j == K - 1) wl = cw[j];
-    acc = fmaf(wl, x, acc);
+    float acc = s.sxcb()[xi * 8 + n];
+    for (int j = 0; j < K - 1; ++j) acc = fmaf(cw[j], __uint_as_float((uint32_t)wn[j * 8] << 16), acc);
+    acc = fmaf(cw[K - 1], x, acc);
     const __nv_bfloat16 ub = __float2bfloat16_rn(silu<true>(acc));
     __nv_bfloat16* ut = s.utile() + (ux & 1) * 128;
     ut[b * 8 + n] = b < B ? ub : __float2bfloat16_rn(0.f);
     if (b < B) {
-      a.u[(size_t)b * E + f] = ub;
-      uint16_t* cs = reinterpret_cast<uint16_t*>(ly.cst);
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-        if (j < K - 2) cs[((size_t)b * (K - 1) + j) * E + f] = (uint16_t)win[j + 1];
-      ly.cst[((size_t)b * (K - 1) + (K - 2)) * E + f] = __float2bfloat16_rn(x);
+      uo[(size_t)b * E + f] = ub;
+      uint16_t* cs = reinterpret_cast<uint16_t*>(cst);
+      for (int j = 0; j < K - 2; ++j) cs[((size_t)b * (K - 1) + j) * E + f] = wn[(j + 1) * 8];
+      cst[((size_t)b * (K - 1) + (K - 2)) * E + f] = __float2bfloat16_rn(x);
     }
     named_bar_sync(2, kEW * 32);
     // x_proj partial of these 8 channels: xp[b][p] += sum_n u[b][n] W_x[p][8i + n]  (m16n8k8)
     const uint32_t a0 = *reinterpret_cast<const uint32_t*>(ut + (lane >> 2) * 8 + 2 * (lane & 3));
     const uint32_t a1 = *reinterpret_cast<const uint32_t*>(ut + ((lane >> 2) + 8) * 8 + 2 * (lane & 3));
+    const uint32_t* wx = s.sxw() + xi * npt * 32 + lane;
 #pragma unroll
     for (int k = 0; k < kMaxPT; ++k)
-      if (ew + kEW * k < npt) mma_1688_bf16(xp[k], a0, a1, wx[k]);
+      if (ew + kEW * k < npt) mma_1688_bf16(xp[k], a0, a1, wx[(ew + kEW * k) * 32]);
     ++ux;
   }
   // this CTA's x_proj partials -> xacc (fp32 reductions)
@@ -395,62 +444,39 @@ __device__ __noinline__ Ctr epi_units_a(const DsArgs& a, uint8_t* base, int l, i
   return ct;
 }
 
-// Phase C epilogue warps: r += the unit's partial (fp32 reductions); the fourth contributor of a row
-// group finalises it (ss for the next pre-norm, xr = bf16(r)) unless this is the last layer.
-__device__ __noinline__ Ctr epi_units_c(const DsArgs& a, uint8_t* base, int l, int u0, int u1, Ctr ct) {
+// Phase C epilogue warps: r += the unit's partial (fp32 reductions; the four K quarters of a row group
+// come from different CTAs and are complete at the grid barrier that ends the phase).
+__device__ __forceinline__ Ctr epi_units_c(const DsArgs& a, uint8_t* base, int u0, int u1, Ctr ct) {
   const Smem s{base, &a};
-  const int e = threadIdx.x - kMW * 32, ew = e >> 5, lane = threadIdx.x & 31;
+  const int e = threadIdx.x - kMW * 32;
   const int b = e >> 3, n = e & 7;
   const int D = a.D;
-  unsigned res = 0u;
-  int ui = 0;
-  for (int u = u0; u < u1; ++u, ++ct.seq, ++ct.useq, ++ui) {
+  float* const r = a.r;
+  for (int u = u0; u < u1; ++u, ++ct.seq, ++ct.useq) {
     const int g8 = u % (D / 8);
     mbar_wait(&s.ready()[ct.useq & 1], (ct.useq >> 1) & 1);
     const float v = reduce_unit(s, ct.useq, b, n);
     mbar_arrive(&s.freeb()[ct.useq & 1]);
-    if (b < a.B) red_add_f32(a.r + (size_t)b * D + 8 * g8 + n, v);
-    __threadfence();
-    named_bar_sync(2, kEW * 32);
-    // contributor count of the row group; the result is only inspected after the last unit
-    if (e == ui) res = atomicAdd(&a.cnt[g8], 1u);
-  }
-  const int nu = u1 - u0;
-  const bool last = e < nu && res == 3u;
-  if (last) a.cnt[(u0 + e) % (D / 8)] = 0u;
-  if (l + 1 < a.L) {
-    if (ew == 0) {
-      const unsigned m = __ballot_sync(0xffffffffu, last);
-      if (lane == 0) s.slist()[0] = __popc(m);
-      if (last) s.slist()[1 + __popc(m & ((1u << lane) - 1u))] = (u0 + lane) % (D / 8);
-    }
-    __threadfence();
-    named_bar_sync(2, kEW * 32);
-    const int nl = s.slist()[0];
-    for (int q = 0; q < nl; ++q) finalize_group(a, s, s.slist()[1 + q], e);
-    named_bar_sync(2, kEW * 32);
-    if (e < a.B) {
-      atomicAdd(&a.ssb[((l & 1) ^ 1) * 16 + e], s.sss()[e]);
-      s.sss()[e] = 0.f;
-    }
+    if (b < a.B) red_add_f32(r + (size_t)b * D + 8 * g8 + n, v);
   }
   return ct;
 }
 
 // Phase B (all work threads): dt_proj + softplus + scan step + D skip + gate for this CTA's channels.
-__device__ __noinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, int gb0, int gb1) {
+__device__ __forceinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, int gb0, int gb1) {
   const Smem s{base, &a};
-  const DsLayer& ly = a.layers[l];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int B = a.B, E = a.E, P = a.P, R = a.R;
   const int nch = 8 * (gb1 - gb0), d0 = 8 * gb0, ng = gb1 - gb0;
+  const int PS = P + 8;  // smem row stride of the dbc rows: 8 banks shift per token (dt_proj A fragments)
+  float* const hglob = a.layers[l].h;
+  __nv_bfloat16* const gout = a.g;
   const float* xacc = a.xacc + (l & 1) * 16 * P;
-  if (blockIdx.x == 0 && tid < 16) a.ssb[((l & 1) ^ 1) * 16 + tid] = 0.f;
   for (int i = tid; i < 16 * (P / 4); i += kWork) {
     const int bb = i / (P / 4), q = i % (P / 4);
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (bb < B) v = __ldcg(reinterpret_cast<const float4*>(xacc + bb * P) + q);
-    reinterpret_cast<float4*>(s.sdbc() + bb * P)[q] = v;
+    reinterpret_cast<float4*>(s.sdbc() + bb * PS)[q] = v;
   }
   // this thread's items (b, ch): u and z loads in flight
   const int nit = B * nch;
@@ -465,14 +491,17 @@ __device__ __noinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, int 
     uu1 = __bfloat162float(__ldcg(a.u + (size_t)bb * E + d0 + ch));
     zz1 = __bfloat162float(__ldcg(a.z + (size_t)bb * E + d0 + ch));
   }
+  if (tid == 0) stamp(a, l, 11);
   mbar_wait(s.mbB(), l & 1);
-  for (int i = tid; i < nch * 16; i += kWork) s.sA()[i] = -expf(s.salog()[i]) * 1.4426950408889634f;
+  if (tid == 0) stamp(a, l, 12);
+  for (int i = tid; i < nch * 16; i += kWork)
+    s.sA()[i] = -ex2_approx(s.salog()[i] * 1.4426950408889634f) * 1.4426950408889634f;  // A log2(e)
   named_bar_sync(1, kWork);
   if (a.bcdt_rmsnorm) {  // weightless RMSNorm of dt_low, B, C per token (Falcon-Mamba, reading Q18)
     for (int bb = warp; bb < B; bb += kMW + kEW) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f;
       for (int p = lane; p < P; p += 32) {
-        const float v = s.sdbc()[bb * P + p];
+        const float v = s.sdbc()[bb * PS + p];
         if (p < R) s0 = fmaf(v, v, s0);
         else if (p < R + 16) s1 = fmaf(v, v, s1);
         else s2 = fmaf(v, v, s2);
@@ -483,10 +512,10 @@ __device__ __noinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, int 
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       }
-      const float r0 = 1.0f / sqrtf(s0 / (float)R + a.rms_eps), r1 = 1.0f / sqrtf(s1 / 16.f + a.rms_eps),
-                  r2 = 1.0f / sqrtf(s2 / 16.f + a.rms_eps);
+      const float r0 = rsqrtf(s0 / (float)R + a.rms_eps), r1 = rsqrtf(s1 * (1.f / 16.f) + a.rms_eps),
+                  r2 = rsqrtf(s2 * (1.f / 16.f) + a.rms_eps);
       __syncwarp();
-      for (int p = lane; p < P; p += 32) s.sdbc()[bb * P + p] *= (p < R ? r0 : p < R + 16 ? r1 : r2);
+      for (int p = lane; p < P; p += 32) s.sdbc()[bb * PS + p] *= (p < R ? r0 : p < R + 16 ? r1 : r2);
     }
     named_bar_sync(1, kWork);
   }
@@ -497,8 +526,8 @@ __device__ __noinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, int 
     const uint2* wb = reinterpret_cast<const uint2*>(s.swdt()) + warp * (R / 16) * 32 + lane;
 #pragma unroll 2
     for (int st = 0; st < R / 16; ++st) {
-      const float* r0 = s.sdbc() + br * P + 16 * st + kq;
-      const float* r1 = r0 + 8 * P;
+      const float* r0 = s.sdbc() + br * PS + 16 * st + kq;
+      const float* r1 = r0 + 8 * PS;
       const uint32_t af[4] = {pack_bf2(r0[0], r0[1]), pack_bf2(r1[0], r1[1]), pack_bf2(r0[8], r0[9]),
                               pack_bf2(r1[8], r1[9])};
       const uint2 w2 = wb[st * 32];
@@ -506,12 +535,15 @@ __device__ __noinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, int 
     }
     const int ch = 8 * warp + kq;
     float* sdt = s.sdt();
-    sdt[br * a.nch_max + ch] = softplus(acc[0] + s.sbdt()[ch]);
-    sdt[br * a.nch_max + ch + 1] = softplus(acc[1] + s.sbdt()[ch + 1]);
-    sdt[(br + 8) * a.nch_max + ch] = softplus(acc[2] + s.sbdt()[ch]);
-    sdt[(br + 8) * a.nch_max + ch + 1] = softplus(acc[3] + s.sbdt()[ch + 1]);
+    // softplus with the linear branch above 20; 2-MUFU form (bf16 mode)
+    auto sp = [](float x) { return x > 20.f ? x : 0.6931471805599453f * __log2f(1.f + ex2_approx(x * 1.4426950408889634f)); };
+    sdt[br * a.nch_max + ch] = sp(acc[0] + s.sbdt()[ch]);
+    sdt[br * a.nch_max + ch + 1] = sp(acc[1] + s.sbdt()[ch + 1]);
+    sdt[(br + 8) * a.nch_max + ch] = sp(acc[2] + s.sbdt()[ch]);
+    sdt[(br + 8) * a.nch_max + ch + 1] = sp(acc[3] + s.sbdt()[ch + 1]);
   }
   named_bar_sync(1, kWork);
+  if (tid == 0) stamp(a, l, 13);
 #pragma unroll 1
   for (int q = 0; q < 2; ++q) {  // (not unrolled: one item's 16 states live at a time)
     const int it = tid + q * kWork;
@@ -522,10 +554,10 @@ __device__ __noinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, int 
       const float du = dt * uq;
       const float* hp = s.sh() + ((size_t)bb * a.nch_max + ch) * 16;
       const float* Ac = s.sA() + ch * 16;
-      const float* Bv = s.sdbc() + bb * P + R;
+      const float* Bv = s.sdbc() + bb * PS + R;
       const float* Cv = Bv + 16;
       float y = 0.f;
-      float* hg = ly.h + ((size_t)bb * E + d0 + ch) * 16;
+      float* hg = hglob + ((size_t)bb * E + d0 + ch) * 16;
 #pragma unroll
       for (int nn = 0; nn < 16; nn += 4) {
         const float4 h4 = *reinterpret_cast<const float4*>(hp + nn);
@@ -541,7 +573,7 @@ __device__ __noinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, int 
         *reinterpret_cast<float4*>(hg + nn) = o;
       }
       y = fmaf(s.sdsk()[ch], uq, y);
-      *reinterpret_cast<__nv_bfloat16*>(a.gf + afrag_off(bb, d0 + ch)) = __float2bfloat16_rn(y * silu<true>(zq));
+      gout[(size_t)bb * E + d0 + ch] = __float2bfloat16_rn(y * silu<true>(zq));
     }
   }
 }
@@ -558,6 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_stack_kernel(const __grid_
   const int ua0 = part(UA, c, nc), ua1 = part(UA, c + 1, nc);
   const int uc0 = part(UC, c, nc), uc1 = part(UC, c + 1, nc);
   const int gb0 = part(E / 8, c, nc), gb1 = part(E / 8, c + 1, nc);
+  const int gx0 = (ua0 + 1) >> 1, gx1 = (ua1 + 1) >> 1;   // x groups of this CTA's in_proj units
 
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
@@ -569,9 +602,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_stack_kernel(const __grid_
       mbar_init(&s.freeb()[i], kEW * 32);
     }
     mbar_init(s.mbB(), 1);
+    mbar_init(s.mbX(), 1);
+    mbar_init(s.mbSS(), kMW * 32);
     fence_barrier_init();
   }
-  if (tid < 16) s.sss()[tid] = 0.f;
   __syncthreads();
 
   // ---------------- ring producer (warp kMW + kEW, lane 0): every layer's A units then C units of this
@@ -584,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_stack_kernel(const __grid_
       p.nA = ua1 - ua0; p.nC = uc1 - uc0; p.ua0 = ua0; p.uc0 = uc0; p.szA = 16 * D; p.szC = 4 * E;
       p.total = a.L * (p.nA + p.nC);
       *pump = p;
-      pump_run(a, s, pump, 0x7fffffff);
+      pump_run(a, s, pump);
     }
     return;
   }
@@ -593,40 +627,44 @@ __global__ void __launch_bounds__(kThreads, 1) decode_stack_kernel(const __grid_
   const bool mw = warp < kMW;
   unsigned nbar = 0;
   Ctr ct{0, 0, 0};
-  if (tid == 0) issue_phase_b_prefetch(a, s, a.layers[0], gb0, gb1);
-
-  // ---- N0: ss and xr of the input residual (row groups of 8 columns, split over the CTAs)
-  if (!mw) {
-    const int g0 = part(D / 8, c, nc), g1 = part(D / 8, c + 1, nc);
-    for (int g = g0; g < g1; ++g) finalize_group(a, s, g, tid - kMW * 32);
+  if (tid == 0) {
+    issue_phase_b_prefetch(a, s, a.layers[0], gb0, gb1);
+    issue_phase_a_prefetch(a, s, a.layers[0], gx0, gx1);
   }
-  named_bar_sync(1, kWork);
-  if (tid < a.B) {
-    atomicAdd(&a.ssb[tid], s.sss()[tid]);
-    s.sss()[tid] = 0.f;
-  }
-  grid_sync(a.bar, (++nbar) * nc);
+  if (!mw) issue_window_prefetch(a, s, a.layers[0], gx0, gx1, tid - kMW * 32);
 
   for (int l = 0; l < a.L; ++l) {
-    const DsLayer& ly = a.layers[l];
-    // ---- A: in_proj + conv step + x_proj partial
-    if (mw) ct = mma_units<kMaxCA>(a, base, a.xr, D / 32, 0, ua0, ua1, 16 * D, ct);
+    // ---- A: pre-norm statistic + in_proj + conv step + x_proj partial
+    if (tid == 0) stamp(a, l, 0);
+    if (mw) ct = mma_units_a(a, base, l, ua0, ua1, ct);
     else ct = epi_units_a(a, base, l, ua0, ua1, ct);
+    if (tid == 0) stamp(a, l, 1);
+    if (tid == kMW * 32) stamp(a, l, 2);
     grid_sync(a.bar, (++nbar) * nc);
+    if (tid == 0) stamp(a, l, 3);
     // ---- B: dt_proj + softplus + scan step + D skip + gate
     phase_b(a, base, l, gb0, gb1);
+    if (tid == 0) stamp(a, l, 4);
     grid_sync(a.bar, (++nbar) * nc);
-    // ---- C: out_proj (K quarters) -> residual
-    if (tid == 0 && l + 1 < a.L) issue_phase_b_prefetch(a, s, a.layers[l + 1], gb0, gb1);
+    if (tid == 0) stamp(a, l, 5);
+    // ---- C: out_proj (K quarters) -> residual; the next layer's phase-A/B operands prefetched now
+    if (l + 1 < a.L) {
+      if (tid == 0) {
+        issue_phase_b_prefetch(a, s, a.layers[l + 1], gb0, gb1);
+        issue_phase_a_prefetch(a, s, a.layers[l + 1], gx0, gx1);
+      }
+      if (!mw) issue_window_prefetch(a, s, a.layers[l + 1], gx0, gx1, tid - kMW * 32);
+    }
     if (c == 0) {
       float* xacc = a.xacc + (l & 1) * 16 * a.P;
       for (int i = tid; i < 16 * a.P; i += kWork) xacc[i] = 0.f;  // re-armed for layer l + 2
-      if (l + 1 == a.L && tid < 32) a.ssb[tid] = 0.f;             // both pre-norm sums zero for the next launch
     }
-    if (mw) ct = mma_units<kMaxCC>(a, base, a.gf, E / 128, D / 8, uc0, uc1, 4 * E, ct);
-    else ct = epi_units_c(a, base, l, uc0, uc1, ct);
-    (void)ly;
+    if (mw) ct = mma_units_c(a, base, l, uc0, uc1, ct);
+    else ct = epi_units_c(a, base, uc0, uc1, ct);
+    if (tid == 0) stamp(a, l, 6);
+    if (tid == kMW * 32) stamp(a, l, 7);
     if (l + 1 < a.L) grid_sync(a.bar, (++nbar) * nc);
+    if (tid == 0) stamp(a, l, 8);
   }
 
   // exit: the last CTA out resets the barrier counter for the next launch
@@ -638,21 +676,16 @@ __global__ void __launch_bounds__(kThreads, 1) decode_stack_kernel(const __grid_
       atomicExch(a.bar + 1, 0u);
     }
   }
-  (void)lane;
 }
 
 // ---------------------------------------------------------------- weight packing (once per plan)
-// B fragments of an 8-row block over a 32-wide k chunk: lane L holds W[row0 + L/4][k0 + 2q + {0,1}],
-// [+8], [+16], [+24] (q = L % 4) = the m16n8k16 registers b0, b1 of two k16 steps.
+// B fragments of an 8-row block over a 32-wide k chunk, k permuted inside the chunk: lane L holds
+// W[row0 + L/4][k0 + 8 (L%4) + 0..7] and uses elements 0-1 / 2-3 as b0 / b1 of the first k16 step and
+// 4-5 / 6-7 as b0 / b1 of the second.  The A fragments use the same permutation (a lane's 8 elements
+// of a row are the activations at k0 + 8 (L%4) + 0..7), so both operands load as contiguous 16-B runs
+// of row-major data; the dot product over the chunk is unchanged (a permutation of its terms).
 __device__ __forceinline__ uint4 bfrag8x32(const __nv_bfloat16* W, int64_t ld, int row, int k0, int lane) {
-  const int q = lane & 3;
-  const __nv_bfloat16* p = W + (int64_t)row * ld + k0 + 2 * q;
-  uint4 o;
-  o.x = *reinterpret_cast<const uint32_t*>(p);
-  o.y = *reinterpret_cast<const uint32_t*>(p + 8);
-  o.z = *reinterpret_cast<const uint32_t*>(p + 16);
-  o.w = *reinterpret_cast<const uint32_t*>(p + 24);
-  return o;
+  return *reinterpret_cast<const uint4*>(W + (int64_t)row * ld + k0 + 8 * (lane & 3));
 }
 
 // in_proj [2E][D] -> units (x group i = 2i, z group i = 2i+1) of D/32 chunks
@@ -718,15 +751,19 @@ DsGeom ds_geometry(int B, int D, int E, int R, int P, int K, int num_sms) {  // 
   auto al = [](int x) { return (x + 127) & ~127; };
   const int sb = al(B * g.nch_max * 64) + al(gmax * (R / 16) * 256) + al(g.nch_max * 64) + al(g.nch_max * 4) * 2;
   const int red = 2 * kMW * 128 * 4;
-  const int pbz = al(16 * P * 4) + al(16 * g.nch_max * 4) + al(g.nch_max * 16 * 4);
+  const int pbB = al(16 * (P + 8) * 4) + al(16 * g.nch_max * 4) + al(g.nch_max * 16 * 4);
+  const int pbA = kMaxXU * P * 16 + kMaxXU * 8 * 4 * 4 + kMaxXU * 8 * 4 + kMaxXU * 16 * 3 * 8 * 2;
+  const int pbz = al(pbB > pbA ? pbB : pbA);
   const int ut = 2 * 16 * 8 * 2;
-  const int misc = 512 + 128;  // mbarriers, rstd, ss, finalise list | pump state
+  const int misc = 1024 + 128;  // mbarriers, pre-norm partials | pump state
   const int fixed = sb + red + pbz + ut + misc;
   const int budget = 227 * 1024 - 1024;  // dynamic smem minus the 1 KB alignment slack
   int ring = (budget - fixed) / 4096 * 4096;
   const int maxunit = 16 * D > 4 * E ? 16 * D : 4 * E;
   if (ring < 2 * maxunit) g.ok = false;
-  if ((D / 2 + num_sms - 1) / num_sms > 32 || B * g.nch_max > 2 * kWork || gmax > kMW + kEW) g.ok = false;
+  if ((D / 2 + num_sms - 1) / num_sms > 32 || B * g.nch_max > 2 * kWork || gmax > kMW + kEW ||
+      (E / 4 + num_sms - 1) / num_sms > 2 * kMaxXU - 1)
+    g.ok = false;
   g.ring_bytes = ring;
   g.off_sb = ring;
   g.off_red = g.off_sb + sb;
@@ -734,8 +771,7 @@ DsGeom ds_geometry(int B, int D, int E, int R, int P, int K, int num_sms) {  // 
   g.off_ut = g.off_pb + pbz;
   g.off_misc = g.off_ut + ut;
   g.smem = g.off_misc + misc + 1024;
-  g.scratch_bytes = (size_t)(D / 32) * 1024 + (size_t)(E / 32) * 1024 + 2 * (size_t)16 * E * 2 +
-                    (size_t)2 * 16 * P * 4 + 2 * 16 * 4 + (size_t)(D / 8) * 4 + 64;
+  g.scratch_bytes = 3 * (size_t)16 * E * 2 + (size_t)2 * 16 * P * 4 + 64;
   return g;
 }
 
@@ -776,7 +812,7 @@ size_t ds_layer_entry_bytes() { return sizeof(DsLayer); }
 
 cudaError_t ds_launch(const DsLayer* layers_dev, int L, int B, int D, int E, int R, int P, int K, float eps,
                       int bcdt_rmsnorm, float rms_eps, float* r, uint8_t* scratch, const DsGeom& g, int num_sms,
-                      cudaStream_t s) {
+                      cudaStream_t s, unsigned long long* trace) {
   DsArgs a{};
   a.layers = layers_dev;
   a.L = L; a.B = B; a.D = D; a.E = E; a.R = R; a.P = P; a.K = K;
@@ -785,13 +821,10 @@ cudaError_t ds_launch(const DsLayer* layers_dev, int L, int B, int D, int E, int
   a.rms_eps = rms_eps;
   a.r = r;
   uint8_t* p = scratch;
-  a.xr = p; p += (size_t)(D / 32) * 1024;
-  a.gf = p; p += (size_t)(E / 32) * 1024;
+  a.g = reinterpret_cast<__nv_bfloat16*>(p); p += (size_t)16 * E * 2;
   a.u = reinterpret_cast<__nv_bfloat16*>(p); p += (size_t)16 * E * 2;
   a.z = reinterpret_cast<__nv_bfloat16*>(p); p += (size_t)16 * E * 2;
   a.xacc = reinterpret_cast<float*>(p); p += (size_t)2 * 16 * P * 4;
-  a.ssb = reinterpret_cast<float*>(p); p += 2 * 16 * 4;
-  a.cnt = reinterpret_cast<unsigned*>(p); p += (size_t)(D / 8) * 4;
   a.bar = reinterpret_cast<unsigned*>(p);
   a.ring_bytes = g.ring_bytes;
   a.nch_max = g.nch_max;
@@ -800,6 +833,12 @@ cudaError_t ds_launch(const DsLayer* layers_dev, int L, int B, int D, int E, int
   a.off_pb = g.off_pb;
   a.off_ut = g.off_ut;
   a.off_misc = g.off_misc;
+  a.trace = trace;
+  {
+    const char* ev = getenv("SSM_DS_INFLIGHT");  // (experiment knob, removed once measured)
+    a.max_inflight = ev ? atoi(ev) : kSlots;
+    if (a.max_inflight < 1 || a.max_inflight > kSlots) a.max_inflight = kSlots;
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(decode_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

@@ -197,7 +197,7 @@ cudaError_t ds_fill_layer(DsLayer* host_entry, const uint8_t* packed, int D, int
                           const float* d_skip, void* cst, float* h);
 cudaError_t ds_launch(const DsLayer* layers_dev, int L, int B, int D, int E, int R, int P, int K, float eps,
                       int bcdt_rmsnorm, float rms_eps, float* r, uint8_t* scratch, const DsGeom& g, int num_ctas,
-                      cudaStream_t s);
+                      cudaStream_t s, unsigned long long* trace = nullptr);
 cudaError_t preload_decode_stack();
 int ds_max_active(int smem);
 
