@@ -31,7 +31,6 @@
 // pipe of mma.sync is far from the bound, what matters is keeping every SM's stream fed.
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
-#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -49,6 +48,7 @@ constexpr int kMaxCA = 8;                   // phase A: 32-wide k chunks per MMA
 constexpr int kMaxCC = 4;                   // phase C: chunks per MMA warp per quarter (E <= 5632)
 constexpr int kMaxPT = 8;                   // x_proj 8-wide p tiles per epilogue warp (P <= 256)
 constexpr int kMaxXU = 5;                   // in_proj x units (8 channels) per CTA
+constexpr int kL2Ahead = 4;                 // ring units prefetched into L2 ahead of the ring
 
 SSM_DEV void mma_1688_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
   asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
@@ -94,7 +94,6 @@ struct DsArgs {
   unsigned* bar;            // [2] grid-barrier counter, exit counter
   int ring_bytes, nch_max;  // ring size; max phase-B channels per CTA
   unsigned long long* trace; // debug (ssm_dbg_dstack_trace): [grid][L][32] globaltimer stamps, or NULL
-  int max_inflight;          // ring units issued but not yet landed, at most
   int off_sb, off_red, off_pb, off_ut, off_misc;
 };
 
@@ -192,10 +191,15 @@ SSM_DEV void issue_window_prefetch(const DsArgs& a, const Smem& s, const DsLayer
 // Ring producer state (lane 0 of the producer warp).
 struct Pump {
   long long issued, released;
-  int seq, oldest, landed, nA, nC, ua0, uc0, szA, szC, total;
+  int seq, oldest, pf, nA, nC, ua0, uc0, szA, szC, total;
 };
 
 SSM_DEV int pump_size(const Pump& p, int q) { return q % (p.nA + p.nC) < p.nA ? p.szA : p.szC; }
+SSM_DEV const uint8_t* pump_src(const DsArgs& a, const Pump& p, int q) {
+  const int l = q / (p.nA + p.nC), pos = q % (p.nA + p.nC);
+  const DsLayer& ly = a.layers[l];
+  return pos < p.nA ? ly.wa + (size_t)(p.ua0 + pos) * p.szA : ly.wc + (size_t)(p.uc0 + pos - p.nA) * p.szC;
+}
 
 // Issue units while the ring has room (waiting for the oldest unit's release when it has none).
 __device__ __forceinline__ void pump_run(const DsArgs& a, const Smem& s, Pump* pp) {
@@ -207,14 +211,12 @@ __device__ __forceinline__ void pump_run(const DsArgs& a, const Smem& s, Pump* p
       p.released += pump_size(p, p.oldest);
       ++p.oldest;
     }
-    // bounded bytes in flight: deep TMA queues delay every other memory access of the step
-    while (p.seq - p.landed >= a.max_inflight) {
-      mbar_wait(&s.full()[p.landed % kSlots], (p.landed / kSlots) & 1);
-      ++p.landed;
-    }
-    const int l = p.seq / (p.nA + p.nC), pos = p.seq % (p.nA + p.nC);
-    const DsLayer& ly = a.layers[l];
-    const uint8_t* src = pos < p.nA ? ly.wa + (size_t)(p.ua0 + pos) * sz : ly.wc + (size_t)(p.uc0 + pos - p.nA) * sz;
+    // L2 prefetch kL2Ahead units beyond the ring: while the ring is full during the latency-bound steps
+    // (scan step, barriers, phase starts) HBM keeps streaming the next units into L2 (deeper lookahead
+    // measured slower: 4 -> 32.0, 8 -> 33.0, 16 -> 35.9 us per Mamba-2.8B layer)
+    for (; p.pf < p.total && p.pf < p.seq + 1 + kL2Ahead; ++p.pf)
+      prefetch_l2(pump_src(a, p, p.pf), (uint32_t)pump_size(p, p.pf));
+    const uint8_t* src = pump_src(a, p, p.seq);
     const int off = (int)(p.issued % a.ring_bytes);
     uint64_t* fb = &s.full()[p.seq % kSlots];
     mbar_arrive_expect_tx(fb, (uint32_t)sz);
@@ -472,13 +474,7 @@ __device__ __forceinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, i
   float* const hglob = a.layers[l].h;
   __nv_bfloat16* const gout = a.g;
   const float* xacc = a.xacc + (l & 1) * 16 * P;
-  for (int i = tid; i < 16 * (P / 4); i += kWork) {
-    const int bb = i / (P / 4), q = i % (P / 4);
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (bb < B) v = __ldcg(reinterpret_cast<const float4*>(xacc + bb * P) + q);
-    reinterpret_cast<float4*>(s.sdbc() + bb * PS)[q] = v;
-  }
-  // this thread's items (b, ch): u and z loads in flight
+  // this thread's items (b, ch): u and z loads in flight first
   const int nit = B * nch;
   float uu0 = 0.f, zz0 = 0.f, uu1 = 0.f, zz1 = 0.f;
   if (tid < nit) {
@@ -491,6 +487,14 @@ __device__ __forceinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, i
     uu1 = __bfloat162float(__ldcg(a.u + (size_t)bb * E + d0 + ch));
     zz1 = __bfloat162float(__ldcg(a.z + (size_t)bb * E + d0 + ch));
   }
+  // the summed x_proj rows (dt_low | B | C) -> shared memory by cp.async, all copies in flight at once
+  // (rows >= B zero-filled)
+  for (int i = tid; i < 16 * (P / 4); i += kWork) {
+    const int bb = i / (P / 4), q = i % (P / 4);
+    cp_async16(s.sdbc() + bb * PS + 4 * q, xacc + (bb < B ? bb : 0) * P + 4 * q, bb < B);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
   if (tid == 0) stamp(a, l, 11);
   mbar_wait(s.mbB(), l & 1);
   if (tid == 0) stamp(a, l, 12);
@@ -521,7 +525,7 @@ __device__ __forceinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, i
   }
   // dt_proj on the tensor pipe: dt[b][ch] = sum_r dt_low[b][r] W_dt[ch][r] (m16n8k16, warp = 8 channels)
   if (warp < ng) {
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};  // even / odd k16 steps
     const int br = lane >> 2, kq = 2 * (lane & 3);
     const uint2* wb = reinterpret_cast<const uint2*>(s.swdt()) + warp * (R / 16) * 32 + lane;
 #pragma unroll 2
@@ -531,8 +535,11 @@ __device__ __forceinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, i
       const uint32_t af[4] = {pack_bf2(r0[0], r0[1]), pack_bf2(r1[0], r1[1]), pack_bf2(r0[8], r0[9]),
                               pack_bf2(r1[8], r1[9])};
       const uint2 w2 = wb[st * 32];
-      mma_16816_bf16(acc, af, w2.x, w2.y);
+      if (st & 1) mma_16816_bf16(acc2, af, w2.x, w2.y);
+      else mma_16816_bf16(acc, af, w2.x, w2.y);
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] += acc2[q];
     const int ch = 8 * warp + kq;
     float* sdt = s.sdt();
     // softplus with the linear branch above 20; 2-MUFU form (bf16 mode)
@@ -834,11 +841,6 @@ cudaError_t ds_launch(const DsLayer* layers_dev, int L, int B, int D, int E, int
   a.off_ut = g.off_ut;
   a.off_misc = g.off_misc;
   a.trace = trace;
-  {
-    const char* ev = getenv("SSM_DS_INFLIGHT");  // (experiment knob, removed once measured)
-    a.max_inflight = ev ? atoi(ev) : kSlots;
-    if (a.max_inflight < 1 || a.max_inflight > kSlots) a.max_inflight = kSlots;
-  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(decode_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
