@@ -116,6 +116,8 @@ struct Smem {
   SSM_DEV float* sdbc() const { return reinterpret_cast<float*>(base + a->off_pb); }  // [16][P + 8] (bank shift per row)
   SSM_DEV float* sdt() const { return sdbc() + 16 * (a->P + 8); }                                   // [16][nch_max]
   SSM_DEV float* sA() const { return sdt() + 16 * a->nch_max; }                                      // [nch_max][16]
+  SSM_DEV __nv_bfloat16* su() const { return reinterpret_cast<__nv_bfloat16*>(sA() + a->nch_max * 16); }  // [16][nch_max]
+  SSM_DEV __nv_bfloat16* sz() const { return su() + 16 * a->nch_max; }                                    // [16][nch_max]
   SSM_DEV __nv_bfloat16* utile() const { return reinterpret_cast<__nv_bfloat16*>(base + a->off_ut); }  // [2][16][8]
   SSM_DEV uint64_t* full() const { return reinterpret_cast<uint64_t*>(base + a->off_misc); }     // [kSlots]
   SSM_DEV uint64_t* empty() const { return full() + kSlots; }                                       // [kSlots]
@@ -474,18 +476,12 @@ __device__ __forceinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, i
   float* const hglob = a.layers[l].h;
   __nv_bfloat16* const gout = a.g;
   const float* xacc = a.xacc + (l & 1) * 16 * P;
-  // this thread's items (b, ch): u and z loads in flight first
+  // u and z rows of this CTA's channels -> shared memory (16-B cp.async pieces of the 2 nch-byte rows)
   const int nit = B * nch;
-  float uu0 = 0.f, zz0 = 0.f, uu1 = 0.f, zz1 = 0.f;
-  if (tid < nit) {
-    const int bb = tid / nch, ch = tid % nch;
-    uu0 = __bfloat162float(__ldcg(a.u + (size_t)bb * E + d0 + ch));
-    zz0 = __bfloat162float(__ldcg(a.z + (size_t)bb * E + d0 + ch));
-  }
-  if (tid + kWork < nit) {
-    const int bb = (tid + kWork) / nch, ch = (tid + kWork) % nch;
-    uu1 = __bfloat162float(__ldcg(a.u + (size_t)bb * E + d0 + ch));
-    zz1 = __bfloat162float(__ldcg(a.z + (size_t)bb * E + d0 + ch));
+  for (int i = tid; i < 2 * B * (nch / 8); i += kWork) {
+    const int which = i / (B * (nch / 8)), r = i % (B * (nch / 8)), bb = r / (nch / 8), c8 = r % (nch / 8);
+    const __nv_bfloat16* src = (which ? a.z : a.u) + (size_t)bb * E + d0 + 8 * c8;
+    cp_async16((which ? s.sz() : s.su()) + bb * a.nch_max + 8 * c8, src, true);
   }
   // the summed x_proj rows (dt_low | B | C) -> shared memory by cp.async, all copies in flight at once
   // (rows >= B zero-filled)
@@ -551,36 +547,34 @@ __device__ __forceinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, i
   }
   named_bar_sync(1, kWork);
   if (tid == 0) stamp(a, l, 13);
-#pragma unroll 1
-  for (int q = 0; q < 2; ++q) {  // (not unrolled: one item's 16 states live at a time)
-    const int it = tid + q * kWork;
-    const float uq = q == 0 ? uu0 : uu1, zq = q == 0 ? zz0 : zz1;
-    if (it < nit) {
-      const int bb = it / nch, ch = it % nch;
-      const float dt = s.sdt()[bb * a.nch_max + ch];
-      const float du = dt * uq;
-      const float* hp = s.sh() + ((size_t)bb * a.nch_max + ch) * 16;
-      const float* Ac = s.sA() + ch * 16;
-      const float* Bv = s.sdbc() + bb * PS + R;
-      const float* Cv = Bv + 16;
-      float y = 0.f;
-      float* hg = hglob + ((size_t)bb * E + d0 + ch) * 16;
-#pragma unroll
-      for (int nn = 0; nn < 16; nn += 4) {
-        const float4 h4 = *reinterpret_cast<const float4*>(hp + nn);
-        const float4 a4 = *reinterpret_cast<const float4*>(Ac + nn);
-        const float4 b4 = *reinterpret_cast<const float4*>(Bv + nn);
-        const float4 c4 = *reinterpret_cast<const float4*>(Cv + nn);
-        float4 o;  // h_t = exp(dt A) h_{t-1} + dt B_t u_t  (ZOH for A, Euler for B: reading Q1)
-        o.x = fmaf(ex2_approx(dt * a4.x), h4.x, du * b4.x);
-        o.y = fmaf(ex2_approx(dt * a4.y), h4.y, du * b4.y);
-        o.z = fmaf(ex2_approx(dt * a4.z), h4.z, du * b4.z);
-        o.w = fmaf(ex2_approx(dt * a4.w), h4.w, du * b4.w);
-        y = fmaf(c4.x, o.x, y); y = fmaf(c4.y, o.y, y); y = fmaf(c4.z, o.z, y); y = fmaf(c4.w, o.w, y);
-        *reinterpret_cast<float4*>(hg + nn) = o;
+  // items (b, ch) with 4 lanes per item, each lane owning 4 of the 16 states (one float4): the h / A rows
+  // of the 8 items of a warp are then contiguous 512-B runs in shared and global memory
+  for (int task0 = 0; task0 < 4 * nit; task0 += kWork) {
+    const int task = task0 + tid, it = task >> 2, nq = 4 * (task & 3);
+    const bool ok = it < nit;   // (all 4 lanes of an item agree; the shuffles below run warp-wide)
+    const int bb = ok ? it / nch : 0, ch = ok ? it % nch : 0;
+    const float dt = s.sdt()[bb * a.nch_max + ch];
+    const float uq = __bfloat162float(s.su()[bb * a.nch_max + ch]);
+    const float du = dt * uq;
+    const float4 h4 = *reinterpret_cast<const float4*>(s.sh() + ((size_t)bb * a.nch_max + ch) * 16 + nq);
+    const float4 a4 = *reinterpret_cast<const float4*>(s.sA() + ch * 16 + nq);
+    const float4 b4 = *reinterpret_cast<const float4*>(s.sdbc() + bb * PS + R + nq);
+    const float4 c4 = *reinterpret_cast<const float4*>(s.sdbc() + bb * PS + R + 16 + nq);
+    float4 o;  // h_t = exp(dt A) h_{t-1} + dt B_t u_t  (ZOH for A, Euler for B: reading Q1)
+    o.x = fmaf(ex2_approx(dt * a4.x), h4.x, du * b4.x);
+    o.y = fmaf(ex2_approx(dt * a4.y), h4.y, du * b4.y);
+    o.z = fmaf(ex2_approx(dt * a4.z), h4.z, du * b4.z);
+    o.w = fmaf(ex2_approx(dt * a4.w), h4.w, du * b4.w);
+    float y = c4.x * o.x;
+    y = fmaf(c4.y, o.y, y); y = fmaf(c4.z, o.z, y); y = fmaf(c4.w, o.w, y);
+    y += __shfl_xor_sync(0xffffffffu, y, 1);
+    y += __shfl_xor_sync(0xffffffffu, y, 2);
+    if (ok) {
+      *reinterpret_cast<float4*>(hglob + ((size_t)bb * E + d0 + ch) * 16 + nq) = o;
+      if (nq == 0) {
+        y = fmaf(s.sdsk()[ch], uq, y);
+        gout[(size_t)bb * E + d0 + ch] = __float2bfloat16_rn(y * silu<true>(__bfloat162float(s.sz()[bb * a.nch_max + ch])));
       }
-      y = fmaf(s.sdsk()[ch], uq, y);
-      gout[(size_t)bb * E + d0 + ch] = __float2bfloat16_rn(y * silu<true>(zq));
     }
   }
 }
@@ -758,7 +752,7 @@ DsGeom ds_geometry(int B, int D, int E, int R, int P, int K, int num_sms) {  // 
   auto al = [](int x) { return (x + 127) & ~127; };
   const int sb = al(B * g.nch_max * 64) + al(gmax * (R / 16) * 256) + al(g.nch_max * 64) + al(g.nch_max * 4) * 2;
   const int red = 2 * kMW * 128 * 4;
-  const int pbB = al(16 * (P + 8) * 4) + al(16 * g.nch_max * 4) + al(g.nch_max * 16 * 4);
+  const int pbB = al(16 * (P + 8) * 4) + al(16 * g.nch_max * 4) + al(g.nch_max * 16 * 4) + 2 * 16 * g.nch_max * 2;
   const int pbA = kMaxXU * P * 16 + kMaxXU * 8 * 4 * 4 + kMaxXU * 8 * 4 + kMaxXU * 16 * 3 * 8 * 2;
   const int pbz = al(pbB > pbA ? pbB : pbA);
   const int ut = 2 * 16 * 8 * 2;
@@ -768,7 +762,7 @@ DsGeom ds_geometry(int B, int D, int E, int R, int P, int K, int num_sms) {  // 
   int ring = (budget - fixed) / 4096 * 4096;
   const int maxunit = 16 * D > 4 * E ? 16 * D : 4 * E;
   if (ring < 2 * maxunit) g.ok = false;
-  if ((D / 2 + num_sms - 1) / num_sms > 32 || B * g.nch_max > 2 * kWork || gmax > kMW + kEW ||
+  if ((D / 2 + num_sms - 1) / num_sms > 32 || gmax > kMW + kEW ||
       (E / 4 + num_sms - 1) / num_sms > 2 * kMaxXU - 1)
     g.ok = false;
   g.ring_bytes = ring;
