@@ -19,6 +19,8 @@ Modules:
              in-process.
 
   agreement_ref  Table 1's agreement metrics, straight-line.
+  attention_ref  Zamba's shared attention + MLP block with its KV cache and TP split (NEXT-1).
+  mamba2_ref     the Mamba-2 (SSD) mixer as a per-timestep recurrence, with its TP split (NEXT-4).
 
 Pins (tests/test_oracle_*.py): SPEC.md worked examples (closed forms),
 scipy.signal.lfilter on constant-parameter scans, torch conv1d, a pure-Python
@@ -27,5 +29,7 @@ ZambaMambaMixer slow paths in float64, the pre-norm stack (model_forward)
 against chained HF MambaBlocks in float64 (eps-sensitive scale), cache/prefix
 invariants, the hand-worked int8 blocks (tests/golden/qar_block.txt,
 qar_twoshot.txt) and the closed-form bounds' hand values
-(tests/golden/qar_bounds.txt: northstar_bound, fp16_error_bound).
+(tests/golden/qar_bounds.txt: northstar_bound, fp16_error_bound), HF
+ZambaAttentionDecoderLayer and Mamba2Mixer.torch_forward in float64 for the NEXT-1 / NEXT-4
+modules.
 """
