@@ -439,10 +439,18 @@ __device__ __forceinline__ Ctr epi_units_a(const DsArgs& a, uint8_t* base, int l
 #pragma unroll
   for (int k = 0; k < kMaxPT; ++k) {
     const int t = ew + kEW * k;
-    if (t < npt) {
-      const int p = 8 * t + 2 * (lane & 3), br = lane >> 2;
-      if (br < B) red_add_v2(xacc + br * P + p, xp[k][0], xp[k][1]);
-      if (br + 8 < B) red_add_v2(xacc + (br + 8) * P + p, xp[k][2], xp[k][3]);
+    if (t < npt) {  // (warp-uniform)
+      // lane pairs (tig even, tig + 1) hold 4 consecutive columns of rows br and br + 8: the even lane
+      // reduces row br's four, the odd lane row br + 8's four (one 16-B reduction each)
+      const bool odd = lane & 1;
+      const float o0 = __shfl_xor_sync(0xffffffffu, odd ? xp[k][0] : xp[k][2], 1);
+      const float o1 = __shfl_xor_sync(0xffffffffu, odd ? xp[k][1] : xp[k][3], 1);
+      const int br = (lane >> 2) + (odd ? 8 : 0), p = 8 * t + 2 * (lane & 2);
+      if (br < B) {
+        float* dst = xacc + br * P + p;
+        if (odd) asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(o0), "f"(o1), "f"(xp[k][2]), "f"(xp[k][3]) : "memory");
+        else asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(xp[k][0]), "f"(xp[k][1]), "f"(o0), "f"(o1) : "memory");
+      }
     }
   }
   return ct;
@@ -549,10 +557,16 @@ __device__ __forceinline__ void phase_b(const DsArgs& a, uint8_t* base, int l, i
   if (tid == 0) stamp(a, l, 13);
   // items (b, ch) with 4 lanes per item, each lane owning 4 of the 16 states (one float4): the h / A rows
   // of the 8 items of a warp are then contiguous 512-B runs in shared and global memory
+  // item it = bb nch + ch advances by kWork / 4 per round: (bb, ch) updated without divisions
+  const int step_b = (kWork / 4) / nch, step_c = (kWork / 4) % nch;
+  int ib = (tid >> 2) / nch, ic = (tid >> 2) % nch;
   for (int task0 = 0; task0 < 4 * nit; task0 += kWork) {
-    const int task = task0 + tid, it = task >> 2, nq = 4 * (task & 3);
+    const int it = (task0 + tid) >> 2, nq = 4 * (tid & 3);
     const bool ok = it < nit;   // (all 4 lanes of an item agree; the shuffles below run warp-wide)
-    const int bb = ok ? it / nch : 0, ch = ok ? it % nch : 0;
+    const int bb = ok ? ib : 0, ch = ok ? ic : 0;
+    ib += step_b;
+    ic += step_c;
+    if (ic >= nch) { ic -= nch; ++ib; }
     const float dt = s.sdt()[bb * a.nch_max + ch];
     const float uq = __bfloat162float(s.su()[bb * a.nch_max + ch]);
     const float du = dt * uq;
