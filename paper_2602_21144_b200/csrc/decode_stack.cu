@@ -48,7 +48,8 @@ constexpr int kMaxCA = 8;                   // phase A: 32-wide k chunks per MMA
 constexpr int kMaxCC = 4;                   // phase C: chunks per MMA warp per quarter (E <= 5632)
 constexpr int kMaxPT = 8;                   // x_proj 8-wide p tiles per epilogue warp (P <= 256)
 constexpr int kMaxXU = 5;                   // in_proj x units (8 channels) per CTA
-constexpr int kL2Ahead = 4;                 // ring units prefetched into L2 ahead of the ring
+constexpr int kRB = 4;                      // reduction buffers: the MMA warps run up to 3 units ahead
+constexpr int kL2Ahead = 3;                 // ring units prefetched into L2 ahead of the ring
 
 SSM_DEV void mma_1688_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
   asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
@@ -112,7 +113,7 @@ struct Smem {
   }
   SSM_DEV float* sbdt() const { return salog() + a->nch_max * 16; }
   SSM_DEV float* sdsk() const { return sbdt() + a->nch_max; }
-  SSM_DEV float* sred() const { return reinterpret_cast<float*>(base + a->off_red); }              // [2][kMW][128]
+  SSM_DEV float* sred() const { return reinterpret_cast<float*>(base + a->off_red); }              // [kRB][kMW][128]
   SSM_DEV float* sdbc() const { return reinterpret_cast<float*>(base + a->off_pb); }  // [16][P + 8] (bank shift per row)
   SSM_DEV float* sdt() const { return sdbc() + 16 * (a->P + 8); }                                   // [16][nch_max]
   SSM_DEV float* sA() const { return sdt() + 16 * a->nch_max; }                                      // [nch_max][16]
@@ -121,12 +122,12 @@ struct Smem {
   SSM_DEV __nv_bfloat16* utile() const { return reinterpret_cast<__nv_bfloat16*>(base + a->off_ut); }  // [2][16][8]
   SSM_DEV uint64_t* full() const { return reinterpret_cast<uint64_t*>(base + a->off_misc); }     // [kSlots]
   SSM_DEV uint64_t* empty() const { return full() + kSlots; }                                       // [kSlots]
-  SSM_DEV uint64_t* ready() const { return full() + 2 * kSlots; }                                   // [2]
-  SSM_DEV uint64_t* freeb() const { return full() + 2 * kSlots + 2; }                               // [2]
-  SSM_DEV uint64_t* mbB() const { return full() + 2 * kSlots + 4; }                                 // phase-B prefetch
-  SSM_DEV uint64_t* mbX() const { return full() + 2 * kSlots + 5; }                                 // phase-A prefetch
-  SSM_DEV uint64_t* mbSS() const { return full() + 2 * kSlots + 6; }                                // pre-norm partials
-  SSM_DEV float* ssp() const { return reinterpret_cast<float*>(full() + 2 * kSlots + 7); }         // [kMW][16]
+  SSM_DEV uint64_t* ready() const { return full() + 2 * kSlots; }                                   // [kRB]
+  SSM_DEV uint64_t* freeb() const { return full() + 2 * kSlots + kRB; }                             // [kRB]
+  SSM_DEV uint64_t* mbB() const { return full() + 2 * kSlots + 2 * kRB; }                           // phase-B prefetch
+  SSM_DEV uint64_t* mbX() const { return full() + 2 * kSlots + 2 * kRB + 1; }                       // phase-A prefetch
+  SSM_DEV uint64_t* mbSS() const { return full() + 2 * kSlots + 2 * kRB + 2; }                      // pre-norm partials
+  SSM_DEV float* ssp() const { return reinterpret_cast<float*>(full() + 2 * kSlots + 2 * kRB + 3); }  // [kMW][16]
   SSM_DEV struct Pump* pump() const { return reinterpret_cast<struct Pump*>(base + a->off_misc + 1024); }
   // phase-A epilogue operands of this CTA's x units (aliasing the phase-B scratch, free during C and A):
   // W_x B fragments [kMaxXU][P/8][32] u32, conv taps [kMaxXU * 8][K], conv bias [kMaxXU * 8], windows
@@ -215,7 +216,7 @@ __device__ __forceinline__ void pump_run(const DsArgs& a, const Smem& s, Pump* p
     }
     // L2 prefetch kL2Ahead units beyond the ring: while the ring is full during the latency-bound steps
     // (scan step, barriers, phase starts) HBM keeps streaming the next units into L2 (deeper lookahead
-    // measured slower: 4 -> 32.0, 8 -> 33.0, 16 -> 35.9 us per Mamba-2.8B layer)
+    // measured: 2-3 best; 6 +1.5%, 8 +3%, 16 +12%, 32 +30% per Mamba-2.8B layer)
     for (; p.pf < p.total && p.pf < p.seq + 1 + kL2Ahead; ++p.pf)
       prefetch_l2(pump_src(a, p, p.pf), (uint32_t)pump_size(p, p.pf));
     const uint8_t* src = pump_src(a, p, p.seq);
@@ -278,10 +279,10 @@ SSM_DEV Ctr unit_loop(const DsArgs& a, const Smem& s, const uint32_t (&xa)[MAXC]
       }
     }
     mbar_arrive(&s.empty()[slot]);
-    mbar_wait(&s.freeb()[ct.useq & 1], ((ct.useq >> 1) & 1) ^ 1);
-    float* sp = s.sred() + (ct.useq & 1) * (kMW * 128) + warp * 128;
+    mbar_wait(&s.freeb()[ct.useq % kRB], ((ct.useq / kRB) & 1) ^ 1);
+    float* sp = s.sred() + (ct.useq % kRB) * (kMW * 128) + warp * 128;
     sp[lane] = acc[0]; sp[32 + lane] = acc[1]; sp[64 + lane] = acc[2]; sp[96 + lane] = acc[3];
-    mbar_arrive(&s.ready()[ct.useq & 1]);
+    mbar_arrive(&s.ready()[ct.useq % kRB]);
     ct.roff += sz;
     if (ct.roff >= a.ring_bytes) ct.roff -= a.ring_bytes;
   }
@@ -363,7 +364,7 @@ __device__ __forceinline__ Ctr mma_units_c(const DsArgs& a, uint8_t* base, int l
 // Epilogue thread e = (b = e / 8, n = e % 8): the unit's output element (token b, row n), summed over
 // the kMW partials in fixed warp order.
 SSM_DEV float reduce_unit(const Smem& s, int useq, int b, int n) {
-  const float* sp = s.sred() + (useq & 1) * (kMW * 128) + ((b >> 3) * 2 + (n & 1)) * 32 + (b & 7) * 4 + (n >> 1);
+  const float* sp = s.sred() + (useq % kRB) * (kMW * 128) + ((b >> 3) * 2 + (n & 1)) * 32 + (b & 7) * 4 + (n >> 1);
   float v = 0.f;
 #pragma unroll
   for (int w = 0; w < kMW; ++w) v += sp[w * 128];
@@ -399,10 +400,10 @@ __device__ __forceinline__ Ctr epi_units_a(const DsArgs& a, uint8_t* base, int l
     const bool is_x = (u & 1) == 0;
     const int i = u >> 1, f = 8 * i + n, xi = i - gx0;
     if (e == 0 && u - u0 < 8) stamp(a, l, 16 + (u - u0));
-    mbar_wait(&s.ready()[ct.useq & 1], (ct.useq >> 1) & 1);
+    mbar_wait(&s.ready()[ct.useq % kRB], (ct.useq / kRB) & 1);
     if (e == 0 && u - u0 < 8) stamp(a, l, 24 + (u - u0));
     float v = reduce_unit(s, ct.useq, b, n);
-    mbar_arrive(&s.freeb()[ct.useq & 1]);
+    mbar_arrive(&s.freeb()[ct.useq % kRB]);
     v *= rs;
     if (!is_x) {
       if (b < B) zo[(size_t)b * E + f] = __float2bfloat16_rn(v);
@@ -466,9 +467,9 @@ __device__ __forceinline__ Ctr epi_units_c(const DsArgs& a, uint8_t* base, int u
   float* const r = a.r;
   for (int u = u0; u < u1; ++u, ++ct.seq, ++ct.useq) {
     const int g8 = u % (D / 8);
-    mbar_wait(&s.ready()[ct.useq & 1], (ct.useq >> 1) & 1);
+    mbar_wait(&s.ready()[ct.useq % kRB], (ct.useq / kRB) & 1);
     const float v = reduce_unit(s, ct.useq, b, n);
-    mbar_arrive(&s.freeb()[ct.useq & 1]);
+    mbar_arrive(&s.freeb()[ct.useq % kRB]);
     if (b < a.B) red_add_f32(r + (size_t)b * D + 8 * g8 + n, v);
   }
   return ct;
@@ -612,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_stack_kernel(const __grid_
       mbar_init(&s.full()[i], 1);
       mbar_init(&s.empty()[i], kMW * 32);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kRB; ++i) {
       mbar_init(&s.ready()[i], kMW * 32);
       mbar_init(&s.freeb()[i], kEW * 32);
     }
@@ -765,7 +766,7 @@ DsGeom ds_geometry(int B, int D, int E, int R, int P, int K, int num_sms) {  // 
   g.nch_max = 8 * gmax;
   auto al = [](int x) { return (x + 127) & ~127; };
   const int sb = al(B * g.nch_max * 64) + al(gmax * (R / 16) * 256) + al(g.nch_max * 64) + al(g.nch_max * 4) * 2;
-  const int red = 2 * kMW * 128 * 4;
+  const int red = kRB * kMW * 128 * 4;
   const int pbB = al(16 * (P + 8) * 4) + al(16 * g.nch_max * 4) + al(g.nch_max * 16 * 4) + 2 * 16 * g.nch_max * 2;
   const int pbA = kMaxXU * P * 16 + kMaxXU * 8 * 4 * 4 + kMaxXU * 8 * 4 + kMaxXU * 16 * 3 * 8 * 2;
   const int pbz = al(pbB > pbA ? pbB : pbA);

@@ -12,6 +12,8 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("DS_PKG_ROOT"):   # same-box A/B of kernel variants (scripts/ab_build.sh)
+    sys.path.insert(0, os.environ["DS_PKG_ROOT"])
 import synth  # noqa: E402
 from paper_2602_21144_b200 import LayerWeights, TPMixer, _lib as L  # noqa: E402
 from paper_2602_21144_b200.stack import MixerStack, synthetic_layer  # noqa: E402
@@ -85,6 +87,15 @@ def main():
     s = t[0, l]
     print("A epi units (CTA 0, layer %d): " % l + "  ".join(
         f"{(s[16 + i] - s[0]) / 1000:.2f}/{(s[24 + i] - s[0]) / 1000:.2f}" for i in range(8) if s[16 + i] > 0))
+    if os.environ.get("DS_FINE"):   # fine stamps inside unit 2 of phase A (a variant built for it)
+        for cc in (0, 50, 100):
+            s = t[cc, 10]
+            print(f"CTA {cc} unit 2: " + "  ".join(f"{k}:{(s[k] - s[16]) / 1000:.2f}" for k in range(16, 23)))
+    if os.environ.get("DS_FINE2"):  # MMA warp 0: unit i wait-start / data-landed (last layer; variant build)
+        for cc in (0, 50, 100):
+            s = t[cc, nl - 1]
+            print(f"CTA {cc} A units (wait/landed, us from layer start): " + "  ".join(
+                f"{(s[16 + i] - s[0]) / 1000:.2f}/{(s[24 + i] - s[0]) / 1000:.2f}" for i in range(8) if s[16 + i] > 0))
     # layer-to-layer: start of layer l+1 - start of layer l, min over CTAs
     st = t[:, :, 0]
     d = (st[:, 3:nl - 1] - st[:, 2:nl - 2]).median(0).values
