@@ -568,6 +568,15 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         reinterpret_cast<float4*>(epi.zero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int64_t i = 4 * n4 + threadIdx.x - 64; i < epi.nzero; i += var_threads(VAR) - 64) epi.zero[i] = 0.f;
     }
+    // VAR 6 (prefill dt_proj): the bias vector staged in shared memory once per CTA, so the epilogue's
+    // per-chunk bias reads are LDS instead of global loads on the drain's critical path (ncu: the
+    // dominant stall of this kernel)
+    float* sbias = reinterpret_cast<float*>(smem + cr.ring + 512);
+    if constexpr (VAR == 6) {
+      if (epi.bias)
+        for (int i = threadIdx.x - 64; i < N; i += var_threads(VAR) - 64) sbias[i] = epi.bias[i];
+      named_bar_sync(1, var_threads(VAR) - 64);
+    }
     if constexpr (VAR == 1) {
       decode_inproj_epilogue<XPN>(epi, ts, M, N, tfull, tempty, tmem_base, cr,
                                   reinterpret_cast<__nv_bfloat16*>(smem + cr.ring + 512));
@@ -603,6 +612,66 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
           if (++acc == 2) { acc = 0; acc_ph ^= 1; }
           continue;
         }
+        if constexpr (VAR == 6) {
+          // dt_proj: the warp drains 64 consecutive columns (chunk pairs 2 half + 4 i, + 1) of its 32 rows,
+          // softplus(+bias) in registers, bf16 rows staged in shared memory (144-B pitch: conflict-free),
+          // then written back as full 128-B row segments (8 lanes per row, 4 rows per store instruction)
+          // instead of 32 rows x 16 B per store (measured: the row-per-lane stores were 140 of 336 us)
+          uint8_t* stg = smem + cr.ring + 512 + ((N * 4 + 127) / 128 * 128) + (warp - 2) * (32 * 144);
+          const int nlim = min(N, nt * BN + BN);  // (an odd chunk count leaves the last pair half empty)
+          for (int cp = 2 * half; cp < (BN + 31) / 32; cp += 4) {
+            const int n0 = nt * BN + cp * 32;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              uint32_t r[32];
+              const int nc = n0 + k * 32;
+              float bb[32];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float4 t4 = (epi.bias && nc + 32 <= N) ? reinterpret_cast<const float4*>(sbias + nc)[q]
+                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                bb[4 * q] = t4.x; bb[4 * q + 1] = t4.y; bb[4 * q + 2] = t4.z; bb[4 * q + 3] = t4.w;
+              }
+              tmem_ld_32x32b_x32(tbase + (cp + k) * 32, r);
+              tmem_ld_wait();
+              uint32_t pk[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                float y[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const float x = __uint_as_float(r[2 * j + h]) + bb[2 * j + h];
+                  const float sp = 0.6931471805599453f * __log2f(1.f + ex2_approx(x * 1.4426950408889634f));
+                  y[h] = x > 20.f ? x : sp;
+                }
+                __nv_bfloat162 t2 = __floats2bfloat162_rn(y[0], y[1]);
+                pk[j] = *reinterpret_cast<uint32_t*>(&t2);
+              }
+              uint4* dst = reinterpret_cast<uint4*>(stg + lane * 144 + k * 64);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int row = it * 4 + (lane >> 3), seg = lane & 7;
+              const int m = m0 + row, n = n0 + seg * 8;
+              const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 144 + seg * 16);
+              if (m < M && n + 8 <= nlim)
+                *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(epi.C) + (int64_t)m * epi.ldc + n) = v;
+              else if (m < M)
+                for (int j = 0; j < 8 && n + j < nlim; ++j)
+                  reinterpret_cast<__nv_bfloat16*>(epi.C)[(int64_t)m * epi.ldc + n + j] =
+                      reinterpret_cast<const __nv_bfloat16*>(&v)[j];
+            }
+            __syncwarp();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+          continue;
+        }
         for (int c = half; c < (BN + 31) / 32; c += 2) {
           uint32_t r[32];
           const int nc = nt * BN + c * 32;
@@ -610,9 +679,10 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
           const bool pre = (VAR == 0 || VAR == 6) && (epi.kind == EPI_SOFTPLUS_BF16 || epi.kind == EPI_SOFTPLUS_F32) &&
                            !epi.trans && nc + 32 <= N && ((reinterpret_cast<uintptr_t>(epi.bias + nc) & 15) == 0);
           if (pre) {
+            const float* bsrc = (VAR == 6 && epi.bias) ? sbias : epi.bias;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const float4 t4 = reinterpret_cast<const float4*>(epi.bias + nc)[q];
+              const float4 t4 = reinterpret_cast<const float4*>(bsrc + nc)[q];
               bpre[4 * q] = t4.x; bpre[4 * q + 1] = t4.y; bpre[4 * q + 2] = t4.z; bpre[4 * q + 3] = t4.w;
             }
           }
@@ -803,6 +873,11 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
         epi.ldc % 16 || (reinterpret_cast<uintptr_t>(epi.C) & 15))
       return cudaErrorInvalidValue;
     extra = 128 * 8 * 4;  // s_am
+    cr.ring -= extra;
+  }
+  if (!epi.trans && epi.kind == EPI_SOFTPLUS_BF16) {  // VAR 6: bias + per-warp row staging in shared memory
+    if (N % 8 || (epi.ldc * 2) % 16 || (reinterpret_cast<uintptr_t>(epi.C) & 15)) return cudaErrorInvalidValue;
+    extra = (N * 4 + 127) / 128 * 128 + 8 * 32 * 144;
     cr.ring -= extra;
   }
   if (epi.zero && (reinterpret_cast<uintptr_t>(epi.zero) & 15)) return cudaErrorInvalidValue;
