@@ -124,77 +124,99 @@ __global__ void __launch_bounds__(CONV_CG) conv1d_silu_kernel(const T* __restric
   }
 }
 
-// bf16 prefill conv, shared-memory staged: a block owns C2_CH channels (4-KB row segments) x C2_TT
-// tokens; all C2_TT + K - 1 input rows (the first K-1 from the cached window when t < 0) are
-// fetched with cp.async at once (~76 KB in flight per block, 2 blocks per SM: the
-// register-pipelined kernel above held 115 registers per thread and ~16 KB in flight per SM),
-// then each thread convolves 8 channels over C2_TT / C2_TL tokens from shared memory and stores
-// 16-B vectors (a warp writes 512 contiguous bytes of a row).
-constexpr int C2_CH = 2048, C2_TT = 16, C2_TL = 1, C2_THREADS = (C2_CH / 8) * C2_TL;
+// bf16 prefill conv v3 (the launched one): persistent blocks, 2 per SM, walk work items (batch row,
+// 1024-channel block, 16-token tile); the (16 + K - 1)-row input tile of the NEXT item is fetched by
+// cp.async while the current one is convolved (double buffer), so each SM keeps ~76 KB in flight
+// continuously instead of in one burst per block (v2: 254 us per Mamba-2.8B layer, 0.4 of HBM).
+// A thread owns 8 channels x 8 tokens of a tile and stores 16-B vectors.
+constexpr int C3_CH = 1024, C3_TT = 16, C3_THREADS = 256;
 template <int K>
-__global__ void __launch_bounds__(C2_THREADS, 2) conv1d_silu_v2_kernel(const __nv_bfloat16* __restrict__ xz, int64_t ldxz,
+__global__ void __launch_bounds__(C3_THREADS, 2) conv1d_silu_v3_kernel(const __nv_bfloat16* __restrict__ xz, int64_t ldxz,
                                                                     const __nv_bfloat16* __restrict__ cst,
                                                                     const float* __restrict__ cw,
                                                                     const float* __restrict__ cb,
                                                                     __nv_bfloat16* __restrict__ u, int64_t ldu, int L,
-                                                                    int Ek) {
+                                                                    int Ek, int batch) {
   pdl_trigger();
   pdl_wait();
-  extern __shared__ __align__(16) __nv_bfloat16 sx_raw[];
-  auto sx = reinterpret_cast<__nv_bfloat16(*)[C2_CH]>(sx_raw);
-  const int c0 = blockIdx.x * C2_CH;
-  const int t0 = blockIdx.y * C2_TT;
-  const int b = blockIdx.z;
-  const int tid = threadIdx.x;
-  constexpr int CPR = C2_CH / 8;  // 16-B chunks per staged row
-  for (int i = tid; i < (C2_TT + K - 1) * CPR; i += C2_THREADS) {
-    const int r = i / CPR, c = (i % CPR) * 8;
-    const int t = t0 - (K - 1) + r;
-    const int ch = c0 + c;
-    const bool ok = t < L && ch < Ek;
-    const __nv_bfloat16* src = t < 0 ? cst + ((int64_t)b * (K - 1) + (K - 1) + t) * Ek + (ok ? ch : 0)
-                                     : xz + ((int64_t)b * L + (ok ? t : 0)) * ldxz + (ok ? ch : 0);
-    cp_async16(&sx[r][c], src, ok);
-  }
-  cp_async_commit();
-  const int cg = tid % CPR, tl = tid / CPR;
-  const int d0 = c0 + cg * 8;
-  float w[K][8], bias[8];
-  if (d0 < Ek) {
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      bias[v] = cb[d0 + v];
-#pragma unroll
-      for (int j = 0; j < K; ++j) w[j][v] = cw[(d0 + v) * K + j];
+  extern __shared__ __align__(16) __nv_bfloat16 sx3_raw[];
+  constexpr int ROWS = C3_TT + K - 1, CPR = C3_CH / 8;
+  auto sx = reinterpret_cast<__nv_bfloat16(*)[ROWS][C3_CH]>(sx3_raw);
+  const int nchb = (Ek + C3_CH - 1) / C3_CH, ntt = (L + C3_TT - 1) / C3_TT;
+  const int items = nchb * ntt * batch;
+  const int tid = threadIdx.x, cg = tid % CPR, tl = tid / CPR;
+  auto coords = [&](int it, int& c0, int& t0, int& b) {
+    t0 = (it % ntt) * C3_TT;
+    const int r = it / ntt;
+    c0 = (r % nchb) * C3_CH;
+    b = r / nchb;
+  };
+  auto load = [&](int buf, int it) {
+    int c0, t0, b;
+    coords(it, c0, t0, b);
+    for (int i = tid; i < ROWS * CPR; i += C3_THREADS) {
+      const int r = i / CPR, c = (i % CPR) * 8;
+      const int t = t0 - (K - 1) + r;
+      const int ch = c0 + c;
+      const bool ok = t < L && ch < Ek;
+      const __nv_bfloat16* src = t < 0 ? cst + ((int64_t)b * (K - 1) + (K - 1) + t) * Ek + (ok ? ch : 0)
+                                       : xz + ((int64_t)b * L + (ok ? t : 0)) * ldxz + (ok ? ch : 0);
+      cp_async16(&sx[buf][r][c], src, ok);
     }
+  };
+  // a contiguous run of items per block (t-tiles fastest): the taps are reloaded only when the
+  // channel block changes
+  const int it0 = (int)((int64_t)items * blockIdx.x / gridDim.x), it1 = (int)((int64_t)items * (blockIdx.x + 1) / gridDim.x);
+  int buf = 0, wc0 = -1;
+  float w[K][8], bias[8];
+  if (it0 < it1) load(0, it0);
+  cp_async_commit();
+  for (int it = it0; it < it1; ++it, buf ^= 1) {
+    if (it + 1 < it1) load(buf ^ 1, it + 1);
+    cp_async_commit();
+    int c0, t0, b;
+    coords(it, c0, t0, b);
+    const int d0 = c0 + cg * 8;
+    if (c0 != wc0 && d0 < Ek) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        bias[v] = cb[d0 + v];
+#pragma unroll
+        for (int j = 0; j < K; ++j) w[j][v] = cw[(d0 + v) * K + j];
+      }
+    }
+    wc0 = c0;
+    cp_async_wait<1>();
+    __syncthreads();
+    if (d0 < Ek) {
+      constexpr int TPT = C3_TT / (C3_THREADS / CPR);  // tokens per thread
+      const int tb = tl * TPT;
+      float win[K][8];
+#pragma unroll
+      for (int j = 0; j < K - 1; ++j) Vec<__nv_bfloat16, 8>::load(&sx[buf][tb + j][cg * 8], win[j + 1]);
+#pragma unroll
+      for (int i = 0; i < TPT; ++i) {
+        const int t = t0 + tb + i;
+        if (t >= L) break;
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) win[j][v] = win[j + 1][v];
+        Vec<__nv_bfloat16, 8>::load(&sx[buf][tb + i + K - 1][cg * 8], win[K - 1]);
+        float o[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          float acc = bias[v];
+#pragma unroll
+          for (int j = 0; j < K; ++j) acc = fmaf(w[j][v], win[j][v], acc);
+          o[v] = silu_tanh(acc);
+        }
+        Vec<__nv_bfloat16, 8>::store(u + ((int64_t)b * L + t) * ldu + d0, o);
+      }
+    }
+    __syncthreads();  // this buffer is refilled by the load issued in the next iteration
   }
   cp_async_wait<0>();
-  __syncthreads();
-  if (d0 >= Ek) return;
-  constexpr int TPT = C2_TT / C2_TL;  // consecutive tokens per thread
-  const int tb = tl * TPT;
-  float win[K][8];
-#pragma unroll
-  for (int j = 0; j < K - 1; ++j) Vec<__nv_bfloat16, 8>::load(&sx[tb + j][cg * 8], win[j + 1]);
-#pragma unroll
-  for (int i = 0; i < TPT; ++i) {
-    const int t = t0 + tb + i;
-    if (t >= L) break;
-#pragma unroll
-    for (int j = 0; j < K - 1; ++j)
-#pragma unroll
-      for (int v = 0; v < 8; ++v) win[j][v] = win[j + 1][v];
-    Vec<__nv_bfloat16, 8>::load(&sx[tb + i + K - 1][cg * 8], win[K - 1]);
-    float o[8];
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      float acc = bias[v];
-#pragma unroll
-      for (int j = 0; j < K; ++j) acc = fmaf(w[j][v], win[j][v], acc);
-      o[v] = silu_tanh(acc);
-    }
-    Vec<__nv_bfloat16, 8>::store(u + ((int64_t)b * L + t) * ldu + d0, o);
-  }
 }
 
 // conv window after the chunk: last K-1 entries of xt = conv_state || x
@@ -841,26 +863,33 @@ template <typename T, bool F>
 cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const float* cw, const float* cb, void* u,
                           int64_t ldu, int batch, int L, int Ek, int K, cudaStream_t s) {
   if constexpr (sizeof(T) == 2 && F) {
-    if (Ek % 8 == 0 && ldxz % 8 == 0 && ldu % 8 == 0) {  // smem-staged kernel (bf16)
-      dim3 grid2((Ek + C2_CH - 1) / C2_CH, (L + C2_TT - 1) / C2_TT, batch);
+    if (Ek % 8 == 0 && ldxz % 8 == 0 && ldu % 8 == 0) {  // persistent smem-pipelined kernel (bf16)
       const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(xz);
       const __nv_bfloat16* c = reinterpret_cast<const __nv_bfloat16*>(cs);
       __nv_bfloat16* uu = reinterpret_cast<__nv_bfloat16*>(u);
-      cudaError_t e_ = cudaSuccess;
-      const size_t sm = (size_t)(C2_TT + K - 1) * C2_CH * 2;
-      static bool attr[5] = {false, false, false, false, false};
-      const void* fn = K == 2 ? (const void*)conv1d_silu_v2_kernel<2> : K == 3 ? (const void*)conv1d_silu_v2_kernel<3>
-                                                                             : (const void*)conv1d_silu_v2_kernel<4>;
       if (K < 2 || K > 4) return cudaErrorInvalidValue;
+      const size_t sm = (size_t)2 * (C3_TT + K - 1) * C3_CH * 2;
+      static bool attr[5] = {false, false, false, false, false};
+      const void* fn = K == 2 ? (const void*)conv1d_silu_v3_kernel<2> : K == 3 ? (const void*)conv1d_silu_v3_kernel<3>
+                                                                             : (const void*)conv1d_silu_v3_kernel<4>;
+      cudaError_t e_ = cudaSuccess;
       if (!attr[K]) {
         e_ = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e_ != cudaSuccess) return e_;
         attr[K] = true;
       }
+      static int sms = 0;
+      if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      }
+      const int items = ((Ek + C3_CH - 1) / C3_CH) * ((L + C3_TT - 1) / C3_TT) * batch;
+      const int grid3 = items < 2 * sms ? items : 2 * sms;
       switch (K) {
-        case 2: e_ = launch(conv1d_silu_v2_kernel<2>, grid2, C2_THREADS, sm, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek); break;
-        case 3: e_ = launch(conv1d_silu_v2_kernel<3>, grid2, C2_THREADS, sm, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek); break;
-        default: e_ = launch(conv1d_silu_v2_kernel<4>, grid2, C2_THREADS, sm, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek); break;
+        case 2: e_ = launch(conv1d_silu_v3_kernel<2>, grid3, C3_THREADS, sm, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek, batch); break;
+        case 3: e_ = launch(conv1d_silu_v3_kernel<3>, grid3, C3_THREADS, sm, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek, batch); break;
+        default: e_ = launch(conv1d_silu_v3_kernel<4>, grid3, C3_THREADS, sm, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek, batch); break;
       }
       if (e_ != cudaSuccess) return e_;
       return cudaGetLastError();
@@ -1141,7 +1170,7 @@ cudaError_t preload_kernels() {
       (const void*)scan_kernel<__nv_bfloat16, 16, true>, (const void*)scan_kernel<__nv_bfloat16, 16, false>,
       (const void*)scan_kernel<__nv_bfloat16, 8, true>, (const void*)scan_kernel<__nv_bfloat16, 8, false>,
       (const void*)scan_kernel<float, 16, false>, (const void*)scan_kernel<float, 8, false>,
-      (const void*)conv1d_silu_v2_kernel<2>, (const void*)conv1d_silu_v2_kernel<3>, (const void*)conv1d_silu_v2_kernel<4>,
+      (const void*)conv1d_silu_v3_kernel<2>, (const void*)conv1d_silu_v3_kernel<3>, (const void*)conv1d_silu_v3_kernel<4>,
       (const void*)decode_step_kernel<__nv_bfloat16, 16, true>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true>,
       (const void*)decode_step_kernel<float, 16, false>, (const void*)decode_step_kernel<float, 8, false>,
       (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>,
