@@ -49,6 +49,7 @@ constexpr int kMaxCC = 4;                   // phase C: chunks per MMA warp per 
 constexpr int kMaxPT = 8;                   // x_proj 8-wide p tiles per epilogue warp (P <= 256)
 constexpr int kMaxXU = 5;                   // in_proj x units (8 channels) per CTA
 constexpr int kRB = 4;                      // reduction buffers: the MMA warps run up to 3 units ahead
+constexpr int kL2AheadIdle = 8;             // ... and while the ring is full (8 / 12 / 16 measured equal)
 constexpr int kL2Ahead = 3;                 // ring units prefetched into L2 ahead of the ring
 
 SSM_DEV void mma_1688_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
@@ -210,7 +211,13 @@ __device__ __forceinline__ void pump_run(const DsArgs& a, const Smem& s, Pump* p
   while (p.seq < p.total) {
     const int sz = pump_size(p, p.seq);
     while (p.seq - p.oldest >= kSlots || p.issued + sz - p.released > a.ring_bytes) {
-      mbar_wait(&s.empty()[p.oldest % kSlots], (p.oldest / kSlots) & 1);
+      // the ring is full, so the consumers are in a latency-bound step (scan step, barrier, phase start)
+      // and HBM is idle: prefetch deeper into L2 while waiting
+      while (!mbar_try_wait(&s.empty()[p.oldest % kSlots], (p.oldest / kSlots) & 1))
+        if (p.pf < p.total && p.pf < p.seq + 1 + kL2AheadIdle) {
+          prefetch_l2(pump_src(a, p, p.pf), (uint32_t)pump_size(p, p.pf));
+          ++p.pf;
+        }
       p.released += pump_size(p, p.oldest);
       ++p.oldest;
     }

@@ -96,6 +96,15 @@ def main():
             s = t[cc, nl - 1]
             print(f"CTA {cc} A units (wait/landed, us from layer start): " + "  ".join(
                 f"{(s[16 + i] - s[0]) / 1000:.2f}/{(s[24 + i] - s[0]) / 1000:.2f}" for i in range(8) if s[16 + i] > 0))
+    if os.environ.get("DS_FINE3"):  # MMA warps 0 / kMW-1, units 0-3 of phase A: wait-full, mma, wait-free (ns)
+        for cc in (0, 70, 140):
+            s = tr.view(nc, nl, 32)[cc, nl - 1].cpu()
+            parts = []
+            for w in (0, 1):
+                for i in range(4):
+                    v0, v1 = int(s[16 + 8 * w + 2 * i]), int(s[17 + 8 * w + 2 * i])
+                    parts.append(f"w{w}u{i}:{(v0 >> 32)}/{v0 & 0xffffffff}/{v1}")
+            print(f"CTA {cc}: " + " ".join(parts))
     # layer-to-layer: start of layer l+1 - start of layer l, min over CTAs
     st = t[:, :, 0]
     d = (st[:, 3:nl - 1] - st[:, 2:nl - 2]).median(0).values
