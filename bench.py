@@ -34,7 +34,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="mamba2.8b",
-                   choices=["mamba2.8b", "falcon7b", "zamba7b", "mamba2.8b-long", "mamba2-2.7b"])
+                   choices=["mamba2.8b", "falcon7b", "zamba7b", "mamba2.8b-long", "mamba2-2.7b", "tiny"],
+                   help="tiny = BASELINE configs[0] (one fp32 layer, D 64, batch 2, 64 + 16): latency of the fp32 mode")
     p.add_argument("--ar2", default="int8", choices=["int8", "int8-requant", "fp16", "bf16", "fp32", "nccl"],
                    help="AR#2: int8 / fp16 / bf16 / fp32 peer-to-peer (library), or nccl = NCCL bf16 all-reduce "
                         "baseline arm")
@@ -228,6 +229,7 @@ def main():
     import synth
     mamba2 = args.config == "mamba2-2.7b"   # Mamba-2 (SSD) stack, SURVEY.md §8(f) NEXT-4 (not a BASELINE config)
     dims = synth.CONFIGS["mamba2.8b" if args.config in ("mamba2.8b-long", "mamba2-2.7b") else args.config]
+    cdt = "fp32" if args.config == "tiny" else "bf16"   # BASELINE configs[0] is the fp32 mode
     wl = dict(synth.WORKLOADS["mamba2.8b" if mamba2 else args.config])
     n_layers = args.layers or dims.n_layers
     if args.prompt:
@@ -269,7 +271,7 @@ def main():
     peer_bufs, nbytes, symm = None, 0, None
     if k > 1:
         import torch.distributed._symmetric_memory as symm_mem
-        cfg = L.make_config(dims, "bf16")
+        cfg = L.make_config(dims, cdt)
         nbytes = L.comm_bytes(cfg, k, B * chunk)
         buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=dev)
         buf.zero_()
@@ -277,16 +279,16 @@ def main():
         peer_bufs = [int(p) for p in hdl.buffer_ptrs]
         symm = (buf, hdl)
         dist.barrier()
-    mx = TPMixer(dims, "bf16", rank=rank, tp_size=k, peer_bufs=peer_bufs, buf_bytes=nbytes, device=dev)
+    mx = TPMixer(dims, cdt, rank=rank, tp_size=k, peer_bufs=peer_bufs, buf_bytes=nbytes, device=dev)
     want_persistent = (args.decode_impl != "layer" and k == 1 and not mamba2 and args.config != "zamba7b"
-                       and wl["batch"] <= 16)
+                       and wl["batch"] <= 16 and cdt == "bf16")
     if args.decode_impl == "persistent" and not want_persistent:
         raise SystemExit("bench.py: --decode-impl persistent needs TP = 1, a pure Mamba stack and batch <= 16")
     layers = []
     for l in range(0 if mamba2 else n_layers):
         full = synthetic_layer(dims, l, device=dev)
-        lw = LayerWeights(dims, full, k, rank, "bf16", dev, naive=naive)
-        if not args.no_pack and not want_persistent:
+        lw = LayerWeights(dims, full, k, rank, cdt, dev, naive=naive)
+        if not args.no_pack and not want_persistent and cdt == "bf16":
             lw.pack(mx)  # pre-tiled copies of w_in / w_x / w_out for the decode weight streams
         layers.append(lw)
         del full
@@ -478,7 +480,8 @@ def main():
         avg = statistics.mean(dec_ms_launch)
         fused = stack.mx.fused_calls() > 0
         P = dims.dt_rank + 2 * dims.d_state
-        byts = 2 * Ek * D * 2 + B * D * 2 + B * 2 * Ek * 2  # weights + x_in + xz (bf16)
+        es_ = 4 if cdt == "fp32" else 2
+        byts = 2 * Ek * D * es_ + B * D * es_ + B * 2 * Ek * es_  # weights + x_in + xz
         if fused:  # + conv window read/write, conv taps, W_x, x_proj accumulator read/write
             byts += 2 * B * (dims.d_conv - 1) * Ek * 2 + Ek * (dims.d_conv + 1) * 4 + P * Ek * 2 + 2 * B * P * 4
         peak = peaks.get("hbm_gbs", 6535.1)
@@ -520,7 +523,7 @@ def main():
     if rank == 0:
         line = {"metric": "batch tokens/sec", "value": value, "unit": "tokens/s", "n_gpus": k, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "vs_baseline": None, "dtype": "f32" if cdt == "fp32" else "bf16", "data": "synthetic",
                 "config": {"workload": f"{args.config}: {n_layers} layers"
                                        + (f" ({len(stack.hybrid)} hybrid: shared attention + MLP block first)"
                                           if getattr(stack, "hybrid", None) else "")
