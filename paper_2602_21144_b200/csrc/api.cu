@@ -1152,10 +1152,25 @@ ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ss
   int* err = len + 1;
   __nv_bfloat16* Kc = reinterpret_cast<__nv_bfloat16*>(kv->buf + 256);
   __nv_bfloat16* Vc = reinterpret_cast<__nv_bfloat16*>(kv->buf + 256 + al256((size_t)batch * kv->max_seq * QW * 2));
+  // Projections: out[M][N] = X[M][K] W[N][K]^T.  Decode-size calls (M <= 32 tokens) stream the weights
+  // through the swap-AB GEMM (weights fill the 128-row MMA tile, the tokens are N; fp32 outputs split
+  // over K with atomics into the zeroed output): with the tokens as the 128-row tile a [16 x 3712]
+  // output ran on 15 CTAs (0.5 TB/s).
+  const bool dec = M <= 32 && tp->bf16;
+  auto proj = [&](const void* X, int ldx, const void* Wt, int ldw, int N, int K, int kind, void* out) -> cudaError_t {
+    if (!dec) return gemm(tp, X, ldx, Wt, ldw, (int)M, N, K, 1, epi(kind, 0, out, N), s);
+    if (kind == EPI_STORE_F32) {
+      tp->launches++;
+      cudaError_t e = cudaMemsetAsync(out, 0, (size_t)M * N * 4, s);
+      if (e != cudaSuccess) return e;
+      return gemm(tp, Wt, ldw, X, ldx, N, (int)M, K, split_for(tp, N, K), epi(EPI_ATOMIC_F32, 1, out, N), s, true);
+    }
+    return gemm(tp, Wt, ldw, X, ldx, N, (int)M, K, 1, epi(kind, 1, out, N), s, true);
+  };
   // x = RMSNorm_1(concat(h, h0)); q | k | v of the owned heads
   tp->launches++;
   CU(launch_rmsnorm2(h, h0, 0, w->norm1, acfg->eps, bf(L.xa), M, D, s));
-  CU(gemm(tp, bf(L.xa), A2, w->w_qkv, A2, (int)M, 3 * QW, A2, 1, epi(EPI_STORE_BF16, 0, bf(L.qkv), 3 * QW), s));
+  CU(proj(bf(L.xa), A2, w->w_qkv, A2, 3 * QW, A2, EPI_STORE_BF16, bf(L.qkv)));
   // K, V appended to the cache; causal attention over it; the cache length advanced
   tp->launches += 3;
   CU(launch_kv_append(bf(L.qkv), len, batch, seqlen, z.hk, z.d, kv->max_seq, Kc, Vc, err, s));
@@ -1172,7 +1187,7 @@ ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ss
   }
   // a = o W_o^T (row-parallel partial), all-reduced at TP > 1
   float* a = reinterpret_cast<float*>(W + L.a);
-  CU(gemm(tp, bf(L.o), QW, w->w_o, QW, (int)M, D, QW, 1, epi(EPI_STORE_F32, 0, a, D), s));
+  CU(proj(bf(L.o), QW, w->w_o, QW, D, QW, EPI_STORE_F32, a));
   if (tp->k > 1) {
     ssm_status_t r = ssm_qallreduce(tp, a, a, (size_t)M * D, attn_ar_flags(flags), stream);
     if (r != SSM_OK) return r;
@@ -1180,10 +1195,10 @@ ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ss
   // y = RMSNorm_2(a); m = GELU(y W_g^T) * (y W_u^T); d = m W_d^T (partial), all-reduced
   tp->launches += 2;
   CU(launch_rmsnorm2(a, nullptr, 1, w->norm2, acfg->eps, bf(L.y), M, D, s));
-  CU(gemm(tp, bf(L.y), D, w->w_gu, D, (int)M, 2 * z.ik, D, 1, epi(EPI_STORE_BF16, 0, bf(L.gu), 2 * z.ik), s));
+  CU(proj(bf(L.y), D, w->w_gu, D, 2 * z.ik, D, EPI_STORE_BF16, bf(L.gu)));
   CU(launch_gelu_mul(bf(L.gu), M, z.ik, bf(L.m), s));
   float* dd = reinterpret_cast<float*>(W + L.dd);
-  CU(gemm(tp, bf(L.m), z.ik, w->w_d, z.ik, (int)M, D, z.ik, 1, epi(EPI_STORE_F32, 0, dd, D), s));
+  CU(proj(bf(L.m), z.ik, w->w_d, z.ik, D, z.ik, EPI_STORE_F32, dd));
   if (tp->k > 1) {
     ssm_status_t r = ssm_qallreduce(tp, dd, dd, (size_t)M * D, attn_ar_flags(flags), stream);
     if (r != SSM_OK) return r;
@@ -1191,7 +1206,7 @@ ssm_status_t ssm_attn_block(ssm_tp_t tp, const ssm_attn_config_t* acfg, const ss
   // t = m W_lin^T (replicated)
   tp->launches++;
   CU(launch_cast_bf16(dd, M * D, bf(L.mb), s));
-  CU(gemm(tp, bf(L.mb), D, w->w_lin, D, (int)M, D, D, 1, epi(EPI_STORE_F32, 0, t_out, D), s));
+  CU(proj(bf(L.mb), D, w->w_lin, D, D, D, EPI_STORE_F32, t_out));
   return SSM_OK;
 }
 
