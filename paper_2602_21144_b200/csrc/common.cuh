@@ -222,6 +222,12 @@ SSM_DEV void ldmatrix_x2_trans(uint32_t (&r)[2], const void* row_addr) {
                : "=r"(r[0]), "=r"(r[1])
                : "r"(smem_u32(row_addr)));
 }
+// Four 8x8 b16 matrices, transposed.
+SSM_DEV void ldmatrix_x4_trans(uint32_t (&r)[4], const void* row_addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(row_addr)));
+}
 // D[16x8] += A[16x16] (row) * B[16x8] (col), bf16 inputs, fp32 accumulate.
 SSM_DEV void mma_16816_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(

@@ -6,7 +6,8 @@
 //                   y[p] = C.h + D x[p]; one CTA per (head, sequence), 256 threads = 64 head
 //                   channels x 4 contiguous quarters of the 128 states (32 fp32 states in
 //                   registers per thread), token tiles of x, B, C, dt staged by cp.async;
-//                   m2_scan_step: the L = 1 decode step as a coalesced stream over the state rows
+//                   m2_scan_step: the L = 1 decode step as a coalesced stream over the state rows;
+//                   m2_ssd_chunk: calls of >= 16 tokens in the chunked SSD (matmul) form
 //   m2_gate_ss      g = y SiLU(z) (fp32, in place) and the row's sum of squares (all-reduced
 //                   over the ranks by the caller at TP > 1: the gated RMSNorm spans d_inner)
 //   m2_norm_apply   o = g / sqrt(ss / E + eps) * w (bf16), the out_proj's input
@@ -19,6 +20,9 @@ namespace ssm {
 namespace {
 
 constexpr int M2_P = 64, M2_Q = 4, M2_THREADS = M2_P * M2_Q, M2_TT = 16, M2_NMAX = 128;
+// multi-token calls at least this long take the chunked SSD form (m2_ssd_chunk); shorter ones (and
+// d_state 16) the per-token recurrence (m2_scan)
+constexpr int kSsdChunkMinL = 16;
 
 // proj [M][ldp] bf16: dt raw at column dt_col + h; u [M][ldu] bf16: x at x_col + h P, B at b_col,
 // C at c_col (group g of the head: + g N).  h_state [batch][Hk][P][N] fp32 in place; y [M][Ek] fp32.
@@ -158,6 +162,258 @@ __global__ void __launch_bounds__(256) m2_scan_step_kernel(
   if (sub == 0) y[b * ldy + (int64_t)h * M2_P + p] = fmaf(Dh, xv, acc);
 }
 
+// ---------------------------------------------------------------------------------------------
+// The multi-token scan in Mamba-2's chunked SSD form (the "chunked matmul" of PAPER.md:367 /
+// SURVEY.md §8 NEXT-4): the sequence is cut into chunks of Q = 64 tokens; with a_s = dt_s A and the
+// in-chunk cumulative sum A_t = sum_{s<=t} a_s, the recurrence h_t = exp(a_t) h_{t-1} + dt_t x_t B_t^T,
+// y_t = h_t C_t unrolls exactly (up to rounding) into
+//   y_t   = exp(A_t) C_t h_prev^T + sum_{s<=t} (C_t . B_s) exp(A_t - A_s) dt_s x_s        (output)
+//   h_end = exp(A_Q) h_prev + sum_s exp(A_Q - A_s) dt_s x_s B_s^T                       (carry)
+// i.e. four small dense contractions per (chunk, head): G = C B^T (Q x Q x N), Y += (G o decay) X
+// (Q x P x Q), Y = C h^T (Q x P x N), h += X^T diag(w) B (P x N x Q).  One CTA per (head, sequence)
+// walks its chunks in order with h (P x N fp32) in the MMA warps' accumulator registers; the
+// contractions are warp-level bf16 mma.sync (fp32 accumulate) from ldmatrix'd shared-memory tiles:
+// the four products are chained through per-element decay masks in registers, 64-wide, too small
+// for a tcgen05 tile pipeline to amortise its TMEM round trips.  8 warps = 4 row blocks x 2 column
+// halves; 108 KB of shared memory (double-buffered x/B/C chunk tiles by cp.async, XOR-swizzled
+// rows), 2 CTAs per SM.  Rounding: G o decay, x w and h enter the MMAs in bf16 (h stays fp32).
+constexpr int SQ = 64;   // chunk length
+
+// element offset of (row, col) in a [rows][W] bf16 tile whose 16-B chunks are XOR-swizzled by row
+SSM_DEV int swz(int row, int col, int W) { return row * W + ((((col >> 3) ^ (row & 7))) << 3) + (col & 7); }
+
+SSM_DEV uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+SSM_DEV uint32_t scale_bf16x2(uint32_t v, float a, float b) {
+  __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&v);
+  return pack_bf16(__low2float(x) * a, __high2float(x) * b);
+}
+
+template <int N>
+constexpr size_t ssd_smem_bytes() {
+  return (size_t)2 * SQ * M2_P * 2 + (size_t)4 * SQ * N * 2 + (size_t)SQ * SQ * 2 + (size_t)M2_P * N * 2 + 6 * SQ * 4;
+}
+
+template <int N>
+__global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
+    const __nv_bfloat16* __restrict__ proj, int64_t ldp, int dt_col, const __nv_bfloat16* __restrict__ u,
+    int64_t ldu, int b_col, int c_col, int heads_per_group, const float* __restrict__ dt_bias,
+    const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ hstate,
+    float* __restrict__ y, int64_t ldy, int L, int Hk) {
+  static_assert(N == 64 || N == 128, "chunked SSD: d_state 64 or 128");
+  constexpr int KS = N / 16;  // k-steps over the state dimension (G, C h^T)
+  constexpr int HT = N / 16;  // 8-wide n-tiles per warp in the carry update (N / 2 columns)
+  extern __shared__ __align__(128) unsigned char ssd_smem[];
+  __nv_bfloat16* sX = reinterpret_cast<__nv_bfloat16*>(ssd_smem);  // [2][SQ][P]
+  __nv_bfloat16* sB = sX + 2 * SQ * M2_P;                           // [2][SQ][N]
+  __nv_bfloat16* sC = sB + 2 * SQ * N;                              // [2][SQ][N]
+  __nv_bfloat16* sM = sC + 2 * SQ * N;                              // [SQ][SQ]  (G o decay)
+  __nv_bfloat16* sH = sM + SQ * SQ;                                 // [P][N]    h_prev (bf16 copy)
+  float* sdt = reinterpret_cast<float*>(sH + M2_P * N);             // [2][SQ]
+  float* sAc = sdt + 2 * SQ;                                        // [2][SQ]   log2-scaled A_t
+  float* sW = sAc + 2 * SQ;                                         // [2][SQ]   exp(A_Q - A_s) dt_s
+  pdl_trigger();
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rb = warp & 3, hf = warp >> 2, gq = lane >> 2, cq = lane & 3;
+  const int g = h / heads_per_group;
+  const int64_t row0 = (int64_t)b * L;
+  const float A = -expf(a_log[h]) * 1.4426950408889634f;
+  const float bias = dt_bias[h], Dh = d_skip[h];
+  pdl_wait();
+
+  // carry h: warp (rb, hf) owns rows p in [16 rb, 16 rb + 16), columns n in [N/2 hf, N/2 hf + N/2)
+  float hacc[HT][4];
+  float* hbase = hstate + ((int64_t)b * Hk + h) * M2_P * N;
+  const int hp0 = rb * 16 + gq, hn0 = hf * (N / 2) + 2 * cq;
+#pragma unroll
+  for (int nt = 0; nt < HT; ++nt) {
+    const float2 v0 = *reinterpret_cast<const float2*>(hbase + (int64_t)hp0 * N + hn0 + nt * 8);
+    const float2 v1 = *reinterpret_cast<const float2*>(hbase + (int64_t)(hp0 + 8) * N + hn0 + nt * 8);
+    hacc[nt][0] = v0.x; hacc[nt][1] = v0.y; hacc[nt][2] = v1.x; hacc[nt][3] = v1.y;
+  }
+  auto store_h = [&]() {
+#pragma unroll
+    for (int nt = 0; nt < HT; ++nt) {
+      *reinterpret_cast<uint32_t*>(sH + swz(hp0, hn0 + nt * 8, N)) = pack_bf16(hacc[nt][0], hacc[nt][1]);
+      *reinterpret_cast<uint32_t*>(sH + swz(hp0 + 8, hn0 + nt * 8, N)) = pack_bf16(hacc[nt][2], hacc[nt][3]);
+    }
+  };
+  auto load_tile = [&](int buf, int t0) {
+    constexpr int XC = M2_P / 8, BC = N / 8, RC = XC + 2 * BC;
+    for (int i = tid; i < SQ * RC; i += 256) {
+      const int r = i / RC, c = i % RC;
+      const bool ok = t0 + r < L;
+      const int64_t row = row0 + (ok ? t0 + r : 0);
+      const __nv_bfloat16* urow = u + row * ldu;
+      if (c < XC) cp_async16(sX + buf * SQ * M2_P + swz(r, c * 8, M2_P), urow + (int64_t)h * M2_P + c * 8, ok);
+      else if (c < XC + BC) cp_async16(sB + buf * SQ * N + swz(r, (c - XC) * 8, N), urow + b_col + (int64_t)g * N + (c - XC) * 8, ok);
+      else cp_async16(sC + buf * SQ * N + swz(r, (c - XC - BC) * 8, N), urow + c_col + (int64_t)g * N + (c - XC - BC) * 8, ok);
+    }
+  };
+  // dt of the chunk at t0 (threads 0..63 each hold one raw value; padded tokens give dt = 0)
+  auto load_dt = [&](int t0) -> float {
+    const int t = t0 + tid;
+    return (tid < SQ && t < L) ? __bfloat162float(proj[(row0 + t) * ldp + dt_col + h]) : -INFINITY;
+  };
+  auto put_dt = [&](int buf, float raw) {
+    if (tid < SQ) sdt[buf * SQ + tid] = raw == -INFINITY ? 0.f : softplus(raw + bias);
+  };
+  // warp 0: inclusive cumsum of a_s = dt_s A (2 tokens per lane) and w_s = exp(A_Q - A_s) dt_s
+  auto scan = [&](int buf) {
+    const float d0 = sdt[buf * SQ + 2 * lane], d1 = sdt[buf * SQ + 2 * lane + 1];
+    const float a0 = d0 * A, a1 = d1 * A;
+    float x = a0 + a1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float v = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += v;
+    }
+    const float c1 = x, c0 = x - a1;
+    const float tot = __shfl_sync(0xffffffffu, x, 31);
+    sAc[buf * SQ + 2 * lane] = c0;
+    sAc[buf * SQ + 2 * lane + 1] = c1;
+    sW[buf * SQ + 2 * lane] = ex2_approx(tot - c0) * d0;
+    sW[buf * SQ + 2 * lane + 1] = ex2_approx(tot - c1) * d1;
+  };
+
+  const int nch = (L + SQ - 1) / SQ;
+  load_tile(0, 0);
+  cp_async_commit();
+  put_dt(0, load_dt(0));
+  store_h();
+  __syncthreads();
+  if (warp == 0) scan(0);
+  for (int ch = 0; ch < nch; ++ch) {
+    const int buf = ch & 1, t0 = ch * SQ;
+    cp_async_wait<0>();
+    __syncthreads();  // chunk tiles, sAc / sW [buf] and sH visible; chunk ch-1's readers are done
+    float dt_next = -INFINITY;
+    if (ch + 1 < nch) {
+      load_tile(buf ^ 1, t0 + SQ);
+      cp_async_commit();
+      dt_next = load_dt(t0 + SQ);
+    }
+    const __nv_bfloat16* Xb = sX + buf * SQ * M2_P;
+    const __nv_bfloat16* Bb = sB + buf * SQ * N;
+    const __nv_bfloat16* Cb = sC + buf * SQ * N;
+    const float* Ac = sAc + buf * SQ;
+    const int t_a = rb * 16 + gq;  // this lane's accumulator rows t_a, t_a + 8
+    const float At0 = Ac[t_a], At1 = Ac[t_a + 8];
+    // C fragments of rows [16 rb, 16 rb + 16), shared by G and C h^T
+    uint32_t cf[KS][4];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+      ldmatrix_x4(cf[ks], Cb + swz(rb * 16 + (lane & 7) + 8 * ((lane >> 3) & 1), ks * 16 + 8 * (lane >> 4), N));
+    {  // G = C B^T on columns s in [32 hf, 32 hf + 32) -> sM = G o (s <= t) exp(A_t - A_s) dt_s
+      float gacc[4][4] = {};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
+          uint32_t bf[4];
+          ldmatrix_x4(bf, Bb + swz(hf * 32 + np * 16 + (lane & 7) + 8 * (lane >> 4), ks * 16 + 8 * ((lane >> 3) & 1), N));
+          mma_16816_bf16(gacc[2 * np], cf[ks], bf[0], bf[1]);
+          mma_16816_bf16(gacc[2 * np + 1], cf[ks], bf[2], bf[3]);
+        }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int s = hf * 32 + nt * 8 + 2 * cq;
+        const float As0 = Ac[s], As1 = Ac[s + 1];
+        const float ds0 = sdt[buf * SQ + s], ds1 = sdt[buf * SQ + s + 1];
+        const float m00 = s <= t_a ? gacc[nt][0] * ex2_approx(At0 - As0) * ds0 : 0.f;
+        const float m01 = s + 1 <= t_a ? gacc[nt][1] * ex2_approx(At0 - As1) * ds1 : 0.f;
+        const float m10 = s <= t_a + 8 ? gacc[nt][2] * ex2_approx(At1 - As0) * ds0 : 0.f;
+        const float m11 = s + 1 <= t_a + 8 ? gacc[nt][3] * ex2_approx(At1 - As1) * ds1 : 0.f;
+        *reinterpret_cast<uint32_t*>(sM + swz(t_a, s, SQ)) = pack_bf16(m00, m01);
+        *reinterpret_cast<uint32_t*>(sM + swz(t_a + 8, s, SQ)) = pack_bf16(m10, m11);
+      }
+    }
+    // Y = exp(A_t) C h_prev^T on columns p in [32 hf, 32 hf + 32)
+    float yacc[4][4] = {};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int np = 0; np < 2; ++np) {
+        uint32_t bf[4];
+        ldmatrix_x4(bf, sH + swz(hf * 32 + np * 16 + (lane & 7) + 8 * (lane >> 4), ks * 16 + 8 * ((lane >> 3) & 1), N));
+        mma_16816_bf16(yacc[2 * np], cf[ks], bf[0], bf[1]);
+        mma_16816_bf16(yacc[2 * np + 1], cf[ks], bf[2], bf[3]);
+      }
+    {
+      const float e0 = ex2_approx(At0), e1 = ex2_approx(At1);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        yacc[nt][0] *= e0; yacc[nt][1] *= e0; yacc[nt][2] *= e1; yacc[nt][3] *= e1;
+      }
+    }
+    if (ch + 1 < nch) put_dt(buf ^ 1, dt_next);
+    __syncthreads();  // sM complete; every warp is done reading sH
+    // Y += (G o decay) X
+#pragma unroll
+    for (int ks = 0; ks < SQ / 16; ++ks) {
+      uint32_t af[4];
+      ldmatrix_x4(af, sM + swz(rb * 16 + (lane & 7) + 8 * ((lane >> 3) & 1), ks * 16 + 8 * (lane >> 4), SQ));
+#pragma unroll
+      for (int np = 0; np < 2; ++np) {
+        uint32_t bf[4];
+        ldmatrix_x4_trans(bf, Xb + swz(ks * 16 + (lane & 7) + 8 * ((lane >> 3) & 1), hf * 32 + np * 16 + 8 * (lane >> 4), M2_P));
+        mma_16816_bf16(yacc[2 * np], af, bf[0], bf[1]);
+        mma_16816_bf16(yacc[2 * np + 1], af, bf[2], bf[3]);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int pc = hf * 32 + nt * 8 + 2 * cq;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int t = t_a + 8 * hh;
+        if (t0 + t < L) {
+          const __nv_bfloat162 xv = *reinterpret_cast<const __nv_bfloat162*>(Xb + swz(t, pc, M2_P));
+          *reinterpret_cast<float2*>(y + (row0 + t0 + t) * ldy + (int64_t)h * M2_P + pc) =
+              make_float2(fmaf(Dh, __low2float(xv), yacc[nt][2 * hh]), fmaf(Dh, __high2float(xv), yacc[nt][2 * hh + 1]));
+        }
+      }
+    }
+    // carry: h = exp(A_Q) h + X^T diag(w) B on this warp's (p, n) block
+    {
+      const float* Wb = sW + buf * SQ;
+      const float dq = ex2_approx(Ac[SQ - 1]);
+#pragma unroll
+      for (int nt = 0; nt < HT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hacc[nt][i] *= dq;
+#pragma unroll
+      for (int ks = 0; ks < SQ / 16; ++ks) {
+        uint32_t af[4];
+        ldmatrix_x4_trans(af, Xb + swz(ks * 16 + (lane & 7) + 8 * (lane >> 4), rb * 16 + 8 * ((lane >> 3) & 1), M2_P));
+        const int s0 = ks * 16 + 2 * cq;
+        const float w0 = Wb[s0], w1 = Wb[s0 + 1], w8 = Wb[s0 + 8], w9 = Wb[s0 + 9];
+        af[0] = scale_bf16x2(af[0], w0, w1);
+        af[1] = scale_bf16x2(af[1], w0, w1);
+        af[2] = scale_bf16x2(af[2], w8, w9);
+        af[3] = scale_bf16x2(af[3], w8, w9);
+#pragma unroll
+        for (int np = 0; np < HT / 2; ++np) {
+          uint32_t bf[4];
+          ldmatrix_x4_trans(bf, Bb + swz(ks * 16 + (lane & 7) + 8 * ((lane >> 3) & 1), hf * (N / 2) + np * 16 + 8 * (lane >> 4), N));
+          mma_16816_bf16(hacc[2 * np], af, bf[0], bf[1]);
+          mma_16816_bf16(hacc[2 * np + 1], af, bf[2], bf[3]);
+        }
+      }
+    }
+    store_h();
+    if (warp == 0 && ch + 1 < nch) scan(buf ^ 1);
+  }
+#pragma unroll
+  for (int nt = 0; nt < HT; ++nt) {
+    *reinterpret_cast<float2*>(hbase + (int64_t)hp0 * N + hn0 + nt * 8) = make_float2(hacc[nt][0], hacc[nt][1]);
+    *reinterpret_cast<float2*>(hbase + (int64_t)(hp0 + 8) * N + hn0 + nt * 8) = make_float2(hacc[nt][2], hacc[nt][3]);
+  }
+}
+
 // g = y * SiLU(z) in place (y fp32 [M][Ek], z bf16 at proj[m][z_col..]); ss[m] = sum g^2
 __global__ void __launch_bounds__(256) m2_gate_ss_kernel(float* __restrict__ y, int Ek,
                                                          const __nv_bfloat16* __restrict__ proj, int64_t ldp,
@@ -220,6 +476,21 @@ cudaError_t launch_m2_scan(const __nv_bfloat16* proj, int64_t ldp, int dt_col, c
     return e != cudaSuccess ? e : cudaGetLastError();
   }
   dim3 grid(Hk, batch);
+  if (L >= kSsdChunkMinL && (N == 128 || N == 64) && (ldu % 8) == 0 && (b_col % 8) == 0 && (c_col % 8) == 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(m2_ssd_chunk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssd_smem_bytes<128>());
+      cudaFuncSetAttribute(m2_ssd_chunk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssd_smem_bytes<64>());
+      attr = true;
+    }
+    if (N == 128)
+      e = launch(m2_ssd_chunk_kernel<128>, grid, 256, ssd_smem_bytes<128>(), s, proj, ldp, dt_col, u, ldu, b_col, c_col,
+                 heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, L, Hk);
+    else
+      e = launch(m2_ssd_chunk_kernel<64>, grid, 256, ssd_smem_bytes<64>(), s, proj, ldp, dt_col, u, ldu, b_col, c_col,
+                 heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, L, Hk);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   switch (N) {
     case 128: e = launch(m2_scan_kernel<128>, grid, M2_THREADS, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
                          heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, L, Hk); break;
@@ -254,6 +525,7 @@ cudaError_t preload_ssd() {
   for (const void* f : {(const void*)m2_scan_kernel<128>, (const void*)m2_scan_kernel<64>,
                         (const void*)m2_scan_kernel<16>, (const void*)m2_scan_step_kernel<128>,
                         (const void*)m2_scan_step_kernel<64>, (const void*)m2_scan_step_kernel<16>,
+                        (const void*)m2_ssd_chunk_kernel<128>, (const void*)m2_ssd_chunk_kernel<64>,
                         (const void*)m2_gate_ss_kernel,
                         (const void*)m2_norm_apply_kernel}) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);

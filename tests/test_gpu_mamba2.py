@@ -87,3 +87,22 @@ def test_mamba2_decode_step_alone_vs_oracle(N, B):
     assert rel(got[0][:, dec] - res[:, dec], ref[:, dec] - res[:, dec]) < TOL["bf16"]
     H, P = m2.n_heads, m2.headdim
     assert rel(mix[0].h.view(B, H, P, N).cpu().double().numpy(), h_ref) < TOL["bf16"]
+
+
+@pytest.mark.parametrize("N", [64, 128])
+def test_mamba2_chunked_ssd_multi_chunk_vs_oracle(N):
+    """Prompts longer than one 64-token SSD chunk, split across calls at chunk-unaligned offsets
+    (150 = 2 x 64 + 22, then 70 carried from the saved state), so the chunk carry h_end, the
+    in-chunk decay masks, the padded tail and the cross-call state all count."""
+    m2 = synth.Mamba2Dims(d_model=256, d_inner=512, d_state=N)
+    got, ref, res, mix, h_ref = _run(m2, 1, 2, [150, 70], 3, L.SSM_AR2_INT8)
+    assert rel(got[0] - res, ref - res) < TOL["bf16"]
+    H, P = m2.n_heads, m2.headdim
+    assert rel(mix[0].h.view(2, H, P, N).cpu().double().numpy(), h_ref) < TOL["bf16"]
+
+
+def test_mamba2_short_calls_per_token_scan_vs_oracle():
+    """Calls shorter than 16 tokens take the per-token recurrence (m2_scan), not the chunked form."""
+    m2 = synth.Mamba2Dims(d_model=256, d_inner=512, d_state=128)
+    got, ref, res, _, _ = _run(m2, 1, 3, [7, 5, 13], 2, L.SSM_AR2_INT8)
+    assert rel(got[0] - res, ref - res) < TOL["bf16"]
