@@ -330,7 +330,11 @@ ssm_status_t ssm_rmsnorm_add(ssm_tp_t tp, const float* a, const float* b, const 
  * on every rank (their W_in rows and conv taps too) -- no all-reduce before the scan; the gated
  * RMSNorm's per-token sum of squares is all-reduced (exact fp32, M floats), out_proj row-parallel
  * -> AR#2 into the residual (flags: SSM_AR2_INT8 one-shot, SSM_AR2_FP32, SSM_AR2_FP16, SSM_AR2_BF16).
- * The handle supplies d_model and the communicator; bf16 only. */
+ * The handle supplies d_model and the communicator; bf16 only.
+ * Kernels: calls of >= 16 tokens scan in the chunked SSD (matmul) form (64-token chunks, d_state 64 or
+ * 128), decode (seqlen 1) as one streaming step, other calls token by token; every scan writes
+ * bf16(y SiLU(z) w) and the per-token sums of squares, and the out_proj applies 1/sqrt(ss/E + eps)
+ * per row after the contraction (reading M3 in DESIGN.md). */
 typedef struct {
   int32_t d_inner;        /* E (global)                                                       */
   int32_t d_state;        /* N: 16, 64 or 128                                                 */

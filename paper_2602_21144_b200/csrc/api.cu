@@ -1242,7 +1242,7 @@ ssm_status_t m2_dims(const ssm_tp_s* t, const ssm_m2_config_t* c, M2Dims* o) {
   return SSM_OK;
 }
 struct M2Ws {
-  size_t proj, u, y, ss, o, part, total;
+  size_t proj, u, ss, o, part, total;
 };
 M2Ws m2_ws(const ssm_tp_s* t, const M2Dims& z, int64_t M) {
   M2Ws L{};
@@ -1250,7 +1250,6 @@ M2Ws m2_ws(const ssm_tp_s* t, const M2Dims& z, int64_t M) {
   auto take = [&](size_t bytes) { size_t o = off; off += al256(bytes); return o; };
   L.proj = take(M * z.ldp * 2);
   L.u = take(M * z.Ck * 2);
-  L.y = take(M * z.Ek * 4);
   L.ss = take(((M + 3) / 4 * 4) * 4);
   L.o = take(M * z.Ek * 2);
   L.part = take(t->k > 1 ? M * z.D * 4 : 0);
@@ -1312,15 +1311,20 @@ ssm_status_t ssm_m2_mixer(ssm_tp_t tp, const ssm_m2_config_t* cfg, const ssm_m2_
   char* W = reinterpret_cast<char*>(workspace);
   __nv_bfloat16* proj = reinterpret_cast<__nv_bfloat16*>(W + L.proj);
   __nv_bfloat16* u = reinterpret_cast<__nv_bfloat16*>(W + L.u);
-  float* y = reinterpret_cast<float*>(W + L.y);
   float* ss = reinterpret_cast<float*>(W + L.ss);
   __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(W + L.o);
   // packed in_proj [z | x | B | C | dt] of the rank (decode: swap-AB, the weights fill the MMA rows)
   const bool swap = seqlen == 1 && batch <= 32;
-  if (swap)
-    CU(gemm(tp, w->w_in, z.D, x_in, z.D, z.Wp, (int)M, z.D, 1, epi(EPI_STORE_BF16, 1, proj, z.ldp), s, true));
-  else
-    CU(gemm(tp, x_in, z.D, w->w_in, z.D, (int)M, z.Wp, z.D, 1, epi(EPI_STORE_BF16, 0, proj, z.ldp), s));
+  // (its epilogue also zeroes ss, which the scan accumulates the gated rows' sums of squares into)
+  {
+    Epilogue e = epi(EPI_STORE_BF16, swap ? 1 : 0, proj, z.ldp);
+    e.zero = ss;
+    e.nzero = (M + 3) / 4 * 4;
+    if (swap)
+      CU(gemm(tp, w->w_in, z.D, x_in, z.D, z.Wp, (int)M, z.D, 1, e, s, true));
+    else
+      CU(gemm(tp, x_in, z.D, w->w_in, z.D, (int)M, z.Wp, z.D, 1, e, s));
+  }
   // causal conv + SiLU over the x | B | C channels (window of the cache updated)
   const __nv_bfloat16* xbc = proj + z.Ek;
   if (seqlen == 1) {
@@ -1332,33 +1336,40 @@ ssm_status_t ssm_m2_mixer(ssm_tp_t tp, const ssm_m2_config_t* cfg, const ssm_m2_
     CU(launch_conv1d_silu(1, xbc, z.ldp, conv_state, w->conv_w, w->conv_b, u, z.Ck, batch, seqlen, z.Ck, z.K, s));
     CU(launch_conv_state_update(1, xbc, z.ldp, conv_state, batch, seqlen, z.Ck, z.K, s));
   }
-  // scan (per head, per sequence); gate + the row's sum of squares; (TP > 1) all-reduce of the
-  // sums; normalise -> out_proj input
-  tp->launches += 3;
+  // scan (per head, per sequence) with the gate, the norm weight and the rows' sums of squares
+  // fused into its output (o = bf16(y SiLU(z) w)); (TP > 1) all-reduce of the sums; the out_proj
+  // epilogues scale each row by 1 / sqrt(ss / E + eps) (reading M3)
+  tp->launches += 1;
   CU(launch_m2_scan(proj, z.ldp, 2 * z.Ek + 2 * z.GN, u, z.Ck, z.Ek, z.Ek + z.GN, z.H / z.G / tp->k > 0 ? z.Hk : 1,
-                    w->dt_bias, w->a_log, w->d_skip, h_state, y, z.Ek, batch, seqlen, z.Hk, z.P, z.N, s));
-  CU(launch_m2_gate_ss(y, z.Ek, proj, z.ldp, ss, M, s));
+                    w->dt_bias, w->a_log, w->d_skip, w->norm_w, h_state, o, z.Ek, ss, batch, seqlen, z.Hk, z.P, z.N,
+                    s));
   if (tp->k > 1) {
     ssm_status_t r = ssm_qallreduce(tp, ss, ss, (size_t)((M + 3) / 4 * 4), SSM_QAR_FP32, stream);
     if (r != SSM_OK) return r;
   }
-  CU(launch_m2_norm_apply(y, z.Ek, ss, z.E, cfg->eps, w->norm_w, o, M, s));
+  auto oepi = [&](int kind, int trans, float* C) {
+    Epilogue e = epi(kind, trans, C, z.D);
+    e.rss = ss;
+    e.rss_inv = 1.0f / (float)z.E;
+    e.rss_eps = cfg->eps;
+    return e;
+  };
   // out_proj (row-parallel): TP = 1 straight into the residual, else partial + AR#2 (decode:
   // swap-AB split-K with fp32 atomics)
   if (tp->k == 1) {
     if (swap)
       CU(gemm(tp, w->w_out, z.Ek, o, z.Ek, z.D, (int)M, z.Ek, split_for(tp, z.D, z.Ek),
-              epi(EPI_ATOMIC_F32, 1, residual, z.D), s, true));
+              oepi(EPI_ATOMIC_F32, 1, residual), s, true));
     else
-      CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, epi(EPI_ADD_F32, 0, residual, z.D), s));
+      CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, oepi(EPI_ADD_F32, 0, residual), s));
   } else {
     float* part = reinterpret_cast<float*>(W + L.part);
     if (swap) {
       CU(cudaMemsetAsync(part, 0, (size_t)M * z.D * 4, s));
       CU(gemm(tp, w->w_out, z.Ek, o, z.Ek, z.D, (int)M, z.Ek, split_for(tp, z.D, z.Ek),
-              epi(EPI_ATOMIC_F32, 1, part, z.D), s, true));
+              oepi(EPI_ATOMIC_F32, 1, part), s, true));
     } else {
-      CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, epi(EPI_STORE_F32, 0, part, z.D), s));
+      CU(gemm(tp, o, z.Ek, w->w_out, z.Ek, (int)M, z.D, z.Ek, 1, oepi(EPI_STORE_F32, 0, part), s));
     }
     const uint32_t qf = (flags & SSM_AR2_FP32) ? SSM_QAR_FP32 : (flags & SSM_AR2_FP16) ? SSM_QAR_FP16
                       : (flags & SSM_AR2_BF16) ? SSM_QAR_BF16 : 0;

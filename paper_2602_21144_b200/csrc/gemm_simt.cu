@@ -13,6 +13,7 @@ constexpr int TM = 64, TN = 64, TK = 16;
 
 __device__ __forceinline__ void epi_one(const Epilogue& e, int m, int n, float v) {
   if (e.kind == EPI_SOFTPLUS_BF16 || e.kind == EPI_SOFTPLUS_F32) v = softplus(v + e.bias[e.trans ? m : n]);
+  if (e.rss) v *= rsqrtf(e.rss[e.trans ? n : m] * e.rss_inv + e.rss_eps);
   const int64_t idx = e.trans ? (int64_t)n * e.ldc + m : (int64_t)m * e.ldc + n;
   switch (e.kind) {
     case EPI_STORE_BF16:
@@ -86,7 +87,11 @@ cudaError_t preload_gemm_simt() {
 
 cudaError_t gemm_simt(const void* A, int64_t lda, const void* B, int64_t ldb, int dtype_bf16, int M, int N, int K,
                       int ksplit, const Epilogue& epi, cudaStream_t s) {
-  if (epi.kind == EPI_DECODE_INPROJ || epi.zero) return cudaErrorInvalidValue;  // tcgen05 path only
+  if (epi.kind == EPI_DECODE_INPROJ) return cudaErrorInvalidValue;  // tcgen05 path only
+  if (epi.zero && epi.nzero > 0) {
+    cudaError_t e = cudaMemsetAsync(epi.zero, 0, (size_t)epi.nzero * 4, s);
+    if (e != cudaSuccess) return e;
+  }
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (ksplit < 1) ksplit = 1;
   int kper = (K + ksplit - 1) / ksplit;

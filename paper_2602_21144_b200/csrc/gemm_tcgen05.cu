@@ -76,6 +76,15 @@ struct TileSched {
   __device__ int first() const { return (int)blockIdx.x; }
 };
 
+// Optional row scale 1 / sqrt(rss[r] * rss_inv + rss_eps) of logical row r (Epilogue::rss).
+__device__ __forceinline__ float rss_scale(const Epilogue& e, int r) { return rsqrtf(e.rss[r] * e.rss_inv + e.rss_eps); }
+// trans = 1: the logical rows are the 32 columns n0..n0+31 of the chunk
+__device__ __forceinline__ void rss_apply_trans(const Epilogue& e, int n0, int N, float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (n0 + j < N) v[j] *= rss_scale(e, n0 + j);
+}
+
 // The only epilogue of the VAR 2 kernel: C[n * ldc + m] += acc atomically (swap-AB split-K).
 __device__ __forceinline__ void epi_chunk_atomic_trans(const Epilogue& e, int m0, int n0, int M, int N,
                                                        uint32_t (&r)[32]) {
@@ -83,9 +92,13 @@ __device__ __forceinline__ void epi_chunk_atomic_trans(const Epilogue& e, int m0
   if (m >= M) return;
   const int nv = min(32, N - n0);
   float* C = reinterpret_cast<float*>(e.C) + (int64_t)n0 * e.ldc + m;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (e.rss) rss_apply_trans(e, n0, N, v);
 #pragma unroll
   for (int j = 0; j < 32; ++j)
-    if (j < nv) atomicAdd(C + (int64_t)j * e.ldc, __uint_as_float(r[j]));
+    if (j < nv) atomicAdd(C + (int64_t)j * e.ldc, v[j]);
 }
 
 // Epilogue for one warp's 32 x 32 chunk: lane = row m0 + lane, columns n0..n0+31, stored
@@ -129,6 +142,15 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = softplus(v[j] + bb[j]);
+    }
+  }
+  if (FK < 0 && e.rss) {
+    if (e.trans) {
+      rss_apply_trans(e, n0, N, v);
+    } else {
+      const float sc = rss_scale(e, m);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= sc;
     }
   }
   if (e.trans) {
@@ -238,13 +260,14 @@ __device__ __forceinline__ void quant_epilogue(const Epilogue& e, int m0, int n_
   const int half = (warp - 2) >> 2, eg = warp & 3;
   const int row = eg * 32 + lane, m = m0 + lane;
   const int nch = BN / 32, cpb = e.qblk / 32;
+  const float rsc = (e.rss && m < M) ? rss_scale(e, m) : 1.f;  // row scale applied before quantising
   for (int c = half; c < nch; c += 2) {
     uint32_t r[32];
     tmem_ld_32x32b_x32(tbase + c * 32, r);
     tmem_ld_wait();
     float am = 0.f;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) am = fmaxf(am, fabsf(__uint_as_float(r[j])));
+    for (int j = 0; j < 32; ++j) am = fmaxf(am, fabsf(__uint_as_float(r[j]) * rsc));
     s_am[row * 8 + c] = am;
   }
   named_bar_sync(1, 256);
@@ -265,7 +288,7 @@ __device__ __forceinline__ void quant_epilogue(const Epilogue& e, int m0, int n_
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           int code = 0;
-          if (s != 0.f) code = max(-127, min(127, __float2int_rn(__fdiv_rn(__uint_as_float(r[4 * q + j]), s))));
+          if (s != 0.f) code = max(-127, min(127, __float2int_rn(__fdiv_rn(__uint_as_float(r[4 * q + j]) * rsc, s))));
           w |= (uint32_t)(code & 0xff) << (8 * j);
         }
         pk[q] = w;
@@ -892,6 +915,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   else if (epi.kind == EPI_ATOMIC_F32 && epi.trans && BN <= 32) var = 2;
   else if (!epi.trans && epi.kind == EPI_SOFTPLUS_BF16) var = 6;
   else if (epi.kind == EPI_QUANT_I8) var = 7;
+  if (epi.rss && (var == 1 || var == 6)) return cudaErrorInvalidValue;  // no row scale in those epilogues
   auto kfn = var == 2 ? gemm_tc_kernel<2> : var == 6 ? gemm_tc_kernel<6> : var == 7 ? gemm_tc_kernel<7> : gemm_tc_kernel<0>;
   if (var == 1) kfn = epi.P <= 64 * 3 ? gemm_tc_kernel<1, 3> : epi.P <= 64 * 4 ? gemm_tc_kernel<1, 4> : gemm_tc_kernel<1>;
   cudaError_t e_ = launch(kfn, grid, var_threads(var), smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi, A_blocked, lda, K,

@@ -38,6 +38,12 @@ struct Epilogue {
   // EPI_QUANT_I8: per-block scales and block size (32 | 64 | 128 | 256, dividing the tile width)
   float* qs;
   int qblk;
+  // Optional row scale (kinds STORE_BF16 / STORE_F32 / ADD_F32 / ATOMIC_F32 / QUANT_I8): acc of the
+  // logical row r (= m if trans = 0, n if trans = 1) is multiplied by 1 / sqrt(rss[r] * rss_inv +
+  // rss_eps) before the store -- the gated RMSNorm's rstd applied after the out_proj contraction
+  // (its weight is folded into the A operand by the scan; reading M3).
+  const float* rss;
+  float rss_inv, rss_eps;
   // EPI_DECODE_INPROJ (SURVEY.md §8 rows a1-a3 fused for one decode token).
   // Output rows m are in_proj features: m < Ek are x channels -> causal conv step over the cached
   // window cst + SiLU -> u (bf16 [N][Ek]) and the window shifted in place; Ek <= m < 2Ek are z
@@ -159,12 +165,8 @@ cudaError_t preload_attn();
 // ---- Mamba-2 (SSD) mixer (ssd.cu) ----
 cudaError_t launch_m2_scan(const __nv_bfloat16* proj, int64_t ldp, int dt_col, const __nv_bfloat16* u, int64_t ldu,
                            int b_col, int c_col, int heads_per_group, const float* dt_bias, const float* a_log,
-                           const float* d_skip, float* hstate, float* y, int64_t ldy, int batch, int L, int Hk, int P,
-                           int N, cudaStream_t s);
-cudaError_t launch_m2_gate_ss(float* y, int Ek, const __nv_bfloat16* proj, int64_t ldp, float* ss, int64_t M,
-                              cudaStream_t s);
-cudaError_t launch_m2_norm_apply(const float* g, int Ek, const float* ss, int E, float eps, const float* w,
-                                 __nv_bfloat16* o, int64_t M, cudaStream_t s);
+                           const float* d_skip, const float* norm_w, float* hstate, __nv_bfloat16* o, int64_t ldo,
+                           float* ss, int batch, int L, int Hk, int P, int N, cudaStream_t s);
 cudaError_t preload_ssd();
 
 

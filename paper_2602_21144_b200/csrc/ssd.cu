@@ -8,9 +8,9 @@
 //                   registers per thread), token tiles of x, B, C, dt staged by cp.async;
 //                   m2_scan_step: the L = 1 decode step as a coalesced stream over the state rows;
 //                   m2_ssd_chunk: calls of >= 16 tokens in the chunked SSD (matmul) form
-//   m2_gate_ss      g = y SiLU(z) (fp32, in place) and the row's sum of squares (all-reduced
-//                   over the ranks by the caller at TP > 1: the gated RMSNorm spans d_inner)
-//   m2_norm_apply   o = g / sqrt(ss / E + eps) * w (bf16), the out_proj's input
+// Each of the three ends in the gated RMSNorm's row-local part: o = bf16(y SiLU(z) w) (the
+// out_proj's input) and ss[m] += sum of g^2 (all-reduced over the ranks by the caller at TP > 1:
+// the norm spans d_inner); the out_proj's epilogue applies 1 / sqrt(ss / E + eps) per row.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -24,14 +24,20 @@ constexpr int M2_P = 64, M2_Q = 4, M2_THREADS = M2_P * M2_Q, M2_TT = 16, M2_NMAX
 // d_state 16) the per-token recurrence (m2_scan)
 constexpr int kSsdChunkMinL = 16;
 
+// The gated RMSNorm's row-local part, fused into every scan kernel's output (reading M3): for
+// channel c of row m, g = y SiLU(z) with z = proj[m][c]; the kernel stores o = bf16(g w[c]) (the
+// out_proj's A operand, norm weight folded in) and adds g^2 into ss[m] (zeroed by the in_proj's
+// epilogue); the out_proj epilogue then scales its row by 1 / sqrt(ss[m] / E + eps).
+SSM_DEV float silu_gate(float yv, float zv) { return yv * (zv / (1.0f + expf(-zv))); }
+
 // proj [M][ldp] bf16: dt raw at column dt_col + h; u [M][ldu] bf16: x at x_col + h P, B at b_col,
 // C at c_col (group g of the head: + g N).  h_state [batch][Hk][P][N] fp32 in place; y [M][Ek] fp32.
 template <int N>
 __global__ void __launch_bounds__(M2_THREADS) m2_scan_kernel(
     const __nv_bfloat16* __restrict__ proj, int64_t ldp, int dt_col, const __nv_bfloat16* __restrict__ u,
     int64_t ldu, int b_col, int c_col, int heads_per_group, const float* __restrict__ dt_bias,
-    const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ hstate,
-    float* __restrict__ y, int64_t ldy, int L, int Hk) {
+    const float* __restrict__ a_log, const float* __restrict__ d_skip, const float* __restrict__ norm_w,
+    float* __restrict__ hstate, __nv_bfloat16* __restrict__ o, int64_t ldo, float* __restrict__ ss, int L, int Hk) {
   constexpr int NPT = N / M2_Q;  // states per thread
   __shared__ __align__(16) __nv_bfloat16 sx[2][M2_TT][M2_P];
   __shared__ __align__(16) __nv_bfloat16 sb[2][M2_TT][N];
@@ -44,7 +50,7 @@ __global__ void __launch_bounds__(M2_THREADS) m2_scan_kernel(
   const int64_t row0 = (int64_t)b * L;
   // the head's weights first (never written by a kernel), then wait for the predecessor's outputs
   const float A = -expf(a_log[h]) * 1.4426950408889634f;  // log2e-scaled: exp(dt A) = 2^(dt A')
-  const float bias = dt_bias[h], Dh = d_skip[h];
+  const float bias = dt_bias[h], Dh = d_skip[h], wn = norm_w[h * M2_P + p];
   pdl_wait();
   float hs[NPT];
   // thread q owns the contiguous states [NPT q, NPT q + NPT): the 4 quarter-threads of a channel read
@@ -106,7 +112,16 @@ __global__ void __launch_bounds__(M2_THREADS) m2_scan_kernel(
       }
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (q == 0) y[(row0 + t0 + r) * ldy + (int64_t)h * M2_P + p] = fmaf(Dh, xv, acc);
+      const int64_t m = row0 + t0 + r;
+      float g2 = 0.f;
+      if (q == 0) {
+        const float gv = silu_gate(fmaf(Dh, xv, acc), __bfloat162float(proj[m * ldp + (int64_t)h * M2_P + p]));
+        o[m * ldo + (int64_t)h * M2_P + p] = __float2bfloat16_rn(gv * wn);
+        g2 = gv * gv;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) g2 += __shfl_xor_sync(0xffffffffu, g2, off);
+      if ((tid & 31) == 0) atomicAdd(ss + m, g2);
     }
     __syncthreads();
   }
@@ -115,51 +130,79 @@ __global__ void __launch_bounds__(M2_THREADS) m2_scan_kernel(
 }
 
 // The decode step (L = 1): the state read + write (B Hk P N fp32 each way; 42 MB per Mamba-2-2.7B
-// layer at batch 16) is the whole cost, so the work is spread as a stream rather than one CTA per
-// (head, sequence) (that form, 66 registers x 256 threads, fits 3 CTAs per SM and runs 1280 CTAs in
-// ~3 latency-bound waves): N / 8 lanes per state row (b, h, p), 8 states per lane (two float4 of h,
-// one 16-B run each of B and C), the row's C.h by shuffles inside the lane group.
+// layer at batch 16) is the whole cost, so the work is spread as a stream rather than one thread
+// per channel (the multi-token kernel's 66 registers x 256 threads fit 3 CTAs per SM and ran 1280
+// CTAs in ~3 latency-bound waves): one CTA per (head, sequence), N / 8 lanes per state row (h, p),
+// 8 states per lane (two float4 of h, one 16-B run each of B and C), each lane group walking
+// 64 N / 8 / threads rows with all its loads issued first; the row's C.h by shuffles inside the lane
+// group; one ss atomic per CTA.
 template <int N>
 __global__ void __launch_bounds__(256) m2_scan_step_kernel(
     const __nv_bfloat16* __restrict__ proj, int64_t ldp, int dt_col, const __nv_bfloat16* __restrict__ u,
     int64_t ldu, int b_col, int c_col, int heads_per_group, const float* __restrict__ dt_bias,
-    const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ hstate,
-    float* __restrict__ y, int64_t ldy, int64_t rows, int Hk) {
-  constexpr int LPR = N / 8;  // lanes per state row (a power of two dividing 32)
+    const float* __restrict__ a_log, const float* __restrict__ d_skip, const float* __restrict__ norm_w,
+    float* __restrict__ hstate, __nv_bfloat16* __restrict__ o, int64_t ldo, float* __restrict__ ss, int Hk) {
+  constexpr int LPR = N / 8;                                 // lanes per state row (power of two <= 16)
+  constexpr int THREADS = M2_P * LPR < 256 ? M2_P * LPR : 256;
+  constexpr int RPT = M2_P * LPR / THREADS;                  // rows per lane group
+  constexpr int RSTEP = THREADS / LPR;
+  __shared__ float sred[THREADS / 32];
   pdl_trigger();
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR;  // (b, h, p)
-  const int sub = threadIdx.x % LPR;
-  const bool live = row < rows;
-  const int64_t rr = live ? row : 0;
-  const int p = (int)(rr % M2_P);
-  const int h = (int)((rr / M2_P) % Hk);
-  const int64_t b = rr / ((int64_t)M2_P * Hk);
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int sub = threadIdx.x % LPR, p0 = threadIdx.x / LPR;
   const int g = h / heads_per_group;
   const float A = -expf(a_log[h]) * 1.4426950408889634f;
   const float bias = dt_bias[h], Dh = d_skip[h];
   pdl_wait();
-  float* hp = hstate + rr * N + 8 * sub;
-  const float4 h0 = *reinterpret_cast<const float4*>(hp), h1 = *reinterpret_cast<const float4*>(hp + 4);
-  const uint4 bv = *reinterpret_cast<const uint4*>(u + b * ldu + b_col + (int64_t)g * N + 8 * sub);
-  const uint4 cv = *reinterpret_cast<const uint4*>(u + b * ldu + c_col + (int64_t)g * N + 8 * sub);
-  const float xv = __bfloat162float(u[b * ldu + (int64_t)h * M2_P + p]);
-  const float dt = softplus(__bfloat162float(proj[b * ldp + dt_col + h]) + bias);
-  const float dA = ex2_approx(dt * A), dtx = dt * xv;
-  float hs[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+  const __nv_bfloat16* urow = u + (int64_t)b * ldu;
+  float* hp = hstate + (((int64_t)b * Hk + h) * M2_P) * N + 8 * sub;
+  float4 h0[RPT], h1[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int p = p0 + k * RSTEP;
+    h0[k] = *reinterpret_cast<const float4*>(hp + (int64_t)p * N);
+    h1[k] = *reinterpret_cast<const float4*>(hp + (int64_t)p * N + 4);
+  }
+  const uint4 bv = *reinterpret_cast<const uint4*>(urow + b_col + (int64_t)g * N + 8 * sub);
+  const uint4 cv = *reinterpret_cast<const uint4*>(urow + c_col + (int64_t)g * N + 8 * sub);
+  const float dt = softplus(__bfloat162float(proj[(int64_t)b * ldp + dt_col + h]) + bias);
+  const float dA = ex2_approx(dt * A);
   const __nv_bfloat16* bb = reinterpret_cast<const __nv_bfloat16*>(&bv);
   const __nv_bfloat16* cc = reinterpret_cast<const __nv_bfloat16*>(&cv);
-  float acc = 0.f;
+  float g2 = 0.f;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    hs[j] = fmaf(dA, hs[j], dtx * __bfloat162float(bb[j]));
-    acc = fmaf(__bfloat162float(cc[j]), hs[j], acc);
+  for (int k = 0; k < RPT; ++k) {
+    const int p = p0 + k * RSTEP;
+    const float xv = __bfloat162float(urow[(int64_t)h * M2_P + p]);
+    const float dtx = dt * xv;
+    float hs[8] = {h0[k].x, h0[k].y, h0[k].z, h0[k].w, h1[k].x, h1[k].y, h1[k].z, h1[k].w};
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      hs[j] = fmaf(dA, hs[j], dtx * __bfloat162float(bb[j]));
+      acc = fmaf(__bfloat162float(cc[j]), hs[j], acc);
+    }
+#pragma unroll
+    for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    *reinterpret_cast<float4*>(hp + (int64_t)p * N) = make_float4(hs[0], hs[1], hs[2], hs[3]);
+    *reinterpret_cast<float4*>(hp + (int64_t)p * N + 4) = make_float4(hs[4], hs[5], hs[6], hs[7]);
+    if (sub == 0) {
+      const int c = h * M2_P + p;
+      const float gv = silu_gate(fmaf(Dh, xv, acc), __bfloat162float(proj[(int64_t)b * ldp + c]));
+      o[(int64_t)b * ldo + c] = __float2bfloat16_rn(gv * norm_w[c]);
+      g2 = fmaf(gv, gv, g2);
+    }
   }
 #pragma unroll
-  for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (!live) return;
-  *reinterpret_cast<float4*>(hp) = make_float4(hs[0], hs[1], hs[2], hs[3]);
-  *reinterpret_cast<float4*>(hp + 4) = make_float4(hs[4], hs[5], hs[6], hs[7]);
-  if (sub == 0) y[b * ldy + (int64_t)h * M2_P + p] = fmaf(Dh, xv, acc);
+  for (int off = 16; off > 0; off >>= 1) g2 += __shfl_xor_sync(0xffffffffu, g2, off);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = g2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < THREADS / 32; ++w) t += sred[w];
+    atomicAdd(ss + b, t);
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -200,8 +243,8 @@ template <int N>
 __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
     const __nv_bfloat16* __restrict__ proj, int64_t ldp, int dt_col, const __nv_bfloat16* __restrict__ u,
     int64_t ldu, int b_col, int c_col, int heads_per_group, const float* __restrict__ dt_bias,
-    const float* __restrict__ a_log, const float* __restrict__ d_skip, float* __restrict__ hstate,
-    float* __restrict__ y, int64_t ldy, int L, int Hk) {
+    const float* __restrict__ a_log, const float* __restrict__ d_skip, const float* __restrict__ norm_w,
+    float* __restrict__ hstate, __nv_bfloat16* __restrict__ o, int64_t ldo, float* __restrict__ ss, int L, int Hk) {
   static_assert(N == 64 || N == 128, "chunked SSD: d_state 64 or 128");
   constexpr int KS = N / 16;  // k-steps over the state dimension (G, C h^T)
   constexpr int HT = N / 16;  // 8-wide n-tiles per warp in the carry update (N / 2 columns)
@@ -242,28 +285,33 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
     }
   };
   auto load_tile = [&](int buf, int t0) {
-    constexpr int XC = M2_P / 8, BC = N / 8, RC = XC + 2 * BC;
-    for (int i = tid; i < SQ * RC; i += 256) {
-      const int r = i / RC, c = i % RC;
+    constexpr int XPT = SQ * (M2_P / 8) / 256, BPT = SQ * (N / 8) / 256;  // 16-B chunks per thread
+#pragma unroll
+    for (int k = 0; k < XPT; ++k) {
+      const int i = tid + 256 * k, r = i / (M2_P / 8), c = i % (M2_P / 8);
       const bool ok = t0 + r < L;
-      const int64_t row = row0 + (ok ? t0 + r : 0);
-      const __nv_bfloat16* urow = u + row * ldu;
-      if (c < XC) cp_async16(sX + buf * SQ * M2_P + swz(r, c * 8, M2_P), urow + (int64_t)h * M2_P + c * 8, ok);
-      else if (c < XC + BC) cp_async16(sB + buf * SQ * N + swz(r, (c - XC) * 8, N), urow + b_col + (int64_t)g * N + (c - XC) * 8, ok);
-      else cp_async16(sC + buf * SQ * N + swz(r, (c - XC - BC) * 8, N), urow + c_col + (int64_t)g * N + (c - XC - BC) * 8, ok);
+      const __nv_bfloat16* urow = u + (row0 + (ok ? t0 + r : 0)) * ldu;
+      cp_async16(sX + buf * SQ * M2_P + swz(r, c * 8, M2_P), urow + (int64_t)h * M2_P + c * 8, ok);
+    }
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+      const int i = tid + 256 * k, r = i / (N / 8), c = i % (N / 8);
+      const bool ok = t0 + r < L;
+      const __nv_bfloat16* urow = u + (row0 + (ok ? t0 + r : 0)) * ldu + (int64_t)g * N + c * 8;
+      const int so = buf * SQ * N + swz(r, c * 8, N);
+      cp_async16(sB + so, urow + b_col, ok);
+      cp_async16(sC + so, urow + c_col, ok);
     }
   };
-  // dt of the chunk at t0 (threads 0..63 each hold one raw value; padded tokens give dt = 0)
-  auto load_dt = [&](int t0) -> float {
-    const int t = t0 + tid;
-    return (tid < SQ && t < L) ? __bfloat162float(proj[(row0 + t) * ldp + dt_col + h]) : -INFINITY;
+  // warp 0 alone handles dt: raw values of the chunk at t0 (tokens t0 + 2 lane, + 1; padded -> dt 0),
+  // then softplus, the inclusive cumsum of a_s = dt_s A and w_s = exp(A_Q - A_s) dt_s, from registers
+  auto load_dt = [&](int t0, float& r0, float& r1) {
+    const int t = t0 + 2 * lane;
+    r0 = t < L ? __bfloat162float(proj[(row0 + t) * ldp + dt_col + h]) : -INFINITY;
+    r1 = t + 1 < L ? __bfloat162float(proj[(row0 + t + 1) * ldp + dt_col + h]) : -INFINITY;
   };
-  auto put_dt = [&](int buf, float raw) {
-    if (tid < SQ) sdt[buf * SQ + tid] = raw == -INFINITY ? 0.f : softplus(raw + bias);
-  };
-  // warp 0: inclusive cumsum of a_s = dt_s A (2 tokens per lane) and w_s = exp(A_Q - A_s) dt_s
-  auto scan = [&](int buf) {
-    const float d0 = sdt[buf * SQ + 2 * lane], d1 = sdt[buf * SQ + 2 * lane + 1];
+  auto scan = [&](int buf, float r0, float r1) {
+    const float d0 = r0 == -INFINITY ? 0.f : softplus(r0 + bias), d1 = r1 == -INFINITY ? 0.f : softplus(r1 + bias);
     const float a0 = d0 * A, a1 = d1 * A;
     float x = a0 + a1;
 #pragma unroll
@@ -273,28 +321,28 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
     }
     const float c1 = x, c0 = x - a1;
     const float tot = __shfl_sync(0xffffffffu, x, 31);
-    sAc[buf * SQ + 2 * lane] = c0;
-    sAc[buf * SQ + 2 * lane + 1] = c1;
-    sW[buf * SQ + 2 * lane] = ex2_approx(tot - c0) * d0;
-    sW[buf * SQ + 2 * lane + 1] = ex2_approx(tot - c1) * d1;
+    *reinterpret_cast<float2*>(sdt + buf * SQ + 2 * lane) = make_float2(d0, d1);
+    *reinterpret_cast<float2*>(sAc + buf * SQ + 2 * lane) = make_float2(c0, c1);
+    *reinterpret_cast<float2*>(sW + buf * SQ + 2 * lane) = make_float2(ex2_approx(tot - c0) * d0, ex2_approx(tot - c1) * d1);
   };
 
   const int nch = (L + SQ - 1) / SQ;
   load_tile(0, 0);
   cp_async_commit();
-  put_dt(0, load_dt(0));
   store_h();
-  __syncthreads();
-  if (warp == 0) scan(0);
+  float dr0 = 0.f, dr1 = 0.f;
+  if (warp == 0) {
+    load_dt(0, dr0, dr1);
+    scan(0, dr0, dr1);
+  }
   for (int ch = 0; ch < nch; ++ch) {
     const int buf = ch & 1, t0 = ch * SQ;
     cp_async_wait<0>();
-    __syncthreads();  // chunk tiles, sAc / sW [buf] and sH visible; chunk ch-1's readers are done
-    float dt_next = -INFINITY;
+    __syncthreads();  // chunk tiles, sdt / sAc / sW [buf] and sH visible; chunk ch-1's readers are done
     if (ch + 1 < nch) {
       load_tile(buf ^ 1, t0 + SQ);
       cp_async_commit();
-      dt_next = load_dt(t0 + SQ);
+      if (warp == 0) load_dt(t0 + SQ, dr0, dr1);
     }
     const __nv_bfloat16* Xb = sX + buf * SQ * M2_P;
     const __nv_bfloat16* Bb = sB + buf * SQ * N;
@@ -349,7 +397,6 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
         yacc[nt][0] *= e0; yacc[nt][1] *= e0; yacc[nt][2] *= e1; yacc[nt][3] *= e1;
       }
     }
-    if (ch + 1 < nch) put_dt(buf ^ 1, dt_next);
     __syncthreads();  // sM complete; every warp is done reading sH
     // Y += (G o decay) X
 #pragma unroll
@@ -364,18 +411,28 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
         mma_16816_bf16(yacc[2 * np + 1], af, bf[2], bf[3]);
       }
     }
+    // y = Y + D x -> gated output o = bf16(y SiLU(z) w) and the rows' partial sums of squares
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      const int pc = hf * 32 + nt * 8 + 2 * cq;
+    for (int hh = 0; hh < 2; ++hh) {
+      const int t = t_a + 8 * hh;
+      const bool ok = t0 + t < L;
+      const int64_t m = row0 + t0 + (ok ? t : 0);
+      float g2 = 0.f;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int t = t_a + 8 * hh;
-        if (t0 + t < L) {
-          const __nv_bfloat162 xv = *reinterpret_cast<const __nv_bfloat162*>(Xb + swz(t, pc, M2_P));
-          *reinterpret_cast<float2*>(y + (row0 + t0 + t) * ldy + (int64_t)h * M2_P + pc) =
-              make_float2(fmaf(Dh, __low2float(xv), yacc[nt][2 * hh]), fmaf(Dh, __high2float(xv), yacc[nt][2 * hh + 1]));
-        }
+      for (int nt = 0; nt < 4; ++nt) {
+        const int pc = hf * 32 + nt * 8 + 2 * cq;
+        const int c = h * M2_P + pc;
+        const __nv_bfloat162 xv = *reinterpret_cast<const __nv_bfloat162*>(Xb + swz(t, pc, M2_P));
+        const __nv_bfloat162 zv = *reinterpret_cast<const __nv_bfloat162*>(proj + m * ldp + c);
+        const float2 wv = *reinterpret_cast<const float2*>(norm_w + c);
+        const float g0 = silu_gate(fmaf(Dh, __low2float(xv), yacc[nt][2 * hh]), __low2float(zv));
+        const float g1 = silu_gate(fmaf(Dh, __high2float(xv), yacc[nt][2 * hh + 1]), __high2float(zv));
+        if (ok) *reinterpret_cast<uint32_t*>(o + m * ldo + c) = pack_bf16(g0 * wv.x, g1 * wv.y);
+        g2 = fmaf(g0, g0, fmaf(g1, g1, g2));
       }
+      g2 += __shfl_xor_sync(0xffffffffu, g2, 1);
+      g2 += __shfl_xor_sync(0xffffffffu, g2, 2);
+      if (ok && cq == 0) atomicAdd(ss + m, g2);
     }
     // carry: h = exp(A_Q) h + X^T diag(w) B on this warp's (p, n) block
     {
@@ -405,7 +462,7 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
       }
     }
     store_h();
-    if (warp == 0 && ch + 1 < nch) scan(buf ^ 1);
+    if (warp == 0 && ch + 1 < nch) scan(buf ^ 1, dr0, dr1);
   }
 #pragma unroll
   for (int nt = 0; nt < HT; ++nt) {
@@ -414,68 +471,28 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
   }
 }
 
-// g = y * SiLU(z) in place (y fp32 [M][Ek], z bf16 at proj[m][z_col..]); ss[m] = sum g^2
-__global__ void __launch_bounds__(256) m2_gate_ss_kernel(float* __restrict__ y, int Ek,
-                                                         const __nv_bfloat16* __restrict__ proj, int64_t ldp,
-                                                         float* __restrict__ ss) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float red[8];
-  const int64_t m = blockIdx.x;
-  float s = 0.f;
-  for (int c = threadIdx.x; c < Ek; c += 256) {
-    const float z = __bfloat162float(proj[m * ldp + c]);
-    const float gv = y[m * Ek + c] * (z / (1.0f + expf(-z)));
-    y[m * Ek + c] = gv;
-    s = fmaf(gv, gv, s);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int i = 0; i < 8; ++i) t += red[i];
-    ss[m] = t;
-  }
-}
-
-// o = g / sqrt(ss / E + eps) * w -> bf16
-__global__ void m2_norm_apply_kernel(const float* __restrict__ g, int Ek, const float* __restrict__ ss, int E,
-                                     float eps, const float* __restrict__ w, __nv_bfloat16* __restrict__ o, int64_t n) {
-  pdl_trigger();
-  pdl_wait();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / Ek;
-    const int c = (int)(i % Ek);
-    o[i] = __float2bfloat16_rn(g[i] * (1.0f / sqrtf(ss[m] / (float)E + eps)) * w[c]);
-  }
-}
-
 }  // namespace
 
 cudaError_t launch_m2_scan(const __nv_bfloat16* proj, int64_t ldp, int dt_col, const __nv_bfloat16* u, int64_t ldu,
                            int b_col, int c_col, int heads_per_group, const float* dt_bias, const float* a_log,
-                           const float* d_skip, float* hstate, float* y, int64_t ldy, int batch, int L, int Hk, int P,
-                           int N, cudaStream_t s) {
+                           const float* d_skip, const float* norm_w, float* hstate, __nv_bfloat16* o, int64_t ldo,
+                           float* ss, int batch, int L, int Hk, int P, int N, cudaStream_t s) {
   if (batch <= 0 || L <= 0) return cudaSuccess;
-  if (P != M2_P) return cudaErrorInvalidValue;
+  if (P != M2_P || (ldp % 2) != 0 || (ldo % 2) != 0) return cudaErrorInvalidValue;
   cudaError_t e;
+  dim3 grid(Hk, batch);
   if (L == 1) {
-    const int64_t rows = (int64_t)batch * Hk * M2_P;
-    const unsigned blocks = (unsigned)((rows * (N / 8) + 255) / 256);
     switch (N) {
-      case 128: e = launch(m2_scan_step_kernel<128>, blocks, 256, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
-                           heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, rows, Hk); break;
-      case 64: e = launch(m2_scan_step_kernel<64>, blocks, 256, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
-                          heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, rows, Hk); break;
-      case 16: e = launch(m2_scan_step_kernel<16>, blocks, 256, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
-                          heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, rows, Hk); break;
+      case 128: e = launch(m2_scan_step_kernel<128>, grid, 256, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
+                           heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, Hk); break;
+      case 64: e = launch(m2_scan_step_kernel<64>, grid, 256, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
+                          heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, Hk); break;
+      case 16: e = launch(m2_scan_step_kernel<16>, grid, 128, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
+                          heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, Hk); break;
       default: return cudaErrorInvalidValue;
     }
     return e != cudaSuccess ? e : cudaGetLastError();
   }
-  dim3 grid(Hk, batch);
   if (L >= kSsdChunkMinL && (N == 128 || N == 64) && (ldu % 8) == 0 && (b_col % 8) == 0 && (c_col % 8) == 0) {
     static bool attr = false;
     if (!attr) {
@@ -485,38 +502,21 @@ cudaError_t launch_m2_scan(const __nv_bfloat16* proj, int64_t ldp, int dt_col, c
     }
     if (N == 128)
       e = launch(m2_ssd_chunk_kernel<128>, grid, 256, ssd_smem_bytes<128>(), s, proj, ldp, dt_col, u, ldu, b_col, c_col,
-                 heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, L, Hk);
+                 heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, L, Hk);
     else
       e = launch(m2_ssd_chunk_kernel<64>, grid, 256, ssd_smem_bytes<64>(), s, proj, ldp, dt_col, u, ldu, b_col, c_col,
-                 heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, L, Hk);
+                 heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, L, Hk);
     return e != cudaSuccess ? e : cudaGetLastError();
   }
   switch (N) {
     case 128: e = launch(m2_scan_kernel<128>, grid, M2_THREADS, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
-                         heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, L, Hk); break;
+                         heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, L, Hk); break;
     case 64: e = launch(m2_scan_kernel<64>, grid, M2_THREADS, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
-                        heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, L, Hk); break;
+                        heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, L, Hk); break;
     case 16: e = launch(m2_scan_kernel<16>, grid, M2_THREADS, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
-                        heads_per_group, dt_bias, a_log, d_skip, hstate, y, ldy, L, Hk); break;
+                        heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, L, Hk); break;
     default: return cudaErrorInvalidValue;
   }
-  return e != cudaSuccess ? e : cudaGetLastError();
-}
-
-cudaError_t launch_m2_gate_ss(float* y, int Ek, const __nv_bfloat16* proj, int64_t ldp, float* ss, int64_t M,
-                              cudaStream_t s) {
-  if (M <= 0) return cudaSuccess;
-  cudaError_t e = launch(m2_gate_ss_kernel, (unsigned)M, 256, 0, s, y, Ek, proj, ldp, ss);
-  return e != cudaSuccess ? e : cudaGetLastError();
-}
-
-cudaError_t launch_m2_norm_apply(const float* g, int Ek, const float* ss, int E, float eps, const float* w,
-                                 __nv_bfloat16* o, int64_t M, cudaStream_t s) {
-  const int64_t n = M * Ek;
-  if (n <= 0) return cudaSuccess;
-  const int64_t blocks = (n + 255) / 256;
-  cudaError_t e = launch(m2_norm_apply_kernel, (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s, g, Ek,
-                         ss, E, eps, w, o, n);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -525,9 +525,7 @@ cudaError_t preload_ssd() {
   for (const void* f : {(const void*)m2_scan_kernel<128>, (const void*)m2_scan_kernel<64>,
                         (const void*)m2_scan_kernel<16>, (const void*)m2_scan_step_kernel<128>,
                         (const void*)m2_scan_step_kernel<64>, (const void*)m2_scan_step_kernel<16>,
-                        (const void*)m2_ssd_chunk_kernel<128>, (const void*)m2_ssd_chunk_kernel<64>,
-                        (const void*)m2_gate_ss_kernel,
-                        (const void*)m2_norm_apply_kernel}) {
+                        (const void*)m2_ssd_chunk_kernel<128>, (const void*)m2_ssd_chunk_kernel<64>}) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
   }
