@@ -133,18 +133,20 @@ __global__ void __launch_bounds__(M2_THREADS) m2_scan_kernel(
 // layer at batch 16) is the whole cost, so the work is spread as a stream rather than one thread
 // per channel (the multi-token kernel's 66 registers x 256 threads fit 3 CTAs per SM and ran 1280
 // CTAs in ~3 latency-bound waves): one CTA per (head, sequence), N / 8 lanes per state row (h, p),
-// 8 states per lane (two float4 of h, one 16-B run each of B and C), each lane group walking
-// 64 N / 8 / threads rows with all its loads issued first; the row's C.h by shuffles inside the lane
+// 8 states per lane (two float4 of h, one 16-B run each of B and C), 128 threads and <= 56
+// registers (9 CTAs per SM: all 1280 CTAs of Mamba-2-2.7B at batch 16 resident at once), each lane
+// group walking 64 N / 8 / 128 rows four at a time with all of a pass's loads issued first; the row's C.h by shuffles inside the lane
 // group; one ss atomic per CTA.
 template <int N>
-__global__ void __launch_bounds__(256) m2_scan_step_kernel(
+__global__ void __launch_bounds__(128, 9) m2_scan_step_kernel(
     const __nv_bfloat16* __restrict__ proj, int64_t ldp, int dt_col, const __nv_bfloat16* __restrict__ u,
     int64_t ldu, int b_col, int c_col, int heads_per_group, const float* __restrict__ dt_bias,
     const float* __restrict__ a_log, const float* __restrict__ d_skip, const float* __restrict__ norm_w,
     float* __restrict__ hstate, __nv_bfloat16* __restrict__ o, int64_t ldo, float* __restrict__ ss, int Hk) {
   constexpr int LPR = N / 8;                                 // lanes per state row (power of two <= 16)
-  constexpr int THREADS = M2_P * LPR < 256 ? M2_P * LPR : 256;
+  constexpr int THREADS = M2_P * LPR < 128 ? M2_P * LPR : 128;
   constexpr int RPT = M2_P * LPR / THREADS;                  // rows per lane group
+  constexpr int PASS = RPT < 4 ? RPT : 4;                    // rows in flight per lane group
   constexpr int RSTEP = THREADS / LPR;
   __shared__ float sred[THREADS / 32];
   pdl_trigger();
@@ -156,13 +158,6 @@ __global__ void __launch_bounds__(256) m2_scan_step_kernel(
   pdl_wait();
   const __nv_bfloat16* urow = u + (int64_t)b * ldu;
   float* hp = hstate + (((int64_t)b * Hk + h) * M2_P) * N + 8 * sub;
-  float4 h0[RPT], h1[RPT];
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int p = p0 + k * RSTEP;
-    h0[k] = *reinterpret_cast<const float4*>(hp + (int64_t)p * N);
-    h1[k] = *reinterpret_cast<const float4*>(hp + (int64_t)p * N + 4);
-  }
   const uint4 bv = *reinterpret_cast<const uint4*>(urow + b_col + (int64_t)g * N + 8 * sub);
   const uint4 cv = *reinterpret_cast<const uint4*>(urow + c_col + (int64_t)g * N + 8 * sub);
   const float dt = softplus(__bfloat162float(proj[(int64_t)b * ldp + dt_col + h]) + bias);
@@ -171,26 +166,38 @@ __global__ void __launch_bounds__(256) m2_scan_step_kernel(
   const __nv_bfloat16* cc = reinterpret_cast<const __nv_bfloat16*>(&cv);
   float g2 = 0.f;
 #pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int p = p0 + k * RSTEP;
-    const float xv = __bfloat162float(urow[(int64_t)h * M2_P + p]);
-    const float dtx = dt * xv;
-    float hs[8] = {h0[k].x, h0[k].y, h0[k].z, h0[k].w, h1[k].x, h1[k].y, h1[k].z, h1[k].w};
-    float acc = 0.f;
+  for (int k0 = 0; k0 < RPT; k0 += PASS) {
+    float4 h0[PASS], h1[PASS];
+    float xr[PASS], zr[PASS];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      hs[j] = fmaf(dA, hs[j], dtx * __bfloat162float(bb[j]));
-      acc = fmaf(__bfloat162float(cc[j]), hs[j], acc);
+    for (int k = 0; k < PASS; ++k) {  // every load of the pass issued before any use
+      const int p = p0 + (k0 + k) * RSTEP;
+      h0[k] = *reinterpret_cast<const float4*>(hp + (int64_t)p * N);
+      h1[k] = *reinterpret_cast<const float4*>(hp + (int64_t)p * N + 4);
+      xr[k] = __bfloat162float(urow[h * M2_P + p]);
+      zr[k] = sub == 0 ? __bfloat162float(proj[(int64_t)b * ldp + h * M2_P + p]) : 0.f;
     }
 #pragma unroll
-    for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    *reinterpret_cast<float4*>(hp + (int64_t)p * N) = make_float4(hs[0], hs[1], hs[2], hs[3]);
-    *reinterpret_cast<float4*>(hp + (int64_t)p * N + 4) = make_float4(hs[4], hs[5], hs[6], hs[7]);
-    if (sub == 0) {
-      const int c = h * M2_P + p;
-      const float gv = silu_gate(fmaf(Dh, xv, acc), __bfloat162float(proj[(int64_t)b * ldp + c]));
-      o[(int64_t)b * ldo + c] = __float2bfloat16_rn(gv * norm_w[c]);
-      g2 = fmaf(gv, gv, g2);
+    for (int k = 0; k < PASS; ++k) {
+      const int p = p0 + (k0 + k) * RSTEP;
+      const float dtx = dt * xr[k];
+      float hs[8] = {h0[k].x, h0[k].y, h0[k].z, h0[k].w, h1[k].x, h1[k].y, h1[k].z, h1[k].w};
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        hs[j] = fmaf(dA, hs[j], dtx * __bfloat162float(bb[j]));
+        acc = fmaf(__bfloat162float(cc[j]), hs[j], acc);
+      }
+#pragma unroll
+      for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      *reinterpret_cast<float4*>(hp + (int64_t)p * N) = make_float4(hs[0], hs[1], hs[2], hs[3]);
+      *reinterpret_cast<float4*>(hp + (int64_t)p * N + 4) = make_float4(hs[4], hs[5], hs[6], hs[7]);
+      if (sub == 0) {
+        const int c = h * M2_P + p;
+        const float gv = silu_gate(fmaf(Dh, xr[k], acc), zr[k]);
+        o[(int64_t)b * ldo + c] = __float2bfloat16_rn(gv * norm_w[c]);
+        g2 = fmaf(gv, gv, g2);
+      }
     }
   }
 #pragma unroll
@@ -235,8 +242,8 @@ SSM_DEV uint32_t scale_bf16x2(uint32_t v, float a, float b) {
 }
 
 template <int N>
-constexpr size_t ssd_smem_bytes() {
-  return (size_t)2 * SQ * M2_P * 2 + (size_t)4 * SQ * N * 2 + (size_t)SQ * SQ * 2 + (size_t)M2_P * N * 2 + 6 * SQ * 4;
+constexpr size_t ssd_smem_bytes() {  // x, z, B double-buffered; C single; G o decay; h_prev; dt, A_t, w
+  return (size_t)4 * SQ * M2_P * 2 + (size_t)3 * SQ * N * 2 + (size_t)SQ * SQ * 2 + (size_t)M2_P * N * 2 + 6 * SQ * 4;
 }
 
 template <int N>
@@ -250,9 +257,10 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
   constexpr int HT = N / 16;  // 8-wide n-tiles per warp in the carry update (N / 2 columns)
   extern __shared__ __align__(128) unsigned char ssd_smem[];
   __nv_bfloat16* sX = reinterpret_cast<__nv_bfloat16*>(ssd_smem);  // [2][SQ][P]
-  __nv_bfloat16* sB = sX + 2 * SQ * M2_P;                           // [2][SQ][N]
-  __nv_bfloat16* sC = sB + 2 * SQ * N;                              // [2][SQ][N]
-  __nv_bfloat16* sM = sC + 2 * SQ * N;                              // [SQ][SQ]  (G o decay)
+  __nv_bfloat16* sZ = sX + 2 * SQ * M2_P;                           // [2][SQ][P]  gate input z
+  __nv_bfloat16* sB = sZ + 2 * SQ * M2_P;                           // [2][SQ][N]
+  __nv_bfloat16* sC = sB + 2 * SQ * N;                              // [SQ][N]  (dead once in registers)
+  __nv_bfloat16* sM = sC + SQ * N;                                  // [SQ][SQ]  (G o decay)
   __nv_bfloat16* sH = sM + SQ * SQ;                                 // [P][N]    h_prev (bf16 copy)
   float* sdt = reinterpret_cast<float*>(sH + M2_P * N);             // [2][SQ]
   float* sAc = sdt + 2 * SQ;                                        // [2][SQ]   log2-scaled A_t
@@ -290,17 +298,29 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
     for (int k = 0; k < XPT; ++k) {
       const int i = tid + 256 * k, r = i / (M2_P / 8), c = i % (M2_P / 8);
       const bool ok = t0 + r < L;
-      const __nv_bfloat16* urow = u + (row0 + (ok ? t0 + r : 0)) * ldu;
-      cp_async16(sX + buf * SQ * M2_P + swz(r, c * 8, M2_P), urow + (int64_t)h * M2_P + c * 8, ok);
+      const int64_t row = row0 + (ok ? t0 + r : 0);
+      const int so = buf * SQ * M2_P + swz(r, c * 8, M2_P);
+      cp_async16(sX + so, u + row * ldu + (int64_t)h * M2_P + c * 8, ok);
+      cp_async16(sZ + so, proj + row * ldp + (int64_t)h * M2_P + c * 8, ok);
     }
 #pragma unroll
     for (int k = 0; k < BPT; ++k) {
       const int i = tid + 256 * k, r = i / (N / 8), c = i % (N / 8);
       const bool ok = t0 + r < L;
       const __nv_bfloat16* urow = u + (row0 + (ok ? t0 + r : 0)) * ldu + (int64_t)g * N + c * 8;
-      const int so = buf * SQ * N + swz(r, c * 8, N);
-      cp_async16(sB + so, urow + b_col, ok);
-      cp_async16(sC + so, urow + c_col, ok);
+      cp_async16(sB + buf * SQ * N + swz(r, c * 8, N), urow + b_col, ok);
+    }
+  };
+  // C of the chunk at t0 into the single C tile (issued once every warp holds the previous chunk's
+  // C fragments in registers)
+  auto load_c = [&](int t0) {
+    constexpr int BPT = SQ * (N / 8) / 256;
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+      const int i = tid + 256 * k, r = i / (N / 8), c = i % (N / 8);
+      const bool ok = t0 + r < L;
+      const __nv_bfloat16* urow = u + (row0 + (ok ? t0 + r : 0)) * ldu + (int64_t)g * N + c * 8;
+      cp_async16(sC + swz(r, c * 8, N), urow + c_col, ok);
     }
   };
   // warp 0 alone handles dt: raw values of the chunk at t0 (tokens t0 + 2 lane, + 1; padded -> dt 0),
@@ -328,6 +348,7 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
 
   const int nch = (L + SQ - 1) / SQ;
   load_tile(0, 0);
+  load_c(0);
   cp_async_commit();
   store_h();
   float dr0 = 0.f, dr1 = 0.f;
@@ -345,8 +366,9 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
       if (warp == 0) load_dt(t0 + SQ, dr0, dr1);
     }
     const __nv_bfloat16* Xb = sX + buf * SQ * M2_P;
+    const __nv_bfloat16* Zb = sZ + buf * SQ * M2_P;
     const __nv_bfloat16* Bb = sB + buf * SQ * N;
-    const __nv_bfloat16* Cb = sC + buf * SQ * N;
+    const __nv_bfloat16* Cb = sC;
     const float* Ac = sAc + buf * SQ;
     const int t_a = rb * 16 + gq;  // this lane's accumulator rows t_a, t_a + 8
     const float At0 = Ac[t_a], At1 = Ac[t_a + 8];
@@ -397,7 +419,11 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
         yacc[nt][0] *= e0; yacc[nt][1] *= e0; yacc[nt][2] *= e1; yacc[nt][3] *= e1;
       }
     }
-    __syncthreads();  // sM complete; every warp is done reading sH
+    __syncthreads();  // sM complete; every warp is done reading sH and sC
+    if (ch + 1 < nch) {
+      load_c(t0 + SQ);
+      cp_async_commit();
+    }
     // Y += (G o decay) X
 #pragma unroll
     for (int ks = 0; ks < SQ / 16; ++ks) {
@@ -423,7 +449,7 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
         const int pc = hf * 32 + nt * 8 + 2 * cq;
         const int c = h * M2_P + pc;
         const __nv_bfloat162 xv = *reinterpret_cast<const __nv_bfloat162*>(Xb + swz(t, pc, M2_P));
-        const __nv_bfloat162 zv = *reinterpret_cast<const __nv_bfloat162*>(proj + m * ldp + c);
+        const __nv_bfloat162 zv = *reinterpret_cast<const __nv_bfloat162*>(Zb + swz(t, pc, M2_P));
         const float2 wv = *reinterpret_cast<const float2*>(norm_w + c);
         const float g0 = silu_gate(fmaf(Dh, __low2float(xv), yacc[nt][2 * hh]), __low2float(zv));
         const float g1 = silu_gate(fmaf(Dh, __high2float(xv), yacc[nt][2 * hh + 1]), __high2float(zv));
@@ -483,9 +509,9 @@ cudaError_t launch_m2_scan(const __nv_bfloat16* proj, int64_t ldp, int dt_col, c
   dim3 grid(Hk, batch);
   if (L == 1) {
     switch (N) {
-      case 128: e = launch(m2_scan_step_kernel<128>, grid, 256, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
+      case 128: e = launch(m2_scan_step_kernel<128>, grid, 128, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
                            heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, Hk); break;
-      case 64: e = launch(m2_scan_step_kernel<64>, grid, 256, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
+      case 64: e = launch(m2_scan_step_kernel<64>, grid, 128, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
                           heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, Hk); break;
       case 16: e = launch(m2_scan_step_kernel<16>, grid, 128, 0, s, proj, ldp, dt_col, u, ldu, b_col, c_col,
                           heads_per_group, dt_bias, a_log, d_skip, norm_w, hstate, o, ldo, ss, Hk); break;
