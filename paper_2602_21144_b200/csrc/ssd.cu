@@ -28,7 +28,7 @@ constexpr int kSsdChunkMinL = 16;
 // channel c of row m, g = y SiLU(z) with z = proj[m][c]; the kernel stores o = bf16(g w[c]) (the
 // out_proj's A operand, norm weight folded in) and adds g^2 into ss[m] (zeroed by the in_proj's
 // epilogue); the out_proj epilogue then scales its row by 1 / sqrt(ss[m] / E + eps).
-SSM_DEV float silu_gate(float yv, float zv) { return yv * (zv / (1.0f + expf(-zv))); }
+SSM_DEV float silu_gate(float yv, float zv) { return yv * silu<true>(zv); }  // MUFU ex2 + rcp (bf16 output)
 
 // proj [M][ldp] bf16: dt raw at column dt_col + h; u [M][ldu] bf16: x at x_col + h P, B at b_col,
 // C at c_col (group g of the head: + g N).  h_state [batch][Hk][P][N] fp32 in place; y [M][Ek] fp32.
@@ -243,7 +243,8 @@ SSM_DEV uint32_t scale_bf16x2(uint32_t v, float a, float b) {
 
 template <int N>
 constexpr size_t ssd_smem_bytes() {  // x, z, B double-buffered; C single; G o decay; h_prev; dt, A_t, w
-  return (size_t)4 * SQ * M2_P * 2 + (size_t)3 * SQ * N * 2 + (size_t)SQ * SQ * 2 + (size_t)M2_P * N * 2 + 6 * SQ * 4;
+  return (size_t)4 * SQ * M2_P * 2 + (size_t)3 * SQ * N * 2 + (size_t)SQ * SQ * 2 + (size_t)M2_P * N * 2 + 6 * SQ * 4 +
+         M2_P * 4;
 }
 
 template <int N>
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
   float* sdt = reinterpret_cast<float*>(sH + M2_P * N);             // [2][SQ]
   float* sAc = sdt + 2 * SQ;                                        // [2][SQ]   log2-scaled A_t
   float* sW = sAc + 2 * SQ;                                         // [2][SQ]   exp(A_Q - A_s) dt_s
+  float* sWn = sW + 2 * SQ;                                         // [P]       gated-norm weights
   pdl_trigger();
   const int h = blockIdx.x, b = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -346,6 +348,7 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
     *reinterpret_cast<float2*>(sW + buf * SQ + 2 * lane) = make_float2(ex2_approx(tot - c0) * d0, ex2_approx(tot - c1) * d1);
   };
 
+  if (tid < M2_P) sWn[tid] = norm_w[h * M2_P + tid];  // the head's norm weights (visible after the first barrier)
   const int nch = (L + SQ - 1) / SQ;
   load_tile(0, 0);
   load_c(0);
@@ -450,7 +453,7 @@ __global__ void __launch_bounds__(256, 2) m2_ssd_chunk_kernel(
         const int c = h * M2_P + pc;
         const __nv_bfloat162 xv = *reinterpret_cast<const __nv_bfloat162*>(Xb + swz(t, pc, M2_P));
         const __nv_bfloat162 zv = *reinterpret_cast<const __nv_bfloat162*>(Zb + swz(t, pc, M2_P));
-        const float2 wv = *reinterpret_cast<const float2*>(norm_w + c);
+        const float2 wv = *reinterpret_cast<const float2*>(sWn + pc);
         const float g0 = silu_gate(fmaf(Dh, __low2float(xv), yacc[nt][2 * hh]), __low2float(zv));
         const float g1 = silu_gate(fmaf(Dh, __high2float(xv), yacc[nt][2 * hh + 1]), __high2float(zv));
         if (ok) *reinterpret_cast<uint32_t*>(o + m * ldo + c) = pack_bf16(g0 * wv.x, g1 * wv.y);
