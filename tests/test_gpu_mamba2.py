@@ -106,3 +106,15 @@ def test_mamba2_short_calls_per_token_scan_vs_oracle():
     m2 = synth.Mamba2Dims(d_model=256, d_inner=512, d_state=128)
     got, ref, res, _, _ = _run(m2, 1, 3, [7, 5, 13], 2, L.SSM_AR2_INT8)
     assert rel(got[0] - res, ref - res) < TOL["bf16"]
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_mamba2_virtual_tp_multi_chunk_vs_oracle(k):
+    """Virtual TP with prompts spanning several 64-token SSD chunks (chunk-unaligned, two calls), so
+    each rank's chunked scan, its partial sums of squares and their all-reduce before the row-scaled
+    out_proj all count; replicas must stay bitwise equal."""
+    m2 = synth.Mamba2Dims(d_model=256, d_inner=512, d_state=128)
+    got, ref, res, _, _ = _run(m2, k, 2, [97, 70], 3, L.SSM_AR2_FP32)
+    for r in range(1, k):
+        np.testing.assert_array_equal(got[r], got[0])
+    assert rel(got[0] - res, ref - res) < TOL["bf16"]
