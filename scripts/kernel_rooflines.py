@@ -6,7 +6,7 @@ stream from HBM), and its ALGORITHMIC work -- SURVEY.md §8(d) per-unit figures 
 launch processes -- is divided by the median launch time and by the binding peak
 (MEASURED_PEAKS.json: hbm_gbs, bf16_tflops_sustained; MUFU from the guide's unit count:
 16 ex2/clk/SM x 148 SMs x the max SM clock).
-    python scripts/kernel_rooflines.py [--layers 4] [--json out.json]
+    python scripts/kernel_rooflines.py [--layers 8] [--json out.json]
 """
 import argparse
 import json
@@ -26,7 +26,7 @@ from paper_2602_21144_b200.stack import MixerStack, synthetic_layer  # noqa: E40
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--config", default="mamba2.8b")
-    p.add_argument("--layers", type=int, default=4)
+    p.add_argument("--layers", type=int, default=8)
     p.add_argument("--json", default="")
     a = p.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -76,6 +76,23 @@ def main():
     tp = probe(["in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj"], pre, 2)
     rt = torch.randn((B, D), generator=g, device="cuda")
     td = probe(["in_proj_decode", "decode_step", "out_proj"], lambda: stack.decode_step(rt), 4)
+    # the persistent whole-stack decode (one cooperative launch per token over the same layers):
+    # CUDA events around eager decode steps on the launching stream
+    pst = MixerStack(mx, layers, B, Lp).persistent()
+    res.copy_(x0)
+    pst.prefill_chunk(res)
+    for _ in range(3):
+        pst.decode_step(rt)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(10):
+        pst.decode_step(rt)
+    ev[1].record()
+    torch.cuda.synchronize()
+    t_pst = ev[0].elapsed_time(ev[1]) / 10 * 1e-3
+    K = dims.d_conv
+    per_layer = (2 * E * D * 2 + D * E * 2 + P * E * 2 + E * R * 2 + E * (K + 3 + N) * 4
+                 + 2 * B * E * N * 4 + 2 * B * (K - 1) * E * 2)
     ch_tok = M * E
     rows = [
         # (row, kernel, seconds, work, unit, peak, bound, work description)
@@ -98,6 +115,9 @@ def main():
          "h r/w fp32 + W_dt + dbc + u, z, g"),
         ("a10", "decode out_proj (split-K)", td["out_proj"], 2.0 * D * E + 2.0 * B * E + 8.0 * B * D, "B", hbm, "hbm",
          "W_out + g + residual r/w"),
+        ("a10", f"persistent whole-stack decode ({a.layers} layers/launch)", t_pst,
+         float(a.layers * per_layer + 2 * B * D * 4), "B", hbm, "hbm",
+         "per layer W_in + W_out + W_x + W_dt + vectors + h r/w + conv window r/w; + residual"),
     ]
     out = []
     print(f"{a.config}: batch {B}, prefill M={M} tokens, d_model {D}, d_inner {E}; peaks: HBM {hbm / 1e9:.0f} GB/s, "
