@@ -3,6 +3,6 @@
 for rep in 1 2; do
   for v in base "$@"; do
     if [ $v = base ]; then R=""; else R="build/ab/$v"; fi
-    echo "== $v"; DS_PKG_ROOT=$R timeout 300 python scripts/dstack_trace.py 2>&1 | grep -E "us/token|^B |B items|bar A|bar B|^layer "
+    echo "== $v"; DS_PKG_ROOT=$R timeout 300 python scripts/dstack_trace.py 2>&1 | grep -E "us/token|^A |^B |bar A|bar B|bar C|^C |^layer |A epi units"
   done
 done
