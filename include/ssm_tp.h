@@ -219,6 +219,28 @@ ssm_status_t ssm_mixer_prefill(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_st
                                const void* x_in, float* residual, int32_t batch, int32_t seqlen,
                                uint32_t flags, void* workspace, size_t ws_bytes, void* stream);
 
+/* Prefill of one pre-norm block with the norm folded around the projections (TP = 1, bf16;
+ * PAPER.md:151-174 with the pre-norm of reading Q16, rounding as reading Q22):
+ *   residual += mixer(RMSNorm(residual))      (RMSNorm weight 1, eps norm_eps)
+ * where x_in = bf16(residual) itself (NOT normalised) and ss_in[m] = sum_d residual[m][d]^2 (from
+ * ssm_rowstats, or from the previous layer's call): the in_proj contracts bf16(r) and scales its row
+ * m by 1 / sqrt(ss_in[m] / D + eps) in the epilogue, so no normalisation pass touches the residual.
+ * If x_next / ss_next are given, the out_proj epilogue that adds into the residual also writes
+ * x_next = bf16(new residual) [batch*seqlen, D] and ss_next = its row sums of squares (fixed-order
+ * reduction of per-32-column partials): the next layer's x_in / ss_in.  x_next may alias x_in (the
+ * in_proj has consumed it by then); ss_next must not alias ss_in.  x_in, x_next and residual
+ * 16-B aligned, ss_in / ss_next 4-B aligned.
+ * Errors: as ssm_mixer_prefill; SSM_ERR_UNSUPPORTED at tp_size > 1, fp32 handles, SSM_TP_NAIVE or
+ * strides the tcgen05 GEMM cannot describe (use ssm_rmsnorm + ssm_mixer_prefill there). */
+ssm_status_t ssm_mixer_prefill_normed(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, const void* x_in,
+                                      const float* ss_in, float norm_eps, float* residual, void* x_next,
+                                      float* ss_next, int32_t batch, int32_t seqlen, uint32_t flags, void* workspace,
+                                      size_t ws_bytes, void* stream);
+
+/* x_out[m] = bf16(residual[m]) and ss_out[m] = sum_d residual[m][d]^2 for M rows of D = d_model (the first
+ * layer's inputs of ssm_mixer_prefill_normed).  bf16 handles; 16-B aligned residual and x_out. */
+ssm_status_t ssm_rowstats(ssm_tp_t tp, const float* residual, void* x_out, float* ss_out, int64_t M, void* stream);
+
 /* One decode step (seqlen = 1) reading and updating the state in place.
  * Same arguments as prefill with seqlen = 1.  Graph-capturable. */
 ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st,

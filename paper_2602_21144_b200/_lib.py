@@ -85,6 +85,9 @@ def _load():
         "ssm_state_reset": (st, [vp, vp]),
         "ssm_state_free": (st, [vp]),
         "ssm_mixer_prefill": (st, [vp, P(ssm_layer_weights_t), vp, vp, vp, i32, i32, C.c_uint32, vp, sz, vp]),
+        "ssm_mixer_prefill_normed": (st, [vp, P(ssm_layer_weights_t), vp, vp, vp, C.c_float, vp, vp, vp, i32, i32,
+                                          C.c_uint32, vp, sz, vp]),
+        "ssm_rowstats": (st, [vp, vp, vp, vp, i64, vp]),
         "ssm_mixer_decode": (st, [vp, P(ssm_layer_weights_t), vp, vp, vp, i32, C.c_uint32, vp, sz, vp]),
         "ssm_mixer_decode_block": (st, [vp, P(ssm_layer_weights_t), vp, vp, i32, C.c_float, C.c_uint32, vp, sz, vp]),
         "ssm_qallreduce": (st, [vp, vp, vp, sz, C.c_uint32, vp]),
@@ -132,6 +135,7 @@ LIB = _load()
 EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "ssm_comm_bytes", "ssm_workspace_bytes",
             "ssm_workspace_bytes_flags",
             "ssm_state_bytes", "ssm_state_alloc", "ssm_state_reset", "ssm_state_free", "ssm_mixer_prefill",
+            "ssm_mixer_prefill_normed", "ssm_rowstats",
             "ssm_mixer_decode", "ssm_mixer_decode_block", "ssm_qallreduce", "ssm_rmsnorm", "ssm_tp_check", "ssm_tp_stats", "ssm_tp_epoch",
             "ssm_tp_barrier", "ssm_tp_launch_count", "ssm_tp_fused_calls", "ssm_tp_probe", "ssm_tp_probe_read",
             "ssm_packed_weight_bytes", "ssm_pack_weight", "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld",

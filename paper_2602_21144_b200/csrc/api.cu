@@ -105,7 +105,7 @@ size_t h_total_bytes(const ssm_tp_s* t, int batch) {
 }
 
 struct WsLayout {
-  size_t xz, u, dbc, dlow, bc, delta, g, part, xn, xzf, uf, total;
+  size_t xz, u, dbc, dlow, bc, delta, g, part, xn, xzf, uf, ssq, total;
 };
 
 // naive: + the all-gathered full-width activations of the SSM_TP_NAIVE arm (xz [M][2E], u [M][E])
@@ -125,6 +125,7 @@ WsLayout ws_layout(const ssm_tp_s* t, int64_t M, bool naive = false) {
   L.xn = take(M * t->cfg.d_model * es);                  // pre-norm output (ssm_mixer_decode_block)
   L.xzf = take(naive ? M * 2 * t->cfg.d_inner * es : 0);
   L.uf = take(naive ? M * t->cfg.d_inner * es : 0);
+  L.ssq = take(M * ((t->cfg.d_model + 31) / 32) * 4);    // out_proj row-chunk sums of squares (prefill_normed)
   L.total = off;
   return L;
 }
@@ -245,7 +246,11 @@ Peers group_peers(const ssm_tp_s* t, int gsize) {
 // Q16) first, by the rmsnorm kernel.
 ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* st, const void* x_in, float* residual,
                        int batch, int seqlen, uint32_t flags, void* ws, bool decode, cudaStream_t s,
-                       const float* norm_res = nullptr, float norm_eps = 0.f) {
+                       const float* norm_res = nullptr, float norm_eps = 0.f, const float* ss_in = nullptr,
+                       void* x_next = nullptr, float* ss_next = nullptr) {
+  // ss_in (prefill_normed): x_in is bf16(residual) itself and the in_proj epilogue applies the pre-norm
+  // 1 / sqrt(ss_in / D + eps) per row; x_next / ss_next: the out_proj epilogue that adds into the
+  // residual also writes bf16(new residual) and its row statistic for the next layer (reading Q22)
   const ssm_config_t& c = t->cfg;
   const int64_t M = (int64_t)batch * seqlen;
   const int D = c.d_model, Ek = t->Ek, R = c.dt_rank, N = c.d_state, K = c.d_conv, P = t->P, hl = t->hloc;
@@ -381,8 +386,15 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       CU(launch_gather_cols(t->peers, t->k, half_off(ep_ag1), M, (int)(wn * es), xzb, ldxz * (int64_t)es, s));
     } else if (swap)
       CU(gemm(t, w->w_in, D, x_in, D, 2 * Ek, (int)M, D, 1, epi(kst, 1, xz, 2 * Ek), s, true, w->w_in_pk));
-    else
-      CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, epi(kst, 0, xz, 2 * Ek), s));
+    else {
+      Epilogue e = epi(kst, 0, xz, 2 * Ek);
+      if (ss_in) {
+        e.rss = ss_in;
+        e.rss_inv = 1.0f / (float)D;
+        e.rss_eps = norm_eps;
+      }
+      CU(gemm(t, x_in, D, w->w_in, D, (int)M, 2 * Ek, D, 1, e, s));
+    }
   }
   // naive: the conv output goes to this rank's half for the second all-gather
   if (naive) u = own_half(ep_ag2);
@@ -491,7 +503,16 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       e.qblk = c.qar_block;
       CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, e, s));
     } else {
-      CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D), s));
+      Epilogue e = epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D);
+      if (x_next) {
+        e.cpy = x_next;
+        e.ssq = reinterpret_cast<float*>(W + L.ssq);
+      }
+      CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, e, s));
+      if (x_next) {
+        t->launches++;
+        CU(launch_ssq_finalize(reinterpret_cast<float*>(W + L.ssq), (D + 31) / 32, ss_next, M, s));
+      }
     }
   }
   // (a9) AR#2 at the residual boundary
@@ -765,6 +786,37 @@ ssm_status_t ssm_mixer_prefill(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_st
   if ((int64_t)batch * seqlen == 0) return SSM_OK;
   return run_layer(tp, w, st, x_in, residual, batch, seqlen, flags, workspace, false,
                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+ssm_status_t ssm_mixer_prefill_normed(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, const void* x_in,
+                                      const float* ss_in, float norm_eps, float* residual, void* x_next,
+                                      float* ss_next, int32_t batch, int32_t seqlen, uint32_t flags, void* workspace,
+                                      size_t ws_bytes, void* stream) {
+  ssm_status_t s = check_call(tp, w, st, x_in, residual, batch, seqlen, flags, workspace, ws_bytes);
+  if (s != SSM_OK) return s;
+  if (!ss_in || ((x_next == nullptr) != (ss_next == nullptr))) return fail(SSM_ERR_ARG, "ss_in NULL, or x_next / ss_next not both set");
+  if (!(norm_eps >= 0.f)) return fail(SSM_ERR_ARG, "norm_eps must be >= 0");
+  const int D = tp->cfg.d_model, Ek = tp->Ek;
+  // the residual is updated by this rank's out_proj epilogue only at TP = 1 (at TP > 1 AR#2 does it);
+  // both projections on the tcgen05 GEMM
+  if (tp->k != 1 || !tp->bf16 || (flags & SSM_TP_NAIVE) || D % 8 ||
+      !gemm_tc_supported(x_in, D, w->w_in, D) || !gemm_tc_supported(w->w_out, Ek, w->w_out, Ek))
+    return fail(SSM_ERR_UNSUPPORTED, "prefill_normed: TP = 1, bf16, tcgen05-compatible strides only");
+  if ((reinterpret_cast<uintptr_t>(x_next) & 15) || ((reinterpret_cast<uintptr_t>(ss_in) | reinterpret_cast<uintptr_t>(ss_next)) & 3))
+    return fail(SSM_ERR_ARG, "x_next must be 16-B aligned, ss_in / ss_next 4-B aligned");
+  if ((int64_t)batch * seqlen == 0) return SSM_OK;
+  return run_layer(tp, w, st, x_in, residual, batch, seqlen, flags, workspace, false,
+                   reinterpret_cast<cudaStream_t>(stream), nullptr, norm_eps, ss_in, x_next, ss_next);
+}
+
+ssm_status_t ssm_rowstats(ssm_tp_t tp, const float* residual, void* x_out, float* ss_out, int64_t M, void* stream) {
+  if (!tp || !residual || !x_out || !ss_out) return fail(SSM_ERR_ARG, "NULL argument");
+  if (!tp->bf16) return fail(SSM_ERR_UNSUPPORTED, "ssm_rowstats: bf16 handles only");
+  if ((reinterpret_cast<uintptr_t>(residual) | reinterpret_cast<uintptr_t>(x_out)) & 15)
+    return fail(SSM_ERR_ARG, "pointers must be 16-B aligned");
+  tp->launches++;
+  CU(launch_rowstats(residual, x_out, ss_out, M, tp->cfg.d_model, reinterpret_cast<cudaStream_t>(stream)));
+  return SSM_OK;
 }
 
 ssm_status_t ssm_mixer_decode(ssm_tp_t tp, const ssm_layer_weights_t* w, ssm_state_t st, const void* x_in,

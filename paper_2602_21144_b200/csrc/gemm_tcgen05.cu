@@ -229,10 +229,34 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
         o[q].x += v[4 * q]; o[q].y += v[4 * q + 1]; o[q].z += v[4 * q + 2]; o[q].w += v[4 * q + 3];
         reinterpret_cast<float4*>(C)[q] = o[q];
       }
+      if (FK < 0 && e.cpy) {  // bf16 copy of the updated rows + their sums of squares (Epilogue::cpy / ssq)
+        uint4* cp = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.cpy) + base);
+        float sq = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 a = o[2 * q], b = o[2 * q + 1];
+          sq = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, sq))));
+          sq = fmaf(b.x, b.x, fmaf(b.y, b.y, fmaf(b.z, b.z, fmaf(b.w, b.w, sq))));
+          __nv_bfloat162 t0 = __floats2bfloat162_rn(a.x, a.y), t1 = __floats2bfloat162_rn(a.z, a.w);
+          __nv_bfloat162 t2 = __floats2bfloat162_rn(b.x, b.y), t3 = __floats2bfloat162_rn(b.z, b.w);
+          cp[q] = make_uint4(*reinterpret_cast<uint32_t*>(&t0), *reinterpret_cast<uint32_t*>(&t1),
+                             *reinterpret_cast<uint32_t*>(&t2), *reinterpret_cast<uint32_t*>(&t3));
+        }
+        e.ssq[(int64_t)m * ((N + 31) / 32) + n0 / 32] = sq;
+      }
     } else {
+      float sq = 0.f;
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) C[j] += v[j];
+        if (n0 + j < N) {
+          const float o = C[j] + v[j];
+          C[j] = o;
+          if (FK < 0 && e.cpy) {
+            reinterpret_cast<__nv_bfloat16*>(e.cpy)[base + j] = __float2bfloat16_rn(o);
+            sq = fmaf(o, o, sq);
+          }
+        }
+      if (FK < 0 && e.cpy) e.ssq[(int64_t)m * ((N + 31) / 32) + n0 / 32] = sq;
     }
   } else {  // EPI_ATOMIC_F32
     if (vec) {
@@ -916,6 +940,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   else if (!epi.trans && epi.kind == EPI_SOFTPLUS_BF16) var = 6;
   else if (epi.kind == EPI_QUANT_I8) var = 7;
   if (epi.rss && (var == 1 || var == 6)) return cudaErrorInvalidValue;  // no row scale in those epilogues
+  if (epi.cpy && (epi.kind != EPI_ADD_F32 || epi.trans || !epi.ssq || ts.ksplit > 1)) return cudaErrorInvalidValue;
   auto kfn = var == 2 ? gemm_tc_kernel<2> : var == 6 ? gemm_tc_kernel<6> : var == 7 ? gemm_tc_kernel<7> : gemm_tc_kernel<0>;
   if (var == 1) kfn = epi.P <= 64 * 3 ? gemm_tc_kernel<1, 3> : epi.P <= 64 * 4 ? gemm_tc_kernel<1, 4> : gemm_tc_kernel<1>;
   cudaError_t e_ = launch(kfn, grid, var_threads(var), smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi, A_blocked, lda, K,

@@ -44,6 +44,11 @@ struct Epilogue {
   // (its weight is folded into the A operand by the scan; reading M3).
   const float* rss;
   float rss_inv, rss_eps;
+  // Optional with EPI_ADD_F32 (trans = 0): the updated value is also stored as bf16 into cpy
+  // ([M][ldc]) and each row's sum of squares over every 32-column chunk into ssq[m * ceil(N/32) + n/32]
+  // (the next layer's pre-norm statistic without a separate pass; reading Q22).
+  void* cpy;
+  float* ssq;
   // EPI_DECODE_INPROJ (SURVEY.md §8 rows a1-a3 fused for one decode token).
   // Output rows m are in_proj features: m < Ek are x channels -> causal conv step over the cached
   // window cst + SiLU -> u (bf16 [N][Ek]) and the window shifted in place; Ek <= m < 2Ek are z
@@ -105,6 +110,8 @@ cudaError_t launch_decode_step(int bf16, Peers src, int nsrc, int64_t src_off, i
                                const void* u, const void* z, int64_t ldz, const void* w_dt, const float* b_dt,
                                const float* a_log, const float* d_skip, float* h, void* g, int batch, int Ek, int R,
                                int N, int ch_per_head, float* zacc, cudaStream_t s);
+cudaError_t launch_rowstats(const float* x, void* y, float* ss, int64_t M, int D, cudaStream_t s);
+cudaError_t launch_ssq_finalize(const float* part, int nchunk, float* ss, int64_t M, cudaStream_t s);
 cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, void* y, int64_t M, int D,
                            cudaStream_t s);
 // int8 quantisation of n fp32 values in blocks of blk: q [n] int8, scale [n/blk] f32.

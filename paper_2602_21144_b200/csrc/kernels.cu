@@ -910,6 +910,57 @@ cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const fl
   return cudaGetLastError();
 }
 
+// Pre-norm statistic without the normalisation (prefill with the norm folded into the in_proj, reading
+// Q22): y = bf16(x) and ss[row] = sum_d x[row][d]^2, one block per row, the same fixed reduction
+// order as rmsnorm_kernel.
+__global__ void __launch_bounds__(128) rowstats_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                                       float* __restrict__ ss, int64_t M, int D) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int MAXV = 16;
+  __shared__ float red[4];
+  const int64_t row = blockIdx.x;
+  const int tid = threadIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * D);
+  const int nv = D / 4;
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int k = tid + i * 128;
+    if (k < nv) {
+      const float4 v = xr[k];
+      acc = fmaf(v.x, v.x, acc); acc = fmaf(v.y, v.y, acc);
+      acc = fmaf(v.z, v.z, acc); acc = fmaf(v.w, v.w, acc);
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(y + row * D)[k] = pk;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((tid & 31) == 0) red[tid >> 5] = acc;
+  __syncthreads();
+  if (tid == 0) ss[row] = (red[0] + red[1]) + (red[2] + red[3]);
+}
+
+// ss[m] = the row's per-32-column partial sums of squares (written by the out_proj epilogue, Epilogue::ssq)
+// summed in a fixed order: one warp per row, lanes stride the partials, then a shuffle tree.
+__global__ void __launch_bounds__(256) ssq_finalize_kernel(const float* __restrict__ part, int nchunk,
+                                                           float* __restrict__ ss, int64_t M) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  float acc = 0.f;
+  for (int c = lane; c < nchunk; c += 32) acc += part[row * nchunk + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) ss[row] = acc;
+}
+
 }  // namespace
 
 // ==================================================================== launchers
@@ -1026,6 +1077,19 @@ cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, 
   else
     { cudaError_t e_ = launch(rmsnorm_kernel<float>, (unsigned)M, 128, 0, s, x, w, eps, reinterpret_cast<float*>(y), M, D); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
+}
+
+cudaError_t launch_rowstats(const float* x, void* y, float* ss, int64_t M, int D, cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  if (D % 4 || D > 16 * 128 * 4) return cudaErrorInvalidValue;
+  cudaError_t e = launch(rowstats_kernel, (unsigned)M, 128, 0, s, x, reinterpret_cast<__nv_bfloat16*>(y), ss, M, D);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_ssq_finalize(const float* part, int nchunk, float* ss, int64_t M, cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  cudaError_t e = launch(ssq_finalize_kernel, (unsigned)((M * 32 + 255) / 256), 256, 0, s, part, nchunk, ss, M);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float* scale, cudaStream_t s) {

@@ -164,6 +164,22 @@ class TPMixer:
         L.call("ssm_mixer_prefill", self.handle, C.byref(w.struct), state.handle, _ptr(x_in), _ptr(residual), B, Lq,
                flags, _ptr(ws), ws.numel(), _stream(stream))
 
+    def prefill_normed(self, w, state, x_in, ss_in, residual, x_next=None, ss_next=None, norm_eps=1e-5,
+                       flags=L.SSM_AR2_INT8, workspace=None, stream=None):
+        """One pre-norm prefill block with the norm folded around the projections
+        (ssm_mixer_prefill_normed): x_in = bf16(residual), ss_in its row sums of squares; the out_proj
+        epilogue writes x_next / ss_next for the next layer."""
+        B, Lq = state.batch, x_in.numel() // (state.batch * self.dims.d_model)
+        ws = workspace if workspace is not None else self.workspace(B, Lq)
+        L.call("ssm_mixer_prefill_normed", self.handle, C.byref(w.struct), state.handle, _ptr(x_in), _ptr(ss_in),
+               C.c_float(norm_eps), _ptr(residual), _ptr(x_next), _ptr(ss_next), B, Lq, flags, _ptr(ws), ws.numel(),
+               _stream(stream))
+
+    def rowstats(self, residual, x_out, ss_out, stream=None):
+        """x_out = bf16(residual), ss_out = row sums of squares (ssm_rowstats)."""
+        L.call("ssm_rowstats", self.handle, _ptr(residual), _ptr(x_out), _ptr(ss_out),
+               residual.numel() // self.dims.d_model, _stream(stream))
+
     def decode(self, w, state, x_in, residual, flags=L.SSM_AR2_INT8, workspace=None, stream=None):
         B = state.batch
         ws = workspace if workspace is not None else self.workspace(B, 1)

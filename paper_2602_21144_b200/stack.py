@@ -106,6 +106,12 @@ class MixerStack:
                 self.hybrid[li] = (w, blk)
             self.t_buf = torch.empty((batch * max_chunk, d.d_model), device=mixer.device)
             self.h0_dec = torch.zeros((batch, d.d_model), device=mixer.device)
+        # prefill with the pre-norm folded around the projections (ssm_mixer_prefill_normed, TP = 1):
+        # x = bf16(residual) and its row statistic come from the previous layer's out_proj epilogue
+        self.prefill_normed = (mixer.tp_size == 1 and mixer.dtype == "bf16" and not self.hybrid
+                               and self.nccl is None and not (flags & L.SSM_TP_NAIVE))
+        if self.prefill_normed:
+            self.ssbuf = torch.empty((2, (batch * max_chunk + 3) // 4 * 4), dtype=torch.float32, device=mixer.device)
         self.graph = None
         self.graph_launches = 0
         self._graph_parity = 0
@@ -131,6 +137,15 @@ class MixerStack:
         h0: the chunk's token embeddings (Zamba hybrid layers)."""
         n = res.shape[0]
         x = self.xbuf[:n]
+        if self.prefill_normed:
+            ss = self.ssbuf[:, :n]
+            self.mx.rowstats(res, x, ss[0], stream)
+            last = len(self.layers) - 1
+            for li, (lw, st) in enumerate(zip(self.layers, self.states)):
+                nxt = li < last
+                self.mx.prefill_normed(lw, st, x, ss[li & 1], res, x if nxt else None, ss[(li + 1) & 1] if nxt else None,
+                                       self.eps, self.flags, self.ws, stream)
+            return
         for li, (lw, st) in enumerate(zip(self.layers, self.states)):
             if li in self.hybrid:
                 w, blk = self.hybrid[li]

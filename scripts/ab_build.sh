@@ -10,10 +10,13 @@ OUT=$ROOT/build/ab/$NAME
 rm -rf "$OUT"; mkdir -p "$OUT"
 cp -r "$ROOT/paper_2602_21144_b200" "$OUT/"
 rm -f "$OUT/paper_2602_21144_b200/libssmtp.so"
-cp "$SRC" "$OUT/$BASE"
-cp "$ROOT"/paper_2602_21144_b200/csrc/*.cuh "$ROOT"/paper_2602_21144_b200/csrc/*.h "$OUT/"
+# the variant sits two levels below a copy of include/ (sources include "../../include/ssm_tp.h")
+mkdir -p "$OUT/src/csrc"
+cp -r "$ROOT/include" "$OUT/include"
+cp "$SRC" "$OUT/src/csrc/$BASE"
+cp "$ROOT"/paper_2602_21144_b200/csrc/*.cuh "$ROOT"/paper_2602_21144_b200/csrc/*.h "$OUT/src/csrc/"
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-  -I"$ROOT/include" --expt-relaxed-constexpr -c "$OUT/$BASE" -o "$OUT/$STEM.o"
+  -I"$ROOT/include" --expt-relaxed-constexpr -c "$OUT/src/csrc/$BASE" -o "$OUT/$STEM.o"
 OBJS=$(ls "$ROOT"/build/libssmtp/*.o | grep -v "/$STEM.o")
 /usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC $OBJS "$OUT/$STEM.o" \
   -o "$OUT/paper_2602_21144_b200/libssmtp.so"
