@@ -19,7 +19,7 @@
 namespace ssm {
 namespace {
 
-constexpr int M2_P = 64, M2_Q = 4, M2_THREADS = M2_P * M2_Q, M2_TT = 16, M2_NMAX = 128;
+constexpr int M2_P = 64, M2_Q = 4, M2_THREADS = M2_P * M2_Q, M2_TT = 16;
 // multi-token calls at least this long take the chunked SSD form (m2_ssd_chunk); shorter ones (and
 // d_state 16) the per-token recurrence (m2_scan)
 constexpr int kSsdChunkMinL = 16;
