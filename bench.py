@@ -345,7 +345,7 @@ def main():
         probe_graph = stack.capture_decode(res_t, probes=[] if (mamba2 or persistent) else [("in_proj_decode", n_layers)])
         graph = stack.capture_decode(res_t, warmup=False)
 
-    def step(timers=None):
+    def prefill_part(timers=None):
         stack.reset()
         for c in range(n_chunks):
             work[c].copy_(prompt_in[c])
@@ -355,6 +355,8 @@ def main():
             stack.prefill_chunk(work[c], h0=prompt_in[c])
         if timers is not None:
             timers[1].record()
+
+    def decode_part(timers=None):
         for j in range(Ld):
             res_t.copy_(dec_in[j])
             if getattr(stack, "hybrid", None):
@@ -363,6 +365,10 @@ def main():
             dec_out[j].copy_(res_t)
         if timers is not None:
             timers[2].record()
+
+    def step(timers=None):
+        prefill_part(timers)
+        decode_part(timers)
 
     def barrier():
         if k > 1:
@@ -430,13 +436,37 @@ def main():
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        # every step's copies are inside the timed region, pipelined on a copy stream: step i + 1's
+        # prompt lands while step i decodes (after its prefill has consumed the prompt buffers), step
+        # i's outputs leave and step i + 1's decode inputs land while step i + 1 prefills
+        cur = torch.cuda.current_stream()
+        cs = torch.cuda.Stream()
         e0.record()
-        for _ in range(args.steps):
+        cs.wait_stream(cur)
+        with torch.cuda.stream(cs):
             for c in range(n_chunks):
                 prompt_in[c].copy_(h_prompt[c], non_blocking=True)
             dec_in.copy_(h_dec, non_blocking=True)
-            step()
-            h_out.copy_(dec_out, non_blocking=True)
+        in_ready = cs.record_event()
+        dec_ready = in_ready
+        for i in range(args.steps):
+            cur.wait_event(in_ready)
+            prefill_part()
+            if i + 1 < args.steps:
+                cs.wait_event(cur.record_event())
+                with torch.cuda.stream(cs):
+                    for c in range(n_chunks):
+                        prompt_in[c].copy_(h_prompt[c], non_blocking=True)
+                in_ready = cs.record_event()
+            cur.wait_event(dec_ready)
+            decode_part()
+            cs.wait_event(cur.record_event())
+            with torch.cuda.stream(cs):
+                h_out.copy_(dec_out, non_blocking=True)
+                if i + 1 < args.steps:
+                    dec_in.copy_(h_dec, non_blocking=True)
+            dec_ready = cs.record_event()
+        cur.wait_event(dec_ready)
         e1.record()
         torch.cuda.synchronize()
         barrier()
