@@ -66,6 +66,21 @@ SSM_DEV float silu(float v) {
   if (kFast) return v * rcp_approx(1.0f + ex2_approx(-v * 1.4426950408889634f));
   return v / (1.0f + expf(-v));
 }
+// softplus for bf16 outputs with ONE MUFU op: max(x, 0) + log1p(exp(-|x|)), log1p(t) = t q(t) with q a
+// degree-5 polynomial fitted on t in [0, 1] (max relative error 1.0e-5 evaluated in fp32, far below the
+// bf16 rounding of the result).  Above 20 the t q term is below half an ulp of x, so the result is x:
+// the linear branch of SPEC.md:48, 63.  (The ex2 + lg2 form spent two MUFU ops per element and made
+// the prefill dt_proj epilogue MUFU-bound.)
+SSM_DEV float softplus_1mufu(float x) {
+  const float t = ex2_approx(-fabsf(x) * 1.4426950408889634f);
+  float q = -0.024527326f;
+  q = fmaf(q, t, 0.10286978f);
+  q = fmaf(q, t, -0.21149261f);
+  q = fmaf(q, t, 0.32572353f);
+  q = fmaf(q, t, -0.49942619f);
+  q = fmaf(q, t, 0.99999291f);
+  return fmaf(t, q, fmaxf(x, 0.f));
+}
 // softplus with the linear branch above 20
 SSM_DEV float softplus(float v) { return v > 20.0f ? v : log1pf(expf(v)); }
 

@@ -132,13 +132,9 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
 #pragma unroll
       for (int j = 0; j < 32; ++j) bb[j] = (n0 + j < N) ? e.bias[n0 + j] : 0.f;
     }
-    if (kind == EPI_SOFTPLUS_BF16) {  // bf16 output: 2-MUFU softplus (error far below bf16 rounding)
+    if (kind == EPI_SOFTPLUS_BF16) {  // bf16 output: one-MUFU softplus (error far below bf16 rounding)
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float x = v[j] + bb[j];
-        const float sp = 0.6931471805599453f * __log2f(1.f + ex2_approx(x * 1.4426950408889634f));
-        v[j] = x > 20.f ? x : sp;
-      }
+      for (int j = 0; j < 32; ++j) v[j] = softplus_1mufu(v[j] + bb[j]);
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = softplus(v[j] + bb[j]);
@@ -687,9 +683,7 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
                 float y[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                  const float x = __uint_as_float(r[2 * j + h]) + bb[2 * j + h];
-                  const float sp = 0.6931471805599453f * __log2f(1.f + ex2_approx(x * 1.4426950408889634f));
-                  y[h] = x > 20.f ? x : sp;
+                  y[h] = softplus_1mufu(__uint_as_float(r[2 * j + h]) + bb[2 * j + h]);
                 }
                 __nv_bfloat162 t2 = __floats2bfloat162_rn(y[0], y[1]);
                 pk[j] = *reinterpret_cast<uint32_t*>(&t2);
