@@ -457,6 +457,12 @@ ssm_status_t ssm_tp_probe_read(ssm_tp_t tp, int32_t kernel, float* ms, int32_t c
  * by the projections (tcgen05 for bf16 when K*2 % 16 == 0, SIMT otherwise). */
 ssm_status_t ssm_dbg_gemm(ssm_tp_t tp, const void* A, const void* B, float* C,
                           int32_t M, int32_t N, int32_t K, int32_t swap_ab, int32_t ksplit, void* stream);
+/* Selects the tcgen05 GEMM's CTA-pair variant (cta_group::2, M = 256 tiles over a 2-CTA cluster)
+ * for every later call in the process: -1 = by shape (default: prefill GEMMs with M >= 4096,
+ * N >= 128, K >= 1024, except the softplus dt_proj), 0 = never, 1 = whenever the call is eligible (non-transposed, no split-K,
+ * M > 128).  Results are identical up to fp32 summation order inside the tensor core.  Returns
+ * SSM_ERR_ARG for any other mode. */
+ssm_status_t ssm_dbg_set_gemm_pair(int32_t mode);
 /* Swap-AB decode GEMM C[M,N] = X[M,K] W[N,K]^T reading W through its packed copy Wpk. */
 ssm_status_t ssm_dbg_gemm_packed(ssm_tp_t tp, const void* X, const void* W, const void* Wpk, float* C, int32_t M,
                                  int32_t N, int32_t K, int32_t ksplit, void* stream);

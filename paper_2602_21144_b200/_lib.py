@@ -113,6 +113,7 @@ def _load():
         "ssm_tp_probe": (st, [vp, i32, i32]),
         "ssm_tp_probe_read": (st, [vp, i32, P(C.c_float), i32, P(i32)]),
         "ssm_dbg_gemm": (st, [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]),
+        "ssm_dbg_set_gemm_pair": (st, [i32]),
         "ssm_packed_weight_bytes": (st, [i32, i32, P(sz)]),
         "ssm_pack_weight": (st, [vp, vp, i32, i32, vp, sz, vp]),
         "ssm_dbg_gemm_packed": (st, [vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]),
@@ -138,7 +139,7 @@ EXPORTED = ["ssm_last_error", "ssm_version", "ssm_tp_init", "ssm_tp_destroy", "s
             "ssm_mixer_prefill_normed", "ssm_rowstats",
             "ssm_mixer_decode", "ssm_mixer_decode_block", "ssm_qallreduce", "ssm_rmsnorm", "ssm_tp_check", "ssm_tp_stats", "ssm_tp_epoch",
             "ssm_tp_barrier", "ssm_tp_launch_count", "ssm_tp_fused_calls", "ssm_tp_probe", "ssm_tp_probe_read",
-            "ssm_packed_weight_bytes", "ssm_pack_weight", "ssm_dbg_gemm", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld",
+            "ssm_packed_weight_bytes", "ssm_pack_weight", "ssm_dbg_gemm", "ssm_dbg_set_gemm_pair", "ssm_dbg_gemm_packed", "ssm_dbg_gemm_ld",
             "ssm_dbg_scan", "ssm_rmsnorm_add", "ssm_kv_bytes", "ssm_kv_alloc", "ssm_kv_reset", "ssm_kv_free",
             "ssm_attn_workspace_bytes", "ssm_attn_block", "ssm_m2_state_bytes", "ssm_m2_workspace_bytes",
             "ssm_m2_mixer", "ssm_dstack_bytes", "ssm_dstack_create", "ssm_dstack_decode", "ssm_dstack_destroy",

@@ -20,6 +20,7 @@ using namespace ssm;
 
 namespace ssm {
 thread_local bool t_launch_pdl = false;
+int t_gemm_pair = -1;
 }
 
 namespace {
@@ -990,6 +991,12 @@ ssm_status_t ssm_tp_barrier(ssm_tp_t tp, void* stream) {
 ssm_status_t ssm_tp_launch_count(ssm_tp_t tp, int64_t* launches) {
   if (!tp || !launches) return fail(SSM_ERR_ARG, "NULL argument");
   *launches = tp->launches;
+  return SSM_OK;
+}
+
+ssm_status_t ssm_dbg_set_gemm_pair(int32_t mode) {
+  if (mode < -1 || mode > 1) return fail(SSM_ERR_ARG, "mode=%d (expected -1, 0 or 1)", mode);
+  ssm::t_gemm_pair = mode;
   return SSM_OK;
 }
 

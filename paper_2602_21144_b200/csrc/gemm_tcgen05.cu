@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 
+#include <algorithm>
 #include <mutex>
 
 #include "common.cuh"
@@ -60,11 +61,12 @@ constexpr int var_kind(int var) { return var == 6 ? EPI_SOFTPLUS_BF16 : var == 7
 // Work decomposition: unit u = (k-split, m-tile, n-tile), CTAs stride over units.
 struct TileSched {
   int m_tiles, n_tiles, kb_total, kbs, ksplit, units;
+  int grp;  // CTAs per unit: 1, or 2 for a CTA pair (cta_group::2) sharing one M = 256 tile
   // iterate units (mt, nt, kb0, kb1) of this CTA; returns false when done
   __device__ bool next(int& cursor, int& mt, int& nt, int& kb0, int& kb1) const {
     const int u = cursor;
     if (u >= units) return false;
-    cursor += gridDim.x;
+    cursor += gridDim.x / grp;
     nt = u % n_tiles;
     const int rest = u / n_tiles;
     mt = rest % m_tiles;
@@ -73,7 +75,7 @@ struct TileSched {
     kb1 = min(kb_total, kb0 + kbs);
     return true;
   }
-  __device__ int first() const { return (int)blockIdx.x; }
+  __device__ int first() const { return (int)blockIdx.x / grp; }
 };
 
 // Optional row scale 1 / sqrt(rss[r] * rss_inv + rss_eps) of logical row r (Epilogue::rss).
@@ -466,21 +468,38 @@ __device__ __forceinline__ void decode_inproj_epilogue(const Epilogue& e, const 
   }
 }
 
+// Epilogue warp done with an accumulator: a pair's MMA issuer (the leader) waits for both CTAs.
+template <int CG>
+__device__ __forceinline__ void tempty_arrive(uint64_t* bar) {
+  if constexpr (CG == 2) mbar_arrive_remote(mapa_shared(bar, 0));
+  else mbar_arrive(bar);
+}
+
 // VAR: 0 = every path (prefill GEMMs); 1 = the fused decode in_proj only; 2 = skinny swap-AB
 // split-K GEMMs with the atomic epilogue only (decode out_proj / x_proj); 6 = prefill dt_proj
 // (softplus epilogue).  The decode variants are separate kernels so their register allocation is
 // not set by paths they never run.
-template <int VAR, int XPN = XP_NT>
+// CG = 2: CTA pair (2-CTA cluster).  The pair computes a 256 x BN tile with cta_group::2 UMMAs
+// issued by the leader (rank 0): each CTA TMA-loads its 128 rows of A and BN / 2 rows of B, both
+// halves' transaction bytes complete on the leader's full barrier, the leader's commits arrive on
+// both CTAs' empty / TMEM-full barriers (multicast), and each CTA's epilogue drains its own 128
+// accumulator lanes, then arrives on the leader's TMEM-empty barrier.  Per CTA and k-block the ring
+// takes 32 KB instead of 48 KB for the same MMA work (the B tile is shared): a third less L2 -> SM
+// operand traffic, the limit of the 1-CTA kernel on the prefill projections.
+template <int VAR, int XPN = XP_NT, int CG = 1>
 __global__ void __launch_bounds__(var_threads(VAR), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int BN, int KBS, TileSched ts, Epilogue epi, const __nv_bfloat16* a_blk, int64_t lda, int K,
                    CtaRes cr, int a_blocked) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int STAGES = num_stages(BN, KBS, cr.ring);
-  const int SB = stage_bytes(BN, KBS);
+  const int BNL = BN / CG;  // B rows this CTA loads
+  const int STAGES = num_stages(BNL, KBS, cr.ring);
+  const int SB = stage_bytes(BNL, KBS);
   const int BOFF = KBS * A_STAGE;  // B tiles follow the KBS A tiles (1024-B aligned)
-  const int BSUB = BN * BK * 2;
+  const int BSUB = BNL * BK * 2;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const int row_off = (int)rank * BM;  // this CTA's rows inside the pair's 256-row tile
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + cr.ring);
   uint64_t* empty = full + MAX_STAGES;
@@ -501,13 +520,17 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], (var_threads(VAR) - 64) / 32);
+      mbar_init(&tempty[i], CG * (var_threads(VAR) - 64) / 32);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, cr.tmem_cols);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_pair(tmem_slot, cr.tmem_cols);
+    else tmem_alloc(tmem_slot, cr.tmem_cols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -516,21 +539,31 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
     // lane 0 alone issues the copies.  (With lane 0 looping alone while lanes 1-31 sat at the
     // teardown barrier, every iteration of the producer loop measured ~0.2-0.45 us.)
     const bool leader = lane == 0;
-    const uint32_t stage_tx = (uint32_t)(BM + BN) * BK * 2;  // per k-block
+    const uint32_t stage_tx = (uint32_t)CG * (BM + BNL) * BK * 2;  // per k-block (both CTAs of a pair)
+    const uint32_t full_remote = CG == 2 ? mapa_shared(full, 0) : 0u;  // leader's full[0]
     auto issue_a = [&](uint8_t* st, uint64_t* bar, int mt, int kb, int nk) {
       if (a_blocked)  // A pre-tiled AND pre-swizzled: the nk blocks (mt, kb..kb+nk) are one
         // contiguous run of nk x 16 KB whose bytes are already the SW128 smem image -> 1D bulk copy
         bulk_load_evict_first(st, a_blk + ((int64_t)mt * ts.kb_total + kb) * (BM * BK), (uint32_t)nk * A_STAGE, bar);
+      else if constexpr (CG == 2)
+        for (int j = 0; j < nk; ++j)
+          tma_load_2d_pair(st + j * A_STAGE, &tmA, full_remote + (uint32_t)((bar - full) * 8), (kb + j) * BK,
+                           mt * BM * CG + row_off);
       else
         for (int j = 0; j < nk; ++j) tma_load_2d(st + j * A_STAGE, &tmA, bar, (kb + j) * BK, mt * BM);
     };
     auto issue_b = [&](uint8_t* st, uint64_t* bar, int nt, int kb, int nk) {
-      for (int j = 0; j < nk; ++j) tma_load_2d(st + BOFF + j * BSUB, &tmB, bar, (kb + j) * BK, nt * BN);
+      if constexpr (CG == 2)
+        for (int j = 0; j < nk; ++j)
+          tma_load_2d_pair(st + BOFF + j * BSUB, &tmB, full_remote + (uint32_t)((bar - full) * 8), (kb + j) * BK,
+                           nt * BN + (int)rank * BNL);
+      else
+        for (int j = 0; j < nk; ++j) tma_load_2d(st + BOFF + j * BSUB, &tmB, bar, (kb + j) * BK, nt * BN);
     };
     // A independent of the predecessor grid (weights): arm the first ring fill and issue its A
     // loads BEFORE griddepcontrol.wait, so the weight stream starts while the predecessor drains.
     int n_pre = 0;
-    if (cr.a_indep) {
+    if (CG == 1 && cr.a_indep) {
       int cur = ts.first(), mt, nt, kb0, kb1;
       while (n_pre < STAGES && ts.next(cur, mt, nt, kb0, kb1))
         for (int kb = kb0; kb < kb1 && n_pre < STAGES; kb += KBS, ++n_pre) {
@@ -553,7 +586,7 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         if (g >= n_pre) {
           mbar_wait(&empty[stage], ph ^ 1);
           if (leader) {
-            mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * stage_tx);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * stage_tx);
             issue_a(st, &full[stage], mt, kb, nk);
           }
         }
@@ -564,11 +597,12 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
     }
   } else if (warp == 1) {
     pdl_wait();
+    if (CG == 2 && rank != 0) goto teardown;  // the leader issues the pair's MMAs
     // ---------------- MMA issuer: the whole warp runs the (warp-uniform) schedule so the UMMA
     // descriptors live in uniform registers; one elected lane issues the tcgen05.mma / commits.
     // (A single-lane loop makes ptxas wrap every UMMA in a uniform-broadcast waterfall loop,
     // ~100 cycles per instruction: that, not the tensor pipe, bounded skinny weight streams.)
-    const uint32_t idesc = umma_idesc_bf16(BM, BN);
+    const uint32_t idesc = umma_idesc_bf16(BM * CG, BN);
     const uint64_t ring_desc = umma_desc_sw128(smem_u32(ring));  // + (byte offset >> 4) addresses inside the ring
     int stage = 0;
     uint32_t ph = 0;
@@ -589,16 +623,24 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         if (elect_one()) {
           for (int j = 0; j < nk; ++j) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              umma_bf16(d, a_desc + (uint64_t)((j * A_STAGE + k * 32) >> 4), b_desc + (uint64_t)((j * BSUB + k * 32) >> 4),
-                        idesc, (kb > kb0 || j > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = a_desc + (uint64_t)((j * A_STAGE + k * 32) >> 4);
+              const uint64_t bd = b_desc + (uint64_t)((j * BSUB + k * 32) >> 4);
+              const uint32_t accum = (kb > kb0 || j > 0 || k > 0) ? 1u : 0u;
+              if constexpr (CG == 2) umma_bf16_pair(d, ad, bd, idesc, accum);
+              else umma_bf16(d, ad, bd, idesc, accum);
+            }
           }
-          umma_commit(&empty[stage]);
+          if constexpr (CG == 2) umma_commit_pair(&empty[stage], 3);
+          else umma_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; ph ^= 1; }
       }
-      if (elect_one()) umma_commit(&tfull[acc]);
+      if (elect_one()) {
+        if constexpr (CG == 2) umma_commit_pair(&tfull[acc], 3);
+        else umma_commit(&tfull[acc]);
+      }
       __syncwarp();
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
@@ -634,7 +676,7 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         // epilogue for microseconds after the weight stream (page walks queue behind it).
         int c2 = cur, mt2, nt2, k0, k1;
         if (ts.next(c2, mt2, nt2, k0, k1)) {
-          const int m = min(M - 1, mt2 * BM + eg * 32), n = min(N - 1, nt2 * BN);
+          const int m = min(M - 1, mt2 * BM * CG + row_off + eg * 32), n = min(N - 1, nt2 * BN);
           const int64_t idx = epi.trans ? (int64_t)n * epi.ldc + m : (int64_t)m * epi.ldc + n;
           const int esz = (epi.kind == EPI_STORE_BF16 || epi.kind == EPI_SOFTPLUS_BF16) ? 2 : 4;
           touch_global(reinterpret_cast<const uint8_t*>(epi.C) + idx * esz);
@@ -645,13 +687,13 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         if (kb0 >= kb1) continue;
         mbar_wait(&tfull[acc], acc_ph);
         tc_fence_after();
-        const int m0 = mt * BM + eg * 32;
+        const int m0 = mt * BM * CG + row_off + eg * 32;
         const uint32_t tbase = tmem_base + ((uint32_t)(eg * 32) << 16) + (uint32_t)(acc * cr.acc_stride);
         if constexpr (VAR == 7) {
           quant_epilogue(epi, m0, nt * BN, BN, M, N, tbase, reinterpret_cast<float*>(smem + cr.ring + 512));
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) tempty_arrive<CG>(&tempty[acc]);
           if (++acc == 2) { acc = 0; acc_ph ^= 1; }
           continue;
         }
@@ -709,7 +751,7 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) tempty_arrive<CG>(&tempty[acc]);
           if (++acc == 2) { acc = 0; acc_ph ^= 1; }
           continue;
         }
@@ -734,16 +776,19 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) tempty_arrive<CG>(&tempty[acc]);
         if (++acc == 2) { acc = 0; acc_ph ^= 1; }
       }
     }
   }
+teardown:
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // the leader's MMAs write the peer's TMEM: free it after both drained
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, cr.tmem_cols);
+    if constexpr (CG == 2) tmem_dealloc_pair(tmem_base, cr.tmem_cols);
+    else tmem_dealloc(tmem_base, cr.tmem_cols);
   }
 }
 
@@ -820,7 +865,37 @@ cudaError_t pack_blocked(const __nv_bfloat16* w, int rows, int cols, int64_t ld,
 
 #define SSM_GEMM_KERNELS (const void*)gemm_tc_kernel<0>, (const void*)gemm_tc_kernel<1>, (const void*)gemm_tc_kernel<1, 3>, \
     (const void*)gemm_tc_kernel<1, 4>, (const void*)gemm_tc_kernel<2>, (const void*)gemm_tc_kernel<6>, \
-    (const void*)gemm_tc_kernel<7>
+    (const void*)gemm_tc_kernel<7>, (const void*)gemm_tc_kernel<0, XP_NT, 2>, (const void*)gemm_tc_kernel<6, XP_NT, 2>, \
+    (const void*)gemm_tc_kernel<7, XP_NT, 2>
+
+// CTA pairs that can be co-resident (one 227 KB CTA per SM): 2-CTA clusters are placed inside a GPC,
+// so this can be below num_sms / 2.  Queried once.
+int max_pairs() {
+  static int pairs = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaFuncSetAttribute((const void*)gemm_tc_kernel<0, XP_NT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_BYTES) == cudaSuccess &&
+        cudaOccupancyMaxActiveClusters(&n, (const void*)gemm_tc_kernel<0, XP_NT, 2>, &cfg) == cudaSuccess)
+      pairs = n;
+    else
+      pairs = 0;
+    cudaGetLastError();
+  });
+  return pairs;
+}
 
 cudaError_t preload_gemm_tc() {
   cudaError_t e = cudaSuccess;
@@ -841,6 +916,16 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
                          int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool a_indep,
                          const __nv_bfloat16* A_blocked) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  // CTA pair (cta_group::2, M = 256 tiles) for the large non-transposed prefill GEMMs: in_proj,
+  // out_proj (fp32 residual add or int8 quantisation) and the generic stores; t_gemm_pair forces
+  // it on (1) or off (0) for tests and A/B runs
+  const bool pair_ok = !epi.trans && ksplit <= 1 && !A_blocked && !a_indep && M > BM && N > 32 &&
+                       (epi.kind == EPI_STORE_BF16 || epi.kind == EPI_STORE_F32 || epi.kind == EPI_ADD_F32 ||
+                        epi.kind == EPI_QUANT_I8 || epi.kind == EPI_SOFTPLUS_BF16);
+  // (measured, Mamba-2.8B prefill chunk of 32768 tokens: in_proj 1356 -> 1209 us, out_proj 690 -> 643 us,
+  // x_proj 86 -> 82 us; the K = 160 dt_proj 139 -> 164 us stays on single CTAs)
+  const bool pair_default = M >= 4096 && K >= 1024 && N >= 128 && epi.kind != EPI_SOFTPLUS_BF16;
+  const int CG = (pair_ok && (t_gemm_pair > 0 || (t_gemm_pair < 0 && pair_default)) && max_pairs() > 0) ? 2 : 1;
   // BN: multiple of 32 in [32, 256] (UMMA needs N % 16 == 0; the epilogue drains TMEM in
   // 32-column chunks) covering N in as few tiles as possible; N <= 16: one 16-column UMMA tile
   // (decode batches) halves the B operand and its smem
@@ -850,7 +935,8 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   if (epi.kind == EPI_QUANT_I8 && epi.qblk > 0) BN = (BN + epi.qblk - 1) / epi.qblk * epi.qblk;  // whole blocks
   n_tiles = (N + BN - 1) / BN;
   TileSched ts;
-  ts.m_tiles = (M + BM - 1) / BM;
+  ts.grp = CG;
+  ts.m_tiles = (M + BM * CG - 1) / (BM * CG);
   ts.n_tiles = n_tiles;
   ts.kb_total = (K + BK - 1) / BK;
   if (ksplit < 1) ksplit = 1;
@@ -861,7 +947,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   if (ts.ksplit > 1 && epi.kind != EPI_ATOMIC_F32) return cudaErrorInvalidValue;
 
   CUtensorMap ma, mb;
-  if (!make_map(&mb, B, N, K, ldb, BN)) return cudaErrorInvalidValue;
+  if (!make_map(&mb, B, N, K, ldb, BN / CG)) return cudaErrorInvalidValue;
   if (A_blocked) {
     if ((reinterpret_cast<uintptr_t>(A_blocked) & 127) != 0) return cudaErrorInvalidValue;
     ma = mb;  // unused: A is fetched by 1D bulk copies
@@ -922,9 +1008,13 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     cr.ring -= extra;
   }
   if (epi.zero && (reinterpret_cast<uintptr_t>(epi.zero) & 15)) return cudaErrorInvalidValue;
-  while (kbs > 1 && num_stages(BN, kbs, cr.ring) < 2) --kbs;
+  while (kbs > 1 && num_stages(BN / CG, kbs, cr.ring) < 2) --kbs;
   const int smem_bytes = 1024 + cr.ring + 512 + extra;
-  const int grid = ts.units < num_sms ? ts.units : num_sms;
+  int grid = ts.units < num_sms ? ts.units : num_sms;
+  if (CG == 2) {
+    const int mp = std::min(num_sms / 2, max_pairs());
+    grid = 2 * (ts.units < mp ? ts.units : mp);
+  }
   // kernel variant (see gemm_tc_kernel): the decode GEMMs and the prefill dt_proj on their own
   // instantiations (fixed-kind in_proj / out_proj variants measured 2-3% slower than the all-paths
   // kernel, x_proj equal; the dt_proj one 249 -> 230 us)
@@ -937,8 +1027,15 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   if (epi.cpy && (epi.kind != EPI_ADD_F32 || epi.trans || !epi.ssq || ts.ksplit > 1)) return cudaErrorInvalidValue;
   auto kfn = var == 2 ? gemm_tc_kernel<2> : var == 6 ? gemm_tc_kernel<6> : var == 7 ? gemm_tc_kernel<7> : gemm_tc_kernel<0>;
   if (var == 1) kfn = epi.P <= 64 * 3 ? gemm_tc_kernel<1, 3> : epi.P <= 64 * 4 ? gemm_tc_kernel<1, 4> : gemm_tc_kernel<1>;
-  cudaError_t e_ = launch(kfn, grid, var_threads(var), smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi, A_blocked, lda, K,
-                          cr, A_blocked ? 1 : 0);
+  cudaError_t e_;
+  if (CG == 2) {
+    kfn = var == 6 ? gemm_tc_kernel<6, XP_NT, 2> : var == 7 ? gemm_tc_kernel<7, XP_NT, 2> : gemm_tc_kernel<0, XP_NT, 2>;
+    e_ = launch_cluster(kfn, grid, var_threads(var), smem_bytes, s, 2, ma, mb, M, N, BN, kbs, ts, epi, A_blocked, lda, K,
+                        cr, 0);
+  } else {
+    e_ = launch(kfn, grid, var_threads(var), smem_bytes, s, ma, mb, M, N, BN, kbs, ts, epi, A_blocked, lda, K, cr,
+                A_blocked ? 1 : 0);
+  }
   if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
 }

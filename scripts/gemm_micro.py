@@ -16,7 +16,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
-from paper_2602_21144_b200 import TPMixer  # noqa: E402
+from paper_2602_21144_b200 import TPMixer, _lib as L  # noqa: E402
 
 SHAPES = {
     # name: (tokens M, out features N, K, swap_ab, ksplit)
@@ -38,7 +38,16 @@ SHAPES = {
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--only", default="")
+    p.add_argument("--pair", default="-1", help="CTA-pair GEMM modes to time (ssm_dbg_set_gemm_pair), e.g. 0,1")
     a = p.parse_args()
+    for mode in [int(v) for v in a.pair.split(",")]:
+        L.call("ssm_dbg_set_gemm_pair", mode)
+        print(f"-- gemm pair mode {mode}", flush=True)
+        run(a)
+    L.call("ssm_dbg_set_gemm_pair", -1)
+
+
+def run(a):
     mx = TPMixer(synth.CONFIGS["tiny"], "bf16")
     for name, (M, N, K, swap, ks) in SHAPES.items():
         if a.only and a.only not in name:

@@ -21,7 +21,9 @@ from paper_2602_21144_b200.stack import synthetic_layer  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--config", default="mamba2.8b")
+ap.add_argument("--pair", type=int, default=-1, help="CTA-pair GEMM mode (ssm_dbg_set_gemm_pair)")
 args = ap.parse_args()
+L.call("ssm_dbg_set_gemm_pair", args.pair)
 dims = synth.CONFIGS[args.config]
 wl = synth.WORKLOADS[args.config]
 B, Lp = wl["batch"], wl["prompt"]
@@ -40,7 +42,8 @@ for _ in range(args.reps + 2):
     st.reset()
     mx.prefill(lw, st, x, r, L.SSM_AR2_INT8, ws)
 torch.cuda.synchronize()
-print(f"{args.config} prefill chunk: batch {B} x {Lp} tokens, one layer (median of {args.reps} after 2 warm-up)")
+print(f"{args.config} prefill chunk: batch {B} x {Lp} tokens, one layer (median of {args.reps} after 2 warm-up), "
+      f"gemm pair mode {args.pair}")
 tot = 0.0
 for k in kinds:
     ms = mx.probe_read(k)[2:]

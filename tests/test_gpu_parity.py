@@ -50,6 +50,42 @@ def test_gemm_packed_weights(M, N, K, ks):
     assert rel(C.cpu(), X.double() @ W.double().T) < 1e-5
 
 
+@pytest.fixture
+def gemm_pair():
+    """Forces the CTA-pair (cta_group::2) GEMM on for every eligible call; restores the default."""
+    L.call("ssm_dbg_set_gemm_pair", 1)
+    yield
+    L.call("ssm_dbg_set_gemm_pair", -1)
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 200, 320), (384, 512, 2560), (1000, 192, 640), (257, 2560, 5120),
+                                   (129, 48, 64), (4096, 10240 // 4, 2560), (2048 + 77, 2560, 640)])
+def test_gemm_cta_pair_bf16(gemm_pair, M, N, K):
+    """The CTA-pair GEMM (two CTAs of a cluster share one 256-row UMMA tile: each loads 128 rows of
+    A and half of B's rows, the leader issues cta_group::2 MMAs into both TMEMs) on ragged shapes:
+    M not a multiple of 256 (the second CTA's rows partly or wholly outside A), N not a multiple of
+    the tile, short and long K."""
+    dims = synth.MixerDims(d_model=64, d_inner=128, dt_rank=4)
+    mx = TPMixer(dims, "bf16")
+    g = torch.Generator().manual_seed(M * 5 + N + K)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, generator=g).to(torch.bfloat16)
+    C = torch.empty(M, N, device="cuda")
+    mx.dbg_gemm(A.cuda(), B.cuda(), C)
+    torch.cuda.synchronize()
+    assert rel(C.cpu(), A.double() @ B.double().T) < 1e-5
+
+
+@pytest.mark.parametrize("dims_name", ["med", "med_zamba"])
+def test_mixer_tp1_bf16_cta_pair_gemms(gemm_pair, dims_name):
+    """Every prefill projection that can run on CTA pairs does (in_proj, x_proj, dt_proj, out_proj
+    with its residual add): same oracle bar as the default path."""
+    dims = {"med": MED, "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2)}[dims_name]
+    gpu, ref, res, st, st_ref, _ = _run_tp1(dims, "bf16", 3, 150, 4)
+    assert rel(gpu - res, ref - res) < TOL["bf16"]
+    assert rel(st[1], st_ref[1]) < TOL["bf16"]
+
+
 def test_gemm_simt_fp32():
     dims = synth.MixerDims(d_model=64, d_inner=128, dt_rank=4)
     mx = TPMixer(dims, "fp32")
@@ -539,14 +575,22 @@ def test_empty_calls_are_noops_and_state_untouched():
     del e
 
 
-@pytest.mark.parametrize("k,qblk", [(2, 128), (4, 128), (2, 64)])
-def test_prefill_out_proj_quant_epilogue_bitexact(k, qblk):
+@pytest.mark.parametrize("k,qblk,pair", [(2, 128, 0), (4, 128, 0), (2, 64, 0), (2, 128, 1), (4, 64, 1)])
+def test_prefill_out_proj_quant_epilogue_bitexact(k, qblk, pair):
     """a8 fused: at prefill with the one-shot int8 schedule the out_proj epilogue quantises its TMEM
     accumulator straight into the symmetric buffer.  Its codes and scales must equal qar_ref's
     quantisation of the rank's fp32 partial (taken from the same prefill run with SSM_AR2_EXTERNAL,
-    which writes that partial instead) bit for bit (reading Q6-Q8)."""
+    which writes that partial instead) bit for bit (reading Q6-Q8).  pair = 1: every eligible GEMM on
+    CTA pairs (the quantising drain then runs in both CTAs of a pair)."""
+    L.call("ssm_dbg_set_gemm_pair", pair if pair else -1)
+    try:
+        _quant_epilogue_bitexact(k, qblk, 2, 150 if pair else 40)
+    finally:
+        L.call("ssm_dbg_set_gemm_pair", -1)
+
+
+def _quant_epilogue_bitexact(k, qblk, B, Lp):
     dims = MED
-    B, Lp = 2, 40
     w = prep_weights(dims, 0, "bf16")
     x, res = prep_acts(B, Lp, dims, "bf16", seed=23)
     n = B * Lp * dims.d_model
