@@ -498,14 +498,18 @@ def main():
     if pre_ms:
         avg = statistics.mean(pre_ms)
         flops = 2 * Mc * D * 2 * Ek
-        peak = peaks.get("bf16_tflops_sustained", 1394.1)
+        # the burst peak (cuBLAS best of 10 at full clocks) is the denominator: the in_proj runs for ~1.2 ms
+        # between MUFU-bound scans, at the bench's full SM clock; the sustained (power-capped) figure beside it
+        peak = peaks.get("bf16_tflops", 1614.6)
+        peak_s = peaks.get("bf16_tflops_sustained", 1364.7)
         ach = flops / (avg / 1000) / 1e12
         roofs["in_proj_prefill"] = {
-            "kernel": "gemm_tc_kernel (prefill in_proj, tcgen05)", "bound": "tensor", "achieved": ach, "peak": peak,
-            "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic.get("in_proj_prefill"), "launch_ms": avg,
+            "kernel": "gemm_tc_kernel (prefill in_proj, tcgen05, CTA pairs)", "bound": "tensor", "achieved": ach,
+            "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "peak_sustained": peak_s,
+            "frac_sustained": ach / peak_s, "traffic": traffic.get("in_proj_prefill"), "launch_ms": avg,
             "launches": len(pre_ms), "step_share_ms": sum(pre_ms) / args.steps,
             "work_per_launch": f"2*M*D*2E_k = {flops:.3e} flop (M={Mc})",
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst); bf16_tflops_sustained beside it"}
     if dec_ms_launch:
         avg = statistics.mean(dec_ms_launch)
         fused = stack.mx.fused_calls() > 0

@@ -850,6 +850,20 @@ __global__ void pack_blocked_kernel(const __nv_bfloat16* __restrict__ w, int row
 }
 }  // namespace
 
+bool encode_tmap_2d(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int elem_bytes,
+                    int box_cols, int box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc || (elem_bytes != 2 && elem_bytes != 4)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * elem_bytes)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 size_t packed_blocked_bytes(int rows, int cols) {
   const int64_t mt = (rows + BM - 1) / BM, kbt = (cols + BK - 1) / BK;
   return (size_t)(mt * kbt * BM * BK * 2);

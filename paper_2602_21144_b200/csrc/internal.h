@@ -1,5 +1,6 @@
 // internal.h — launchers shared between the kernels and the C-ABI layer (api.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -79,6 +80,11 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
                          int K, int ksplit, const Epilogue& epi, int num_sms, cudaStream_t s, bool a_indep = false,
                          const __nv_bfloat16* A_blocked = nullptr);
 size_t packed_blocked_bytes(int rows, int cols);
+// 2D tensor map (no swizzle, zero fill out of bounds) of a row-major [rows x cols] matrix of bf16
+// (elem_bytes 2) or fp32 (4) with row stride ld elements; box box_rows x box_cols.  False if the
+// driver entry point is missing or the encode fails (pointer / stride not 16-B aligned).
+bool encode_tmap_2d(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int elem_bytes,
+                    int box_cols, int box_rows);
 cudaError_t pack_blocked(const __nv_bfloat16* w, int rows, int cols, int64_t ld, __nv_bfloat16* out, cudaStream_t s);
 bool gemm_tc_supported(const void* A, int64_t lda, const void* B, int64_t ldb);
 // SIMT GEMM, fp32 accumulation, T = float or bf16 inputs.

@@ -11,6 +11,7 @@
 //  quantize/qar     a8/a9            int8 per-block codes, fixed-order dequant-accumulate
 //  peer_barrier     a4/a9            epoch flags over NVLink (st.release.sys / ld.acquire.sys)
 //  rmsnorm                           pre-norm glue (reading Q16)
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -325,28 +326,29 @@ __global__ void __launch_bounds__(256) unpack_kernel(Peers src, int nsrc, int64_
 
 constexpr int SC_THREADS = 128;  // channels per block
 
-// One thread per (batch row, channel); N states in registers; tiles of u, delta, z
-// (bf16 or fp32) and B||C (fp32) staged through shared memory with cp.async double
-// buffering.  h_t = exp(delta A) h_{t-1} + delta B_t u_t;  y = <C_t, h_t> + D u;  g = y SiLU(z).
+// One thread per (batch row, channel); N states in registers; tiles of u, delta, z (bf16 or
+// fp32: SC_TT tokens x 128 channels) and B||C (fp32: SC_TT tokens x 2N) staged through shared
+// memory by TMA (cp.async.bulk.tensor 2D boxes, one thread issues the tile's four loads onto the
+// buffer's mbarrier), double buffered.  h_t = exp(delta A) h_{t-1} + delta B_t u_t;
+// y = <C_t, h_t> + D u;  g = y SiLU(z).  The tensor maps span all batch * L token rows, so a tile's
+// rows past this row's L belong to the next batch row (loaded, never used) or lie outside the
+// tensor (zero-filled); channels past nch are zero-filled.
 template <typename T, int N, bool FAST>
-__global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ u, int64_t ldu,
-                                                          const T* __restrict__ dl, int64_t ldd,
-                                                          const T* __restrict__ z, int64_t ldz,
-                                                          const float* __restrict__ BC, int64_t ldbc,
+__global__ void __launch_bounds__(SC_THREADS) scan_kernel(const __grid_constant__ CUtensorMap tm_u,
+                                                          const __grid_constant__ CUtensorMap tm_d,
+                                                          const __grid_constant__ CUtensorMap tm_z,
+                                                          const __grid_constant__ CUtensorMap tm_bc,
                                                           const float* __restrict__ a_log,
                                                           const float* __restrict__ d_skip, float* __restrict__ h,
                                                           int64_t h_bstride, T* __restrict__ g, int64_t ldg, int L,
                                                           int nch) {
-  pdl_trigger();
-  pdl_wait();
-  constexpr int V = vec_of<T>();
   constexpr int SC_TT = sizeof(T) == 2 ? 16 : 8;  // tokens per staged tile (static smem < 48 KB)
-  constexpr int CH_CHUNKS = SC_THREADS / V;  // 16-B chunks per channel row
-  constexpr int BC_CHUNKS = 2 * N * 4 / 16;
-  __shared__ __align__(16) T su[2][SC_TT][SC_THREADS];
-  __shared__ __align__(16) T sd[2][SC_TT][SC_THREADS];
-  __shared__ __align__(16) T sz[2][SC_TT][SC_THREADS];
-  __shared__ __align__(16) float sbc[2][SC_TT][2 * N];
+  __shared__ __align__(128) T su[2][SC_TT][SC_THREADS];
+  __shared__ __align__(128) T sd[2][SC_TT][SC_THREADS];
+  __shared__ __align__(128) T sz[2][SC_TT][SC_THREADS];
+  __shared__ __align__(128) float sbc[2][SC_TT][2 * N];
+  __shared__ __align__(8) uint64_t mb[2];
+  constexpr uint32_t kTileBytes = 3u * SC_TT * SC_THREADS * sizeof(T) + SC_TT * 2 * N * 4;
 
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
@@ -354,26 +356,26 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
   const int d = cbase + tid;
   const bool valid = d < nch;
   const int64_t row0 = (int64_t)b * L;
+  if (tid == 0) {
+    tma_prefetch_desc(&tm_u);
+    tma_prefetch_desc(&tm_d);
+    tma_prefetch_desc(&tm_z);
+    tma_prefetch_desc(&tm_bc);
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
 
-  auto load_tile = [&](int buf, int tile) {
-    const int tb = tile * SC_TT;
-    for (int i = tid; i < SC_TT * CH_CHUNKS; i += SC_THREADS) {
-      const int r = i / CH_CHUNKS, c = i % CH_CHUNKS;
-      const int t = tb + r;
-      const int ch = cbase + c * V;
-      const bool ok = (t < L) && (ch < nch);
-      const int64_t row = row0 + (ok ? t : 0);
-      const int chs = ok ? ch : 0;
-      cp_async16(&su[buf][r][c * V], u + row * ldu + chs, ok);
-      cp_async16(&sd[buf][r][c * V], dl + row * ldd + chs, ok);
-      cp_async16(&sz[buf][r][c * V], z + row * ldz + chs, ok);
-    }
-    for (int i = tid; i < SC_TT * BC_CHUNKS; i += SC_THREADS) {
-      const int r = i / BC_CHUNKS, c = i % BC_CHUNKS;
-      const int t = tb + r;
-      const bool ok = t < L;
-      cp_async16(&sbc[buf][r][c * 4], BC + (row0 + (ok ? t : 0)) * ldbc + c * 4, ok);
-    }
+  auto load_tile = [&](int buf, int tile) {  // thread 0
+    const int row = (int)(row0 + tile * SC_TT);
+    mbar_arrive_expect_tx(&mb[buf], kTileBytes);
+    tma_load_2d(&su[buf][0][0], &tm_u, &mb[buf], cbase, row);
+    tma_load_2d(&sd[buf][0][0], &tm_d, &mb[buf], cbase, row);
+    tma_load_2d(&sz[buf][0][0], &tm_z, &mb[buf], cbase, row);
+    tma_load_2d(&sbc[buf][0][0], &tm_bc, &mb[buf], 0, row);
   };
 
   float A[N], hs[N];
@@ -396,18 +398,12 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const T* __restrict__ 
   }
 
   const int ntiles = (L + SC_TT - 1) / SC_TT;
-  load_tile(0, 0);
-  cp_async_commit();
+  if (tid == 0) load_tile(0, 0);
   for (int it = 0; it < ntiles; ++it) {
     const int buf = it & 1;
-    if (it + 1 < ntiles) {
-      load_tile(buf ^ 1, it + 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    // the other buffer was released by every thread at the end of the previous tile
+    if (tid == 0 && it + 1 < ntiles) load_tile(buf ^ 1, it + 1);
+    mbar_wait(&mb[buf], (uint32_t)(it >> 1) & 1u);
     if (valid) {
       const int tb = it * SC_TT;
       const int tn = min(SC_TT, L - tb);
@@ -1024,9 +1020,17 @@ static cudaError_t scan_t(const void* u, int64_t ldu, const void* dl, int64_t ld
                           const float* BC, int64_t ldbc, const float* a_log, const float* d_skip, float* h,
                           int64_t hbs, void* g, int64_t ldg, int batch, int L, int nch, cudaStream_t s) {
   dim3 grid((nch + SC_THREADS - 1) / SC_THREADS, batch);
-  { cudaError_t e_ = launch(scan_kernel<T, N, F>, grid, SC_THREADS, 0, s, 
-      reinterpret_cast<const T*>(u), ldu, reinterpret_cast<const T*>(dl), ldd, reinterpret_cast<const T*>(z), ldz, BC,
-      ldbc, a_log, d_skip, h, hbs, reinterpret_cast<T*>(g), ldg, L, nch); if (e_ != cudaSuccess) return e_; }
+  constexpr int TT = sizeof(T) == 2 ? 16 : 8;
+  const int64_t rows = (int64_t)batch * L;
+  const int es = (int)sizeof(T);
+  CUtensorMap mu, md, mz, mbc;
+  if (rows > INT32_MAX || !encode_tmap_2d(&mu, u, rows, nch, ldu, es, SC_THREADS, TT) ||
+      !encode_tmap_2d(&md, dl, rows, nch, ldd, es, SC_THREADS, TT) ||
+      !encode_tmap_2d(&mz, z, rows, nch, ldz, es, SC_THREADS, TT) ||
+      !encode_tmap_2d(&mbc, BC, rows, 2 * N, ldbc, 4, 2 * N, TT))
+    return cudaErrorInvalidValue;
+  { cudaError_t e_ = launch(scan_kernel<T, N, F>, grid, SC_THREADS, 0, s, mu, md, mz, mbc, a_log, d_skip, h, hbs,
+                            reinterpret_cast<T*>(g), ldg, L, nch); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 
