@@ -20,4 +20,5 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:m2_s
   python bench.py --config mamba2-2.7b --steps 1 --warmup 1 --no-cpu --no-e2e --layers 2 > /dev/null 2>&1
 timeout 600 python scripts/dstack_trace.py > $O/ev_dstack_trace.txt 2>&1
 timeout 600 python scripts/prefill_time.py --reps 5 > $O/ev_prefill_time.txt 2>&1
+timeout 600 python scripts/kernel_rooflines.py --json $O/ev_rooflines.json > $O/ev_rooflines.txt 2>&1
 ls -la $O/ev_*

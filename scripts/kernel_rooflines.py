@@ -4,7 +4,7 @@ prompt 2048 (one chunk) and single-token decode, TP=1.  Each kernel kind is time
 library's CUDA-event probes (eager launches, weights of `--layers` distinct layers so they
 stream from HBM), and its ALGORITHMIC work -- SURVEY.md §8(d) per-unit figures x the units one
 launch processes -- is divided by the median launch time and by the binding peak
-(MEASURED_PEAKS.json: hbm_gbs, bf16_tflops_sustained; MUFU from the guide's unit count:
+(MEASURED_PEAKS.json: hbm_gbs, bf16_tflops -- the burst figure: each GEMM runs ~1 ms at full clock; MUFU from the guide's unit count:
 16 ex2/clk/SM x 148 SMs x the max SM clock).
     python scripts/kernel_rooflines.py [--layers 8] [--json out.json]
 """
@@ -31,7 +31,7 @@ def main():
     a = p.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     hbm = peaks["hbm_gbs"] * 1e9
-    tc = peaks["bf16_tflops_sustained"] * 1e12
+    tc = peaks["bf16_tflops"] * 1e12
     mufu = 16 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # ex2 per second
     dims = synth.CONFIGS[a.config]
     wl = synth.WORKLOADS[a.config]
