@@ -121,7 +121,7 @@ def main():
     ]
     out = []
     print(f"{a.config}: batch {B}, prefill M={M} tokens, d_model {D}, d_inner {E}; peaks: HBM {hbm / 1e9:.0f} GB/s, "
-          f"bf16 {tc / 1e12:.0f} TF/s (sustained), MUFU {mufu / 1e12:.2f} T ex2/s")
+          f"bf16 {tc / 1e12:.0f} TF/s (burst), MUFU {mufu / 1e12:.2f} T ex2/s")
     print(f"{'row':6s} {'kernel':52s} {'us':>9s} {'achieved':>12s} {'peak':>10s} {'frac':>6s}")
     for row, name, t, work, unit, peak, bound, desc in rows:
         ach = work / t
