@@ -505,12 +505,12 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
       CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, e, s));
     } else {
       Epilogue e = epi(oacc ? EPI_ADD_F32 : EPI_STORE_F32, 0, odst, D);
-      if (x_next) {
+      if (x_next && t->k == 1) {
         e.cpy = x_next;
         e.ssq = reinterpret_cast<float*>(W + L.ssq);
       }
       CU(gemm(t, g, Ek, w->w_out, Ek, (int)M, D, Ek, 1, e, s));
-      if (x_next) {
+      if (x_next && t->k == 1) {
         t->launches++;
         CU(launch_ssq_finalize(reinterpret_cast<float*>(W + L.ssq), (D + 31) / 32, ss_next, M, s));
       }
@@ -548,7 +548,8 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->launches += 7;
     t->ar_count++;
     t->bytes_sent += (nD + 2 * nD / t->k) * (t->k - 1) / t->k + nD / c.qar_block * 4;
-    CU(launch_qar_twoshot(t->peers, t->rank, t->k, half_off(ep2), part, nD, c.qar_block, residual, 1, s));
+    CU(launch_qar_twoshot(t->peers, t->rank, t->k, half_off(ep2), part, nD, c.qar_block, residual, 1, s, x_next,
+                          x_next ? reinterpret_cast<float*>(W + L.ssq) : nullptr, D));
   } else if (omode == OUT_INT8) {
     Probe pr(t, SSM_PROBE_AR2, s);
     int8_t* q = reinterpret_cast<int8_t*>(own_half(ep2));
@@ -559,7 +560,13 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     t->bytes_sent += nD + nD / c.qar_block * 4;
     CU(launch_peer_barrier(t->peers, t->rank, t->k, s));
     CU(launch_qar_reduce(t->peers, t->k, half_off(ep2), half_off(ep2) + (int64_t)al256(nD), nD, c.qar_block, residual,
-                         1, s));
+                         1, s, x_next, x_next ? reinterpret_cast<float*>(W + L.ssq) : nullptr, D));
+  }
+  // TP > 1 with the pre-norm folded (prefill_normed): the AR#2 kernel that finished the residual rows
+  // wrote their bf16 copy and per-chunk sums of squares; the row statistic for the next in_proj
+  if (x_next && t->k > 1) {
+    t->launches++;
+    CU(launch_ssq_finalize(reinterpret_cast<float*>(W + L.ssq), (D + 31) / 32, ss_next, M, s));
   }
   return SSM_OK;
 }
@@ -798,11 +805,14 @@ ssm_status_t ssm_mixer_prefill_normed(ssm_tp_t tp, const ssm_layer_weights_t* w,
   if (!ss_in || ((x_next == nullptr) != (ss_next == nullptr))) return fail(SSM_ERR_ARG, "ss_in NULL, or x_next / ss_next not both set");
   if (!(norm_eps >= 0.f)) return fail(SSM_ERR_ARG, "norm_eps must be >= 0");
   const int D = tp->cfg.d_model, Ek = tp->Ek;
-  // the residual is updated by this rank's out_proj epilogue only at TP = 1 (at TP > 1 AR#2 does it);
-  // both projections on the tcgen05 GEMM
-  if (tp->k != 1 || !tp->bf16 || (flags & SSM_TP_NAIVE) || D % 8 ||
-      !gemm_tc_supported(x_in, D, w->w_in, D) || !gemm_tc_supported(w->w_out, Ek, w->w_out, Ek))
-    return fail(SSM_ERR_UNSUPPORTED, "prefill_normed: TP = 1, bf16, tcgen05-compatible strides only");
+  // the residual (and, with x_next, the next layer's pre-norm inputs) is finished by this rank's out_proj
+  // epilogue at TP = 1 and by the int8 AR#2's reduce / all-gather kernel at TP > 1 (one-shot or
+  // two-shot schedule); both projections on the tcgen05 GEMM
+  const bool ar2_int8 = (flags & SSM_AR2_INT8) || !(flags & (SSM_AR2_FP16 | SSM_AR2_BF16 | SSM_AR2_FP32 | SSM_AR2_EXTERNAL));
+  if ((tp->k > 1 && (!ar2_int8 || (flags & SSM_QAR_REQUANT) || D % 32)) || !tp->bf16 || (flags & SSM_TP_NAIVE) ||
+      D % 8 || !gemm_tc_supported(x_in, D, w->w_in, D) || !gemm_tc_supported(w->w_out, Ek, w->w_out, Ek))
+    return fail(SSM_ERR_UNSUPPORTED,
+                "prefill_normed: bf16, tcgen05-compatible strides, and at TP > 1 the int8 AR#2 (one- or two-shot)");
   if ((reinterpret_cast<uintptr_t>(x_next) & 15) || ((reinterpret_cast<uintptr_t>(ss_in) | reinterpret_cast<uintptr_t>(ss_next)) & 3))
     return fail(SSM_ERR_ARG, "x_next must be 16-B aligned, ss_in / ss_next 4-B aligned");
   if ((int64_t)batch * seqlen == 0) return SSM_OK;

@@ -122,9 +122,11 @@ cudaError_t launch_rmsnorm(int bf16, const float* x, const float* w, float eps, 
                            cudaStream_t s);
 // int8 quantisation of n fp32 values in blocks of blk: q [n] int8, scale [n/blk] f32.
 cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float* scale, cudaStream_t s);
-// out (+)= sum_r s_r q_r over k sources (fixed order 0..k-1).
+// out (+)= sum_r s_r q_r over k sources (fixed order 0..k-1).  cpy != NULL: also the next layer's
+// pre-norm inputs of the updated [n / D][D] rows: cpy = bf16(out) and per-32-column sums of squares -> ssq
+// (launch_ssq_finalize forms the row statistic); D % 32 == 0.  Same for the two-shot schedule's all-gather.
 cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, int64_t n, int blk, float* out,
-                              int accumulate, cudaStream_t s);
+                              int accumulate, cudaStream_t s, void* cpy = nullptr, float* ssq = nullptr, int D = 0);
 cudaError_t launch_f32_reduce(Peers src, int k, int64_t off, int64_t n, float* out, int accumulate, cudaStream_t s);
 // Requantised two-shot int8 (labelled variant of reading Q6): quantise, barrier, shard owner sums and
 // requantises, barrier, all-gather + dequantise; n % (k blk) == 0.
@@ -136,7 +138,8 @@ cudaError_t launch_w16_cast(int bf16, const float* x, int64_t n, void* out, cuda
 cudaError_t launch_w16_reduce(int bf16, Peers src, int k, int64_t off, int64_t n, float* out, int accumulate,
                               cudaStream_t s);
 cudaError_t launch_qar_twoshot(Peers peers, int rank, int k, int64_t off, const float* x, int64_t n, int blk,
-                               float* out, int accumulate, cudaStream_t s);
+                               float* out, int accumulate, cudaStream_t s, void* cpy = nullptr, float* ssq = nullptr,
+                               int D = 0);
 // All-gather of column slices (naive TP arm): out[m][r * wbytes + j] = src_r[off + m * wbytes + j] for
 // every rank r < k, bytes j < wbytes (multiple of 16); out row stride ldo_bytes.
 cudaError_t launch_gather_cols(Peers src, int k, int64_t off, int64_t M, int wbytes, void* out, int64_t ldo_bytes,

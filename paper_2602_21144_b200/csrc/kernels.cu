@@ -588,8 +588,39 @@ __global__ void quantize_kernel(const float* __restrict__ x, int64_t nblocks, in
   if (lane == 0) scale[blk] = s;
 }
 
+// Optional next-layer pre-norm statistics of the updated residual rows (RowOut, reading Q22 at TP > 1):
+// 16 consecutive values v of element group i (row m = 16 i / D) -> cpy = bf16(v) and, per 32-column chunk
+// (groups i, i ^ 1), its sum of squares -> ssq[m * D/32 + chunk] (the finalize kernel sums the chunks of
+// a row in fixed order, as after the TP = 1 out_proj epilogue).  Every rank runs the same arithmetic on
+// the same bits, so the replicas stay equal.
+struct RowOut {
+  __nv_bfloat16* cpy;
+  float* ssq;
+  int D;
+};
+SSM_DEV void rowout16(const RowOut& ro, int64_t i, const float (&v)[16]) {
+  uint32_t pk[8];
+  float sq = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    __nv_bfloat162 t2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+    pk[j] = *reinterpret_cast<uint32_t*>(&t2);
+    sq = fmaf(v[2 * j], v[2 * j], sq);
+    sq = fmaf(v[2 * j + 1], v[2 * j + 1], sq);
+  }
+  uint4* c = reinterpret_cast<uint4*>(ro.cpy + i * 16);
+  c[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  c[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+  // the partner group of the chunk is active whenever this one is (n16 even)
+  sq += __shfl_xor_sync(__activemask(), sq, 1);
+  if ((i & 1) == 0) {
+    const int64_t e0 = i * 16;
+    ro.ssq[(e0 / ro.D) * (ro.D / 32) + (e0 % ro.D) / 32] = sq;
+  }
+}
+
 __global__ void qar_reduce_kernel(Peers src, int k, int64_t q_off, int64_t s_off, int64_t n16, int blk,
-                                  float* __restrict__ out, int accumulate) {
+                                  float* __restrict__ out, int accumulate, RowOut ro) {
   pdl_trigger();
   pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -607,12 +638,15 @@ __global__ void qar_reduce_kernel(Peers src, int k, int64_t q_off, int64_t s_off
     for (int j = 0; j < 16; ++j) acc[j] = fmaf(s, (float)qq[j], acc[j]);
   }
   float4* o = reinterpret_cast<float4*>(out + i * 16);
+  float fin[16];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     float4 v = accumulate ? o[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     v.x += acc[4 * q]; v.y += acc[4 * q + 1]; v.z += acc[4 * q + 2]; v.w += acc[4 * q + 3];
     o[q] = v;
+    fin[4 * q] = v.x; fin[4 * q + 1] = v.y; fin[4 * q + 2] = v.z; fin[4 * q + 3] = v.w;
   }
+  if (ro.cpy) rowout16(ro, i, fin);
 }
 
 __global__ void f32_reduce_kernel(Peers src, int k, int64_t off, int64_t n4, float* __restrict__ out, int accumulate) {
@@ -702,7 +736,7 @@ __global__ void rs16_kernel(Peers src, int k, int64_t q_off, int64_t lo, int64_t
 }
 
 __global__ void ag16_kernel(Peers src, int64_t sum_off, int64_t shard, int64_t n16, const float* __restrict__ scale,
-                            int blk, float* __restrict__ out, int accumulate) {
+                            int blk, float* __restrict__ out, int accumulate, RowOut ro) {
   pdl_trigger();
   pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -715,6 +749,7 @@ __global__ void ag16_kernel(Peers src, int64_t sum_off, int64_t shard, int64_t n
   reinterpret_cast<int4*>(qv)[1] = reinterpret_cast<const int4*>(sp)[1];
   const float s = scale[e0 / blk];  // blk % 16 == 0: one block per group
   float4* o = reinterpret_cast<float4*>(out + e0);
+  float fin[16];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     float4 v = accumulate ? o[q] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -722,7 +757,9 @@ __global__ void ag16_kernel(Peers src, int64_t sum_off, int64_t shard, int64_t n
     v.x = __fadd_rn(v.x, __fmul_rn(s, (float)qv[4 * q])); v.y = __fadd_rn(v.y, __fmul_rn(s, (float)qv[4 * q + 1]));
     v.z = __fadd_rn(v.z, __fmul_rn(s, (float)qv[4 * q + 2])); v.w = __fadd_rn(v.w, __fmul_rn(s, (float)qv[4 * q + 3]));
     o[q] = v;
+    fin[4 * q] = v.x; fin[4 * q + 1] = v.y; fin[4 * q + 2] = v.z; fin[4 * q + 3] = v.w;
   }
+  if (ro.cpy) rowout16(ro, i, fin);
 }
 
 // ---------------------------------------------------------------- requantised two-shot int8 (labelled variant)
@@ -1133,17 +1170,21 @@ cudaError_t launch_quantize(const float* x, int64_t n, int blk, int8_t* q, float
 }
 
 cudaError_t launch_qar_reduce(Peers src, int k, int64_t q_off, int64_t s_off, int64_t n, int blk, float* out,
-                              int accumulate, cudaStream_t s) {
+                              int accumulate, cudaStream_t s, void* cpy, float* ssq, int D) {
   if (n <= 0) return cudaSuccess;
+  if (cpy && (!ssq || D % 32 || n % D)) return cudaErrorInvalidValue;
   const int64_t n16 = n / 16;
-  { cudaError_t e_ = launch(qar_reduce_kernel, (int)((n16 + 255) / 256), 256, 0, s, src, k, q_off, s_off, n16, blk, out, accumulate); if (e_ != cudaSuccess) return e_; }
+  const RowOut ro{reinterpret_cast<__nv_bfloat16*>(cpy), ssq, D};
+  { cudaError_t e_ = launch(qar_reduce_kernel, (int)((n16 + 255) / 256), 256, 0, s, src, k, q_off, s_off, n16, blk, out, accumulate, ro); if (e_ != cudaSuccess) return e_; }
   return cudaGetLastError();
 }
 
 // Two-shot int8 all-reduce (reading Q6).  Layout in every rank's buffer half at byte offset `off`:
 // amax [n/blk] f32 | scale [n/blk] f32 | codes [n] i8 | sums [n/k] i16 (each 256-B aligned).
 cudaError_t launch_qar_twoshot(Peers peers, int rank, int k, int64_t off, const float* x, int64_t n, int blk,
-                               float* out, int accumulate, cudaStream_t s) {
+                               float* out, int accumulate, cudaStream_t s, void* cpy, float* ssq, int D) {
+  if (cpy && (!ssq || D % 32 || n % D)) return cudaErrorInvalidValue;
+  const RowOut ro{reinterpret_cast<__nv_bfloat16*>(cpy), ssq, D};
   if (n <= 0) return cudaSuccess;
   if (n % (16 * k) || n % blk || blk % 16) return cudaErrorInvalidValue;
   const int64_t nb = n / blk;
@@ -1175,7 +1216,7 @@ cudaError_t launch_qar_twoshot(Peers peers, int rank, int k, int64_t off, const 
   if ((e_ = launch_peer_barrier(peers, rank, k, s)) != cudaSuccess) return e_;
   const int64_t n16 = n / 16;
   e_ = launch(ag16_kernel, (int)((n16 + 255) / 256), 256, 0, s, peers, o_sum, shard, n16,
-              reinterpret_cast<const float*>(own + o_scale), blk, out, accumulate);
+              reinterpret_cast<const float*>(own + o_scale), blk, out, accumulate, ro);
   if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
 }

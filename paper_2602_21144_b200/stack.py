@@ -106,10 +106,13 @@ class MixerStack:
                 self.hybrid[li] = (w, blk)
             self.t_buf = torch.empty((batch * max_chunk, d.d_model), device=mixer.device)
             self.h0_dec = torch.zeros((batch, d.d_model), device=mixer.device)
-        # prefill with the pre-norm folded around the projections (ssm_mixer_prefill_normed, TP = 1):
-        # x = bf16(residual) and its row statistic come from the previous layer's out_proj epilogue
-        self.prefill_normed = (mixer.tp_size == 1 and mixer.dtype == "bf16" and not self.hybrid
-                               and self.nccl is None and not (flags & L.SSM_TP_NAIVE))
+        # prefill with the pre-norm folded around the projections (ssm_mixer_prefill_normed): x =
+        # bf16(residual) and its row statistic come from the kernel that finished the previous layer's
+        # residual rows -- the out_proj epilogue at TP = 1, the int8 AR#2's reduce / all-gather at TP > 1
+        other_ar2 = L.SSM_AR2_FP16 | L.SSM_AR2_BF16 | L.SSM_AR2_FP32 | L.SSM_AR2_EXTERNAL | L.SSM_QAR_REQUANT
+        self.prefill_normed = (mixer.dtype == "bf16" and not self.hybrid and self.nccl is None
+                               and not (flags & L.SSM_TP_NAIVE)
+                               and (mixer.tp_size == 1 or (not (flags & other_ar2) and d.d_model % 32 == 0)))
         if self.prefill_normed:
             self.ssbuf = torch.empty((2, (batch * max_chunk + 3) // 4 * 4), dtype=torch.float32, device=mixer.device)
         self.graph = None

@@ -461,13 +461,16 @@ def test_rmsnorm_kernel():
     assert rel(y.cpu(), M.rmsnorm(x.numpy(), w.numpy(), 1e-5)) < 1e-6
 
 
-@pytest.mark.parametrize("k,mode", [(2, "int8"), (4, "fp32")])
-def test_virtual_tp_stack_prefill_then_graph_decode(k, mode):
+@pytest.mark.parametrize("k,mode,L_in", [(2, "int8", 12), (4, "fp32", 12), (4, "int8", 40), (8, "int8", 12)])
+def test_virtual_tp_stack_prefill_then_graph_decode(k, mode, L_in):
     """Two-layer pre-norm stack on k virtual ranks: eager chunked prefill, then decode steps
-    replayed from per-rank CUDA graphs (device-side AR epochs, alternating buffer halves)."""
+    replayed from per-rank CUDA graphs (device-side AR epochs, alternating buffer halves).  With the
+    int8 AR#2 the prefill runs ssm_mixer_prefill_normed at TP > 1: the one-shot reduce (k = 2, 8 at
+    24 tokens) or the two-shot all-gather (k = 4 at 80 tokens) writes the next layer's bf16 input and
+    row sums of squares -- no normalisation pass."""
     from paper_2602_21144_b200.stack import MixerStack
     dims = synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_layers=2)
-    B, L_in, L_out = 2, 12, 3
+    B, L_out = 2, 3
     flags = L.SSM_AR2_INT8 if mode == "int8" else L.SSM_AR2_FP32
     ws = [prep_weights(dims, l, "bf16") for l in range(2)]
     g = torch.Generator().manual_seed(5)
@@ -475,6 +478,7 @@ def test_virtual_tp_stack_prefill_then_graph_decode(k, mode):
     grp = VirtualGroup(dims, k, "bf16", B * L_in)
     stacks = [MixerStack(grp.mixers[r], [LayerWeights(dims, w, k, r, "bf16") for w in ws], B, L_in, flags)
               for r in range(k)]
+    assert stacks[0].prefill_normed == (mode == "int8")
     pre = [res0[:, :L_in].float().cuda().contiguous().view(B * L_in, -1) for _ in range(k)]
     rt = [torch.empty(B, dims.d_model, device="cuda") for _ in range(k)]
     torch.cuda.synchronize()
