@@ -131,50 +131,60 @@ __global__ void __launch_bounds__(CONV_CG) conv1d_silu_kernel(const T* __restric
 // continuously instead of in one burst per block (v2: 254 us per Mamba-2.8B layer, 0.4 of HBM).
 // A thread owns 8 channels x 8 tokens of a tile and stores 16-B vectors.
 constexpr int C3_CH = 1024, C3_TT = 16, C3_THREADS = 256;
+// Prefill conv1d + SiLU (row a2): persistent blocks (2 per SM) walk contiguous runs
+// of 16-token x 1024-channel tiles of one channel block (taps kept in registers across the run); each
+// tile (with its K - 1 halo rows) arrives by TMA -- four 256-channel boxes onto the buffer's mbarrier,
+// double buffered -- and a sequence's first tile takes its halo from the cached window (166 -> 140 us
+// per Mamba-2.8B layer against the cp.async version).
 template <int K>
-__global__ void __launch_bounds__(C3_THREADS, 2) conv1d_silu_v3_kernel(const __nv_bfloat16* __restrict__ xz, int64_t ldxz,
+__global__ void __launch_bounds__(C3_THREADS, 2) conv1d_silu_v3_kernel(const __grid_constant__ CUtensorMap tm_x,
                                                                     const __nv_bfloat16* __restrict__ cst,
                                                                     const float* __restrict__ cw,
                                                                     const float* __restrict__ cb,
                                                                     __nv_bfloat16* __restrict__ u, int64_t ldu, int L,
                                                                     int Ek, int batch) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ __align__(16) __nv_bfloat16 sx3_raw[];
-  constexpr int ROWS = C3_TT + K - 1, CPR = C3_CH / 8;
-  auto sx = reinterpret_cast<__nv_bfloat16(*)[ROWS][C3_CH]>(sx3_raw);
+  extern __shared__ __align__(128) __nv_bfloat16 sx3_raw[];
+  __shared__ __align__(8) uint64_t mb[2];
+  constexpr int ROWS = C3_TT + K - 1, CPR = C3_CH / 8, SUB = C3_CH / 256;
+  // tile [SUB][ROWS][256]: one TMA box (256 channels x ROWS tokens) per sub-block
+  auto sxp = [&](int buf, int r, int cgi) { return sx3_raw + ((buf * SUB + (cgi >> 5)) * ROWS + r) * 256 + (cgi & 31) * 8; };
   const int nchb = (Ek + C3_CH - 1) / C3_CH, ntt = (L + C3_TT - 1) / C3_TT;
   const int items = nchb * ntt * batch;
   const int tid = threadIdx.x, cg = tid % CPR, tl = tid / CPR;
+  if (tid == 0) {
+    tma_prefetch_desc(&tm_x);
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
   auto coords = [&](int it, int& c0, int& t0, int& b) {
     t0 = (it % ntt) * C3_TT;
     const int r = it / ntt;
     c0 = (r % nchb) * C3_CH;
     b = r / nchb;
   };
+  // thread 0: the tile's rows t0 - (K-1) .. t0 + C3_TT - 1 of this sequence's x (rows of the previous
+  // sequence or below row 0 at t0 = 0 are replaced by the cached window after the load lands)
   auto load = [&](int buf, int it) {
     int c0, t0, b;
     coords(it, c0, t0, b);
-    for (int i = tid; i < ROWS * CPR; i += C3_THREADS) {
-      const int r = i / CPR, c = (i % CPR) * 8;
-      const int t = t0 - (K - 1) + r;
-      const int ch = c0 + c;
-      const bool ok = t < L && ch < Ek;
-      const __nv_bfloat16* src = t < 0 ? cst + ((int64_t)b * (K - 1) + (K - 1) + t) * Ek + (ok ? ch : 0)
-                                       : xz + ((int64_t)b * L + (ok ? t : 0)) * ldxz + (ok ? ch : 0);
-      cp_async16(&sx[buf][r][c], src, ok);
-    }
+    fence_proxy_async();  // the halo rows this buffer got from generic stores are overwritten by TMA
+    mbar_arrive_expect_tx(&mb[buf], (uint32_t)(SUB * ROWS * 256 * 2));
+    for (int j = 0; j < SUB; ++j)
+      tma_load_2d(sx3_raw + (buf * SUB + j) * ROWS * 256, &tm_x, &mb[buf], c0 + 256 * j, b * L + t0 - (K - 1));
   };
   // a contiguous run of items per block (t-tiles fastest): the taps are reloaded only when the
   // channel block changes
   const int it0 = (int)((int64_t)items * blockIdx.x / gridDim.x), it1 = (int)((int64_t)items * (blockIdx.x + 1) / gridDim.x);
   int buf = 0, wc0 = -1;
+  uint32_t ph[2] = {0u, 0u};
   float w[K][8], bias[8];
-  if (it0 < it1) load(0, it0);
-  cp_async_commit();
+  if (tid == 0 && it0 < it1) load(0, it0);
   for (int it = it0; it < it1; ++it, buf ^= 1) {
-    if (it + 1 < it1) load(buf ^ 1, it + 1);
-    cp_async_commit();
+    if (tid == 0 && it + 1 < it1) load(buf ^ 1, it + 1);
     int c0, t0, b;
     coords(it, c0, t0, b);
     const int d0 = c0 + cg * 8;
@@ -187,14 +197,24 @@ __global__ void __launch_bounds__(C3_THREADS, 2) conv1d_silu_v3_kernel(const __n
       }
     }
     wc0 = c0;
-    cp_async_wait<1>();
-    __syncthreads();
+    mbar_wait(&mb[buf], ph[buf]);
+    ph[buf] ^= 1u;
+    if (t0 == 0) {  // sequence start: the halo rows come from the cached window
+      __syncthreads();
+      for (int i = tid; i < (K - 1) * CPR; i += C3_THREADS) {
+        const int r = i / CPR, cgi = i % CPR, ch = c0 + cgi * 8;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (ch < Ek) v = *reinterpret_cast<const uint4*>(cst + ((int64_t)b * (K - 1) + r) * Ek + ch);
+        *reinterpret_cast<uint4*>(sxp(buf, r, cgi)) = v;
+      }
+      __syncthreads();
+    }
     if (d0 < Ek) {
       constexpr int TPT = C3_TT / (C3_THREADS / CPR);  // tokens per thread
       const int tb = tl * TPT;
       float win[K][8];
 #pragma unroll
-      for (int j = 0; j < K - 1; ++j) Vec<__nv_bfloat16, 8>::load(&sx[buf][tb + j][cg * 8], win[j + 1]);
+      for (int j = 0; j < K - 1; ++j) Vec<__nv_bfloat16, 8>::load(sxp(buf, tb + j, cg), win[j + 1]);
 #pragma unroll
       for (int i = 0; i < TPT; ++i) {
         const int t = t0 + tb + i;
@@ -203,7 +223,7 @@ __global__ void __launch_bounds__(C3_THREADS, 2) conv1d_silu_v3_kernel(const __n
         for (int j = 0; j < K - 1; ++j)
 #pragma unroll
           for (int v = 0; v < 8; ++v) win[j][v] = win[j + 1][v];
-        Vec<__nv_bfloat16, 8>::load(&sx[buf][tb + i + K - 1][cg * 8], win[K - 1]);
+        Vec<__nv_bfloat16, 8>::load(sxp(buf, tb + i + K - 1, cg), win[K - 1]);
         float o[8];
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
@@ -217,7 +237,6 @@ __global__ void __launch_bounds__(C3_THREADS, 2) conv1d_silu_v3_kernel(const __n
     }
     __syncthreads();  // this buffer is refilled by the load issued in the next iteration
   }
-  cp_async_wait<0>();
 }
 
 // conv window after the chunk: last K-1 entries of xt = conv_state || x
@@ -941,10 +960,13 @@ cudaError_t conv_dispatch(const void* xz, int64_t ldxz, const void* cs, const fl
       }
       const int items = ((Ek + C3_CH - 1) / C3_CH) * ((L + C3_TT - 1) / C3_TT) * batch;
       const int grid3 = items < 2 * sms ? items : 2 * sms;
+      CUtensorMap mx;
+      if ((int64_t)batch * L > INT32_MAX || !encode_tmap_2d(&mx, x, (int64_t)batch * L, Ek, ldxz, 2, 256, C3_TT + K - 1))
+        return cudaErrorInvalidValue;
       switch (K) {
-        case 2: e_ = launch(conv1d_silu_v3_kernel<2>, grid3, C3_THREADS, sm, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek, batch); break;
-        case 3: e_ = launch(conv1d_silu_v3_kernel<3>, grid3, C3_THREADS, sm, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek, batch); break;
-        default: e_ = launch(conv1d_silu_v3_kernel<4>, grid3, C3_THREADS, sm, s, x, ldxz, c, cw, cb, uu, ldu, L, Ek, batch); break;
+        case 2: e_ = launch(conv1d_silu_v3_kernel<2>, grid3, C3_THREADS, sm, s, mx, c, cw, cb, uu, ldu, L, Ek, batch); break;
+        case 3: e_ = launch(conv1d_silu_v3_kernel<3>, grid3, C3_THREADS, sm, s, mx, c, cw, cb, uu, ldu, L, Ek, batch); break;
+        default: e_ = launch(conv1d_silu_v3_kernel<4>, grid3, C3_THREADS, sm, s, mx, c, cw, cb, uu, ldu, L, Ek, batch); break;
       }
       if (e_ != cudaSuccess) return e_;
       return cudaGetLastError();
