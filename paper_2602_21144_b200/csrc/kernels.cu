@@ -303,18 +303,31 @@ __global__ void __launch_bounds__(256) unpack_kernel(Peers src, int nsrc, int64_
   constexpr int CPL = kMaxP / 32;
   float v[CPL];
   float ss[3] = {0.f, 0.f, 0.f};
+  // fixed rank order 0..nsrc-1 (reading Q12): every load of a source issued before any add, so a row's
+  // loads are in flight together (a per-element source loop serialised them: latency-bound)
+  {
+    const float* s0 = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[0]) + off) + base;
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = lane + 32 * i;
+      v[i] = c < P ? s0[c] : 0.f;
+    }
+  }
+  for (int sr = 1; sr < nsrc; ++sr) {
+    const float* sp = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[sr]) + off) + base;
+    float t[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) t[i] = lane + 32 * i < P ? sp[lane + 32 * i] : 0.f;
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) v[i] = v[i] + t[i];
+  }
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
     const int c = lane + 32 * i;
-    float acc = 0.f;
     if (c < P) {
-      for (int s = 0; s < nsrc; ++s)  // fixed rank order 0..nsrc-1 (reading Q12)
-        acc = (s == 0) ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[s]) + off)[base + c]
-                       : acc + reinterpret_cast<const float*>(reinterpret_cast<const char*>(src.p[s]) + off)[base + c];
       const int f = c < R ? 0 : (c < R + N ? 1 : 2);
-      ss[f] = fmaf(acc, acc, ss[f]);
+      ss[f] = fmaf(v[i], v[i], ss[f]);
     }
-    v[i] = acc;
   }
   float scale[3] = {1.f, 1.f, 1.f};
   if (rmsnorm) {
