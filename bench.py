@@ -210,7 +210,7 @@ def launch_ranks(args):
     import socket
     import torch
     n = torch.cuda.device_count()
-    if n < args.gpus:
+    if n < args.gpus and not os.environ.get("BENCH_RANKS_SHARE_GPU"):
         sys.stderr.write(f"bench.py: --gpus {args.gpus} but this node has {n} CUDA device(s)\n")
         sys.exit(2)
     with socket.socket() as s:
@@ -247,10 +247,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (TP degree = number of ranks)")
+    # BENCH_RANKS_SHARE_GPU=1 (test only: exercises the multi-rank launch, rendezvous and collectives on a
+    # one-GPU box; the ranks' contexts are time-sliced, so its numbers are not TP measurements)
+    if os.environ.get("BENCH_RANKS_SHARE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("BENCH_RANKS_SHARE_GPU"):  # NCCL refuses two ranks on one device
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     k = world
 
     from paper_2602_21144_b200 import _lib as L
@@ -268,16 +275,32 @@ def main():
     if naive:
         flags |= L.SSM_TP_NAIVE
 
-    peer_bufs, nbytes, symm = None, 0, None
+    peer_bufs, nbytes, symm, comm_kind = None, 0, None, None
     if k > 1:
-        import torch.distributed._symmetric_memory as symm_mem
         cfg = L.make_config(dims, cdt)
         nbytes = L.comm_bytes(cfg, k, B * chunk)
-        buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=dev)
-        buf.zero_()
-        hdl = symm_mem.rendezvous(buf, dist.group.WORLD.group_name)
-        peer_bufs = [int(p) for p in hdl.buffer_ptrs]
-        symm = (buf, hdl)
+        try:  # peer-mapped symmetric buffers (torch symmetric memory over NVLink)
+            if os.environ.get("BENCH_RANKS_SHARE_GPU"):
+                raise RuntimeError("ranks share one GPU")
+            import torch.distributed._symmetric_memory as symm_mem
+            buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=dev)
+            buf.zero_()
+            hdl = symm_mem.rendezvous(buf, dist.group.WORLD.group_name)
+            peer_bufs = [int(p) for p in hdl.buffer_ptrs]
+            symm = (buf, hdl)
+            comm_kind = "symmetric_memory"
+        except Exception as exc:  # the same buffers mapped by CUDA IPC handles (peer access over NVLink)
+            from torch.multiprocessing.reductions import reduce_tensor
+            if rank == 0:
+                sys.stderr.write(f"bench.py: symmetric memory unavailable ({type(exc).__name__}: {exc}); CUDA IPC\n")
+            buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+            torch.cuda.synchronize()
+            handles = [None] * k
+            dist.all_gather_object(handles, reduce_tensor(buf))
+            peers = [buf if r == rank else handles[r][0](*handles[r][1]) for r in range(k)]
+            peer_bufs = [int(t.data_ptr()) for t in peers]
+            symm = (buf, peers)
+            comm_kind = "cuda_ipc"
         dist.barrier()
     mx = TPMixer(dims, cdt, rank=rank, tp_size=k, peer_bufs=peer_bufs, buf_bytes=nbytes, device=dev)
     want_persistent = (args.decode_impl != "layer" and k == 1 and not mamba2 and args.config != "zamba7b"
@@ -566,7 +589,7 @@ def main():
                                        + f", d_model {dims.d_model}, batch {B}, prompt {Lp} + {Ld} decode",
                            "model": args.config, "global_batch": B,
                            "seq_len": Lp + Ld, "parallelism": f"tp{k}", "ar2": args.ar2 if k > 1 else "none",
-                           "tp_design": args.tp_design if k > 1 else "none",
+                           "tp_design": args.tp_design if k > 1 else "none", "comm": comm_kind or "none",
                            "prefill_chunk": chunk, "packed_decode_weights": not args.no_pack,
                            "decode_impl": "persistent" if persistent else "layer",
                            "l2": "inputs larger than L2 (prompt residual "
@@ -577,6 +600,14 @@ def main():
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if k > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+        # release the peers' mappings (CUDA IPC: every consumer drops its handles before any owner exits)
+        stack = mx = None
+        symm = peer_bufs = None
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
         dist.barrier()
         dist.destroy_process_group()
 
