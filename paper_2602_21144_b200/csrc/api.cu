@@ -433,13 +433,24 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     ldux = E;
   }
 
+  // TP = 1 prefill without the Falcon dt/B/C RMSNorm: the x_proj epilogue writes the unpacked fields
+  const bool split_dbc = bf && !decode && !swap && !ar1 && !naive && !c.bcdt_rmsnorm && R % 32 == 0 && P % 32 == 0 &&
+                         gemm_tc_supported(ux, ldux, w->w_x, Ek);
   // (a3) x_proj partial [M, hloc*P] fp32, straight into the symmetric buffer when AR#1 follows
   if (!fuse) {
     Probe pr(t, SSM_PROBE_X_PROJ, s);
     if (swap)
       CU(gemm(t, w->w_x, Ek, ux, ldux, hl * P, (int)M, Ek, ks_x,
               epi(ks_x != 1 ? EPI_ATOMIC_F32 : EPI_STORE_F32, 1, xdst, hl * P), s, true, naive ? nullptr : w->w_x_pk));
-    else
+    else if (split_dbc) {  // TP = 1: dt_low (bf16) and B || C (fp32) stored by the epilogue (no unpack pass)
+      Epilogue e = epi(EPI_SPLIT_DBC, 0, xdst, hl * P);
+      e.dbc_low = dlow;
+      e.dbc_bc = BC;
+      e.dbc_R = R;
+      e.dbc_P = P;
+      e.dbc_M = (int)M;
+      CU(gemm(t, ux, ldux, w->w_x, Ek, (int)M, hl * P, Ek, 1, e, s));
+    } else
       CU(gemm(t, ux, ldux, w->w_x, Ek, (int)M, hl * P, Ek, 1, epi(EPI_STORE_F32, 0, xdst, hl * P), s));
   }
 
@@ -467,9 +478,12 @@ ssm_status_t run_layer(ssm_tp_s* t, const ssm_layer_weights_t* w, ssm_state_s* s
     CU(launch_decode_step(bf, dsrc, nsrc, doff, hl * P, c.bcdt_rmsnorm, c.rms_eps, u, xzb + zoff * es, ldxz, w->w_dt,
                           w->b_dt, w->a_log, w->d_skip, st->h, g, batch, Ek, R, N, t->cph, nullptr, s));
   } else {
-    // (a4) unpack dt_low / B / C; (a5) dt_proj + softplus; (a6)+(a7) scan, D skip, gate
-    t->launches++;
-    CU(launch_unpack(bf, dsrc, nsrc, doff, (int)M, hl, R, N, c.bcdt_rmsnorm, c.rms_eps, dlow, BC, s));
+    // (a4) unpack dt_low / B / C (unless the x_proj epilogue split them); (a5) dt_proj + softplus;
+    // (a6)+(a7) scan, D skip, gate
+    if (!split_dbc) {
+      t->launches++;
+      CU(launch_unpack(bf, dsrc, nsrc, doff, (int)M, hl, R, N, c.bcdt_rmsnorm, c.rms_eps, dlow, BC, s));
+    }
     {
       Probe pr(t, SSM_PROBE_DT_PROJ, s);
       for (int j = 0; j < hl; ++j) {

@@ -182,6 +182,28 @@ __device__ __forceinline__ void epi_chunk(const Epilogue& e, int m0, int n0, int
     }
     return;
   }
+  if (FK < 0 && kind == EPI_SPLIT_DBC) {  // the chunk lies in one field of one head (R, P multiples of 32)
+    const int hd = n0 / e.dbc_P, c = n0 % e.dbc_P;
+    if (c < e.dbc_R) {
+      uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.dbc_low) +
+                                           ((int64_t)hd * e.dbc_M + m) * e.dbc_R + c);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t pw[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          __nv_bfloat162 t2 = __floats2bfloat162_rn(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]);
+          pw[j] = *reinterpret_cast<uint32_t*>(&t2);
+        }
+        d4[q] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+      }
+    } else {
+      float4* d4 = reinterpret_cast<float4*>(e.dbc_bc + ((int64_t)hd * e.dbc_M + m) * (e.dbc_P - e.dbc_R) + c - e.dbc_R);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    return;
+  }
   const bool full = (n0 + 32 <= N);
   const int64_t base = (int64_t)m * e.ldc + n0;
   if (kind == EPI_STORE_BF16 || kind == EPI_SOFTPLUS_BF16) {
@@ -935,7 +957,7 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
   // it on (1) or off (0) for tests and A/B runs
   const bool pair_ok = !epi.trans && ksplit <= 1 && !A_blocked && !a_indep && M > BM && N > 32 &&
                        (epi.kind == EPI_STORE_BF16 || epi.kind == EPI_STORE_F32 || epi.kind == EPI_ADD_F32 ||
-                        epi.kind == EPI_QUANT_I8 || epi.kind == EPI_SOFTPLUS_BF16);
+                        epi.kind == EPI_QUANT_I8 || epi.kind == EPI_SOFTPLUS_BF16 || epi.kind == EPI_SPLIT_DBC);
   // (measured, Mamba-2.8B prefill chunk of 32768 tokens: in_proj 1356 -> 1209 us, out_proj 690 -> 643 us,
   // x_proj 86 -> 82 us; the K = 160 dt_proj 139 -> 164 us stays on single CTAs)
   const bool pair_default = M >= 4096 && K >= 1024 && N >= 128 && epi.kind != EPI_SOFTPLUS_BF16;
@@ -1021,6 +1043,10 @@ cudaError_t gemm_tc_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat1
     extra = (N * 4 + 127) / 128 * 128 + 8 * 32 * 144;
     cr.ring -= extra;
   }
+  if (epi.kind == EPI_SPLIT_DBC &&
+      (epi.trans || ts.ksplit != 1 || epi.dbc_R % 32 || epi.dbc_P % 32 || epi.dbc_R >= epi.dbc_P || N % epi.dbc_P ||
+       epi.dbc_M != M || (reinterpret_cast<uintptr_t>(epi.dbc_low) & 15) || (reinterpret_cast<uintptr_t>(epi.dbc_bc) & 15)))
+    return cudaErrorInvalidValue;
   if (epi.zero && (reinterpret_cast<uintptr_t>(epi.zero) & 15)) return cudaErrorInvalidValue;
   while (kbs > 1 && num_stages(BN / CG, kbs, cr.ring) < 2) --kbs;
   const int smem_bytes = 1024 + cr.ring + 512 + extra;

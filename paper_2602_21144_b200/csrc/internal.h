@@ -20,6 +20,9 @@ enum EpiKind : int {
   EPI_ADD_F32 = 4,        // C f32 += acc            (read-modify-write; ksplit must be 1)
   EPI_ATOMIC_F32 = 5,     // C f32 += acc atomically (split-K; C pre-initialised)
   EPI_DECODE_INPROJ = 6,  // decode in_proj (swap-AB, bf16, N = batch <= 32), fused conv + x_proj; see below
+  EPI_SPLIT_DBC = 8,      // x_proj at TP = 1 (no AR#1): column n = hd P + c of row m -> c < R: bf16 into
+                          // dlow[(hd M + m) R + c], else fp32 into BC[(hd M + m) 2N + c - R] (the unpack
+                          // layout; trans = 0, R % 32 == 0, P % 32 == 0, ldc = P, M = rows; fields dbc_*)
   EPI_QUANT_I8 = 7,       // int8 per-block quantisation of the accumulator (prefill out_proj at TP > 1, the
                           // one-shot AR#2 schedule): per qblk consecutive columns n of a row m, amax = max |acc|,
                           // s = fl32(amax / 127), code = clamp(rint(fl32(acc / s)), +-127) (0 if s == 0) ->
@@ -55,6 +58,10 @@ struct Epilogue {
   // window cst + SiLU -> u (bf16 [N][Ek]) and the window shifted in place; Ek <= m < 2Ek are z
   // -> C[n * ldc + m] (bf16).  The CTA then contracts its 128 u channels with the matching
   // columns of W_x (mma.sync) and adds the partial x_proj [N][hl*P] into xacc (pre-zeroed).
+  // EPI_SPLIT_DBC
+  void* dbc_low;              // bf16 [hloc][M][R]
+  float* dbc_bc;              // fp32 [hloc][M][2N]
+  int dbc_R, dbc_P, dbc_M;
   void* cst;                  // [N][K-1][Ek] bf16
   const float* cw;            // [Ek][K]
   const float* cb;            // [Ek]

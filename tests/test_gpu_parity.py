@@ -173,11 +173,18 @@ def test_mixer_tp1_fp32_tiny_prefill_decode():
 
 
 @pytest.mark.parametrize("dims_name,pack", [("med", False), ("med_falcon", False), ("med_zamba", False),
-                                            ("med", True), ("med_zamba", True)])
+                                            ("med", True), ("med_zamba", True), ("med_r32", False),
+                                            ("med_zamba_r32", False), ("med_falcon_r32", False)])
 def test_mixer_tp1_bf16_prefill_decode(dims_name, pack):
+    """TP = 1 bf16 prefill + decode vs the oracle.  dt_rank 32 (P a multiple of 32): the x_proj epilogue
+    writes dt_low (bf16) and B || C (fp32) itself (EPI_SPLIT_DBC, per head for Zamba; Falcon keeps the
+    unpack pass for its dt/B/C RMSNorm)."""
     dims = {"med": MED,
             "med_falcon": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, bcdt_rmsnorm=True),
-            "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2)}[dims_name]
+            "med_zamba": synth.MixerDims(d_model=256, d_inner=512, dt_rank=16, n_heads=2),
+            "med_r32": synth.MixerDims(d_model=256, d_inner=512, dt_rank=32),
+            "med_zamba_r32": synth.MixerDims(d_model=256, d_inner=512, dt_rank=32, n_heads=2),
+            "med_falcon_r32": synth.MixerDims(d_model=256, d_inner=512, dt_rank=32, bcdt_rmsnorm=True)}[dims_name]
     gpu, ref, res, st, st_ref, mx = _run_tp1(dims, "bf16", 3, 150, 6, pack=pack)
     assert rel(gpu - res, ref - res) < TOL["bf16"]
     assert rel(st[1], st_ref[1]) < TOL["bf16"]
