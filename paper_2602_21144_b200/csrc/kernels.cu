@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(C3_THREADS, 2) conv1d_silu_v3_kernel(const __g
   // channel block changes
   const int it0 = (int)((int64_t)items * blockIdx.x / gridDim.x), it1 = (int)((int64_t)items * (blockIdx.x + 1) / gridDim.x);
   int buf = 0, wc0 = -1;
-  uint32_t ph[2] = {0u, 0u};
+  uint32_t ph = 0u;  // bit b: the parity buffer b waits for next
   float w[K][8], bias[8];
   if (tid == 0 && it0 < it1) load(0, it0);
   for (int it = it0; it < it1; ++it, buf ^= 1) {
@@ -197,8 +197,8 @@ __global__ void __launch_bounds__(C3_THREADS, 2) conv1d_silu_v3_kernel(const __g
       }
     }
     wc0 = c0;
-    mbar_wait(&mb[buf], ph[buf]);
-    ph[buf] ^= 1u;
+    mbar_wait(&mb[buf], (ph >> buf) & 1u);
+    ph ^= 1u << buf;
     if (t0 == 0) {  // sequence start: the halo rows come from the cached window
       __syncthreads();
       for (int i = tid; i < (K - 1) * CPR; i += C3_THREADS) {
