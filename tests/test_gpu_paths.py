@@ -156,3 +156,39 @@ def test_decode_block_variants_vs_oracle(dims_name, B):
     d_ref = got["unfused"] - r0[:, L_in:]
     for name in ("default",):
         assert rel(got[name] - r0[:, L_in:], d_ref) < (1e-2 if dims.bcdt_rmsnorm else 5e-3), name
+
+
+def test_bench_prefill_path_cta_pairs_normed_persistent_vs_model_forward():
+    """The bench's exact TP = 1 path at Mamba-2.8B dimensions with a prefill big enough for the
+    default CTA-pair GEMMs (batch 16 x 256 = 4096 rows): pre-norm folded around the projections
+    (rowstats, in_proj row scale, out_proj epilogue writing the next layer's bf16 input and sums of
+    squares), x_proj epilogue splitting dt_low / B || C (no unpack), TMA conv and scan tiles; then
+    the persistent whole-stack decode.  Sampled batch rows vs the fp64 oracle stack."""
+    dims = synth.MixerDims(**{**synth.CONFIGS["mamba2.8b"].asdict(), "n_layers": 2})
+    B, L_in, L_out = synth.WORKLOADS["mamba2.8b"]["batch"], 256, 3
+    mx = TPMixer(dims, "bf16")
+    fulls = [synthetic_layer(dims, l) for l in range(2)]
+    lws = [LayerWeights(dims, f, 1, 0, "bf16") for f in fulls]
+    ws = [_host_weights(f) for f in fulls]
+    del fulls
+    stack = MixerStack(mx, lws, B, L_in, L.SSM_AR2_INT8)
+    assert stack.prefill_normed
+    stack.persistent()
+    g = torch.Generator().manual_seed(9)
+    res0 = torch.randn(B, L_in + L_out, dims.d_model, generator=g, dtype=torch.float64).float()
+    pre = res0[:, :L_in].cuda().contiguous().view(B * L_in, -1)
+    stack.prefill_chunk(pre)
+    outs = []
+    res_t = torch.empty(B, dims.d_model, device="cuda")
+    for t in range(L_in, L_in + L_out):
+        res_t.copy_(res0[:, t].cuda())
+        stack.decode_step(res_t)
+        outs.append(res_t.cpu().clone())
+    torch.cuda.synchronize()
+    got_pre = pre.view(B, L_in, -1).cpu().double().numpy()
+    got_dec = torch.stack(outs, 1).double().numpy()
+    r0 = res0.double().numpy()
+    for b in (0, B - 1):
+        ref, _ = M.model_forward(dims, ws, r0[b:b + 1])
+        assert rel(got_pre[b] - r0[b, :L_in], ref[0, :L_in] - r0[b, :L_in]) < TOL["bf16"], b
+        assert rel(got_dec[b] - r0[b, L_in:], ref[0, L_in:] - r0[b, L_in:]) < TOL["bf16"], b
