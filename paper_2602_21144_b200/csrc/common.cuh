@@ -147,18 +147,6 @@ SSM_DEV void tma_load_3d(void* smem_dst, const void* desc, uint64_t* bar, int32_
       : "memory");
 }
 
-// 2D tiled store shared -> global (bulk-group completion; out-of-bounds box parts are dropped).
-SSM_DEV void tma_store_2d(const void* desc, const void* smem_src, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(desc)),
-               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
-               : "memory");
-}
-SSM_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-// the issuing thread's bulk stores have finished READING shared memory (the buffer may be reused)
-SSM_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-SSM_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 // 1D bulk copy global -> shared of `bytes` (multiple of 16, 16-B aligned both sides), completing
 // on bar's transaction count; L2 evict-first (streamed weights are read once per step).
 SSM_DEV void bulk_load_evict_first(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {

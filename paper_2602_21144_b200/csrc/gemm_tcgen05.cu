@@ -619,52 +619,53 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
     }
   } else if (warp == 1) {
     pdl_wait();
-    if (CG == 2 && rank != 0) goto teardown;  // the leader issues the pair's MMAs
-    // ---------------- MMA issuer: the whole warp runs the (warp-uniform) schedule so the UMMA
-    // descriptors live in uniform registers; one elected lane issues the tcgen05.mma / commits.
-    // (A single-lane loop makes ptxas wrap every UMMA in a uniform-broadcast waterfall loop,
-    // ~100 cycles per instruction: that, not the tensor pipe, bounded skinny weight streams.)
-    const uint32_t idesc = umma_idesc_bf16(BM * CG, BN);
-    const uint64_t ring_desc = umma_desc_sw128(smem_u32(ring));  // + (byte offset >> 4) addresses inside the ring
-    int stage = 0;
-    uint32_t ph = 0;
-    int acc = 0;
-    uint32_t acc_ph = 0;
-    int cur = ts.first(), mt, nt, kb0, kb1;
-    while (ts.next(cur, mt, nt, kb0, kb1)) {
-      if (kb0 >= kb1) continue;
-      mbar_wait(&tempty[acc], acc_ph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem_base + (uint32_t)(acc * cr.acc_stride);
-      for (int kb = kb0; kb < kb1; kb += KBS) {
-        const int nk = min(KBS, kb1 - kb);
-        mbar_wait(&full[stage], ph);
+    if (CG == 1 || rank == 0) {  // the leader issues the pair's MMAs
+      // ---------------- MMA issuer: the whole warp runs the (warp-uniform) schedule so the UMMA
+      // descriptors live in uniform registers; one elected lane issues the tcgen05.mma / commits.
+      // (A single-lane loop makes ptxas wrap every UMMA in a uniform-broadcast waterfall loop,
+      // ~100 cycles per instruction: that, not the tensor pipe, bounded skinny weight streams.)
+      const uint32_t idesc = umma_idesc_bf16(BM * CG, BN);
+      const uint64_t ring_desc = umma_desc_sw128(smem_u32(ring));  // + (byte offset >> 4) addresses inside the ring
+      int stage = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      int cur = ts.first(), mt, nt, kb0, kb1;
+      while (ts.next(cur, mt, nt, kb0, kb1)) {
+        if (kb0 >= kb1) continue;
+        mbar_wait(&tempty[acc], acc_ph ^ 1);
         tc_fence_after();
-        const uint64_t a_desc = ring_desc + (uint64_t)((stage * SB) >> 4);
-        const uint64_t b_desc = a_desc + (uint64_t)(BOFF >> 4);
-        if (elect_one()) {
-          for (int j = 0; j < nk; ++j) {
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              const uint64_t ad = a_desc + (uint64_t)((j * A_STAGE + k * 32) >> 4);
-              const uint64_t bd = b_desc + (uint64_t)((j * BSUB + k * 32) >> 4);
-              const uint32_t accum = (kb > kb0 || j > 0 || k > 0) ? 1u : 0u;
-              if constexpr (CG == 2) umma_bf16_pair(d, ad, bd, idesc, accum);
-              else umma_bf16(d, ad, bd, idesc, accum);
+        const uint32_t d = tmem_base + (uint32_t)(acc * cr.acc_stride);
+        for (int kb = kb0; kb < kb1; kb += KBS) {
+          const int nk = min(KBS, kb1 - kb);
+          mbar_wait(&full[stage], ph);
+          tc_fence_after();
+          const uint64_t a_desc = ring_desc + (uint64_t)((stage * SB) >> 4);
+          const uint64_t b_desc = a_desc + (uint64_t)(BOFF >> 4);
+          if (elect_one()) {
+            for (int j = 0; j < nk; ++j) {
+  #pragma unroll
+              for (int k = 0; k < BK / 16; ++k) {
+                const uint64_t ad = a_desc + (uint64_t)((j * A_STAGE + k * 32) >> 4);
+                const uint64_t bd = b_desc + (uint64_t)((j * BSUB + k * 32) >> 4);
+                const uint32_t accum = (kb > kb0 || j > 0 || k > 0) ? 1u : 0u;
+                if constexpr (CG == 2) umma_bf16_pair(d, ad, bd, idesc, accum);
+                else umma_bf16(d, ad, bd, idesc, accum);
+              }
             }
+            if constexpr (CG == 2) umma_commit_pair(&empty[stage], 3);
+            else umma_commit(&empty[stage]);
           }
-          if constexpr (CG == 2) umma_commit_pair(&empty[stage], 3);
-          else umma_commit(&empty[stage]);
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
+        if (elect_one()) {
+          if constexpr (CG == 2) umma_commit_pair(&tfull[acc], 3);
+          else umma_commit(&tfull[acc]);
         }
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
       }
-      if (elect_one()) {
-        if constexpr (CG == 2) umma_commit_pair(&tfull[acc], 3);
-        else umma_commit(&tfull[acc]);
-      }
-      __syncwarp();
-      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
   } else {
     // ---------------- epilogue warps 2..9; TMEM lane group = warp % 4, column half = (warp-2)/4
@@ -803,7 +804,6 @@ __global__ void __launch_bounds__(var_threads(VAR), 1)
       }
     }
   }
-teardown:
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync();  // the leader's MMAs write the peer's TMEM: free it after both drained
   else __syncthreads();
