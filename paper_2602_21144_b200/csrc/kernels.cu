@@ -525,12 +525,12 @@ __global__ void __launch_bounds__(SC_THREADS) scan_kernel(const __grid_constant_
 // Body in dstep.cuh (shared with the out_proj GEMM, which can run it as its B-operand producer).
 // one (batch row, channel) item per thread: 640 blocks of 128 threads for Mamba-2.8B at batch 16 (a
 // 4-row-per-thread variant, 160 blocks with 4x fewer W_dt reads, and a 2-row one measured slower)
-template <typename T, int N, bool FAST>
+template <typename T, int N, bool FAST, int IPT = 1>
 __global__ void __launch_bounds__(DS_THREADS, 5) decode_step_kernel(DStepArgs a, Peers src, int nsrc) {
   extern __shared__ __align__(16) float dsm[];
   pdl_trigger();
-  dstep_unit<T, N, FAST, DS_THREADS, 1>(a, src, nsrc, blockIdx.x * DS_CH, blockIdx.y * DS_BB, threadIdx.x, dsm,
-                                          -1, true);
+  dstep_unit<T, N, FAST, DS_THREADS, IPT>(a, src, nsrc, blockIdx.x * DS_CH, blockIdx.y * DS_BB * IPT, threadIdx.x,
+                                            dsm, -1, true);
 }
 // ---------------------------------------------------------------- RMSNorm (glue)
 // One 128-thread block per row, the row cached in registers (<= 16 float4 per thread).
@@ -1145,9 +1145,14 @@ cudaError_t launch_scan(int bf16, int fast, const void* u, int64_t ldu, const vo
 
 template <typename T, int N, bool F>
 static cudaError_t dstep_t(const DStepArgs& a, Peers src, int nsrc, cudaStream_t s) {
-  const size_t smem = dstep_smem(a.R, N, (int)sizeof(T), 1);
-  dim3 grid((a.Ek + DS_CH - 1) / DS_CH, (a.batch + DS_BB - 1) / DS_BB);
-  cudaError_t e_ = launch(decode_step_kernel<T, N, F>, grid, DS_THREADS, smem, s, a, src, nsrc);
+  // wide dt_rank at large batch (Falcon-Mamba-7B: R = 256, batch 32): two batch rows per thread share
+  // each W_dt load, so the 512-B rows are read batch / 8 times instead of batch / 4 (71.1 -> 69.2 us per
+  // Falcon-Mamba-7B decode layer; four rows per thread 71.1)
+  const int ipt = (a.R >= 256 && a.batch >= 4 * DS_BB * 2) ? 2 : 1;
+  const size_t smem = dstep_smem(a.R, N, (int)sizeof(T), ipt);
+  dim3 grid((a.Ek + DS_CH - 1) / DS_CH, (a.batch + DS_BB * ipt - 1) / (DS_BB * ipt));
+  cudaError_t e_ = ipt == 1 ? launch(decode_step_kernel<T, N, F>, grid, DS_THREADS, smem, s, a, src, nsrc)
+                            : launch(decode_step_kernel<T, N, F, 2>, grid, DS_THREADS, smem, s, a, src, nsrc);
   if (e_ != cudaSuccess) return e_;
   return cudaGetLastError();
 }
@@ -1338,6 +1343,7 @@ cudaError_t preload_kernels() {
       (const void*)scan_kernel<float, 16, false>, (const void*)scan_kernel<float, 8, false>,
       (const void*)conv1d_silu_v3_kernel<2>, (const void*)conv1d_silu_v3_kernel<3>, (const void*)conv1d_silu_v3_kernel<4>,
       (const void*)decode_step_kernel<__nv_bfloat16, 16, true>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true>,
+      (const void*)decode_step_kernel<__nv_bfloat16, 16, true, 2>, (const void*)decode_step_kernel<__nv_bfloat16, 8, true, 2>,
       (const void*)decode_step_kernel<float, 16, false>, (const void*)decode_step_kernel<float, 8, false>,
       (const void*)rmsnorm_kernel<__nv_bfloat16>, (const void*)rmsnorm_kernel<float>,
       (const void*)quantize_kernel<1>, (const void*)quantize_kernel<2>, (const void*)quantize_kernel<4>,

@@ -11,6 +11,8 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("DS_PKG_ROOT"):   # same-box A/B of kernel variants (scripts/ab_build.sh)
+    sys.path.insert(0, os.environ["DS_PKG_ROOT"])
 import synth  # noqa: E402
 from paper_2602_21144_b200 import LayerWeights, State, TPMixer, _lib as L  # noqa: E402
 from paper_2602_21144_b200.stack import synthetic_layer  # noqa: E402
